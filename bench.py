@@ -1,0 +1,318 @@
+#!/usr/bin/env python
+"""bench.py — rank-k randomized PCA (Szlam, Kluger & Tygert, arXiv 1412.3510) on B200.
+
+Metric (BASELINE.json): rank-k PCA wall time (s) and per-pass HBM GB/s vs the
+roofline.  A step = one whole rpca_pca call (Ω, 2·its+2 passes over A, LU/QR
+renormalisations, the small SVD and the lift U = Q·W) on the workload of
+BASELINE.json configs[1] (C2: dense fp64 A 100000×4000 = 3.2 GB, k = 20,
+l = 22, its = 2), A resident in HBM; A is larger than L2, so no flush is needed.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config C2]
+
+Prints ONE JSON line (rank 0).  `roofline` is for the dominant kernel (the
+A-streaming pass), timed with CUDA events on the library's stream inside the
+timed region; `cpu_baseline` is the CPU oracle (oracle/, plain C + OpenMP) on
+a bounded row sample of the same workload, extrapolated linearly in m.
+--impl reference times that oracle as the reference arm.
+"""
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+import torch
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import synth  # noqa: E402
+
+PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
+FALLBACK_HBM = 6650.0  # B200_PROFILING.md fallback, GB/s
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=20)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--config", default="C2", choices=["C1", "C2", "C3", "C4"])
+    p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--cpu-seconds", type=float, default=8.0, help="target oracle seconds per sample run")
+    return p.parse_args()
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def peaks():
+    try:
+        with open(PEAKS_PATH) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json copy test)"
+    except Exception:
+        return FALLBACK_HBM, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """NVML sampling of SM clock and throttle reasons during the timed region."""
+
+    REASONS = {
+        "gpu_idle": 0x1, "applications_clocks_setting": 0x2, "sw_power_cap": 0x4, "hw_slowdown": 0x8,
+        "sync_boost": 0x10, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
+        "hw_power_brake_slowdown": 0x80, "display_clock_setting": 0x100,
+    }
+
+    def __init__(self, index):
+        self.index = index
+        self.samples = []
+        self.reasons = 0
+        self.ok = False
+        self._stop = threading.Event()
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception:
+            self.max_mhz = None
+
+    def _run(self):
+        nv = self.nv
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                self.reasons |= nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+            except Exception:
+                pass
+            time.sleep(0.005)
+
+    def __enter__(self):
+        if self.ok:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        if self.ok:
+            self._stop.set()
+            self.t.join()
+
+    def summary(self):
+        if not self.ok or not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["nvml unavailable"]}
+        reasons = [k for k, v in self.REASONS.items() if self.reasons & v and k != "gpu_idle"]
+        return {"sm_mhz": float(statistics.median(self.samples)), "sm_max_mhz": self.max_mhz,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+def workload(name):
+    cfg = synth.CONFIGS[name]
+    return cfg, {
+        "workload": f"{name}: {cfg.desc}",
+        "m": cfg.m, "n": cfg.n, "k": cfg.k, "l": cfg.l, "its": cfg.its, "raw": cfg.raw,
+        "passes_over_A": (cfg.its + 2) if cfg.op == "eigens" else (2 * cfg.its + 2),
+    }
+
+
+def make_input(cfg, device):
+    A = synth.make(cfg.name, device=device)
+    torch.cuda.synchronize()
+    return A
+
+
+def run_step(rp, cfg, A):
+    if cfg.op == "eigens":
+        return rp.eigens(A, cfg.k, its=cfg.its, l=cfg.l, seed=0)
+    return rp.pca(A, cfg.k, raw=cfg.raw, its=cfg.its, l=cfg.l, seed=0)
+
+
+# ------------------------------------------------------------------ CPU oracle
+def oracle_sample(cfg, A_host, target_s):
+    """Time the oracle (as it stands) on a leading-row sample of the workload,
+    growing the sample until one run takes ≥ target_s / 4; extrapolate to full m."""
+    import oracle
+
+    m = A_host.shape[0]
+    ms = min(m, max(cfg.l * 4, 2000))
+    while True:
+        As = np.ascontiguousarray(A_host[:ms])
+        t0 = time.perf_counter()
+        if cfg.op == "eigens":
+            # the Nyström path needs a square matrix: sample its leading ms×ms block
+            As = np.ascontiguousarray(A_host[:ms, :ms])
+            oracle.eigens(As, cfg.k, its=cfg.its, l=cfg.l, seed=0)
+        else:
+            oracle.pca(As, cfg.k, raw=cfg.raw, its=cfg.its, l=cfg.l, seed=0)
+        dt = time.perf_counter() - t0
+        if dt >= target_s / 4 or ms >= m:
+            break
+        ms = min(m, int(ms * max(2.0, target_s / max(dt, 1e-3) * 0.9)))
+    scale = (m / ms) ** (2 if cfg.op == "eigens" else 1)
+    return ms, dt, scale
+
+
+def cpu_baseline(cfg, A_host, target_s):
+    import oracle
+
+    ms, dt, scale = oracle_sample(cfg, A_host, target_s)
+    what = (f"leading {ms}x{ms} block" if cfg.op == "eigens" else f"leading {ms} of {cfg.m} rows")
+    return {"value": dt * scale, "unit": "s", "cores": oracle.num_threads(), "kind": "oracle",
+            "sample": f"oracle on the {what} ({dt:.2f} s), extrapolated "
+                      f"{'quadratically in n' if cfg.op == 'eigens' else 'linearly in m'} (x{scale:.1f})"}
+
+
+def reference_arm(args):
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return
+    cfg, conf = workload(args.config)
+    import oracle
+
+    A = synth.make(cfg.name, device="cuda" if torch.cuda.is_available() else "cpu")
+    A_host = A.cpu().numpy()
+    del A
+    ms, dt, scale = oracle_sample(cfg, A_host, args.cpu_seconds)
+    times = []
+    for it in range(args.warmup + args.steps):
+        As = np.ascontiguousarray(A_host[:ms, :ms] if cfg.op == "eigens" else A_host[:ms])
+        t0 = time.perf_counter()
+        if cfg.op == "eigens":
+            oracle.eigens(As, cfg.k, its=cfg.its, l=cfg.l, seed=0)
+        else:
+            oracle.pca(As, cfg.k, raw=cfg.raw, its=cfg.its, l=cfg.l, seed=0)
+        if it >= args.warmup:
+            times.append((time.perf_counter() - t0) * scale)
+    v = float(np.mean(times))
+    what = (f"leading {ms}x{ms} block" if cfg.op == "eigens" else f"leading {ms} of {cfg.m} rows")
+    line = {"impl": "reference", "metric": "rank-k PCA wall time (s)", "value": v, "unit": "s",
+            "n_gpus": ws, "steps": args.steps, "warmup": args.warmup, "ms_per_step": v * 1e3,
+            "higher_is_better": False, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": conf,
+            "cpu_baseline": {"value": v, "unit": "s", "cores": oracle.num_threads(), "kind": "oracle",
+                             "sample": f"oracle on the {what} per step, extrapolated x{scale:.1f}"},
+            "e2e": {"value": v, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------ our arm
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return reference_arm(args)
+    ws, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if ws > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+    import paper_1412_3510_b200 as rp
+
+    cfg, conf = workload(args.config)
+    A = make_input(cfg, dev)
+    abytes = A.numel() * A.element_size()
+    passes = conf["passes_over_A"]
+    conf.update({"l2": f"A ({abytes / 1e9:.2f} GB) > L2 (126 MB): no flush needed",
+                 "parallelism": f"replicas x{ws}" if ws > 1 else "single GPU"})
+
+    for _ in range(args.warmup):
+        run_step(rp, cfg, A)
+    torch.cuda.synchronize()
+
+    def barrier():
+        if ws > 1:
+            import torch.distributed as dist
+            dist.barrier()
+
+    stream = torch.cuda.current_stream(dev)
+    launches0 = rp.launch_count()
+    barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk, rp.profile() as prof:
+        e0.record(stream)
+        for _ in range(args.steps):
+            run_step(rp, cfg, A)
+        e1.record(stream)
+        torch.cuda.synchronize()
+    barrier()
+    ms_total = e0.elapsed_time(e1)
+    launches = rp.launch_count() - launches0
+    t_step = ms_total / 1e3 / args.steps
+    if ws > 1:
+        import torch.distributed as dist
+        t = torch.tensor([t_step], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        t_step = float(t.item())
+
+    # dominant kernel: the A-streaming passes
+    hbm, peak_src = peaks()
+    kern = {}
+    for name, msec in prof.records:
+        c, s = kern.get(name, (0, 0.0))
+        kern[name] = (c + 1, s + msec)
+    step_ms = ms_total / args.steps
+    passes_k = {k: v for k, v in kern.items() if k.startswith(("ax_", "aty_f64", "aty_generic"))}
+    dom = max(passes_k.items(), key=lambda kv: kv[1][1]) if passes_k else None
+    roof = None
+    if dom:
+        cnt, tot = dom[1]
+        avg_ms = tot / cnt
+        achieved = abytes / (avg_ms / 1e3) / 1e9
+        roof = {"bound": "hbm", "kernel": dom[0], "achieved": round(achieved, 1), "peak": hbm, "unit": "GB/s",
+                "frac": round(achieved / hbm, 4), "traffic": None, "peak_source": peak_src,
+                "algorithmic_bytes_per_launch": abytes, "avg_launch_ms": round(avg_ms, 5),
+                "share_of_step": round(tot / args.steps / step_ms, 4)}
+        all_pass_ms = sum(v[1] for v in passes_k.values()) / args.steps
+        roof["all_passes"] = {"launches_per_step": sum(v[0] for v in passes_k.values()) // args.steps,
+                              "gbs_per_pass": round(abytes * passes / (all_pass_ms / 1e3) / 1e9, 1)}
+    breakdown = {k: {"launches_per_step": v[0] / args.steps, "ms_per_step": round(v[1] / args.steps, 5)}
+                 for k, v in sorted(kern.items(), key=lambda kv: -kv[1][1])}
+
+    e2e = None
+    if not args.no_e2e and rank == 0:
+        Ah = A.cpu().pin_memory()
+        run_step(rp, cfg, Ah)  # warm
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        ne = max(3, min(args.steps, 10))
+        for _ in range(ne):
+            out = run_step(rp, cfg, Ah)
+        te = (time.perf_counter() - t0) / ne
+        d2h = sum(o.numel() * o.element_size() for o in out)
+        e2e = {"value": te, "unit": "s", "h2d_bytes_per_step": abytes, "d2h_bytes_per_step": d2h,
+               "note": "host-pinned A copied H2D and U,S,V copied D2H inside each rpca_pca call; host wall clock"}
+        del Ah
+
+    cpu = None
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(cfg, A.cpu().numpy(), args.cpu_seconds)
+
+    if rank == 0:
+        line = {"metric": "rank-k PCA wall time (s)", "value": t_step, "unit": "s", "n_gpus": ws,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_step * 1e3,
+                "higher_is_better": False, "scaling": "weak", "vs_baseline": None,
+                "dtype": "f64" if A.dtype == torch.float64 else "f32", "data": "synthetic", "config": conf,
+                "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
+                "clocks": clk.summary(), "kernels": breakdown,
+                "roofline_time_s": abytes * passes / (hbm * 1e9)}
+        print(json.dumps(line), flush=True)
+    if ws > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

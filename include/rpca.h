@@ -1,0 +1,203 @@
+/*
+ * rpca.h — C ABI of the B200-native randomized PCA / SVD hot path of
+ * Szlam, Kluger & Tygert, "An implementation of a randomized algorithm for
+ * principal component analysis", arXiv:1412.3510 (PAPER.md in the survey).
+ *
+ * Every entry point takes plain pointers and sizes.  Unless a field says
+ * otherwise, matrices are ROW-MAJOR, thin blocks (m×l, n×l, l×l) are fp64
+ * with leading dimension = number of columns, and all buffers are DEVICE
+ * memory of the context's GPU owned by the caller.  The library keeps no
+ * pointer past the return of a call (its workspace is context-owned).
+ * Calls enqueue on the context's stream; calls that return host scalars or
+ * statuses computed on the device synchronise that stream (noted per call).
+ *
+ * Errors: every call returns an rpca_status; RPCA_OK = 0.  On error the
+ * outputs are unspecified, and rpca_last_error() gives a message.  Invalid
+ * shapes never launch a kernel.  A context is not thread-safe.
+ */
+#ifndef RPCA_H_
+#define RPCA_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  RPCA_OK = 0,
+  RPCA_E_ARG = 1,       /* null pointer, bad enum, bad flags, misaligned pointer */
+  RPCA_E_SHAPE = 2,     /* k<1, l<k, l>min(m,n), its<0, m,n<1, bad shard, non-square for eigens */
+  RPCA_E_NONFINITE = 3, /* non-finite input seen (only with RPCA_FLAG_CHECK_FINITE) */
+  RPCA_E_NOTPSD = 4,    /* Nyström: shifted Cholesky failed after all retries / SQRT found a
+                           negative eigenvalue of B2 below -1e-6·‖B2‖ */
+  RPCA_E_CUDA = 5,
+  RPCA_E_NCCL = 6,
+  RPCA_E_WORKSPACE = 7,
+  RPCA_E_NOTIMPL = 8,
+  RPCA_E_NOMEM = 9
+} rpca_status;
+
+/* matrix kinds / dtypes / locations */
+enum { RPCA_DENSE = 0, RPCA_CSR = 1 };
+enum { RPCA_F64 = 0, RPCA_F32 = 1 };
+enum { RPCA_DEVICE = 0, RPCA_HOST = 1 };
+
+/* Ω distributions (PAPER.md:163-168 normal; PAPER.md:437-440 uniform [-1,1]) */
+enum { RPCA_GAUSSIAN = 0, RPCA_UNIFORM = 1 };
+
+/* Nyström stabilisations (§3, l.257-282) */
+enum { RPCA_SHIFT_CHOL = 0, RPCA_SQRT = 1 };
+
+/* flags for rpca_ctx_create / the drivers */
+#define RPCA_FLAG_UNIFORM_OMEGA 0x1u  /* draw Ω from U[-1,1] instead of N(0,1) */
+#define RPCA_FLAG_OUTPUTS_HOST 0x2u   /* U, S, V / lam are HOST buffers (copied back inside the call) */
+#define RPCA_FLAG_CHECK_FINITE 0x4u   /* validate A during pass 1 → RPCA_E_NONFINITE */
+
+/*
+ * The matrix A (§2 l.107-114: m×n, k ≪ min(m,n)).
+ *   kind = RPCA_DENSE: `a` points at row i*lda (elements), lda ≥ n.
+ *   kind = RPCA_CSR:   rowptr[m_local+1] (int64, rowptr[0] = 0), colind[nnz]
+ *                      (int32, sorted within a row, < n), vals[nnz].
+ *   dtype: element type of a / vals (fp64 or fp32).  fp32 inputs are computed
+ *   with fp32 products (dense: 3×TF32 tensor-core split) and fp64 reductions.
+ *   m, n: GLOBAL shape.  row0, m_local: the rows [row0, row0+m_local) this
+ *   rank holds (single GPU: 0, m).  location: RPCA_DEVICE or RPCA_HOST (host
+ *   A is copied to the device inside the call — the end-to-end mode).
+ */
+typedef struct {
+  int32_t kind;
+  int32_t dtype;
+  int64_t m, n;
+  int64_t row0, m_local;
+  const void* a;
+  int64_t lda;
+  const int64_t* rowptr;
+  const int32_t* colind;
+  const void* vals;
+  int64_t nnz;
+  int32_t location;
+  int32_t reserved;
+} rpca_mat;
+
+typedef struct rpca_ctx rpca_ctx;
+
+/* ---- context ------------------------------------------------------------
+ * rpca_ctx_create: binds to CUDA `device` and `stream` (a cudaStream_t; NULL
+ * = the legacy default stream).  flags: default driver flags (RPCA_FLAG_*).
+ * The context owns a growable device workspace; the first call of a given
+ * size allocates (cudaMalloc), later calls of the same or smaller size do
+ * not, so steady-state calls are CUDA-graph capturable.                    */
+rpca_status rpca_ctx_create(rpca_ctx** ctx, int device, void* stream, uint32_t flags);
+rpca_status rpca_ctx_destroy(rpca_ctx* ctx);
+rpca_status rpca_ctx_set_stream(rpca_ctx* ctx, void* stream);
+rpca_status rpca_ctx_set_flags(rpca_ctx* ctx, uint32_t flags);
+rpca_status rpca_ctx_sync(rpca_ctx* ctx);
+/* bytes of workspace currently held by the context */
+rpca_status rpca_workspace_size(rpca_ctx* ctx, size_t* bytes);
+const char* rpca_strerror(rpca_status s);
+const char* rpca_last_error(void);
+/* number of kernels this library launched since the context was created */
+rpca_status rpca_launch_count(rpca_ctx* ctx, int64_t* count);
+/* per-launch timing: after rpca_profile_begin, an event is recorded on the
+ * context stream behind every kernel launch; rpca_profile_end synchronises the
+ * stream, stops recording and writes "name<TAB>milliseconds\n" per launch
+ * (duration = gap to the previous event; launches are stream-serialised) into
+ * buf (NUL-terminated, truncated to cap); *needed = full length.            */
+rpca_status rpca_profile_begin(rpca_ctx* ctx);
+rpca_status rpca_profile_end(rpca_ctx* ctx, char* buf, size_t cap, size_t* needed);
+
+/* ---- multi-GPU (rows of A sharded across ranks) ---------
+ * rpca_comm_unique_id: writes an ncclUniqueId (128 bytes) into `id` (host).
+ * rpca_comm_init: ncclCommInitRank(nranks, id, rank) on the context's device;
+ * afterwards the drivers treat A as the row shard [row0, row0+m_local).      */
+rpca_status rpca_comm_unique_id(void* id, size_t bytes);
+rpca_status rpca_comm_init(rpca_ctx* ctx, int nranks, int rank, const void* id);
+
+/* ---- §8(a) step a1: Ω ------------------------------------------------------
+ * out (rows×cols, row-major, fp64, device) = the test block of PAPER.md:163-168
+ * (dist RPCA_GAUSSIAN) or PAPER.md:437-440 (RPCA_UNIFORM).  Element e =
+ * i·cols + j takes Philox4x32-10 call p = e>>1 with counter (lo32 p, hi32 p,
+ * 0, stream_id) and key (lo32 seed, hi32 seed); a, b = the two 53-bit
+ * uniforms of the call; Gaussian: r = sqrt(-2 ln(1-a)), e even → r cos 2πb,
+ * e odd → r sin 2πb; uniform: 2a-1 / 2b-1 (reading Q7).
+ * round_f32 != 0 rounds every value to fp32 (the fp32 path's Ω).            */
+rpca_status rpca_omega(rpca_ctx* ctx, uint64_t seed, uint32_t stream_id, int64_t rows, int64_t cols,
+                       int dist, int round_f32, double* out);
+
+/* ---- column means: c[j] = (1/m)·Σ_i A_ij (global rows). */
+rpca_status rpca_colmeans(rpca_ctx* ctx, const rpca_mat* A, double* c);
+
+/* ---- §8(a) steps a2, a4, a6: applications of A --------
+ * adjoint = 0: Y (m_local×l) = A·X (X n×l) [ − 1·(c·X) if c != NULL ]
+ * adjoint = 1: Y (n×l)       = Aᵀ·X (X m_local×l) [ − cᵀ·(1ᵀX) if c != NULL ]
+ *   (with a communicator, the adjoint result is all-reduced over ranks.)
+ * c: column means (n, fp64, device) or NULL (no centring).
+ * Dense fp64 A uses the fp64 tensor cores (DMMA); fp32 A uses 3×TF32
+ * products; every sum across K-chunks, CTAs and ranks is fp64 and runs in a
+ * fixed order, so results are bitwise reproducible for a fixed device/grid. */
+rpca_status rpca_apply(rpca_ctx* ctx, const rpca_mat* A, const double* c, int adjoint, const double* X,
+                       int64_t l, double* Y);
+
+/* ---- §8(a) step a3: LU renormalisation ("[Q,R]=lu(Q)") ---
+ * In place: Y (m×l, m ≥ l) ← L with Y = L·U, L in the ORIGINAL row order
+ * (unit lower triangular in the pivot rows, reading Q3).  Pivot rows are
+ * chosen by tournament pivoting (GEPP on row blocks, then on stacked
+ * candidates; lowest row index on ties); a pivot that is exactly 0 makes
+ * L's column the unit vector at its row.  U (l×l, device) and piv (l int64,
+ * device) may be NULL.                                                     */
+rpca_status rpca_lu_renorm(rpca_ctx* ctx, double* Y, int64_t m, int64_t l, double* U, int64_t* piv);
+
+/* ---- §8(a) steps a5/a7: Householder QR --------
+ * In place: Y (m×l, m ≥ l) ← Q with orthonormal columns, Y = Q·R, R upper
+ * triangular with diag(R) ≥ 0 (R: l×l device, may be NULL).  Tall-skinny
+ * Householder (TSQR tree); rank-deficient Y still yields orthonormal Q.   */
+rpca_status rpca_qr(rpca_ctx* ctx, double* Y, int64_t m, int64_t l, double* R);
+
+/* ---- §8(a) step a7: small SVD (eq. i3) ------------------
+ * G (n×l, n ≥ l) = Vt · diag(sigma) · Wᵀ: Vt (n×l) orthonormal, sigma (l)
+ * non-increasing ≥ 0, W (l×l) orthogonal.  TSQR of G, then one-sided Jacobi
+ * on the l×l R in one CTA (threshold 2^-52, ≤ 30 sweeps).  All device.      */
+rpca_status rpca_small_svd(rpca_ctx* ctx, const double* G, int64_t n, int64_t l, double* Vt, double* sigma,
+                           double* W);
+
+/* ---- the whole path: rank-k PCA (§2 eqs. i1-i4, §5) -------------
+ *   Y = A·Ω [centred]; Q = its==0 ? qr(Y) : lu(Y)
+ *   for it = 1..its: Z = lu(Aᵀ·Q); Y = A·Z; Q = it<its ? lu(Y) : qr(Y)
+ *   Bᵀ = Aᵀ·Q; Bᵀ = V·Σ·Wᵀ; U = Q·W; truncate to k.
+ * raw != 0: no centring; raw == 0: implicit column centring.
+ * its ≥ 0 extra power rounds: 2·its+2 passes over A.
+ * l ≤ 0 means l = k+2.  When m < n the path sketches Aᵀ and swaps U and V.
+ * Outputs in A's dtype: U (m_local×k, ld ldu ≥ k), S (k, non-increasing),
+ * V (n×k, ld ldv ≥ k, replicated on every rank).  Sign convention: the
+ * largest-|·| entry of every column of V is positive (lowest index on ties).
+ * Synchronises the stream (reads the device status word).                  */
+rpca_status rpca_pca(rpca_ctx* ctx, const rpca_mat* A, int64_t k, int raw, int its, int64_t l, uint64_t seed,
+                     void* U, int64_t ldu, void* S, void* V, int64_t ldv);
+
+/* ---- the stabilised Nyström path (§3, l.214-282) -----------------
+ * A square, self-adjoint, nonnegative definite (not checked).  Q from the
+ * self-adjoint loop of PAPER.md:386-412 (its+1 applications, LU inside, QR
+ * last); B1 = A·Q; B2 = sym(QᵀB1); variant RPCA_SHIFT_CHOL: ν = u·√n·‖B1‖_F,
+ * C = chol(B2 + νI) (ν ×10 up to 5 retries), F = (B1 + νQ)·C⁻¹;
+ * RPCA_SQRT: C = B2^{1/2} with a 1e-12-regularised pseudo-inverse.  F = U·S·Wᵀ,
+ * lam = max(S² − ν, 0).  Outputs in A's dtype: U (n_local×k, ld ldu), lam (k).
+ * Synchronises the stream.                                                  */
+rpca_status rpca_eigens(rpca_ctx* ctx, const rpca_mat* A, int64_t k, int its, int64_t l, uint64_t seed,
+                        int variant, void* U, int64_t ldu, void* lam);
+
+/* ---- accuracy: ‖A − U·diag(S)·Vᵀ‖ by the randomized power method ----------
+ * PAPER.md §4 l.362-371.  x = stream-1 Gaussian n-vector (seed), normalised;
+ * its times: y = E·x, z = Eᵀ·y, est = sqrt(‖z‖), x = z/‖z‖.  E = A [centred
+ * if raw == 0] − U·diag(S)·Vᵀ, never formed.  U (m_local×k, ld ldu), S (k),
+ * V (n×k, ld ldv), fp64 device (k = 0 allowed: estimates ‖A‖).  For eigens
+ * factors pass V = U and S = lam.  *out (host) gets the estimate; synchronises. */
+rpca_status rpca_diffsnorm(rpca_ctx* ctx, const rpca_mat* A, int raw, const double* U, int64_t ldu,
+                           const double* S, const double* V, int64_t ldv, int64_t k, int its, uint64_t seed,
+                           double* out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* RPCA_H_ */

@@ -1,0 +1,307 @@
+"""B200-native randomized PCA / SVD (Szlam, Kluger & Tygert, arXiv 1412.3510).
+
+Thin Python binding over the C ABI in ``include/rpca.h`` (``librpca.so``,
+sm_100a).  This module only marshals arguments: every step of the path —
+Ω generation, the passes over A, LU/QR renormalisation, the small SVD, the
+lift U = Q·W and the Nyström and power-method extras — runs in the library's
+CUDA kernels.  PyTorch supplies device memory and the current stream.
+
+There is no CPU fallback: importing works anywhere, but every call raises
+``RuntimeError`` if the library is missing or no sm_100 GPU is present.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import threading
+
+import torch
+
+__all__ = ["pca", "eigens", "diffsnorm", "omega", "apply", "colmeans", "lu_renorm", "qr", "small_svd",
+           "launch_count", "library_path", "RPCAError"]
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_LIB_PATH = os.path.join(_HERE, "librpca.so")
+
+OK, E_ARG, E_SHAPE, E_NONFINITE, E_NOTPSD, E_CUDA, E_NCCL, E_WORKSPACE, E_NOTIMPL, E_NOMEM = range(10)
+DENSE, CSR = 0, 1
+F64, F32 = 0, 1
+DEVICE, HOST = 0, 1
+GAUSSIAN, UNIFORM = 0, 1
+SHIFT_CHOL, SQRT = 0, 1
+FLAG_UNIFORM_OMEGA, FLAG_OUTPUTS_HOST, FLAG_CHECK_FINITE = 0x1, 0x2, 0x4
+
+
+class RPCAError(RuntimeError):
+    def __init__(self, code, msg):
+        super().__init__(f"rpca status {code}: {msg}")
+        self.code = code
+
+
+class rpca_mat(C.Structure):
+    _fields_ = [("kind", C.c_int32), ("dtype", C.c_int32), ("m", C.c_int64), ("n", C.c_int64),
+                ("row0", C.c_int64), ("m_local", C.c_int64), ("a", C.c_void_p), ("lda", C.c_int64),
+                ("rowptr", C.c_void_p), ("colind", C.c_void_p), ("vals", C.c_void_p), ("nnz", C.c_int64),
+                ("location", C.c_int32), ("reserved", C.c_int32)]
+
+
+_lib = None
+_lock = threading.Lock()
+_ctxs = {}
+
+
+def library_path() -> str:
+    return _LIB_PATH
+
+
+def _load():
+    global _lib
+    with _lock:
+        if _lib is not None:
+            return _lib
+        if not os.path.exists(_LIB_PATH):
+            raise RuntimeError(f"{_LIB_PATH} is missing: run `make` (or __graft_entry__.build()) first")
+        L = C.CDLL(_LIB_PATH)
+        vp, i64, i32, u64, u32, dp = C.c_void_p, C.c_int64, C.c_int, C.c_uint64, C.c_uint32, C.c_void_p
+        pm = C.POINTER(rpca_mat)
+        sig = {
+            "rpca_ctx_create": [C.POINTER(vp), i32, vp, u32],
+            "rpca_ctx_destroy": [vp],
+            "rpca_ctx_set_stream": [vp, vp],
+            "rpca_ctx_set_flags": [vp, u32],
+            "rpca_ctx_sync": [vp],
+            "rpca_launch_count": [vp, C.POINTER(i64)],
+            "rpca_workspace_size": [vp, C.POINTER(C.c_size_t)],
+            "rpca_profile_begin": [vp],
+            "rpca_profile_end": [vp, C.c_char_p, C.c_size_t, C.POINTER(C.c_size_t)],
+            "rpca_comm_unique_id": [vp, C.c_size_t],
+            "rpca_comm_init": [vp, i32, i32, vp],
+            "rpca_omega": [vp, u64, u32, i64, i64, i32, i32, dp],
+            "rpca_colmeans": [vp, pm, dp],
+            "rpca_apply": [vp, pm, dp, i32, dp, i64, dp],
+            "rpca_lu_renorm": [vp, dp, i64, i64, dp, vp],
+            "rpca_qr": [vp, dp, i64, i64, dp],
+            "rpca_small_svd": [vp, dp, i64, i64, dp, dp, dp],
+            "rpca_pca": [vp, pm, i64, i32, i32, i64, u64, vp, i64, vp, vp, i64],
+            "rpca_eigens": [vp, pm, i64, i32, i64, u64, i32, vp, i64, vp],
+            "rpca_diffsnorm": [vp, pm, i32, dp, i64, dp, dp, i64, i64, i32, u64, C.POINTER(C.c_double)],
+        }
+        for name, args in sig.items():
+            f = getattr(L, name)
+            f.argtypes = args
+            f.restype = C.c_int
+        L.rpca_last_error.restype = C.c_char_p
+        L.rpca_strerror.restype = C.c_char_p
+        L.rpca_strerror.argtypes = [C.c_int]
+        _lib = L
+        return L
+
+
+def _check(code):
+    if code != OK:
+        L = _load()
+        raise RPCAError(code, f"{L.rpca_strerror(code).decode()}: {L.rpca_last_error().decode()}")
+
+
+def _ctx(device: torch.device, flags: int = 0):
+    if not torch.cuda.is_available():
+        raise RuntimeError("no CUDA device: the randomized-PCA kernels need an sm_100a GPU (no CPU fallback)")
+    L = _load()
+    idx = device.index if device.index is not None else torch.cuda.current_device()
+    key = (threading.get_ident(), idx)
+    h = _ctxs.get(key)
+    if h is None:
+        h = C.c_void_p()
+        _check(L.rpca_ctx_create(C.byref(h), idx, None, 0))
+        _ctxs[key] = h
+    stream = torch.cuda.current_stream(idx).cuda_stream
+    _check(L.rpca_ctx_set_stream(h, C.c_void_p(stream)))
+    return L, h
+
+
+def _ctx_flags(h, flags):
+    _check(_load().rpca_ctx_set_flags(h, flags))
+
+
+def _ptr(t):
+    return None if t is None else C.c_void_p(t.data_ptr())
+
+
+def _dtype_code(dt):
+    if dt == torch.float64:
+        return F64
+    if dt == torch.float32:
+        return F32
+    raise TypeError("A must be float64 or float32")
+
+
+def _dense(A: torch.Tensor, host=False) -> rpca_mat:
+    if A.dim() != 2 or A.stride(1) != 1:
+        raise ValueError("A must be a 2-D row-major tensor (stride(1) == 1)")
+    m, n = A.shape
+    return rpca_mat(DENSE, _dtype_code(A.dtype), m, n, 0, m, A.data_ptr(), A.stride(0), None, None, None, 0,
+                    HOST if host else DEVICE, 0)
+
+
+def launch_count(device=None) -> int:
+    dev = torch.device("cuda", torch.cuda.current_device() if device is None else device)
+    L, h = _ctx(dev)
+    n = C.c_int64(0)
+    _check(L.rpca_launch_count(h, C.byref(n)))
+    return n.value
+
+
+class profile:
+    """Context manager timing every library launch on the current stream:
+    ``with profile() as p: ...`` then ``p.records`` = [(kernel, ms), ...]."""
+
+    def __init__(self, device=None):
+        self.device = torch.device("cuda", torch.cuda.current_device() if device is None else device)
+        self.records = []
+
+    def __enter__(self):
+        L, h = _ctx(self.device)
+        _check(L.rpca_profile_begin(h))
+        return self
+
+    def __exit__(self, *exc):
+        L, h = _ctx(self.device)
+        need = C.c_size_t(0)
+        _check(L.rpca_profile_end(h, None, 0, C.byref(need)))
+        buf = C.create_string_buffer(need.value + 1)
+        # second call returns the same text (records are kept until the next begin)
+        _check(L.rpca_profile_end(h, buf, need.value + 1, C.byref(need)))
+        for line in buf.value.decode().splitlines():
+            name, ms = line.split("\t")
+            self.records.append((name, float(ms)))
+        return False
+
+    def total(self, prefix):
+        v = [ms for n, ms in self.records if n.startswith(prefix)]
+        return len(v), sum(v)
+
+
+def omega(rows: int, cols: int, seed: int = 0, stream_id: int = 0, dist: int = GAUSSIAN, round_f32: bool = False,
+          device=None) -> torch.Tensor:
+    """Ω (rows×cols, fp64) — PAPER.md:163-168 / 437-440; counter layout in include/rpca.h."""
+    dev = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
+    L, h = _ctx(dev)
+    out = torch.empty(rows, cols, dtype=torch.float64, device=dev)
+    _check(L.rpca_omega(h, seed, stream_id, rows, cols, dist, int(round_f32), _ptr(out)))
+    return out
+
+
+def colmeans(A: torch.Tensor) -> torch.Tensor:
+    L, h = _ctx(A.device)
+    c = torch.empty(A.shape[1], dtype=torch.float64, device=A.device)
+    mat = _dense(A)
+    _check(L.rpca_colmeans(h, C.byref(mat), _ptr(c)))
+    return c
+
+
+def apply(A: torch.Tensor, X: torch.Tensor, adjoint: bool = False, cmean: torch.Tensor | None = None):
+    """Y = A·X (adjoint=False) or Aᵀ·X, optionally centred by the column means `cmean`."""
+    L, h = _ctx(A.device)
+    X = X.contiguous()
+    assert X.dtype == torch.float64
+    l = X.shape[1]
+    rows = A.shape[1] if adjoint else A.shape[0]
+    Y = torch.empty(rows, l, dtype=torch.float64, device=A.device)
+    mat = _dense(A)
+    _check(L.rpca_apply(h, C.byref(mat), _ptr(cmean), int(adjoint), _ptr(X), l, _ptr(Y)))
+    return Y
+
+
+def lu_renorm(Y: torch.Tensor):
+    """(L, U, piv): L = Y·U⁻¹ in original row order (reading Q3)."""
+    L_, h = _ctx(Y.device)
+    Lm = Y.contiguous().clone()
+    m, l = Lm.shape
+    U = torch.zeros(l, l, dtype=torch.float64, device=Y.device)
+    piv = torch.zeros(l, dtype=torch.int64, device=Y.device)
+    _check(L_.rpca_lu_renorm(h, _ptr(Lm), m, l, _ptr(U), _ptr(piv)))
+    return Lm, U, piv
+
+
+def qr(Y: torch.Tensor):
+    """(Q, R) Householder TSQR, diag(R) ≥ 0."""
+    L_, h = _ctx(Y.device)
+    Q = Y.contiguous().clone()
+    m, l = Q.shape
+    R = torch.zeros(l, l, dtype=torch.float64, device=Y.device)
+    _check(L_.rpca_qr(h, _ptr(Q), m, l, _ptr(R)))
+    return Q, R
+
+
+def small_svd(G: torch.Tensor):
+    """G = Vt·diag(s)·Wᵀ (eq. i3 applied to Bᵀ)."""
+    L_, h = _ctx(G.device)
+    G = G.contiguous()
+    n, l = G.shape
+    Vt = torch.empty(n, l, dtype=torch.float64, device=G.device)
+    s = torch.empty(l, dtype=torch.float64, device=G.device)
+    W = torch.empty(l, l, dtype=torch.float64, device=G.device)
+    _check(L_.rpca_small_svd(h, _ptr(G), n, l, _ptr(Vt), _ptr(s), _ptr(W)))
+    return Vt, s, W
+
+
+def pca(A: torch.Tensor, k: int, raw: bool = True, its: int = 2, l: int | None = None, seed: int = 0,
+        uniform_omega: bool = False):
+    """Rank-k PCA / SVD of A (§2 eqs. i1-i4, §5): returns (U m×k, S k, V n×k) on A's device.
+
+    raw=False centres the columns implicitly.  A may also be
+    a pinned host tensor: then the host→device copy and the device→host copy of
+    the factors happen inside the call (the end-to-end mode)."""
+    host = A.device.type == "cpu"
+    dev = torch.device("cuda", torch.cuda.current_device()) if host else A.device
+    L_, h = _ctx(dev)
+    m, n = A.shape
+    flags = (FLAG_UNIFORM_OMEGA if uniform_omega else 0) | (FLAG_OUTPUTS_HOST if host else 0)
+    _ctx_flags(h, flags)
+    outdev = torch.device("cpu") if host else dev
+    pin = host
+    U = torch.empty(m, k, dtype=A.dtype, device=outdev, pin_memory=pin)
+    S = torch.empty(k, dtype=A.dtype, device=outdev, pin_memory=pin)
+    V = torch.empty(n, k, dtype=A.dtype, device=outdev, pin_memory=pin)
+    mat = _dense(A, host=host)
+    try:
+        _check(L_.rpca_pca(h, C.byref(mat), k, int(bool(raw)), its, -1 if l is None else l, seed,
+                           _ptr(U), k, _ptr(S), _ptr(V), k))
+    finally:
+        _ctx_flags(h, 0)
+    return U, S, V
+
+
+def eigens(A: torch.Tensor, k: int, its: int = 2, l: int | None = None, seed: int = 0,
+           variant: str = "shift_chol", uniform_omega: bool = False):
+    """Stabilised Nyström (§3) of a PSD A: returns (U n×k, lam k)."""
+    host = A.device.type == "cpu"
+    dev = torch.device("cuda", torch.cuda.current_device()) if host else A.device
+    L_, h = _ctx(dev)
+    n = A.shape[0]
+    v = {"shift_chol": SHIFT_CHOL, "sqrt": SQRT}[variant]
+    _ctx_flags(h, (FLAG_UNIFORM_OMEGA if uniform_omega else 0) | (FLAG_OUTPUTS_HOST if host else 0))
+    outdev = torch.device("cpu") if host else dev
+    U = torch.empty(n, k, dtype=A.dtype, device=outdev, pin_memory=host)
+    lam = torch.empty(k, dtype=A.dtype, device=outdev, pin_memory=host)
+    mat = _dense(A, host=host)
+    try:
+        _check(L_.rpca_eigens(h, C.byref(mat), k, its, -1 if l is None else l, seed, v, _ptr(U), k, _ptr(lam)))
+    finally:
+        _ctx_flags(h, 0)
+    return U, lam
+
+
+def diffsnorm(A: torch.Tensor, U: torch.Tensor, S: torch.Tensor, V: torch.Tensor, raw: bool = True, its: int = 20,
+              seed: int = 1) -> float:
+    """Power-method estimate of ‖A − U·diag(S)·Vᵀ‖ (§4 l.362-371)."""
+    L_, h = _ctx(A.device)
+    U = U.to(torch.float64).contiguous()
+    V = V.to(torch.float64).contiguous()
+    S = S.to(torch.float64).contiguous()
+    k = S.shape[0]
+    out = C.c_double(0.0)
+    mat = _dense(A)
+    _check(L_.rpca_diffsnorm(h, C.byref(mat), int(bool(raw)), _ptr(U), max(k, 1), _ptr(S), _ptr(V), max(k, 1), k,
+                             its, seed, C.byref(out)))
+    return out.value

@@ -1,0 +1,273 @@
+// dense_ax.cu — §8(a) steps a2/a5: Y = A·X for a dense row-major A (m×n) and
+// a thin X (n×l), the "A*Q" of PAPER.md:398/430 — the pass that streams A.
+//
+// fp64 design (B200, sm_100a):
+//   * persistent CTAs (one per SM), each walks row tiles of BM = 128 rows;
+//   * one producer warp streams A with 2-D TMA boxes [128 rows × 16 doubles]
+//     (SWIZZLE_128B, zero fill past m and n) plus the matching 32-row chunk of
+//     the packed X with a 1-D bulk copy into a STAGES-deep mbarrier ring;
+//   * eight consumer warps run the fp64 tensor-core MMA (mma.m8n8k4 f64,
+//     "DMMA"); each warp owns 16 rows × 8·NT columns in registers.  The k
+//     order inside a 32-wide chunk is permuted so that every lane fetches its
+//     two A values with one conflict-free 16-byte LDS (see the layout note);
+//     X is pre-packed in exactly the fragment order (thin.cu pack_x).
+//   Per element of A: 8 bytes and 2·l flops — at l = 22 the fp64 pipe (≈37
+//   TF/s measured) and HBM (≈6.5-7.3 TB/s) bind together.
+// Generic fallback (fp32 A until the tcgen05 path lands, or lda·8 not a
+// multiple of 16): CUDA-core kernel with the same result contract.
+#include <cudaTypedefs.h>
+
+#include "internal.cuh"
+
+namespace rpca {
+namespace {
+
+constexpr int BM = 128;          // rows per tile
+constexpr int BK = 32;           // k per stage (two TMA boxes of 16 doubles)
+constexpr int kConsumerWarps = 8;
+constexpr int kThreads = (kConsumerWarps + 1) * 32;
+
+template <int NT>
+struct AxCfg {
+  static constexpr int kABytes = BM * BK * 8;             // 32 KB
+  static constexpr int kXBytes = 8 * NT * 32 * 8;         // packed X chunk
+  static constexpr int kStageBytes = kABytes + kXBytes;   // multiple of 1024
+  static constexpr int kStages = (212 * 1024) / kStageBytes > 8 ? 8 : (212 * 1024) / kStageBytes;
+  static constexpr int kSmem = kStages * kStageBytes + 1024 /*align*/ + 2 * kStages * 8;
+};
+
+// Layout note.  Stage s holds A rows [tile·128, +128) × k [kb·32, +32) as
+// two boxes (k 0-15, k 16-31), each 128 rows × 128 B, 128B-swizzled.  DMMA
+// k-step st (0..7) gives lane (row r = lane>>2, kpos c = lane&3) the value
+// A[r][kb·32 + 8·(st>>1) + 2c + (st&1)]: for st = 2q, 2q+1 both values sit in
+// 16-byte chunk 4·(q&1) + c of box q>>1, loaded once as a double2.  Packed X
+// holds X[that same k][nt·8 + (lane>>2)] at Xp[kb][st][nt][lane].
+template <int NT>
+__global__ void __launch_bounds__(kThreads, 1)
+    ax_f64_tma_kernel(const __grid_constant__ CUtensorMap tmA, const double* __restrict__ Xp, int64_t m, int l,
+                      int64_t ntiles, int KB, double* __restrict__ Y) {
+  using Cfg = AxCfg<NT>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + Cfg::kStages * Cfg::kStageBytes);
+  uint64_t* empty = full + Cfg::kStages;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < Cfg::kStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], kConsumerWarps);
+    }
+    fence_barrier_init();
+  }
+  __syncthreads();
+
+  if (warp == kConsumerWarps) {
+    // ------------------------------------------------------------ producer
+    if (lane == 0) {
+      prefetch_tmap(&tmA);
+      int s = 0;
+      uint32_t ph = 0;
+      for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        for (int kb = 0; kb < KB; ++kb) {
+          mbar_wait(&empty[s], ph ^ 1);
+          uint8_t* st = smem + s * Cfg::kStageBytes;
+          mbar_arrive_expect_tx(&full[s], Cfg::kStageBytes);
+          tma_load_2d(st, &tmA, kb * BK, (int32_t)(tile * BM), &full[s]);
+          tma_load_2d(st + BM * 128, &tmA, kb * BK + 16, (int32_t)(tile * BM), &full[s]);
+          bulk_load(st + Cfg::kABytes, Xp + (int64_t)kb * 256 * NT, Cfg::kXBytes, &full[s]);
+          if (++s == Cfg::kStages) { s = 0; ph ^= 1; }
+        }
+      }
+    }
+    return;
+  }
+
+  // -------------------------------------------------------------- consumers
+  int s = 0;
+  uint32_t ph = 0;
+  const int rsel = lane >> 2;
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    double acc[2][NT][2];
+#pragma unroll
+    for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) acc[mt][nt][0] = acc[mt][nt][1] = 0.0;
+
+    for (int kb = 0; kb < KB; ++kb) {
+      mbar_wait(&full[s], ph);
+      const uint8_t* As = smem + s * Cfg::kStageBytes;
+      const double* Xs = reinterpret_cast<const double*>(As + Cfg::kABytes);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const uint8_t* box = As + (q >> 1) * (BM * 128);
+        const int chunk = 4 * (q & 1) + (lane & 3);
+        double2 a[2];
+#pragma unroll
+        for (int mt = 0; mt < 2; ++mt) {
+          const int r = warp * 16 + mt * 8 + rsel;
+          a[mt] = *reinterpret_cast<const double2*>(box + r * 128 + ((chunk ^ rsel) << 4));
+        }
+#pragma unroll
+        for (int ss = 0; ss < 2; ++ss) {
+          const int st = 2 * q + ss;
+#pragma unroll
+          for (int nt = 0; nt < NT; ++nt) {
+            const double b = Xs[(st * NT + nt) * 32 + lane];
+            dmma(acc[0][nt], ss ? a[0].y : a[0].x, b);
+            dmma(acc[1][nt], ss ? a[1].y : a[1].x, b);
+          }
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);
+      if (++s == Cfg::kStages) { s = 0; ph ^= 1; }
+    }
+    // epilogue: D rows = lane>>2, cols 2·(lane&3) + {0,1}
+#pragma unroll
+    for (int mt = 0; mt < 2; ++mt) {
+      const int64_t row = tile * BM + warp * 16 + mt * 8 + rsel;
+      if (row >= m) continue;
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) {
+        const int col = nt * 8 + 2 * (lane & 3);
+        double* y = Y + row * l + col;
+        if (col + 1 < l) {
+          if ((l & 1) == 0)
+            *reinterpret_cast<double2*>(y) = make_double2(acc[mt][nt][0], acc[mt][nt][1]);
+          else {
+            y[0] = acc[mt][nt][0];
+            y[1] = acc[mt][nt][1];
+          }
+        } else if (col < l) {
+          y[0] = acc[mt][nt][0];
+        }
+      }
+    }
+  }
+}
+
+// Generic CUDA-core fallback: 64-row tiles, X and A chunks staged in smem (fp64).
+template <class T>
+__global__ void __launch_bounds__(256) ax_generic_kernel(const T* __restrict__ A, int64_t m, int64_t n, int64_t lda,
+                                                         const double* __restrict__ X, int l,
+                                                         double* __restrict__ Y) {
+  __shared__ double As[64][33];
+  __shared__ double Xs[32][kMaxL];
+  const int64_t r0 = (int64_t)blockIdx.x * 64;
+  // thread → (row = tid & 63, column phase = tid >> 6): columns j = ph, ph+4, ...
+  const int r = threadIdx.x & 63, ph = threadIdx.x >> 6;
+  double acc[kMaxL / 4];
+#pragma unroll
+  for (int t = 0; t < kMaxL / 4; ++t) acc[t] = 0.0;
+  for (int64_t k0 = 0; k0 < n; k0 += 32) {
+    __syncthreads();
+    for (int idx = threadIdx.x; idx < 64 * 32; idx += 256) {
+      const int rr = idx >> 5, kk = idx & 31;
+      const int64_t gi = r0 + rr, gk = k0 + kk;
+      As[rr][kk] = (gi < m && gk < n) ? static_cast<double>(A[gi * lda + gk]) : 0.0;
+    }
+    for (int idx = threadIdx.x; idx < 32 * l; idx += 256) {
+      const int kk = idx / l, j = idx % l;
+      const int64_t gk = k0 + kk;
+      Xs[kk][j] = gk < n ? X[gk * l + j] : 0.0;
+    }
+    __syncthreads();
+#pragma unroll 4
+    for (int kk = 0; kk < 32; ++kk) {
+      const double a = As[r][kk];
+#pragma unroll
+      for (int t = 0; t < kMaxL / 4; ++t) {
+        const int j = ph + 4 * t;
+        if (j < l) acc[t] += a * Xs[kk][j];
+      }
+    }
+  }
+  const int64_t gi = r0 + r;
+  if (gi < m) {
+#pragma unroll
+    for (int t = 0; t < kMaxL / 4; ++t) {
+      const int j = ph + 4 * t;
+      if (j < l) Y[gi * l + j] = acc[t];
+    }
+  }
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    RPCA_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q));
+    RPCA_REQUIRE(q == cudaDriverEntryPointSuccess && p, RPCA_E_CUDA, "cuTensorMapEncodeTiled unavailable");
+    fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+template <int NT>
+void launch_ax_tma(Ctx& c, const DenseA& A, const double* Xp, int l, double* Y) {
+  using Cfg = AxCfg<NT>;
+  CUtensorMap tm;
+  cuuint64_t dims[2] = {(cuuint64_t)A.n, (cuuint64_t)A.m};
+  cuuint64_t strides[1] = {(cuuint64_t)A.lda * 8};
+  cuuint32_t box[2] = {16, BM};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = get_encode()(&tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<void*>(A.a), dims, strides, box, estr,
+                            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  RPCA_REQUIRE(r == CUDA_SUCCESS, RPCA_E_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+  static bool attr = false;
+  if (!attr) {
+    RPCA_CUDA(cudaFuncSetAttribute(ax_f64_tma_kernel<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmem));
+    attr = true;
+  }
+  const int64_t ntiles = cdiv(A.m, BM);
+  const int KB = (int)cdiv(A.n, BK);
+  const int grid = (int)std::min<int64_t>(ntiles, c.num_sms);
+  ax_f64_tma_kernel<NT><<<grid, kThreads, Cfg::kSmem, c.stream>>>(tm, Xp, A.m, l, ntiles, KB, Y);
+  RPCA_CHECK_LAUNCH();
+  count_launch(c, 1, "ax_f64_dmma");
+}
+
+bool tma_ok(const DenseA& A) {
+  return A.dtype == RPCA_F64 && ((reinterpret_cast<uintptr_t>(A.a) & 15u) == 0) && ((A.lda * 8) % 16 == 0) &&
+         A.n >= 1 && A.m >= 1 && A.lda * 8 < (int64_t(1) << 40);
+}
+
+}  // namespace
+
+size_t ax_ws_bytes(const DenseA& A, int l) {
+  Sizer s;
+  s.add<double>(packx_elems(A.n, l));
+  return s.total;
+}
+
+void dense_ax(Ctx& c, const DenseA& A, const double* X, int l, double* Y, Arena& ar) {
+  RPCA_REQUIRE(l >= 1 && l <= kMaxL, RPCA_E_SHAPE, "l=%d out of range [1,%d]", l, kMaxL);
+  if (A.m == 0) return;
+  if (tma_ok(A)) {
+    double* Xp = ar.get<double>(packx_elems(A.n, l));
+    pack_x(c, X, A.n, l, Xp);
+    switch ((l + 7) / 8) {
+      case 1: launch_ax_tma<1>(c, A, Xp, l, Y); break;
+      case 2: launch_ax_tma<2>(c, A, Xp, l, Y); break;
+      case 3: launch_ax_tma<3>(c, A, Xp, l, Y); break;
+      case 4: launch_ax_tma<4>(c, A, Xp, l, Y); break;
+      case 5: launch_ax_tma<5>(c, A, Xp, l, Y); break;
+      case 6: launch_ax_tma<6>(c, A, Xp, l, Y); break;
+      case 7: launch_ax_tma<7>(c, A, Xp, l, Y); break;
+      default: launch_ax_tma<8>(c, A, Xp, l, Y); break;
+    }
+    return;
+  }
+  const unsigned grid = (unsigned)cdiv(A.m, 64);
+  if (A.dtype == RPCA_F64)
+    ax_generic_kernel<double><<<grid, 256, 0, c.stream>>>((const double*)A.a, A.m, A.n, A.lda, X, l, Y);
+  else
+    ax_generic_kernel<float><<<grid, 256, 0, c.stream>>>((const float*)A.a, A.m, A.n, A.lda, X, l, Y);
+  RPCA_CHECK_LAUNCH();
+  count_launch(c, 1, "ax_generic");
+}
+
+}  // namespace rpca

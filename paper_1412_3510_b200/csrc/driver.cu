@@ -1,0 +1,435 @@
+// driver.cu — host orchestration of the randomized PCA path and the C ABI
+// (include/rpca.h).  Every arithmetic step runs in the kernels of this
+// library; this file only validates arguments, plans the workspace and
+// enqueues launches on the context's stream.
+//
+//   rpca_pca      — PAPER.md §2 eqs. (i1)-(i4) l.116-149, power iterations
+//                   l.186-204, LU inside / QR last §5 l.382-425, centring and
+//                   adjoint l.427-435.
+//   rpca_eigens   — PAPER.md §3 l.214-282 (stabilised Nyström), self-adjoint
+//                   loop l.386-412.
+//   rpca_diffsnorm— PAPER.md §4 l.362-371.
+#include <cstdarg>
+#include <cstring>
+#include <string>
+
+#include "internal.cuh"
+
+namespace rpca {
+
+static thread_local std::string g_last_error;
+
+void set_last_error(const char* fmt, ...) {
+  char buf[1024];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_last_error = buf;
+}
+
+const char* last_error_cstr() { return g_last_error.c_str(); }
+
+void prof_mark(Ctx& c, const char* name) {
+  if (c.prof_used == c.prof_pool.size()) {
+    cudaEvent_t e;
+    RPCA_CUDA(cudaEventCreate(&e));
+    c.prof_pool.push_back(e);
+  }
+  cudaEvent_t e = c.prof_pool[c.prof_used++];
+  RPCA_CUDA(cudaEventRecord(e, c.stream));
+  c.prof_recs.push_back(ProfRec{name, e});
+}
+
+Arena Ctx::arena(size_t bytes) {
+  if (bytes > ws_cap) {
+    if (ws) {
+      RPCA_CUDA(cudaStreamSynchronize(stream));
+      RPCA_CUDA(cudaFree(ws));
+      ws = nullptr;
+      ws_cap = 0;
+    }
+    const size_t want = bytes + (bytes >> 4) + (1 << 20);
+    cudaError_t e = cudaMalloc(&ws, want);
+    if (e != cudaSuccess) {
+      (void)cudaGetLastError();
+      set_last_error("workspace cudaMalloc(%zu) failed: %s", want, cudaGetErrorString(e));
+      throw Error{RPCA_E_NOMEM};
+    }
+    ws_cap = want;
+  }
+  Arena a;
+  a.base = ws;
+  a.cap = ws_cap;
+  a.off = 0;
+  return a;
+}
+
+namespace {
+
+int elem_size(int dtype) { return dtype == RPCA_F64 ? 8 : 4; }
+
+void validate_mat(const rpca_mat* A) {
+  RPCA_REQUIRE(A, RPCA_E_ARG, "A is NULL");
+  RPCA_REQUIRE(A->kind == RPCA_DENSE || A->kind == RPCA_CSR, RPCA_E_ARG, "bad kind %d", A->kind);
+  RPCA_REQUIRE(A->dtype == RPCA_F64 || A->dtype == RPCA_F32, RPCA_E_ARG, "bad dtype %d", A->dtype);
+  RPCA_REQUIRE(A->location == RPCA_DEVICE || A->location == RPCA_HOST, RPCA_E_ARG, "bad location");
+  RPCA_REQUIRE(A->m >= 1 && A->n >= 1, RPCA_E_SHAPE, "m=%lld n=%lld", (long long)A->m, (long long)A->n);
+  RPCA_REQUIRE(A->row0 >= 0 && A->m_local >= 0 && A->row0 + A->m_local <= A->m, RPCA_E_SHAPE, "bad row shard");
+  if (A->kind == RPCA_DENSE) {
+    RPCA_REQUIRE(A->a || A->m_local == 0, RPCA_E_ARG, "A.a is NULL");
+    RPCA_REQUIRE(A->lda >= A->n, RPCA_E_SHAPE, "lda < n");
+  } else {
+    RPCA_REQUIRE(A->kind != RPCA_CSR, RPCA_E_NOTIMPL, "CSR inputs are not implemented yet");
+  }
+}
+
+// Device view of A's local shard; copies a host A into the workspace.
+DenseA device_view(Ctx& c, const rpca_mat* A, Arena& ar) {
+  DenseA d{A->a, A->dtype, A->m_local, A->n, A->lda};
+  if (A->location == RPCA_HOST && A->m_local > 0) {
+    const size_t bytes = (size_t)A->m_local * A->lda * elem_size(A->dtype);
+    void* dev = ar.get<char>(bytes);
+    RPCA_CUDA(cudaMemcpyAsync(dev, A->a, bytes, cudaMemcpyHostToDevice, c.stream));
+    d.a = dev;
+  }
+  return d;
+}
+
+size_t host_copy_bytes(const rpca_mat* A) {
+  return A->location == RPCA_HOST ? (size_t)A->m_local * A->lda * elem_size(A->dtype) + 256 : 0;
+}
+
+// The operator the range finder sketches (reading Q6): F = A, or Aᵀ if m < n.
+struct Op {
+  DenseA A;
+  const double* cmean;
+  bool trans;
+};
+
+void apply_ax(Ctx& c, const DenseA& A, const double* cmean, const double* X, int l, double* Y, Arena& ar) {
+  const size_t mark = ar.off;
+  dense_ax(c, A, X, l, Y, ar);
+  if (cmean) {  // Y −= 1·(c·X)
+    double* cx = ar.get<double>(kMaxL);
+    weighted_colsum(c, cmean, X, A.n, l, cx, ar);
+    sub_rank1(c, Y, A.m, l, nullptr, cx);
+  }
+  ar.off = mark;
+}
+
+void apply_aty(Ctx& c, const DenseA& A, const double* cmean, const double* Y, int l, double* Z, Arena& ar) {
+  const size_t mark = ar.off;
+  dense_aty(c, A, Y, l, cmean, Z, ar);
+  ar.off = mark;
+}
+
+void fwd(Ctx& c, const Op& F, const double* X, int l, double* Y, Arena& ar) {
+  if (F.trans) apply_aty(c, F.A, F.cmean, X, l, Y, ar);
+  else apply_ax(c, F.A, F.cmean, X, l, Y, ar);
+}
+void adj(Ctx& c, const Op& F, const double* Y, int l, double* Z, Arena& ar) {
+  if (F.trans) apply_ax(c, F.A, F.cmean, Y, l, Z, ar);
+  else apply_aty(c, F.A, F.cmean, Y, l, Z, ar);
+}
+
+size_t op_ws(Ctx& c, const DenseA& A, int l) {
+  return std::max(ax_ws_bytes(A, l) + 4096 * 4, aty_ws_bytes(c, A, l)) + 65536;
+}
+
+void renorm_lu(Ctx& c, double* Y, int64_t rows, int l, Arena& ar) {
+  const size_t mark = ar.off;
+  lu_renorm(c, Y, rows, l, nullptr, nullptr, ar);
+  ar.off = mark;
+}
+void renorm_qr(Ctx& c, double* Y, int64_t rows, int l, double* R, Arena& ar) {
+  const size_t mark = ar.off;
+  qr(c, Y, rows, l, R, ar);
+  ar.off = mark;
+}
+
+void check_single_gpu(Ctx& c, const rpca_mat* A) {
+  RPCA_REQUIRE(c.comm != nullptr || (A->row0 == 0 && A->m_local == A->m), RPCA_E_SHAPE,
+               "row shard given but no communicator (rpca_comm_init)");
+  RPCA_REQUIRE(c.comm == nullptr, RPCA_E_NOTIMPL, "multi-GPU path not implemented yet");
+}
+
+void sync_status(Ctx& c) { RPCA_CUDA(cudaStreamSynchronize(c.stream)); }
+
+}  // namespace
+
+// ============================================================ rpca_pca
+void pca(Ctx& c, const rpca_mat* Am, int64_t k, int raw, int its, int64_t l, uint64_t seed, void* U, int64_t ldu,
+         void* S, void* V, int64_t ldv) {
+  validate_mat(Am);
+  check_single_gpu(c, Am);
+  if (l <= 0) l = k + 2;
+  const int64_t mn = std::min(Am->m, Am->n);
+  RPCA_REQUIRE(k >= 1 && l >= k && l <= mn && its >= 0, RPCA_E_SHAPE, "need 1 ≤ k ≤ l ≤ min(m,n), its ≥ 0");
+  RPCA_REQUIRE(l <= kMaxL, RPCA_E_SHAPE, "l=%lld > %d not supported", (long long)l, kMaxL);
+  RPCA_REQUIRE(U && S && V, RPCA_E_ARG, "U, S, V must not be NULL");
+  RPCA_REQUIRE(ldu >= k && ldv >= k, RPCA_E_SHAPE, "ldu, ldv must be ≥ k");
+  const int L = (int)l, K = (int)k;
+  const bool out_host = (c.flags & RPCA_FLAG_OUTPUTS_HOST) != 0;
+  const int dist = (c.flags & RPCA_FLAG_UNIFORM_OMEGA) ? RPCA_UNIFORM : RPCA_GAUSSIAN;
+  const int odt = Am->dtype, osz = elem_size(odt);
+  const int64_t m = Am->m, n = Am->n;
+
+  // ---- workspace plan
+  DenseA probe{Am->a, Am->dtype, m, n, Am->lda};
+  const bool trans = m < n;
+  const int64_t nin = trans ? m : n, nout = trans ? n : m;
+  Sizer sz;
+  sz.add<char>(host_copy_bytes(Am));
+  sz.add<double>(nin * l);   // Zb
+  sz.add<double>(nout * l);  // Yb
+  sz.add<double>(n);         // cmean
+  sz.add<double>(4 * l * l + 4 * l);
+  sz.add<double>(std::max(nin, nout) * k);  // V-side temp
+  sz.add<double>(k);                        // signs
+  if (out_host) {
+    sz.add<char>((size_t)m * ldu * osz);
+    sz.add<char>((size_t)n * ldv * osz);
+    sz.add<char>((size_t)k * osz);
+  }
+  const size_t fixed = sz.total;
+  size_t scratch = op_ws(c, probe, L);
+  scratch = std::max(scratch, lu_ws_bytes(std::max(nin, nout), L));
+  scratch = std::max(scratch, qr_ws_bytes(std::max(nin, nout), L));
+  scratch = std::max(scratch, (size_t)(cdiv(std::max(m, n), 8192) + 2) * (n + 2 * k) * 8 + 65536);
+  Arena ar = c.arena(fixed + scratch + 65536);
+
+  const DenseA dA = device_view(c, Am, ar);
+  double* Zb = ar.get<double>(nin * l);
+  double* Yb = ar.get<double>(nout * l);
+  double* cmean = ar.get<double>(n);
+  double* R = ar.get<double>(l * l);
+  double* W = ar.get<double>(l * l);
+  double* Vr = ar.get<double>(l * l);
+  double* sig = ar.get<double>(l);
+  double* side = ar.get<double>(std::max(nin, nout) * k);
+  double* sign = ar.get<double>(k);
+  void *Ud = U, *Vd = V, *Sd = S;
+  if (out_host) {
+    Ud = ar.get<char>((size_t)m * ldu * osz);
+    Vd = ar.get<char>((size_t)n * ldv * osz);
+    Sd = ar.get<char>((size_t)k * osz);
+  }
+
+  Op F{dA, nullptr, trans};
+  if (!raw) {
+    const size_t mark = ar.off;
+    colmeans_dense(c, dA.a, dA.dtype, dA.m, dA.n, dA.lda, m, cmean, ar);
+    ar.off = mark;
+    F.cmean = cmean;
+  }
+  // Ω (nin×l); the fp32 path consumes fl32(Ω) exactly as the oracle does
+  omega(c, seed, 0u, nin, l, dist, odt == RPCA_F32, Zb);
+  fwd(c, F, Zb, L, Yb, ar);
+  if (its == 0) renorm_qr(c, Yb, nout, L, nullptr, ar);
+  else renorm_lu(c, Yb, nout, L, ar);
+  for (int it = 1; it <= its; ++it) {
+    adj(c, F, Yb, L, Zb, ar);
+    renorm_lu(c, Zb, nin, L, ar);
+    fwd(c, F, Zb, L, Yb, ar);
+    if (it < its) renorm_lu(c, Yb, nout, L, ar);
+    else renorm_qr(c, Yb, nout, L, nullptr, ar);
+  }
+  // Bᵀ = F*·Q (eq. i2), Bᵀ = Q_B·R, R = Vr·Σ·Wᵀ ⇒ B = W Σ (Q_B Vr)ᵀ (eq. i3)
+  adj(c, F, Yb, L, Zb, ar);
+  renorm_qr(c, Zb, nin, L, R, ar);
+  jacobi_svd_small(c, R, L, sig, W, Vr);
+  {
+    const size_t mark = ar.off;
+    if (!trans) {
+      // V = Q_B·Vr[:, :k] (n×k), U = Q·W[:, :k] (m×k)  (eq. i4)
+      thin_gemm(c, Zb, nin, L, Vr, K, nullptr, side, k, RPCA_F64);
+      column_signs(c, side, n, K, k, sign, ar);
+      scale_cast(c, side, n, K, sign, Vd, ldv, odt);
+      thin_gemm(c, Yb, nout, L, W, K, sign, Ud, ldu, odt);
+    } else {
+      // sketched Aᵀ: its "U" = Q·W is A's V (n×k); its "V" = Q_B·Vr is A's U
+      thin_gemm(c, Yb, nout, L, W, K, nullptr, side, k, RPCA_F64);
+      column_signs(c, side, n, K, k, sign, ar);
+      scale_cast(c, side, n, K, sign, Vd, ldv, odt);
+      thin_gemm(c, Zb, nin, L, Vr, K, sign, Ud, ldu, odt);
+    }
+    copy_cast(c, sig, Sd, k, odt);
+    ar.off = mark;
+  }
+  if (out_host) {
+    RPCA_CUDA(cudaMemcpyAsync(U, Ud, (size_t)m * ldu * osz, cudaMemcpyDeviceToHost, c.stream));
+    RPCA_CUDA(cudaMemcpyAsync(V, Vd, (size_t)n * ldv * osz, cudaMemcpyDeviceToHost, c.stream));
+    RPCA_CUDA(cudaMemcpyAsync(S, Sd, (size_t)k * osz, cudaMemcpyDeviceToHost, c.stream));
+  }
+  sync_status(c);
+}
+
+// ============================================================ rpca_eigens
+void eigens(Ctx& c, const rpca_mat* Am, int64_t k, int its, int64_t l, uint64_t seed, int variant, void* U,
+            int64_t ldu, void* lam) {
+  validate_mat(Am);
+  check_single_gpu(c, Am);
+  RPCA_REQUIRE(Am->m == Am->n, RPCA_E_SHAPE, "eigens needs a square A");
+  RPCA_REQUIRE(variant == RPCA_SHIFT_CHOL || variant == RPCA_SQRT, RPCA_E_ARG, "bad variant");
+  if (l <= 0) l = k + 2;
+  const int64_t n = Am->n;
+  RPCA_REQUIRE(k >= 1 && l >= k && l <= n && its >= 0 && l <= kMaxL, RPCA_E_SHAPE, "bad k/l/its");
+  RPCA_REQUIRE(U && lam && ldu >= k, RPCA_E_ARG, "bad outputs");
+  const int L = (int)l, K = (int)k;
+  const bool out_host = (c.flags & RPCA_FLAG_OUTPUTS_HOST) != 0;
+  const int dist = (c.flags & RPCA_FLAG_UNIFORM_OMEGA) ? RPCA_UNIFORM : RPCA_GAUSSIAN;
+  const int odt = Am->dtype, osz = elem_size(odt);
+
+  DenseA probe{Am->a, Am->dtype, n, n, Am->lda};
+  Sizer sz;
+  sz.add<char>(host_copy_bytes(Am));
+  sz.add<double>(3 * n * l);
+  sz.add<double>(6 * l * l + 8 * l + 16);
+  if (out_host) {
+    sz.add<char>((size_t)n * ldu * osz);
+    sz.add<char>((size_t)k * osz);
+  }
+  size_t scratch = op_ws(c, probe, L);
+  scratch = std::max(scratch, lu_ws_bytes(n, L));
+  scratch = std::max(scratch, qr_ws_bytes(n, L));
+  scratch = std::max(scratch, (size_t)(cdiv(n, 8192) + 2) * l * l * 8 + 65536);
+  Arena ar = c.arena(sz.total + scratch + 65536);
+  const DenseA dA = device_view(c, Am, ar);
+  double* Q = ar.get<double>(n * l);
+  double* B1 = ar.get<double>(n * l);
+  double* Fm = ar.get<double>(n * l);
+  double* G = ar.get<double>(l * l);
+  double* Minv = ar.get<double>(l * l);
+  double* R = ar.get<double>(l * l);
+  double* W = ar.get<double>(l * l);
+  double* Vr = ar.get<double>(l * l);
+  double* sig = ar.get<double>(l);
+  double* scal = ar.get<double>(8);  // [0] = ‖B1‖_F², [1] = ν
+  int* status = ar.get<int>(4);
+  void *Ud = U, *Ld = lam;
+  if (out_host) {
+    Ud = ar.get<char>((size_t)n * ldu * osz);
+    Ld = ar.get<char>((size_t)k * osz);
+  }
+  // self-adjoint loop: Y = AΩ, then its × (Q = A·Q)
+  omega(c, seed, 0u, n, l, dist, odt == RPCA_F32, B1);
+  apply_ax(c, dA, nullptr, B1, L, Q, ar);
+  if (its == 0) renorm_qr(c, Q, n, L, nullptr, ar);
+  else renorm_lu(c, Q, n, L, ar);
+  for (int it = 1; it <= its; ++it) {
+    apply_ax(c, dA, nullptr, Q, L, B1, ar);
+    std::swap(Q, B1);
+    if (it < its) renorm_lu(c, Q, n, L, ar);
+    else renorm_qr(c, Q, n, L, nullptr, ar);
+  }
+  apply_ax(c, dA, nullptr, Q, L, B1, ar);  // (start) B1 = A·Q
+  {
+    const size_t mark = ar.off;
+    gram(c, Q, B1, n, L, G, ar);  // (second) QᵀB1, symmetrised in the kernel below
+    if (variant == RPCA_SHIFT_CHOL) {
+      // ‖B1‖_F² as a 1-column weighted sum over the n·l entries
+      weighted_colsum(c, B1, B1, n * l, 1, scal, ar);
+      nystrom_shift_chol(c, G, scal, L, n, odt == RPCA_F32 ? 0x1p-23 : 0x1p-52, Minv, scal + 1, status);
+      right_mult(c, B1, Q, scal + 1, Minv, n, L, Fm);  // F = (B1 + νQ)·C⁻¹ (eq. pseudo)
+    } else {
+      nystrom_sqrt(c, G, L, Minv, scal + 1, status);
+      right_mult(c, B1, nullptr, nullptr, Minv, n, L, Fm);  // F = B1·C⁺
+    }
+    ar.off = mark;
+  }
+  // F = U S Vᵀ: Q_F R_F = F, R_F = Vr Σ Wᵀ ⇒ U = Q_F·Vr; Σ = S² (eq. finish)
+  renorm_qr(c, Fm, n, L, R, ar);
+  jacobi_svd_small(c, R, L, sig, W, Vr);
+  {
+    const size_t mark = ar.off;
+    double* side = ar.get<double>(n * k);
+    double* sign = ar.get<double>(k);
+    thin_gemm(c, Fm, n, L, Vr, K, nullptr, side, k, RPCA_F64);
+    column_signs(c, side, n, K, k, sign, ar);
+    scale_cast(c, side, n, K, sign, Ud, ldu, odt);
+    nystrom_lambda(c, sig, scal + 1, K, Ld, odt);
+    ar.off = mark;
+  }
+  int st = 0;
+  RPCA_CUDA(cudaMemcpyAsync(&st, status, sizeof(int), cudaMemcpyDeviceToHost, c.stream));
+  sync_status(c);
+  RPCA_REQUIRE(st != 1, RPCA_E_NOTPSD, "Nyström: B2 is not positive definite after the shifts (PAPER.md:262-273)");
+  if (st == 2) {  // A·Q = 0: λ = 0, U = Q[:, :k] (DESIGN.md reading)
+    const size_t mark = ar.off;
+    double* sign = ar.get<double>(k);
+    double* side = ar.get<double>(n * k);
+    RPCA_CUDA(cudaMemcpy2DAsync(side, k * 8, Q, l * 8, k * 8, n, cudaMemcpyDeviceToDevice, c.stream));
+    column_signs(c, side, n, K, k, sign, ar);
+    scale_cast(c, side, n, K, sign, Ud, ldu, odt);
+    RPCA_CUDA(cudaMemsetAsync(Ld, 0, (size_t)k * osz, c.stream));
+    ar.off = mark;
+  }
+  if (out_host) {
+    RPCA_CUDA(cudaMemcpyAsync(U, Ud, (size_t)n * ldu * osz, cudaMemcpyDeviceToHost, c.stream));
+    RPCA_CUDA(cudaMemcpyAsync(lam, Ld, (size_t)k * osz, cudaMemcpyDeviceToHost, c.stream));
+  }
+  sync_status(c);
+}
+
+// ============================================================ rpca_diffsnorm
+void diffsnorm(Ctx& c, const rpca_mat* Am, int raw, const double* U, int64_t ldu, const double* S, const double* V,
+               int64_t ldv, int64_t k, int its, uint64_t seed, double* out) {
+  validate_mat(Am);
+  check_single_gpu(c, Am);
+  RPCA_REQUIRE(k >= 0 && its >= 1 && out, RPCA_E_SHAPE, "bad k/its/out");
+  RPCA_REQUIRE(k == 0 || (U && S && V && ldu >= k && ldv >= k), RPCA_E_ARG, "bad factors");
+  const int64_t m = Am->m, n = Am->n;
+  DenseA probe{Am->a, Am->dtype, m, n, Am->lda};
+  Sizer sz;
+  sz.add<char>(host_copy_bytes(Am));
+  sz.add<double>(2 * n + m + n + k + 64);
+  size_t scratch = op_ws(c, probe, 1) + (size_t)(cdiv(std::max(m, n), 8192) + 2) * (n + 64) * 8;
+  Arena ar = c.arena(sz.total + scratch + 65536);
+  const DenseA dA = device_view(c, Am, ar);
+  double* x = ar.get<double>(n);
+  double* z = ar.get<double>(n);
+  double* y = ar.get<double>(m);
+  double* cmean = ar.get<double>(n);
+  double* t = ar.get<double>(std::max<int64_t>(k, 1));
+  double* sc = ar.get<double>(8);  // [0] nz2, [1] est
+  int* done = ar.get<int>(4);
+  if (!raw) {
+    const size_t mark = ar.off;
+    colmeans_dense(c, dA.a, dA.dtype, dA.m, dA.n, dA.lda, m, cmean, ar);
+    ar.off = mark;
+  }
+  const double* cm = raw ? nullptr : cmean;
+  RPCA_CUDA(cudaMemsetAsync(done, 0, sizeof(int), c.stream));
+  RPCA_CUDA(cudaMemsetAsync(sc, 0, 8 * sizeof(double), c.stream));
+  omega(c, seed, 1u, n, 1, RPCA_GAUSSIAN, 0, z);
+  {
+    const size_t mark = ar.off;
+    weighted_colsum(c, z, z, n, 1, sc, ar);
+    ar.off = mark;
+  }
+  // normalise the start vector without touching est/done: use a scratch est slot
+  power_step(c, sc, z, x, n, sc + 2, done + 1);
+  for (int it = 0; it < its; ++it) {
+    const size_t mark = ar.off;
+    apply_ax(c, dA, cm, x, 1, y, ar);  // y = A x [− 1 (c·x)]
+    if (k > 0) {                       // y −= U (S ⊙ (Vᵀx))
+      weighted_colsum(c, x, V, n, (int)k, t, ar, ldv);
+      hadamard(c, t, S, (int)k);
+      rank_k_sub(c, y, U, ldu, t, m, (int)k);
+    }
+    apply_aty(c, dA, cm, y, 1, z, ar);  // z = Aᵀ y [− cᵀ (1ᵀy)]
+    if (k > 0) {                        // z −= V (S ⊙ (Uᵀy))
+      weighted_colsum(c, y, U, m, (int)k, t, ar, ldu);
+      hadamard(c, t, S, (int)k);
+      rank_k_sub(c, z, V, ldv, t, n, (int)k);
+    }
+    weighted_colsum(c, z, z, n, 1, sc, ar);  // ‖z‖²
+    power_step(c, sc, z, x, n, sc + 1, done);
+    ar.off = mark;
+  }
+  RPCA_CUDA(cudaMemcpyAsync(out, sc + 1, sizeof(double), cudaMemcpyDeviceToHost, c.stream));
+  sync_status(c);
+}
+
+}  // namespace rpca

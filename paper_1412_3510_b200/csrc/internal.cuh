@@ -1,0 +1,144 @@
+// internal.cuh — host-side interfaces between the driver and the kernel
+// launchers of the randomized-PCA path.  Not part of the C ABI.
+#pragma once
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstddef>
+#include <cstdint>
+#include <vector>
+
+#include "common.cuh"
+
+namespace rpca {
+
+constexpr int kMaxL = 64;  // widest sketch the l×l kernels (one CTA) support
+
+// ---------------------------------------------------------------- workspace
+struct Arena {
+  char* base = nullptr;
+  size_t cap = 0;
+  size_t off = 0;
+  static size_t align(size_t b) { return (b + 255) & ~size_t(255); }
+  template <class T>
+  T* get(size_t count) {
+    size_t bytes = align(count * sizeof(T));
+    RPCA_REQUIRE(off + bytes <= cap, RPCA_E_WORKSPACE, "workspace overflow (%zu + %zu > %zu)", off, bytes, cap);
+    T* p = reinterpret_cast<T*>(base + off);
+    off += bytes;
+    return p;
+  }
+};
+
+// Bytes a sequence of get<T>(count) calls needs (same rounding as Arena).
+struct Sizer {
+  size_t total = 0;
+  template <class T>
+  void add(size_t count) { total += Arena::align(count * sizeof(T)); }
+};
+
+struct Comm;  // multi-GPU communicator (comm.cu)
+
+// Optional per-launch timing (rpca_profile): an event is recorded on the
+// context stream after every launch; a launch's duration is the gap to the
+// previous event (launches are stream-serialised).
+struct ProfRec {
+  const char* name;
+  cudaEvent_t ev;
+};
+
+struct Ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  uint32_t flags = 0;
+  int num_sms = 148;
+  char* ws = nullptr;
+  size_t ws_cap = 0;
+  int64_t launches = 0;
+  Comm* comm = nullptr;
+  bool prof = false;
+  std::vector<ProfRec> prof_recs;
+  std::vector<cudaEvent_t> prof_pool;
+  size_t prof_used = 0;
+  Arena arena(size_t bytes);  // ensures capacity, returns an arena over the workspace
+};
+
+void prof_mark(Ctx& c, const char* name);
+inline void count_launch(Ctx& c, int n = 1, const char* name = "misc") {
+  c.launches += n;
+  if (c.prof) prof_mark(c, name);
+}
+
+// ---------------------------------------------------------------- kernels
+// omega.cu
+void omega(Ctx& c, uint64_t seed, uint32_t sid, int64_t rows, int64_t cols, int dist, int round32, double* out);
+
+// thin.cu — small kernels on thin blocks
+// Packed operand layouts for the DMMA kernels (see dense_ax.cu / dense_aty.cu)
+int64_t packx_elems(int64_t n, int l);   // doubles in the packed X of an n×l block
+int64_t packy_elems(int64_t m, int l);   // doubles in the packed Y of an m×l block
+void pack_x(Ctx& c, const double* X, int64_t n, int l, double* Xp);
+void pack_y(Ctx& c, const double* Y, int64_t m, int l, double* Yp);
+// v[j] = Σ_k a[k]·X[k][j] (a may be NULL ⇒ all-ones), fixed-order reduction
+void weighted_colsum(Ctx& c, const double* a, const double* X, int64_t rows, int l, double* v, Arena& ar,
+                     int64_t ldx = 0);
+void sub_rank1(Ctx& c, double* Y, int64_t rows, int l, const double* u /*rows or NULL=ones*/, const double* v);
+void colmeans_dense(Ctx& c, const void* A, int dtype, int64_t m, int64_t n, int64_t lda, int64_t m_total,
+                    double* cmean, Arena& ar);
+// Out (rows×k, ld ldo, dtype out_dtype) = In (rows×l) · W[:, :k] (W l×l) · diag(sign)
+void thin_gemm(Ctx& c, const double* In, int64_t rows, int l, const double* W, int k, const double* sign,
+               void* Out, int64_t ldo, int out_dtype);
+// sign[j] = sign of the largest-|·| entry of column j of V (rows×k), lowest index on ties
+void column_signs(Ctx& c, const double* V, int64_t rows, int k, int64_t ldv, double* sign, Arena& ar);
+void copy_cast(Ctx& c, const double* src, void* dst, int64_t count, int dtype);
+// dst (rows×k, ld ldd, dtype) = src (rows×k, ld k) · diag(sign)   (sign may be NULL)
+void scale_cast(Ctx& c, const double* src, int64_t rows, int k, const double* sign, void* dst, int64_t ldd, int dtype);
+// G (l×l) = Xᵀ·Y over rows (fixed-order two-stage reduction)
+void gram(Ctx& c, const double* X, const double* Y, int64_t rows, int l, double* G, Arena& ar);
+// Out (rows×l) = (In + ν·Q)·M, ν read from device (Q may be NULL ⇒ Out = In·M)
+void right_mult(Ctx& c, const double* In, const double* Q, const double* nu, const double* M, int64_t rows, int l,
+                double* Out);
+// y −= U·t  (U rows×k, ld ldu)
+void rank_k_sub(Ctx& c, double* y, const double* U, int64_t ldu, const double* t, int64_t rows, int k);
+// t ← t ⊙ S
+void hadamard(Ctx& c, double* t, const double* S, int k);
+
+// dense_ax.cu / dense_aty.cu
+struct DenseA {
+  const void* a;
+  int dtype;
+  int64_t m, n, lda;  // m = local rows
+};
+size_t ax_ws_bytes(const DenseA& A, int l);
+void dense_ax(Ctx& c, const DenseA& A, const double* X, int l, double* Y, Arena& ar);
+size_t aty_ws_bytes(Ctx& c, const DenseA& A, int l);
+// Z (n×l) = Aᵀ·Y [− cmean ⊗ colsum(Y)] (cmean may be NULL)
+void dense_aty(Ctx& c, const DenseA& A, const double* Y, int l, const double* cmean, double* Z, Arena& ar);
+
+// tslu.cu
+size_t lu_ws_bytes(int64_t m, int l);
+void lu_renorm(Ctx& c, double* Y, int64_t m, int l, double* U_out, int64_t* piv_out, Arena& ar);
+
+// tsqr.cu
+size_t qr_ws_bytes(int64_t m, int l);
+void qr(Ctx& c, double* Y, int64_t m, int l, double* R_out, Arena& ar);
+
+// small.cu — one-CTA l×l kernels
+// R (l×l) → Jacobi: R·W = Vr·diag(sigma); sigma sorted, Vr completed.
+void jacobi_svd_small(Ctx& c, const double* R, int l, double* sigma, double* W, double* Vr);
+// Nyström SHIFT_CHOL: from G = QᵀB1 (l×l) and fro2 = ‖B1‖_F²:
+// B2 = sym(G), ν = u·√n·‖B1‖_F, C = chol(B2 + νI) with ν ×10 on failure (≤ 5
+// retries); writes Minv = C⁻¹ (upper), nu, status (0 ok, 1 not PSD, 2 zero B1).
+void nystrom_shift_chol(Ctx& c, const double* G, const double* fro2, int l, int64_t n, double unit_roundoff,
+                        double* Minv, double* nu, int* status);
+// Nyström SQRT: B2 = sym(G) = E·diag(μ)·Eᵀ (Jacobi), Minv =
+// E·diag(μ^-1/2 or 0)·Eᵀ (cut-off 1e-12·sqrt(max μ)); status 1 if min μ < -1e-6·max|μ|.
+void nystrom_sqrt(Ctx& c, const double* G, int l, double* Minv, double* nu, int* status);
+// lam[j] = max(σ_j² − ν, 0)   (eq. finish), cast to dtype
+void nystrom_lambda(Ctx& c, const double* sigma, const double* nu, int k, void* lam, int dtype);
+// power-method scalar step: nz = sqrt(nz2); est = done ? est : (nz == 0 ? 0 : sqrt(nz));
+// x = nz > 0 ? z/nz : 0
+void power_step(Ctx& c, const double* nz2, double* z, double* x, int64_t n, double* est, int* done);
+
+}  // namespace rpca

@@ -1,0 +1,383 @@
+// small.cu — the l×l work of §8(a) step a7 and of the Nyström path, in one
+// CTA each (l ≤ 64: a 32 KB fp64 matrix in shared memory).
+//
+// jacobi_svd_small: the SVD of eq. (i3), PAPER.md:133-139 ("W Σ V* = B"),
+// applied to the l×l triangular factor R of Bᵀ = Q_B·R (so B = Rᵀ Q_Bᵀ).
+// One-sided Hestenes Jacobi on the columns of R (readings Q9/Q18):
+// rotate a pair iff |γ| > 2^-52·sqrt(αβ), stop after a sweep without a
+// rotation or after 30 sweeps.  Pairs are scheduled in parallel rounds
+// (round-robin tournament: l/2 disjoint pairs per round, one warp per pair);
+// the oracle sweeps cyclically — same fixed point up to rounding.
+// Result: R·W = Vr·diag(σ), σ sorted non-increasing (stable), zero-σ
+// columns of Vr completed by Gram–Schmidt of e_1, e_2, ….
+#include "internal.cuh"
+
+namespace rpca {
+namespace {
+
+constexpr int kThreads = 256;
+constexpr int kWarps = kThreads / 32;
+
+__global__ void __launch_bounds__(kThreads) jacobi_kernel(const double* __restrict__ R, int l,
+                                                          double* __restrict__ sigma, double* __restrict__ Wout,
+                                                          double* __restrict__ Vout) {
+  // column-major: Mc[p*l + i] = M[i][p]; Wc likewise
+  extern __shared__ double sm[];
+  double* Mc = sm;
+  double* Wc = sm + l * l;
+  __shared__ double nrm[kMaxL];
+  __shared__ int rank_[kMaxL];
+  __shared__ int rotated;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int idx = tid; idx < l * l; idx += kThreads) {
+    const int i = idx / l, p = idx % l;
+    Mc[p * l + i] = R[idx];
+    Wc[p * l + i] = (i == p) ? 1.0 : 0.0;
+  }
+  __syncthreads();
+  const int lp = (l + 1) & ~1;  // players (one dummy if l is odd)
+  const double eps = 0x1p-52;
+  for (int sweep = 0; sweep < 30 && l > 1; ++sweep) {
+    if (tid == 0) rotated = 0;
+    __syncthreads();
+    for (int round = 0; round < lp - 1; ++round) {
+      for (int k = warp; k < lp / 2; k += kWarps) {
+        auto player = [&](int i) { return i == 0 ? 0 : 1 + ((i - 1 + round) % (lp - 1)); };
+        int p = player(k), q = player(lp - 1 - k);
+        if (p > q) { const int t = p; p = q; q = t; }
+        if (q >= l) continue;  // dummy
+        double a = 0.0, b = 0.0, g = 0.0;
+        for (int i = lane; i < l; i += 32) {
+          const double x = Mc[p * l + i], y = Mc[q * l + i];
+          a += x * x;
+          b += y * y;
+          g += x * y;
+        }
+        a = warp_sum(a);
+        b = warp_sum(b);
+        g = warp_sum(g);
+        if (!(fabs(g) > eps * sqrt(a * b))) continue;
+        if (lane == 0) rotated = 1;
+        const double zeta = (b - a) / (2.0 * g);
+        const double t = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
+        const double cs = 1.0 / sqrt(1.0 + t * t), sn = cs * t;
+        for (int i = lane; i < l; i += 32) {
+          const double x = Mc[p * l + i], y = Mc[q * l + i];
+          Mc[p * l + i] = cs * x - sn * y;
+          Mc[q * l + i] = sn * x + cs * y;
+          const double u = Wc[p * l + i], v = Wc[q * l + i];
+          Wc[p * l + i] = cs * u - sn * v;
+          Wc[q * l + i] = sn * u + cs * v;
+        }
+      }
+      __syncthreads();
+    }
+    if (!rotated) break;
+    __syncthreads();
+  }
+  // σ_p = ‖M[:, p]‖
+  for (int p = warp; p < l; p += kWarps) {
+    double s = 0.0;
+    for (int i = lane; i < l; i += 32) s += Mc[p * l + i] * Mc[p * l + i];
+    s = warp_sum(s);
+    if (lane == 0) nrm[p] = sqrt(s);
+  }
+  __syncthreads();
+  if (tid < l) {  // stable descending rank
+    int r = 0;
+    for (int i = 0; i < l; ++i) r += (nrm[i] > nrm[tid]) || (nrm[i] == nrm[tid] && i < tid);
+    rank_[tid] = r;
+  }
+  __syncthreads();
+  for (int idx = tid; idx < l * l; idx += kThreads) {
+    const int p = idx / l, i = idx % l;
+    const int rp = rank_[p];
+    Wout[i * l + rp] = Wc[p * l + i];
+    Vout[i * l + rp] = nrm[p] > 0.0 ? Mc[p * l + i] / nrm[p] : 0.0;
+  }
+  if (tid < l) sigma[rank_[tid]] = nrm[tid];
+  __syncthreads();
+  __threadfence_block();
+  // zero-σ completion (rare): Gram–Schmidt of e_t against the other columns
+  if (tid == 0) {
+    for (int col = 0; col < l; ++col) {
+      if (sigma[col] > 0.0) continue;
+      double best = -1.0;
+      double v[kMaxL], bv[kMaxL];
+      for (int t = 0; t < l; ++t) {
+        for (int i = 0; i < l; ++i) v[i] = (i == t) ? 1.0 : 0.0;
+        for (int pass = 0; pass < 2; ++pass)
+          for (int s = 0; s < l; ++s) {
+            if (s == col || (sigma[s] == 0.0 && s > col)) continue;
+            double d = 0.0;
+            for (int i = 0; i < l; ++i) d += Vout[i * l + s] * v[i];
+            for (int i = 0; i < l; ++i) v[i] -= d * Vout[i * l + s];
+          }
+        double nv = 0.0;
+        for (int i = 0; i < l; ++i) nv += v[i] * v[i];
+        nv = sqrt(nv);
+        if (nv > best) {
+          best = nv;
+          for (int i = 0; i < l; ++i) bv[i] = v[i];
+        }
+        if (nv >= 0.5) break;
+      }
+      for (int i = 0; i < l; ++i) Vout[i * l + col] = bv[i] / best;
+    }
+  }
+}
+
+
+// ---------------------------------------------------------------- Nyström
+// Upper inverse X = C⁻¹ of an upper-triangular l×l C (thread per column).
+__device__ void upper_inverse(const double* C, int l, double* X) {
+  const int j = threadIdx.x;
+  if (j < l) {
+    for (int i = 0; i < l; ++i) X[i * l + j] = 0.0;
+    X[j * l + j] = 1.0 / C[j * l + j];
+    for (int i = j - 1; i >= 0; --i) {
+      double s = 0.0;
+      for (int t = i + 1; t <= j; ++t) s += C[i * l + t] * X[t * l + j];
+      X[i * l + j] = -s / C[i * l + i];
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kThreads) shift_chol_kernel(const double* __restrict__ G,
+                                                              const double* __restrict__ fro2, int l, double sqrt_n,
+                                                              double u, double* __restrict__ Minv,
+                                                              double* __restrict__ nu_out, int* __restrict__ status) {
+  extern __shared__ double sm[];
+  double* B = sm;          // l×l, B2 = sym(G)
+  double* C = sm + l * l;  // upper Cholesky factor
+  __shared__ int fail;
+  __shared__ double nu_s;
+  const int tid = threadIdx.x;
+  for (int idx = tid; idx < l * l; idx += kThreads) {
+    const int p = idx / l, q = idx % l;
+    B[idx] = 0.5 * (G[p * l + q] + G[q * l + p]);
+  }
+  const double fro = sqrt(*fro2);
+  if (tid == 0) nu_s = u * sqrt_n * fro;
+  __syncthreads();
+  if (fro == 0.0) {  // A·Q = 0: nothing to approximate (DESIGN.md reading)
+    for (int idx = tid; idx < l * l; idx += kThreads) Minv[idx] = (idx / l == idx % l) ? 1.0 : 0.0;
+    if (tid == 0) { *nu_out = 0.0; *status = 2; }
+    return;
+  }
+  int ok = 0;
+  for (int attempt = 0; attempt <= 5 && !ok; ++attempt) {
+    if (tid == 0) fail = 0;
+    for (int idx = tid; idx < l * l; idx += kThreads) C[idx] = 0.0;
+    __syncthreads();
+    const double nu = nu_s;
+    for (int j = 0; j < l; ++j) {
+      if (tid == 0) {
+        double d = B[j * l + j] + nu;
+        for (int t = 0; t < j; ++t) d -= C[t * l + j] * C[t * l + j];
+        if (!(d > 0.0)) fail = 1;
+        else C[j * l + j] = sqrt(d);
+      }
+      __syncthreads();
+      if (fail) break;
+      for (int i = j + 1 + tid; i < l; i += kThreads) {
+        double s = B[j * l + i];
+        for (int t = 0; t < j; ++t) s -= C[t * l + j] * C[t * l + i];
+        C[j * l + i] = s / C[j * l + j];
+      }
+      __syncthreads();
+    }
+    if (!fail) ok = 1;
+    else {
+      __syncthreads();
+      if (tid == 0) nu_s *= 10.0;
+      __syncthreads();
+    }
+  }
+  if (!ok) {
+    if (tid == 0) { *nu_out = nu_s; *status = 1; }
+    return;
+  }
+  upper_inverse(C, l, B);  // reuse B as X
+  __syncthreads();
+  for (int idx = tid; idx < l * l; idx += kThreads) Minv[idx] = B[idx];
+  if (tid == 0) { *nu_out = nu_s; *status = 0; }
+}
+
+// Parallel (Brent–Luk) two-sided Jacobi on the symmetric l×l B2; then the
+// regularised inverse square root Minv = E·diag(d)·Eᵀ.
+__global__ void __launch_bounds__(kThreads) sqrt_inv_kernel(const double* __restrict__ G, int l,
+                                                            double* __restrict__ Minv, double* __restrict__ nu_out,
+                                                            int* __restrict__ status) {
+  extern __shared__ double sm[];
+  double* A = sm;          // l×l row-major
+  double* E = sm + l * l;  // eigenvectors (columns)
+  __shared__ double cs_[kMaxL / 2], sn_[kMaxL / 2];
+  __shared__ int pp_[kMaxL / 2], qq_[kMaxL / 2];
+  __shared__ int rotated;
+  __shared__ double mu[kMaxL], dd[kMaxL];
+  __shared__ int rk[kMaxL];
+  const int tid = threadIdx.x;
+  for (int idx = tid; idx < l * l; idx += kThreads) {
+    const int p = idx / l, q = idx % l;
+    A[idx] = 0.5 * (G[p * l + q] + G[q * l + p]);
+    E[idx] = (p == q) ? 1.0 : 0.0;
+  }
+  __syncthreads();
+  const int lp = (l + 1) & ~1;
+  const double eps = 0x1p-52;
+  for (int sweep = 0; sweep < 30 && l > 1; ++sweep) {
+    if (tid == 0) rotated = 0;
+    __syncthreads();
+    for (int round = 0; round < lp - 1; ++round) {
+      for (int k = tid; k < lp / 2; k += kThreads) {
+        auto player = [&](int i) { return i == 0 ? 0 : 1 + ((i - 1 + round) % (lp - 1)); };
+        int p = player(k), q = player(lp - 1 - k);
+        if (p > q) { const int t = p; p = q; q = t; }
+        double c = 1.0, s = 0.0;
+        if (q < l) {
+          const double apq = A[p * l + q], app = A[p * l + p], aqq = A[q * l + q];
+          if (fabs(apq) > eps * sqrt(fabs(app * aqq))) {
+            const double zeta = (aqq - app) / (2.0 * apq);
+            const double t = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
+            c = 1.0 / sqrt(1.0 + t * t);
+            s = c * t;
+            rotated = 1;
+          }
+        }
+        pp_[k] = p; qq_[k] = q; cs_[k] = c; sn_[k] = s;
+      }
+      __syncthreads();
+      // columns: A ← A·J, E ← E·J
+      for (int idx = tid; idx < (lp / 2) * l; idx += kThreads) {
+        const int k = idx / l, r = idx % l;
+        const int p = pp_[k], q = qq_[k];
+        if (q >= l || sn_[k] == 0.0) continue;
+        const double c = cs_[k], s = sn_[k];
+        const double x = A[r * l + p], y = A[r * l + q];
+        A[r * l + p] = c * x - s * y;
+        A[r * l + q] = s * x + c * y;
+        const double u = E[r * l + p], v = E[r * l + q];
+        E[r * l + p] = c * u - s * v;
+        E[r * l + q] = s * u + c * v;
+      }
+      __syncthreads();
+      // rows: A ← Jᵀ·A
+      for (int idx = tid; idx < (lp / 2) * l; idx += kThreads) {
+        const int k = idx / l, r = idx % l;
+        const int p = pp_[k], q = qq_[k];
+        if (q >= l || sn_[k] == 0.0) continue;
+        const double c = cs_[k], s = sn_[k];
+        const double x = A[p * l + r], y = A[q * l + r];
+        A[p * l + r] = c * x - s * y;
+        A[q * l + r] = s * x + c * y;
+      }
+      __syncthreads();
+      for (int k = tid; k < lp / 2; k += kThreads)
+        if (qq_[k] < l && sn_[k] != 0.0) A[pp_[k] * l + qq_[k]] = A[qq_[k] * l + pp_[k]] = 0.0;
+      __syncthreads();
+    }
+    if (!rotated) break;
+    __syncthreads();
+  }
+  if (tid < l) {
+    int r = 0;
+    const double v = A[tid * l + tid];
+    for (int i = 0; i < l; ++i) {
+      const double w = A[i * l + i];
+      r += (w > v) || (w == v && i < tid);
+    }
+    rk[tid] = r;
+  }
+  __syncthreads();
+  if (tid < l) mu[rk[tid]] = A[tid * l + tid];
+  __syncthreads();
+  if (tid == 0) {
+    double mx = 0.0;
+    for (int j = 0; j < l; ++j) mx = fmax(mx, fabs(mu[j]));
+    const int bad = mu[l - 1] < -1e-6 * mx;
+    const double smax = sqrt(fmax(mu[0], 0.0));
+    for (int j = 0; j < l; ++j) {
+      const double sj = sqrt(fmax(mu[j], 0.0));
+      dd[j] = (sj > 1e-12 * smax && sj > 0.0) ? 1.0 / sj : 0.0;
+    }
+    *status = bad ? 1 : 0;
+    *nu_out = 0.0;
+  }
+  __syncthreads();
+  // Minv[p][q] = Σ_t E[p][t'] d_t E[q][t'] where t' is the column of rank t
+  for (int idx = tid; idx < l * l; idx += kThreads) {
+    const int p = idx / l, q = idx % l;
+    double s = 0.0;
+    for (int t = 0; t < l; ++t) s += E[p * l + t] * dd[rk[t]] * E[q * l + t];
+    Minv[idx] = s;
+  }
+}
+
+template <class T>
+__global__ void lambda_kernel(const double* __restrict__ sigma, const double* __restrict__ nu, int k,
+                              T* __restrict__ lam) {
+  const int j = threadIdx.x;
+  if (j < k) {
+    const double v = sigma[j] * sigma[j] - *nu;
+    lam[j] = static_cast<T>(v > 0.0 ? v : 0.0);
+  }
+}
+
+__global__ void power_step_kernel(const double* __restrict__ nz2, double* __restrict__ z, double* __restrict__ x,
+                                  int64_t n, double* __restrict__ est, int* __restrict__ done) {
+  const double nz = sqrt(*nz2);
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    if (!*done) {
+      if (nz == 0.0) { *est = 0.0; *done = 1; }
+      else *est = sqrt(nz);
+    }
+  }
+  const double inv = nz > 0.0 ? 1.0 / nz : 0.0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    x[i] = z[i] * inv;
+}
+
+}  // namespace
+
+void jacobi_svd_small(Ctx& c, const double* R, int l, double* sigma, double* W, double* Vr) {
+  RPCA_REQUIRE(l >= 1 && l <= kMaxL, RPCA_E_SHAPE, "jacobi: l=%d", l);
+  const int smem = 2 * l * l * 8;
+  RPCA_CUDA(cudaFuncSetAttribute(jacobi_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * kMaxL * kMaxL * 8));
+  jacobi_kernel<<<1, kThreads, smem, c.stream>>>(R, l, sigma, W, Vr);
+  RPCA_CHECK_LAUNCH();
+  count_launch(c, 1, "jacobi");
+}
+
+
+void nystrom_shift_chol(Ctx& c, const double* G, const double* fro2, int l, int64_t n, double unit_roundoff,
+                        double* Minv, double* nu, int* status) {
+  RPCA_CUDA(cudaFuncSetAttribute(shift_chol_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * kMaxL * kMaxL * 8));
+  shift_chol_kernel<<<1, kThreads, 2 * l * l * 8, c.stream>>>(G, fro2, l, sqrt((double)n), unit_roundoff, Minv, nu,
+                                                              status);
+  RPCA_CHECK_LAUNCH();
+  count_launch(c);
+}
+
+void nystrom_sqrt(Ctx& c, const double* G, int l, double* Minv, double* nu, int* status) {
+  RPCA_CUDA(cudaFuncSetAttribute(sqrt_inv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * kMaxL * kMaxL * 8));
+  sqrt_inv_kernel<<<1, kThreads, 2 * l * l * 8, c.stream>>>(G, l, Minv, nu, status);
+  RPCA_CHECK_LAUNCH();
+  count_launch(c);
+}
+
+void nystrom_lambda(Ctx& c, const double* sigma, const double* nu, int k, void* lam, int dtype) {
+  if (dtype == RPCA_F64) lambda_kernel<double><<<1, 64, 0, c.stream>>>(sigma, nu, k, (double*)lam);
+  else lambda_kernel<float><<<1, 64, 0, c.stream>>>(sigma, nu, k, (float*)lam);
+  RPCA_CHECK_LAUNCH();
+  count_launch(c);
+}
+
+void power_step(Ctx& c, const double* nz2, double* z, double* x, int64_t n, double* est, int* done) {
+  const unsigned grid = (unsigned)std::min<int64_t>(std::max<int64_t>(1, cdiv(n, 256)), (int64_t)c.num_sms * 8);
+  power_step_kernel<<<grid, 256, 0, c.stream>>>(nz2, z, x, n, est, done);
+  RPCA_CHECK_LAUNCH();
+  count_launch(c);
+}
+
+}  // namespace rpca

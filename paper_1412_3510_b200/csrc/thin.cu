@@ -1,0 +1,414 @@
+// thin.cu — kernels on the thin blocks (m×l, n×l, l×l) of the randomized PCA
+// path: operand packing for the DMMA kernels, the rank-1 centring corrections
+// of PAPER.md:427-435 ("Q = A*Q - ones(m,1)*(c*Q)"), column means
+// (PAPER.md:428-429), the lift U = Q·W of eq. (i4) and
+// the sign convention of DESIGN.md reading Q10.  All HBM-bound; every
+// reduction runs in a fixed order (fixed row chunks, ascending).
+#include "internal.cuh"
+
+namespace rpca {
+namespace {
+
+constexpr int kChunk = 8192;  // rows per partial in the two-stage reductions
+
+// Packed X for dense_ax (fragment-major, see dense_ax.cu):
+// Xp[kb][s][nt][lane] = X[kb*32 + 8*(s>>1) + 2*(lane&3) + (s&1)][nt*8 + (lane>>2)]
+__global__ void pack_x_kernel(const double* __restrict__ X, int64_t n, int l, int NT, int64_t total,
+                              double* __restrict__ Xp) {
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int lane = (int)(idx & 31);
+    int64_t t = idx >> 5;
+    const int nt = (int)(t % NT);
+    t /= NT;
+    const int s = (int)(t & 7);
+    const int64_t kb = t >> 3;
+    const int64_t k = kb * 32 + 8 * (s >> 1) + 2 * (lane & 3) + (s & 1);
+    const int j = nt * 8 + (lane >> 2);
+    Xp[idx] = (k < n && j < l) ? X[k * l + j] : 0.0;
+  }
+}
+
+// Packed Y for dense_aty: Yp[g][s][nt][lane] = Y[8g + 2*(lane&3) + s][nt*8 + (lane>>2)]
+__global__ void pack_y_kernel(const double* __restrict__ Y, int64_t m, int l, int NT, int64_t total,
+                              double* __restrict__ Yp) {
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int lane = (int)(idx & 31);
+    int64_t t = idx >> 5;
+    const int nt = (int)(t % NT);
+    t /= NT;
+    const int s = (int)(t & 1);
+    const int64_t g = t >> 1;
+    const int64_t i = 8 * g + 2 * (lane & 3) + s;
+    const int j = nt * 8 + (lane >> 2);
+    Yp[idx] = (i < m && j < l) ? Y[i * l + j] : 0.0;
+  }
+}
+
+// partial[b][j] = Σ_{i in chunk b} a[i]·X[i][j]  (a == NULL ⇒ 1)
+__global__ void wcolsum_partial(const double* __restrict__ a, const double* __restrict__ X, int64_t rows, int l,
+                                int64_t ldx, double* __restrict__ part) {
+  __shared__ double red[256];
+  const int64_t r0 = (int64_t)blockIdx.x * kChunk;
+  const int64_t r1 = min(rows, r0 + kChunk);
+  const int phases = 256 / l;  // l ≤ 64 ⇒ ≥ 4 phases
+  const int ph = threadIdx.x / l, j = threadIdx.x % l;
+  double s = 0.0;
+  if (ph < phases) {
+    for (int64_t i = r0 + ph; i < r1; i += phases) s += (a ? a[i] : 1.0) * X[i * ldx + j];
+  }
+  red[threadIdx.x] = s;
+  __syncthreads();
+  if (threadIdx.x < l) {
+    double t = 0.0;
+    for (int p = 0; p < phases; ++p) t += red[p * l + threadIdx.x];
+    part[(int64_t)blockIdx.x * l + threadIdx.x] = t;
+  }
+}
+
+__global__ void sum_partials(const double* __restrict__ part, int64_t nparts, int l, double scale,
+                             double* __restrict__ v) {
+  const int j = threadIdx.x;
+  if (j >= l) return;
+  double s = 0.0;
+  for (int64_t b = 0; b < nparts; ++b) s += part[b * l + j];
+  v[j] = s * scale;
+}
+
+
+__global__ void sum_partials_wide_kernel(const double* __restrict__ part, int64_t nparts, int w,
+                                         double* __restrict__ v) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= w) return;
+  double s = 0.0;
+  for (int64_t b = 0; b < nparts; ++b) s += part[b * w + j];
+  v[j] = s;
+}
+
+__global__ void sub_rank1_kernel(double* __restrict__ Y, int64_t rows, int l, const double* __restrict__ u,
+                                 const double* __restrict__ v) {
+  const int64_t total = rows * l;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = idx / l;
+    const int j = (int)(idx - i * l);
+    Y[idx] -= (u ? u[i] : 1.0) * v[j];
+  }
+}
+
+template <class T>
+__global__ void colsum_dense_partial(const T* __restrict__ A, int64_t m, int64_t n, int64_t lda,
+                                     double* __restrict__ part) {
+  const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (j >= n) return;
+  const int64_t r0 = (int64_t)blockIdx.y * kChunk, r1 = min(m, r0 + kChunk);
+  double s = 0.0;
+  for (int64_t i = r0; i < r1; ++i) s += static_cast<double>(A[i * lda + j]);
+  part[(int64_t)blockIdx.y * n + j] = s;
+}
+
+__global__ void colsum_dense_final(const double* __restrict__ part, int64_t nparts, int64_t n, double inv_m,
+                                   double* __restrict__ c) {
+  const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (j >= n) return;
+  double s = 0.0;
+  for (int64_t b = 0; b < nparts; ++b) s += part[b * n + j];
+  c[j] = s * inv_m;
+}
+
+template <class T>
+__device__ __forceinline__ T cast_out(double v) { return static_cast<T>(v); }
+
+// Out[i][j] = sign[j]·Σ_t In[i][t]·W[t][j], j < k; rows staged through smem.
+template <class T>
+__global__ void thin_gemm_kernel(const double* __restrict__ In, int64_t rows, int l, const double* __restrict__ W,
+                                 int k, const double* __restrict__ sign, T* __restrict__ Out, int64_t ldo) {
+  extern __shared__ double sm[];
+  double* Ws = sm;             // l×k
+  double* Is = sm + l * k;     // 64×l
+  for (int idx = threadIdx.x; idx < l * k; idx += blockDim.x) {
+    const int t = idx / k, j = idx % k;
+    Ws[idx] = W[t * l + j] * (sign ? sign[j] : 1.0);
+  }
+  for (int64_t r0 = (int64_t)blockIdx.x * 64; r0 < rows; r0 += (int64_t)gridDim.x * 64) {
+    __syncthreads();
+    const int nr = (int)imin64(64, rows - r0);
+    for (int idx = threadIdx.x; idx < nr * l; idx += blockDim.x) Is[idx] = In[r0 * l + idx];
+    __syncthreads();
+    for (int idx = threadIdx.x; idx < nr * k; idx += blockDim.x) {
+      const int r = idx / k, j = idx % k;
+      double s = 0.0;
+      for (int t = 0; t < l; ++t) s += Is[r * l + t] * Ws[t * k + j];
+      Out[(r0 + r) * ldo + j] = cast_out<T>(s);
+    }
+  }
+}
+
+struct ArgBest {
+  double v;
+  int64_t i;
+};
+__device__ __forceinline__ bool better(double v, int64_t i, double bv, int64_t bi) {
+  return v > bv || (v == bv && i < bi);
+}
+
+// per (chunk, column) largest |V[i][j]| with the lowest i on ties
+__global__ void argmax_partial(const double* __restrict__ V, int64_t rows, int k, int64_t ldv,
+                               double* __restrict__ pv, int64_t* __restrict__ pi) {
+  __shared__ double sv[256];
+  __shared__ int64_t si[256];
+  const int j = blockIdx.y;
+  const int64_t r0 = (int64_t)blockIdx.x * kChunk, r1 = min(rows, r0 + kChunk);
+  double bv = -1.0;
+  int64_t bi = INT64_MAX;
+  for (int64_t i = r0 + threadIdx.x; i < r1; i += blockDim.x) {
+    const double v = fabs(V[i * ldv + j]);
+    if (better(v, i, bv, bi)) { bv = v; bi = i; }
+  }
+  sv[threadIdx.x] = bv;
+  si[threadIdx.x] = bi;
+  __syncthreads();
+  for (int o = 128; o > 0; o >>= 1) {
+    if (threadIdx.x < o && better(sv[threadIdx.x + o], si[threadIdx.x + o], sv[threadIdx.x], si[threadIdx.x])) {
+      sv[threadIdx.x] = sv[threadIdx.x + o];
+      si[threadIdx.x] = si[threadIdx.x + o];
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    pv[(int64_t)blockIdx.x * k + j] = sv[0];
+    pi[(int64_t)blockIdx.x * k + j] = si[0];
+  }
+}
+
+__global__ void argmax_final(const double* __restrict__ V, int64_t ldv, const double* __restrict__ pv,
+                             const int64_t* __restrict__ pi, int64_t nparts, int k, double* __restrict__ sign) {
+  const int j = threadIdx.x;
+  if (j >= k) return;
+  double bv = -1.0;
+  int64_t bi = INT64_MAX;
+  for (int64_t b = 0; b < nparts; ++b) {
+    if (better(pv[b * k + j], pi[b * k + j], bv, bi)) { bv = pv[b * k + j]; bi = pi[b * k + j]; }
+  }
+  sign[j] = (bi != INT64_MAX && V[bi * ldv + j] < 0.0) ? -1.0 : 1.0;
+}
+
+template <class T>
+__global__ void copy_cast_kernel(const double* __restrict__ s, T* __restrict__ d, int64_t count) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count; i += (int64_t)gridDim.x * blockDim.x)
+    d[i] = static_cast<T>(s[i]);
+}
+
+
+template <class T>
+__global__ void scale_cast_kernel(const double* __restrict__ src, int64_t rows, int k, const double* __restrict__ sign,
+                                  T* __restrict__ dst, int64_t ldd) {
+  const int64_t total = rows * k;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = idx / k;
+    const int j = (int)(idx - i * k);
+    dst[i * ldd + j] = static_cast<T>(src[idx] * (sign ? sign[j] : 1.0));
+  }
+}
+
+// partial[b][p][q] = Σ_{i in chunk b} X[i][p]·Y[i][q]   (X, Y rows×l)
+__global__ void gram_partial(const double* __restrict__ X, const double* __restrict__ Y, int64_t rows, int l,
+                             double* __restrict__ part) {
+  const int64_t r0 = (int64_t)blockIdx.x * kChunk, r1 = min(rows, r0 + kChunk);
+  for (int pq = threadIdx.x; pq < l * l; pq += blockDim.x) {
+    const int p = pq / l, q = pq % l;
+    double s = 0.0;
+    for (int64_t i = r0; i < r1; ++i) s += X[i * l + p] * Y[i * l + q];
+    part[(int64_t)blockIdx.x * l * l + pq] = s;
+  }
+}
+
+// Out[i][j] = Σ_{t} (In[i][t] + nu·Q[i][t])·M[t][j]   (M l×l; nu from device; Q may be NULL)
+__global__ void right_mult_kernel(const double* __restrict__ In, const double* __restrict__ Q,
+                                  const double* __restrict__ nu_p, const double* __restrict__ M, int64_t rows, int l,
+                                  double* __restrict__ Out) {
+  extern __shared__ double sm[];
+  double* Ms = sm;
+  double* Is = sm + l * l;
+  const double nu = (Q && nu_p) ? *nu_p : 0.0;
+  for (int idx = threadIdx.x; idx < l * l; idx += blockDim.x) Ms[idx] = M[idx];
+  for (int64_t r0 = (int64_t)blockIdx.x * 64; r0 < rows; r0 += (int64_t)gridDim.x * 64) {
+    const int nr = (int)imin64(64, rows - r0);
+    __syncthreads();
+    for (int idx = threadIdx.x; idx < nr * l; idx += blockDim.x)
+      Is[idx] = In[r0 * l + idx] + (Q ? nu * Q[r0 * l + idx] : 0.0);
+    __syncthreads();
+    for (int idx = threadIdx.x; idx < nr * l; idx += blockDim.x) {
+      const int r = idx / l, j = idx % l;
+      double s = 0.0;
+      for (int t = 0; t < l; ++t) s += Is[r * l + t] * Ms[t * l + j];
+      Out[(r0 + r) * l + j] = s;
+    }
+  }
+}
+
+// y[i] -= Σ_j U[i][j]·t[j]   (U rows×k, ld ldu)
+__global__ void rank_k_sub_kernel(double* __restrict__ y, const double* __restrict__ U, int64_t ldu,
+                                  const double* __restrict__ t, int64_t rows, int k) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < rows; i += (int64_t)gridDim.x * blockDim.x) {
+    double s = 0.0;
+    for (int j = 0; j < k; ++j) s += U[i * ldu + j] * t[j];
+    y[i] -= s;
+  }
+}
+
+__global__ void hadamard_kernel(double* __restrict__ t, const double* __restrict__ S, int k) {
+  const int j = threadIdx.x;
+  if (j < k) t[j] *= S[j];
+}
+
+unsigned grid_for(Ctx& c, int64_t work, int per = 256) {
+  int64_t b = cdiv(work, per);
+  const int64_t cap = (int64_t)c.num_sms * 16;
+  if (b > cap) b = cap;
+  if (b < 1) b = 1;
+  return (unsigned)b;
+}
+
+void sum_partials_wide(Ctx& c, const double* part, int64_t nparts, int w, double* v) {
+  sum_partials_wide_kernel<<<(unsigned)cdiv(w, 256), 256, 0, c.stream>>>(part, nparts, w, v);
+  RPCA_CHECK_LAUNCH();
+}
+
+}  // namespace
+
+int64_t packx_elems(int64_t n, int l) { return cdiv(n, 32) * 256 * cdiv(l, 8); }
+int64_t packy_elems(int64_t m, int l) { return cdiv(m, 32) * 4 * 64 * cdiv(l, 8); }
+
+void pack_x(Ctx& c, const double* X, int64_t n, int l, double* Xp) {
+  const int NT = (int)cdiv(l, 8);
+  const int64_t total = packx_elems(n, l);
+  pack_x_kernel<<<grid_for(c, total), 256, 0, c.stream>>>(X, n, l, NT, total, Xp);
+  RPCA_CHECK_LAUNCH();
+  count_launch(c, 1, "pack_x");
+}
+
+void pack_y(Ctx& c, const double* Y, int64_t m, int l, double* Yp) {
+  const int NT = (int)cdiv(l, 8);
+  const int64_t total = packy_elems(m, l);
+  pack_y_kernel<<<grid_for(c, total), 256, 0, c.stream>>>(Y, m, l, NT, total, Yp);
+  RPCA_CHECK_LAUNCH();
+  count_launch(c, 1, "pack_y");
+}
+
+void weighted_colsum(Ctx& c, const double* a, const double* X, int64_t rows, int l, double* v, Arena& ar,
+                     int64_t ldx) {
+  if (ldx <= 0) ldx = l;
+  const int64_t nparts = std::max<int64_t>(1, cdiv(rows, kChunk));
+  double* part = ar.get<double>(nparts * l);
+  wcolsum_partial<<<(unsigned)nparts, 256, 0, c.stream>>>(a, X, rows, l, ldx, part);
+  RPCA_CHECK_LAUNCH();
+  sum_partials<<<1, 64, 0, c.stream>>>(part, nparts, l, 1.0, v);
+  RPCA_CHECK_LAUNCH();
+  count_launch(c, 2);
+}
+
+void sub_rank1(Ctx& c, double* Y, int64_t rows, int l, const double* u, const double* v) {
+  sub_rank1_kernel<<<grid_for(c, rows * l), 256, 0, c.stream>>>(Y, rows, l, u, v);
+  RPCA_CHECK_LAUNCH();
+  count_launch(c);
+}
+
+void colmeans_dense(Ctx& c, const void* A, int dtype, int64_t m, int64_t n, int64_t lda, int64_t m_total,
+                    double* cmean, Arena& ar) {
+  const int64_t nparts = std::max<int64_t>(1, cdiv(m, kChunk));
+  double* part = ar.get<double>(nparts * n);
+  dim3 grid((unsigned)cdiv(n, 256), (unsigned)nparts);
+  if (dtype == RPCA_F64)
+    colsum_dense_partial<double><<<grid, 256, 0, c.stream>>>((const double*)A, m, n, lda, part);
+  else
+    colsum_dense_partial<float><<<grid, 256, 0, c.stream>>>((const float*)A, m, n, lda, part);
+  RPCA_CHECK_LAUNCH();
+  colsum_dense_final<<<(unsigned)cdiv(n, 256), 256, 0, c.stream>>>(part, nparts, n, 1.0 / (double)m_total, cmean);
+  RPCA_CHECK_LAUNCH();
+  count_launch(c, 2, "colmeans");
+}
+
+void thin_gemm(Ctx& c, const double* In, int64_t rows, int l, const double* W, int k, const double* sign, void* Out,
+               int64_t ldo, int out_dtype) {
+  const size_t smem = (size_t)(l * k + 64 * l) * sizeof(double);
+  const unsigned grid = grid_for(c, rows, 64);
+  const int smax = (kMaxL * kMaxL + 64 * kMaxL) * (int)sizeof(double);
+  RPCA_CUDA(cudaFuncSetAttribute(thin_gemm_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, smax));
+  RPCA_CUDA(cudaFuncSetAttribute(thin_gemm_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, smax));
+  if (out_dtype == RPCA_F64)
+    thin_gemm_kernel<double><<<grid, 256, smem, c.stream>>>(In, rows, l, W, k, sign, (double*)Out, ldo);
+  else
+    thin_gemm_kernel<float><<<grid, 256, smem, c.stream>>>(In, rows, l, W, k, sign, (float*)Out, ldo);
+  RPCA_CHECK_LAUNCH();
+  count_launch(c, 1, "thin_gemm");
+}
+
+void column_signs(Ctx& c, const double* V, int64_t rows, int k, int64_t ldv, double* sign, Arena& ar) {
+  const int64_t nparts = std::max<int64_t>(1, cdiv(rows, kChunk));
+  double* pv = ar.get<double>(nparts * k);
+  int64_t* pi = ar.get<int64_t>(nparts * k);
+  argmax_partial<<<dim3((unsigned)nparts, (unsigned)k), 256, 0, c.stream>>>(V, rows, k, ldv, pv, pi);
+  RPCA_CHECK_LAUNCH();
+  argmax_final<<<1, 64, 0, c.stream>>>(V, ldv, pv, pi, nparts, k, sign);
+  RPCA_CHECK_LAUNCH();
+  count_launch(c, 2);
+}
+
+
+void scale_cast(Ctx& c, const double* src, int64_t rows, int k, const double* sign, void* dst, int64_t ldd,
+                int dtype) {
+  if (dtype == RPCA_F64)
+    scale_cast_kernel<double><<<grid_for(c, rows * k), 256, 0, c.stream>>>(src, rows, k, sign, (double*)dst, ldd);
+  else
+    scale_cast_kernel<float><<<grid_for(c, rows * k), 256, 0, c.stream>>>(src, rows, k, sign, (float*)dst, ldd);
+  RPCA_CHECK_LAUNCH();
+  count_launch(c);
+}
+
+void gram(Ctx& c, const double* X, const double* Y, int64_t rows, int l, double* G, Arena& ar) {
+  const int64_t nparts = std::max<int64_t>(1, cdiv(rows, kChunk));
+  double* part = ar.get<double>(nparts * l * l);
+  gram_partial<<<(unsigned)nparts, 256, 0, c.stream>>>(X, Y, rows, l, part);
+  RPCA_CHECK_LAUNCH();
+  // reuse sum_partials with "l" = l*l columns (≤ 4096): one thread per entry
+  sum_partials_wide(c, part, nparts, l * l, G);
+  count_launch(c);
+}
+
+void right_mult(Ctx& c, const double* In, const double* Q, const double* nu, const double* M, int64_t rows, int l,
+                double* Out) {
+  const size_t smem = (size_t)(l * l + 64 * l) * 8;
+  RPCA_CUDA(cudaFuncSetAttribute(right_mult_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)((kMaxL * kMaxL + 64 * kMaxL) * 8)));
+  right_mult_kernel<<<grid_for(c, rows, 64), 256, smem, c.stream>>>(In, Q, nu, M, rows, l, Out);
+  RPCA_CHECK_LAUNCH();
+  count_launch(c);
+}
+
+void rank_k_sub(Ctx& c, double* y, const double* U, int64_t ldu, const double* t, int64_t rows, int k) {
+  if (k == 0) return;
+  rank_k_sub_kernel<<<grid_for(c, rows), 256, 0, c.stream>>>(y, U, ldu, t, rows, k);
+  RPCA_CHECK_LAUNCH();
+  count_launch(c);
+}
+
+void hadamard(Ctx& c, double* t, const double* S, int k) {
+  if (k == 0) return;
+  hadamard_kernel<<<1, 256, 0, c.stream>>>(t, S, k);
+  RPCA_CHECK_LAUNCH();
+  count_launch(c);
+}
+
+void copy_cast(Ctx& c, const double* src, void* dst, int64_t count, int dtype) {
+  if (dtype == RPCA_F64)
+    copy_cast_kernel<double><<<grid_for(c, count), 256, 0, c.stream>>>(src, (double*)dst, count);
+  else
+    copy_cast_kernel<float><<<grid_for(c, count), 256, 0, c.stream>>>(src, (float*)dst, count);
+  RPCA_CHECK_LAUNCH();
+  count_launch(c);
+}
+
+}  // namespace rpca

@@ -1,0 +1,288 @@
+"""GPU parity: the sm_100a path (through the C ABI) against the CPU oracle on the
+same seeded inputs.  Tolerances:
+
+* integer / bit work (Philox stream): bit-exact;
+* one application of A (A·X, Aᵀ·Y): both sides are fp64 dot products of
+  length K, so |gpu − oracle| ≤ 2·γ_K·(|A||X|), γ_K = K·u/(1−K·u) (Higham);
+* whole pipelines (BASELINE.json north_star): leading-k σ relative 1e-10 and
+  largest principal angle (sine form, reading Q10) < 1e-8 for fp64;
+  diffsnorm within 1% of the oracle's.
+"""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import paper_1412_3510_b200 as rp
+import synth
+from tests.helpers import cluster_sin_angle, sin_angle
+
+pytestmark = pytest.mark.gpu
+U64 = 2.0**-53
+
+
+def dev():
+    return torch.device("cuda", 0)
+
+
+def gamma(K):
+    return K * U64 / (1 - K * U64)
+
+
+# ----------------------------------------------------------------- a1: Ω
+@pytest.mark.parametrize("rows,cols,seed,sid", [(1000, 12, 0, 0), (4001, 22, 7, 1), (33, 7, 2**40 + 5, 3)])
+def test_omega_uniform_bit_exact(rows, cols, seed, sid):
+    g = rp.omega(rows, cols, seed=seed, stream_id=sid, dist=rp.UNIFORM).cpu().numpy()
+    o = oracle.omega(seed, rows, cols, dist=oracle.UNIFORM, stream=sid)
+    assert np.array_equal(g, o)
+
+
+@pytest.mark.parametrize("rows,cols,seed", [(1000, 12, 0), (4001, 22, 7), (32768, 42, 0)])
+def test_omega_gaussian_within_ulps(rows, cols, seed):
+    g = rp.omega(rows, cols, seed=seed).cpu().numpy()
+    o = oracle.omega(seed, rows, cols)
+    # same integer stream; log/cos/sin of two libms differ by a few ulp
+    assert np.max(np.abs(g - o) / np.maximum(np.abs(o), 1.0)) <= 8 * U64 * 8
+    g32 = rp.omega(rows, cols, seed=seed, round_f32=True).cpu().numpy()
+    assert np.array_equal(g32, g32.astype(np.float32).astype(np.float64))
+    assert np.max(np.abs(g32 - o)) <= 2.0**-23 * 6
+
+
+# ----------------------------------------------------------------- a2/a4/a6: A·X, Aᵀ·Y
+SHAPES = [(1000, 500), (1003, 518), (257, 129), (4097, 64), (300, 517), (64, 64), (33, 1000)]
+
+
+@pytest.mark.parametrize("m,n", SHAPES)
+@pytest.mark.parametrize("l", [1, 12, 22, 42, 64])
+def test_apply_dense_f64(m, n, l):
+    g = torch.Generator(device="cuda").manual_seed(m * 131 + n + l)
+    A = torch.randn(m, n, generator=g, device=dev(), dtype=torch.float64)
+    X = torch.randn(n, l, generator=g, device=dev(), dtype=torch.float64)
+    Y = torch.randn(m, l, generator=g, device=dev(), dtype=torch.float64)
+    An, Xn, Yn = A.cpu().numpy(), X.cpu().numpy(), Y.cpu().numpy()
+    got = rp.apply(A, X).cpu().numpy()
+    ref = oracle.apply(An, Xn)
+    assert np.all(np.abs(got - ref) <= 2 * gamma(n) * (np.abs(An) @ np.abs(Xn)) + 1e-300)
+    got = rp.apply(A, Y, adjoint=True).cpu().numpy()
+    ref = oracle.apply(An, Yn, adjoint=True)
+    assert np.all(np.abs(got - ref) <= 2 * gamma(m) * (np.abs(An).T @ np.abs(Yn)) + 1e-300)
+
+
+@pytest.mark.parametrize("m,n,l", [(1000, 500, 12), (2050, 130, 22), (300, 517, 7)])
+def test_apply_centered(m, n, l):
+    g = torch.Generator(device="cuda").manual_seed(5)
+    A = torch.randn(m, n, generator=g, device=dev(), dtype=torch.float64) + 3.0
+    X = torch.randn(n, l, generator=g, device=dev(), dtype=torch.float64)
+    Y = torch.randn(m, l, generator=g, device=dev(), dtype=torch.float64)
+    An = A.cpu().numpy()
+    c = rp.colmeans(A)
+    assert np.allclose(c.cpu().numpy(), oracle.colmeans(An), rtol=1e-14, atol=1e-14)
+    Ac = An - An.mean(axis=0)
+    tol = 4 * gamma(max(m, n)) * (np.abs(An).max() * max(m, n) * np.abs(X.cpu().numpy()).max())
+    assert np.allclose(rp.apply(A, X, cmean=c).cpu().numpy(), oracle.apply(An, X.cpu().numpy(), raw=False),
+                       atol=tol, rtol=0)
+    assert np.allclose(rp.apply(A, Y, adjoint=True, cmean=c).cpu().numpy(),
+                       oracle.apply(An, Y.cpu().numpy(), adjoint=True, raw=False), atol=tol * 4, rtol=0)
+    del Ac
+
+
+def test_apply_f32_input():
+    g = torch.Generator(device="cuda").manual_seed(8)
+    A = torch.randn(777, 300, generator=g, device=dev(), dtype=torch.float32)
+    X = torch.randn(300, 20, generator=g, device=dev(), dtype=torch.float64)
+    An = A.cpu().numpy()
+    ref = oracle.apply(An, X.cpu().numpy())
+    got = rp.apply(A, X).cpu().numpy()
+    assert np.all(np.abs(got - ref) <= 1e-5 * (np.abs(An.astype(np.float64)) @ np.abs(X.cpu().numpy())))
+
+
+# ----------------------------------------------------------------- a3: LU
+@pytest.mark.parametrize("m,l", [(100, 12), (1000, 22), (100000, 22), (70000, 42), (4096, 64), (257, 64), (22, 22)])
+def test_lu_span_and_factorisation(m, l):
+    g = torch.Generator(device="cuda").manual_seed(m + l)
+    Y = torch.randn(m, l, generator=g, device=dev(), dtype=torch.float64)
+    L, U, piv = rp.lu_renorm(Y)
+    Yn, Ln, Un, pv = Y.cpu().numpy(), L.cpu().numpy(), U.cpu().numpy(), piv.cpu().numpy()
+    assert len(set(pv.tolist())) == l
+    Lp = Ln[pv]
+    assert np.array_equal(np.diag(Lp), np.ones(l)) and np.all(np.triu(Lp, 1) == 0)
+    assert np.linalg.norm(Ln @ Un - Yn) <= 1e-13 * np.linalg.norm(Yn) * np.sqrt(l)
+    assert np.all(np.triu(Un) == Un)
+    # span(L) = span(Y) = span(oracle's L)
+    Lo, _, _ = oracle.lu_renorm(Yn)
+    Qo = np.linalg.qr(Lo)[0]
+    Qg = np.linalg.qr(Ln)[0]
+    assert sin_angle(Qo, Qg) < 1e-11
+    assert np.abs(Ln).max() < 50  # tournament pivoting keeps L bounded in practice
+
+
+def test_lu_zero_pivots():
+    Y = np.zeros((600, 6))
+    Y[:, 0] = np.arange(1, 601)
+    Y[:, 1] = 2 * Y[:, 0]
+    Y[5, 2] = 3.0
+    Y[400, 4] = -1.0
+    L, U, piv = rp.lu_renorm(torch.tensor(Y, device=dev()))
+    Ln, Un, pv = L.cpu().numpy(), U.cpu().numpy(), piv.cpu().numpy()
+    assert np.allclose(Ln @ Un, Y, atol=1e-12)
+    for j in np.nonzero(np.diag(Un) == 0)[0]:
+        col = Ln[:, j]
+        assert col[pv[j]] == 1.0 and np.count_nonzero(col) == 1
+
+
+# ----------------------------------------------------------------- a5: QR
+@pytest.mark.parametrize("m,l", [(100, 12), (1000, 22), (100000, 22), (70001, 42), (4096, 64), (300, 64), (64, 64)])
+def test_qr_matches_oracle(m, l):
+    g = torch.Generator(device="cuda").manual_seed(m * 3 + l)
+    Y = torch.randn(m, l, generator=g, device=dev(), dtype=torch.float64)
+    Q, R = rp.qr(Y)
+    Qn, Rn, Yn = Q.cpu().numpy(), R.cpu().numpy(), Y.cpu().numpy()
+    assert np.linalg.norm(Qn.T @ Qn - np.eye(l)) < 1e-14 * l * np.sqrt(m / 100 + 1)
+    assert np.linalg.norm(Qn @ Rn - Yn) < 1e-14 * np.linalg.norm(Yn) * np.sqrt(l)
+    assert np.all(np.tril(Rn, -1) == 0) and np.all(np.diag(Rn) >= 0)
+    Qo, Ro = oracle.house_qr(Yn)
+    assert np.max(np.abs(Rn - Ro)) <= 1e-12 * np.abs(Ro).max()
+    assert np.max(np.abs(Qn - Qo)) <= 1e-11
+
+
+def test_qr_rank_deficient():
+    Y = np.zeros((5000, 8))
+    rng = np.random.default_rng(1)
+    Y[:, :3] = rng.standard_normal((5000, 3))
+    Y[:, 3] = Y[:, 0] - Y[:, 2]
+    Q, R = rp.qr(torch.tensor(Y, device=dev()))
+    Qn, Rn = Q.cpu().numpy(), R.cpu().numpy()
+    assert np.linalg.norm(Qn.T @ Qn - np.eye(8)) < 1e-13
+    assert np.linalg.norm(Qn @ Rn - Y) < 1e-13 * np.linalg.norm(Y)
+
+
+# ----------------------------------------------------------------- a7: small SVD
+@pytest.mark.parametrize("n,l", [(500, 12), (4000, 22), (32768, 42), (64, 64)])
+def test_small_svd(n, l):
+    g = torch.Generator(device="cuda").manual_seed(n + l)
+    G = torch.randn(n, l, generator=g, device=dev(), dtype=torch.float64) * torch.logspace(
+        0, -4, l, device=dev(), dtype=torch.float64)
+    Vt, s, W = rp.small_svd(G)
+    Gn = G.cpu().numpy()
+    Vo, so, Wo = oracle.jacobi_svd(Gn)
+    sn = s.cpu().numpy()
+    assert np.allclose(sn, so, rtol=1e-12)
+    Vn, Wn = Vt.cpu().numpy(), W.cpu().numpy()
+    assert np.linalg.norm(Vn * sn @ Wn.T - Gn) < 1e-13 * np.linalg.norm(Gn)
+    assert np.linalg.norm(Vn.T @ Vn - np.eye(l)) < 1e-13 * l
+    assert cluster_sin_angle(Vo, Vn, so, l) < 1e-9
+
+
+# ----------------------------------------------------------------- whole pca
+def compare(res_g, res_o, k, tol_s=1e-10, tol_a=1e-8, skip_zero=True):
+    Ug, Sg, Vg = [t.cpu().numpy().astype(np.float64) for t in res_g]
+    Uo, So, Vo = res_o
+    nz = So > 1e-12 * So[0] if skip_zero else np.ones(k, bool)
+    assert np.max(np.abs(Sg[nz] - So[nz]) / So[nz]) < tol_s, (Sg, So)
+    assert cluster_sin_angle(Uo, Ug, So, k) < tol_a
+    assert cluster_sin_angle(Vo, Vg, So, k) < tol_a
+
+
+def test_pca_c1_full():
+    A = synth.make_c1(device=dev())
+    An = A.cpu().numpy()
+    res = rp.pca(A, 10, raw=True, its=2, l=12, seed=0)
+    compare(res, oracle.pca(An, 10, its=2, l=12, seed=0), 10)
+    # the same call again is bitwise identical (fixed-order reductions, T6)
+    res2 = rp.pca(A, 10, raw=True, its=2, l=12, seed=0)
+    assert all(torch.equal(a, b) for a, b in zip(res, res2))
+
+
+@pytest.mark.parametrize("m,n,k,l,its,raw", [(2000, 700, 8, 10, 0, True), (700, 2000, 8, 10, 2, True),
+                                             (3001, 257, 20, 22, 3, False), (513, 1025, 5, 12, 1, False),
+                                             (4000, 64, 40, 64, 2, True)])
+def test_pca_shapes(m, n, k, l, its, raw):
+    g = torch.Generator(device="cuda").manual_seed(m + n)
+    sig = torch.exp(-torch.arange(min(m, n), dtype=torch.float64) / 4.0)
+    A = synth.synth_dense(m, n, sig, seed=m * 7 + n, device=dev()).contiguous()
+    if not raw:
+        A += torch.rand(n, generator=g, device=dev(), dtype=torch.float64) * 10 - 5
+    An = A.cpu().numpy()
+    res = rp.pca(A, k, raw=raw, its=its, l=l, seed=3)
+    compare(res, oracle.pca(An, k, raw=raw, its=its, l=l, seed=3), k)
+
+
+def test_pca_propack_diagonal():
+    """the matrices PROPACK gets wrong; zero pivots on the GPU too."""
+    A = synth.propack_diag(30).to(dev())
+    for seed in range(5):
+        U, S, V = rp.pca(A, 20, its=2, seed=seed)
+        exp = np.array([1, 1, 1] + [0.999] * 17)
+        assert np.max(np.abs(S.cpu().numpy() - exp)) < 1e-10
+    A = synth.propack_diag(100).to(dev())
+    U, S, V = rp.pca(A, 50, its=2, seed=1)
+    Sn = S.cpu().numpy()
+    assert np.max(np.abs(Sn[:20] - np.array([1, 1, 1] + [0.999] * 17))) < 1e-10
+    assert np.all(np.abs(Sn[20:]) < 1e-10)
+    Un, Vn = U.cpu().numpy(), V.cpu().numpy()
+    assert np.linalg.norm(Un.T @ Un - np.eye(50)) < 1e-10
+    assert np.linalg.norm(Vn.T @ Vn - np.eye(50)) < 1e-10
+
+
+def test_pca_fp32_input():
+    A32 = synth.make_c1(m=3000, n=400, seed=9, device=dev()).to(torch.float32).contiguous()
+    res = rp.pca(A32, 10, its=2, l=12, seed=0)
+    assert res[0].dtype == torch.float32
+    o = oracle.pca(A32.cpu().numpy(), 10, its=2, l=12, seed=0)
+    compare(res, o, 10, tol_s=1e-4, tol_a=1e-3)
+
+
+def test_pca_host_buffers_e2e():
+    A = synth.make_c1(device=dev())
+    Ah = A.cpu().pin_memory()
+    Ug, Sg, Vg = rp.pca(Ah, 10, its=2, l=12, seed=0)
+    assert Ug.device.type == "cpu"
+    Ud, Sd, Vd = rp.pca(A, 10, its=2, l=12, seed=0)
+    assert torch.equal(Sg, Sd.cpu()) and torch.equal(Ug, Ud.cpu()) and torch.equal(Vg, Vd.cpu())
+
+
+def test_pca_errors():
+    A = torch.ones(10, 8, device=dev(), dtype=torch.float64)
+    for k, l, its in [(0, None, 2), (5, 4, 2), (3, 9, 2), (2, None, -1)]:
+        with pytest.raises(rp.RPCAError) as e:
+            rp.pca(A, k, l=l, its=its)
+        assert e.value.code == rp.E_SHAPE
+
+
+# ----------------------------------------------------------------- eigens, diffsnorm
+@pytest.mark.parametrize("variant", ["shift_chol", "sqrt"])
+def test_eigens_psd(variant):
+    n, k, l = 2048, 40, 42
+    A = synth.make_c3(n=n, device=dev())
+    U, lam = rp.eigens(A, k, its=2, l=l, seed=0, variant=variant)
+    Uo, lo = oracle.eigens(A.cpu().numpy(), k, its=2, l=l, seed=0,
+                           variant=oracle.SHIFT_CHOL if variant == "shift_chol" else oracle.SQRT)
+    ln = lam.cpu().numpy()
+    assert np.max(np.abs(ln - lo) / lo) < 1e-10
+    assert cluster_sin_angle(Uo, U.cpu().numpy(), lo, k) < 1e-8
+
+
+def test_diffsnorm_matches_oracle():
+    A = synth.make_c1(device=dev())
+    U, S, V = rp.pca(A, 10, its=2, l=12, seed=0)
+    est = rp.diffsnorm(A, U, S, V, its=20, seed=1)
+    An = A.cpu().numpy()
+    ref = oracle.diffsnorm(An, U.cpu().numpy(), S.cpu().numpy(), V.cpu().numpy(), its=20, seed=1)
+    assert abs(est - ref) <= 1e-10 * ref
+    exact = np.linalg.norm(An - (U.cpu().numpy() * S.cpu().numpy()) @ V.cpu().numpy().T, 2)
+    assert exact / 2 <= est <= exact * (1 + 1e-10)
+    Ac = A + 2.0
+    U, S, V = rp.pca(Ac, 10, raw=False, its=2, l=12, seed=0)
+    est = rp.diffsnorm(Ac, U, S, V, raw=False, its=20, seed=1)
+    ref = oracle.diffsnorm(Ac.cpu().numpy(), U.cpu().numpy(), S.cpu().numpy(), V.cpu().numpy(), raw=False, its=20,
+                           seed=1)
+    assert abs(est - ref) <= 1e-9 * ref
+
+
+# ----------------------------------------------------------------- full-size C2 (BASELINE configs[1])
+@pytest.mark.slow
+def test_pca_c2_full_size():
+    A = synth.make_c2(device=dev())
+    res = rp.pca(A, 20, raw=True, its=2, l=22, seed=0)
+    o = oracle.pca(A.cpu().numpy(), 20, its=2, l=22, seed=0)
+    compare(res, o, 20)
