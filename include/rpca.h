@@ -54,6 +54,7 @@ enum { RPCA_SHIFT_CHOL = 0, RPCA_SQRT = 1 };
 #define RPCA_FLAG_UNIFORM_OMEGA 0x1u  /* draw Ω from U[-1,1] instead of N(0,1) */
 #define RPCA_FLAG_OUTPUTS_HOST 0x2u   /* U, S, V / lam are HOST buffers (copied back inside the call) */
 #define RPCA_FLAG_CHECK_FINITE 0x4u   /* validate A during pass 1 → RPCA_E_NONFINITE */
+#define RPCA_FLAG_NO_GRAPH 0x8u       /* do not capture/replay driver calls as CUDA graphs */
 
 /*
  * The matrix A (§2 l.107-114: m×n, k ≪ min(m,n)).

@@ -79,10 +79,17 @@ rpca_status rpca_ctx_destroy(rpca_ctx* c) {
   return guard([&] {
     DeviceScope ds(c->device);
     if (c->comm) rpca::comm_destroy(*c);
-    if (c->ws) {
-      cudaStreamSynchronize(c->stream);
-      cudaFree(c->ws);
+    cudaStreamSynchronize(c->stream);
+    for (auto& g : c->graphs) cudaGraphExecDestroy(g.second.exec);
+    for (auto e : c->prof_pool) cudaEventDestroy(e);
+    if (c->status_host) cudaFreeHost(c->status_host);
+    if (c->work) {
+      cudaStreamSynchronize(c->work);
+      cudaStreamDestroy(c->work);
+      cudaEventDestroy(c->fence_in);
+      cudaEventDestroy(c->fence_out);
     }
+    if (c->ws) cudaFree(c->ws);
     delete c;
   });
 }
@@ -95,7 +102,8 @@ rpca_status rpca_ctx_set_stream(rpca_ctx* c, void* stream) {
 
 rpca_status rpca_ctx_set_flags(rpca_ctx* c, uint32_t flags) {
   if (!c) return RPCA_E_ARG;
-  if (flags & ~(uint32_t)(RPCA_FLAG_UNIFORM_OMEGA | RPCA_FLAG_OUTPUTS_HOST | RPCA_FLAG_CHECK_FINITE)) return RPCA_E_ARG;
+  if (flags & ~(uint32_t)(RPCA_FLAG_UNIFORM_OMEGA | RPCA_FLAG_OUTPUTS_HOST | RPCA_FLAG_CHECK_FINITE | RPCA_FLAG_NO_GRAPH))
+    return RPCA_E_ARG;
   c->flags = flags;
   return RPCA_OK;
 }
@@ -120,10 +128,8 @@ rpca_status rpca_launch_count(rpca_ctx* c, int64_t* count) {
 rpca_status rpca_profile_begin(rpca_ctx* c) {
   if (!c) return RPCA_E_ARG;
   return guard([&] {
-    c->prof_recs.clear();
-    c->prof_used = 0;
+    c->prof_out.clear();
     c->prof = true;
-    rpca::prof_mark(*c, "start");
   });
 }
 
@@ -134,10 +140,8 @@ rpca_status rpca_profile_end(rpca_ctx* c, char* buf, size_t cap, size_t* needed)
     RPCA_CUDA(cudaStreamSynchronize(c->stream));
     std::string out;
     char line[160];
-    for (size_t i = 1; i < c->prof_recs.size(); ++i) {
-      float ms = 0.f;
-      RPCA_CUDA(cudaEventElapsedTime(&ms, c->prof_recs[i - 1].ev, c->prof_recs[i].ev));
-      snprintf(line, sizeof(line), "%s\t%.6f\n", c->prof_recs[i].name, ms);
+    for (auto& r : c->prof_out) {
+      snprintf(line, sizeof(line), "%s\t%.6f\n", r.first, r.second);
       out += line;
     }
     if (needed) *needed = out.size() + 1;
@@ -259,12 +263,12 @@ rpca_status rpca_small_svd(rpca_ctx* c, const double* G, int64_t n, int64_t l, d
     rpca::Sizer s;
     s.add<double>(n * l);
     s.add<double>(2 * l * l);
-    rpca::Arena ar = c->arena(s.total + rpca::qr_ws_bytes(n, (int)l) + 65536);
+    rpca::Arena ar = c->arena(s.total + rpca::orth_ws_bytes(n, (int)l) + 65536);
     double* Qb = ar.get<double>(n * l);
     double* R = ar.get<double>(l * l);
     double* Vr = ar.get<double>(l * l);
     RPCA_CUDA(cudaMemcpyAsync(Qb, G, sizeof(double) * n * l, cudaMemcpyDeviceToDevice, c->stream));
-    rpca::qr(*c, Qb, n, (int)l, R, ar);
+    rpca::orthonormalize(*c, Qb, n, (int)l, R, ar);
     rpca::jacobi_svd_small(*c, R, (int)l, sigma, W, Vr);
     rpca::thin_gemm(*c, Qb, n, (int)l, Vr, (int)l, nullptr, Vt, l, RPCA_F64);
   });

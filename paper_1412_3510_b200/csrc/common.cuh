@@ -18,6 +18,8 @@ struct Error {
 };
 
 void set_last_error(const char* fmt, ...);
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per (device, kernel, size increase)
+void ensure_smem(const void* kernel, int bytes);
 
 #define RPCA_CUDA(call)                                                              \
   do {                                                                               \

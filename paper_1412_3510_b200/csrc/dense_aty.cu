@@ -278,7 +278,7 @@ void launch_aty_tma(Ctx& c, const DenseA& A, const double* Yp, const Split& sp, 
                             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   RPCA_REQUIRE(r == CUDA_SUCCESS, RPCA_E_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
-  RPCA_CUDA(cudaFuncSetAttribute(aty_f64_tma_kernel<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmem));
+  ensure_smem((const void*)aty_f64_tma_kernel<NT>, Cfg::kSmem);
   aty_f64_tma_kernel<NT><<<(unsigned)sp.P, kThreads, Cfg::kSmem, c.stream>>>(tm, Yp, sp, maxslots, part);
   RPCA_CHECK_LAUNCH();
   count_launch(c, 1, "aty_f64_dmma");

@@ -217,11 +217,7 @@ void launch_ax_tma(Ctx& c, const DenseA& A, const double* Xp, int l, double* Y) 
                             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   RPCA_REQUIRE(r == CUDA_SUCCESS, RPCA_E_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
-  static bool attr = false;
-  if (!attr) {
-    RPCA_CUDA(cudaFuncSetAttribute(ax_f64_tma_kernel<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmem));
-    attr = true;
-  }
+  ensure_smem((const void*)ax_f64_tma_kernel<NT>, Cfg::kSmem);
   const int64_t ntiles = cdiv(A.m, BM);
   const int KB = (int)cdiv(A.n, BK);
   const int grid = (int)std::min<int64_t>(ntiles, c.num_sms);

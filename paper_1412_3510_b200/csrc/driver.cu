@@ -11,6 +11,8 @@
 //   rpca_diffsnorm— PAPER.md §4 l.362-371.
 #include <cstdarg>
 #include <cstring>
+#include <map>
+#include <mutex>
 #include <string>
 
 #include "internal.cuh"
@@ -37,14 +39,139 @@ void prof_mark(Ctx& c, const char* name) {
     c.prof_pool.push_back(e);
   }
   cudaEvent_t e = c.prof_pool[c.prof_used++];
-  RPCA_CUDA(cudaEventRecord(e, c.stream));
+  if (c.capturing) RPCA_CUDA(cudaEventRecordWithFlags(e, c.stream, cudaEventRecordExternal));
+  else RPCA_CUDA(cudaEventRecord(e, c.stream));
   c.prof_recs.push_back(ProfRec{name, e});
+}
+
+void ensure_smem(const void* kernel, int bytes) {
+  static std::mutex mu;
+  static std::map<std::pair<int, const void*>, int> done;
+  int dev = 0;
+  RPCA_CUDA(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> g(mu);
+  auto key = std::make_pair(dev, kernel);
+  auto it = done.find(key);
+  if (it != done.end() && it->second >= bytes) return;
+  RPCA_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+  done[key] = bytes;
+}
+
+namespace {
+
+void harvest(Ctx& c, const std::vector<ProfRec>& marks) {
+  for (size_t i = 1; i < marks.size(); ++i) {
+    float ms = 0.f;
+    RPCA_CUDA(cudaEventElapsedTime(&ms, marks[i - 1].ev, marks[i].ev));
+    c.prof_out.emplace_back(marks[i].name, ms);
+  }
+}
+
+struct KeyHasher {
+  uint64_t h = 1469598103934665603ull;
+  template <class T>
+  KeyHasher& operator<<(const T& v) {
+    const unsigned char* p = reinterpret_cast<const unsigned char*>(&v);
+    for (size_t i = 0; i < sizeof(T); ++i) { h ^= p[i]; h *= 1099511628211ull; }
+    return *this;
+  }
+};
+
+}  // namespace
+
+// Run `body` (which only enqueues work on c.stream) either directly or as a
+// cached CUDA graph; then synchronise the stream and harvest profile marks.
+template <class F>
+void execute_on(Ctx& c, uint64_t key, bool graphable, F&& body) {
+  const bool use_graph = graphable && c.use_graphs && !(c.flags & RPCA_FLAG_NO_GRAPH);
+  key ^= (uint64_t)c.prof * 0x9E3779B97F4A7C15ull;
+  if (use_graph) {
+    for (auto& g : c.graphs)
+      if (g.first == key) {
+        RPCA_CUDA(cudaGraphLaunch(g.second.exec, c.stream));
+        c.launches += g.second.nlaunch;
+        RPCA_CUDA(cudaStreamSynchronize(c.stream));
+        if (c.prof) harvest(c, g.second.marks);
+        return;
+      }
+  }
+  c.prof_recs.clear();
+  c.prof_used = 0;
+  const int64_t l0 = c.launches;
+  if (use_graph) {
+    RPCA_CUDA(cudaStreamBeginCapture(c.stream, cudaStreamCaptureModeThreadLocal));
+    c.capturing = true;
+    cudaGraph_t graph = nullptr;
+    try {
+      if (c.prof) prof_mark(c, "start");
+      body();
+    } catch (...) {
+      c.capturing = false;
+      cudaStreamEndCapture(c.stream, &graph);
+      if (graph) cudaGraphDestroy(graph);
+      (void)cudaGetLastError();
+      throw;
+    }
+    c.capturing = false;
+    RPCA_CUDA(cudaStreamEndCapture(c.stream, &graph));
+    CachedGraph cg;
+    RPCA_CUDA(cudaGraphInstantiate(&cg.exec, graph, 0));
+    RPCA_CUDA(cudaGraphDestroy(graph));
+    cg.marks = c.prof_recs;
+    cg.nlaunch = c.launches - l0;
+    if (c.graphs.size() >= 16) {
+      for (auto& g : c.graphs) cudaGraphExecDestroy(g.second.exec);
+      c.graphs.clear();
+    }
+    c.graphs.emplace_back(key, cg);
+    RPCA_CUDA(cudaGraphLaunch(cg.exec, c.stream));
+    RPCA_CUDA(cudaStreamSynchronize(c.stream));
+    if (c.prof) harvest(c, cg.marks);
+  } else {
+    if (c.prof) prof_mark(c, "start");
+    body();
+    RPCA_CUDA(cudaStreamSynchronize(c.stream));
+    if (c.prof) harvest(c, c.prof_recs);
+  }
+}
+
+// Run `body` (which only enqueues work on c.stream) on the context's private
+// non-blocking stream — fenced by events against the caller's stream, which
+// may be the legacy default stream that cannot be captured — either directly
+// or as a cached CUDA graph; then synchronise and harvest profile marks.
+template <class F>
+void execute(Ctx& c, uint64_t key, bool graphable, F&& body) {
+  if (!c.work) {
+    RPCA_CUDA(cudaStreamCreateWithFlags(&c.work, cudaStreamNonBlocking));
+    RPCA_CUDA(cudaEventCreateWithFlags(&c.fence_in, cudaEventDisableTiming));
+    RPCA_CUDA(cudaEventCreateWithFlags(&c.fence_out, cudaEventDisableTiming));
+  }
+  cudaStream_t user = c.stream;
+  RPCA_CUDA(cudaEventRecord(c.fence_in, user));
+  RPCA_CUDA(cudaStreamWaitEvent(c.work, c.fence_in, 0));
+  c.stream = c.work;
+  try {
+    execute_on(c, key, graphable, body);
+  } catch (...) {
+    c.stream = user;
+    throw;
+  }
+  c.stream = user;
+  RPCA_CUDA(cudaEventRecord(c.fence_out, c.work));
+  RPCA_CUDA(cudaStreamWaitEvent(user, c.fence_out, 0));
+}
+
+void drop_graphs(Ctx& c) {
+  for (auto& g : c.graphs) cudaGraphExecDestroy(g.second.exec);
+  c.graphs.clear();
 }
 
 Arena Ctx::arena(size_t bytes) {
   if (bytes > ws_cap) {
     if (ws) {
       RPCA_CUDA(cudaStreamSynchronize(stream));
+      for (auto& g : graphs) cudaGraphExecDestroy(g.second.exec);
+      graphs.clear();
       RPCA_CUDA(cudaFree(ws));
       ws = nullptr;
       ws_cap = 0;
@@ -142,9 +269,10 @@ void renorm_lu(Ctx& c, double* Y, int64_t rows, int l, Arena& ar) {
   lu_renorm(c, Y, rows, l, nullptr, nullptr, ar);
   ar.off = mark;
 }
+// the last renormalisation and the QR of Bᵀ: LU-Cholesky-QR
 void renorm_qr(Ctx& c, double* Y, int64_t rows, int l, double* R, Arena& ar) {
   const size_t mark = ar.off;
-  qr(c, Y, rows, l, R, ar);
+  orthonormalize(c, Y, rows, l, R, ar);
   ar.off = mark;
 }
 
@@ -175,7 +303,7 @@ void pca(Ctx& c, const rpca_mat* Am, int64_t k, int raw, int its, int64_t l, uin
   const int odt = Am->dtype, osz = elem_size(odt);
   const int64_t m = Am->m, n = Am->n;
 
-  // ---- workspace plan
+  // ---- workspace plan (allocation happens before any capture)
   DenseA probe{Am->a, Am->dtype, m, n, Am->lda};
   const bool trans = m < n;
   const int64_t nin = trans ? m : n, nout = trans ? n : m;
@@ -195,74 +323,78 @@ void pca(Ctx& c, const rpca_mat* Am, int64_t k, int raw, int its, int64_t l, uin
   const size_t fixed = sz.total;
   size_t scratch = op_ws(c, probe, L);
   scratch = std::max(scratch, lu_ws_bytes(std::max(nin, nout), L));
-  scratch = std::max(scratch, qr_ws_bytes(std::max(nin, nout), L));
+  scratch = std::max(scratch, orth_ws_bytes(std::max(nin, nout), L));
   scratch = std::max(scratch, (size_t)(cdiv(std::max(m, n), 8192) + 2) * (n + 2 * k) * 8 + 65536);
   Arena ar = c.arena(fixed + scratch + 65536);
 
-  const DenseA dA = device_view(c, Am, ar);
-  double* Zb = ar.get<double>(nin * l);
-  double* Yb = ar.get<double>(nout * l);
-  double* cmean = ar.get<double>(n);
-  double* R = ar.get<double>(l * l);
-  double* W = ar.get<double>(l * l);
-  double* Vr = ar.get<double>(l * l);
-  double* sig = ar.get<double>(l);
-  double* side = ar.get<double>(std::max(nin, nout) * k);
-  double* sign = ar.get<double>(k);
-  void *Ud = U, *Vd = V, *Sd = S;
-  if (out_host) {
-    Ud = ar.get<char>((size_t)m * ldu * osz);
-    Vd = ar.get<char>((size_t)n * ldv * osz);
-    Sd = ar.get<char>((size_t)k * osz);
-  }
+  KeyHasher kh;
+  kh << 1 << *Am << k << raw << its << l << seed << U << ldu << S << V << ldv << c.flags << c.ws;
+  const bool graphable = Am->location == RPCA_DEVICE && !out_host;
 
-  Op F{dA, nullptr, trans};
-  if (!raw) {
-    const size_t mark = ar.off;
-    colmeans_dense(c, dA.a, dA.dtype, dA.m, dA.n, dA.lda, m, cmean, ar);
-    ar.off = mark;
-    F.cmean = cmean;
-  }
-  // Ω (nin×l); the fp32 path consumes fl32(Ω) exactly as the oracle does
-  omega(c, seed, 0u, nin, l, dist, odt == RPCA_F32, Zb);
-  fwd(c, F, Zb, L, Yb, ar);
-  if (its == 0) renorm_qr(c, Yb, nout, L, nullptr, ar);
-  else renorm_lu(c, Yb, nout, L, ar);
-  for (int it = 1; it <= its; ++it) {
-    adj(c, F, Yb, L, Zb, ar);
-    renorm_lu(c, Zb, nin, L, ar);
-    fwd(c, F, Zb, L, Yb, ar);
-    if (it < its) renorm_lu(c, Yb, nout, L, ar);
-    else renorm_qr(c, Yb, nout, L, nullptr, ar);
-  }
-  // Bᵀ = F*·Q (eq. i2), Bᵀ = Q_B·R, R = Vr·Σ·Wᵀ ⇒ B = W Σ (Q_B Vr)ᵀ (eq. i3)
-  adj(c, F, Yb, L, Zb, ar);
-  renorm_qr(c, Zb, nin, L, R, ar);
-  jacobi_svd_small(c, R, L, sig, W, Vr);
-  {
-    const size_t mark = ar.off;
-    if (!trans) {
-      // V = Q_B·Vr[:, :k] (n×k), U = Q·W[:, :k] (m×k)  (eq. i4)
-      thin_gemm(c, Zb, nin, L, Vr, K, nullptr, side, k, RPCA_F64);
-      column_signs(c, side, n, K, k, sign, ar);
-      scale_cast(c, side, n, K, sign, Vd, ldv, odt);
-      thin_gemm(c, Yb, nout, L, W, K, sign, Ud, ldu, odt);
-    } else {
-      // sketched Aᵀ: its "U" = Q·W is A's V (n×k); its "V" = Q_B·Vr is A's U
-      thin_gemm(c, Yb, nout, L, W, K, nullptr, side, k, RPCA_F64);
-      column_signs(c, side, n, K, k, sign, ar);
-      scale_cast(c, side, n, K, sign, Vd, ldv, odt);
-      thin_gemm(c, Zb, nin, L, Vr, K, sign, Ud, ldu, odt);
+  execute(c, kh.h, graphable, [&] {
+    const DenseA dA = device_view(c, Am, ar);
+    double* Zb = ar.get<double>(nin * l);
+    double* Yb = ar.get<double>(nout * l);
+    double* cmean = ar.get<double>(n);
+    double* R = ar.get<double>(l * l);
+    double* W = ar.get<double>(l * l);
+    double* Vr = ar.get<double>(l * l);
+    double* sig = ar.get<double>(l);
+    double* side = ar.get<double>(std::max(nin, nout) * k);
+    double* sign = ar.get<double>(k);
+    void *Ud = U, *Vd = V, *Sd = S;
+    if (out_host) {
+      Ud = ar.get<char>((size_t)m * ldu * osz);
+      Vd = ar.get<char>((size_t)n * ldv * osz);
+      Sd = ar.get<char>((size_t)k * osz);
     }
-    copy_cast(c, sig, Sd, k, odt);
-    ar.off = mark;
-  }
-  if (out_host) {
-    RPCA_CUDA(cudaMemcpyAsync(U, Ud, (size_t)m * ldu * osz, cudaMemcpyDeviceToHost, c.stream));
-    RPCA_CUDA(cudaMemcpyAsync(V, Vd, (size_t)n * ldv * osz, cudaMemcpyDeviceToHost, c.stream));
-    RPCA_CUDA(cudaMemcpyAsync(S, Sd, (size_t)k * osz, cudaMemcpyDeviceToHost, c.stream));
-  }
-  sync_status(c);
+    Op F{dA, nullptr, trans};
+    if (!raw) {
+      const size_t mark = ar.off;
+      colmeans_dense(c, dA.a, dA.dtype, dA.m, dA.n, dA.lda, m, cmean, ar);
+      ar.off = mark;
+      F.cmean = cmean;
+    }
+    // Ω (nin×l); the fp32 path consumes fl32(Ω) exactly as the oracle does
+    omega(c, seed, 0u, nin, l, dist, odt == RPCA_F32, Zb);
+    fwd(c, F, Zb, L, Yb, ar);
+    if (its == 0) renorm_qr(c, Yb, nout, L, nullptr, ar);
+    else renorm_lu(c, Yb, nout, L, ar);
+    for (int it = 1; it <= its; ++it) {
+      adj(c, F, Yb, L, Zb, ar);
+      renorm_lu(c, Zb, nin, L, ar);
+      fwd(c, F, Zb, L, Yb, ar);
+      if (it < its) renorm_lu(c, Yb, nout, L, ar);
+      else renorm_qr(c, Yb, nout, L, nullptr, ar);
+    }
+    // Bᵀ = F*·Q (eq. i2), Bᵀ = Q_B·R, R = Vr·Σ·Wᵀ ⇒ B = W Σ (Q_B Vr)ᵀ (eq. i3)
+    adj(c, F, Yb, L, Zb, ar);
+    renorm_qr(c, Zb, nin, L, R, ar);
+    jacobi_svd_small(c, R, L, sig, W, Vr);
+    {
+      const size_t mark = ar.off;
+      if (!trans) {
+        // V = Q_B·Vr[:, :k] (n×k), U = Q·W[:, :k] (m×k)  (eq. i4)
+        thin_gemm(c, Zb, nin, L, Vr, K, nullptr, side, k, RPCA_F64);
+        column_signs(c, side, n, K, k, sign, ar);
+        scale_cast(c, side, n, K, sign, Vd, ldv, odt);
+        thin_gemm(c, Yb, nout, L, W, K, sign, Ud, ldu, odt);
+      } else {
+        // sketched Aᵀ: its "U" = Q·W is A's V (n×k); its "V" = Q_B·Vr is A's U
+        thin_gemm(c, Yb, nout, L, W, K, nullptr, side, k, RPCA_F64);
+        column_signs(c, side, n, K, k, sign, ar);
+        scale_cast(c, side, n, K, sign, Vd, ldv, odt);
+        thin_gemm(c, Zb, nin, L, Vr, K, sign, Ud, ldu, odt);
+      }
+      copy_cast(c, sig, Sd, k, odt);
+      ar.off = mark;
+    }
+    if (out_host) {
+      RPCA_CUDA(cudaMemcpyAsync(U, Ud, (size_t)m * ldu * osz, cudaMemcpyDeviceToHost, c.stream));
+      RPCA_CUDA(cudaMemcpyAsync(V, Vd, (size_t)n * ldv * osz, cudaMemcpyDeviceToHost, c.stream));
+      RPCA_CUDA(cudaMemcpyAsync(S, Sd, (size_t)k * osz, cudaMemcpyDeviceToHost, c.stream));
+    }
+  });
 }
 
 // ============================================================ rpca_eigens
@@ -286,74 +418,84 @@ void eigens(Ctx& c, const rpca_mat* Am, int64_t k, int its, int64_t l, uint64_t 
   sz.add<char>(host_copy_bytes(Am));
   sz.add<double>(3 * n * l);
   sz.add<double>(6 * l * l + 8 * l + 16);
+  sz.add<double>(n * k + k);
   if (out_host) {
     sz.add<char>((size_t)n * ldu * osz);
     sz.add<char>((size_t)k * osz);
   }
   size_t scratch = op_ws(c, probe, L);
   scratch = std::max(scratch, lu_ws_bytes(n, L));
-  scratch = std::max(scratch, qr_ws_bytes(n, L));
+  scratch = std::max(scratch, orth_ws_bytes(n, L));
   scratch = std::max(scratch, (size_t)(cdiv(n, 8192) + 2) * l * l * 8 + 65536);
   Arena ar = c.arena(sz.total + scratch + 65536);
-  const DenseA dA = device_view(c, Am, ar);
-  double* Q = ar.get<double>(n * l);
-  double* B1 = ar.get<double>(n * l);
-  double* Fm = ar.get<double>(n * l);
-  double* G = ar.get<double>(l * l);
-  double* Minv = ar.get<double>(l * l);
-  double* R = ar.get<double>(l * l);
-  double* W = ar.get<double>(l * l);
-  double* Vr = ar.get<double>(l * l);
-  double* sig = ar.get<double>(l);
-  double* scal = ar.get<double>(8);  // [0] = ‖B1‖_F², [1] = ν
-  int* status = ar.get<int>(4);
-  void *Ud = U, *Ld = lam;
-  if (out_host) {
-    Ud = ar.get<char>((size_t)n * ldu * osz);
-    Ld = ar.get<char>((size_t)k * osz);
-  }
-  // self-adjoint loop: Y = AΩ, then its × (Q = A·Q)
-  omega(c, seed, 0u, n, l, dist, odt == RPCA_F32, B1);
-  apply_ax(c, dA, nullptr, B1, L, Q, ar);
-  if (its == 0) renorm_qr(c, Q, n, L, nullptr, ar);
-  else renorm_lu(c, Q, n, L, ar);
-  for (int it = 1; it <= its; ++it) {
-    apply_ax(c, dA, nullptr, Q, L, B1, ar);
-    std::swap(Q, B1);
-    if (it < its) renorm_lu(c, Q, n, L, ar);
-    else renorm_qr(c, Q, n, L, nullptr, ar);
-  }
-  apply_ax(c, dA, nullptr, Q, L, B1, ar);  // (start) B1 = A·Q
-  {
-    const size_t mark = ar.off;
-    gram(c, Q, B1, n, L, G, ar);  // (second) QᵀB1, symmetrised in the kernel below
-    if (variant == RPCA_SHIFT_CHOL) {
-      // ‖B1‖_F² as a 1-column weighted sum over the n·l entries
-      weighted_colsum(c, B1, B1, n * l, 1, scal, ar);
-      nystrom_shift_chol(c, G, scal, L, n, odt == RPCA_F32 ? 0x1p-23 : 0x1p-52, Minv, scal + 1, status);
-      right_mult(c, B1, Q, scal + 1, Minv, n, L, Fm);  // F = (B1 + νQ)·C⁻¹ (eq. pseudo)
-    } else {
-      nystrom_sqrt(c, G, L, Minv, scal + 1, status);
-      right_mult(c, B1, nullptr, nullptr, Minv, n, L, Fm);  // F = B1·C⁺
-    }
-    ar.off = mark;
-  }
-  // F = U S Vᵀ: Q_F R_F = F, R_F = Vr Σ Wᵀ ⇒ U = Q_F·Vr; Σ = S² (eq. finish)
-  renorm_qr(c, Fm, n, L, R, ar);
-  jacobi_svd_small(c, R, L, sig, W, Vr);
-  {
-    const size_t mark = ar.off;
+  if (!c.status_host) RPCA_CUDA(cudaMallocHost(&c.status_host, 64));
+
+  KeyHasher kh;
+  kh << 2 << *Am << k << its << l << seed << variant << U << ldu << lam << c.flags << c.ws;
+  const bool graphable = Am->location == RPCA_DEVICE && !out_host;
+  double* Q = nullptr;
+  int* status = nullptr;
+  void* Ud = U;
+  void* Ld = lam;
+  execute(c, kh.h, graphable, [&] {
+    const DenseA dA = device_view(c, Am, ar);
+    Q = ar.get<double>(n * l);
+    double* B1 = ar.get<double>(n * l);
+    double* Fm = ar.get<double>(n * l);
+    double* G = ar.get<double>(l * l);
+    double* Minv = ar.get<double>(l * l);
+    double* R = ar.get<double>(l * l);
+    double* W = ar.get<double>(l * l);
+    double* Vr = ar.get<double>(l * l);
+    double* sig = ar.get<double>(l);
+    double* scal = ar.get<double>(8);  // [0] = ‖B1‖_F², [1] = ν
+    status = ar.get<int>(4);
     double* side = ar.get<double>(n * k);
     double* sign = ar.get<double>(k);
-    thin_gemm(c, Fm, n, L, Vr, K, nullptr, side, k, RPCA_F64);
-    column_signs(c, side, n, K, k, sign, ar);
-    scale_cast(c, side, n, K, sign, Ud, ldu, odt);
-    nystrom_lambda(c, sig, scal + 1, K, Ld, odt);
-    ar.off = mark;
-  }
-  int st = 0;
-  RPCA_CUDA(cudaMemcpyAsync(&st, status, sizeof(int), cudaMemcpyDeviceToHost, c.stream));
+    if (out_host) {
+      Ud = ar.get<char>((size_t)n * ldu * osz);
+      Ld = ar.get<char>((size_t)k * osz);
+    }
+    // self-adjoint loop: Y = AΩ, then its × (Q = A·Q)
+    omega(c, seed, 0u, n, l, dist, odt == RPCA_F32, B1);
+    apply_ax(c, dA, nullptr, B1, L, Q, ar);
+    if (its == 0) renorm_qr(c, Q, n, L, nullptr, ar);
+    else renorm_lu(c, Q, n, L, ar);
+    for (int it = 1; it <= its; ++it) {
+      apply_ax(c, dA, nullptr, Q, L, B1, ar);
+      std::swap(Q, B1);
+      if (it < its) renorm_lu(c, Q, n, L, ar);
+      else renorm_qr(c, Q, n, L, nullptr, ar);
+    }
+    apply_ax(c, dA, nullptr, Q, L, B1, ar);  // (start) B1 = A·Q
+    {
+      const size_t mark = ar.off;
+      gram(c, Q, B1, n, L, G, ar);  // (second) QᵀB1, symmetrised in the kernels below
+      if (variant == RPCA_SHIFT_CHOL) {
+        weighted_colsum(c, B1, B1, n * l, 1, scal, ar);  // ‖B1‖_F²
+        nystrom_shift_chol(c, G, scal, L, n, odt == RPCA_F32 ? 0x1p-23 : 0x1p-52, Minv, scal + 1, status);
+        right_mult(c, B1, Q, scal + 1, Minv, n, L, Fm);  // F = (B1 + νQ)·C⁻¹ (eq. pseudo)
+      } else {
+        nystrom_sqrt(c, G, L, Minv, scal + 1, status);
+        right_mult(c, B1, nullptr, nullptr, Minv, n, L, Fm);  // F = B1·C⁺
+      }
+      ar.off = mark;
+    }
+    // F = U S Wᵀ: Q_F R_F = F, R_F = Vr Σ Wᵀ ⇒ U = Q_F·Vr; Σ = S² (eq. finish)
+    renorm_qr(c, Fm, n, L, R, ar);
+    jacobi_svd_small(c, R, L, sig, W, Vr);
+    {
+      const size_t mark = ar.off;
+      thin_gemm(c, Fm, n, L, Vr, K, nullptr, side, k, RPCA_F64);
+      column_signs(c, side, n, K, k, sign, ar);
+      scale_cast(c, side, n, K, sign, Ud, ldu, odt);
+      nystrom_lambda(c, sig, scal + 1, K, Ld, odt);
+      ar.off = mark;
+    }
+  });
+  RPCA_CUDA(cudaMemcpyAsync(c.status_host, status, sizeof(int), cudaMemcpyDeviceToHost, c.stream));
   sync_status(c);
+  const int st = *c.status_host;
   RPCA_REQUIRE(st != 1, RPCA_E_NOTPSD, "Nyström: B2 is not positive definite after the shifts (PAPER.md:262-273)");
   if (st == 2) {  // A·Q = 0: λ = 0, U = Q[:, :k] (DESIGN.md reading)
     const size_t mark = ar.off;
@@ -386,50 +528,57 @@ void diffsnorm(Ctx& c, const rpca_mat* Am, int raw, const double* U, int64_t ldu
   sz.add<double>(2 * n + m + n + k + 64);
   size_t scratch = op_ws(c, probe, 1) + (size_t)(cdiv(std::max(m, n), 8192) + 2) * (n + 64) * 8;
   Arena ar = c.arena(sz.total + scratch + 65536);
-  const DenseA dA = device_view(c, Am, ar);
-  double* x = ar.get<double>(n);
-  double* z = ar.get<double>(n);
-  double* y = ar.get<double>(m);
-  double* cmean = ar.get<double>(n);
-  double* t = ar.get<double>(std::max<int64_t>(k, 1));
-  double* sc = ar.get<double>(8);  // [0] nz2, [1] est
-  int* done = ar.get<int>(4);
-  if (!raw) {
-    const size_t mark = ar.off;
-    colmeans_dense(c, dA.a, dA.dtype, dA.m, dA.n, dA.lda, m, cmean, ar);
-    ar.off = mark;
-  }
-  const double* cm = raw ? nullptr : cmean;
-  RPCA_CUDA(cudaMemsetAsync(done, 0, sizeof(int), c.stream));
-  RPCA_CUDA(cudaMemsetAsync(sc, 0, 8 * sizeof(double), c.stream));
-  omega(c, seed, 1u, n, 1, RPCA_GAUSSIAN, 0, z);
-  {
-    const size_t mark = ar.off;
-    weighted_colsum(c, z, z, n, 1, sc, ar);
-    ar.off = mark;
-  }
-  // normalise the start vector without touching est/done: use a scratch est slot
-  power_step(c, sc, z, x, n, sc + 2, done + 1);
-  for (int it = 0; it < its; ++it) {
-    const size_t mark = ar.off;
-    apply_ax(c, dA, cm, x, 1, y, ar);  // y = A x [− 1 (c·x)]
-    if (k > 0) {                       // y −= U (S ⊙ (Vᵀx))
-      weighted_colsum(c, x, V, n, (int)k, t, ar, ldv);
-      hadamard(c, t, S, (int)k);
-      rank_k_sub(c, y, U, ldu, t, m, (int)k);
+  if (!c.status_host) RPCA_CUDA(cudaMallocHost(&c.status_host, 64));
+  KeyHasher kh;
+  kh << 3 << *Am << raw << U << ldu << S << V << ldv << k << its << seed << c.ws;
+  double* sc = nullptr;
+  execute(c, kh.h, Am->location == RPCA_DEVICE, [&] {
+    const DenseA dA = device_view(c, Am, ar);
+    double* x = ar.get<double>(n);
+    double* z = ar.get<double>(n);
+    double* y = ar.get<double>(m);
+    double* cmean = ar.get<double>(n);
+    double* t = ar.get<double>(std::max<int64_t>(k, 1));
+    sc = ar.get<double>(8);  // [0] nz2, [1] est, [2] scratch
+    int* done = ar.get<int>(4);
+    if (!raw) {
+      const size_t mark = ar.off;
+      colmeans_dense(c, dA.a, dA.dtype, dA.m, dA.n, dA.lda, m, cmean, ar);
+      ar.off = mark;
     }
-    apply_aty(c, dA, cm, y, 1, z, ar);  // z = Aᵀ y [− cᵀ (1ᵀy)]
-    if (k > 0) {                        // z −= V (S ⊙ (Uᵀy))
-      weighted_colsum(c, y, U, m, (int)k, t, ar, ldu);
-      hadamard(c, t, S, (int)k);
-      rank_k_sub(c, z, V, ldv, t, n, (int)k);
+    const double* cm = raw ? nullptr : cmean;
+    RPCA_CUDA(cudaMemsetAsync(done, 0, 4 * sizeof(int), c.stream));
+    RPCA_CUDA(cudaMemsetAsync(sc, 0, 8 * sizeof(double), c.stream));
+    omega(c, seed, 1u, n, 1, RPCA_GAUSSIAN, 0, z);
+    {
+      const size_t mark = ar.off;
+      weighted_colsum(c, z, z, n, 1, sc, ar);
+      ar.off = mark;
     }
-    weighted_colsum(c, z, z, n, 1, sc, ar);  // ‖z‖²
-    power_step(c, sc, z, x, n, sc + 1, done);
-    ar.off = mark;
-  }
-  RPCA_CUDA(cudaMemcpyAsync(out, sc + 1, sizeof(double), cudaMemcpyDeviceToHost, c.stream));
+    // normalise the start vector (est/done of this call go to scratch slots)
+    power_step(c, sc, z, x, n, sc + 2, done + 1);
+    for (int it = 0; it < its; ++it) {
+      const size_t mark = ar.off;
+      apply_ax(c, dA, cm, x, 1, y, ar);  // y = A x [− 1 (c·x)]
+      if (k > 0) {                       // y −= U (S ⊙ (Vᵀx))
+        weighted_colsum(c, x, V, n, (int)k, t, ar, ldv);
+        hadamard(c, t, S, (int)k);
+        rank_k_sub(c, y, U, ldu, t, m, (int)k);
+      }
+      apply_aty(c, dA, cm, y, 1, z, ar);  // z = Aᵀ y [− cᵀ (1ᵀy)]
+      if (k > 0) {                        // z −= V (S ⊙ (Uᵀy))
+        weighted_colsum(c, y, U, m, (int)k, t, ar, ldu);
+        hadamard(c, t, S, (int)k);
+        rank_k_sub(c, z, V, ldv, t, n, (int)k);
+      }
+      weighted_colsum(c, z, z, n, 1, sc, ar);  // ‖z‖²
+      power_step(c, sc, z, x, n, sc + 1, done);
+      ar.off = mark;
+    }
+  });
+  RPCA_CUDA(cudaMemcpyAsync(c.status_host, sc + 1, sizeof(double), cudaMemcpyDeviceToHost, c.stream));
   sync_status(c);
+  memcpy(out, c.status_host, sizeof(double));
 }
 
 }  // namespace rpca

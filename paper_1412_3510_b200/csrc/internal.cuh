@@ -48,6 +48,14 @@ struct ProfRec {
   cudaEvent_t ev;
 };
 
+// A captured driver call: replayed with cudaGraphLaunch when the same call
+// (same pointers, shapes, flags) comes again — one launch instead of ~50.
+struct CachedGraph {
+  cudaGraphExec_t exec = nullptr;
+  std::vector<ProfRec> marks;
+  int64_t nlaunch = 0;
+};
+
 struct Ctx {
   int device = 0;
   cudaStream_t stream = nullptr;
@@ -58,9 +66,16 @@ struct Ctx {
   int64_t launches = 0;
   Comm* comm = nullptr;
   bool prof = false;
+  bool capturing = false;
+  bool use_graphs = true;
   std::vector<ProfRec> prof_recs;
   std::vector<cudaEvent_t> prof_pool;
   size_t prof_used = 0;
+  std::vector<std::pair<const char*, float>> prof_out;
+  std::vector<std::pair<uint64_t, CachedGraph>> graphs;
+  int* status_host = nullptr;  // pinned scratch for device status words
+  cudaStream_t work = nullptr;   // private stream the drivers run (and capture) on
+  cudaEvent_t fence_in = nullptr, fence_out = nullptr;
   Arena arena(size_t bytes);  // ensures capacity, returns an arena over the workspace
 };
 
@@ -118,11 +133,18 @@ void dense_aty(Ctx& c, const DenseA& A, const double* Y, int l, const double* cm
 
 // tslu.cu
 size_t lu_ws_bytes(int64_t m, int l);
-void lu_renorm(Ctx& c, double* Y, int64_t m, int l, double* U_out, int64_t* piv_out, Arena& ar);
+// gpart (optional): per-CTA upper-triangle Gram partials of L (lu_apply_grid × l(l+1)/2)
+void lu_renorm(Ctx& c, double* Y, int64_t m, int l, double* U_out, int64_t* piv_out, Arena& ar,
+               double* gpart = nullptr);
+int lu_apply_grid(Ctx& c, int64_t m);
 
 // tsqr.cu
 size_t qr_ws_bytes(int64_t m, int l);
 void qr(Ctx& c, double* Y, int64_t m, int l, double* R_out, Arena& ar);
+
+// cholqr.cu — LU-Cholesky-QR: Y ← Q (orthonormal, span Y), R (l×l upper, diag ≥ 0, Y = Q·R)
+size_t orth_ws_bytes(int64_t m, int l);
+void orthonormalize(Ctx& c, double* Y, int64_t m, int l, double* R_out, Arena& ar);
 
 // small.cu — one-CTA l×l kernels
 // R (l×l) → Jacobi: R·W = Vr·diag(sigma); sigma sorted, Vr completed.

@@ -18,65 +18,78 @@ namespace {
 constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
 
-__global__ void __launch_bounds__(kThreads) jacobi_kernel(const double* __restrict__ R, int l,
-                                                          double* __restrict__ sigma, double* __restrict__ Wout,
-                                                          double* __restrict__ Vout) {
+constexpr int kJThreads = 1024;  // one warp per column pair: l/2 ≤ 32 pairs in flight
+
+__global__ void __launch_bounds__(kJThreads) jacobi_kernel(const double* __restrict__ R, int l,
+                                                           double* __restrict__ sigma, double* __restrict__ Wout,
+                                                           double* __restrict__ Vout) {
   // column-major: Mc[p*l + i] = M[i][p]; Wc likewise
   extern __shared__ double sm[];
   double* Mc = sm;
   double* Wc = sm + l * l;
   __shared__ double nrm[kMaxL];
   __shared__ int rank_[kMaxL];
-  __shared__ int rotated;
+  __shared__ int rotated[2];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  for (int idx = tid; idx < l * l; idx += kThreads) {
+  for (int idx = tid; idx < l * l; idx += kJThreads) {
     const int i = idx / l, p = idx % l;
     Mc[p * l + i] = R[idx];
     Wc[p * l + i] = (i == p) ? 1.0 : 0.0;
   }
+  if (tid < 2) rotated[tid] = 0;
   __syncthreads();
   const int lp = (l + 1) & ~1;  // players (one dummy if l is odd)
   const double eps = 0x1p-52;
   for (int sweep = 0; sweep < 30 && l > 1; ++sweep) {
-    if (tid == 0) rotated = 0;
-    __syncthreads();
     for (int round = 0; round < lp - 1; ++round) {
-      for (int k = warp; k < lp / 2; k += kWarps) {
+      const int k = warp;
+      if (k < lp / 2) {
         auto player = [&](int i) { return i == 0 ? 0 : 1 + ((i - 1 + round) % (lp - 1)); };
         int p = player(k), q = player(lp - 1 - k);
         if (p > q) { const int t = p; p = q; q = t; }
-        if (q >= l) continue;  // dummy
-        double a = 0.0, b = 0.0, g = 0.0;
-        for (int i = lane; i < l; i += 32) {
-          const double x = Mc[p * l + i], y = Mc[q * l + i];
-          a += x * x;
-          b += y * y;
-          g += x * y;
-        }
-        a = warp_sum(a);
-        b = warp_sum(b);
-        g = warp_sum(g);
-        if (!(fabs(g) > eps * sqrt(a * b))) continue;
-        if (lane == 0) rotated = 1;
-        const double zeta = (b - a) / (2.0 * g);
-        const double t = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
-        const double cs = 1.0 / sqrt(1.0 + t * t), sn = cs * t;
-        for (int i = lane; i < l; i += 32) {
-          const double x = Mc[p * l + i], y = Mc[q * l + i];
-          Mc[p * l + i] = cs * x - sn * y;
-          Mc[q * l + i] = sn * x + cs * y;
-          const double u = Wc[p * l + i], v = Wc[q * l + i];
-          Wc[p * l + i] = cs * u - sn * v;
-          Wc[q * l + i] = sn * u + cs * v;
+        if (q < l) {
+          // lanes own rows i = lane, lane + 32 (l ≤ 64)
+          const double x0 = lane < l ? Mc[p * l + lane] : 0.0, y0 = lane < l ? Mc[q * l + lane] : 0.0;
+          const double x1 = lane + 32 < l ? Mc[p * l + lane + 32] : 0.0;
+          const double y1 = lane + 32 < l ? Mc[q * l + lane + 32] : 0.0;
+          double a = x0 * x0 + x1 * x1, b = y0 * y0 + y1 * y1, g = x0 * y0 + x1 * y1;
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) {
+            a += __shfl_xor_sync(0xffffffffu, a, o);
+            b += __shfl_xor_sync(0xffffffffu, b, o);
+            g += __shfl_xor_sync(0xffffffffu, g, o);
+          }
+          if (fabs(g) > eps * sqrt(a * b)) {
+            if (lane == 0) rotated[sweep & 1] = 1;
+            const double zeta = (b - a) / (2.0 * g);
+            const double t = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
+            const double cs = 1.0 / sqrt(1.0 + t * t), sn = cs * t;
+            if (lane < l) {
+              Mc[p * l + lane] = cs * x0 - sn * y0;
+              Mc[q * l + lane] = sn * x0 + cs * y0;
+              const double u = Wc[p * l + lane], v = Wc[q * l + lane];
+              Wc[p * l + lane] = cs * u - sn * v;
+              Wc[q * l + lane] = sn * u + cs * v;
+            }
+            if (lane + 32 < l) {
+              Mc[p * l + lane + 32] = cs * x1 - sn * y1;
+              Mc[q * l + lane + 32] = sn * x1 + cs * y1;
+              const double u = Wc[p * l + lane + 32], v = Wc[q * l + lane + 32];
+              Wc[p * l + lane + 32] = cs * u - sn * v;
+              Wc[q * l + lane + 32] = sn * u + cs * v;
+            }
+          }
         }
       }
       __syncthreads();
     }
-    if (!rotated) break;
+    const int any = rotated[sweep & 1];
     __syncthreads();
+    if (tid == 0) rotated[sweep & 1] = 0;
+    if (!any) break;
   }
   // σ_p = ‖M[:, p]‖
-  for (int p = warp; p < l; p += kWarps) {
+  for (int p = warp; p < l; p += (kJThreads / 32)) {
     double s = 0.0;
     for (int i = lane; i < l; i += 32) s += Mc[p * l + i] * Mc[p * l + i];
     s = warp_sum(s);
@@ -89,7 +102,7 @@ __global__ void __launch_bounds__(kThreads) jacobi_kernel(const double* __restri
     rank_[tid] = r;
   }
   __syncthreads();
-  for (int idx = tid; idx < l * l; idx += kThreads) {
+  for (int idx = tid; idx < l * l; idx += kJThreads) {
     const int p = idx / l, i = idx % l;
     const int rp = rank_[p];
     Wout[i * l + rp] = Wc[p * l + i];
@@ -343,8 +356,8 @@ __global__ void power_step_kernel(const double* __restrict__ nz2, double* __rest
 void jacobi_svd_small(Ctx& c, const double* R, int l, double* sigma, double* W, double* Vr) {
   RPCA_REQUIRE(l >= 1 && l <= kMaxL, RPCA_E_SHAPE, "jacobi: l=%d", l);
   const int smem = 2 * l * l * 8;
-  RPCA_CUDA(cudaFuncSetAttribute(jacobi_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * kMaxL * kMaxL * 8));
-  jacobi_kernel<<<1, kThreads, smem, c.stream>>>(R, l, sigma, W, Vr);
+  ensure_smem((const void*)jacobi_kernel, 2 * kMaxL * kMaxL * 8);
+  jacobi_kernel<<<1, kJThreads, smem, c.stream>>>(R, l, sigma, W, Vr);
   RPCA_CHECK_LAUNCH();
   count_launch(c, 1, "jacobi");
 }
@@ -352,7 +365,7 @@ void jacobi_svd_small(Ctx& c, const double* R, int l, double* sigma, double* W, 
 
 void nystrom_shift_chol(Ctx& c, const double* G, const double* fro2, int l, int64_t n, double unit_roundoff,
                         double* Minv, double* nu, int* status) {
-  RPCA_CUDA(cudaFuncSetAttribute(shift_chol_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * kMaxL * kMaxL * 8));
+  ensure_smem((const void*)shift_chol_kernel, 2 * kMaxL * kMaxL * 8);
   shift_chol_kernel<<<1, kThreads, 2 * l * l * 8, c.stream>>>(G, fro2, l, sqrt((double)n), unit_roundoff, Minv, nu,
                                                               status);
   RPCA_CHECK_LAUNCH();
@@ -360,7 +373,7 @@ void nystrom_shift_chol(Ctx& c, const double* G, const double* fro2, int l, int6
 }
 
 void nystrom_sqrt(Ctx& c, const double* G, int l, double* Minv, double* nu, int* status) {
-  RPCA_CUDA(cudaFuncSetAttribute(sqrt_inv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * kMaxL * kMaxL * 8));
+  ensure_smem((const void*)sqrt_inv_kernel, 2 * kMaxL * kMaxL * 8);
   sqrt_inv_kernel<<<1, kThreads, 2 * l * l * 8, c.stream>>>(G, l, Minv, nu, status);
   RPCA_CHECK_LAUNCH();
   count_launch(c);

@@ -336,8 +336,8 @@ void thin_gemm(Ctx& c, const double* In, int64_t rows, int l, const double* W, i
   const size_t smem = (size_t)(l * k + 64 * l) * sizeof(double);
   const unsigned grid = grid_for(c, rows, 64);
   const int smax = (kMaxL * kMaxL + 64 * kMaxL) * (int)sizeof(double);
-  RPCA_CUDA(cudaFuncSetAttribute(thin_gemm_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, smax));
-  RPCA_CUDA(cudaFuncSetAttribute(thin_gemm_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, smax));
+  ensure_smem((const void*)thin_gemm_kernel<double>, smax);
+  ensure_smem((const void*)thin_gemm_kernel<float>, smax);
   if (out_dtype == RPCA_F64)
     thin_gemm_kernel<double><<<grid, 256, smem, c.stream>>>(In, rows, l, W, k, sign, (double*)Out, ldo);
   else
@@ -381,8 +381,7 @@ void gram(Ctx& c, const double* X, const double* Y, int64_t rows, int l, double*
 void right_mult(Ctx& c, const double* In, const double* Q, const double* nu, const double* M, int64_t rows, int l,
                 double* Out) {
   const size_t smem = (size_t)(l * l + 64 * l) * 8;
-  RPCA_CUDA(cudaFuncSetAttribute(right_mult_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)((kMaxL * kMaxL + 64 * kMaxL) * 8)));
+  ensure_smem((const void*)right_mult_kernel, (int)((kMaxL * kMaxL + 64 * kMaxL) * 8));
   right_mult_kernel<<<grid_for(c, rows, 64), 256, smem, c.stream>>>(In, Q, nu, M, rows, l, Out);
   RPCA_CHECK_LAUNCH();
   count_launch(c);

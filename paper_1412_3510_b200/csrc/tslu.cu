@@ -6,244 +6,363 @@
 // L with Y = L·U (MATLAB's two-output lu; reading Q3).
 //
 // B200 design — tournament pivoting (CALU):
-//   1. leaf kernel: one CTA per block of 256 (l ≤ 32) or 128 rows runs GEPP in
-//      shared memory and nominates l candidate pivot rows (original rows);
+//   1. leaf kernel: one CTA per block of 256 rows runs GEPP and nominates l
+//      candidate pivot rows (original rows);
 //   2. tree kernel: groups of G candidate sets are stacked (original values
 //      gathered from Y) and reduced by GEPP again, until one set is left; the
 //      last GEPP gives the pivot order, U (l×l) and the multipliers of the pivot
-//      rows (Lp), and the substitution matrix M with x = y·M ⇔ x·U = y
-//      (x_j = 0 where U_jj = 0 — the exact-zero-pivot rule of reading Q3);
-//   3. apply kernel: L = Y·M for every row (HBM-bound), pivot rows overwritten
-//      with their exact unit-lower rows from Lp.
-// Pivot choice: largest |·| among active rows, lowest original row on ties.
-// Tournament pivots differ from plain GEPP, so L differs from the oracle's L
-// but span(L) = span(Y) whenever U is nonsingular (compare spans, Q3).
+//      rows (Lp);
+//   3. apply kernel: every CTA first forms the substitution matrix M with
+//      x = y·M ⇔ x·U = y (x_j = 0 where U_jj = 0 — the exact-zero-pivot rule of
+//      reading Q3), then L = Y·M for its rows (HBM-bound); pivot rows are
+//      overwritten with their exact unit-lower rows from Lp.  Optionally the
+//      CTA also accumulates LᵀL for the Cholesky-QR that follows (cholqr.cu).
+// GEPP inside a CTA: thread t owns rows t, t+256, … held in REGISTERS (the
+// kernel is templated on l rounded up to 8); the pivot row is read from a
+// shared-memory mirror that every thread refreshes after its update; the
+// argmax of column j+1 is reduced while column j is eliminated, so each column
+// costs one __syncthreads.  Pivot: largest |·| among active rows, lowest
+// original row on ties.  Tournament pivots differ from plain GEPP, so L differs
+// from the oracle's L but span(L) = span(Y) whenever U is nonsingular.
 #include "internal.cuh"
 
 namespace rpca {
 namespace {
 
 constexpr int kThreads = 256;
+constexpr int kWarps = kThreads / 32;
 
-struct Best {
+struct Cand {
   double v;
-  int64_t id;
-  int r;
+  int r;  // local row (ties are broken by ids[r])
 };
 
-__device__ __forceinline__ bool better(double v, int64_t id, double bv, int64_t bid) {
-  return v > bv || (v == bv && id < bid);
+__device__ __forceinline__ bool better(double v, int r, double bv, int br, const int64_t* ids) {
+  if (v != bv) return v > bv;
+  if (br < 0) return r >= 0;
+  if (r < 0) return false;
+  return ids[r] < ids[br];
 }
 
-// GEPP on W (rows × ldw, shared), ids = original row numbers.  After return,
-// piv[j] = local row of pivot j (j < steps), active[] = 0 for pivot rows, and
-// W holds multipliers left of each row's pivot column (for pivot rows) / of
-// every column (others) and the eliminated values right of it.
-__device__ void gepp(double* W, int ldw, const int64_t* ids, int rows, int l, int steps, int* piv, uint8_t* active,
-                     double* rv, int64_t* ri, int* rr) {
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  for (int j = 0; j < steps; ++j) {
-    double bv = -1.0;
-    int64_t bid = INT64_MAX;
-    int br = -1;
-    for (int r = tid; r < rows; r += kThreads) {
-      if (!active[r]) continue;
-      const double v = fabs(W[r * ldw + j]);
-      if (better(v, ids[r], bv, bid)) { bv = v; bid = ids[r]; br = r; }
-    }
+__device__ __forceinline__ Cand warp_best(Cand c, const int64_t* ids) {
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
-      const int64_t oid = __shfl_xor_sync(0xffffffffu, bid, o);
-      const int orr = __shfl_xor_sync(0xffffffffu, br, o);
-      if (better(ov, oid, bv, bid)) { bv = ov; bid = oid; br = orr; }
+  for (int o = 16; o > 0; o >>= 1) {
+    const double ov = __shfl_xor_sync(0xffffffffu, c.v, o);
+    const int orr = __shfl_xor_sync(0xffffffffu, c.r, o);
+    if (better(ov, orr, c.v, c.r, ids)) { c.v = ov; c.r = orr; }
+  }
+  return c;
+}
+
+// GEPP on W (rows × ldw, shared; ldw odd ⇒ conflict-free row-per-thread
+// access).  Thread t owns rows t, t+256, … (active flags in registers).  One
+// __syncthreads per column: the argmax of column j+1 is reduced while column j
+// is eliminated and every thread redundantly combines the eight warp winners.
+// piv[j] = local pivot row of column j; W ends with the multipliers left of
+// each row's pivot column and its eliminated values right of it.
+__device__ void gepp(double* W, int ldw, const int64_t* ids, int rows, int l, int steps, int* piv,
+                     Cand (*slot)[kWarps]) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  constexpr int kMaxR = 3;
+  bool act[kMaxR];
+  Cand c{-1.0, -1};
+#pragma unroll
+  for (int q = 0; q < kMaxR; ++q) {
+    const int r = tid + q * kThreads;
+    act[q] = r < rows;
+    if (act[q]) {
+      const double v = fabs(W[r * ldw]);
+      if (better(v, r, c.v, c.r, ids)) c = Cand{v, r};
     }
-    if (lane == 0) { rv[warp] = bv; ri[warp] = bid; rr[warp] = br; }
-    __syncthreads();
-    if (tid == 0) {
-      double b = rv[0];
-      int64_t bi = ri[0];
-      int r = rr[0];
-      for (int w = 1; w < kThreads / 32; ++w)
-        if (better(rv[w], ri[w], b, bi)) { b = rv[w]; bi = ri[w]; r = rr[w]; }
-      piv[j] = r;
-      active[r] = 0;
+  }
+  c = warp_best(c, ids);
+  if (lane == 0) slot[0][warp] = c;
+  __syncthreads();
+  for (int j = 0; j < steps; ++j) {
+    Cand b = slot[j & 1][0];
+#pragma unroll
+    for (int wi = 1; wi < kWarps; ++wi) {
+      const Cand o = slot[j & 1][wi];
+      if (better(o.v, o.r, b.v, b.r, ids)) b = o;
     }
-    __syncthreads();
-    const int pr = piv[j];
-    const double u = W[pr * ldw + j];
-    for (int r = tid; r < rows; r += kThreads)
-      if (active[r]) W[r * ldw + j] = (u != 0.0) ? W[r * ldw + j] / u : 0.0;
-    __syncthreads();
-    const int nt = l - j - 1;
-    if (nt > 0 && u != 0.0) {
-      for (int idx = tid; idx < rows * nt; idx += kThreads) {
-        const int r = idx / nt, t = j + 1 + idx % nt;
-        if (active[r]) W[r * ldw + t] -= W[r * ldw + j] * W[pr * ldw + t];
+    const int p = b.r;
+    if (tid == 0) piv[j] = p;
+    const double* prow = W + p * ldw;
+    const double u = prow[j];
+    const double uinv = (u != 0.0) ? __drcp_rn(u) : 0.0;
+    Cand nc{-1.0, -1};
+#pragma unroll
+    for (int q = 0; q < kMaxR; ++q) {
+      const int r = tid + q * kThreads;
+      if (!act[q]) continue;
+      if (r == p) { act[q] = false; continue; }
+      double* wr = W + r * ldw;
+      const double mult = wr[j] * uinv;
+      wr[j] = mult;
+      if (mult != 0.0) {
+        // chunks of 8: all loads issued before the stores (a row never aliases the pivot row)
+        int t = j + 1;
+        for (; t + 8 <= l; t += 8) {
+          double pv[8], wv[8];
+#pragma unroll
+          for (int u8 = 0; u8 < 8; ++u8) { pv[u8] = prow[t + u8]; wv[u8] = wr[t + u8]; }
+#pragma unroll
+          for (int u8 = 0; u8 < 8; ++u8) wr[t + u8] = wv[u8] - mult * pv[u8];
+        }
+        for (; t < l; ++t) wr[t] -= mult * prow[t];
+      }
+      if (j + 1 < steps) {
+        const double v = fabs(wr[j + 1]);
+        if (better(v, r, nc.v, nc.r, ids)) nc = Cand{v, r};
       }
     }
+    nc = warp_best(nc, ids);
+    if (lane == 0) slot[(j + 1) & 1][warp] = nc;
     __syncthreads();
   }
 }
 
 // One CTA: rows from Y (leaf: contiguous block; tree: a group of candidate
 // sets), GEPP, l nominated original rows → cand_out[blockIdx.x*l ...] (-1 pad).
-// If final, also U, Lp, piv and the substitution matrix M.
-__global__ void __launch_bounds__(kThreads) lu_select_kernel(const double* __restrict__ Y, int64_t m, int l,
-                                                             int leaf, int64_t leaf_rows,
-                                                             const int64_t* __restrict__ cand_in, int64_t n_in,
-                                                             int G, int64_t* __restrict__ cand_out, int final_,
-                                                             double* __restrict__ U, double* __restrict__ Lp,
-                                                             double* __restrict__ M, int64_t* __restrict__ piv_out) {
+// If final, also U, Lp and the original pivot rows piv_out.
+__global__ void __launch_bounds__(kThreads) lu_select_kernel(const double* __restrict__ Y, int64_t m, int l, int leaf,
+                                                             int64_t leaf_rows, const int64_t* __restrict__ cand_in,
+                                                             int64_t n_in, int G, int64_t* __restrict__ cand_out,
+                                                             int final_, double* __restrict__ U,
+                                                             double* __restrict__ Lp, int64_t* __restrict__ piv_out,
+                                                             double* __restrict__ M) {
   extern __shared__ double sm[];
-  __shared__ double rv[kThreads / 32];
-  __shared__ int64_t ri[kThreads / 32];
-  __shared__ int rr[kThreads / 32];
+  __shared__ Cand slot[2][kWarps];
   __shared__ int piv[kMaxL];
   __shared__ int nrows_s;
   const int cap = leaf ? (int)leaf_rows : G * l;
-  const int ldw = l;
+  const int ldw = l | 1;
   double* W = sm;
   int64_t* ids = reinterpret_cast<int64_t*>(W + (size_t)cap * ldw);
-  uint8_t* active = reinterpret_cast<uint8_t*>(ids + cap);
   const int tid = threadIdx.x;
 
   if (leaf) {
     const int64_t r0 = (int64_t)blockIdx.x * leaf_rows;
-    const int rows = (int)imin64(leaf_rows, m - r0);
-    if (tid == 0) nrows_s = rows;
-    for (int r = tid; r < rows; r += kThreads) { ids[r] = r0 + r; active[r] = 1; }
-    for (int idx = tid; idx < rows * l; idx += kThreads) W[idx] = Y[r0 * l + idx];
+    if (tid == 0) nrows_s = (int)imin64(leaf_rows, m - r0);
+    for (int r = tid; r < cap; r += kThreads) ids[r] = r0 + r;
   } else {
     // compact the valid candidates of this group (ascending slot order)
-    if (tid == 0) {
-      int cnt = 0;
+    if (tid < 32) {
       const int64_t s0 = (int64_t)blockIdx.x * G * l, s1 = imin64(n_in * l, s0 + (int64_t)G * l);
-      for (int64_t s = s0; s < s1; ++s)
-        if (cand_in[s] >= 0) { ids[cnt] = cand_in[s]; active[cnt] = 1; ++cnt; }
-      nrows_s = cnt;
-    }
-    __syncthreads();
-    const int rows = nrows_s;
-    for (int idx = tid; idx < rows * l; idx += kThreads) {
-      const int r = idx / l, t = idx % l;
-      W[idx] = Y[ids[r] * l + t];
+      int base = 0;
+      for (int64_t s = s0; s < s1; s += 32) {
+        const int64_t id = (s + tid < s1) ? cand_in[s + tid] : -1;
+        const unsigned mask = __ballot_sync(0xffffffffu, id >= 0);
+        if (id >= 0) ids[base + __popc(mask & ((1u << tid) - 1u))] = id;
+        base += __popc(mask);
+      }
+      if (tid == 0) nrows_s = base;
     }
   }
   __syncthreads();
   const int rows = nrows_s;
+  for (int idx = tid; idx < rows * l; idx += kThreads) {
+    const int r = idx / l, t = idx - r * l;
+    W[r * ldw + t] = Y[ids[r] * l + t];
+  }
+  __syncthreads();
   const int steps = min(rows, l);
-  gepp(W, ldw, ids, rows, l, steps, piv, active, rv, ri, rr);
-  for (int j = tid; j < l; j += kThreads)
-    cand_out[(int64_t)blockIdx.x * l + j] = j < steps ? ids[piv[j]] : -1;
+  gepp(W, ldw, ids, rows, l, steps, piv, slot);
+  for (int j = tid; j < l; j += kThreads) cand_out[(int64_t)blockIdx.x * l + j] = j < steps ? ids[piv[j]] : -1;
   if (!final_) return;
-  // final set: U (upper), Lp (unit lower of the pivot rows), piv, M
+  __syncthreads();
   for (int idx = tid; idx < l * l; idx += kThreads) {
-    const int j = idx / l, t = idx % l;
-    const double w = W[piv[j] * ldw + t];
-    U[idx] = t >= j ? w : 0.0;
-    Lp[idx] = t < j ? w : (t == j ? 1.0 : 0.0);
+    const int j = idx / l, t = idx - j * l;
+    const double v = W[piv[j] * ldw + t];
+    U[idx] = t >= j ? v : 0.0;
+    Lp[idx] = t < j ? v : (t == j ? 1.0 : 0.0);
   }
   for (int j = tid; j < l; j += kThreads) piv_out[j] = ids[piv[j]];
   __syncthreads();
-  // M row t = solution x of x·U = e_t with the zero-pivot rule
-  if (tid < l) {
-    const int t = tid;
-    for (int j = 0; j < l; ++j) {
-      double s = (j == t) ? 1.0 : 0.0;
-      for (int q = 0; q < j; ++q) s -= M[t * l + q] * U[q * l + j];
-      const double ujj = U[j * l + j];
-      M[t * l + j] = (ujj != 0.0) ? s / ujj : 0.0;
+  // M = U⁻¹ with the zero-pivot rule (a zero U_ii zeroes row i of M: x_i = 0
+  // for every input of the row substitution x·U = y, reading Q3): column j by
+  // one warp, M[j][j] = 1/U_jj, M[i][j] = −(Σ_{t=i+1..j} U_it M_tj)/U_ii.
+  double* Ms = reinterpret_cast<double*>(ids + cap);  // l×l after the row ids
+  const int lane = tid & 31, warp = tid >> 5;
+  for (int j = warp; j < l; j += kWarps) {
+    for (int i = lane; i < l; i += 32) Ms[i * l + j] = 0.0;
+    __syncwarp();
+    for (int i = j; i >= 0; --i) {
+      double acc = 0.0;
+      for (int t = i + 1 + lane; t <= j; t += 32) acc += W[piv[i] * ldw + t] * Ms[t * l + j];
+      acc = warp_sum(acc);
+      const double uii = W[piv[i] * ldw + i];
+      if (lane == 0) Ms[i * l + j] = (uii != 0.0) ? ((i == j ? 1.0 : 0.0) - acc) / uii : 0.0;
+      __syncwarp();
     }
   }
+  __syncthreads();
+  for (int idx = tid; idx < l * l; idx += kThreads) M[idx] = Ms[idx];
 }
 
-// L = Y·M (in place), pivot rows ← Lp rows.  One CTA per 128 rows.
-__global__ void __launch_bounds__(kThreads) lu_apply_kernel(double* __restrict__ Y, int64_t m, int l,
+// L = Y·M (in place) with M = U⁻¹ formed per CTA (zero-pivot rule: a zero
+// U_ii zeroes row i of M, i.e. x_i = 0 for every input, as the row
+// substitution x·U = y of reading Q3 prescribes), pivot rows ← Lp rows.  CTAs
+// walk 128-row tiles; if `gpart` is given each CTA also writes its partial
+// Gram Σ L_rᵀ L_r (upper triangle) for the Cholesky-QR that follows.
+__global__ void __launch_bounds__(kThreads, 2) lu_apply_kernel(double* __restrict__ Y, int64_t m, int l,
                                                             const double* __restrict__ M,
                                                             const double* __restrict__ Lp,
-                                                            const int64_t* __restrict__ piv) {
+                                                            const int64_t* __restrict__ piv,
+                                                            double* __restrict__ gpart) {
   extern __shared__ double sm[];
-  double* Ms = sm;               // l×l
-  double* Ys = sm + l * l;       // 128×l
-  __shared__ int64_t ps[kMaxL];
+  const int ldw = l | 1;
+  double* Ms = sm;                 // l×l
+  double* Ys = sm + l * l;         // 128×ldw
+  __shared__ int pivpos[128];
   for (int idx = threadIdx.x; idx < l * l; idx += kThreads) Ms[idx] = M[idx];
-  for (int j = threadIdx.x; j < l; j += kThreads) ps[j] = piv[j];
+  const int r = threadIdx.x & 127, jph = threadIdx.x >> 7;  // 2 column phases
+  constexpr int kPairs = kMaxL * (kMaxL + 1) / 2 / kThreads + 1;
+  double g[kPairs];
+  uint16_t gp[kPairs], gq[kPairs];
+  const int npairs = l * (l + 1) / 2;
+#pragma unroll
+  for (int i = 0; i < kPairs; ++i) {
+    g[i] = 0.0;
+    const int pq = threadIdx.x + i * kThreads;
+    int p = 0, rem = pq < npairs ? pq : 0;
+    while (rem >= l - p) { rem -= l - p; ++p; }
+    gp[i] = (uint16_t)p;
+    gq[i] = (uint16_t)(p + rem);
+  }
   for (int64_t r0 = (int64_t)blockIdx.x * 128; r0 < m; r0 += (int64_t)gridDim.x * 128) {
     const int rows = (int)imin64(128, m - r0);
     __syncthreads();
-    for (int idx = threadIdx.x; idx < rows * l; idx += kThreads) Ys[idx] = Y[r0 * l + idx];
-    __syncthreads();
+    for (int idx = threadIdx.x; idx < 128; idx += kThreads) pivpos[idx] = -1;
     for (int idx = threadIdx.x; idx < rows * l; idx += kThreads) {
-      const int r = idx / l, j = idx % l;
-      const int64_t gi = r0 + r;
-      int pj = -1;
-      for (int q = 0; q < l; ++q)
-        if (ps[q] == gi) pj = q;
-      double s;
-      if (pj >= 0) {
-        s = Lp[pj * l + j];
-      } else {
-        s = 0.0;
-        for (int t = 0; t <= j; ++t) s += Ys[r * l + t] * Ms[t * l + j];
+      const int rr = idx / l, t = idx - rr * l;
+      Ys[rr * ldw + t] = Y[r0 * l + idx];
+    }
+    __syncthreads();
+    if (threadIdx.x < l) {
+      const int64_t pr = piv[threadIdx.x] - r0;
+      if (pr >= 0 && pr < rows) pivpos[pr] = threadIdx.x;
+    }
+    __syncthreads();
+    double out[kMaxL / 2];
+    if (r < rows) {
+      const int pj = pivpos[r];
+#pragma unroll
+      for (int q = 0; q < kMaxL / 2; ++q) {
+        const int j = jph + 2 * q;
+        if (j >= l) break;
+        double s;
+        if (pj >= 0) {
+          s = Lp[pj * l + j];
+        } else {
+          double s0 = 0.0, s1 = 0.0;
+          int t = 0;
+          for (; t + 1 <= j; t += 2) {
+            s0 += Ys[r * ldw + t] * Ms[t * l + j];
+            s1 += Ys[r * ldw + t + 1] * Ms[(t + 1) * l + j];
+          }
+          if (t <= j) s0 += Ys[r * ldw + t] * Ms[t * l + j];
+          s = s0 + s1;
+        }
+        out[q] = s;
       }
-      Y[gi * l + j] = s;
+    }
+    __syncthreads();
+    if (r < rows) {
+#pragma unroll
+      for (int q = 0; q < kMaxL / 2; ++q) {
+        const int j = jph + 2 * q;
+        if (j >= l) break;
+        Ys[r * ldw + j] = out[q];
+        Y[(r0 + r) * l + j] = out[q];
+      }
+    }
+    if (gpart) {
+      __syncthreads();
+#pragma unroll
+      for (int i = 0; i < kPairs; ++i) {
+        if (threadIdx.x + i * kThreads >= npairs) break;
+        const int p = gp[i], q = gq[i];
+        double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+        int rr = 0;
+        for (; rr + 4 <= rows; rr += 4) {
+          s0 += Ys[rr * ldw + p] * Ys[rr * ldw + q];
+          s1 += Ys[(rr + 1) * ldw + p] * Ys[(rr + 1) * ldw + q];
+          s2 += Ys[(rr + 2) * ldw + p] * Ys[(rr + 2) * ldw + q];
+          s3 += Ys[(rr + 3) * ldw + p] * Ys[(rr + 3) * ldw + q];
+        }
+        for (; rr < rows; ++rr) s0 += Ys[rr * ldw + p] * Ys[rr * ldw + q];
+        g[i] += (s0 + s1) + (s2 + s3);
+      }
+    }
+  }
+  if (gpart) {
+#pragma unroll
+    for (int i = 0; i < kPairs; ++i) {
+      const int pq = threadIdx.x + i * kThreads;
+      if (pq < npairs) gpart[(int64_t)blockIdx.x * npairs + pq] = g[i];
     }
   }
 }
 
-int leaf_rows_for(int l) { return l <= 32 ? 256 : 128; }
-int group_for(int l) { return std::max(2, std::min(32, 20480 / (l * l))); }
+constexpr int kLeafRows = 256;
 
-size_t select_smem(int cap, int l) { return (size_t)cap * l * 8 + (size_t)cap * 8 + (size_t)cap + 16; }
+// a tree group holds ≤ 3·256 rows (3 rows per thread in gepp) and ≤ ~200 KB
+int group_for(int l) {
+  const int max_rows = std::min(kThreads * 3, 21000 / (l | 1));
+  return std::max(2, std::min(32, max_rows / l));
+}
+
+size_t select_smem(int cap, int l) { return (size_t)cap * (l | 1) * 8 + (size_t)cap * 8 + (size_t)l * l * 8 + 16; }
+
+void select(Ctx& c, unsigned grid, const double* Y, int64_t m, int l, int leaf, const int64_t* cin, int64_t n_in,
+            int G, int64_t* cout, int final_, double* U, double* Lp, int64_t* piv, double* M) {
+  const int cap = leaf ? kLeafRows : G * l;
+  ensure_smem((const void*)lu_select_kernel, 220 * 1024);
+  lu_select_kernel<<<grid, kThreads, select_smem(cap, l), c.stream>>>(Y, m, l, leaf, kLeafRows, cin, n_in, G, cout,
+                                                                     final_, U, Lp, piv, M);
+  RPCA_CHECK_LAUNCH();
+  count_launch(c, 1, leaf ? "lu_leaf" : "lu_tree");
+}
 
 }  // namespace
 
 size_t lu_ws_bytes(int64_t m, int l) {
   Sizer s;
-  const int64_t nblk = cdiv(m, leaf_rows_for(l));
+  const int64_t nblk = cdiv(m, kLeafRows);
   s.add<int64_t>(nblk * l);
   s.add<int64_t>(nblk * l);
-  s.add<double>(3 * (size_t)l * l);
+  s.add<double>(4 * (size_t)l * l);
   s.add<int64_t>(l);
   return s.total;
 }
 
-void lu_renorm(Ctx& c, double* Y, int64_t m, int l, double* U_out, int64_t* piv_out, Arena& ar) {
+int lu_apply_grid(Ctx& c, int64_t m) { return (int)std::min<int64_t>(cdiv(m, 128), (int64_t)c.num_sms * 2); }
+
+void lu_renorm(Ctx& c, double* Y, int64_t m, int l, double* U_out, int64_t* piv_out, Arena& ar, double* gpart) {
   RPCA_REQUIRE(l >= 1 && l <= kMaxL && m >= l, RPCA_E_SHAPE, "lu_renorm: need 1 ≤ l ≤ %d and m ≥ l", kMaxL);
-  const int lr = leaf_rows_for(l);
   const int G = group_for(l);
-  const int64_t nblk = cdiv(m, lr);
+  const int64_t nblk = cdiv(m, kLeafRows);
   int64_t* ca = ar.get<int64_t>(nblk * l);
   int64_t* cb = ar.get<int64_t>(nblk * l);
-  double* U = ar.get<double>((size_t)l * l);
+  double* U = U_out ? U_out : ar.get<double>((size_t)l * l);
   double* Lp = ar.get<double>((size_t)l * l);
-  double* M = ar.get<double>((size_t)l * l);
   int64_t* piv = ar.get<int64_t>(l);
-  const size_t smem_leaf = select_smem(lr, l), smem_tree = select_smem(G * l, l);
-  RPCA_CUDA(cudaFuncSetAttribute(lu_select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)std::max(smem_leaf, smem_tree)));
-  lu_select_kernel<<<(unsigned)nblk, kThreads, smem_leaf, c.stream>>>(Y, m, l, 1, lr, nullptr, 0, G, ca,
-                                                                      nblk == 1, U, Lp, M, piv);
-  RPCA_CHECK_LAUNCH();
-  count_launch(c, 1, "lu_leaf");
+  double* M = ar.get<double>((size_t)l * l);
+  select(c, (unsigned)nblk, Y, m, l, 1, nullptr, 0, G, ca, nblk == 1, U, Lp, piv, M);
   int64_t n = nblk;
   while (n > 1) {
     const int64_t ng = cdiv(n, G);
-    lu_select_kernel<<<(unsigned)ng, kThreads, smem_tree, c.stream>>>(Y, m, l, 0, lr, ca, n, G, cb, ng == 1, U, Lp,
-                                                                      M, piv);
-    RPCA_CHECK_LAUNCH();
-    count_launch(c, 1, "lu_tree");
+    select(c, (unsigned)ng, Y, m, l, 0, ca, n, G, cb, ng == 1, U, Lp, piv, M);
     std::swap(ca, cb);
     n = ng;
   }
-  const size_t smem_apply = (size_t)(l * l + 128 * l) * 8;
-  RPCA_CUDA(cudaFuncSetAttribute(lu_apply_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_apply));
-  const unsigned grid = (unsigned)std::min<int64_t>(cdiv(m, 128), (int64_t)c.num_sms * 4);
-  lu_apply_kernel<<<grid, kThreads, smem_apply, c.stream>>>(Y, m, l, M, Lp, piv);
+  const size_t smem_apply = (size_t)(l * l + 128 * (l | 1)) * 8;
+  ensure_smem((const void*)lu_apply_kernel, (int)((kMaxL * kMaxL + 128 * (kMaxL | 1)) * 8));
+  const unsigned grid = (unsigned)lu_apply_grid(c, m);
+  lu_apply_kernel<<<grid, kThreads, smem_apply, c.stream>>>(Y, m, l, M, Lp, piv, gpart);
   RPCA_CHECK_LAUNCH();
   count_launch(c, 1, "lu_apply");
-  if (U_out) RPCA_CUDA(cudaMemcpyAsync(U_out, U, sizeof(double) * l * l, cudaMemcpyDeviceToDevice, c.stream));
   if (piv_out) RPCA_CUDA(cudaMemcpyAsync(piv_out, piv, sizeof(int64_t) * l, cudaMemcpyDeviceToDevice, c.stream));
 }
 

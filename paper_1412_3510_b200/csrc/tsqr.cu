@@ -221,8 +221,8 @@ void qr(Ctx& c, double* Y, int64_t m, int l, double* R_out, Arena& ar) {
   int maxcap = 0;
   for (auto& x : lv) maxcap = std::max(maxcap, x.cap);
   const size_t smem_max = (size_t)2 * maxcap * l * 8;
-  RPCA_CUDA(cudaFuncSetAttribute(qr_factor_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_max));
-  RPCA_CUDA(cudaFuncSetAttribute(qr_expand_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_max));
+  ensure_smem((const void*)qr_factor_kernel, (int)smem_max);
+  ensure_smem((const void*)qr_expand_kernel, (int)smem_max);
   // factor, bottom-up
   for (size_t i = 0; i < lv.size(); ++i) {
     const size_t smem = (size_t)2 * lv[i].cap * l * 8;
