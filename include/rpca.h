@@ -95,6 +95,10 @@ rpca_status rpca_ctx_destroy(rpca_ctx* ctx);
 rpca_status rpca_ctx_set_stream(rpca_ctx* ctx, void* stream);
 rpca_status rpca_ctx_set_flags(rpca_ctx* ctx, uint32_t flags);
 rpca_status rpca_ctx_sync(rpca_ctx* ctx);
+/* drop cached state: captured CUDA graphs and the cached CSR(Aᵀ) of a sparse A
+ * (the transpose is keyed by the CSR pointers and shape — call this after
+ * modifying a sparse A in place).                                          */
+rpca_status rpca_ctx_clear_cache(rpca_ctx* ctx);
 /* bytes of workspace currently held by the context */
 rpca_status rpca_workspace_size(rpca_ctx* ctx, size_t* bytes);
 const char* rpca_strerror(rpca_status s);

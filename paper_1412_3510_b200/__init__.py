@@ -18,13 +18,13 @@ import threading
 import torch
 
 __all__ = ["pca", "eigens", "diffsnorm", "omega", "apply", "colmeans", "lu_renorm", "qr", "small_svd",
-           "launch_count", "library_path", "RPCAError"]
+           "launch_count", "library_path", "RPCAError", "CSR", "profile", "clear_cache"]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _LIB_PATH = os.path.join(_HERE, "librpca.so")
 
 OK, E_ARG, E_SHAPE, E_NONFINITE, E_NOTPSD, E_CUDA, E_NCCL, E_WORKSPACE, E_NOTIMPL, E_NOMEM = range(10)
-DENSE, CSR = 0, 1
+DENSE, CSR_KIND = 0, 1
 F64, F32 = 0, 1
 DEVICE, HOST = 0, 1
 GAUSSIAN, UNIFORM = 0, 1
@@ -70,6 +70,7 @@ def _load():
             "rpca_ctx_set_stream": [vp, vp],
             "rpca_ctx_set_flags": [vp, u32],
             "rpca_ctx_sync": [vp],
+            "rpca_ctx_clear_cache": [vp],
             "rpca_launch_count": [vp, C.POINTER(i64)],
             "rpca_workspace_size": [vp, C.POINTER(C.c_size_t)],
             "rpca_profile_begin": [vp],
@@ -143,6 +144,42 @@ def _dense(A: torch.Tensor, host=False) -> rpca_mat:
                     HOST if host else DEVICE, 0)
 
 
+class CSR:
+    """A sparse row-major matrix for the library: rowptr (int64, m+1), colind
+    (int32, sorted within rows), vals (float64/float32), shape (m, n), on one GPU."""
+
+    def __init__(self, rowptr, colind, vals, shape):
+        self.rowptr = rowptr.to(torch.int64).contiguous()
+        self.colind = colind.to(torch.int32).contiguous()
+        self.vals = vals.contiguous()
+        self.shape = tuple(int(x) for x in shape)
+        self.device = self.vals.device
+        self.dtype = self.vals.dtype
+
+    @classmethod
+    def from_torch(cls, T):
+        return cls(T.crow_indices(), T.col_indices(), T.values(), T.shape)
+
+
+def _as_mat(A, host=False):
+    """(rpca_mat, keepalive) for a dense tensor, a CSR, or a torch sparse CSR tensor."""
+    if isinstance(A, torch.Tensor) and A.layout == torch.sparse_csr:
+        A = CSR.from_torch(A)
+    if isinstance(A, CSR):
+        m, n = A.shape
+        mat = rpca_mat(CSR_KIND, _dtype_code(A.dtype), m, n, 0, m, None, n, A.rowptr.data_ptr(),
+                       A.colind.data_ptr(), A.vals.data_ptr(), A.vals.numel(), DEVICE, 0)
+        return mat, A
+    return _dense(A, host=host), A
+
+
+def clear_cache(device=None):
+    """Drop captured graphs and the cached CSR(Aᵀ) (after modifying a sparse A in place)."""
+    dev = torch.device("cuda", torch.cuda.current_device() if device is None else device)
+    L, h = _ctx(dev)
+    _check(L.rpca_ctx_clear_cache(h))
+
+
 def launch_count(device=None) -> int:
     dev = torch.device("cuda", torch.cuda.current_device() if device is None else device)
     L, h = _ctx(dev)
@@ -191,10 +228,10 @@ def omega(rows: int, cols: int, seed: int = 0, stream_id: int = 0, dist: int = G
     return out
 
 
-def colmeans(A: torch.Tensor) -> torch.Tensor:
+def colmeans(A) -> torch.Tensor:
     L, h = _ctx(A.device)
     c = torch.empty(A.shape[1], dtype=torch.float64, device=A.device)
-    mat = _dense(A)
+    mat, keep = _as_mat(A)
     _check(L.rpca_colmeans(h, C.byref(mat), _ptr(c)))
     return c
 
@@ -207,7 +244,7 @@ def apply(A: torch.Tensor, X: torch.Tensor, adjoint: bool = False, cmean: torch.
     l = X.shape[1]
     rows = A.shape[1] if adjoint else A.shape[0]
     Y = torch.empty(rows, l, dtype=torch.float64, device=A.device)
-    mat = _dense(A)
+    mat, keep = _as_mat(A)
     _check(L.rpca_apply(h, C.byref(mat), _ptr(cmean), int(adjoint), _ptr(X), l, _ptr(Y)))
     return Y
 
@@ -263,7 +300,7 @@ def pca(A: torch.Tensor, k: int, raw: bool = True, its: int = 2, l: int | None =
     U = torch.empty(m, k, dtype=A.dtype, device=outdev, pin_memory=pin)
     S = torch.empty(k, dtype=A.dtype, device=outdev, pin_memory=pin)
     V = torch.empty(n, k, dtype=A.dtype, device=outdev, pin_memory=pin)
-    mat = _dense(A, host=host)
+    mat, keep = _as_mat(A, host=host)
     try:
         _check(L_.rpca_pca(h, C.byref(mat), k, int(bool(raw)), its, -1 if l is None else l, seed,
                            _ptr(U), k, _ptr(S), _ptr(V), k))
@@ -284,7 +321,7 @@ def eigens(A: torch.Tensor, k: int, its: int = 2, l: int | None = None, seed: in
     outdev = torch.device("cpu") if host else dev
     U = torch.empty(n, k, dtype=A.dtype, device=outdev, pin_memory=host)
     lam = torch.empty(k, dtype=A.dtype, device=outdev, pin_memory=host)
-    mat = _dense(A, host=host)
+    mat, keep = _as_mat(A, host=host)
     try:
         _check(L_.rpca_eigens(h, C.byref(mat), k, its, -1 if l is None else l, seed, v, _ptr(U), k, _ptr(lam)))
     finally:
@@ -301,7 +338,7 @@ def diffsnorm(A: torch.Tensor, U: torch.Tensor, S: torch.Tensor, V: torch.Tensor
     S = S.to(torch.float64).contiguous()
     k = S.shape[0]
     out = C.c_double(0.0)
-    mat = _dense(A)
+    mat, keep = _as_mat(A)
     _check(L_.rpca_diffsnorm(h, C.byref(mat), int(bool(raw)), _ptr(U), max(k, 1), _ptr(S), _ptr(V), max(k, 1), k,
                              its, seed, C.byref(out)))
     return out.value

@@ -15,6 +15,9 @@ void eigens(Ctx&, const rpca_mat*, int64_t, int, int64_t, uint64_t, int, void*, 
 void diffsnorm(Ctx&, const rpca_mat*, int, const double*, int64_t, const double*, const double*, int64_t, int64_t,
                int, uint64_t, double*);
 const char* last_error_cstr();
+void apply_step(Ctx&, const rpca_mat*, const double*, int, const double*, int64_t, double*);
+void colmeans_step(Ctx&, const rpca_mat*, double*);
+void clear_cache(Ctx&);
 }  // namespace rpca
 
 namespace {
@@ -48,7 +51,6 @@ struct DeviceScope {
   }
 };
 
-rpca::DenseA dense_of(const rpca_mat* A) { return rpca::DenseA{A->a, A->dtype, A->m_local, A->n, A->lda}; }
 
 }  // namespace
 
@@ -90,6 +92,7 @@ rpca_status rpca_ctx_destroy(rpca_ctx* c) {
       cudaEventDestroy(c->fence_out);
     }
     if (c->ws) cudaFree(c->ws);
+    if (c->tcache.mem) cudaFree(c->tcache.mem);
     delete c;
   });
 }
@@ -201,11 +204,8 @@ rpca_status rpca_omega(rpca_ctx* c, uint64_t seed, uint32_t stream_id, int64_t r
 rpca_status rpca_colmeans(rpca_ctx* c, const rpca_mat* A, double* cm) {
   if (!c || !A || !cm) return RPCA_E_ARG;
   return guard([&] {
-    RPCA_REQUIRE(A->kind == RPCA_DENSE, RPCA_E_NOTIMPL, "colmeans: dense only");
-    RPCA_REQUIRE(A->location == RPCA_DEVICE, RPCA_E_ARG, "colmeans: device A only");
     DeviceScope ds(c->device);
-    rpca::Arena ar = c->arena((size_t)(rpca::cdiv(A->m_local, 8192) + 2) * A->n * 8 + 65536);
-    rpca::colmeans_dense(*c, A->a, A->dtype, A->m_local, A->n, A->lda, A->m, cm, ar);
+    rpca::colmeans_step(*c, A, cm);
   });
 }
 
@@ -213,24 +213,16 @@ rpca_status rpca_apply(rpca_ctx* c, const rpca_mat* A, const double* cm, int adj
                        double* Y) {
   if (!c || !A || !X || !Y) return RPCA_E_ARG;
   return guard([&] {
-    RPCA_REQUIRE(A->kind == RPCA_DENSE, RPCA_E_NOTIMPL, "apply: CSR not implemented yet");
-    RPCA_REQUIRE(A->location == RPCA_DEVICE, RPCA_E_ARG, "apply: device A only");
-    RPCA_REQUIRE(l >= 1 && l <= rpca::kMaxL, RPCA_E_SHAPE, "l out of range");
-    RPCA_REQUIRE(A->lda >= A->n && A->m_local >= 0, RPCA_E_SHAPE, "bad A");
     DeviceScope ds(c->device);
-    const rpca::DenseA d = dense_of(A);
-    rpca::Arena ar = c->arena(std::max(rpca::ax_ws_bytes(d, (int)l), rpca::aty_ws_bytes(*c, d, (int)l)) +
-                              (size_t)(rpca::cdiv(std::max(A->m_local, A->n), 8192) + 4) * 64 * 8 + 65536);
-    if (!adjoint) {
-      rpca::dense_ax(*c, d, X, (int)l, Y, ar);
-      if (cm) {
-        double* cx = ar.get<double>(rpca::kMaxL);
-        rpca::weighted_colsum(*c, cm, X, A->n, (int)l, cx, ar);
-        rpca::sub_rank1(*c, Y, A->m_local, (int)l, nullptr, cx);
-      }
-    } else {
-      rpca::dense_aty(*c, d, X, (int)l, cm, Y, ar);
-    }
+    rpca::apply_step(*c, A, cm, adjoint, X, l, Y);
+  });
+}
+
+rpca_status rpca_ctx_clear_cache(rpca_ctx* c) {
+  if (!c) return RPCA_E_ARG;
+  return guard([&] {
+    DeviceScope ds(c->device);
+    rpca::clear_cache(*c);
   });
 }
 

@@ -1,0 +1,205 @@
+// csr.cu — §8(a) row a9: sparse A in CSR.  PAPER.md:427-435 (§5): "A little
+// care in the implementation ensures that the same code can efficiently handle
+// both dense and sparse matrices" — A is applied as A*Q, its adjoint as
+// (Q'*A)' and the centring as a rank-1 correction, so the sparsity is never
+// destroyed.
+//
+// B200 design:
+//   * A·X (X n×l row-major): one warp per row of A; lane j owns columns j and
+//     j+32 of the output row, so every nonzero gathers one contiguous 8·l-byte
+//     row of X (coalesced); the row's (colind, value) pairs are loaded 32 at a
+//     time by the lanes and broadcast with shuffles.  Gather-bound: the bytes
+//     are CSR + nnz·8·l (X rows, partly L2-resident) + m·8·l.
+//   * Aᵀ·Y: the same kernel on CSR(Aᵀ).  The transpose is built on the device
+//     by a STABLE radix sort of the column indices (entry order inside a column
+//     = ascending row), so every Aᵀ·Y sum runs over rows in ascending order —
+//     deterministic, no float atomics.  It is cached on the context, keyed by
+//     the CSR pointers and shape (rpca_ctx_clear_cache drops it).
+//   * column means: per-column sums over CSR(Aᵀ) (ascending row order) / m.
+#include <cub/device/device_radix_sort.cuh>
+
+#include "internal.cuh"
+
+namespace rpca {
+namespace {
+
+constexpr int kThreads = 256;
+
+template <class T>
+__global__ void __launch_bounds__(kThreads) csr_spmm_kernel(const int64_t* __restrict__ rowptr,
+                                                            const int32_t* __restrict__ colind,
+                                                            const T* __restrict__ vals, int64_t rows,
+                                                            const double* __restrict__ X, int l,
+                                                            double* __restrict__ Y) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = (int64_t)gridDim.x * (kThreads / 32);
+  for (int64_t i = (int64_t)blockIdx.x * (kThreads / 32) + (threadIdx.x >> 5); i < rows; i += warps) {
+    const int64_t t0 = rowptr[i], t1 = rowptr[i + 1];
+    double a0 = 0.0, a1 = 0.0;
+    for (int64_t tb = t0; tb < t1; tb += 32) {
+      const int cnt = (int)imin64(32, t1 - tb);
+      int myc = 0;
+      double myv = 0.0;
+      if (lane < cnt) {
+        myc = colind[tb + lane];
+        myv = static_cast<double>(vals[tb + lane]);
+      }
+      int k = 0;
+      for (; k + 4 <= cnt; k += 4) {  // four gathers in flight
+        const int c0 = __shfl_sync(0xffffffffu, myc, k), c1 = __shfl_sync(0xffffffffu, myc, k + 1);
+        const int c2 = __shfl_sync(0xffffffffu, myc, k + 2), c3 = __shfl_sync(0xffffffffu, myc, k + 3);
+        const double v0 = __shfl_sync(0xffffffffu, myv, k), v1 = __shfl_sync(0xffffffffu, myv, k + 1);
+        const double v2 = __shfl_sync(0xffffffffu, myv, k + 2), v3 = __shfl_sync(0xffffffffu, myv, k + 3);
+        if (lane < l) {
+          const double x0 = X[(int64_t)c0 * l + lane], x1 = X[(int64_t)c1 * l + lane];
+          const double x2 = X[(int64_t)c2 * l + lane], x3 = X[(int64_t)c3 * l + lane];
+          a0 += v0 * x0;
+          a0 += v1 * x1;
+          a0 += v2 * x2;
+          a0 += v3 * x3;
+        }
+        if (lane + 32 < l) {
+          const double x0 = X[(int64_t)c0 * l + lane + 32], x1 = X[(int64_t)c1 * l + lane + 32];
+          const double x2 = X[(int64_t)c2 * l + lane + 32], x3 = X[(int64_t)c3 * l + lane + 32];
+          a1 += v0 * x0;
+          a1 += v1 * x1;
+          a1 += v2 * x2;
+          a1 += v3 * x3;
+        }
+      }
+      for (; k < cnt; ++k) {
+        const int cc = __shfl_sync(0xffffffffu, myc, k);
+        const double vv = __shfl_sync(0xffffffffu, myv, k);
+        if (lane < l) a0 += vv * X[(int64_t)cc * l + lane];
+        if (lane + 32 < l) a1 += vv * X[(int64_t)cc * l + lane + 32];
+      }
+    }
+    if (lane < l) Y[i * l + lane] = a0;
+    if (lane + 32 < l) Y[i * l + lane + 32] = a1;
+  }
+}
+
+__global__ void row_of_entry_kernel(const int64_t* __restrict__ rowptr, int64_t rows, int32_t* __restrict__ rowidx) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = (int64_t)gridDim.x * (blockDim.x / 32);
+  for (int64_t i = (int64_t)blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5); i < rows; i += warps)
+    for (int64_t t = rowptr[i] + lane; t < rowptr[i + 1]; t += 32) rowidx[t] = (int32_t)i;
+}
+
+__global__ void iota_kernel(int64_t n, int64_t* __restrict__ v) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    v[i] = i;
+}
+
+template <class T>
+__global__ void permute_kernel(const int64_t* __restrict__ perm, const int32_t* __restrict__ rowidx,
+                               const T* __restrict__ vals, int64_t nnz, int32_t* __restrict__ trow,
+                               T* __restrict__ tvals) {
+  for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < nnz; p += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t t = perm[p];
+    trow[p] = rowidx[t];
+    tvals[p] = vals[t];
+  }
+}
+
+// colptr[c] = first position of column c in the sorted keys (lower bound)
+__global__ void colptr_kernel(const int32_t* __restrict__ skeys, int64_t nnz, int64_t n, int64_t* __restrict__ colptr) {
+  for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c <= n; c += (int64_t)gridDim.x * blockDim.x) {
+    int64_t lo = 0, hi = nnz;
+    while (lo < hi) {
+      const int64_t mid = (lo + hi) >> 1;
+      if (skeys[mid] < c) lo = mid + 1;
+      else hi = mid;
+    }
+    colptr[c] = lo;
+  }
+}
+
+template <class T>
+__global__ void csr_rowsum_kernel(const int64_t* __restrict__ ptr, const T* __restrict__ v, int64_t rows,
+                                  double scale, double* __restrict__ out) {
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < rows; r += (int64_t)gridDim.x * blockDim.x) {
+    double s = 0.0;
+    for (int64_t t = ptr[r]; t < ptr[r + 1]; ++t) s += static_cast<double>(v[t]);
+    out[r] = s * scale;
+  }
+}
+
+unsigned grid_cap(Ctx& c, int64_t work, int per) {
+  int64_t b = cdiv(work, per);
+  b = std::max<int64_t>(1, std::min<int64_t>(b, (int64_t)c.num_sms * 32));
+  return (unsigned)b;
+}
+
+}  // namespace
+
+void csr_spmm(Ctx& c, const CsrA& A, const double* X, int l, double* Y) {
+  RPCA_REQUIRE(l >= 1 && l <= kMaxL, RPCA_E_SHAPE, "l out of range");
+  if (A.rows == 0) return;
+  const unsigned grid = grid_cap(c, A.rows, kThreads / 32);
+  if (A.dtype == RPCA_F64)
+    csr_spmm_kernel<double><<<grid, kThreads, 0, c.stream>>>(A.ptr, A.idx, (const double*)A.vals, A.rows, X, l, Y);
+  else
+    csr_spmm_kernel<float><<<grid, kThreads, 0, c.stream>>>(A.ptr, A.idx, (const float*)A.vals, A.rows, X, l, Y);
+  RPCA_CHECK_LAUNCH();
+  count_launch(c, 1, "csr_spmm");
+}
+
+size_t csr_transpose_ws_bytes(const CsrA& A) {
+  size_t tmp = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, tmp, (const int32_t*)nullptr, (int32_t*)nullptr, (const int64_t*)nullptr,
+                                  (int64_t*)nullptr, (size_t)A.nnz);
+  Sizer s;
+  s.add<int32_t>(A.nnz);  // rowidx
+  s.add<int32_t>(A.nnz);  // sorted keys
+  s.add<int64_t>(A.nnz);  // iota
+  s.add<int64_t>(A.nnz);  // perm
+  s.add<char>(tmp + 256);
+  return s.total;
+}
+
+void csr_transpose(Ctx& c, const CsrA& A, int64_t n, CsrA& T, Arena& scratch) {
+  const int64_t nnz = A.nnz;
+  const int es = A.dtype == RPCA_F64 ? 8 : 4;
+  int32_t* rowidx = scratch.get<int32_t>(nnz);
+  int32_t* skeys = scratch.get<int32_t>(nnz);
+  int64_t* iota = scratch.get<int64_t>(nnz);
+  int64_t* perm = scratch.get<int64_t>(nnz);
+  size_t tmp = 0;
+  RPCA_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp, A.idx, skeys, iota, perm, (size_t)nnz));
+  void* tmpbuf = scratch.get<char>(tmp + 256);
+  row_of_entry_kernel<<<grid_cap(c, A.rows, 8), 256, 0, c.stream>>>(A.ptr, A.rows, rowidx);
+  RPCA_CHECK_LAUNCH();
+  iota_kernel<<<grid_cap(c, nnz, 256), 256, 0, c.stream>>>(nnz, iota);
+  RPCA_CHECK_LAUNCH();
+  int bits = 1;
+  while ((int64_t(1) << bits) < n && bits < 31) ++bits;
+  RPCA_CUDA(cub::DeviceRadixSort::SortPairs(tmpbuf, tmp, A.idx, skeys, iota, perm, (size_t)nnz, 0, bits, c.stream));
+  int64_t* colptr = const_cast<int64_t*>(T.ptr);
+  colptr_kernel<<<grid_cap(c, n + 1, 256), 256, 0, c.stream>>>(skeys, nnz, n, colptr);
+  RPCA_CHECK_LAUNCH();
+  if (es == 8)
+    permute_kernel<double><<<grid_cap(c, nnz, 256), 256, 0, c.stream>>>(
+        perm, rowidx, (const double*)A.vals, nnz, const_cast<int32_t*>(T.idx), (double*)const_cast<void*>(T.vals));
+  else
+    permute_kernel<float><<<grid_cap(c, nnz, 256), 256, 0, c.stream>>>(
+        perm, rowidx, (const float*)A.vals, nnz, const_cast<int32_t*>(T.idx), (float*)const_cast<void*>(T.vals));
+  RPCA_CHECK_LAUNCH();
+  count_launch(c, 5, "csr_transpose");
+  T.rows = n;
+  T.nnz = nnz;
+  T.dtype = A.dtype;
+}
+
+void csr_colmeans(Ctx& c, const CsrA& T, int64_t m_total, double* cmean) {
+  if (T.dtype == RPCA_F64)
+    csr_rowsum_kernel<double><<<grid_cap(c, T.rows, 256), 256, 0, c.stream>>>(T.ptr, (const double*)T.vals, T.rows,
+                                                                              1.0 / (double)m_total, cmean);
+  else
+    csr_rowsum_kernel<float><<<grid_cap(c, T.rows, 256), 256, 0, c.stream>>>(T.ptr, (const float*)T.vals, T.rows,
+                                                                             1.0 / (double)m_total, cmean);
+  RPCA_CHECK_LAUNCH();
+  count_launch(c, 1, "csr_colmeans");
+}
+
+}  // namespace rpca

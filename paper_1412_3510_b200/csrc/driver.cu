@@ -207,37 +207,97 @@ void validate_mat(const rpca_mat* A) {
     RPCA_REQUIRE(A->a || A->m_local == 0, RPCA_E_ARG, "A.a is NULL");
     RPCA_REQUIRE(A->lda >= A->n, RPCA_E_SHAPE, "lda < n");
   } else {
-    RPCA_REQUIRE(A->kind != RPCA_CSR, RPCA_E_NOTIMPL, "CSR inputs are not implemented yet");
+    RPCA_REQUIRE(A->rowptr && (A->nnz == 0 || (A->colind && A->vals)), RPCA_E_ARG, "CSR arrays are NULL");
+    RPCA_REQUIRE(A->nnz >= 0 && A->n <= INT32_MAX, RPCA_E_SHAPE, "bad nnz / n > 2^31-1");
+    RPCA_REQUIRE(A->location == RPCA_DEVICE, RPCA_E_NOTIMPL, "host CSR inputs are not supported");
   }
 }
 
-// Device view of A's local shard; copies a host A into the workspace.
-DenseA device_view(Ctx& c, const rpca_mat* A, Arena& ar) {
-  DenseA d{A->a, A->dtype, A->m_local, A->n, A->lda};
+// Device view of A's local shard (dense or CSR + cached CSR(Aᵀ)).
+struct MatV {
+  bool csr = false;
+  DenseA d{};
+  CsrA a{}, at{};
+  int64_t m = 0, n = 0;  // local rows, columns
+  int dtype = RPCA_F64;
+};
+
+MatV probe_of(const rpca_mat* A) {
+  MatV v;
+  v.csr = A->kind == RPCA_CSR;
+  v.m = A->m_local;
+  v.n = A->n;
+  v.dtype = A->dtype;
+  v.d = DenseA{A->a, A->dtype, A->m_local, A->n, A->lda};
+  v.a = CsrA{A->rowptr, A->colind, A->vals, A->dtype, A->m_local, A->nnz};
+  return v;
+}
+
+// CSR(Aᵀ) is built once per sparse A (before any graph capture) and cached.
+void ensure_transpose(Ctx& c, const rpca_mat* A) {
+  if (A->kind != RPCA_CSR) return;
+  KeyHasher kh;
+  kh << A->rowptr << A->colind << A->vals << A->m_local << A->n << A->nnz << A->dtype;
+  if (c.tcache.mem && c.tcache.key == kh.h) return;
+  if (c.tcache.mem) {
+    RPCA_CUDA(cudaStreamSynchronize(c.stream));
+    RPCA_CUDA(cudaFree(c.tcache.mem));
+    c.tcache.mem = nullptr;
+  }
+  const int es = elem_size(A->dtype);
+  const size_t b_ptr = Arena::align((A->n + 1) * 8), b_idx = Arena::align(A->nnz * 4 + 4);
+  const size_t b_val = Arena::align(A->nnz * es + 8);
+  char* mem = nullptr;
+  RPCA_CUDA(cudaMalloc(&mem, b_ptr + b_idx + b_val));
+  CsrA src{A->rowptr, A->colind, A->vals, A->dtype, A->m_local, A->nnz};
+  CsrA T{reinterpret_cast<int64_t*>(mem), reinterpret_cast<int32_t*>(mem + b_ptr), mem + b_ptr + b_idx, A->dtype,
+         A->n, A->nnz};
+  const size_t sb = csr_transpose_ws_bytes(src) + 65536;
+  char* scratch = nullptr;
+  RPCA_CUDA(cudaMalloc(&scratch, sb));
+  Arena ar{scratch, sb, 0};
+  csr_transpose(c, src, A->n, T, ar);
+  RPCA_CUDA(cudaStreamSynchronize(c.stream));
+  RPCA_CUDA(cudaFree(scratch));
+  c.tcache.mem = mem;
+  c.tcache.key = kh.h;
+  c.tcache.T = T;
+}
+
+MatV device_view(Ctx& c, const rpca_mat* A, Arena& ar) {
+  MatV v = probe_of(A);
+  if (v.csr) {
+    v.at = c.tcache.T;
+    return v;
+  }
   if (A->location == RPCA_HOST && A->m_local > 0) {
     const size_t bytes = (size_t)A->m_local * A->lda * elem_size(A->dtype);
     void* dev = ar.get<char>(bytes);
     RPCA_CUDA(cudaMemcpyAsync(dev, A->a, bytes, cudaMemcpyHostToDevice, c.stream));
-    d.a = dev;
+    v.d.a = dev;
   }
-  return d;
+  return v;
 }
 
 size_t host_copy_bytes(const rpca_mat* A) {
-  return A->location == RPCA_HOST ? (size_t)A->m_local * A->lda * elem_size(A->dtype) + 256 : 0;
+  return (A->kind == RPCA_DENSE && A->location == RPCA_HOST)
+             ? (size_t)A->m_local * A->lda * elem_size(A->dtype) + 256
+             : 0;
 }
 
 // The operator the range finder sketches (reading Q6): F = A, or Aᵀ if m < n.
 struct Op {
-  DenseA A;
+  MatV A;
   const double* cmean;
   bool trans;
 };
 
-void apply_ax(Ctx& c, const DenseA& A, const double* cmean, const double* X, int l, double* Y, Arena& ar) {
+// Y = A·X [− 1·(c·X)]
+void apply_ax(Ctx& c, const MatV& A, const double* cmean, const double* X, int l, double* Y, Arena& ar) {
   const size_t mark = ar.off;
-  dense_ax(c, A, X, l, Y, ar);
-  if (cmean) {  // Y −= 1·(c·X)
+  if (A.csr) csr_spmm(c, A.a, X, l, Y);
+  else dense_ax(c, A.d, X, l, Y, ar);
+  if (cmean) {
     double* cx = ar.get<double>(kMaxL);
     weighted_colsum(c, cmean, X, A.n, l, cx, ar);
     sub_rank1(c, Y, A.m, l, nullptr, cx);
@@ -245,9 +305,26 @@ void apply_ax(Ctx& c, const DenseA& A, const double* cmean, const double* X, int
   ar.off = mark;
 }
 
-void apply_aty(Ctx& c, const DenseA& A, const double* cmean, const double* Y, int l, double* Z, Arena& ar) {
+// Z = Aᵀ·Y [− cᵀ·(1ᵀY)]
+void apply_aty(Ctx& c, const MatV& A, const double* cmean, const double* Y, int l, double* Z, Arena& ar) {
   const size_t mark = ar.off;
-  dense_aty(c, A, Y, l, cmean, Z, ar);
+  if (A.csr) {
+    csr_spmm(c, A.at, Y, l, Z);
+    if (cmean) {
+      double* sy = ar.get<double>(kMaxL);
+      weighted_colsum(c, nullptr, Y, A.m, l, sy, ar);
+      sub_rank1(c, Z, A.n, l, cmean, sy);
+    }
+  } else {
+    dense_aty(c, A.d, Y, l, cmean, Z, ar);
+  }
+  ar.off = mark;
+}
+
+void colmeans(Ctx& c, const MatV& A, int64_t m_total, double* cmean, Arena& ar) {
+  const size_t mark = ar.off;
+  if (A.csr) csr_colmeans(c, A.at, m_total, cmean);
+  else colmeans_dense(c, A.d.a, A.d.dtype, A.d.m, A.d.n, A.d.lda, m_total, cmean, ar);
   ar.off = mark;
 }
 
@@ -260,8 +337,10 @@ void adj(Ctx& c, const Op& F, const double* Y, int l, double* Z, Arena& ar) {
   else apply_aty(c, F.A, F.cmean, Y, l, Z, ar);
 }
 
-size_t op_ws(Ctx& c, const DenseA& A, int l) {
-  return std::max(ax_ws_bytes(A, l) + 4096 * 4, aty_ws_bytes(c, A, l)) + 65536;
+size_t op_ws(Ctx& c, const MatV& A, int l) {
+  const size_t small = (size_t)(cdiv(std::max(A.m, A.n), 8192) + 4) * kMaxL * 8 * 2 + 65536;
+  if (A.csr) return small;
+  return std::max(ax_ws_bytes(A.d, l) + 4096 * 4, aty_ws_bytes(c, A.d, l)) + small;
 }
 
 void renorm_lu(Ctx& c, double* Y, int64_t rows, int l, Arena& ar) {
@@ -286,6 +365,39 @@ void sync_status(Ctx& c) { RPCA_CUDA(cudaStreamSynchronize(c.stream)); }
 
 }  // namespace
 
+// ============================================================ step APIs
+void apply_step(Ctx& c, const rpca_mat* Am, const double* cm, int adjoint, const double* X, int64_t l, double* Y) {
+  validate_mat(Am);
+  RPCA_REQUIRE(Am->location == RPCA_DEVICE, RPCA_E_ARG, "apply: device A only");
+  RPCA_REQUIRE(l >= 1 && l <= kMaxL && X && Y, RPCA_E_SHAPE, "apply: bad l / NULL X, Y");
+  ensure_transpose(c, Am);
+  const MatV probe = probe_of(Am);
+  Arena ar = c.arena(op_ws(c, probe, (int)l) + 65536);
+  const MatV A = device_view(c, Am, ar);
+  if (adjoint) apply_aty(c, A, cm, X, (int)l, Y, ar);
+  else apply_ax(c, A, cm, X, (int)l, Y, ar);
+}
+
+void colmeans_step(Ctx& c, const rpca_mat* Am, double* cm) {
+  validate_mat(Am);
+  RPCA_REQUIRE(Am->location == RPCA_DEVICE && cm, RPCA_E_ARG, "colmeans: device A and c only");
+  ensure_transpose(c, Am);
+  const MatV probe = probe_of(Am);
+  Arena ar = c.arena((size_t)(cdiv(probe.m, 8192) + 2) * probe.n * 8 + 65536);
+  const MatV A = device_view(c, Am, ar);
+  colmeans(c, A, Am->m, cm, ar);
+}
+
+void clear_cache(Ctx& c) {
+  if (c.tcache.mem) {
+    RPCA_CUDA(cudaStreamSynchronize(c.stream));
+    RPCA_CUDA(cudaFree(c.tcache.mem));
+    c.tcache.mem = nullptr;
+    c.tcache.key = 0;
+  }
+  drop_graphs(c);
+}
+
 // ============================================================ rpca_pca
 void pca(Ctx& c, const rpca_mat* Am, int64_t k, int raw, int its, int64_t l, uint64_t seed, void* U, int64_t ldu,
          void* S, void* V, int64_t ldv) {
@@ -304,7 +416,7 @@ void pca(Ctx& c, const rpca_mat* Am, int64_t k, int raw, int its, int64_t l, uin
   const int64_t m = Am->m, n = Am->n;
 
   // ---- workspace plan (allocation happens before any capture)
-  DenseA probe{Am->a, Am->dtype, m, n, Am->lda};
+  const MatV probe = probe_of(Am);
   const bool trans = m < n;
   const int64_t nin = trans ? m : n, nout = trans ? n : m;
   Sizer sz;
@@ -325,14 +437,15 @@ void pca(Ctx& c, const rpca_mat* Am, int64_t k, int raw, int its, int64_t l, uin
   scratch = std::max(scratch, lu_ws_bytes(std::max(nin, nout), L));
   scratch = std::max(scratch, orth_ws_bytes(std::max(nin, nout), L));
   scratch = std::max(scratch, (size_t)(cdiv(std::max(m, n), 8192) + 2) * (n + 2 * k) * 8 + 65536);
+  ensure_transpose(c, Am);
   Arena ar = c.arena(fixed + scratch + 65536);
 
   KeyHasher kh;
-  kh << 1 << *Am << k << raw << its << l << seed << U << ldu << S << V << ldv << c.flags << c.ws;
+  kh << 1 << *Am << k << raw << its << l << seed << U << ldu << S << V << ldv << c.flags << c.ws << c.tcache.mem;
   const bool graphable = Am->location == RPCA_DEVICE && !out_host;
 
   execute(c, kh.h, graphable, [&] {
-    const DenseA dA = device_view(c, Am, ar);
+    const MatV dA = device_view(c, Am, ar);
     double* Zb = ar.get<double>(nin * l);
     double* Yb = ar.get<double>(nout * l);
     double* cmean = ar.get<double>(n);
@@ -351,7 +464,7 @@ void pca(Ctx& c, const rpca_mat* Am, int64_t k, int raw, int its, int64_t l, uin
     Op F{dA, nullptr, trans};
     if (!raw) {
       const size_t mark = ar.off;
-      colmeans_dense(c, dA.a, dA.dtype, dA.m, dA.n, dA.lda, m, cmean, ar);
+      colmeans(c, dA, m, cmean, ar);
       ar.off = mark;
       F.cmean = cmean;
     }
@@ -413,7 +526,7 @@ void eigens(Ctx& c, const rpca_mat* Am, int64_t k, int its, int64_t l, uint64_t 
   const int dist = (c.flags & RPCA_FLAG_UNIFORM_OMEGA) ? RPCA_UNIFORM : RPCA_GAUSSIAN;
   const int odt = Am->dtype, osz = elem_size(odt);
 
-  DenseA probe{Am->a, Am->dtype, n, n, Am->lda};
+  const MatV probe = probe_of(Am);
   Sizer sz;
   sz.add<char>(host_copy_bytes(Am));
   sz.add<double>(3 * n * l);
@@ -438,7 +551,7 @@ void eigens(Ctx& c, const rpca_mat* Am, int64_t k, int its, int64_t l, uint64_t 
   void* Ud = U;
   void* Ld = lam;
   execute(c, kh.h, graphable, [&] {
-    const DenseA dA = device_view(c, Am, ar);
+    const MatV dA = device_view(c, Am, ar);
     Q = ar.get<double>(n * l);
     double* B1 = ar.get<double>(n * l);
     double* Fm = ar.get<double>(n * l);
@@ -522,18 +635,19 @@ void diffsnorm(Ctx& c, const rpca_mat* Am, int raw, const double* U, int64_t ldu
   RPCA_REQUIRE(k >= 0 && its >= 1 && out, RPCA_E_SHAPE, "bad k/its/out");
   RPCA_REQUIRE(k == 0 || (U && S && V && ldu >= k && ldv >= k), RPCA_E_ARG, "bad factors");
   const int64_t m = Am->m, n = Am->n;
-  DenseA probe{Am->a, Am->dtype, m, n, Am->lda};
+  const MatV probe = probe_of(Am);
   Sizer sz;
   sz.add<char>(host_copy_bytes(Am));
   sz.add<double>(2 * n + m + n + k + 64);
   size_t scratch = op_ws(c, probe, 1) + (size_t)(cdiv(std::max(m, n), 8192) + 2) * (n + 64) * 8;
+  ensure_transpose(c, Am);
   Arena ar = c.arena(sz.total + scratch + 65536);
   if (!c.status_host) RPCA_CUDA(cudaMallocHost(&c.status_host, 64));
   KeyHasher kh;
-  kh << 3 << *Am << raw << U << ldu << S << V << ldv << k << its << seed << c.ws;
+  kh << 3 << *Am << raw << U << ldu << S << V << ldv << k << its << seed << c.ws << c.tcache.mem;
   double* sc = nullptr;
   execute(c, kh.h, Am->location == RPCA_DEVICE, [&] {
-    const DenseA dA = device_view(c, Am, ar);
+    const MatV dA = device_view(c, Am, ar);
     double* x = ar.get<double>(n);
     double* z = ar.get<double>(n);
     double* y = ar.get<double>(m);
@@ -543,7 +657,7 @@ void diffsnorm(Ctx& c, const rpca_mat* Am, int raw, const double* U, int64_t ldu
     int* done = ar.get<int>(4);
     if (!raw) {
       const size_t mark = ar.off;
-      colmeans_dense(c, dA.a, dA.dtype, dA.m, dA.n, dA.lda, m, cmean, ar);
+      colmeans(c, dA, m, cmean, ar);
       ar.off = mark;
     }
     const double* cm = raw ? nullptr : cmean;

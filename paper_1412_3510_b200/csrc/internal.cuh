@@ -40,6 +40,16 @@ struct Sizer {
 
 struct Comm;  // multi-GPU communicator (comm.cu)
 
+// sparse A (row-major CSR, int64 row pointers, int32 sorted column indices)
+struct CsrA {
+  const int64_t* ptr;
+  const int32_t* idx;
+  const void* vals;
+  int dtype;
+  int64_t rows, nnz;
+};
+
+
 // Optional per-launch timing (rpca_profile): an event is recorded on the
 // context stream after every launch; a launch's duration is the gap to the
 // previous event (launches are stream-serialised).
@@ -75,6 +85,12 @@ struct Ctx {
   std::vector<std::pair<uint64_t, CachedGraph>> graphs;
   int* status_host = nullptr;  // pinned scratch for device status words
   cudaStream_t work = nullptr;   // private stream the drivers run (and capture) on
+  // cached CSR(Aᵀ) of the last sparse A (keyed by its pointers and shape)
+  struct TransposeCache {
+    uint64_t key = 0;
+    void* mem = nullptr;
+    CsrA T{};
+  } tcache;
   cudaEvent_t fence_in = nullptr, fence_out = nullptr;
   Arena arena(size_t bytes);  // ensures capacity, returns an arena over the workspace
 };
@@ -130,6 +146,15 @@ void dense_ax(Ctx& c, const DenseA& A, const double* X, int l, double* Y, Arena&
 size_t aty_ws_bytes(Ctx& c, const DenseA& A, int l);
 // Z (n×l) = Aᵀ·Y [− cmean ⊗ colsum(Y)] (cmean may be NULL)
 void dense_aty(Ctx& c, const DenseA& A, const double* Y, int l, const double* cmean, double* Z, Arena& ar);
+
+// csr.cu — sparse A (row-major CSR, int64 row pointers, int32 sorted column indices)
+// Y (rows×l) = A·X   (X has as many rows as A has columns)
+void csr_spmm(Ctx& c, const CsrA& A, const double* X, int l, double* Y);
+size_t csr_transpose_ws_bytes(const CsrA& A);
+// T = CSR(Aᵀ) (n rows) into caller buffers T.ptr (n+1), T.idx, T.vals (nnz); stable in rows
+void csr_transpose(Ctx& c, const CsrA& A, int64_t n, CsrA& T, Arena& scratch);
+// cmean[j] = (Σ_i A_ij)/m_total from CSR(Aᵀ), rows ascending
+void csr_colmeans(Ctx& c, const CsrA& T, int64_t m_total, double* cmean);
 
 // tslu.cu
 size_t lu_ws_bytes(int64_t m, int l);

@@ -286,3 +286,52 @@ def test_pca_c2_full_size():
     res = rp.pca(A, 20, raw=True, its=2, l=22, seed=0)
     o = oracle.pca(A.cpu().numpy(), 20, its=2, l=22, seed=0)
     compare(res, o, 20)
+
+
+# ----------------------------------------------------------------- a9: sparse CSR
+def csr_case(m, n, seed=7, planted_rows=None):
+    rp_, ci, va = synth.make_c5(m=m, n=n, seed=seed, device=dev(), planted_rows=planted_rows,
+                                planted_cols=min(200, n))
+    A = rp.CSR(rp_, ci, va, (m, n))
+    host = (rp_.cpu().numpy(), ci.cpu().numpy(), va.cpu().numpy(), (m, n))
+    return A, host
+
+
+def dense_of(host):
+    rp_, ci, va, (m, n) = host
+    D = np.zeros((m, n))
+    for i in range(m):
+        D[i, ci[rp_[i]:rp_[i + 1]]] += va[rp_[i]:rp_[i + 1]]
+    return D
+
+
+@pytest.mark.parametrize("m,n,l", [(3000, 700, 32), (1000, 2500, 12), (5000, 300, 64)])
+def test_csr_apply_and_colmeans(m, n, l):
+    A, host = csr_case(m, n, planted_rows=30)
+    g = torch.Generator(device="cuda").manual_seed(11)
+    X = torch.randn(n, l, generator=g, device=dev(), dtype=torch.float64)
+    Y = torch.randn(m, l, generator=g, device=dev(), dtype=torch.float64)
+    D = dense_of(host)
+    Xn, Yn = X.cpu().numpy(), Y.cpu().numpy()
+    got = rp.apply(A, X).cpu().numpy()
+    assert np.all(np.abs(got - oracle.apply(host, Xn)) <= 2 * gamma(64) * (np.abs(D) @ np.abs(Xn)) + 1e-300)
+    got = rp.apply(A, Y, adjoint=True).cpu().numpy()
+    assert np.all(np.abs(got - oracle.apply(host, Yn, adjoint=True)) <= 2 * gamma(64) * (np.abs(D).T @ np.abs(Yn)) + 1e-300)
+    c = rp.colmeans(A).cpu().numpy()
+    assert np.allclose(c, oracle.colmeans(host), rtol=1e-13, atol=1e-15)
+    got = rp.apply(A, Y, adjoint=True, cmean=rp.colmeans(A)).cpu().numpy()
+    ref = oracle.apply(host, Yn, adjoint=True, raw=False)
+    assert np.allclose(got, ref, atol=1e-11 * np.abs(ref).max())
+
+
+@pytest.mark.parametrize("m,n,raw", [(10000, 1000, True), (10000, 1000, False), (800, 3000, True)])
+def test_pca_csr_scaled_c5(m, n, raw):
+    """C5 recipe at m = 1e4, n = 1e3 (scaled C5 pinned vs the oracle)."""
+    A, host = csr_case(m, n, planted_rows=max(1, m // 100))
+    k, l, its = 30, 32, 2
+    res = rp.pca(A, k, raw=raw, its=its, l=l, seed=0)
+    o = oracle.pca(host, k, raw=raw, its=its, l=l, seed=0)
+    compare(res, o, k)
+    est = rp.diffsnorm(A, *res, raw=raw, its=20, seed=1)
+    ref = oracle.diffsnorm(host, *[t.cpu().numpy() for t in res], raw=raw, its=20, seed=1)
+    assert abs(est - ref) <= 1e-9 * ref
