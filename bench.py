@@ -41,7 +41,7 @@ def parse():
     p.add_argument("--steps", type=int, default=20)
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    p.add_argument("--config", default="C2", choices=["C1", "C2", "C3", "C4"])
+    p.add_argument("--config", default="C2", choices=["C1", "C2", "C3", "C4", "C5"])
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-seconds", type=float, default=8.0, help="target oracle seconds per sample run")
@@ -127,10 +127,29 @@ def workload(name):
     }
 
 
-def make_input(cfg, device):
+def make_input(cfg, device, rp=None):
     A = synth.make(cfg.name, device=device)
     torch.cuda.synchronize()
+    if cfg.kind == "csr":
+        rowptr, colind, vals = A
+        return rp.CSR(rowptr, colind, vals, (cfg.m, cfg.n))
     return A
+
+
+def a_bytes(A):
+    """bytes of A as stored (dense elements, or CSR row pointers + indices + values)."""
+    if isinstance(A, torch.Tensor):
+        return A.numel() * A.element_size()
+    return (A.rowptr.numel() * 8 + A.colind.numel() * 4 + A.vals.numel() * A.vals.element_size())
+
+
+def pass_bytes(A, cfg):
+    """algorithmic bytes of one pass of the dominant kernel: all of A, plus for CSR
+    the gathered operand rows (8·l per nonzero) and the written output rows."""
+    if isinstance(A, torch.Tensor):
+        return a_bytes(A)
+    nnz = A.vals.numel()
+    return a_bytes(A) + nnz * 8 * cfg.l + cfg.m * 8 * cfg.l
 
 
 def run_step(rp, cfg, A):
@@ -221,8 +240,9 @@ def main():
     import paper_1412_3510_b200 as rp
 
     cfg, conf = workload(args.config)
-    A = make_input(cfg, dev)
-    abytes = A.numel() * A.element_size()
+    A = make_input(cfg, dev, rp)
+    abytes = a_bytes(A)
+    pbytes = pass_bytes(A, cfg)
     passes = conf["passes_over_A"]
     conf.update({"l2": f"A ({abytes / 1e9:.2f} GB) > L2 (126 MB): no flush needed",
                  "parallelism": f"replicas x{ws}" if ws > 1 else "single GPU"})
@@ -264,16 +284,16 @@ def main():
         c, s = kern.get(name, (0, 0.0))
         kern[name] = (c + 1, s + msec)
     step_ms = ms_total / args.steps
-    passes_k = {k: v for k, v in kern.items() if k.startswith(("ax_", "aty_f64", "aty_generic"))}
+    passes_k = {k: v for k, v in kern.items() if k.startswith(("ax_", "aty_f64", "aty_generic", "csr_spmm"))}
     dom = max(passes_k.items(), key=lambda kv: kv[1][1]) if passes_k else None
     roof = None
     if dom:
         cnt, tot = dom[1]
         avg_ms = tot / cnt
-        achieved = abytes / (avg_ms / 1e3) / 1e9
+        achieved = pbytes / (avg_ms / 1e3) / 1e9
         roof = {"bound": "hbm", "kernel": dom[0], "achieved": round(achieved, 1), "peak": hbm, "unit": "GB/s",
                 "frac": round(achieved / hbm, 4), "traffic": None, "peak_source": peak_src,
-                "algorithmic_bytes_per_launch": abytes, "avg_launch_ms": round(avg_ms, 5),
+                "algorithmic_bytes_per_launch": pbytes, "avg_launch_ms": round(avg_ms, 5),
                 "share_of_step": round(tot / args.steps / step_ms, 4)}
         all_pass_ms = sum(v[1] for v in passes_k.values()) / args.steps
         roof["all_passes"] = {"launches_per_step": sum(v[0] for v in passes_k.values()) // args.steps,
@@ -282,7 +302,7 @@ def main():
                  for k, v in sorted(kern.items(), key=lambda kv: -kv[1][1])}
 
     e2e = None
-    if not args.no_e2e and rank == 0:
+    if not args.no_e2e and rank == 0 and isinstance(A, torch.Tensor):
         Ah = A.cpu().pin_memory()
         run_step(rp, cfg, Ah)  # warm
         torch.cuda.synchronize()
@@ -297,14 +317,15 @@ def main():
         del Ah
 
     cpu = None
-    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline and isinstance(A, torch.Tensor):
         cpu = cpu_baseline(cfg, A.cpu().numpy(), args.cpu_seconds)
 
     if rank == 0:
         line = {"metric": "rank-k PCA wall time (s)", "value": t_step, "unit": "s", "n_gpus": ws,
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_step * 1e3,
                 "higher_is_better": False, "scaling": "weak", "vs_baseline": None,
-                "dtype": "f64" if A.dtype == torch.float64 else "f32", "data": "synthetic", "config": conf,
+                "dtype": "f64" if A.dtype == torch.float64 else "f32",
+                "a_bytes": abytes, "data": "synthetic", "config": conf,
                 "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
                 "clocks": clk.summary(), "kernels": breakdown,
                 "roofline_time_s": abytes * passes / (hbm * 1e9)}

@@ -546,29 +546,34 @@ void eigens(Ctx& c, const rpca_mat* Am, int64_t k, int its, int64_t l, uint64_t 
   KeyHasher kh;
   kh << 2 << *Am << k << its << l << seed << variant << U << ldu << lam << c.flags << c.ws;
   const bool graphable = Am->location == RPCA_DEVICE && !out_host;
-  double* Q = nullptr;
-  int* status = nullptr;
+  // fixed buffers are carved before execute() so that graph replays (which do
+  // not run the lambda) see the same pointers
+  const MatV dA0 = probe_of(Am);
+  (void)dA0;
+  double* Qbuf = ar.get<double>(n * l);
+  double* Bbuf = ar.get<double>(n * l);
+  double* Fm = ar.get<double>(n * l);
+  double* G = ar.get<double>(l * l);
+  double* Minv = ar.get<double>(l * l);
+  double* R = ar.get<double>(l * l);
+  double* W = ar.get<double>(l * l);
+  double* Vr = ar.get<double>(l * l);
+  double* sig = ar.get<double>(l);
+  double* scal = ar.get<double>(8);  // [0] = ‖B1‖_F², [1] = ν
+  int* status = ar.get<int>(4);
   void* Ud = U;
   void* Ld = lam;
+  if (out_host) {
+    Ud = ar.get<char>((size_t)n * ldu * osz);
+    Ld = ar.get<char>((size_t)k * osz);
+  }
+  double* Q = (its & 1) ? Bbuf : Qbuf;  // where the final Q lives after the loop's swaps
   execute(c, kh.h, graphable, [&] {
     const MatV dA = device_view(c, Am, ar);
-    Q = ar.get<double>(n * l);
-    double* B1 = ar.get<double>(n * l);
-    double* Fm = ar.get<double>(n * l);
-    double* G = ar.get<double>(l * l);
-    double* Minv = ar.get<double>(l * l);
-    double* R = ar.get<double>(l * l);
-    double* W = ar.get<double>(l * l);
-    double* Vr = ar.get<double>(l * l);
-    double* sig = ar.get<double>(l);
-    double* scal = ar.get<double>(8);  // [0] = ‖B1‖_F², [1] = ν
-    status = ar.get<int>(4);
+    double* Q = Qbuf;
+    double* B1 = Bbuf;
     double* side = ar.get<double>(n * k);
     double* sign = ar.get<double>(k);
-    if (out_host) {
-      Ud = ar.get<char>((size_t)n * ldu * osz);
-      Ld = ar.get<char>((size_t)k * osz);
-    }
     // self-adjoint loop: Y = AΩ, then its × (Q = A·Q)
     omega(c, seed, 0u, n, l, dist, odt == RPCA_F32, B1);
     apply_ax(c, dA, nullptr, B1, L, Q, ar);
@@ -583,7 +588,9 @@ void eigens(Ctx& c, const rpca_mat* Am, int64_t k, int its, int64_t l, uint64_t 
     apply_ax(c, dA, nullptr, Q, L, B1, ar);  // (start) B1 = A·Q
     {
       const size_t mark = ar.off;
-      gram(c, Q, B1, n, L, G, ar);  // (second) QᵀB1, symmetrised in the kernels below
+      // (second) B2 = QᵀB1 (symmetrised in the kernels below) — an "Aᵀ·Y" with
+      // A := Q (n×l), Y := B1, so it runs on the fp64 tensor-core adjoint kernel
+      dense_aty(c, DenseA{Q, RPCA_F64, n, L, L}, B1, L, nullptr, G, ar);
       if (variant == RPCA_SHIFT_CHOL) {
         weighted_colsum(c, B1, B1, n * l, 1, scal, ar);  // ‖B1‖_F²
         nystrom_shift_chol(c, G, scal, L, n, odt == RPCA_F32 ? 0x1p-23 : 0x1p-52, Minv, scal + 1, status);
@@ -645,16 +652,15 @@ void diffsnorm(Ctx& c, const rpca_mat* Am, int raw, const double* U, int64_t ldu
   if (!c.status_host) RPCA_CUDA(cudaMallocHost(&c.status_host, 64));
   KeyHasher kh;
   kh << 3 << *Am << raw << U << ldu << S << V << ldv << k << its << seed << c.ws << c.tcache.mem;
-  double* sc = nullptr;
+  double* x = ar.get<double>(n);
+  double* z = ar.get<double>(n);
+  double* y = ar.get<double>(m);
+  double* cmean = ar.get<double>(n);
+  double* t = ar.get<double>(std::max<int64_t>(k, 1));
+  double* sc = ar.get<double>(8);  // [0] nz2, [1] est, [2] scratch
+  int* done = ar.get<int>(4);
   execute(c, kh.h, Am->location == RPCA_DEVICE, [&] {
     const MatV dA = device_view(c, Am, ar);
-    double* x = ar.get<double>(n);
-    double* z = ar.get<double>(n);
-    double* y = ar.get<double>(m);
-    double* cmean = ar.get<double>(n);
-    double* t = ar.get<double>(std::max<int64_t>(k, 1));
-    sc = ar.get<double>(8);  // [0] nz2, [1] est, [2] scratch
-    int* done = ar.get<int>(4);
     if (!raw) {
       const size_t mark = ar.off;
       colmeans(c, dA, m, cmean, ar);

@@ -260,6 +260,9 @@ def test_eigens_psd(variant):
     ln = lam.cpu().numpy()
     assert np.max(np.abs(ln - lo) / lo) < 1e-10
     assert cluster_sin_angle(Uo, U.cpu().numpy(), lo, k) < 1e-8
+    # the second identical call replays the captured CUDA graph: same bits
+    U2, lam2 = rp.eigens(A, k, its=2, l=l, seed=0, variant=variant)
+    assert torch.equal(U, U2) and torch.equal(lam, lam2)
 
 
 def test_diffsnorm_matches_oracle():
