@@ -39,9 +39,11 @@ struct AxCfg {
 // Layout note.  Stage s holds A rows [tile·128, +128) × k [kb·32, +32) as
 // two boxes (k 0-15, k 16-31), each 128 rows × 128 B, 128B-swizzled.  DMMA
 // k-step st (0..7) gives lane (row r = lane>>2, kpos c = lane&3) the value
-// A[r][kb·32 + 8·(st>>1) + 2c + (st&1)]: for st = 2q, 2q+1 both values sit in
-// 16-byte chunk 4·(q&1) + c of box q>>1, loaded once as a double2.  Packed X
-// holds X[that same k][nt·8 + (lane>>2)] at Xp[kb][st][nt][lane].
+// A[r][kb·32 + 16·(q>>1) + 4c + 2(q&1) + (st&1)], q = st>>1: for st = 2q,
+// 2q+1 both values sit in 16-byte chunk 2c + (q&1) of box q>>1, loaded once
+// as a double2.  Within each 8-lane LDS.128 phase (rows r, r+1) the swizzled
+// chunk positions (2c + (q&1)) ^ (r&7) are all distinct: conflict-free.
+// Packed X holds X[that same k][nt·8 + (lane>>2)] at Xp[kb][st][nt][lane].
 template <int NT>
 __global__ void __launch_bounds__(kThreads, 1)
     ax_f64_tma_kernel(const __grid_constant__ CUtensorMap tmA, const double* __restrict__ Xp, int64_t m, int l,
@@ -101,7 +103,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
         const uint8_t* box = As + (q >> 1) * (BM * 128);
-        const int chunk = 4 * (q & 1) + (lane & 3);
+        const int chunk = 2 * (lane & 3) + (q & 1);  // rows r, r+1 of a phase hit chunks of opposite parity
         double2 a[2];
 #pragma unroll
         for (int mt = 0; mt < 2; ++mt) {

@@ -12,7 +12,7 @@ namespace {
 constexpr int kChunk = 8192;  // rows per partial in the two-stage reductions
 
 // Packed X for dense_ax (fragment-major, see dense_ax.cu):
-// Xp[kb][s][nt][lane] = X[kb*32 + 8*(s>>1) + 2*(lane&3) + (s&1)][nt*8 + (lane>>2)]
+// Xp[kb][s][nt][lane] = X[kb*32 + 16*(s>>2) + 4*(lane&3) + 2*((s>>1)&1) + (s&1)][nt*8 + (lane>>2)]
 __global__ void pack_x_kernel(const double* __restrict__ X, int64_t n, int l, int NT, int64_t total,
                               double* __restrict__ Xp) {
   for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
@@ -23,7 +23,7 @@ __global__ void pack_x_kernel(const double* __restrict__ X, int64_t n, int l, in
     t /= NT;
     const int s = (int)(t & 7);
     const int64_t kb = t >> 3;
-    const int64_t k = kb * 32 + 8 * (s >> 1) + 2 * (lane & 3) + (s & 1);
+    const int64_t k = kb * 32 + 16 * (s >> 2) + 4 * (lane & 3) + 2 * ((s >> 1) & 1) + (s & 1);
     const int j = nt * 8 + (lane >> 2);
     Xp[idx] = (k < n && j < l) ? X[k * l + j] : 0.0;
   }
