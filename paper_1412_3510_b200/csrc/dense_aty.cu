@@ -286,11 +286,26 @@ void launch_aty_tma(Ctx& c, const DenseA& A, const double* Yp, const Split& sp, 
 
 }  // namespace
 
+void aty_reduce_partials(Ctx& c, const double* part, int64_t U, int64_t P, int64_t cpc, int maxslots, int64_t n,
+                         int l, int LP, const double* cmean, const double* sy, double* Z) {
+  Split sp;
+  sp.U = U;
+  sp.P = P;
+  sp.cpc = cpc;
+  const int64_t total = n * l;
+  const unsigned grid = (unsigned)std::min<int64_t>(cdiv(total, 256), (int64_t)c.num_sms * 8);
+  aty_reduce_kernel<<<grid, 256, 0, c.stream>>>(part, sp, maxslots, n, l, LP, cmean, sy, Z);
+  RPCA_CHECK_LAUNCH();
+  count_launch(c, 1, "aty_reduce");
+}
+
 size_t aty_ws_bytes(Ctx& c, const DenseA& A, int l) {
   Sizer s;
   s.add<double>(kMaxL);                                            // sy
   s.add<double>(std::max<int64_t>(1, cdiv(A.m, 8192)) * kMaxL);    // colsum partials
-  if (tma_ok(A)) {
+  if (f32_tc_ok(A)) {
+    s.add<char>(aty_f32_ws_bytes(c, A, l));
+  } else if (tma_ok(A)) {
     const Split sp = make_split(c, A);
     s.add<double>(packy_elems(A.m, l));
     s.add<double>(sp.P * (int64_t)max_slots(sp) * BN * cdiv(l, 8) * 8);
@@ -306,6 +321,16 @@ void dense_aty(Ctx& c, const DenseA& A, const double* Y, int l, const double* cm
   if (cmean) {
     sy = ar.get<double>(kMaxL);
     weighted_colsum(c, nullptr, Y, A.m, l, sy, ar);
+  }
+  if (f32_tc_ok(A) && A.m > 0) {
+    int64_t P = 0, cpc = 0;
+    int ms = 0, LP = 0;
+    const size_t mark = ar.off;
+    double* part = nullptr;
+    dense_aty_f32_partials(c, A, Y, l, &part, &P, &ms, &cpc, &LP, ar);
+    aty_reduce_partials(c, part, cdiv(A.n, 128) * cpc, P, cpc, ms, A.n, l, LP, cmean, sy, Z);
+    ar.off = mark;
+    return;
   }
   if (tma_ok(A) && A.m > 0) {
     const Split sp = make_split(c, A);

@@ -236,6 +236,7 @@ bool tma_ok(const DenseA& A) {
 }  // namespace
 
 size_t ax_ws_bytes(const DenseA& A, int l) {
+  if (f32_tc_ok(A)) return ax_f32_ws_bytes(A, l);
   Sizer s;
   s.add<double>(packx_elems(A.n, l));
   return s.total;
@@ -244,6 +245,10 @@ size_t ax_ws_bytes(const DenseA& A, int l) {
 void dense_ax(Ctx& c, const DenseA& A, const double* X, int l, double* Y, Arena& ar) {
   RPCA_REQUIRE(l >= 1 && l <= kMaxL, RPCA_E_SHAPE, "l=%d out of range [1,%d]", l, kMaxL);
   if (A.m == 0) return;
+  if (f32_tc_ok(A)) {
+    dense_ax_f32(c, A, X, l, Y, ar);
+    return;
+  }
   if (tma_ok(A)) {
     double* Xp = ar.get<double>(packx_elems(A.n, l));
     pack_x(c, X, A.n, l, Xp);

@@ -156,6 +156,16 @@ void csr_transpose(Ctx& c, const CsrA& A, int64_t n, CsrA& T, Arena& scratch);
 // cmean[j] = (Σ_i A_ij)/m_total from CSR(Aᵀ), rows ascending
 void csr_colmeans(Ctx& c, const CsrA& T, int64_t m_total, double* cmean);
 
+// dense_f32_tc.cu — fp32 A on tcgen05 (3×TF32)
+bool f32_tc_ok(const DenseA& A);
+size_t ax_f32_ws_bytes(const DenseA& A, int l);
+void dense_ax_f32(Ctx& c, const DenseA& A, const double* X, int l, double* Y, Arena& ar);
+size_t aty_f32_ws_bytes(Ctx& c, const DenseA& A, int l);
+void dense_aty_f32_partials(Ctx& c, const DenseA& A, const double* Y, int l, double** part, int64_t* P, int* maxslots,
+                            int64_t* cpc, int* LP, Arena& ar);
+void aty_reduce_partials(Ctx& c, const double* part, int64_t U, int64_t P, int64_t cpc, int maxslots, int64_t n,
+                         int l, int LP, const double* cmean, const double* sy, double* Z);
+
 // tslu.cu
 size_t lu_ws_bytes(int64_t m, int l);
 // gpart (optional): per-CTA upper-triangle Gram partials of L (lu_apply_grid × l(l+1)/2)

@@ -86,14 +86,24 @@ def test_apply_centered(m, n, l):
     del Ac
 
 
-def test_apply_f32_input():
-    g = torch.Generator(device="cuda").manual_seed(8)
-    A = torch.randn(777, 300, generator=g, device=dev(), dtype=torch.float32)
-    X = torch.randn(300, 20, generator=g, device=dev(), dtype=torch.float64)
-    An = A.cpu().numpy()
-    ref = oracle.apply(An, X.cpu().numpy())
+@pytest.mark.parametrize("m,n", [(777, 300), (4100, 260), (300, 4096), (1000, 518), (129, 33 * 4)])
+@pytest.mark.parametrize("l", [1, 12, 22, 52, 64])
+def test_apply_f32_input(m, n, l):
+    """fp32 A: tcgen05 3×TF32 (lda·4 ≡ 0 mod 16) or the CUDA-core fallback; the
+    3×TF32 product error is ≈ 2^-21·|a||x| per term, fp32 accumulation adds K·2^-24."""
+    g = torch.Generator(device="cuda").manual_seed(8 + m + l)
+    A = torch.randn(m, n, generator=g, device=dev(), dtype=torch.float32)
+    X = torch.randn(n, l, generator=g, device=dev(), dtype=torch.float64)
+    Y = torch.randn(m, l, generator=g, device=dev(), dtype=torch.float64)
+    An = A.cpu().numpy().astype(np.float64)
+    bound = (3 * 2.0**-21 + 2 * n * 2.0**-24)
     got = rp.apply(A, X).cpu().numpy()
-    assert np.all(np.abs(got - ref) <= 1e-5 * (np.abs(An.astype(np.float64)) @ np.abs(X.cpu().numpy())))
+    ref = oracle.apply(A.cpu().numpy(), X.cpu().numpy())
+    assert np.all(np.abs(got - ref) <= bound * (np.abs(An) @ np.abs(X.cpu().numpy())) + 1e-300)
+    bound = (3 * 2.0**-21 + 2 * m * 2.0**-24)
+    got = rp.apply(A, Y, adjoint=True).cpu().numpy()
+    ref = oracle.apply(A.cpu().numpy(), Y.cpu().numpy(), adjoint=True)
+    assert np.all(np.abs(got - ref) <= bound * (np.abs(An).T @ np.abs(Y.cpu().numpy())) + 1e-300)
 
 
 # ----------------------------------------------------------------- a3: LU
