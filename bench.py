@@ -284,7 +284,7 @@ def main():
         c, s = kern.get(name, (0, 0.0))
         kern[name] = (c + 1, s + msec)
     step_ms = ms_total / args.steps
-    passes_k = {k: v for k, v in kern.items() if k.startswith(("ax_", "aty_f64", "aty_generic", "csr_spmm"))}
+    passes_k = {k: v for k, v in kern.items() if k.startswith(("ax_", "aty_f64", "aty_f32", "aty_generic", "csr_spmm"))}
     dom = max(passes_k.items(), key=lambda kv: kv[1][1]) if passes_k else None
     roof = None
     if dom:

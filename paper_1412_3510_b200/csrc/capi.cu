@@ -255,7 +255,7 @@ rpca_status rpca_small_svd(rpca_ctx* c, const double* G, int64_t n, int64_t l, d
     rpca::Sizer s;
     s.add<double>(n * l);
     s.add<double>(2 * l * l);
-    rpca::Arena ar = c->arena(s.total + rpca::orth_ws_bytes(n, (int)l) + 65536);
+    rpca::Arena ar = c->arena(s.total + rpca::orth_ws_bytes(*c, n, (int)l) + 65536);
     double* Qb = ar.get<double>(n * l);
     double* R = ar.get<double>(l * l);
     double* Vr = ar.get<double>(l * l);

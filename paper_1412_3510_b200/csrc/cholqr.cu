@@ -11,8 +11,9 @@
 // as accurately as Householder (Terao, Ozaki, Ogita 2020, "LU-Cholesky QR").
 // Exact zero pivots (rank-deficient Y) make L's column a unit vector, so L —
 // and hence Q — stays full rank and orthonormal.
-// Cost: the LU passes + one more read/write of Y per Cholesky step; the Gram
-// matrices are accumulated inside the kernels that write L and Q1 (fused).
+// The two Grams (LᵀL, Q1ᵀQ1) run on the fp64 tensor-core adjoint pass
+// (dense_aty with A := Y) and the two triangular products on the A·X pass
+// (dense_ax, in place); only the l×l Cholesky/inverse is a one-CTA kernel.
 #include "internal.cuh"
 
 namespace rpca {
@@ -20,56 +21,26 @@ namespace {
 
 constexpr int kThreads = 256;
 
-// One CTA: G (upper, from per-CTA partials summed in ascending CTA order) →
-// R = chol(G) (upper, CᵀC = G) → Rinv; Rtot = R·Rprev (Rprev upper or NULL);
-// if `signfix`, D = sign(diag(Rtot)): Minv = Rinv·D, Rtot ← D·Rtot.
-constexpr int kCholThreads = 1024;
-
-__global__ void __launch_bounds__(kCholThreads) chol_partials_kernel(const double* __restrict__ part, int nparts, int l,
-                                                                 const double* __restrict__ Rprev, int signfix,
-                                                                 double* __restrict__ Minv,
-                                                                 double* __restrict__ Rtot) {
+// One CTA: R = chol(G) (upper, RᵀR = G, G full l×l) → X = R⁻¹ (upper);
+// Rtot = R·Rprev (Rprev upper or NULL); if `signfix`, D = sign(diag(Rtot)):
+// Minv = X·D, Rtot ← D·Rtot.
+__global__ void __launch_bounds__(kThreads) chol_kernel(const double* __restrict__ Gin, int l,
+                                                        const double* __restrict__ Rprev, int signfix,
+                                                        double* __restrict__ Minv, double* __restrict__ Rtot) {
   extern __shared__ double sm[];
   double* G = sm;              // l×l
   double* R = sm + l * l;      // l×l
   double* X = sm + 2 * l * l;  // l×l (inverse)
-  double* Red = sm + 3 * l * l; // 8 × l(l+1)/2 reduction slices
   __shared__ double d[kMaxL];
   const int tid = threadIdx.x;
-  const int npairs = l * (l + 1) / 2;
-  // fixed-order two-level sum of the CTA partials: kSub interleaved slices per
-  // entry (8 independent loads in flight each), then the slices in order
-  constexpr int kSub = 8;
-  double* red = Red;
-  for (int e = tid; e < npairs * kSub; e += kCholThreads) {
-    const int pq = e % npairs, sub = e / npairs;
-    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
-    int b = sub;
-    for (; b + 3 * kSub < nparts; b += 4 * kSub) {
-      a0 += part[(int64_t)b * npairs + pq];
-      a1 += part[(int64_t)(b + kSub) * npairs + pq];
-      a2 += part[(int64_t)(b + 2 * kSub) * npairs + pq];
-      a3 += part[(int64_t)(b + 3 * kSub) * npairs + pq];
-    }
-    for (; b < nparts; b += kSub) a0 += part[(int64_t)b * npairs + pq];
-    red[sub * npairs + pq] = (a0 + a1) + (a2 + a3);
+  for (int idx = tid; idx < l * l; idx += kThreads) {
+    const int p = idx / l, q = idx - p * l;
+    G[idx] = 0.5 * (Gin[idx] + Gin[q * l + p]);
+    R[idx] = 0.0;
   }
   __syncthreads();
-  for (int pq = tid; pq < npairs; pq += kCholThreads) {
-    double s = 0.0;
-    for (int sub = 0; sub < kSub; ++sub) s += red[sub * npairs + pq];
-    int p = 0, rem = pq;
-    while (rem >= l - p) { rem -= l - p; ++p; }
-    G[p * l + p + rem] = s;
-  }
-  __syncthreads();
-  for (int idx = tid; idx < l * l; idx += kCholThreads) R[idx] = 0.0;
-  __syncthreads();
-  const double gmax = [&] {
-    double v = 0.0;
-    for (int j = 0; j < l; ++j) v = fmax(v, G[j * l + j]);
-    return v;
-  }();
+  double gmax = 0.0;
+  for (int j = 0; j < l; ++j) gmax = fmax(gmax, G[j * l + j]);
   for (int j = 0; j < l; ++j) {
     if (tid == 0) {
       double dj = G[j * l + j];
@@ -79,166 +50,95 @@ __global__ void __launch_bounds__(kCholThreads) chol_partials_kernel(const doubl
       R[j * l + j] = sqrt(dj > floor_ ? dj : (floor_ > 0.0 ? floor_ : 1.0));
     }
     __syncthreads();
-    for (int i = j + 1 + tid; i < l; i += kCholThreads) {
+    for (int i = j + 1 + tid; i < l; i += kThreads) {
       double s = G[j * l + i];
       for (int t = 0; t < j; ++t) s -= R[t * l + j] * R[t * l + i];
       R[j * l + i] = s / R[j * l + j];
     }
     __syncthreads();
   }
-  // X = R⁻¹ (upper), thread per column
-  if (tid < l) {
-    const int j = tid;
-    for (int i = 0; i < l; ++i) X[i * l + j] = 0.0;
-    X[j * l + j] = 1.0 / R[j * l + j];
-    for (int i = j - 1; i >= 0; --i) {
+  // X = R⁻¹ (upper): warp per column, M[i][j] = −(Σ_{t=i+1..j} R_it X_tj)/R_ii
+  const int lane = tid & 31, warp = tid >> 5;
+  for (int j = warp; j < l; j += kThreads / 32) {
+    for (int i = lane; i < l; i += 32) X[i * l + j] = 0.0;
+    __syncwarp();
+    for (int i = j; i >= 0; --i) {
       double s = 0.0;
-      for (int t = i + 1; t <= j; ++t) s += R[i * l + t] * X[t * l + j];
-      X[i * l + j] = -s / R[i * l + i];
+      for (int t = i + 1 + lane; t <= j; t += 32) s += R[i * l + t] * X[t * l + j];
+      s = warp_sum(s);
+      if (lane == 0) X[i * l + j] = ((i == j ? 1.0 : 0.0) - s) / R[i * l + i];
+      __syncwarp();
     }
   }
   __syncthreads();
   // Rtot = R·Rprev (both upper)
-  for (int idx = tid; idx < l * l; idx += kCholThreads) {
+  for (int idx = tid; idx < l * l; idx += kThreads) {
     const int i = idx / l, j = idx - i * l;
     double s;
     if (!Rprev) s = R[idx];
     else {
       s = 0.0;
       for (int t = i; t <= j; ++t) s += R[i * l + t] * Rprev[t * l + j];
-      if (j < i) s = 0.0;
     }
     G[idx] = s;  // reuse G for Rtot
   }
   __syncthreads();
   if (tid < l) d[tid] = (signfix && G[tid * l + tid] < 0.0) ? -1.0 : 1.0;
   __syncthreads();
-  for (int idx = tid; idx < l * l; idx += kCholThreads) {
+  for (int idx = tid; idx < l * l; idx += kThreads) {
     const int i = idx / l, j = idx - i * l;
     Minv[idx] = X[idx] * d[j];
     Rtot[idx] = G[idx] * d[i];
   }
 }
 
-// Out = In·M (M upper l×l), in place allowed (tiles staged in smem); optional
-// per-CTA upper Gram partial of Out.
-__global__ void __launch_bounds__(kThreads, 2) right_mult_upper_kernel(double* __restrict__ Y, int64_t m, int l,
-                                                                    const double* __restrict__ M,
-                                                                    double* __restrict__ gpart) {
-  extern __shared__ double sm[];
-  const int ldw = l | 1;
-  double* Ms = sm;
-  double* Ys = sm + l * l;
-  for (int idx = threadIdx.x; idx < l * l; idx += kThreads) Ms[idx] = M[idx];
-  const int r = threadIdx.x & 127, jph = threadIdx.x >> 7;
-  constexpr int kPairs = kMaxL * (kMaxL + 1) / 2 / kThreads + 1;
-  double g[kPairs];
-  uint16_t gp[kPairs], gq[kPairs];
-  const int npairs = l * (l + 1) / 2;
-#pragma unroll
-  for (int i = 0; i < kPairs; ++i) {
-    g[i] = 0.0;
-    const int pq = threadIdx.x + i * kThreads;
-    int p = 0, rem = pq < npairs ? pq : 0;
-    while (rem >= l - p) { rem -= l - p; ++p; }
-    gp[i] = (uint16_t)p;
-    gq[i] = (uint16_t)(p + rem);
-  }
-  for (int64_t r0 = (int64_t)blockIdx.x * 128; r0 < m; r0 += (int64_t)gridDim.x * 128) {
-    const int rows = (int)imin64(128, m - r0);
-    __syncthreads();
-    for (int idx = threadIdx.x; idx < rows * l; idx += kThreads) {
-      const int rr = idx / l, t = idx - rr * l;
-      Ys[rr * ldw + t] = Y[r0 * l + idx];
-    }
-    __syncthreads();
-    double out[kMaxL / 2];
-    if (r < rows) {
-#pragma unroll
-      for (int q = 0; q < kMaxL / 2; ++q) {
-        const int j = jph + 2 * q;
-        if (j >= l) break;
-        double s = 0.0;
-        for (int t = 0; t <= j; ++t) s += Ys[r * ldw + t] * Ms[t * l + j];
-        out[q] = s;
-      }
-    }
-    __syncthreads();
-    if (r < rows) {
-#pragma unroll
-      for (int q = 0; q < kMaxL / 2; ++q) {
-        const int j = jph + 2 * q;
-        if (j >= l) break;
-        Ys[r * ldw + j] = out[q];
-        Y[(r0 + r) * l + j] = out[q];
-      }
-    }
-    if (gpart) {
-      __syncthreads();
-#pragma unroll
-      for (int i = 0; i < kPairs; ++i) {
-        if (threadIdx.x + i * kThreads >= npairs) break;
-        const int p = gp[i], q = gq[i];
-        double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
-        int rr = 0;
-        for (; rr + 4 <= rows; rr += 4) {
-          s0 += Ys[rr * ldw + p] * Ys[rr * ldw + q];
-          s1 += Ys[(rr + 1) * ldw + p] * Ys[(rr + 1) * ldw + q];
-          s2 += Ys[(rr + 2) * ldw + p] * Ys[(rr + 2) * ldw + q];
-          s3 += Ys[(rr + 3) * ldw + p] * Ys[(rr + 3) * ldw + q];
-        }
-        for (; rr < rows; ++rr) s0 += Ys[rr * ldw + p] * Ys[rr * ldw + q];
-        g[i] += (s0 + s1) + (s2 + s3);
-      }
-    }
-  }
-  if (gpart) {
-#pragma unroll
-    for (int i = 0; i < kPairs; ++i) {
-      const int pq = threadIdx.x + i * kThreads;
-      if (pq < npairs) gpart[(int64_t)blockIdx.x * npairs + pq] = g[i];
-    }
-  }
+void chol(Ctx& c, const double* G, int l, const double* Rprev, int signfix, double* Minv, double* Rtot) {
+  ensure_smem((const void*)chol_kernel, 3 * kMaxL * kMaxL * 8);
+  chol_kernel<<<1, kThreads, 3 * l * l * 8, c.stream>>>(G, l, Rprev, signfix, Minv, Rtot);
+  RPCA_CHECK_LAUNCH();
+  count_launch(c, 1, "cholqr_chol");
 }
 
 }  // namespace
 
 size_t orth_ws_bytes(int64_t m, int l) {
   Sizer s;
-  s.add<double>((size_t)296 * l * (l + 1) / 2 + 64);  // partials (≤ 2·148 CTAs)
-  s.add<double>((size_t)296 * l * (l + 1) / 2 + 64);
   s.add<double>(6 * (size_t)l * l);
-  return s.total + lu_ws_bytes(m, l);
+  const DenseA Y{nullptr, RPCA_F64, m, l, l};
+  return s.total + lu_ws_bytes(m, l) + ax_ws_bytes(Y, l) + 4096;
+}
+
+size_t orth_ws_bytes(Ctx& c, int64_t m, int l) {
+  const DenseA Y{nullptr, RPCA_F64, m, l, l};
+  return orth_ws_bytes(m, l) + aty_ws_bytes(c, Y, l);
 }
 
 void orthonormalize(Ctx& c, double* Y, int64_t m, int l, double* R_out, Arena& ar) {
   RPCA_REQUIRE(l >= 1 && l <= kMaxL && m >= l, RPCA_E_SHAPE, "orthonormalize: need 1 ≤ l ≤ %d, m ≥ l", kMaxL);
-  const int P = lu_apply_grid(c, m);
-  const int npairs = l * (l + 1) / 2;
-  double* p1 = ar.get<double>((size_t)P * npairs);
-  double* p2 = ar.get<double>((size_t)P * npairs);
   double* U = ar.get<double>((size_t)l * l);
+  double* G = ar.get<double>((size_t)l * l);
   double* M1 = ar.get<double>((size_t)l * l);
   double* R1 = ar.get<double>((size_t)l * l);
   double* M2 = ar.get<double>((size_t)l * l);
   double* R2 = ar.get<double>((size_t)l * l);
-  lu_renorm(c, Y, m, l, U, nullptr, ar, p1);
-  const int smem_c = (3 * l * l + 8 * npairs) * 8;
-  ensure_smem((const void*)chol_partials_kernel, (3 * kMaxL * kMaxL + 8 * kMaxL * (kMaxL + 1) / 2) * 8);
-  chol_partials_kernel<<<1, kCholThreads, smem_c, c.stream>>>(p1, P, l, U, 0, M1, R1);
-  RPCA_CHECK_LAUNCH();
-  count_launch(c, 1, "cholqr_chol");
-  const int smem_r = (l * l + 128 * (l | 1)) * 8;
-  ensure_smem((const void*)right_mult_upper_kernel, (kMaxL * kMaxL + 128 * (kMaxL | 1)) * 8);
-  right_mult_upper_kernel<<<P, kThreads, smem_r, c.stream>>>(Y, m, l, M1, p2);
-  RPCA_CHECK_LAUNCH();
-  count_launch(c, 1, "cholqr_trmm");
-  chol_partials_kernel<<<1, kCholThreads, smem_c, c.stream>>>(p2, P, l, R1, 1, M2, R2);
-  RPCA_CHECK_LAUNCH();
-  count_launch(c, 1, "cholqr_chol");
-  right_mult_upper_kernel<<<P, kThreads, smem_r, c.stream>>>(Y, m, l, M2, nullptr);
-  RPCA_CHECK_LAUNCH();
-  count_launch(c, 1, "cholqr_trmm");
+  const DenseA Yd{Y, RPCA_F64, m, l, l};
+  const size_t mark = ar.off;
+  lu_renorm(c, Y, m, l, U, nullptr, ar);  // Y ← L
+  ar.off = mark;
+  TagScope ts(c, "cholqr_gram");
+  dense_aty(c, Yd, Y, l, nullptr, G, ar);  // G = LᵀL
+  ar.off = mark;
+  chol(c, G, l, U, 0, M1, R1);             // R1·U
+  c.tag = "cholqr_trmm";
+  dense_ax(c, Yd, M1, l, Y, ar);           // Q1 = L·R1⁻¹
+  ar.off = mark;
+  c.tag = "cholqr_gram";
+  dense_aty(c, Yd, Y, l, nullptr, G, ar);  // G = Q1ᵀQ1
+  ar.off = mark;
+  chol(c, G, l, R1, 1, M2, R2);            // R = D·R2·R1·U
+  c.tag = "cholqr_trmm";
+  dense_ax(c, Yd, M2, l, Y, ar);           // Q = Q1·R2⁻¹·D
+  ar.off = mark;
   if (R_out) RPCA_CUDA(cudaMemcpyAsync(R_out, R2, sizeof(double) * l * l, cudaMemcpyDeviceToDevice, c.stream));
 }
 

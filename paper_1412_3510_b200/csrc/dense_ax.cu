@@ -225,7 +225,7 @@ void launch_ax_tma(Ctx& c, const DenseA& A, const double* Xp, int l, double* Y) 
   const int grid = (int)std::min<int64_t>(ntiles, c.num_sms);
   ax_f64_tma_kernel<NT><<<grid, kThreads, Cfg::kSmem, c.stream>>>(tm, Xp, A.m, l, ntiles, KB, Y);
   RPCA_CHECK_LAUNCH();
-  count_launch(c, 1, "ax_f64_dmma");
+  count_launch(c, 1, c.tag ? c.tag : "ax_f64_dmma");
 }
 
 bool tma_ok(const DenseA& A) {

@@ -392,17 +392,27 @@ __global__ void __launch_bounds__(kThreads, 1)
 
 // Xᵀ split: Xt_hi[j][k] = tf32(X[k][j]) (as fp32 with the low 13 bits cleared),
 // Xt_lo[j][k] = fp32(X[k][j] − Xt_hi[j][k]); zero padding to (Npad × Kpad).
-__global__ void split_transpose_kernel(const double* __restrict__ X, int64_t K, int l, int Npad, int64_t Kpad,
-                                       float* __restrict__ hi, float* __restrict__ lo) {
-  const int64_t total = (int64_t)Npad * Kpad;
-  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
-       idx += (int64_t)gridDim.x * blockDim.x) {
-    const int j = (int)(idx / Kpad);
-    const int64_t k = idx - (int64_t)j * Kpad;
-    const double x = (k < K && j < l) ? X[k * l + j] : 0.0;
-    const float h = __uint_as_float(__float_as_uint((float)x) & 0xFFFFE000u);
-    hi[idx] = h;
-    lo[idx] = (float)(x - (double)h);
+// 64-row tiles go through shared memory so both the read of X (rows of l
+// doubles) and the writes of Xᵀ (runs of 64 k) are coalesced.
+__global__ void __launch_bounds__(256) split_transpose_kernel(const double* __restrict__ X, int64_t K, int l, int Npad,
+                                                              int64_t Kpad, float* __restrict__ hi,
+                                                              float* __restrict__ lo) {
+  __shared__ double tile[64][kMaxL + 1];
+  for (int64_t k0 = (int64_t)blockIdx.x * 64; k0 < Kpad; k0 += (int64_t)gridDim.x * 64) {
+    __syncthreads();
+    for (int idx = threadIdx.x; idx < 64 * l; idx += 256) {
+      const int r = idx / l, j = idx - r * l;
+      const int64_t k = k0 + r;
+      tile[r][j] = k < K ? X[k * l + j] : 0.0;
+    }
+    __syncthreads();
+    for (int idx = threadIdx.x; idx < 64 * Npad; idx += 256) {
+      const int j = idx >> 6, r = idx & 63;
+      const double x = j < l ? tile[r][j] : 0.0;
+      const float h = __uint_as_float(__float_as_uint((float)x) & 0xFFFFE000u);
+      hi[(int64_t)j * Kpad + k0 + r] = h;
+      lo[(int64_t)j * Kpad + k0 + r] = (float)(x - (double)h);
+    }
   }
 }
 
@@ -434,8 +444,7 @@ CUtensorMap tmap_f32(const void* base, int64_t inner, int64_t outer, int64_t ld_
 int npad_for(int l) { return l <= 16 ? 16 : (l <= 32 ? 32 : (l <= 48 ? 48 : 64)); }
 
 void split_transpose(Ctx& c, const double* X, int64_t K, int l, int Npad, int64_t Kpad, float* hi, float* lo) {
-  const int64_t total = (int64_t)Npad * Kpad;
-  const unsigned grid = (unsigned)std::min<int64_t>(cdiv(total, 256), (int64_t)c.num_sms * 16);
+  const unsigned grid = (unsigned)std::min<int64_t>(cdiv(Kpad, 64), (int64_t)c.num_sms * 8);
   split_transpose_kernel<<<grid, 256, 0, c.stream>>>(X, K, l, Npad, Kpad, hi, lo);
   RPCA_CHECK_LAUNCH();
   count_launch(c, 1, "split_tf32");
@@ -452,7 +461,7 @@ void launch_ax(Ctx& c, const DenseA& A, const float* hi, const float* lo, int64_
   const int grid = (int)std::min<int64_t>(ntiles, c.num_sms);
   ax_f32_tc_kernel<N><<<grid, kThreads, Cfg::kSmem, c.stream>>>(tA, tH, tL, A.m, l, ntiles, (int)(Kpad / 32), Y);
   RPCA_CHECK_LAUNCH();
-  count_launch(c, 1, "ax_f32_tc");
+  count_launch(c, 1, c.tag ? c.tag : "ax_f32_tc");
 }
 
 template <int N>
@@ -465,7 +474,7 @@ void launch_aty(Ctx& c, const DenseA& A, const float* hi, const float* lo, int64
   ensure_smem((const void*)aty_f32_tc_kernel<N>, Cfg::kSmem);
   aty_f32_tc_kernel<N><<<(unsigned)sp.P, kThreads, Cfg::kSmem, c.stream>>>(tA, tH, tL, sp, maxslots, N, part);
   RPCA_CHECK_LAUNCH();
-  count_launch(c, 1, "aty_f32_tc");
+  count_launch(c, 1, c.tag ? c.tag : "aty_f32_tc");
 }
 
 SplitF make_split(Ctx& c, const DenseA& A) {
@@ -494,7 +503,7 @@ bool f32_tc_ok(const DenseA& A) {
 
 size_t ax_f32_ws_bytes(const DenseA& A, int l) {
   Sizer s;
-  const int64_t Kpad = cdiv(A.n, 32) * 32;
+  const int64_t Kpad = cdiv(A.n, 64) * 64;
   s.add<float>((size_t)npad_for(l) * Kpad);
   s.add<float>((size_t)npad_for(l) * Kpad);
   return s.total;
@@ -502,7 +511,7 @@ size_t ax_f32_ws_bytes(const DenseA& A, int l) {
 
 void dense_ax_f32(Ctx& c, const DenseA& A, const double* X, int l, double* Y, Arena& ar) {
   const int Np = npad_for(l);
-  const int64_t Kpad = cdiv(A.n, 32) * 32;
+  const int64_t Kpad = cdiv(A.n, 64) * 64;
   float* hi = ar.get<float>((size_t)Np * Kpad);
   float* lo = ar.get<float>((size_t)Np * Kpad);
   split_transpose(c, X, A.n, l, Np, Kpad, hi, lo);
@@ -517,7 +526,7 @@ void dense_ax_f32(Ctx& c, const DenseA& A, const double* X, int l, double* Y, Ar
 size_t aty_f32_ws_bytes(Ctx& c, const DenseA& A, int l) {
   const SplitF sp = make_split(c, A);
   Sizer s;
-  const int64_t Kpad = cdiv(A.m, 32) * 32;
+  const int64_t Kpad = cdiv(A.m, 64) * 64;
   s.add<float>((size_t)npad_for(l) * Kpad);
   s.add<float>((size_t)npad_for(l) * Kpad);
   s.add<double>((size_t)sp.P * max_slots(sp) * 128 * npad_for(l));
@@ -528,7 +537,7 @@ size_t aty_f32_ws_bytes(Ctx& c, const DenseA& A, int l) {
 void dense_aty_f32_partials(Ctx& c, const DenseA& A, const double* Y, int l, double** part_out, int64_t* P,
                             int* maxslots, int64_t* cpc, int* LP, Arena& ar) {
   const int Np = npad_for(l);
-  const int64_t Kpad = cdiv(A.m, 32) * 32;
+  const int64_t Kpad = cdiv(A.m, 64) * 64;
   float* hi = ar.get<float>((size_t)Np * Kpad);
   float* lo = ar.get<float>((size_t)Np * Kpad);
   split_transpose(c, Y, A.m, l, Np, Kpad, hi, lo);

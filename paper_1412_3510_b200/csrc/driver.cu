@@ -435,7 +435,7 @@ void pca(Ctx& c, const rpca_mat* Am, int64_t k, int raw, int its, int64_t l, uin
   const size_t fixed = sz.total;
   size_t scratch = op_ws(c, probe, L);
   scratch = std::max(scratch, lu_ws_bytes(std::max(nin, nout), L));
-  scratch = std::max(scratch, orth_ws_bytes(std::max(nin, nout), L));
+  scratch = std::max(scratch, orth_ws_bytes(c, std::max(nin, nout), L));
   scratch = std::max(scratch, (size_t)(cdiv(std::max(m, n), 8192) + 2) * (n + 2 * k) * 8 + 65536);
   ensure_transpose(c, Am);
   Arena ar = c.arena(fixed + scratch + 65536);
@@ -538,7 +538,7 @@ void eigens(Ctx& c, const rpca_mat* Am, int64_t k, int its, int64_t l, uint64_t 
   }
   size_t scratch = op_ws(c, probe, L);
   scratch = std::max(scratch, lu_ws_bytes(n, L));
-  scratch = std::max(scratch, orth_ws_bytes(n, L));
+  scratch = std::max(scratch, orth_ws_bytes(c, n, L));
   scratch = std::max(scratch, (size_t)(cdiv(n, 8192) + 2) * l * l * 8 + 65536);
   Arena ar = c.arena(sz.total + scratch + 65536);
   if (!c.status_host) RPCA_CUDA(cudaMallocHost(&c.status_host, 64));

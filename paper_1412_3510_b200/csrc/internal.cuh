@@ -76,6 +76,7 @@ struct Ctx {
   int64_t launches = 0;
   Comm* comm = nullptr;
   bool prof = false;
+  const char* tag = nullptr;  // profile name for the pass kernels when used on thin blocks
   bool capturing = false;
   bool use_graphs = true;
   std::vector<ProfRec> prof_recs;
@@ -96,6 +97,13 @@ struct Ctx {
 };
 
 void prof_mark(Ctx& c, const char* name);
+struct TagScope {
+  Ctx& c;
+  const char* prev;
+  TagScope(Ctx& c_, const char* t) : c(c_), prev(c_.tag) { c.tag = t; }
+  ~TagScope() { c.tag = prev; }
+};
+
 inline void count_launch(Ctx& c, int n = 1, const char* name = "misc") {
   c.launches += n;
   if (c.prof) prof_mark(c, name);
@@ -168,10 +176,7 @@ void aty_reduce_partials(Ctx& c, const double* part, int64_t U, int64_t P, int64
 
 // tslu.cu
 size_t lu_ws_bytes(int64_t m, int l);
-// gpart (optional): per-CTA upper-triangle Gram partials of L (lu_apply_grid × l(l+1)/2)
-void lu_renorm(Ctx& c, double* Y, int64_t m, int l, double* U_out, int64_t* piv_out, Arena& ar,
-               double* gpart = nullptr);
-int lu_apply_grid(Ctx& c, int64_t m);
+void lu_renorm(Ctx& c, double* Y, int64_t m, int l, double* U_out, int64_t* piv_out, Arena& ar);
 
 // tsqr.cu
 size_t qr_ws_bytes(int64_t m, int l);
@@ -179,6 +184,7 @@ void qr(Ctx& c, double* Y, int64_t m, int l, double* R_out, Arena& ar);
 
 // cholqr.cu — LU-Cholesky-QR: Y ← Q (orthonormal, span Y), R (l×l upper, diag ≥ 0, Y = Q·R)
 size_t orth_ws_bytes(int64_t m, int l);
+size_t orth_ws_bytes(Ctx& c, int64_t m, int l);
 void orthonormalize(Ctx& c, double* Y, int64_t m, int l, double* R_out, Arena& ar);
 
 // small.cu — one-CTA l×l kernels

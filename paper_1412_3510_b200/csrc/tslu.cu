@@ -200,108 +200,12 @@ __global__ void __launch_bounds__(kThreads) lu_select_kernel(const double* __res
   for (int idx = tid; idx < l * l; idx += kThreads) M[idx] = Ms[idx];
 }
 
-// L = Y·M (in place) with M = U⁻¹ formed per CTA (zero-pivot rule: a zero
-// U_ii zeroes row i of M, i.e. x_i = 0 for every input, as the row
-// substitution x·U = y of reading Q3 prescribes), pivot rows ← Lp rows.  CTAs
-// walk 128-row tiles; if `gpart` is given each CTA also writes its partial
-// Gram Σ L_rᵀ L_r (upper triangle) for the Cholesky-QR that follows.
-__global__ void __launch_bounds__(kThreads, 2) lu_apply_kernel(double* __restrict__ Y, int64_t m, int l,
-                                                            const double* __restrict__ M,
-                                                            const double* __restrict__ Lp,
-                                                            const int64_t* __restrict__ piv,
-                                                            double* __restrict__ gpart) {
-  extern __shared__ double sm[];
-  const int ldw = l | 1;
-  double* Ms = sm;                 // l×l
-  double* Ys = sm + l * l;         // 128×ldw
-  __shared__ int pivpos[128];
-  for (int idx = threadIdx.x; idx < l * l; idx += kThreads) Ms[idx] = M[idx];
-  const int r = threadIdx.x & 127, jph = threadIdx.x >> 7;  // 2 column phases
-  constexpr int kPairs = kMaxL * (kMaxL + 1) / 2 / kThreads + 1;
-  double g[kPairs];
-  uint16_t gp[kPairs], gq[kPairs];
-  const int npairs = l * (l + 1) / 2;
-#pragma unroll
-  for (int i = 0; i < kPairs; ++i) {
-    g[i] = 0.0;
-    const int pq = threadIdx.x + i * kThreads;
-    int p = 0, rem = pq < npairs ? pq : 0;
-    while (rem >= l - p) { rem -= l - p; ++p; }
-    gp[i] = (uint16_t)p;
-    gq[i] = (uint16_t)(p + rem);
-  }
-  for (int64_t r0 = (int64_t)blockIdx.x * 128; r0 < m; r0 += (int64_t)gridDim.x * 128) {
-    const int rows = (int)imin64(128, m - r0);
-    __syncthreads();
-    for (int idx = threadIdx.x; idx < 128; idx += kThreads) pivpos[idx] = -1;
-    for (int idx = threadIdx.x; idx < rows * l; idx += kThreads) {
-      const int rr = idx / l, t = idx - rr * l;
-      Ys[rr * ldw + t] = Y[r0 * l + idx];
-    }
-    __syncthreads();
-    if (threadIdx.x < l) {
-      const int64_t pr = piv[threadIdx.x] - r0;
-      if (pr >= 0 && pr < rows) pivpos[pr] = threadIdx.x;
-    }
-    __syncthreads();
-    double out[kMaxL / 2];
-    if (r < rows) {
-      const int pj = pivpos[r];
-#pragma unroll
-      for (int q = 0; q < kMaxL / 2; ++q) {
-        const int j = jph + 2 * q;
-        if (j >= l) break;
-        double s;
-        if (pj >= 0) {
-          s = Lp[pj * l + j];
-        } else {
-          double s0 = 0.0, s1 = 0.0;
-          int t = 0;
-          for (; t + 1 <= j; t += 2) {
-            s0 += Ys[r * ldw + t] * Ms[t * l + j];
-            s1 += Ys[r * ldw + t + 1] * Ms[(t + 1) * l + j];
-          }
-          if (t <= j) s0 += Ys[r * ldw + t] * Ms[t * l + j];
-          s = s0 + s1;
-        }
-        out[q] = s;
-      }
-    }
-    __syncthreads();
-    if (r < rows) {
-#pragma unroll
-      for (int q = 0; q < kMaxL / 2; ++q) {
-        const int j = jph + 2 * q;
-        if (j >= l) break;
-        Ys[r * ldw + j] = out[q];
-        Y[(r0 + r) * l + j] = out[q];
-      }
-    }
-    if (gpart) {
-      __syncthreads();
-#pragma unroll
-      for (int i = 0; i < kPairs; ++i) {
-        if (threadIdx.x + i * kThreads >= npairs) break;
-        const int p = gp[i], q = gq[i];
-        double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
-        int rr = 0;
-        for (; rr + 4 <= rows; rr += 4) {
-          s0 += Ys[rr * ldw + p] * Ys[rr * ldw + q];
-          s1 += Ys[(rr + 1) * ldw + p] * Ys[(rr + 1) * ldw + q];
-          s2 += Ys[(rr + 2) * ldw + p] * Ys[(rr + 2) * ldw + q];
-          s3 += Ys[(rr + 3) * ldw + p] * Ys[(rr + 3) * ldw + q];
-        }
-        for (; rr < rows; ++rr) s0 += Ys[rr * ldw + p] * Ys[rr * ldw + q];
-        g[i] += (s0 + s1) + (s2 + s3);
-      }
-    }
-  }
-  if (gpart) {
-#pragma unroll
-    for (int i = 0; i < kPairs; ++i) {
-      const int pq = threadIdx.x + i * kThreads;
-      if (pq < npairs) gpart[(int64_t)blockIdx.x * npairs + pq] = g[i];
-    }
+// Y[piv[j]] ← Lp[j] (the pivot rows' exact unit-lower rows)
+__global__ void pivot_rows_kernel(double* __restrict__ Y, int l, const double* __restrict__ Lp,
+                                  const int64_t* __restrict__ piv) {
+  for (int idx = threadIdx.x; idx < l * l; idx += blockDim.x) {
+    const int j = idx / l, t = idx - j * l;
+    Y[piv[j] * l + t] = Lp[idx];
   }
 }
 
@@ -319,7 +223,8 @@ void select(Ctx& c, unsigned grid, const double* Y, int64_t m, int l, int leaf, 
             int G, int64_t* cout, int final_, double* U, double* Lp, int64_t* piv, double* M) {
   const int cap = leaf ? kLeafRows : G * l;
   ensure_smem((const void*)lu_select_kernel, 220 * 1024);
-  lu_select_kernel<<<grid, kThreads, select_smem(cap, l), c.stream>>>(Y, m, l, leaf, kLeafRows, cin, n_in, G, cout,
+  const size_t smem = select_smem(cap, l) - (final_ ? 0 : (size_t)l * l * 8);
+  lu_select_kernel<<<grid, kThreads, smem, c.stream>>>(Y, m, l, leaf, kLeafRows, cin, n_in, G, cout,
                                                                      final_, U, Lp, piv, M);
   RPCA_CHECK_LAUNCH();
   count_launch(c, 1, leaf ? "lu_leaf" : "lu_tree");
@@ -329,6 +234,7 @@ void select(Ctx& c, unsigned grid, const double* Y, int64_t m, int l, int leaf, 
 
 size_t lu_ws_bytes(int64_t m, int l) {
   Sizer s;
+  s.add<char>(ax_ws_bytes(DenseA{nullptr, RPCA_F64, m, l, l}, l) + 4096);
   const int64_t nblk = cdiv(m, kLeafRows);
   s.add<int64_t>(nblk * l);
   s.add<int64_t>(nblk * l);
@@ -337,9 +243,7 @@ size_t lu_ws_bytes(int64_t m, int l) {
   return s.total;
 }
 
-int lu_apply_grid(Ctx& c, int64_t m) { return (int)std::min<int64_t>(cdiv(m, 128), (int64_t)c.num_sms * 2); }
-
-void lu_renorm(Ctx& c, double* Y, int64_t m, int l, double* U_out, int64_t* piv_out, Arena& ar, double* gpart) {
+void lu_renorm(Ctx& c, double* Y, int64_t m, int l, double* U_out, int64_t* piv_out, Arena& ar) {
   RPCA_REQUIRE(l >= 1 && l <= kMaxL && m >= l, RPCA_E_SHAPE, "lu_renorm: need 1 ≤ l ≤ %d and m ≥ l", kMaxL);
   const int G = group_for(l);
   const int64_t nblk = cdiv(m, kLeafRows);
@@ -357,12 +261,16 @@ void lu_renorm(Ctx& c, double* Y, int64_t m, int l, double* U_out, int64_t* piv_
     std::swap(ca, cb);
     n = ng;
   }
-  const size_t smem_apply = (size_t)(l * l + 128 * (l | 1)) * 8;
-  ensure_smem((const void*)lu_apply_kernel, (int)((kMaxL * kMaxL + 128 * (kMaxL | 1)) * 8));
-  const unsigned grid = (unsigned)lu_apply_grid(c, m);
-  lu_apply_kernel<<<grid, kThreads, smem_apply, c.stream>>>(Y, m, l, M, Lp, piv, gpart);
+  // L = Y·M on the fp64 tensor-core pass kernel (in place: every output row is
+  // written only after all of its own K-chunks were read), then the pivot rows
+  // get their exact unit-lower rows
+  {
+    TagScope ts(c, "lu_apply");
+    dense_ax(c, DenseA{Y, RPCA_F64, m, l, l}, M, l, Y, ar);
+  }
+  pivot_rows_kernel<<<1, 256, 0, c.stream>>>(Y, l, Lp, piv);
   RPCA_CHECK_LAUNCH();
-  count_launch(c, 1, "lu_apply");
+  count_launch(c, 1, "lu_pivot_rows");
   if (piv_out) RPCA_CUDA(cudaMemcpyAsync(piv_out, piv, sizeof(int64_t) * l, cudaMemcpyDeviceToDevice, c.stream));
 }
 
