@@ -115,10 +115,24 @@ rpca_status rpca_profile_end(rpca_ctx* ctx, char* buf, size_t cap, size_t* neede
 
 /* ---- multi-GPU (rows of A sharded across ranks) ---------
  * rpca_comm_unique_id: writes an ncclUniqueId (128 bytes) into `id` (host).
- * rpca_comm_init: ncclCommInitRank(nranks, id, rank) on the context's device;
- * afterwards the drivers treat A as the row shard [row0, row0+m_local).      */
+ * rpca_comm_init: ncclCommInitRank(nranks, id, rank) on the context's device
+ * (NCCL is dlopen'ed: libnccl.so.2 as loaded by the process, else
+ * $RPCA_NCCL_PATH; RPCA_E_NCCL if none).  With nranks > 1 the drivers treat
+ * A as this rank's row shard [row0, row0+m_local) (m_local ≥ 1 on every
+ * rank): vectors of length m are row shards, vectors of length n are
+ * replicated, Aᵀ·(·) and the l×l Grams are all-reduced (fp64 sum), the LU's
+ * tournament candidates are all-gathered.  Every rank must make the same
+ * sequence of calls with the same scalar arguments.
+ * rpca_virtual_group_create / rpca_comm_init_virtual: a test communicator —
+ * P contexts on ONE device, each driven by its own host thread, meeting at
+ * host barriers; collectives are device copies and a fixed-order sum kernel
+ * (no kernel ever waits on another rank's kernel).  Not CUDA-graph captured.
+ * The group must outlive the contexts attached to it.                     */
 rpca_status rpca_comm_unique_id(void* id, size_t bytes);
 rpca_status rpca_comm_init(rpca_ctx* ctx, int nranks, int rank, const void* id);
+rpca_status rpca_virtual_group_create(int nranks, void** group);
+rpca_status rpca_virtual_group_destroy(void* group);
+rpca_status rpca_comm_init_virtual(rpca_ctx* ctx, void* group, int rank);
 
 /* ---- §8(a) step a1: Ω ------------------------------------------------------
  * out (rows×cols, row-major, fp64, device) = the test block of PAPER.md:163-168
@@ -131,7 +145,8 @@ rpca_status rpca_comm_init(rpca_ctx* ctx, int nranks, int rank, const void* id);
 rpca_status rpca_omega(rpca_ctx* ctx, uint64_t seed, uint32_t stream_id, int64_t rows, int64_t cols,
                        int dist, int round_f32, double* out);
 
-/* ---- column means: c[j] = (1/m)·Σ_i A_ij (global rows). */
+/* ---- column means: c[j] = (1/m)·Σ_i A_ij over the global
+ * rows (sharded: local sums ÷ m, all-reduced).                              */
 rpca_status rpca_colmeans(rpca_ctx* ctx, const rpca_mat* A, double* c);
 
 /* ---- §8(a) steps a2, a4, a6: applications of A --------
@@ -187,8 +202,10 @@ rpca_status rpca_pca(rpca_ctx* ctx, const rpca_mat* A, int64_t k, int raw, int i
  * last); B1 = A·Q; B2 = sym(QᵀB1); variant RPCA_SHIFT_CHOL: ν = u·√n·‖B1‖_F,
  * C = chol(B2 + νI) (ν ×10 up to 5 retries), F = (B1 + νQ)·C⁻¹;
  * RPCA_SQRT: C = B2^{1/2} with a 1e-12-regularised pseudo-inverse.  F = U·S·Wᵀ,
- * lam = max(S² − ν, 0).  Outputs in A's dtype: U (n_local×k, ld ldu), lam (k).
- * Synchronises the stream.                                                  */
+ * lam = max(S² − ν, 0).  Outputs in A's dtype: U (m_local×k, ld ldu), lam (k).
+ * Sharded: the shards must be the uniform partition, rank r holding rows
+ * [r·⌈n/P⌉, min(n, (r+1)·⌈n/P⌉)) (Q is all-gathered for A_r·Q), else
+ * RPCA_E_SHAPE.  Synchronises the stream.                                   */
 rpca_status rpca_eigens(rpca_ctx* ctx, const rpca_mat* A, int64_t k, int its, int64_t l, uint64_t seed,
                         int variant, void* U, int64_t ldu, void* lam);
 

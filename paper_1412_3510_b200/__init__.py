@@ -18,7 +18,8 @@ import threading
 import torch
 
 __all__ = ["pca", "eigens", "diffsnorm", "omega", "apply", "colmeans", "lu_renorm", "qr", "small_svd",
-           "launch_count", "library_path", "RPCAError", "CSR", "profile", "clear_cache"]
+           "launch_count", "library_path", "RPCAError", "CSR", "profile", "clear_cache", "comm_unique_id",
+           "comm_init", "comm_init_torch", "VirtualGroup", "uniform_shard"]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _LIB_PATH = os.path.join(_HERE, "librpca.so")
@@ -77,6 +78,9 @@ def _load():
             "rpca_profile_end": [vp, C.c_char_p, C.c_size_t, C.POINTER(C.c_size_t)],
             "rpca_comm_unique_id": [vp, C.c_size_t],
             "rpca_comm_init": [vp, i32, i32, vp],
+            "rpca_virtual_group_create": [i32, C.POINTER(vp)],
+            "rpca_virtual_group_destroy": [vp],
+            "rpca_comm_init_virtual": [vp, vp, i32],
             "rpca_omega": [vp, u64, u32, i64, i64, i32, i32, dp],
             "rpca_colmeans": [vp, pm, dp],
             "rpca_apply": [vp, pm, dp, i32, dp, i64, dp],
@@ -120,6 +124,15 @@ def _ctx(device: torch.device, flags: int = 0):
     return L, h
 
 
+def release_context(device=None):
+    """Destroy this thread's context on `device` (and its communicator)."""
+    dev = torch.device("cuda", torch.cuda.current_device() if device is None else device)
+    key = (threading.get_ident(), dev.index)
+    h = _ctxs.pop(key, None)
+    if h is not None:
+        _check(_load().rpca_ctx_destroy(h))
+
+
 def _ctx_flags(h, flags):
     _check(_load().rpca_ctx_set_flags(h, flags))
 
@@ -136,12 +149,13 @@ def _dtype_code(dt):
     raise TypeError("A must be float64 or float32")
 
 
-def _dense(A: torch.Tensor, host=False) -> rpca_mat:
+def _dense(A: torch.Tensor, host=False, m_total=None, row0=0) -> rpca_mat:
     if A.dim() != 2 or A.stride(1) != 1:
         raise ValueError("A must be a 2-D row-major tensor (stride(1) == 1)")
-    m, n = A.shape
-    return rpca_mat(DENSE, _dtype_code(A.dtype), m, n, 0, m, A.data_ptr(), A.stride(0), None, None, None, 0,
-                    HOST if host else DEVICE, 0)
+    ml, n = A.shape
+    m = ml if m_total is None else int(m_total)
+    return rpca_mat(DENSE, _dtype_code(A.dtype), m, n, int(row0), ml, A.data_ptr(), max(A.stride(0), n), None, None,
+                    None, 0, HOST if host else DEVICE, 0)
 
 
 class CSR:
@@ -161,16 +175,75 @@ class CSR:
         return cls(T.crow_indices(), T.col_indices(), T.values(), T.shape)
 
 
-def _as_mat(A, host=False):
-    """(rpca_mat, keepalive) for a dense tensor, a CSR, or a torch sparse CSR tensor."""
+def _as_mat(A, host=False, m_total=None, row0=0):
+    """(rpca_mat, keepalive) for a dense tensor, a CSR, or a torch sparse CSR
+    tensor.  With m_total given, A holds rows [row0, row0 + A.shape[0]) of an
+    m_total-row matrix sharded over the ranks of the communicator."""
     if isinstance(A, torch.Tensor) and A.layout == torch.sparse_csr:
         A = CSR.from_torch(A)
     if isinstance(A, CSR):
-        m, n = A.shape
-        mat = rpca_mat(CSR_KIND, _dtype_code(A.dtype), m, n, 0, m, None, n, A.rowptr.data_ptr(),
+        ml, n = A.shape
+        m = ml if m_total is None else int(m_total)
+        mat = rpca_mat(CSR_KIND, _dtype_code(A.dtype), m, n, int(row0), ml, None, n, A.rowptr.data_ptr(),
                        A.colind.data_ptr(), A.vals.data_ptr(), A.vals.numel(), DEVICE, 0)
         return mat, A
-    return _dense(A, host=host), A
+    return _dense(A, host=host, m_total=m_total, row0=row0), A
+
+
+# ---------------------------------------------------------------- multi-GPU
+def uniform_shard(m: int, nranks: int, rank: int):
+    """(row0, m_local) of the uniform row partition (required by eigens)."""
+    pad = -(-m // nranks)
+    row0 = min(m, rank * pad)
+    return row0, min(pad, m - row0)
+
+
+def comm_unique_id() -> bytes:
+    """A fresh ncclUniqueId (128 bytes) for comm_init."""
+    L = _load()
+    buf = C.create_string_buffer(128)
+    _check(L.rpca_comm_unique_id(buf, 128))
+    return buf.raw
+
+
+def comm_init(nranks: int, rank: int, uid: bytes, device=None):
+    """Attach an NCCL communicator to this thread's context on `device`; later
+    calls treat their A as this rank's row shard (m_total=, row0=)."""
+    dev = torch.device("cuda", torch.cuda.current_device() if device is None else device)
+    L, h = _ctx(dev)
+    _check(L.rpca_comm_init(h, nranks, rank, C.create_string_buffer(bytes(uid), 128)))
+
+
+def comm_init_torch(group=None, device=None):
+    """comm_init over the ranks of an initialised torch.distributed group (rank 0
+    draws the id, a broadcast_object_list shares it)."""
+    import torch.distributed as dist
+    obj = [comm_unique_id() if dist.get_rank(group) == 0 else None]
+    dist.broadcast_object_list(obj, src=0, group=group)
+    comm_init(dist.get_world_size(group), dist.get_rank(group), obj[0], device)
+
+
+class VirtualGroup:
+    """P virtual ranks on ONE GPU for testing the sharded path: each rank is a
+    host thread with its own context; collectives are host-barrier-synchronised
+    device copies (include/rpca.h)."""
+
+    def __init__(self, nranks: int):
+        L = _load()
+        self.nranks = nranks
+        self.h = C.c_void_p()
+        _check(L.rpca_virtual_group_create(nranks, C.byref(self.h)))
+
+    def attach(self, rank: int, device=None):
+        """Call from the thread that will act as `rank`."""
+        dev = torch.device("cuda", torch.cuda.current_device() if device is None else device)
+        L, h = _ctx(dev)
+        _check(L.rpca_comm_init_virtual(h, self.h, rank))
+
+    def close(self):
+        if self.h:
+            _check(_load().rpca_virtual_group_destroy(self.h))
+            self.h = C.c_void_p()
 
 
 def clear_cache(device=None):
@@ -228,23 +301,25 @@ def omega(rows: int, cols: int, seed: int = 0, stream_id: int = 0, dist: int = G
     return out
 
 
-def colmeans(A) -> torch.Tensor:
+def colmeans(A, m_total=None, row0=0) -> torch.Tensor:
     L, h = _ctx(A.device)
     c = torch.empty(A.shape[1], dtype=torch.float64, device=A.device)
-    mat, keep = _as_mat(A)
+    mat, keep = _as_mat(A, m_total=m_total, row0=row0)
     _check(L.rpca_colmeans(h, C.byref(mat), _ptr(c)))
     return c
 
 
-def apply(A: torch.Tensor, X: torch.Tensor, adjoint: bool = False, cmean: torch.Tensor | None = None):
-    """Y = A·X (adjoint=False) or Aᵀ·X, optionally centred by the column means `cmean`."""
+def apply(A: torch.Tensor, X: torch.Tensor, adjoint: bool = False, cmean: torch.Tensor | None = None,
+          m_total=None, row0=0):
+    """Y = A·X (adjoint=False) or Aᵀ·X, optionally centred by the column means `cmean`
+    (sharded: A·X gives this rank's rows, Aᵀ·X is all-reduced)."""
     L, h = _ctx(A.device)
     X = X.contiguous()
     assert X.dtype == torch.float64
     l = X.shape[1]
     rows = A.shape[1] if adjoint else A.shape[0]
     Y = torch.empty(rows, l, dtype=torch.float64, device=A.device)
-    mat, keep = _as_mat(A)
+    mat, keep = _as_mat(A, m_total=m_total, row0=row0)
     _check(L.rpca_apply(h, C.byref(mat), _ptr(cmean), int(adjoint), _ptr(X), l, _ptr(Y)))
     return Y
 
@@ -283,16 +358,19 @@ def small_svd(G: torch.Tensor):
 
 
 def pca(A: torch.Tensor, k: int, raw: bool = True, its: int = 2, l: int | None = None, seed: int = 0,
-        uniform_omega: bool = False):
+        uniform_omega: bool = False, m_total: int | None = None, row0: int = 0):
     """Rank-k PCA / SVD of A (§2 eqs. i1-i4, §5): returns (U m×k, S k, V n×k) on A's device.
 
     raw=False centres the columns implicitly.  A may also be
     a pinned host tensor: then the host→device copy and the device→host copy of
-    the factors happen inside the call (the end-to-end mode)."""
+    the factors happen inside the call (the end-to-end mode).  With a
+    communicator attached (comm_init / VirtualGroup.attach), A is this rank's
+    row shard [row0, row0 + A.shape[0]) of an m_total-row matrix and U is
+    returned for those rows (V replicated)."""
     host = A.device.type == "cpu"
     dev = torch.device("cuda", torch.cuda.current_device()) if host else A.device
     L_, h = _ctx(dev)
-    m, n = A.shape
+    m, n = A.shape  # m: local rows
     flags = (FLAG_UNIFORM_OMEGA if uniform_omega else 0) | (FLAG_OUTPUTS_HOST if host else 0)
     _ctx_flags(h, flags)
     outdev = torch.device("cpu") if host else dev
@@ -300,7 +378,7 @@ def pca(A: torch.Tensor, k: int, raw: bool = True, its: int = 2, l: int | None =
     U = torch.empty(m, k, dtype=A.dtype, device=outdev, pin_memory=pin)
     S = torch.empty(k, dtype=A.dtype, device=outdev, pin_memory=pin)
     V = torch.empty(n, k, dtype=A.dtype, device=outdev, pin_memory=pin)
-    mat, keep = _as_mat(A, host=host)
+    mat, keep = _as_mat(A, host=host, m_total=m_total, row0=row0)
     try:
         _check(L_.rpca_pca(h, C.byref(mat), k, int(bool(raw)), its, -1 if l is None else l, seed,
                            _ptr(U), k, _ptr(S), _ptr(V), k))
@@ -310,18 +388,19 @@ def pca(A: torch.Tensor, k: int, raw: bool = True, its: int = 2, l: int | None =
 
 
 def eigens(A: torch.Tensor, k: int, its: int = 2, l: int | None = None, seed: int = 0,
-           variant: str = "shift_chol", uniform_omega: bool = False):
-    """Stabilised Nyström (§3) of a PSD A: returns (U n×k, lam k)."""
+           variant: str = "shift_chol", uniform_omega: bool = False, m_total: int | None = None, row0: int = 0):
+    """Stabilised Nyström (§3) of a PSD A: returns (U n×k, lam k).
+    Sharded: A holds rows uniform_shard(n, P, rank) and U comes back for them."""
     host = A.device.type == "cpu"
     dev = torch.device("cuda", torch.cuda.current_device()) if host else A.device
     L_, h = _ctx(dev)
-    n = A.shape[0]
+    n = A.shape[0]  # local rows
     v = {"shift_chol": SHIFT_CHOL, "sqrt": SQRT}[variant]
     _ctx_flags(h, (FLAG_UNIFORM_OMEGA if uniform_omega else 0) | (FLAG_OUTPUTS_HOST if host else 0))
     outdev = torch.device("cpu") if host else dev
     U = torch.empty(n, k, dtype=A.dtype, device=outdev, pin_memory=host)
     lam = torch.empty(k, dtype=A.dtype, device=outdev, pin_memory=host)
-    mat, keep = _as_mat(A, host=host)
+    mat, keep = _as_mat(A, host=host, m_total=m_total, row0=row0)
     try:
         _check(L_.rpca_eigens(h, C.byref(mat), k, its, -1 if l is None else l, seed, v, _ptr(U), k, _ptr(lam)))
     finally:
@@ -330,15 +409,16 @@ def eigens(A: torch.Tensor, k: int, its: int = 2, l: int | None = None, seed: in
 
 
 def diffsnorm(A: torch.Tensor, U: torch.Tensor, S: torch.Tensor, V: torch.Tensor, raw: bool = True, its: int = 20,
-              seed: int = 1) -> float:
-    """Power-method estimate of ‖A − U·diag(S)·Vᵀ‖ (§4 l.362-371)."""
+              seed: int = 1, m_total: int | None = None, row0: int = 0) -> float:
+    """Power-method estimate of ‖A − U·diag(S)·Vᵀ‖ (§4 l.362-371).
+    Sharded: A and U are this rank's rows, V replicated."""
     L_, h = _ctx(A.device)
     U = U.to(torch.float64).contiguous()
     V = V.to(torch.float64).contiguous()
     S = S.to(torch.float64).contiguous()
     k = S.shape[0]
     out = C.c_double(0.0)
-    mat, keep = _as_mat(A)
+    mat, keep = _as_mat(A, m_total=m_total, row0=row0)
     _check(L_.rpca_diffsnorm(h, C.byref(mat), int(bool(raw)), _ptr(U), max(k, 1), _ptr(S), _ptr(V), max(k, 1), k,
                              its, seed, C.byref(out)))
     return out.value

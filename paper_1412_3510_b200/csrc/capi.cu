@@ -189,6 +189,25 @@ rpca_status rpca_comm_init(rpca_ctx* c, int nranks, int rank, const void* id) {
   });
 }
 
+rpca_status rpca_virtual_group_create(int nranks, void** group) {
+  return guard([&] {
+    RPCA_REQUIRE(group, RPCA_E_ARG, "group is NULL");
+    *group = rpca::virtual_group_create(nranks);
+  });
+}
+
+rpca_status rpca_virtual_group_destroy(void* group) {
+  return guard([&] { rpca::virtual_group_destroy(group); });
+}
+
+rpca_status rpca_comm_init_virtual(rpca_ctx* c, void* group, int rank) {
+  if (!c) return RPCA_E_ARG;
+  return guard([&] {
+    DeviceScope ds(c->device);
+    rpca::comm_init_virtual(*c, group, rank);
+  });
+}
+
 rpca_status rpca_omega(rpca_ctx* c, uint64_t seed, uint32_t stream_id, int64_t rows, int64_t cols, int dist,
                        int round_f32, double* out) {
   if (!c) return RPCA_E_ARG;

@@ -14,7 +14,7 @@
 // The two Grams (LᵀL, Q1ᵀQ1) run on the fp64 tensor-core adjoint pass
 // (dense_aty with A := Y) and the two triangular products on the A·X pass
 // (dense_ax, in place); only the l×l Cholesky/inverse is a one-CTA kernel.
-#include "internal.cuh"
+#include "comm.cuh"
 
 namespace rpca {
 namespace {
@@ -139,6 +139,44 @@ void orthonormalize(Ctx& c, double* Y, int64_t m, int l, double* R_out, Arena& a
   c.tag = "cholqr_trmm";
   dense_ax(c, Yd, M2, l, Y, ar);           // Q = Q1·R2⁻¹·D
   ar.off = mark;
+  if (R_out) RPCA_CUDA(cudaMemcpyAsync(R_out, R2, sizeof(double) * l * l, cudaMemcpyDeviceToDevice, c.stream));
+}
+
+// Row-sharded variant: the LU is the sharded tournament,
+// each Gram is the all-reduced sum of the per-shard Grams (fixed rank order),
+// the l×l Cholesky runs redundantly on every rank and the triangular products
+// stay local.
+void orthonormalize_sharded(Ctx& c, double* Y, int64_t m, int64_t row0, int l, double* R_out, Arena& ar) {
+  RPCA_REQUIRE(l >= 1 && l <= kMaxL && m >= 0, RPCA_E_SHAPE, "orthonormalize: need 1 ≤ l ≤ %d", kMaxL);
+  double* U = ar.get<double>((size_t)l * l);
+  double* G = ar.get<double>((size_t)l * l);
+  double* M1 = ar.get<double>((size_t)l * l);
+  double* R1 = ar.get<double>((size_t)l * l);
+  double* M2 = ar.get<double>((size_t)l * l);
+  double* R2 = ar.get<double>((size_t)l * l);
+  const DenseA Yd{Y, RPCA_F64, m, l, l};
+  const size_t mark = ar.off;
+  lu_renorm_sharded(c, Y, m, row0, l, U, ar);  // Y ← L (local rows)
+  ar.off = mark;
+  auto gram = [&] {
+    c.tag = "cholqr_gram";
+    if (m > 0) dense_aty(c, Yd, Y, l, nullptr, G, ar);
+    else RPCA_CUDA(cudaMemsetAsync(G, 0, sizeof(double) * l * l, c.stream));
+    ar.off = mark;
+    allreduce_sum(c, G, (size_t)l * l);
+  };
+  auto trmm = [&](const double* Mx) {
+    c.tag = "cholqr_trmm";
+    if (m > 0) dense_ax(c, Yd, Mx, l, Y, ar);
+    ar.off = mark;
+  };
+  TagScope ts(c, "cholqr_gram");
+  gram();
+  chol(c, G, l, U, 0, M1, R1);
+  trmm(M1);
+  gram();
+  chol(c, G, l, R1, 1, M2, R2);
+  trmm(M2);
   if (R_out) RPCA_CUDA(cudaMemcpyAsync(R_out, R2, sizeof(double) * l * l, cudaMemcpyDeviceToDevice, c.stream));
 }
 

@@ -1,12 +1,21 @@
 // comm.cu — the multi-GPU plumbing of SURVEY.md §8(e): rows of A are sharded
 // across ranks (one process per GPU), A·X stays local, Aᵀ·Y and the small
-// l×l reductions are summed with NCCL all-reduce over NVLink/NVSwitch and the
-// TSLU/TSQR candidates are exchanged with all-gather.  NCCL is loaded at run
-// time (dlopen of the libnccl.so.2 PyTorch already brings), so the library
-// has no link-time NCCL dependency and single-GPU users never load it.
+// l×l Grams are summed with NCCL all-reduce over NVLink/NVSwitch and the
+// TSLU candidates are exchanged with all-gather.  NCCL is loaded at run time
+// (dlopen of the libnccl.so.2 PyTorch brings), so single-GPU users never load it.
+//
+// VirtualComm runs P ranks as P contexts (one host thread each) on ONE GPU
+// for testing the sharded algorithms: every collective synchronises the
+// caller's stream, meets the other ranks at a host barrier, and moves data
+// with device copies / a fixed-order sum kernel.  No kernel ever waits on
+// another rank's kernel (B200_PROFILING.md: ranks must not spin on each other
+// on one device).
 #include <dlfcn.h>
 
+#include <condition_variable>
 #include <cstring>
+#include <mutex>
+#include <vector>
 
 #include "comm.cuh"
 
@@ -66,6 +75,92 @@ constexpr int kNcclFloat64 = 8;  // ncclFloat64
 constexpr int kNcclInt8 = 0;     // ncclInt8 (bytes)
 constexpr int kNcclSum = 0;      // ncclSum
 
+struct NcclComm : Comm {
+  void* handle = nullptr;
+  // NCCL collectives can be stream-captured, but that path cannot be exercised
+  // on a one-GPU test box; it stays opt-in (RPCA_NCCL_GRAPH=1) until measured.
+  bool graph = false;
+  bool graphable() const override { return graph; }
+  void allreduce_sum(Ctx& c, double* buf, size_t count) override {
+    check(nccl().allreduce(buf, buf, count, kNcclFloat64, kNcclSum, handle, c.stream), "ncclAllReduce");
+  }
+  void allgather(Ctx& c, const void* send, void* recv, size_t bytes) override {
+    check(nccl().allgather(send, recv, bytes, kNcclInt8, handle, c.stream), "ncclAllGather");
+  }
+  ~NcclComm() override {
+    if (handle) nccl().destroy(handle);
+  }
+};
+
+// ------------------------------------------------------------------ virtual
+struct Group {
+  int n;
+  std::mutex mu;
+  std::condition_variable cv;
+  int arrived = 0;
+  uint64_t gen = 0;
+  std::vector<const void*> ptrs;
+  double* scratch = nullptr;
+  size_t scratch_count = 0;
+  explicit Group(int n_) : n(n_), ptrs(n_, nullptr) {}
+  void barrier() {
+    std::unique_lock<std::mutex> lk(mu);
+    const uint64_t g = gen;
+    if (++arrived == n) {
+      arrived = 0;
+      ++gen;
+      cv.notify_all();
+    } else {
+      cv.wait(lk, [&] { return gen != g; });
+    }
+  }
+};
+
+__global__ void sum_ranks_kernel(const double* const* __restrict__ src, int n, size_t count, double* __restrict__ dst) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < count; i += (size_t)gridDim.x * blockDim.x) {
+    double s = 0.0;
+    for (int r = 0; r < n; ++r) s += src[r][i];  // fixed rank order
+    dst[i] = s;
+  }
+}
+
+struct VirtualComm : Comm {
+  Group* g = nullptr;
+  bool graphable() const override { return false; }
+  void allreduce_sum(Ctx& c, double* buf, size_t count) override {
+    RPCA_CUDA(cudaStreamSynchronize(c.stream));
+    g->ptrs[rank] = buf;
+    g->barrier();
+    if (rank == 0) {
+      if (g->scratch_count < count) {
+        if (g->scratch) RPCA_CUDA(cudaFree(g->scratch));
+        RPCA_CUDA(cudaMalloc(&g->scratch, count * sizeof(double) + g->n * sizeof(double*)));
+        g->scratch_count = count;
+      }
+      const double** table = reinterpret_cast<const double**>(g->scratch + g->scratch_count);
+      RPCA_CUDA(cudaMemcpyAsync(table, g->ptrs.data(), g->n * sizeof(double*), cudaMemcpyHostToDevice, c.stream));
+      sum_ranks_kernel<<<(unsigned)std::min<size_t>(cdiv(count, 256), 1024), 256, 0, c.stream>>>(table, g->n, count,
+                                                                                                 g->scratch);
+      RPCA_CHECK_LAUNCH();
+      RPCA_CUDA(cudaStreamSynchronize(c.stream));
+    }
+    g->barrier();
+    RPCA_CUDA(cudaMemcpyAsync(buf, g->scratch, count * sizeof(double), cudaMemcpyDeviceToDevice, c.stream));
+    RPCA_CUDA(cudaStreamSynchronize(c.stream));
+    g->barrier();
+  }
+  void allgather(Ctx& c, const void* send, void* recv, size_t bytes) override {
+    RPCA_CUDA(cudaStreamSynchronize(c.stream));
+    g->ptrs[rank] = send;
+    g->barrier();
+    for (int r = 0; r < g->n; ++r)
+      RPCA_CUDA(cudaMemcpyAsync(static_cast<char*>(recv) + r * bytes, g->ptrs[r], bytes, cudaMemcpyDeviceToDevice,
+                                c.stream));
+    RPCA_CUDA(cudaStreamSynchronize(c.stream));
+    g->barrier();
+  }
+};
+
 }  // namespace
 
 rpca_status comm_unique_id(void* id, size_t bytes) {
@@ -79,25 +174,46 @@ rpca_status comm_unique_id(void* id, size_t bytes) {
 void comm_init(Ctx& c, int nranks, int rank, const void* id) {
   RPCA_REQUIRE(nranks >= 1 && rank >= 0 && rank < nranks && id, RPCA_E_ARG, "bad rank/nranks/id");
   if (c.comm) comm_destroy(c);
-  Comm* cm = new Comm();
+  NcclComm* cm = new NcclComm();
+  const char* g = getenv("RPCA_NCCL_GRAPH");
+  cm->graph = g && g[0] == '1';
   cm->nranks = nranks;
   cm->rank = rank;
   NcclUniqueId u;
   memcpy(&u, id, sizeof(u));
-  check(nccl().init(&cm->handle, nranks, u, rank), "ncclCommInitRank");
+  const int r = nccl().init(&cm->handle, nranks, u, rank);
+  if (r != 0) {
+    delete cm;
+    check(r, "ncclCommInitRank");
+  }
   c.comm = cm;
 }
 
-void comm_destroy(Ctx& c) {
-  if (!c.comm) return;
-  if (c.comm->handle) nccl().destroy(c.comm->handle);
-  delete c.comm;
-  c.comm = nullptr;
+void* virtual_group_create(int nranks) {
+  RPCA_REQUIRE(nranks >= 1 && nranks <= 64, RPCA_E_ARG, "virtual group size %d", nranks);
+  return new Group(nranks);
 }
 
-void allreduce_sum(Ctx& c, double* buf, size_t count) {
-  if (!c.comm || c.comm->nranks == 1 || count == 0) return;
-  check(nccl().allreduce(buf, buf, count, kNcclFloat64, kNcclSum, c.comm->handle, c.stream), "ncclAllReduce");
+void virtual_group_destroy(void* group) {
+  Group* g = static_cast<Group*>(group);
+  if (g && g->scratch) cudaFree(g->scratch);
+  delete g;
+}
+
+void comm_init_virtual(Ctx& c, void* group, int rank) {
+  Group* g = static_cast<Group*>(group);
+  RPCA_REQUIRE(g && rank >= 0 && rank < g->n, RPCA_E_ARG, "bad virtual group / rank");
+  if (c.comm) comm_destroy(c);
+  VirtualComm* vc = new VirtualComm();
+  vc->g = g;
+  vc->nranks = g->n;
+  vc->rank = rank;
+  c.comm = vc;
+}
+
+void comm_destroy(Ctx& c) {
+  delete c.comm;
+  c.comm = nullptr;
 }
 
 void allgather_bytes(Ctx& c, const void* send, void* recv, size_t bytes_per_rank) {
@@ -105,7 +221,7 @@ void allgather_bytes(Ctx& c, const void* send, void* recv, size_t bytes_per_rank
     if (send != recv) RPCA_CUDA(cudaMemcpyAsync(recv, send, bytes_per_rank, cudaMemcpyDeviceToDevice, c.stream));
     return;
   }
-  check(nccl().allgather(send, recv, bytes_per_rank, kNcclInt8, c.comm->handle, c.stream), "ncclAllGather");
+  c.comm->allgather(c, send, recv, bytes_per_rank);
 }
 
 }  // namespace rpca

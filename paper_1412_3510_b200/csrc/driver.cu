@@ -15,7 +15,7 @@
 #include <mutex>
 #include <string>
 
-#include "internal.cuh"
+#include "comm.cuh"
 
 namespace rpca {
 
@@ -286,10 +286,14 @@ size_t host_copy_bytes(const rpca_mat* A) {
 }
 
 // The operator the range finder sketches (reading Q6): F = A, or Aᵀ if m < n.
+// With a multi-rank communicator A's rows are sharded: vectors of length m
+// are row shards, vectors of length n are replicated, and every Aᵀ·(·) —
+// a sum over rows — is all-reduced.
 struct Op {
   MatV A;
   const double* cmean;
   bool trans;
+  bool sharded;
 };
 
 // Y = A·X [− 1·(c·X)]
@@ -305,7 +309,7 @@ void apply_ax(Ctx& c, const MatV& A, const double* cmean, const double* X, int l
   ar.off = mark;
 }
 
-// Z = Aᵀ·Y [− cᵀ·(1ᵀY)]
+// Z = Aᵀ·Y [− cᵀ·(1ᵀY)] — this shard's rows only
 void apply_aty(Ctx& c, const MatV& A, const double* cmean, const double* Y, int l, double* Z, Arena& ar) {
   const size_t mark = ar.off;
   if (A.csr) {
@@ -321,20 +325,30 @@ void apply_aty(Ctx& c, const MatV& A, const double* cmean, const double* Y, int 
   ar.off = mark;
 }
 
-void colmeans(Ctx& c, const MatV& A, int64_t m_total, double* cmean, Arena& ar) {
+// cmean = column means of the whole A (local sums ÷ m_total, all-reduced)
+void colmeans(Ctx& c, const MatV& A, int64_t m_total, double* cmean, Arena& ar, bool sharded = false) {
   const size_t mark = ar.off;
   if (A.csr) csr_colmeans(c, A.at, m_total, cmean);
   else colmeans_dense(c, A.d.a, A.d.dtype, A.d.m, A.d.n, A.d.lda, m_total, cmean, ar);
   ar.off = mark;
+  if (sharded) allreduce_sum(c, cmean, A.n);
 }
 
 void fwd(Ctx& c, const Op& F, const double* X, int l, double* Y, Arena& ar) {
-  if (F.trans) apply_aty(c, F.A, F.cmean, X, l, Y, ar);
-  else apply_ax(c, F.A, F.cmean, X, l, Y, ar);
+  if (F.trans) {
+    apply_aty(c, F.A, F.cmean, X, l, Y, ar);
+    if (F.sharded) allreduce_sum(c, Y, (size_t)F.A.n * l);
+  } else {
+    apply_ax(c, F.A, F.cmean, X, l, Y, ar);
+  }
 }
 void adj(Ctx& c, const Op& F, const double* Y, int l, double* Z, Arena& ar) {
-  if (F.trans) apply_ax(c, F.A, F.cmean, Y, l, Z, ar);
-  else apply_aty(c, F.A, F.cmean, Y, l, Z, ar);
+  if (F.trans) {
+    apply_ax(c, F.A, F.cmean, Y, l, Z, ar);
+  } else {
+    apply_aty(c, F.A, F.cmean, Y, l, Z, ar);
+    if (F.sharded) allreduce_sum(c, Z, (size_t)F.A.n * l);
+  }
 }
 
 size_t op_ws(Ctx& c, const MatV& A, int l) {
@@ -343,23 +357,42 @@ size_t op_ws(Ctx& c, const MatV& A, int l) {
   return std::max(ax_ws_bytes(A.d, l) + 4096 * 4, aty_ws_bytes(c, A.d, l)) + small;
 }
 
-void renorm_lu(Ctx& c, double* Y, int64_t rows, int l, Arena& ar) {
+// A block of `rows` rows that is either whole (replicated) or this rank's
+// shard starting at global row `row0` of a row-sharded block.
+struct Blk {
+  double* p;
+  int64_t rows;
+  bool sharded;
+  int64_t row0;
+};
+
+void renorm_lu(Ctx& c, const Blk& Y, int l, Arena& ar) {
   const size_t mark = ar.off;
-  lu_renorm(c, Y, rows, l, nullptr, nullptr, ar);
+  if (Y.sharded) lu_renorm_sharded(c, Y.p, Y.rows, Y.row0, l, nullptr, ar);
+  else lu_renorm(c, Y.p, Y.rows, l, nullptr, nullptr, ar);
   ar.off = mark;
 }
 // the last renormalisation and the QR of Bᵀ: LU-Cholesky-QR
-void renorm_qr(Ctx& c, double* Y, int64_t rows, int l, double* R, Arena& ar) {
+void renorm_qr(Ctx& c, const Blk& Y, int l, double* R, Arena& ar) {
   const size_t mark = ar.off;
-  orthonormalize(c, Y, rows, l, R, ar);
+  if (Y.sharded) orthonormalize_sharded(c, Y.p, Y.rows, Y.row0, l, R, ar);
+  else orthonormalize(c, Y.p, Y.rows, l, R, ar);
   ar.off = mark;
 }
 
-void check_single_gpu(Ctx& c, const rpca_mat* A) {
-  RPCA_REQUIRE(c.comm != nullptr || (A->row0 == 0 && A->m_local == A->m), RPCA_E_SHAPE,
-               "row shard given but no communicator (rpca_comm_init)");
-  RPCA_REQUIRE(c.comm == nullptr, RPCA_E_NOTIMPL, "multi-GPU path not implemented yet");
+// Without a multi-rank communicator A must be whole; with one, every rank
+// holds a non-empty row shard.  Returns whether the call runs sharded.
+bool check_shard(Ctx& c, const rpca_mat* A) {
+  if (comm_size(c) <= 1) {
+    RPCA_REQUIRE(A->row0 == 0 && A->m_local == A->m, RPCA_E_SHAPE,
+                 "row shard given but no multi-rank communicator (rpca_comm_init)");
+    return false;
+  }
+  RPCA_REQUIRE(A->m_local >= 1, RPCA_E_SHAPE, "sharded call: every rank needs ≥ 1 row (m_local = 0)");
+  return true;
 }
+
+bool graphable_comm(const Ctx& c) { return !c.comm || c.comm->graphable(); }
 
 void sync_status(Ctx& c) { RPCA_CUDA(cudaStreamSynchronize(c.stream)); }
 
@@ -374,8 +407,13 @@ void apply_step(Ctx& c, const rpca_mat* Am, const double* cm, int adjoint, const
   const MatV probe = probe_of(Am);
   Arena ar = c.arena(op_ws(c, probe, (int)l) + 65536);
   const MatV A = device_view(c, Am, ar);
-  if (adjoint) apply_aty(c, A, cm, X, (int)l, Y, ar);
-  else apply_ax(c, A, cm, X, (int)l, Y, ar);
+  const bool sh = check_shard(c, Am);
+  if (adjoint) {
+    apply_aty(c, A, cm, X, (int)l, Y, ar);
+    if (sh) allreduce_sum(c, Y, (size_t)A.n * l);
+  } else {
+    apply_ax(c, A, cm, X, (int)l, Y, ar);
+  }
 }
 
 void colmeans_step(Ctx& c, const rpca_mat* Am, double* cm) {
@@ -385,7 +423,7 @@ void colmeans_step(Ctx& c, const rpca_mat* Am, double* cm) {
   const MatV probe = probe_of(Am);
   Arena ar = c.arena((size_t)(cdiv(probe.m, 8192) + 2) * probe.n * 8 + 65536);
   const MatV A = device_view(c, Am, ar);
-  colmeans(c, A, Am->m, cm, ar);
+  colmeans(c, A, Am->m, cm, ar, check_shard(c, Am));
 }
 
 void clear_cache(Ctx& c) {
@@ -402,7 +440,7 @@ void clear_cache(Ctx& c) {
 void pca(Ctx& c, const rpca_mat* Am, int64_t k, int raw, int its, int64_t l, uint64_t seed, void* U, int64_t ldu,
          void* S, void* V, int64_t ldv) {
   validate_mat(Am);
-  check_single_gpu(c, Am);
+  const bool sh = check_shard(c, Am);
   if (l <= 0) l = k + 2;
   const int64_t mn = std::min(Am->m, Am->n);
   RPCA_REQUIRE(k >= 1 && l >= k && l <= mn && its >= 0, RPCA_E_SHAPE, "need 1 ≤ k ≤ l ≤ min(m,n), its ≥ 0");
@@ -413,12 +451,13 @@ void pca(Ctx& c, const rpca_mat* Am, int64_t k, int raw, int its, int64_t l, uin
   const bool out_host = (c.flags & RPCA_FLAG_OUTPUTS_HOST) != 0;
   const int dist = (c.flags & RPCA_FLAG_UNIFORM_OMEGA) ? RPCA_UNIFORM : RPCA_GAUSSIAN;
   const int odt = Am->dtype, osz = elem_size(odt);
-  const int64_t m = Am->m, n = Am->n;
+  const int64_t m = Am->m, n = Am->n, ml = Am->m_local, r0 = Am->row0;
 
-  // ---- workspace plan (allocation happens before any capture)
+  // ---- workspace plan (allocation happens before any capture).  Vectors of
+  // length m are this rank's rows (ml of them); U is returned for those rows.
   const MatV probe = probe_of(Am);
   const bool trans = m < n;
-  const int64_t nin = trans ? m : n, nout = trans ? n : m;
+  const int64_t nin = trans ? ml : n, nout = trans ? n : ml;
   Sizer sz;
   sz.add<char>(host_copy_bytes(Am));
   sz.add<double>(nin * l);   // Zb
@@ -428,7 +467,7 @@ void pca(Ctx& c, const rpca_mat* Am, int64_t k, int raw, int its, int64_t l, uin
   sz.add<double>(std::max(nin, nout) * k);  // V-side temp
   sz.add<double>(k);                        // signs
   if (out_host) {
-    sz.add<char>((size_t)m * ldu * osz);
+    sz.add<char>((size_t)ml * ldu * osz);
     sz.add<char>((size_t)n * ldv * osz);
     sz.add<char>((size_t)k * osz);
   }
@@ -436,13 +475,14 @@ void pca(Ctx& c, const rpca_mat* Am, int64_t k, int raw, int its, int64_t l, uin
   size_t scratch = op_ws(c, probe, L);
   scratch = std::max(scratch, lu_ws_bytes(std::max(nin, nout), L));
   scratch = std::max(scratch, orth_ws_bytes(c, std::max(nin, nout), L));
-  scratch = std::max(scratch, (size_t)(cdiv(std::max(m, n), 8192) + 2) * (n + 2 * k) * 8 + 65536);
+  scratch = std::max(scratch, (size_t)(cdiv(std::max(ml, n), 8192) + 2) * (n + 2 * k) * 8 + 65536);
   ensure_transpose(c, Am);
   Arena ar = c.arena(fixed + scratch + 65536);
 
   KeyHasher kh;
-  kh << 1 << *Am << k << raw << its << l << seed << U << ldu << S << V << ldv << c.flags << c.ws << c.tcache.mem;
-  const bool graphable = Am->location == RPCA_DEVICE && !out_host;
+  kh << 1 << *Am << k << raw << its << l << seed << U << ldu << S << V << ldv << c.flags << c.ws << c.tcache.mem
+     << c.comm;
+  const bool graphable = Am->location == RPCA_DEVICE && !out_host && graphable_comm(c);
 
   execute(c, kh.h, graphable, [&] {
     const MatV dA = device_view(c, Am, ar);
@@ -457,35 +497,39 @@ void pca(Ctx& c, const rpca_mat* Am, int64_t k, int raw, int its, int64_t l, uin
     double* sign = ar.get<double>(k);
     void *Ud = U, *Vd = V, *Sd = S;
     if (out_host) {
-      Ud = ar.get<char>((size_t)m * ldu * osz);
+      Ud = ar.get<char>((size_t)ml * ldu * osz);
       Vd = ar.get<char>((size_t)n * ldv * osz);
       Sd = ar.get<char>((size_t)k * osz);
     }
-    Op F{dA, nullptr, trans};
+    // the m-long block is the sharded one
+    const Blk Y{Yb, nout, sh && !trans, r0}, Z{Zb, nin, sh && trans, r0};
+    Op F{dA, nullptr, trans, sh};
     if (!raw) {
       const size_t mark = ar.off;
-      colmeans(c, dA, m, cmean, ar);
+      colmeans(c, dA, m, cmean, ar, sh);
       ar.off = mark;
       F.cmean = cmean;
     }
-    // Ω (nin×l); the fp32 path consumes fl32(Ω) exactly as the oracle does
-    omega(c, seed, 0u, nin, l, dist, odt == RPCA_F32, Zb);
+    // Ω (nin×l; for the sketched Aᵀ, this rank's rows of the m×l Ω); the fp32
+    // path consumes fl32(Ω) exactly as the oracle does
+    omega(c, seed, 0u, nin, l, dist, odt == RPCA_F32, Zb, trans ? r0 : 0);
     fwd(c, F, Zb, L, Yb, ar);
-    if (its == 0) renorm_qr(c, Yb, nout, L, nullptr, ar);
-    else renorm_lu(c, Yb, nout, L, ar);
+    if (its == 0) renorm_qr(c, Y, L, nullptr, ar);
+    else renorm_lu(c, Y, L, ar);
     for (int it = 1; it <= its; ++it) {
       adj(c, F, Yb, L, Zb, ar);
-      renorm_lu(c, Zb, nin, L, ar);
+      renorm_lu(c, Z, L, ar);
       fwd(c, F, Zb, L, Yb, ar);
-      if (it < its) renorm_lu(c, Yb, nout, L, ar);
-      else renorm_qr(c, Yb, nout, L, nullptr, ar);
+      if (it < its) renorm_lu(c, Y, L, ar);
+      else renorm_qr(c, Y, L, nullptr, ar);
     }
     // Bᵀ = F*·Q (eq. i2), Bᵀ = Q_B·R, R = Vr·Σ·Wᵀ ⇒ B = W Σ (Q_B Vr)ᵀ (eq. i3)
     adj(c, F, Yb, L, Zb, ar);
-    renorm_qr(c, Zb, nin, L, R, ar);
+    renorm_qr(c, Z, L, R, ar);
     jacobi_svd_small(c, R, L, sig, W, Vr);
     {
       const size_t mark = ar.off;
+      // V (n×k, replicated) fixes the column signs; U is this rank's rows
       if (!trans) {
         // V = Q_B·Vr[:, :k] (n×k), U = Q·W[:, :k] (m×k)  (eq. i4)
         thin_gemm(c, Zb, nin, L, Vr, K, nullptr, side, k, RPCA_F64);
@@ -503,7 +547,7 @@ void pca(Ctx& c, const rpca_mat* Am, int64_t k, int raw, int its, int64_t l, uin
       ar.off = mark;
     }
     if (out_host) {
-      RPCA_CUDA(cudaMemcpyAsync(U, Ud, (size_t)m * ldu * osz, cudaMemcpyDeviceToHost, c.stream));
+      RPCA_CUDA(cudaMemcpyAsync(U, Ud, (size_t)ml * ldu * osz, cudaMemcpyDeviceToHost, c.stream));
       RPCA_CUDA(cudaMemcpyAsync(V, Vd, (size_t)n * ldv * osz, cudaMemcpyDeviceToHost, c.stream));
       RPCA_CUDA(cudaMemcpyAsync(S, Sd, (size_t)k * osz, cudaMemcpyDeviceToHost, c.stream));
     }
@@ -511,16 +555,26 @@ void pca(Ctx& c, const rpca_mat* Am, int64_t k, int raw, int its, int64_t l, uin
 }
 
 // ============================================================ rpca_eigens
+// Row-sharded: the shards must be the uniform partition
+// (rank r holds rows [r·⌈n/P⌉, min(n, (r+1)·⌈n/P⌉))) so that Q can be
+// all-gathered into one n×l block for A_r·Q; B2 = Σ_r Q_rᵀB1_r and ‖B1‖_F²
+// are all-reduced; U is returned for this rank's rows.
 void eigens(Ctx& c, const rpca_mat* Am, int64_t k, int its, int64_t l, uint64_t seed, int variant, void* U,
             int64_t ldu, void* lam) {
   validate_mat(Am);
-  check_single_gpu(c, Am);
+  const bool sh = check_shard(c, Am);
   RPCA_REQUIRE(Am->m == Am->n, RPCA_E_SHAPE, "eigens needs a square A");
   RPCA_REQUIRE(variant == RPCA_SHIFT_CHOL || variant == RPCA_SQRT, RPCA_E_ARG, "bad variant");
   if (l <= 0) l = k + 2;
-  const int64_t n = Am->n;
+  const int64_t n = Am->n, ml = Am->m_local, r0 = Am->row0;
   RPCA_REQUIRE(k >= 1 && l >= k && l <= n && its >= 0 && l <= kMaxL, RPCA_E_SHAPE, "bad k/l/its");
   RPCA_REQUIRE(U && lam && ldu >= k, RPCA_E_ARG, "bad outputs");
+  const int P = comm_size(c), rank = c.comm ? c.comm->rank : 0;
+  const int64_t pad = sh ? cdiv(n, P) : n;  // rows per gathered slot
+  if (sh)
+    RPCA_REQUIRE(r0 == rank * pad && ml == std::min(pad, n - r0), RPCA_E_SHAPE,
+                 "sharded eigens: rank %d must hold rows [%lld, %lld) (uniform partition)", rank,
+                 (long long)(rank * pad), (long long)std::min(n, (rank + 1) * pad));
   const int L = (int)l, K = (int)k;
   const bool out_host = (c.flags & RPCA_FLAG_OUTPUTS_HOST) != 0;
   const int dist = (c.flags & RPCA_FLAG_UNIFORM_OMEGA) ? RPCA_UNIFORM : RPCA_GAUSSIAN;
@@ -529,30 +583,29 @@ void eigens(Ctx& c, const rpca_mat* Am, int64_t k, int its, int64_t l, uint64_t 
   const MatV probe = probe_of(Am);
   Sizer sz;
   sz.add<char>(host_copy_bytes(Am));
-  sz.add<double>(3 * n * l);
+  sz.add<double>(2 * P * pad * l + 2 * ml * l);
   sz.add<double>(6 * l * l + 8 * l + 16);
-  sz.add<double>(n * k + k);
+  sz.add<double>(ml * k + k);
   if (out_host) {
-    sz.add<char>((size_t)n * ldu * osz);
+    sz.add<char>((size_t)ml * ldu * osz);
     sz.add<char>((size_t)k * osz);
   }
   size_t scratch = op_ws(c, probe, L);
-  scratch = std::max(scratch, lu_ws_bytes(n, L));
-  scratch = std::max(scratch, orth_ws_bytes(c, n, L));
-  scratch = std::max(scratch, (size_t)(cdiv(n, 8192) + 2) * l * l * 8 + 65536);
+  scratch = std::max(scratch, lu_ws_bytes(ml, L));
+  scratch = std::max(scratch, orth_ws_bytes(c, ml, L));
+  scratch = std::max(scratch, (size_t)(cdiv(n, 8192) + 2) * l * l * 8 + 65536 + (size_t)P * 3 * l * 8);
   Arena ar = c.arena(sz.total + scratch + 65536);
   if (!c.status_host) RPCA_CUDA(cudaMallocHost(&c.status_host, 64));
 
   KeyHasher kh;
-  kh << 2 << *Am << k << its << l << seed << variant << U << ldu << lam << c.flags << c.ws;
-  const bool graphable = Am->location == RPCA_DEVICE && !out_host;
+  kh << 2 << *Am << k << its << l << seed << variant << U << ldu << lam << c.flags << c.ws << c.comm;
+  const bool graphable = Am->location == RPCA_DEVICE && !out_host && graphable_comm(c);
   // fixed buffers are carved before execute() so that graph replays (which do
   // not run the lambda) see the same pointers
-  const MatV dA0 = probe_of(Am);
-  (void)dA0;
-  double* Qbuf = ar.get<double>(n * l);
-  double* Bbuf = ar.get<double>(n * l);
-  double* Fm = ar.get<double>(n * l);
+  double* Qa = ar.get<double>(P * pad * l);  // gathered n×l Q (this rank's rows at slot `rank`)
+  double* Qb = ar.get<double>(P * pad * l);
+  double* B1 = ar.get<double>(ml * l);
+  double* Fm = ar.get<double>(ml * l);
   double* G = ar.get<double>(l * l);
   double* Minv = ar.get<double>(l * l);
   double* R = ar.get<double>(l * l);
@@ -564,51 +617,63 @@ void eigens(Ctx& c, const rpca_mat* Am, int64_t k, int its, int64_t l, uint64_t 
   void* Ud = U;
   void* Ld = lam;
   if (out_host) {
-    Ud = ar.get<char>((size_t)n * ldu * osz);
+    Ud = ar.get<char>((size_t)ml * ldu * osz);
     Ld = ar.get<char>((size_t)k * osz);
   }
-  double* Q = (its & 1) ? Bbuf : Qbuf;  // where the final Q lives after the loop's swaps
+  const int64_t slot = (int64_t)rank * pad * l;
+  auto signs = [&](const double* X, double* sign) {
+    if (sh) column_signs_sharded(c, X, ml, r0, K, k, sign, ar);
+    else column_signs(c, X, ml, K, k, sign, ar);
+  };
+  double* Qfin = ((its & 1) ? Qb : Qa) + slot;  // this rank's final Q after the loop's swaps
   execute(c, kh.h, graphable, [&] {
     const MatV dA = device_view(c, Am, ar);
-    double* Q = Qbuf;
-    double* B1 = Bbuf;
-    double* side = ar.get<double>(n * k);
+    double* Qf = Qa;  // gathered Q
+    double* Qo = Qb;  // the other gather buffer
+    double* side = ar.get<double>(ml * k);
     double* sign = ar.get<double>(k);
+    auto gather = [&] { allgather_bytes(c, Qf + slot, Qf, sizeof(double) * pad * l); };
     // self-adjoint loop: Y = AΩ, then its × (Q = A·Q)
-    omega(c, seed, 0u, n, l, dist, odt == RPCA_F32, B1);
-    apply_ax(c, dA, nullptr, B1, L, Q, ar);
-    if (its == 0) renorm_qr(c, Q, n, L, nullptr, ar);
-    else renorm_lu(c, Q, n, L, ar);
+    omega(c, seed, 0u, n, l, dist, odt == RPCA_F32, Qo);  // the whole n×l Ω on every rank
+    apply_ax(c, dA, nullptr, Qo, L, Qf + slot, ar);
+    const Blk Q0{Qf + slot, ml, sh, r0};
+    if (its == 0) renorm_qr(c, Q0, L, nullptr, ar);
+    else renorm_lu(c, Q0, L, ar);
     for (int it = 1; it <= its; ++it) {
-      apply_ax(c, dA, nullptr, Q, L, B1, ar);
-      std::swap(Q, B1);
-      if (it < its) renorm_lu(c, Q, n, L, ar);
-      else renorm_qr(c, Q, n, L, nullptr, ar);
+      gather();
+      apply_ax(c, dA, nullptr, Qf, L, Qo + slot, ar);
+      std::swap(Qf, Qo);
+      const Blk Qi{Qf + slot, ml, sh, r0};
+      if (it < its) renorm_lu(c, Qi, L, ar);
+      else renorm_qr(c, Qi, L, nullptr, ar);
     }
-    apply_ax(c, dA, nullptr, Q, L, B1, ar);  // (start) B1 = A·Q
+    gather();
+    apply_ax(c, dA, nullptr, Qf, L, B1, ar);  // (start) B1 = A·Q (this rank's rows)
     {
       const size_t mark = ar.off;
       // (second) B2 = QᵀB1 (symmetrised in the kernels below) — an "Aᵀ·Y" with
       // A := Q (n×l), Y := B1, so it runs on the fp64 tensor-core adjoint kernel
-      dense_aty(c, DenseA{Q, RPCA_F64, n, L, L}, B1, L, nullptr, G, ar);
+      dense_aty(c, DenseA{Qf + slot, RPCA_F64, ml, L, L}, B1, L, nullptr, G, ar);
+      if (sh) allreduce_sum(c, G, (size_t)l * l);
       if (variant == RPCA_SHIFT_CHOL) {
-        weighted_colsum(c, B1, B1, n * l, 1, scal, ar);  // ‖B1‖_F²
+        weighted_colsum(c, B1, B1, ml * l, 1, scal, ar);  // ‖B1‖_F²
+        if (sh) allreduce_sum(c, scal, 1);
         nystrom_shift_chol(c, G, scal, L, n, odt == RPCA_F32 ? 0x1p-23 : 0x1p-52, Minv, scal + 1, status);
-        right_mult(c, B1, Q, scal + 1, Minv, n, L, Fm);  // F = (B1 + νQ)·C⁻¹ (eq. pseudo)
+        right_mult(c, B1, Qf + slot, scal + 1, Minv, ml, L, Fm);  // F = (B1 + νQ)·C⁻¹ (eq. pseudo)
       } else {
         nystrom_sqrt(c, G, L, Minv, scal + 1, status);
-        right_mult(c, B1, nullptr, nullptr, Minv, n, L, Fm);  // F = B1·C⁺
+        right_mult(c, B1, nullptr, nullptr, Minv, ml, L, Fm);  // F = B1·C⁺
       }
       ar.off = mark;
     }
     // F = U S Wᵀ: Q_F R_F = F, R_F = Vr Σ Wᵀ ⇒ U = Q_F·Vr; Σ = S² (eq. finish)
-    renorm_qr(c, Fm, n, L, R, ar);
+    renorm_qr(c, Blk{Fm, ml, sh, r0}, L, R, ar);
     jacobi_svd_small(c, R, L, sig, W, Vr);
     {
       const size_t mark = ar.off;
-      thin_gemm(c, Fm, n, L, Vr, K, nullptr, side, k, RPCA_F64);
-      column_signs(c, side, n, K, k, sign, ar);
-      scale_cast(c, side, n, K, sign, Ud, ldu, odt);
+      thin_gemm(c, Fm, ml, L, Vr, K, nullptr, side, k, RPCA_F64);
+      signs(side, sign);
+      scale_cast(c, side, ml, K, sign, Ud, ldu, odt);
       nystrom_lambda(c, sig, scal + 1, K, Ld, odt);
       ar.off = mark;
     }
@@ -620,50 +685,52 @@ void eigens(Ctx& c, const rpca_mat* Am, int64_t k, int its, int64_t l, uint64_t 
   if (st == 2) {  // A·Q = 0: λ = 0, U = Q[:, :k] (DESIGN.md reading)
     const size_t mark = ar.off;
     double* sign = ar.get<double>(k);
-    double* side = ar.get<double>(n * k);
-    RPCA_CUDA(cudaMemcpy2DAsync(side, k * 8, Q, l * 8, k * 8, n, cudaMemcpyDeviceToDevice, c.stream));
-    column_signs(c, side, n, K, k, sign, ar);
-    scale_cast(c, side, n, K, sign, Ud, ldu, odt);
+    double* side = ar.get<double>(ml * k);
+    RPCA_CUDA(cudaMemcpy2DAsync(side, k * 8, Qfin, l * 8, k * 8, ml, cudaMemcpyDeviceToDevice, c.stream));
+    signs(side, sign);
+    scale_cast(c, side, ml, K, sign, Ud, ldu, odt);
     RPCA_CUDA(cudaMemsetAsync(Ld, 0, (size_t)k * osz, c.stream));
     ar.off = mark;
   }
   if (out_host) {
-    RPCA_CUDA(cudaMemcpyAsync(U, Ud, (size_t)n * ldu * osz, cudaMemcpyDeviceToHost, c.stream));
+    RPCA_CUDA(cudaMemcpyAsync(U, Ud, (size_t)ml * ldu * osz, cudaMemcpyDeviceToHost, c.stream));
     RPCA_CUDA(cudaMemcpyAsync(lam, Ld, (size_t)k * osz, cudaMemcpyDeviceToHost, c.stream));
   }
   sync_status(c);
 }
 
 // ============================================================ rpca_diffsnorm
+// Row-sharded: x, z (length n) are replicated, y (length m) and U are this
+// rank's rows; z — linear in y — is all-reduced once per iteration.
 void diffsnorm(Ctx& c, const rpca_mat* Am, int raw, const double* U, int64_t ldu, const double* S, const double* V,
                int64_t ldv, int64_t k, int its, uint64_t seed, double* out) {
   validate_mat(Am);
-  check_single_gpu(c, Am);
+  const bool sh = check_shard(c, Am);
   RPCA_REQUIRE(k >= 0 && its >= 1 && out, RPCA_E_SHAPE, "bad k/its/out");
   RPCA_REQUIRE(k == 0 || (U && S && V && ldu >= k && ldv >= k), RPCA_E_ARG, "bad factors");
-  const int64_t m = Am->m, n = Am->n;
+  const int64_t m = Am->m, n = Am->n, ml = Am->m_local;
   const MatV probe = probe_of(Am);
   Sizer sz;
   sz.add<char>(host_copy_bytes(Am));
-  sz.add<double>(2 * n + m + n + k + 64);
-  size_t scratch = op_ws(c, probe, 1) + (size_t)(cdiv(std::max(m, n), 8192) + 2) * (n + 64) * 8;
+  sz.add<double>(2 * n + ml + n + k + 64);
+  size_t scratch = op_ws(c, probe, 1) + (size_t)(cdiv(std::max(ml, n), 8192) + 2) * (n + 64) * 8;
   ensure_transpose(c, Am);
   Arena ar = c.arena(sz.total + scratch + 65536);
   if (!c.status_host) RPCA_CUDA(cudaMallocHost(&c.status_host, 64));
   KeyHasher kh;
-  kh << 3 << *Am << raw << U << ldu << S << V << ldv << k << its << seed << c.ws << c.tcache.mem;
+  kh << 3 << *Am << raw << U << ldu << S << V << ldv << k << its << seed << c.ws << c.tcache.mem << c.comm;
   double* x = ar.get<double>(n);
   double* z = ar.get<double>(n);
-  double* y = ar.get<double>(m);
+  double* y = ar.get<double>(ml);
   double* cmean = ar.get<double>(n);
   double* t = ar.get<double>(std::max<int64_t>(k, 1));
   double* sc = ar.get<double>(8);  // [0] nz2, [1] est, [2] scratch
   int* done = ar.get<int>(4);
-  execute(c, kh.h, Am->location == RPCA_DEVICE, [&] {
+  execute(c, kh.h, Am->location == RPCA_DEVICE && graphable_comm(c), [&] {
     const MatV dA = device_view(c, Am, ar);
     if (!raw) {
       const size_t mark = ar.off;
-      colmeans(c, dA, m, cmean, ar);
+      colmeans(c, dA, m, cmean, ar, sh);
       ar.off = mark;
     }
     const double* cm = raw ? nullptr : cmean;
@@ -683,14 +750,15 @@ void diffsnorm(Ctx& c, const rpca_mat* Am, int raw, const double* U, int64_t ldu
       if (k > 0) {                       // y −= U (S ⊙ (Vᵀx))
         weighted_colsum(c, x, V, n, (int)k, t, ar, ldv);
         hadamard(c, t, S, (int)k);
-        rank_k_sub(c, y, U, ldu, t, m, (int)k);
+        rank_k_sub(c, y, U, ldu, t, ml, (int)k);
       }
       apply_aty(c, dA, cm, y, 1, z, ar);  // z = Aᵀ y [− cᵀ (1ᵀy)]
       if (k > 0) {                        // z −= V (S ⊙ (Uᵀy))
-        weighted_colsum(c, y, U, m, (int)k, t, ar, ldu);
+        weighted_colsum(c, y, U, ml, (int)k, t, ar, ldu);
         hadamard(c, t, S, (int)k);
         rank_k_sub(c, z, V, ldv, t, n, (int)k);
       }
+      if (sh) allreduce_sum(c, z, n);
       weighted_colsum(c, z, z, n, 1, sc, ar);  // ‖z‖²
       power_step(c, sc, z, x, n, sc + 1, done);
       ar.off = mark;

@@ -111,7 +111,9 @@ inline void count_launch(Ctx& c, int n = 1, const char* name = "misc") {
 
 // ---------------------------------------------------------------- kernels
 // omega.cu
-void omega(Ctx& c, uint64_t seed, uint32_t sid, int64_t rows, int64_t cols, int dist, int round32, double* out);
+// rows [row0, row0+rows) of the rows×cols Ω of PAPER.md (eq. i1), row-major
+void omega(Ctx& c, uint64_t seed, uint32_t sid, int64_t rows, int64_t cols, int dist, int round32, double* out,
+           int64_t row0 = 0);
 
 // thin.cu — small kernels on thin blocks
 // Packed operand layouts for the DMMA kernels (see dense_ax.cu / dense_aty.cu)
@@ -130,6 +132,9 @@ void thin_gemm(Ctx& c, const double* In, int64_t rows, int l, const double* W, i
                void* Out, int64_t ldo, int out_dtype);
 // sign[j] = sign of the largest-|·| entry of column j of V (rows×k), lowest index on ties
 void column_signs(Ctx& c, const double* V, int64_t rows, int k, int64_t ldv, double* sign, Arena& ar);
+// same rule over a V whose rows [row0, row0+rows) are this rank's shard
+void column_signs_sharded(Ctx& c, const double* V, int64_t rows, int64_t row0, int k, int64_t ldv, double* sign,
+                          Arena& ar);
 void copy_cast(Ctx& c, const double* src, void* dst, int64_t count, int dtype);
 // dst (rows×k, ld ldd, dtype) = src (rows×k, ld k) · diag(sign)   (sign may be NULL)
 void scale_cast(Ctx& c, const double* src, int64_t rows, int k, const double* sign, void* dst, int64_t ldd, int dtype);
@@ -177,6 +182,8 @@ void aty_reduce_partials(Ctx& c, const double* part, int64_t U, int64_t P, int64
 // tslu.cu
 size_t lu_ws_bytes(int64_t m, int l);
 void lu_renorm(Ctx& c, double* Y, int64_t m, int l, double* U_out, int64_t* piv_out, Arena& ar);
+// row shard [row0, row0+m) of a matrix distributed over the context's communicator
+void lu_renorm_sharded(Ctx& c, double* Y, int64_t m, int64_t row0, int l, double* U_out, Arena& ar);
 
 // tsqr.cu
 size_t qr_ws_bytes(int64_t m, int l);
@@ -186,6 +193,7 @@ void qr(Ctx& c, double* Y, int64_t m, int l, double* R_out, Arena& ar);
 size_t orth_ws_bytes(int64_t m, int l);
 size_t orth_ws_bytes(Ctx& c, int64_t m, int l);
 void orthonormalize(Ctx& c, double* Y, int64_t m, int l, double* R_out, Arena& ar);
+void orthonormalize_sharded(Ctx& c, double* Y, int64_t m, int64_t row0, int l, double* R_out, Arena& ar);
 
 // small.cu — one-CTA l×l kernels
 // R (l×l) → Jacobi: R·W = Vr·diag(sigma); sigma sorted, Vr completed.

@@ -27,11 +27,14 @@ __device__ __forceinline__ void philox_round(uint32_t& c0, uint32_t& c1, uint32_
   c3 = lo0;
 }
 
-__global__ void omega_kernel(uint64_t seed, uint32_t sid, int64_t total, int dist, int round32,
+// elements [e0, e0 + total) of the row-major Ω stream (e = i·l + j); pair p
+// covers elements 2p and 2p+1
+__global__ void omega_kernel(uint64_t seed, uint32_t sid, int64_t e0, int64_t total, int dist, int round32,
                              double* __restrict__ out) {
-  const int64_t calls = (total + 1) >> 1;
+  const int64_t p0 = e0 >> 1, calls = ((e0 + total + 1) >> 1) - p0;
   const uint32_t key0 = static_cast<uint32_t>(seed), key1 = static_cast<uint32_t>(seed >> 32);
-  for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < calls; p += (int64_t)gridDim.x * blockDim.x) {
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < calls; q += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t p = p0 + q;
     uint32_t c0 = static_cast<uint32_t>(p), c1 = static_cast<uint32_t>(static_cast<uint64_t>(p) >> 32), c2 = 0u,
              c3 = sid;
     uint32_t k0 = key0, k1 = key1;
@@ -61,11 +64,11 @@ __global__ void omega_kernel(uint64_t seed, uint32_t sid, int64_t total, int dis
       v0 = static_cast<double>(static_cast<float>(v0));
       v1 = static_cast<double>(static_cast<float>(v1));
     }
-    const int64_t e = p << 1;
-    if (e + 1 < total && ((reinterpret_cast<uintptr_t>(out) & 15u) == 0)) {
+    const int64_t e = (p << 1) - e0;  // local index of element 2p
+    if (e >= 0 && e + 1 < total && ((reinterpret_cast<uintptr_t>(out + e) & 15u) == 0)) {
       *reinterpret_cast<double2*>(out + e) = make_double2(v0, v1);
     } else {
-      out[e] = v0;
+      if (e >= 0) out[e] = v0;
       if (e + 1 < total) out[e + 1] = v1;
     }
   }
@@ -73,14 +76,15 @@ __global__ void omega_kernel(uint64_t seed, uint32_t sid, int64_t total, int dis
 
 }  // namespace
 
-void omega(Ctx& c, uint64_t seed, uint32_t sid, int64_t rows, int64_t cols, int dist, int round32, double* out) {
-  const int64_t total = rows * cols;
+void omega(Ctx& c, uint64_t seed, uint32_t sid, int64_t rows, int64_t cols, int dist, int round32, double* out,
+           int64_t row0) {
+  const int64_t total = rows * cols, e0 = row0 * cols;
   if (total <= 0) return;
-  const int64_t calls = (total + 1) / 2;
+  const int64_t calls = ((e0 + total + 1) >> 1) - (e0 >> 1);
   int64_t blocks = cdiv(calls, 256);
   const int64_t cap = (int64_t)c.num_sms * 8;
   if (blocks > cap) blocks = cap;
-  omega_kernel<<<(unsigned)blocks, 256, 0, c.stream>>>(seed, sid, total, dist, round32, out);
+  omega_kernel<<<(unsigned)blocks, 256, 0, c.stream>>>(seed, sid, e0, total, dist, round32, out);
   RPCA_CHECK_LAUNCH();
   count_launch(c, 1, "omega");
 }

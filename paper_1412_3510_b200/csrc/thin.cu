@@ -4,7 +4,7 @@
 // (PAPER.md:428-429), the lift U = Q·W of eq. (i4) and
 // the sign convention of DESIGN.md reading Q10.  All HBM-bound; every
 // reduction runs in a fixed order (fixed row chunks, ascending).
-#include "internal.cuh"
+#include "comm.cuh"
 
 namespace rpca {
 namespace {
@@ -194,6 +194,36 @@ __global__ void argmax_final(const double* __restrict__ V, int64_t ldv, const do
   sign[j] = (bi != INT64_MAX && V[bi * ldv + j] < 0.0) ? -1.0 : 1.0;
 }
 
+// Row-sharded variant, stage 1: this shard's winner of column j as the triple
+// (|v|, global row, sign) — the row index is exact as a double below 2^53
+__global__ void argmax_local_triple(const double* __restrict__ V, int64_t ldv, const double* __restrict__ pv,
+                                    const int64_t* __restrict__ pi, int64_t nparts, int k, int64_t row0,
+                                    double* __restrict__ trip) {
+  const int j = threadIdx.x;
+  if (j >= k) return;
+  double bv = -1.0;
+  int64_t bi = INT64_MAX;
+  for (int64_t b = 0; b < nparts; ++b) {
+    if (better(pv[b * k + j], pi[b * k + j], bv, bi)) { bv = pv[b * k + j]; bi = pi[b * k + j]; }
+  }
+  trip[3 * j] = bv;
+  trip[3 * j + 1] = bi == INT64_MAX ? 9.0e15 : (double)(row0 + bi);
+  trip[3 * j + 2] = (bi != INT64_MAX && V[bi * ldv + j] < 0.0) ? -1.0 : 1.0;
+}
+
+// stage 2 (after the all-gather): the best triple over the ranks, same rule
+__global__ void argmax_ranks(const double* __restrict__ trip, int P, int k, double* __restrict__ sign) {
+  const int j = threadIdx.x;
+  if (j >= k) return;
+  double bv = -1.0, bs = 1.0;
+  int64_t bi = INT64_MAX;
+  for (int r = 0; r < P; ++r) {
+    const double* t = trip + ((size_t)r * k + j) * 3;
+    if (better(t[0], (int64_t)t[1], bv, bi)) { bv = t[0]; bi = (int64_t)t[1]; bs = t[2]; }
+  }
+  sign[j] = bs;
+}
+
 template <class T>
 __global__ void copy_cast_kernel(const double* __restrict__ s, T* __restrict__ d, int64_t count) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count; i += (int64_t)gridDim.x * blockDim.x)
@@ -355,6 +385,24 @@ void column_signs(Ctx& c, const double* V, int64_t rows, int k, int64_t ldv, dou
   argmax_final<<<1, 64, 0, c.stream>>>(V, ldv, pv, pi, nparts, k, sign);
   RPCA_CHECK_LAUNCH();
   count_launch(c, 2);
+}
+
+void column_signs_sharded(Ctx& c, const double* V, int64_t rows, int64_t row0, int k, int64_t ldv, double* sign,
+                          Arena& ar) {
+  const int P = comm_size(c);
+  const int64_t nparts = std::max<int64_t>(1, cdiv(rows, kChunk));
+  double* pv = ar.get<double>(nparts * k);
+  int64_t* pi = ar.get<int64_t>(nparts * k);
+  double* trip = ar.get<double>(3 * (size_t)k);
+  double* all = ar.get<double>(3 * (size_t)k * P);
+  argmax_partial<<<dim3((unsigned)nparts, (unsigned)k), 256, 0, c.stream>>>(V, rows, k, ldv, pv, pi);
+  RPCA_CHECK_LAUNCH();
+  argmax_local_triple<<<1, 64, 0, c.stream>>>(V, ldv, pv, pi, nparts, k, row0, trip);
+  RPCA_CHECK_LAUNCH();
+  allgather_bytes(c, trip, all, 3 * sizeof(double) * k);
+  argmax_ranks<<<1, 64, 0, c.stream>>>(all, P, k, sign);
+  RPCA_CHECK_LAUNCH();
+  count_launch(c, 3);
 }
 
 

@@ -24,7 +24,7 @@
 // costs one __syncthreads.  Pivot: largest |·| among active rows, lowest
 // original row on ties.  Tournament pivots differ from plain GEPP, so L differs
 // from the oracle's L but span(L) = span(Y) whenever U is nonsingular.
-#include "internal.cuh"
+#include "comm.cuh"
 
 namespace rpca {
 namespace {
@@ -130,18 +130,24 @@ __global__ void __launch_bounds__(kThreads) lu_select_kernel(const double* __res
                                                              int64_t n_in, int G, int64_t* __restrict__ cand_out,
                                                              int final_, double* __restrict__ U,
                                                              double* __restrict__ Lp, int64_t* __restrict__ piv_out,
-                                                             double* __restrict__ M) {
+                                                             double* __restrict__ M,
+                                                             const double* __restrict__ rows_in,
+                                                             double* __restrict__ rows_out) {
+  // leaf: 1 = contiguous rows of Y; 0 = candidate ids into Y; 2 = candidate
+  // rows given directly (rows_in, one l-vector per slot; ids are global rows
+  // — the all-gathered local winners of a row-sharded LU)
   extern __shared__ double sm[];
   __shared__ Cand slot[2][kWarps];
   __shared__ int piv[kMaxL];
   __shared__ int nrows_s;
-  const int cap = leaf ? (int)leaf_rows : G * l;
+  const int cap = leaf == 1 ? (int)leaf_rows : G * l;
   const int ldw = l | 1;
   double* W = sm;
   int64_t* ids = reinterpret_cast<int64_t*>(W + (size_t)cap * ldw);
+  int* slot_of = reinterpret_cast<int*>(ids + cap);
   const int tid = threadIdx.x;
 
-  if (leaf) {
+  if (leaf == 1) {
     const int64_t r0 = (int64_t)blockIdx.x * leaf_rows;
     if (tid == 0) nrows_s = (int)imin64(leaf_rows, m - r0);
     for (int r = tid; r < cap; r += kThreads) ids[r] = r0 + r;
@@ -153,7 +159,11 @@ __global__ void __launch_bounds__(kThreads) lu_select_kernel(const double* __res
       for (int64_t s = s0; s < s1; s += 32) {
         const int64_t id = (s + tid < s1) ? cand_in[s + tid] : -1;
         const unsigned mask = __ballot_sync(0xffffffffu, id >= 0);
-        if (id >= 0) ids[base + __popc(mask & ((1u << tid) - 1u))] = id;
+        if (id >= 0) {
+          const int pos = base + __popc(mask & ((1u << tid) - 1u));
+          ids[pos] = id;
+          slot_of[pos] = (int)(s + tid - s0);
+        }
         base += __popc(mask);
       }
       if (tid == 0) nrows_s = base;
@@ -163,12 +173,19 @@ __global__ void __launch_bounds__(kThreads) lu_select_kernel(const double* __res
   const int rows = nrows_s;
   for (int idx = tid; idx < rows * l; idx += kThreads) {
     const int r = idx / l, t = idx - r * l;
-    W[r * ldw + t] = Y[ids[r] * l + t];
+    W[r * ldw + t] = leaf == 2 ? rows_in[((int64_t)blockIdx.x * G * l + slot_of[r]) * l + t] : Y[ids[r] * l + t];
   }
   __syncthreads();
   const int steps = min(rows, l);
   gepp(W, ldw, ids, rows, l, steps, piv, slot);
   for (int j = tid; j < l; j += kThreads) cand_out[(int64_t)blockIdx.x * l + j] = j < steps ? ids[piv[j]] : -1;
+  if (rows_out) {  // direct mode: forward the winners' original rows to the next level
+    for (int idx = tid; idx < l * l; idx += kThreads) {
+      const int j = idx / l, t = idx - j * l;
+      rows_out[(int64_t)blockIdx.x * l * l + idx] =
+          j < steps ? rows_in[((int64_t)blockIdx.x * G * l + slot_of[piv[j]]) * l + t] : 0.0;
+    }
+  }
   if (!final_) return;
   __syncthreads();
   for (int idx = tid; idx < l * l; idx += kThreads) {
@@ -182,7 +199,7 @@ __global__ void __launch_bounds__(kThreads) lu_select_kernel(const double* __res
   // M = U⁻¹ with the zero-pivot rule (a zero U_ii zeroes row i of M: x_i = 0
   // for every input of the row substitution x·U = y, reading Q3): column j by
   // one warp, M[j][j] = 1/U_jj, M[i][j] = −(Σ_{t=i+1..j} U_it M_tj)/U_ii.
-  double* Ms = reinterpret_cast<double*>(ids + cap);  // l×l after the row ids
+  double* Ms = reinterpret_cast<double*>(ids + cap) + (cap + 1) / 2;  // l×l after ids and slot_of
   const int lane = tid & 31, warp = tid >> 5;
   for (int j = warp; j < l; j += kWarps) {
     for (int i = lane; i < l; i += 32) Ms[i * l + j] = 0.0;
@@ -200,12 +217,27 @@ __global__ void __launch_bounds__(kThreads) lu_select_kernel(const double* __res
   for (int idx = tid; idx < l * l; idx += kThreads) M[idx] = Ms[idx];
 }
 
-// Y[piv[j]] ← Lp[j] (the pivot rows' exact unit-lower rows)
-__global__ void pivot_rows_kernel(double* __restrict__ Y, int l, const double* __restrict__ Lp,
-                                  const int64_t* __restrict__ piv) {
+// Y[piv[j] − row0] ← Lp[j] for the pivot rows this shard holds (their exact
+// unit-lower rows)
+__global__ void pivot_rows_kernel(double* __restrict__ Y, int64_t m, int64_t row0, int l,
+                                  const double* __restrict__ Lp, const int64_t* __restrict__ piv) {
   for (int idx = threadIdx.x; idx < l * l; idx += blockDim.x) {
     const int j = idx / l, t = idx - j * l;
-    Y[piv[j] * l + t] = Lp[idx];
+    const int64_t r = piv[j] - row0;
+    if (r >= 0 && r < m) Y[r * l + t] = Lp[idx];
+  }
+}
+
+// rows_out[j] = Y[cand[j]] (l-vectors), gid[j] = row0 + cand[j] (−1 kept) — the
+// local tournament winners packaged for the all-gather of a sharded LU
+__global__ void pack_candidates_kernel(const double* __restrict__ Y, int l, int64_t row0,
+                                       const int64_t* __restrict__ cand, double* __restrict__ rows_out,
+                                       int64_t* __restrict__ gid) {
+  for (int idx = threadIdx.x; idx < l * l; idx += blockDim.x) {
+    const int j = idx / l, t = idx - j * l;
+    const int64_t r = cand[j];
+    rows_out[idx] = r >= 0 ? Y[r * l + t] : 0.0;
+    if (t == 0) gid[j] = r >= 0 ? row0 + r : -1;
   }
 }
 
@@ -217,17 +249,58 @@ int group_for(int l) {
   return std::max(2, std::min(32, max_rows / l));
 }
 
-size_t select_smem(int cap, int l) { return (size_t)cap * (l | 1) * 8 + (size_t)cap * 8 + (size_t)l * l * 8 + 16; }
+size_t select_smem(int cap, int l) {
+  return (size_t)cap * (l | 1) * 8 + (size_t)cap * 8 + (size_t)(cap + 1) / 2 * 8 + (size_t)l * l * 8 + 16;
+}
 
 void select(Ctx& c, unsigned grid, const double* Y, int64_t m, int l, int leaf, const int64_t* cin, int64_t n_in,
-            int G, int64_t* cout, int final_, double* U, double* Lp, int64_t* piv, double* M) {
-  const int cap = leaf ? kLeafRows : G * l;
+            int G, int64_t* cout, int final_, double* U, double* Lp, int64_t* piv, double* M,
+            const double* rows_in = nullptr, double* rows_out = nullptr) {
+  const int cap = leaf == 1 ? kLeafRows : G * l;
   ensure_smem((const void*)lu_select_kernel, 220 * 1024);
   const size_t smem = select_smem(cap, l) - (final_ ? 0 : (size_t)l * l * 8);
-  lu_select_kernel<<<grid, kThreads, smem, c.stream>>>(Y, m, l, leaf, kLeafRows, cin, n_in, G, cout,
-                                                                     final_, U, Lp, piv, M);
+  lu_select_kernel<<<grid, kThreads, smem, c.stream>>>(Y, m, l, leaf, kLeafRows, cin, n_in, G, cout, final_, U, Lp,
+                                                       piv, M, rows_in, rows_out);
   RPCA_CHECK_LAUNCH();
-  count_launch(c, 1, leaf ? "lu_leaf" : "lu_tree");
+  count_launch(c, 1, leaf == 1 ? "lu_leaf" : "lu_tree");
+}
+
+// Tournament over rows [0, m) of Y down to one candidate set; returns the set
+// (l entries, local row indices, −1 padded).  If `finalize`, the last level
+// also writes U, Lp, piv and M.
+int64_t* tournament(Ctx& c, const double* Y, int64_t m, int l, bool finalize, double* U, double* Lp, int64_t* piv,
+                    double* M, Arena& ar) {
+  const int G = group_for(l);
+  const int64_t nblk = std::max<int64_t>(1, cdiv(m, kLeafRows));
+  int64_t* ca = ar.get<int64_t>(nblk * l);
+  int64_t* cb = ar.get<int64_t>(nblk * l);
+  if (m == 0) {
+    RPCA_CUDA(cudaMemsetAsync(ca, 0xFF, sizeof(int64_t) * l, c.stream));  // no local rows: all −1
+    return ca;
+  }
+  select(c, (unsigned)nblk, Y, m, l, 1, nullptr, 0, G, ca, finalize && nblk == 1, U, Lp, piv, M);
+  int64_t n = nblk;
+  while (n > 1) {
+    const int64_t ng = cdiv(n, G);
+    select(c, (unsigned)ng, Y, m, l, 0, ca, n, G, cb, finalize && ng == 1, U, Lp, piv, M);
+    std::swap(ca, cb);
+    n = ng;
+  }
+  return ca;
+}
+
+// L = Y·M on the fp64 tensor-core pass kernel (in place: every output row is
+// written only after all of its own K-chunks were read), then the pivot rows
+// this shard holds get their exact unit-lower rows
+void apply_l(Ctx& c, double* Y, int64_t m, int64_t row0, int l, const double* M, const double* Lp,
+             const int64_t* piv, Arena& ar) {
+  if (m > 0) {
+    TagScope ts(c, "lu_apply");
+    dense_ax(c, DenseA{Y, RPCA_F64, m, l, l}, M, l, Y, ar);
+  }
+  pivot_rows_kernel<<<1, 256, 0, c.stream>>>(Y, m, row0, l, Lp, piv);
+  RPCA_CHECK_LAUNCH();
+  count_launch(c, 1, "lu_pivot_rows");
 }
 
 }  // namespace
@@ -235,43 +308,68 @@ void select(Ctx& c, unsigned grid, const double* Y, int64_t m, int l, int leaf, 
 size_t lu_ws_bytes(int64_t m, int l) {
   Sizer s;
   s.add<char>(ax_ws_bytes(DenseA{nullptr, RPCA_F64, m, l, l}, l) + 4096);
-  const int64_t nblk = cdiv(m, kLeafRows);
+  const int64_t nblk = std::max<int64_t>(1, cdiv(m, kLeafRows));
   s.add<int64_t>(nblk * l);
   s.add<int64_t>(nblk * l);
   s.add<double>(4 * (size_t)l * l);
   s.add<int64_t>(l);
+  s.add<double>((size_t)2 * kMaxL * (size_t)(kMaxL + 1) * 64 + 2 * kMaxL * kMaxL);  // sharded: gathered rows + ids
   return s.total;
 }
 
 void lu_renorm(Ctx& c, double* Y, int64_t m, int l, double* U_out, int64_t* piv_out, Arena& ar) {
   RPCA_REQUIRE(l >= 1 && l <= kMaxL && m >= l, RPCA_E_SHAPE, "lu_renorm: need 1 ≤ l ≤ %d and m ≥ l", kMaxL);
-  const int G = group_for(l);
-  const int64_t nblk = cdiv(m, kLeafRows);
-  int64_t* ca = ar.get<int64_t>(nblk * l);
-  int64_t* cb = ar.get<int64_t>(nblk * l);
   double* U = U_out ? U_out : ar.get<double>((size_t)l * l);
   double* Lp = ar.get<double>((size_t)l * l);
   int64_t* piv = ar.get<int64_t>(l);
   double* M = ar.get<double>((size_t)l * l);
-  select(c, (unsigned)nblk, Y, m, l, 1, nullptr, 0, G, ca, nblk == 1, U, Lp, piv, M);
-  int64_t n = nblk;
-  while (n > 1) {
+  const size_t mark = ar.off;
+  tournament(c, Y, m, l, true, U, Lp, piv, M, ar);
+  ar.off = mark;
+  apply_l(c, Y, m, 0, l, M, Lp, piv, ar);
+  if (piv_out) RPCA_CUDA(cudaMemcpyAsync(piv_out, piv, sizeof(int64_t) * l, cudaMemcpyDeviceToDevice, c.stream));
+}
+
+// Row-sharded LU: every rank runs the tournament on its rows
+// [row0, row0+m); the winners (l rows + their global ids) are all-gathered and
+// every rank runs the final GEPP on the same P·l rows — identical U, pivots and
+// M everywhere — then applies L = Y·M to its own rows.
+void lu_renorm_sharded(Ctx& c, double* Y, int64_t m, int64_t row0, int l, double* U_out, Arena& ar) {
+  RPCA_REQUIRE(l >= 1 && l <= kMaxL && m >= 0, RPCA_E_SHAPE, "lu_renorm: need 1 ≤ l ≤ %d", kMaxL);
+  const int P = comm_size(c);
+  RPCA_REQUIRE(P <= 64, RPCA_E_ARG, "at most 64 ranks");
+  double* U = U_out ? U_out : ar.get<double>((size_t)l * l);
+  double* Lp = ar.get<double>((size_t)l * l);
+  int64_t* piv = ar.get<int64_t>(l);
+  double* M = ar.get<double>((size_t)l * l);
+  double* rows_send = ar.get<double>((size_t)l * l);
+  int64_t* ids_send = ar.get<int64_t>(l);
+  double* rows_a = ar.get<double>((size_t)l * l * P);
+  double* rows_b = ar.get<double>((size_t)l * l * P);
+  int64_t* ids_a = ar.get<int64_t>((size_t)l * P);
+  int64_t* ids_b = ar.get<int64_t>((size_t)l * P);
+  const size_t mark = ar.off;
+  const int64_t* cand = tournament(c, Y, m, l, false, nullptr, nullptr, nullptr, nullptr, ar);
+  pack_candidates_kernel<<<1, 256, 0, c.stream>>>(Y, l, row0, cand, rows_send, ids_send);
+  RPCA_CHECK_LAUNCH();
+  count_launch(c, 1, "lu_pack");
+  ar.off = mark;
+  allgather_bytes(c, rows_send, rows_a, sizeof(double) * l * l);
+  allgather_bytes(c, ids_send, ids_a, sizeof(int64_t) * l);
+  // tournament over the P gathered sets with rows given directly; every rank
+  // runs the same launches on the same bytes, so U, piv and M agree bitwise
+  const int G = group_for(l);
+  int64_t n = P;
+  for (;;) {
     const int64_t ng = cdiv(n, G);
-    select(c, (unsigned)ng, Y, m, l, 0, ca, n, G, cb, ng == 1, U, Lp, piv, M);
-    std::swap(ca, cb);
+    select(c, (unsigned)ng, nullptr, 0, l, 2, ids_a, n, G, ids_b, ng == 1, U, Lp, piv, M, rows_a,
+           ng == 1 ? nullptr : rows_b);
+    if (ng == 1) break;
+    std::swap(rows_a, rows_b);
+    std::swap(ids_a, ids_b);
     n = ng;
   }
-  // L = Y·M on the fp64 tensor-core pass kernel (in place: every output row is
-  // written only after all of its own K-chunks were read), then the pivot rows
-  // get their exact unit-lower rows
-  {
-    TagScope ts(c, "lu_apply");
-    dense_ax(c, DenseA{Y, RPCA_F64, m, l, l}, M, l, Y, ar);
-  }
-  pivot_rows_kernel<<<1, 256, 0, c.stream>>>(Y, l, Lp, piv);
-  RPCA_CHECK_LAUNCH();
-  count_launch(c, 1, "lu_pivot_rows");
-  if (piv_out) RPCA_CUDA(cudaMemcpyAsync(piv_out, piv, sizeof(int64_t) * l, cudaMemcpyDeviceToDevice, c.stream));
+  apply_l(c, Y, m, row0, l, M, Lp, piv, ar);
 }
 
 }  // namespace rpca
