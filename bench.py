@@ -14,6 +14,13 @@ A-streaming pass), timed with CUDA events on the library's stream inside the
 timed region; `cpu_baseline` is the CPU oracle (oracle/, plain C + OpenMP) on
 a bounded row sample of the same workload, extrapolated linearly in m.
 --impl reference times that oracle as the reference arm.
+
+Multi-GPU (torchrun, one rank per GPU, NCCL): A is sharded by rows
+(SURVEY.md §8(e)).  The dense-PCA and CSR configs scale WEAKLY — every rank
+holds one full per-GPU instance of the config as its row block (seed offset
+by rank), so global m = N·m — and `value` stays the whole-job step time (max
+over ranks).  The Nyström config C3 scales STRONGLY: the same n×n matrix, rows
+split uniformly.
 """
 import argparse
 import json
@@ -118,6 +125,30 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.samples)}
 
 
+def plan_shard(cfg, ws, rank):
+    """How rank `rank` of `ws` holds the workload: weak scaling stacks ws
+    per-GPU instances (rank r's seed = base + r) into an (ws·m)-row A; strong
+    scaling (the square Nyström config) splits one matrix's rows uniformly."""
+    if ws == 1:
+        return {"scaling": "weak", "m_total": cfg.m, "row0": 0, "m_local": cfg.m, "seed_offset": 0}
+    if cfg.op == "eigens":
+        pad = -(-cfg.m // ws)
+        row0 = min(cfg.m, rank * pad)
+        return {"scaling": "strong", "m_total": cfg.m, "row0": row0, "m_local": min(pad, cfg.m - row0),
+                "seed_offset": 0}
+    return {"scaling": "weak", "m_total": ws * cfg.m, "row0": rank * cfg.m, "m_local": cfg.m, "seed_offset": rank}
+
+
+def max_over_ranks(x, ws, device):
+    """max of a per-rank float over the process group (identity at ws = 1)."""
+    if ws == 1:
+        return float(x)
+    import torch.distributed as dist
+    t = torch.tensor([float(x)], device=device, dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
 def workload(name):
     cfg = synth.CONFIGS[name]
     return cfg, {
@@ -127,8 +158,14 @@ def workload(name):
     }
 
 
-def make_input(cfg, device, rp=None):
-    A = synth.make(cfg.name, device=device)
+def make_input(cfg, device, rp=None, plan=None):
+    plan = plan or {"seed_offset": 0, "row0": 0, "m_local": cfg.m, "scaling": "weak"}
+    kw = {}
+    if plan["seed_offset"]:
+        kw["seed"] = synth.GEN_SEEDS[cfg.name] + plan["seed_offset"]
+    A = synth.make(cfg.name, device=device, **kw)
+    if plan["scaling"] == "strong" and plan["m_local"] != cfg.m:
+        A = A[plan["row0"]:plan["row0"] + plan["m_local"]].clone()
     torch.cuda.synchronize()
     if cfg.kind == "csr":
         rowptr, colind, vals = A
@@ -152,10 +189,12 @@ def pass_bytes(A, cfg):
     return a_bytes(A) + nnz * 8 * cfg.l + cfg.m * 8 * cfg.l
 
 
-def run_step(rp, cfg, A):
+def run_step(rp, cfg, A, plan=None):
+    sh = {} if plan is None or plan["m_total"] == plan["m_local"] else {"m_total": plan["m_total"],
+                                                                         "row0": plan["row0"]}
     if cfg.op == "eigens":
-        return rp.eigens(A, cfg.k, its=cfg.its, l=cfg.l, seed=0)
-    return rp.pca(A, cfg.k, raw=cfg.raw, its=cfg.its, l=cfg.l, seed=0)
+        return rp.eigens(A, cfg.k, its=cfg.its, l=cfg.l, seed=0, **sh)
+    return rp.pca(A, cfg.k, raw=cfg.raw, its=cfg.its, l=cfg.l, seed=0, **sh)
 
 
 # ------------------------------------------------------------------ CPU oracle
@@ -234,21 +273,24 @@ def main():
     ws, rank, local = dist_env()
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
+    import paper_1412_3510_b200 as rp
     if ws > 1:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=dev)
-    import paper_1412_3510_b200 as rp
+        rp.comm_init_torch()  # the library's own NCCL communicator over the same ranks
 
     cfg, conf = workload(args.config)
-    A = make_input(cfg, dev, rp)
-    abytes = a_bytes(A)
+    plan = plan_shard(cfg, ws, rank)
+    A = make_input(cfg, dev, rp, plan)
+    abytes = a_bytes(A)  # this rank's shard
     pbytes = pass_bytes(A, cfg)
     passes = conf["passes_over_A"]
-    conf.update({"l2": f"A ({abytes / 1e9:.2f} GB) > L2 (126 MB): no flush needed",
-                 "parallelism": f"replicas x{ws}" if ws > 1 else "single GPU"})
+    conf.update({"l2": f"A ({abytes / 1e9:.2f} GB per GPU) > L2 (126 MB): no flush needed",
+                 "parallelism": f"row-sharded dp{ws} ({plan['scaling']} scaling, m_total={plan['m_total']})"
+                 if ws > 1 else "single GPU"})
 
     for _ in range(args.warmup):
-        run_step(rp, cfg, A)
+        run_step(rp, cfg, A, plan)
     torch.cuda.synchronize()
 
     def barrier():
@@ -264,18 +306,13 @@ def main():
     with ClockSampler(local) as clk, rp.profile() as prof:
         e0.record(stream)
         for _ in range(args.steps):
-            run_step(rp, cfg, A)
+            run_step(rp, cfg, A, plan)
         e1.record(stream)
         torch.cuda.synchronize()
     barrier()
     ms_total = e0.elapsed_time(e1)
     launches = rp.launch_count() - launches0
-    t_step = ms_total / 1e3 / args.steps
-    if ws > 1:
-        import torch.distributed as dist
-        t = torch.tensor([t_step], device=dev, dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        t_step = float(t.item())
+    t_step = max_over_ranks(ms_total / 1e3 / args.steps, ws, dev)
 
     # dominant kernel: the A-streaming passes
     hbm, peak_src = peaks()
@@ -291,6 +328,7 @@ def main():
         cnt, tot = dom[1]
         avg_ms = tot / cnt
         achieved = pbytes / (avg_ms / 1e3) / 1e9
+        achieved = max_over_ranks(-achieved, ws, dev) * -1.0  # slowest rank
         roof = {"bound": "hbm", "kernel": dom[0], "achieved": round(achieved, 1), "peak": hbm, "unit": "GB/s",
                 "frac": round(achieved / hbm, 4), "traffic": None, "peak_source": peak_src,
                 "algorithmic_bytes_per_launch": pbytes, "avg_launch_ms": round(avg_ms, 5),
@@ -298,22 +336,27 @@ def main():
         all_pass_ms = sum(v[1] for v in passes_k.values()) / args.steps
         roof["all_passes"] = {"launches_per_step": sum(v[0] for v in passes_k.values()) // args.steps,
                               "gbs_per_pass": round(abytes * passes / (all_pass_ms / 1e3) / 1e9, 1)}
+        if ws > 1:  # whole-job A-streaming rate: all shards' bytes over the step time
+            roof["aggregate"] = {"gbs_per_pass_step": round(abytes * ws * passes / t_step / 1e9, 1),
+                                 "peak": hbm * ws, "frac": round(abytes * passes / t_step / 1e9 / hbm, 4)}
     breakdown = {k: {"launches_per_step": v[0] / args.steps, "ms_per_step": round(v[1] / args.steps, 5)}
                  for k, v in sorted(kern.items(), key=lambda kv: -kv[1][1])}
 
     e2e = None
-    if not args.no_e2e and rank == 0 and isinstance(A, torch.Tensor):
+    if not args.no_e2e and isinstance(A, torch.Tensor):  # every rank (the call has collectives)
         Ah = A.cpu().pin_memory()
-        run_step(rp, cfg, Ah)  # warm
+        run_step(rp, cfg, Ah, plan)  # warm
         torch.cuda.synchronize()
+        barrier()
         t0 = time.perf_counter()
         ne = max(3, min(args.steps, 10))
         for _ in range(ne):
-            out = run_step(rp, cfg, Ah)
-        te = (time.perf_counter() - t0) / ne
+            out = run_step(rp, cfg, Ah, plan)
+        te = max_over_ranks((time.perf_counter() - t0) / ne, ws, dev)
         d2h = sum(o.numel() * o.element_size() for o in out)
-        e2e = {"value": te, "unit": "s", "h2d_bytes_per_step": abytes, "d2h_bytes_per_step": d2h,
-               "note": "host-pinned A copied H2D and U,S,V copied D2H inside each rpca_pca call; host wall clock"}
+        e2e = {"value": te, "unit": "s", "h2d_bytes_per_step": abytes * ws, "d2h_bytes_per_step": d2h * ws,
+               "note": "host-pinned A (shard) copied H2D and the factors copied D2H inside each library call; "
+                       "host wall clock, max over ranks"}
         del Ah
 
     cpu = None
@@ -323,12 +366,14 @@ def main():
     if rank == 0:
         line = {"metric": "rank-k PCA wall time (s)", "value": t_step, "unit": "s", "n_gpus": ws,
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_step * 1e3,
-                "higher_is_better": False, "scaling": "weak", "vs_baseline": None,
+                "higher_is_better": False, "scaling": plan["scaling"], "vs_baseline": None,
                 "dtype": "f64" if A.dtype == torch.float64 else "f32",
                 "a_bytes": abytes, "data": "synthetic", "config": conf,
                 "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
                 "clocks": clk.summary(), "kernels": breakdown,
                 "roofline_time_s": abytes * passes / (hbm * 1e9)}
+        if ws > 1:
+            line["a_bytes_total"] = abytes * ws
         print(json.dumps(line), flush=True)
     if ws > 1:
         import torch.distributed as dist

@@ -217,7 +217,7 @@ void comm_destroy(Ctx& c) {
 }
 
 void allgather_bytes(Ctx& c, const void* send, void* recv, size_t bytes_per_rank) {
-  if (!c.comm || c.comm->nranks == 1) {
+  if (!c.comm) {
     if (send != recv) RPCA_CUDA(cudaMemcpyAsync(recv, send, bytes_per_rank, cudaMemcpyDeviceToDevice, c.stream));
     return;
   }

@@ -29,8 +29,10 @@ void virtual_group_destroy(void* group);
 void comm_destroy(Ctx& c);
 
 inline int comm_size(const Ctx& c) { return c.comm ? c.comm->nranks : 1; }
+// With a communicator attached the collectives always run (a 1-rank NCCL
+// communicator exercises the same calls as P ranks).
 inline void allreduce_sum(Ctx& c, double* buf, size_t count) {
-  if (c.comm && c.comm->nranks > 1 && count) c.comm->allreduce_sum(c, buf, count);
+  if (c.comm && count) c.comm->allreduce_sum(c, buf, count);
 }
 void allgather_bytes(Ctx& c, const void* send, void* recv, size_t bytes_per_rank);
 

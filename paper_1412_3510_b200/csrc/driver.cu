@@ -380,12 +380,13 @@ void renorm_qr(Ctx& c, const Blk& Y, int l, double* R, Arena& ar) {
   ar.off = mark;
 }
 
-// Without a multi-rank communicator A must be whole; with one, every rank
-// holds a non-empty row shard.  Returns whether the call runs sharded.
+// Without a communicator A must be whole; with one (any size), every rank
+// holds a non-empty row shard and the sharded schedule runs.  Returns whether
+// the call runs sharded.
 bool check_shard(Ctx& c, const rpca_mat* A) {
-  if (comm_size(c) <= 1) {
+  if (!c.comm) {
     RPCA_REQUIRE(A->row0 == 0 && A->m_local == A->m, RPCA_E_SHAPE,
-                 "row shard given but no multi-rank communicator (rpca_comm_init)");
+                 "row shard given but no communicator (rpca_comm_init)");
     return false;
   }
   RPCA_REQUIRE(A->m_local >= 1, RPCA_E_SHAPE, "sharded call: every rank needs ≥ 1 row (m_local = 0)");

@@ -239,3 +239,48 @@ def test_shard_errors():
         return None
 
     assert run_ranks(2, bad_eigens) == [rp.E_SHAPE, rp.E_SHAPE]
+
+
+@pytest.mark.parametrize("graph", ["0", "1"])
+def test_nccl_single_rank_runs_sharded_schedule(graph, monkeypatch):
+    """A 1-rank NCCL communicator drives the whole sharded schedule through real
+    ncclAllReduce / ncclAllGather calls (with RPCA_NCCL_GRAPH=1 also inside the
+    captured CUDA graph, replayed on the second call)."""
+    monkeypatch.setenv("RPCA_NCCL_GRAPH", graph)
+    A = synth.make_c1(device=dev())
+    C3 = synth.make_c3(n=1024, device=dev())
+    out = {}
+
+    def body():
+        torch.cuda.set_device(0)
+        rp.comm_init(1, 0, rp.comm_unique_id())
+        try:
+            r1 = rp.pca(A, 10, its=2, l=12, seed=0, m_total=1000, row0=0)
+            r2 = rp.pca(A, 10, its=2, l=12, seed=0, m_total=1000, row0=0)
+            e1 = rp.eigens(C3, 20, its=2, l=22, seed=0, m_total=1024, row0=0)
+            e2 = rp.eigens(C3, 20, its=2, l=22, seed=0, m_total=1024, row0=0)
+            d = rp.diffsnorm(A, *r1, its=20, seed=1, m_total=1000, row0=0)
+            torch.cuda.synchronize()
+            out.update(r1=r1, r2=r2, e1=e1, e2=e2, d=d)
+        finally:
+            rp.release_context()
+
+    th = threading.Thread(target=lambda: out.update(err=None) if body() is None else None, daemon=True)
+    th.start()
+    th.join(300)
+    assert not th.is_alive()
+    assert "r1" in out, "NCCL single-rank run failed"
+    U, S, V = [t.cpu().numpy() for t in out["r1"]]
+    compare(U, S, V, oracle.pca(A.cpu().numpy(), 10, its=2, l=12, seed=0), 10)
+    assert all(torch.equal(a, b) for a, b in zip(out["r1"], out["r2"]))
+    assert all(torch.equal(a, b) for a, b in zip(out["e1"], out["e2"]))
+    Uo, lo = oracle.eigens(C3.cpu().numpy(), 20, its=2, l=22, seed=0)
+    assert np.max(np.abs(out["e1"][1].cpu().numpy() - lo) / lo) < 1e-10
+    ref = oracle.diffsnorm(A.cpu().numpy(), U, S, V, its=20, seed=1)
+    assert abs(out["d"] - ref) <= 1e-9 * ref
+
+
+def test_virtual_single_rank():
+    A = synth.make_c1(device=dev())
+    U, S, V = sharded_pca(A, 1, 10, its=2, l=12, seed=0)
+    compare(U, S, V, oracle.pca(A.cpu().numpy(), 10, its=2, l=12, seed=0), 10)
