@@ -265,11 +265,18 @@ def test_nccl_single_rank_runs_sharded_schedule(graph, monkeypatch):
         finally:
             rp.release_context()
 
-    th = threading.Thread(target=lambda: out.update(err=None) if body() is None else None, daemon=True)
+    def run():
+        try:
+            body()
+        except BaseException as e:  # noqa: BLE001 - re-raised below
+            out["err"] = e
+
+    th = threading.Thread(target=run, daemon=True)
     th.start()
     th.join(300)
     assert not th.is_alive()
-    assert "r1" in out, "NCCL single-rank run failed"
+    if out.get("err") is not None:
+        raise out["err"]
     U, S, V = [t.cpu().numpy() for t in out["r1"]]
     compare(U, S, V, oracle.pca(A.cpu().numpy(), 10, its=2, l=12, seed=0), 10)
     assert all(torch.equal(a, b) for a, b in zip(out["r1"], out["r2"]))
