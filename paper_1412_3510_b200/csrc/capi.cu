@@ -251,7 +251,7 @@ rpca_status rpca_lu_renorm(rpca_ctx* c, double* Y, int64_t m, int64_t l, double*
     RPCA_REQUIRE(l >= 1 && l <= rpca::kMaxL && m >= l, RPCA_E_SHAPE, "need 1 ≤ l ≤ 64, m ≥ l");
     DeviceScope ds(c->device);
     rpca::Arena ar = c->arena(rpca::lu_ws_bytes(m, (int)l) + 65536);
-    rpca::lu_renorm(*c, Y, m, (int)l, U, piv, ar);
+    rpca::profiled_step(*c, [&] { rpca::lu_renorm(*c, Y, m, (int)l, U, piv, ar); });
   });
 }
 
@@ -261,7 +261,7 @@ rpca_status rpca_qr(rpca_ctx* c, double* Y, int64_t m, int64_t l, double* R) {
     RPCA_REQUIRE(l >= 1 && l <= rpca::kMaxL && m >= l, RPCA_E_SHAPE, "need 1 ≤ l ≤ 64, m ≥ l");
     DeviceScope ds(c->device);
     rpca::Arena ar = c->arena(rpca::qr_ws_bytes(m, (int)l) + 65536);
-    rpca::qr(*c, Y, m, (int)l, R, ar);
+    rpca::profiled_step(*c, [&] { rpca::qr(*c, Y, m, (int)l, R, ar); });
   });
 }
 

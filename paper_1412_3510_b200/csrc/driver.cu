@@ -11,6 +11,7 @@
 //   rpca_diffsnorm— PAPER.md §4 l.362-371.
 #include <cstdarg>
 #include <cstring>
+#include <functional>
 #include <map>
 #include <mutex>
 #include <string>
@@ -78,6 +79,21 @@ struct KeyHasher {
 };
 
 }  // namespace
+
+// A step API call (rpca_lu_renorm, rpca_qr, …) enqueued directly on the
+// caller's stream: with profiling on, its launch marks are harvested here.
+void profiled_step(Ctx& c, const std::function<void()>& body) {
+  if (!c.prof) {
+    body();
+    return;
+  }
+  c.prof_recs.clear();
+  c.prof_used = 0;
+  prof_mark(c, "start");
+  body();
+  RPCA_CUDA(cudaStreamSynchronize(c.stream));
+  harvest(c, c.prof_recs);
+}
 
 // Run `body` (which only enqueues work on c.stream) either directly or as a
 // cached CUDA graph; then synchronise the stream and harvest profile marks.

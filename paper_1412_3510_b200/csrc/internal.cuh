@@ -7,6 +7,7 @@
 #include <algorithm>
 #include <cstddef>
 #include <cstdint>
+#include <functional>
 #include <vector>
 
 #include "common.cuh"
@@ -97,6 +98,8 @@ struct Ctx {
 };
 
 void prof_mark(Ctx& c, const char* name);
+// run a step-API body; with profiling on, harvest its launch marks
+void profiled_step(Ctx& c, const std::function<void()>& body);
 struct TagScope {
   Ctx& c;
   const char* prev;

@@ -6,7 +6,7 @@
 // L with Y = L·U (MATLAB's two-output lu; reading Q3).
 //
 // B200 design — tournament pivoting (CALU):
-//   1. leaf kernel: one CTA per block of 256 rows runs GEPP and nominates l
+//   1. leaf kernel: one CTA per block of R·256 rows runs GEPP and nominates l
 //      candidate pivot rows (original rows);
 //   2. tree kernel: groups of G candidate sets are stacked (original values
 //      gathered from Y) and reduced by GEPP again, until one set is left; the
@@ -15,15 +15,22 @@
 //   3. apply kernel: every CTA first forms the substitution matrix M with
 //      x = y·M ⇔ x·U = y (x_j = 0 where U_jj = 0 — the exact-zero-pivot rule of
 //      reading Q3), then L = Y·M for its rows (HBM-bound); pivot rows are
-//      overwritten with their exact unit-lower rows from Lp.  Optionally the
-//      CTA also accumulates LᵀL for the Cholesky-QR that follows (cholqr.cu).
-// GEPP inside a CTA: thread t owns rows t, t+256, … held in REGISTERS (the
-// kernel is templated on l rounded up to 8); the pivot row is read from a
-// shared-memory mirror that every thread refreshes after its update; the
-// argmax of column j+1 is reduced while column j is eliminated, so each column
-// costs one __syncthreads.  Pivot: largest |·| among active rows, lowest
-// original row on ties.  Tournament pivots differ from plain GEPP, so L differs
-// from the oracle's L but span(L) = span(Y) whenever U is nonsingular.
+//      overwritten with their exact unit-lower rows from Lp.
+// GEPP inside a CTA: thread t owns rows t·R … t·R+R−1 held in REGISTERS (the
+// kernel is templated on l rounded up to 8, every column step is unrolled so
+// all register indices are static).  Per column: the argmax over the warp is
+// two redux.sync.max on the bits of |v| (a non-negative double orders like its
+// bit pattern) plus a ballot for the lowest lane on ties; each warp's winner
+// lane publishes its (key, row) and its whole row to shared memory; ONE
+// __syncthreads; every warp then reduces the 8 warp winners the same way and
+// reads the pivot row with broadcast loads.  Local row order = original row
+// order (leaves are contiguous; tree candidates are sorted by id within each
+// set and sets cover ascending row ranges), so "lowest local row" is the
+// lowest-original-row tie rule.  Tournament pivots differ from plain GEPP, so
+// L differs from the oracle's L but span(L) = span(Y) whenever U is
+// nonsingular.
+#include <utility>
+
 #include "comm.cuh"
 
 namespace rpca {
@@ -32,152 +39,171 @@ namespace {
 constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
 
-struct Cand {
-  double v;
-  int r;  // local row (ties are broken by ids[r])
+template <int LP>
+struct SelCfg {
+  static constexpr int R = LP <= 8 ? 4 : (LP <= 16 ? 2 : 1);  // rows per thread
+  static constexpr int kCap = kThreads * R;                    // rows per CTA
+  static constexpr int kMinBlocks = LP <= 32 ? 2 : 1;
 };
 
-__device__ __forceinline__ bool better(double v, int r, double bv, int br, const int64_t* ids) {
-  if (v != bv) return v > bv;
-  if (br < 0) return r >= 0;
-  if (r < 0) return false;
-  return ids[r] < ids[br];
-}
-
-__device__ __forceinline__ Cand warp_best(Cand c, const int64_t* ids) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    const double ov = __shfl_xor_sync(0xffffffffu, c.v, o);
-    const int orr = __shfl_xor_sync(0xffffffffu, c.r, o);
-    if (better(ov, orr, c.v, c.r, ids)) { c.v = ov; c.r = orr; }
-  }
-  return c;
-}
-
-// GEPP on W (rows × ldw, shared; ldw odd ⇒ conflict-free row-per-thread
-// access).  Thread t owns rows t, t+256, … (active flags in registers).  One
-// __syncthreads per column: the argmax of column j+1 is reduced while column j
-// is eliminated and every thread redundantly combines the eight warp winners.
-// piv[j] = local pivot row of column j; W ends with the multipliers left of
-// each row's pivot column and its eliminated values right of it.
-__device__ void gepp(double* W, int ldw, const int64_t* ids, int rows, int l, int steps, int* piv,
-                     Cand (*slot)[kWarps]) {
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  constexpr int kMaxR = 3;
-  bool act[kMaxR];
-  Cand c{-1.0, -1};
-#pragma unroll
-  for (int q = 0; q < kMaxR; ++q) {
-    const int r = tid + q * kThreads;
-    act[q] = r < rows;
-    if (act[q]) {
-      const double v = fabs(W[r * ldw]);
-      if (better(v, r, c.v, c.r, ids)) c = Cand{v, r};
-    }
-  }
-  c = warp_best(c, ids);
-  if (lane == 0) slot[0][warp] = c;
-  __syncthreads();
-  for (int j = 0; j < steps; ++j) {
-    Cand b = slot[j & 1][0];
-#pragma unroll
-    for (int wi = 1; wi < kWarps; ++wi) {
-      const Cand o = slot[j & 1][wi];
-      if (better(o.v, o.r, b.v, b.r, ids)) b = o;
-    }
-    const int p = b.r;
-    if (tid == 0) piv[j] = p;
-    const double* prow = W + p * ldw;
-    const double u = prow[j];
-    const double uinv = (u != 0.0) ? __drcp_rn(u) : 0.0;
-    Cand nc{-1.0, -1};
-#pragma unroll
-    for (int q = 0; q < kMaxR; ++q) {
-      const int r = tid + q * kThreads;
-      if (!act[q]) continue;
-      if (r == p) { act[q] = false; continue; }
-      double* wr = W + r * ldw;
-      const double mult = wr[j] * uinv;
-      wr[j] = mult;
-      if (mult != 0.0) {
-        // chunks of 8: all loads issued before the stores (a row never aliases the pivot row)
-        int t = j + 1;
-        for (; t + 8 <= l; t += 8) {
-          double pv[8], wv[8];
-#pragma unroll
-          for (int u8 = 0; u8 < 8; ++u8) { pv[u8] = prow[t + u8]; wv[u8] = wr[t + u8]; }
-#pragma unroll
-          for (int u8 = 0; u8 < 8; ++u8) wr[t + u8] = wv[u8] - mult * pv[u8];
-        }
-        for (; t < l; ++t) wr[t] -= mult * prow[t];
-      }
-      if (j + 1 < steps) {
-        const double v = fabs(wr[j + 1]);
-        if (better(v, r, nc.v, nc.r, ids)) nc = Cand{v, r};
-      }
-    }
-    nc = warp_best(nc, ids);
-    if (lane == 0) slot[(j + 1) & 1][warp] = nc;
-    __syncthreads();
-  }
+// Pivot key of a value: the high word of |v| (11 exponent + 20 mantissa bits)
+// + 1, so 0 means "no candidate".  The pivot of a column is therefore a row
+// whose |value| is within 2^-20 (relative) of the column maximum — the lowest
+// such row (tournament LU): multipliers stay ≤ 1 + 2^-20.
+__device__ __forceinline__ uint32_t piv_key(double v) {
+  return ((uint32_t)__double2hiint(v) & 0x7FFFFFFFu) + 1u;
 }
 
 // One CTA: rows from Y (leaf: contiguous block; tree: a group of candidate
 // sets), GEPP, l nominated original rows → cand_out[blockIdx.x*l ...] (-1 pad).
-// If final, also U, Lp and the original pivot rows piv_out.
-__global__ void __launch_bounds__(kThreads) lu_select_kernel(const double* __restrict__ Y, int64_t m, int l, int leaf,
-                                                             int64_t leaf_rows, const int64_t* __restrict__ cand_in,
-                                                             int64_t n_in, int G, int64_t* __restrict__ cand_out,
-                                                             int final_, double* __restrict__ U,
-                                                             double* __restrict__ Lp, int64_t* __restrict__ piv_out,
-                                                             double* __restrict__ M,
-                                                             const double* __restrict__ rows_in,
-                                                             double* __restrict__ rows_out) {
-  // leaf: 1 = contiguous rows of Y; 0 = candidate ids into Y; 2 = candidate
-  // rows given directly (rows_in, one l-vector per slot; ids are global rows
-  // — the all-gathered local winners of a row-sharded LU)
-  extern __shared__ double sm[];
-  __shared__ Cand slot[2][kWarps];
-  __shared__ int piv[kMaxL];
+// If final, also U, Lp, the original pivot rows piv_out and M = U⁻¹.
+//   leaf: 1 = contiguous rows of Y; 0 = candidate ids into Y; 2 = candidate
+//   rows given directly (rows_in, one l-vector per slot; ids are global rows
+//   — the all-gathered local winners of a row-sharded LU)
+template <int LP>
+__global__ void __launch_bounds__(kThreads, SelCfg<LP>::kMinBlocks)
+    lu_select_kernel(const double* __restrict__ Y, int64_t m, int l, int leaf, const int64_t* __restrict__ cand_in,
+                     int64_t n_in, int G, int64_t* __restrict__ cand_out, int final_, double* __restrict__ U,
+                     double* __restrict__ Lp, int64_t* __restrict__ piv_out, double* __restrict__ M,
+                     const double* __restrict__ rows_in, double* __restrict__ rows_out) {
+  using Cfg = SelCfg<LP>;
+  constexpr int R = Cfg::R, CAP = Cfg::kCap;
+  __shared__ int64_t ids[CAP];
+  __shared__ int slot_of[CAP];
+  __shared__ uint2 slot[2][kWarps];  // {pivot key, local row} of each warp's winner
+  __shared__ double suinv[2][kWarps];
+  __shared__ __align__(16) double buf[2][kWarps][LP];
+  __shared__ int piv[LP];
   __shared__ int nrows_s;
-  const int cap = leaf == 1 ? (int)leaf_rows : G * l;
-  const int ldw = l | 1;
-  double* W = sm;
-  int64_t* ids = reinterpret_cast<int64_t*>(W + (size_t)cap * ldw);
-  int* slot_of = reinterpret_cast<int*>(ids + cap);
-  const int tid = threadIdx.x;
+  __shared__ int setcnt[CAP + 1];
+  extern __shared__ double keep[];  // final only: LP × LP published pivot rows, U, M, multipliers
+  double* msm = keep + LP * LP + l * l;  // final only: multiplier of (step j, row r) at j·CAP + r
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
 
   if (leaf == 1) {
-    const int64_t r0 = (int64_t)blockIdx.x * leaf_rows;
-    if (tid == 0) nrows_s = (int)imin64(leaf_rows, m - r0);
-    for (int r = tid; r < cap; r += kThreads) ids[r] = r0 + r;
+    const int64_t r0 = (int64_t)blockIdx.x * CAP;
+    if (tid == 0) nrows_s = (int)imin64(CAP, m - r0);
+    for (int r = tid; r < CAP; r += kThreads) ids[r] = r0 + r;
   } else {
-    // compact the valid candidates of this group (ascending slot order)
-    if (tid < 32) {
-      const int64_t s0 = (int64_t)blockIdx.x * G * l, s1 = imin64(n_in * l, s0 + (int64_t)G * l);
-      int base = 0;
-      for (int64_t s = s0; s < s1; s += 32) {
-        const int64_t id = (s + tid < s1) ? cand_in[s + tid] : -1;
-        const unsigned mask = __ballot_sync(0xffffffffu, id >= 0);
-        if (id >= 0) {
-          const int pos = base + __popc(mask & ((1u << tid) - 1u));
-          ids[pos] = id;
-          slot_of[pos] = (int)(s + tid - s0);
-        }
-        base += __popc(mask);
-      }
-      if (tid == 0) nrows_s = base;
+    // compact the valid candidates of this group: sets in ascending order,
+    // each set's ids sorted ascending (rank = #smaller valid ids in the set)
+    const int64_t s0 = (int64_t)blockIdx.x * G * l, s1 = imin64(n_in * l, s0 + (int64_t)G * l);
+    const int nslots = (int)(s1 - s0), nsets = (nslots + l - 1) / l;
+    for (int s = tid; s < nslots; s += kThreads) ids[s] = cand_in[s0 + s];
+    __syncthreads();
+    for (int st = tid; st < nsets; st += kThreads) {
+      int cnt = 0;
+      for (int t = st * l; t < min(nslots, st * l + l); ++t) cnt += ids[t] >= 0;
+      setcnt[st + 1] = cnt;
     }
+    __syncthreads();
+    if (tid == 0) {
+      setcnt[0] = 0;
+      for (int st = 0; st < nsets; ++st) setcnt[st + 1] += setcnt[st];
+      nrows_s = setcnt[nsets];
+    }
+    __syncthreads();
+    int64_t myid[(CAP + kThreads - 1) / kThreads];
+    int mypos[(CAP + kThreads - 1) / kThreads];
+#pragma unroll
+    for (int q = 0; q < (CAP + kThreads - 1) / kThreads; ++q) {
+      const int s = tid + q * kThreads;
+      mypos[q] = -1;
+      myid[q] = -1;
+      if (s < nslots && ids[s] >= 0) {
+        const int st = s / l;
+        const int64_t id = ids[s];
+        int rank = 0;
+        for (int t = st * l; t < min(nslots, st * l + l); ++t) rank += (ids[t] >= 0 && ids[t] < id);
+        mypos[q] = setcnt[st] + rank;
+        myid[q] = id;
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < (CAP + kThreads - 1) / kThreads; ++q)
+      if (mypos[q] >= 0) {
+        ids[mypos[q]] = myid[q];
+        slot_of[mypos[q]] = tid + q * kThreads;
+      }
   }
   __syncthreads();
   const int rows = nrows_s;
-  for (int idx = tid; idx < rows * l; idx += kThreads) {
-    const int r = idx / l, t = idx - r * l;
-    W[r * ldw + t] = leaf == 2 ? rows_in[((int64_t)blockIdx.x * G * l + slot_of[r]) * l + t] : Y[ids[r] * l + t];
+  const int steps = min(rows, l);
+
+  // this thread's rows → registers (zero beyond l / beyond rows)
+  double w[R][LP];
+  bool act[R];
+#pragma unroll
+  for (int q = 0; q < R; ++q) {
+    const int r = tid * R + q;
+    act[q] = r < rows;
+    const double* src = nullptr;
+    if (act[q])
+      src = leaf == 2 ? rows_in + ((int64_t)blockIdx.x * G * l + slot_of[r]) * l : Y + ids[r] * l;
+#pragma unroll
+    for (int t = 0; t < LP; ++t) w[q][t] = (act[q] && t < l) ? src[t] : 0.0;
+  }
+
+  // Rolled column loop (a straight-line unroll over all columns overflows the
+  // instruction cache).  Registers hold the row SHIFTED: at step j, w[q][t] is
+  // column j+t (zero beyond LP−j); each elimination writes w[t−1] ← w[t] −
+  // mult·p[t].  Only the final level keeps the multipliers (msm, shared) and
+  // the published pivot rows (keep) for U and Lp.
+  for (int j = 0; j < steps; ++j) {
+    uint32_t best = 0;
+    int bq = 0;
+#pragma unroll
+    for (int q = 0; q < R; ++q)
+      if (act[q]) {
+        const uint32_t k = piv_key(w[q][0]);
+        if (k > best) { best = k; bq = q; }
+      }
+    const uint32_t mk = __reduce_max_sync(0xffffffffu, best);
+    const int wl = __ffs(__ballot_sync(0xffffffffu, best == mk)) - 1;  // lowest lane = lowest row
+    if (lane == wl) {
+#pragma unroll
+      for (int q = 0; q < R; ++q)
+        if (q == bq) {
+          const double u = w[q][0];
+          slot[j & 1][warp] = make_uint2(mk, (uint32_t)(tid * R + q));
+          suinv[j & 1][warp] = (u != 0.0) ? __drcp_rn(u) : 0.0;
+          double2* dst = reinterpret_cast<double2*>(buf[j & 1][warp]);
+#pragma unroll
+          for (int t = 0; t < LP; t += 2) dst[t >> 1] = make_double2(w[q][t], w[q][t + 1]);
+        }
+    }
+    __syncthreads();
+    // max over the 8 warp winners in a fixed 3-level tree (lower warp on ties)
+    uint2 k[kWarps];
+    int wi[kWarps];
+#pragma unroll
+    for (int i = 0; i < kWarps; ++i) {
+      k[i] = slot[j & 1][i];
+      wi[i] = i;
+    }
+#pragma unroll
+    for (int st = 1; st < kWarps; st <<= 1)
+#pragma unroll
+      for (int i = 0; i < kWarps; i += 2 * st)
+        if (k[i + st].x > k[i].x) { k[i] = k[i + st]; wi[i] = wi[i + st]; }
+    const int p = (int)k[0].y;
+    const double uinv = suinv[j & 1][wi[0]];
+    const double* prow = buf[j & 1][wi[0]];
+    if (tid == 0) piv[j] = p;
+    if (final_ && tid < LP) keep[j * LP + tid] = prow[tid];
+#pragma unroll
+    for (int q = 0; q < R; ++q) {
+      if (!act[q]) continue;
+      if (tid * R + q == p) { act[q] = false; continue; }
+      const double mult = w[q][0] * uinv;
+      if (final_) msm[j * CAP + tid * R + q] = mult;
+#pragma unroll
+      for (int t = 1; t < LP; ++t) w[q][t - 1] = fma(-mult, prow[t], w[q][t]);
+      w[q][LP - 1] = 0.0;
+    }
   }
   __syncthreads();
-  const int steps = min(rows, l);
-  gepp(W, ldw, ids, rows, l, steps, piv, slot);
   for (int j = tid; j < l; j += kThreads) cand_out[(int64_t)blockIdx.x * l + j] = j < steps ? ids[piv[j]] : -1;
   if (rows_out) {  // direct mode: forward the winners' original rows to the next level
     for (int idx = tid; idx < l * l; idx += kThreads) {
@@ -187,30 +213,28 @@ __global__ void __launch_bounds__(kThreads) lu_select_kernel(const double* __res
     }
   }
   if (!final_) return;
-  __syncthreads();
+  // keep[j] = pivot row j as published (columns j.. at 0..LP−j−1); its
+  // multiplier of step s < j is msm[s·CAP + piv[j]]
+  double* Ms = keep + LP * LP;  // l×l M = U⁻¹ (U_ic = keep[i·LP + c − i])
   for (int idx = tid; idx < l * l; idx += kThreads) {
-    const int j = idx / l, t = idx - j * l;
-    const double v = W[piv[j] * ldw + t];
-    U[idx] = t >= j ? v : 0.0;
-    Lp[idx] = t < j ? v : (t == j ? 1.0 : 0.0);
+    const int j = idx / l, c = idx - j * l;
+    const double u = c >= j ? keep[j * LP + c - j] : 0.0;
+    U[idx] = u;
+    Lp[idx] = c < j ? msm[c * CAP + piv[j]] : (c == j ? 1.0 : 0.0);
   }
   for (int j = tid; j < l; j += kThreads) piv_out[j] = ids[piv[j]];
   __syncthreads();
   // M = U⁻¹ with the zero-pivot rule (a zero U_ii zeroes row i of M: x_i = 0
-  // for every input of the row substitution x·U = y, reading Q3): column j by
-  // one warp, M[j][j] = 1/U_jj, M[i][j] = −(Σ_{t=i+1..j} U_it M_tj)/U_ii.
-  double* Ms = reinterpret_cast<double*>(ids + cap) + (cap + 1) / 2;  // l×l after ids and slot_of
-  const int lane = tid & 31, warp = tid >> 5;
-  for (int j = warp; j < l; j += kWarps) {
-    for (int i = lane; i < l; i += 32) Ms[i * l + j] = 0.0;
-    __syncwarp();
-    for (int i = j; i >= 0; --i) {
+  // for every input of the row substitution x·U = y, reading Q3).  Thread j
+  // owns column j: back substitution M[i][j] = (δ_ij − Σ_{t=i+1..j} U_it M_tj)/U_ii
+  // with i descending in lock-step over all threads (U reads are broadcasts).
+  if (tid < l) {
+    const int j = tid;
+    for (int i = l - 1; i >= 0; --i) {
       double acc = 0.0;
-      for (int t = i + 1 + lane; t <= j; t += 32) acc += W[piv[i] * ldw + t] * Ms[t * l + j];
-      acc = warp_sum(acc);
-      const double uii = W[piv[i] * ldw + i];
-      if (lane == 0) Ms[i * l + j] = (uii != 0.0) ? ((i == j ? 1.0 : 0.0) - acc) / uii : 0.0;
-      __syncwarp();
+      for (int t = i + 1; t <= j; ++t) acc += keep[i * LP + t - i] * Ms[t * l + j];
+      const double uii = keep[i * LP];
+      Ms[i * l + j] = (i <= j && uii != 0.0) ? ((i == j ? 1.0 : 0.0) - acc) / uii : 0.0;
     }
   }
   __syncthreads();
@@ -241,26 +265,46 @@ __global__ void pack_candidates_kernel(const double* __restrict__ Y, int l, int6
   }
 }
 
-constexpr int kLeafRows = 256;
-
-// a tree group holds ≤ 3·256 rows (3 rows per thread in gepp) and ≤ ~200 KB
-int group_for(int l) {
-  const int max_rows = std::min(kThreads * 3, 21000 / (l | 1));
-  return std::max(2, std::min(32, max_rows / l));
+int lp_of(int l) { return (l + 7) & ~7; }
+int cap_of(int l) {
+  switch (lp_of(l)) {
+    case 8: return SelCfg<8>::kCap;
+    case 16: return SelCfg<16>::kCap;
+    default: return kThreads;
+  }
 }
+// a tree group stacks G candidate sets of l rows into one CTA's rows
+int group_for(int l) { return std::max(2, cap_of(l) / l); }
 
-size_t select_smem(int cap, int l) {
-  return (size_t)cap * (l | 1) * 8 + (size_t)cap * 8 + (size_t)(cap + 1) / 2 * 8 + (size_t)l * l * 8 + 16;
+template <int LP>
+void select_lp(Ctx& c, unsigned grid, const double* Y, int64_t m, int l, int leaf, const int64_t* cin, int64_t n_in,
+               int G, int64_t* cout, int final_, double* U, double* Lp, int64_t* piv, double* M,
+               const double* rows_in, double* rows_out) {
+  const size_t smem = final_ ? (size_t)(LP * LP + l * l + (size_t)SelCfg<LP>::kCap * l) * 8 : 0;
+  if (smem) ensure_smem((const void*)lu_select_kernel<LP>, (int)smem);
+  lu_select_kernel<LP><<<grid, kThreads, smem, c.stream>>>(Y, m, l, leaf, cin, n_in, G, cout, final_, U, Lp, piv,
+                                                           M, rows_in, rows_out);
 }
 
 void select(Ctx& c, unsigned grid, const double* Y, int64_t m, int l, int leaf, const int64_t* cin, int64_t n_in,
             int G, int64_t* cout, int final_, double* U, double* Lp, int64_t* piv, double* M,
             const double* rows_in = nullptr, double* rows_out = nullptr) {
-  const int cap = leaf == 1 ? kLeafRows : G * l;
-  ensure_smem((const void*)lu_select_kernel, 220 * 1024);
-  const size_t smem = select_smem(cap, l) - (final_ ? 0 : (size_t)l * l * 8);
-  lu_select_kernel<<<grid, kThreads, smem, c.stream>>>(Y, m, l, leaf, kLeafRows, cin, n_in, G, cout, final_, U, Lp,
-                                                       piv, M, rows_in, rows_out);
+#define RPCA_SEL(LPV)                                                                                 \
+  case LPV:                                                                                           \
+    select_lp<LPV>(c, grid, Y, m, l, leaf, cin, n_in, G, cout, final_, U, Lp, piv, M, rows_in, rows_out); \
+    break;
+  switch (lp_of(l)) {
+    RPCA_SEL(8)
+    RPCA_SEL(16)
+    RPCA_SEL(24)
+    RPCA_SEL(32)
+    RPCA_SEL(40)
+    RPCA_SEL(48)
+    RPCA_SEL(56)
+    RPCA_SEL(64)
+    default: RPCA_REQUIRE(false, RPCA_E_SHAPE, "lu: l=%d > %d", l, kMaxL);
+  }
+#undef RPCA_SEL
   RPCA_CHECK_LAUNCH();
   count_launch(c, 1, leaf == 1 ? "lu_leaf" : "lu_tree");
 }
@@ -271,7 +315,7 @@ void select(Ctx& c, unsigned grid, const double* Y, int64_t m, int l, int leaf, 
 int64_t* tournament(Ctx& c, const double* Y, int64_t m, int l, bool finalize, double* U, double* Lp, int64_t* piv,
                     double* M, Arena& ar) {
   const int G = group_for(l);
-  const int64_t nblk = std::max<int64_t>(1, cdiv(m, kLeafRows));
+  const int64_t nblk = std::max<int64_t>(1, cdiv(m, cap_of(l)));
   int64_t* ca = ar.get<int64_t>(nblk * l);
   int64_t* cb = ar.get<int64_t>(nblk * l);
   if (m == 0) {
@@ -308,7 +352,7 @@ void apply_l(Ctx& c, double* Y, int64_t m, int64_t row0, int l, const double* M,
 size_t lu_ws_bytes(int64_t m, int l) {
   Sizer s;
   s.add<char>(ax_ws_bytes(DenseA{nullptr, RPCA_F64, m, l, l}, l) + 4096);
-  const int64_t nblk = std::max<int64_t>(1, cdiv(m, kLeafRows));
+  const int64_t nblk = std::max<int64_t>(1, cdiv(m, 256));
   s.add<int64_t>(nblk * l);
   s.add<int64_t>(nblk * l);
   s.add<double>(4 * (size_t)l * l);
