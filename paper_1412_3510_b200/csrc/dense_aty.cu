@@ -327,12 +327,8 @@ void dense_aty(Ctx& c, const DenseA& A, const double* Y, int l, const double* cm
     weighted_colsum(c, nullptr, Y, A.m, l, sy, ar);
   }
   if (f32_tc_ok(A) && A.m > 0) {
-    int64_t P = 0, cpc = 0;
-    int ms = 0, LP = 0;
     const size_t mark = ar.off;
-    double* part = nullptr;
-    dense_aty_f32_partials(c, A, Y, l, &part, &P, &ms, &cpc, &LP, ar);
-    aty_reduce_partials(c, part, cdiv(A.n, 128) * cpc, P, cpc, ms, A.n, l, LP, cmean, sy, Z);
+    dense_aty_f32(c, A, Y, l, cmean, sy, Z, ar);
     ar.off = mark;
     return;
   }

@@ -242,11 +242,16 @@ size_t ax_ws_bytes(const DenseA& A, int l) {
   return s.total;
 }
 
-void dense_ax(Ctx& c, const DenseA& A, const double* X, int l, double* Y, Arena& ar) {
+void dense_ax(Ctx& c, const DenseA& A, const double* X, int l, double* Y, Arena& ar, const double* cx) {
   RPCA_REQUIRE(l >= 1 && l <= kMaxL, RPCA_E_SHAPE, "l=%d out of range [1,%d]", l, kMaxL);
   if (A.m == 0) return;
   if (f32_tc_ok(A)) {
-    dense_ax_f32(c, A, X, l, Y, ar);
+    dense_ax_f32(c, A, X, l, cx, Y, ar);  // centring folded into the epilogue
+    return;
+  }
+  if (cx) {  // fp64 / generic kernels: the rank-1 correction as a separate thin pass
+    dense_ax(c, A, X, l, Y, ar, nullptr);
+    sub_rank1(c, Y, A.m, l, nullptr, cx);
     return;
   }
   if (tma_ok(A)) {

@@ -10,23 +10,31 @@
 // tools/microbench/tc_tf32_probe.cu), so the raw fp32 tile is the "hi"
 // operand as loaded and only A_lo = A − trunc13(A) has to be formed.
 //
-// A·X  (D[128 rows × N] += A[128 × K] · X[K × N]):
-//   warp 0 — TMA producer: A box [128 rows × 32 fp32] (SWIZZLE_128B) and the
-//            matching K-chunk of Xᵀ_hi / Xᵀ_lo ([N × 32], K-major) per stage;
-//   warps 2-5 — split: thread t owns row t, reads its 128-byte row from the
-//            swizzled tile and writes A_lo in the same layout (conflict-free
-//            16-byte accesses), then the epilogue (tcgen05.ld → fp64 → Y);
-//   warp 1 — one thread issues tcgen05.mma kind::tf32 (M=128, N = 16..64,
-//            K=8) ×3 per k-step into a TMEM fp32 accumulator, and commits
-//            stage releases / the tile to mbarriers.
-// Aᵀ·Y (D[128 cols × N] += Aᵀ[128 × K rows] · Y[K × N]): the same roles on
-//   (128-column block × 32-row chunk) units split evenly over the CTAs
-//   (stream-K, as the fp64 kernel); the split warps transpose the tile into
-//   K-major Aᵀ_hi / Aᵀ_lo, partial accumulators are flushed in fp64 and
-//   reduced in ascending CTA order by dense_aty.cu's reducer.
-// Per element of A: 4 bytes, 3·2·N tensor flops.  fp32 accumulation runs over
-// the whole K of one tile (≤ 4096 for C4); everything across tiles, CTAs and
-// ranks is fp64.
+// In-place split: a stage holds ONE copy of the A tile.  The MMA warp first
+// issues the two "hi" products (A·X_hi, A·X_lo) and commits them to the
+// stage's hi_done barrier; the split warps then overwrite the tile with A_lo
+// in place (the transform is elementwise, so any layout works) and the MMA
+// warp issues A_lo·X_hi two stages later (fixed lag), whose commit frees the
+// stage.  One copy per stage buys 6-8 stages of A in flight per SM.
+//
+// A·X  (D[128 rows × N] += A[128 × K] · Xᵀ[N × K]ᵀ, both K-major):
+//   warp 0 producer (TMA A box [128 rows × 32 fp32] + Xᵀ_hi/lo chunks),
+//   warp 1 MMA issuer, warps 2-5 split, warps 6-9 epilogue.  Units are
+//   (128-row tile, ≤ 4096-wide K chunk) — fp32 accumulation never runs over
+//   more than 4096 products; two TMEM accumulators
+//   alternate so the epilogue of unit u overlaps the MMAs of unit u+1; the
+//   epilogue writes (first chunk) or adds (later chunks) fp64 into Y and
+//   folds the centring correction −1·(c·X) of PAPER.md:430.
+// Aᵀ·Y (D[128 cols × N] += Aᵀ[128 cols × K rows] · Y[K × N]): the A tile is
+//   read as an MN-major operand straight from the TMA layout (no transpose;
+//   tf32 MN-major requires the 128B_ATOM_32B swizzle).
+//   A CTA owns a group of ≤ 512/N column blocks (all accumulators live in
+//   TMEM) and a contiguous row range; each 32-row chunk of Yᵀ_hi/lo is loaded
+//   once and used for every column block of the group, so Y is read
+//   ⌈n/(128·group)⌉ times instead of once per column block.  Every 4096 rows
+//   the accumulators are flushed (fp64 adds into the CTA's partial); the
+//   partials are reduced over the row ranges in ascending order.
+// Per element of A: 4 bytes, 3·2·N tensor flops.
 #include <cudaTypedefs.h>
 
 #include "internal.cuh"
@@ -34,7 +42,6 @@
 namespace rpca {
 namespace {
 
-constexpr int kThreads = 192;  // 6 warps
 
 __device__ __forceinline__ uint64_t desc_sw128(uint32_t saddr) {
   uint64_t d = 0;
@@ -50,13 +57,23 @@ __host__ __device__ constexpr uint32_t idesc_tf32(int M, int N) {
   return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
 }
 
-// element (r, k) of a K-major tile with 32 fp32 per row, SWIZZLE_128B
-__device__ __forceinline__ uint32_t kmaj(int r, int k) {
-  return r * 128 + ((((k >> 2) ^ (r & 7)) & 7) << 4) + ((k & 3) << 2);
-}
-
 __device__ __forceinline__ float lo_part(float a) {
   return a - __uint_as_float(__float_as_uint(a) & 0xFFFFE000u);
+}
+
+// MN-major tf32 operand: the only smem layout the tensor core takes for it is
+// SWIZZLE_128B_BASE32B (descriptor layout type 1; TMA mode 128B_ATOM_32B:
+// 32-byte chunks of each 128-byte MN row XOR-ed with the row index mod 4).
+// 128-byte MN rows (32 fp32), 4 K-rows per 512-byte atom (SBO), 32-wide MN
+// chunks 4096 bytes apart (LBO).
+__device__ __forceinline__ uint64_t desc_mn_sw128_32b(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+  d |= (uint64_t)(4096 >> 4) << 16;  // LBO: next 32 MN elements
+  d |= (uint64_t)(512 >> 4) << 32;   // SBO: next 4 K rows
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)1 << 61;            // SWIZZLE_128B_BASE32B
+  return d;
 }
 
 __device__ __forceinline__ void mma_tf32(uint32_t tmem, uint64_t da, uint64_t db, uint32_t idesc, uint32_t acc) {
@@ -64,6 +81,28 @@ __device__ __forceinline__ void mma_tf32(uint32_t tmem, uint64_t da, uint64_t db
       "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
       "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem),
       "l"(da), "l"(db), "r"(idesc), "r"(acc));
+}
+
+// D[tmem] (+)= A[tmem] · B[smem]: the A operand read from TMEM (lane = M row,
+// one 32-bit column per K element)
+__device__ __forceinline__ void mma_tf32_ts(uint32_t dt, uint32_t at, uint64_t db, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}" ::"r"(dt),
+      "r"(at), "l"(db), "r"(idesc), "r"(acc));
+}
+
+// this thread's 32 consecutive TMEM columns of its lane ← v
+__device__ __forceinline__ void tmem_st32(uint32_t addr, const float (&v)[32]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+      "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(addr),
+      "f"(v[0]), "f"(v[1]), "f"(v[2]), "f"(v[3]), "f"(v[4]), "f"(v[5]), "f"(v[6]), "f"(v[7]), "f"(v[8]), "f"(v[9]),
+      "f"(v[10]), "f"(v[11]), "f"(v[12]), "f"(v[13]), "f"(v[14]), "f"(v[15]), "f"(v[16]), "f"(v[17]), "f"(v[18]),
+      "f"(v[19]), "f"(v[20]), "f"(v[21]), "f"(v[22]), "f"(v[23]), "f"(v[24]), "f"(v[25]), "f"(v[26]), "f"(v[27]),
+      "f"(v[28]), "f"(v[29]), "f"(v[30]), "f"(v[31])
+      : "memory");
+  asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
 }
 
 __device__ __forceinline__ void mma_commit(uint64_t* bar) {
@@ -83,310 +122,492 @@ __device__ __forceinline__ void tmem_ld16(uint32_t addr, float (&v)[16]) {
   for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
 }
 
-// Stage layout: raw A tile (16 KB) | NT split tiles of 16 KB (AX: A_lo; AtY:
-// Aᵀ_hi, Aᵀ_lo) | Xᵀ_hi chunk | Xᵀ_lo chunk (N rows × 128 B each).
-template <int N, int NT>
-struct F32Cfg {
-  static constexpr int kA = 128 * 128;
-  static constexpr int kAlo = 128 * 128;
-  static constexpr int kX = N * 128;
-  static constexpr int kXoff = kA + NT * kAlo;
-  static constexpr int kStage = kXoff + 2 * kX;
-  static constexpr int kStages = (216 * 1024) / kStage > 4 ? 4 : (216 * 1024) / kStage;
-  static constexpr int kSmem = kStages * kStage + 1024 + 256;
-  static constexpr int kTmemCols = N <= 32 ? 32 : 64;
+// one lane of a converged warp (the same one every time) — the issuing lane of
+// TMA / tcgen05.mma / tcgen05.commit; the rest of the warp keeps the loop
+// state uniform so operands stay in uniform registers
+__device__ __forceinline__ bool elect_one() {
+  uint32_t pred = 0;
+  asm volatile("{\n\t.reg .pred P;\n\telect.sync _|P, 0xffffffff;\n\tselp.b32 %0, 1, 0, P;\n\t}" : "=r"(pred));
+  return pred != 0;
+}
+
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+
+constexpr int kThreadsTC = 352;  // 11 warps: producer, hi-MMA, lo-MMA, 4 split, 4 epilogue
+constexpr int kTileBytes = 128 * 128;  // 16 KB A tile
+constexpr int kKChunk = 4096;          // max products per fp32 accumulation (Q15)
+
+// stage index + phase of an S-deep mbarrier ring, advanced without division
+template <int S>
+struct Ring {
+  int s = 0;
+  uint32_t ph = 0;
+  __device__ __forceinline__ void next() {
+    if (++s == S) { s = 0; ph ^= 1u; }
+  }
+};
+
+template <int N>
+struct AxCfg {
+  static constexpr int kX = N * 128;  // one Xᵀ chunk: N rows × 32 fp32
+  static constexpr int kStage = kTileBytes + 2 * kX;
+  static constexpr int kStages = (212 * 1024) / kStage > 8 ? 8 : (212 * 1024) / kStage;
+  static constexpr int kSmem = kStages * kStage + 1024 + 512;
+  // TMEM per accumulator: [0, N) A·X_hi, [N, 2N) A·X_lo (one N = 2N MMA),
+  // [2N, 3N) A_lo·X_hi (the lo issuer's own columns); two accumulators, then
+  // two 32-column A_lo slots
+  static constexpr int kW = (3 * N + 31) / 32 * 32;
+  static constexpr int kSlot0 = 2 * kW;
+  static constexpr int kCols = kSlot0 + 64 <= 256 ? 256 : 512;
 };
 
 // ---------------------------------------------------------------- Y = A·X
+// warps: 0 TMA producer, 1 hi-MMA issuer, 2 lo-MMA issuer, 3-6 split
+// (A_lo → TMEM), 7-10 epilogue
 template <int N>
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __launch_bounds__(kThreadsTC, 1)
     ax_f32_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmXh,
                      const __grid_constant__ CUtensorMap tmXl, int64_t m, int l, int64_t ntiles, int KB,
-                     double* __restrict__ Y) {
-  using Cfg = F32Cfg<N, 1>;
-  constexpr int kStagesF = Cfg::kStages;
+                     const double* __restrict__ cx, double* __restrict__ Y) {
+  using Cfg = AxCfg<N>;
+  constexpr int S = Cfg::kStages;
+  constexpr int KC = kKChunk / 32;  // k-blocks per unit
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kStagesF * Cfg::kStage);
-  uint64_t* lo_full = full + kStagesF;
-  uint64_t* empty = lo_full + kStagesF;
-  uint64_t* acc_full = empty + kStagesF;
-  uint64_t* acc_empty = acc_full + 1;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 1);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + S * Cfg::kStage);
+  uint64_t* empty = full + S;       // hi commit + lo commit
+  uint64_t* lo_full = empty + S;    // 4 split warps (A_lo in TMEM)
+  uint64_t* tfree = lo_full + S;    // [2] A_lo slot free (lo commit)
+  uint64_t* ustart = tfree + 2;     // [2] first hi MMAs of unit u done (lo may accumulate), by u & 1
+  uint64_t* acc_full = ustart + 2;  // [2] hi commit + lo commit
+  uint64_t* acc_empty = acc_full + 2;  // [2] 4 epilogue warps
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nkc = (KB + KC - 1) / KC;  // K chunks per tile
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < kStagesF; ++s) {
+    for (int s = 0; s < S; ++s) {
       mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 2);
       mbar_init(&lo_full[s], 4);
-      mbar_init(&empty[s], 1);
     }
-    mbar_init(acc_full, 1);
-    mbar_init(acc_empty, 4);
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfree[a], 1);
+      mbar_init(&ustart[a], 1);
+      mbar_init(&acc_full[a], 2);
+      mbar_init(&acc_empty[a], 4);
+    }
     fence_barrier_init();
   }
   if (warp == 1) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
-                 "n"(Cfg::kTmemCols));
+                 "n"(Cfg::kCols));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
-  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  tc_fence_before();
   __syncthreads();
-  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
-  if (warp == 0) {
-    if (lane == 0) {  // ------------------------------------------ producer
-      prefetch_tmap(&tmA);
-      prefetch_tmap(&tmXh);
-      prefetch_tmap(&tmXl);
-      int s = 0;
-      uint32_t ph = 0;
-      for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x)
-        for (int kb = 0; kb < KB; ++kb) {
-          mbar_wait(&empty[s], ph ^ 1);
-          uint8_t* st = smem + s * Cfg::kStage;
-          mbar_arrive_expect_tx(&full[s], Cfg::kA + 2 * Cfg::kX);
-          tma_load_2d(st, &tmA, kb * 32, (int32_t)(tile * 128), &full[s]);
-          tma_load_2d(st + Cfg::kXoff, &tmXh, kb * 32, 0, &full[s]);
-          tma_load_2d(st + Cfg::kXoff + Cfg::kX, &tmXl, kb * 32, 0, &full[s]);
-          if (++s == kStagesF) { s = 0; ph ^= 1; }
+  if (warp == 0) {  // ----------------------------------------------- producer
+    const bool leader = elect_one();
+    prefetch_tmap(&tmA);
+    prefetch_tmap(&tmXh);
+    prefetch_tmap(&tmXl);
+    Ring<S> rg;
+    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x)
+      for (int kb = 0; kb < KB; ++kb, rg.next()) {
+        mbar_wait(&empty[rg.s], rg.ph ^ 1u);
+        uint8_t* st = smem + rg.s * Cfg::kStage;
+        if (leader) {
+          mbar_arrive_expect_tx(&full[rg.s], kTileBytes + 2 * Cfg::kX);
+          tma_load_2d(st, &tmA, kb * 32, (int32_t)(tile * 128), &full[rg.s]);
+          tma_load_2d(st + kTileBytes, &tmXh, kb * 32, 0, &full[rg.s]);
+          tma_load_2d(st + kTileBytes + Cfg::kX, &tmXl, kb * 32, 0, &full[rg.s]);
         }
-    }
-  } else if (warp == 1) {
-    if (lane == 0) {  // ------------------------------------------ MMA issuer
-      constexpr uint32_t idesc = idesc_tf32(128, N);
-      int s = 0;
-      uint32_t ph = 0, aph = 0;
-      for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-        mbar_wait(acc_empty, aph ^ 1);
-        aph ^= 1;
-        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        for (int kb = 0; kb < KB; ++kb) {
-          mbar_wait(&lo_full[s], ph);
-          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-          const uint32_t a0 = smem_u32(smem + s * Cfg::kStage);
-          const uint32_t al = a0 + Cfg::kA;
-          const uint32_t xh = a0 + Cfg::kXoff, xl = xh + Cfg::kX;
-#pragma unroll
-          for (int ks = 0; ks < 4; ++ks) {
-            const uint32_t acc = (kb | ks) != 0;
-            mma_tf32(tmem, desc_sw128(a0 + ks * 32), desc_sw128(xh + ks * 32), idesc, acc);
-            mma_tf32(tmem, desc_sw128(a0 + ks * 32), desc_sw128(xl + ks * 32), idesc, 1);
-            mma_tf32(tmem, desc_sw128(al + ks * 32), desc_sw128(xh + ks * 32), idesc, 1);
-          }
-          mma_commit(&empty[s]);
-          if (kb == KB - 1) mma_commit(acc_full);
-          if (++s == kStagesF) { s = 0; ph ^= 1; }
-        }
-      }
-    }
-  } else {  // ---------------------------------------------------- split + epilogue
-    const int t = threadIdx.x - 64;  // row of the tile, 0..127
-    const int q = warp & 3;          // TMEM lane quarter this warp may access
-    int s = 0;
-    uint32_t ph = 0, aph = 0;
-    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-      for (int kb = 0; kb < KB; ++kb) {
-        mbar_wait(&full[s], ph);
-        const uint8_t* a = smem + s * Cfg::kStage;
-        uint8_t* al = smem + s * Cfg::kStage + Cfg::kA;
-#pragma unroll
-        for (int c = 0; c < 8; ++c) {
-          const uint32_t off = kmaj(t, 4 * c);
-          float4 v = *reinterpret_cast<const float4*>(a + off);
-          v.x = lo_part(v.x);
-          v.y = lo_part(v.y);
-          v.z = lo_part(v.z);
-          v.w = lo_part(v.w);
-          *reinterpret_cast<float4*>(al + off) = v;
-        }
-        fence_proxy_async();  // generic-proxy writes → visible to the tensor core
         __syncwarp();
-        if (lane == 0) mbar_arrive(&lo_full[s]);
-        if (++s == kStagesF) { s = 0; ph ^= 1; }
       }
-      // epilogue: rows 32q..32q+31 of the accumulator live in TMEM lanes of quarter q
-      mbar_wait(acc_full, aph);
-      aph ^= 1;
-      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      const int64_t row = tile * 128 + 32 * q + lane;
-#pragma unroll
-      for (int c0 = 0; c0 < N; c0 += 16) {
-        float v[16];
-        tmem_ld16(tmem + ((uint32_t)(32 * q) << 16) + c0, v);
-        if (row < m) {
-#pragma unroll
-          for (int j = 0; j < 16; ++j)
-            if (c0 + j < l) Y[row * l + c0 + j] = (double)v[j];
+  } else if (warp == 1) {  // ---------------------------------------- hi-MMA issuer
+    // D[:, 0:2N] += A·[X_hi | X_lo] — one N = 2N MMA per k-step (the two Xᵀ
+    // chunks are adjacent in the stage: a 2N-row K-major operand)
+    const bool leader = elect_one();
+    constexpr uint32_t idesc = idesc_tf32(128, 2 * N);
+    Ring<S> rg;
+    int64_t u = -1;
+    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x)
+      for (int kb = 0; kb < KB; ++kb, rg.next()) {
+        const int kin = kb & (KC - 1);
+        if (kin == 0) {  // first stage of a unit: its accumulator must have been drained
+          ++u;
+          mbar_wait(&acc_empty[u & 1], (uint32_t)((u >> 1) & 1) ^ 1u);
+          tc_fence_after();
         }
+        mbar_wait(&full[rg.s], rg.ph);
+        tc_fence_after();
+        const uint32_t d = tmem + (uint32_t)((u & 1) * Cfg::kW);
+        const uint32_t a0 = smem_u32(smem + rg.s * Cfg::kStage);
+        const uint64_t da = desc_sw128(a0), dx = desc_sw128(a0 + kTileBytes);
+        if (leader) {
+#pragma unroll
+          for (int ks = 0; ks < 4; ++ks) mma_tf32(d, da + 2 * ks, dx + 2 * ks, idesc, (kin != 0 || ks != 0) ? 1u : 0u);
+          mma_commit(&empty[rg.s]);
+          if (kin == 0) mma_commit(&ustart[u & 1]);
+          if (kb == KB - 1 || kin == KC - 1) mma_commit(&acc_full[u & 1]);
+        }
+        __syncwarp();
       }
-      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-      __syncwarp();
-      if (lane == 0) mbar_arrive(acc_empty);
+  } else if (warp == 2) {  // ---------------------------------------- lo-MMA issuer
+    // D[:, 2N:3N] (+)= A_lo·X_hi with A_lo read from TMEM
+    const bool leader = elect_one();
+    constexpr uint32_t idesc = idesc_tf32(128, N);
+    Ring<S> rg;
+    Ring<2> rt;
+    int64_t u = -1;
+    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x)
+      for (int kb = 0; kb < KB; ++kb, rg.next(), rt.next()) {
+        const int kin = kb & (KC - 1);
+        if (kin == 0) {  // the unit's accumulator was drained once the hi issuer started it
+          ++u;
+          mbar_wait(&ustart[u & 1], (uint32_t)((u >> 1) & 1));
+          tc_fence_after();
+        }
+        mbar_wait(&lo_full[rg.s], rg.ph);
+        tc_fence_after();
+        const uint32_t d = tmem + (uint32_t)((u & 1) * Cfg::kW + 2 * N);
+        const uint32_t at = tmem + (uint32_t)(Cfg::kSlot0 + 32 * rt.s);
+        const uint64_t dx = desc_sw128(smem_u32(smem + rg.s * Cfg::kStage) + kTileBytes);
+        if (leader) {
+#pragma unroll
+          for (int ks = 0; ks < 4; ++ks) mma_tf32_ts(d, at + 8 * ks, dx + 2 * ks, idesc, (kin != 0 || ks != 0) ? 1u : 0u);
+          mma_commit(&empty[rg.s]);
+          mma_commit(&tfree[rt.s]);
+          if (kb == KB - 1 || kin == KC - 1) mma_commit(&acc_full[u & 1]);
+        }
+        __syncwarp();
+      }
+  } else if (warp < 7) {  // ---------------------------------------- split: A_lo → TMEM
+    const int q = warp & 3;
+    const int t = 32 * q + lane;  // tile row = TMEM lane
+    Ring<S> rg;
+    Ring<2> rt;
+    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x)
+      for (int kb = 0; kb < KB; ++kb, rg.next(), rt.next()) {
+        mbar_wait(&full[rg.s], rg.ph);
+        mbar_wait(&tfree[rt.s], rt.ph ^ 1u);
+        tc_fence_after();
+        const uint8_t* row = smem + rg.s * Cfg::kStage + t * 128;
+        float v[32];
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {  // logical 16-byte chunk c (k = 4c..4c+3) sits at c ^ (t mod 8)
+          const float4 x = *reinterpret_cast<const float4*>(row + ((c ^ (t & 7)) << 4));
+          v[4 * c] = lo_part(x.x);
+          v[4 * c + 1] = lo_part(x.y);
+          v[4 * c + 2] = lo_part(x.z);
+          v[4 * c + 3] = lo_part(x.w);
+        }
+        tmem_st32(tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(Cfg::kSlot0 + 32 * rt.s), v);
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&lo_full[rg.s]);
+      }
+  } else {  // ---------------------------------------------------- epilogue
+    const int q = warp & 3;  // TMEM lane quarter this warp may access
+    int64_t lt = 0;
+    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++lt) {
+      const int64_t row = tile * 128 + 32 * q + lane;
+      for (int kc = 0; kc < nkc; ++kc) {
+        const int64_t u = lt * nkc + kc;
+        mbar_wait(&acc_full[u & 1], (uint32_t)((u >> 1) & 1));
+        tc_fence_after();
+        const uint32_t d = tmem + (uint32_t)((u & 1) * Cfg::kW) + ((uint32_t)(32 * q) << 16);
+#pragma unroll
+        for (int c0 = 0; c0 < N; c0 += 16) {
+          float v[16], w[16], z[16];
+          tmem_ld16(d + c0, v);
+          tmem_ld16(d + N + c0, w);
+          tmem_ld16(d + 2 * N + c0, z);
+          if (row < m) {
+#pragma unroll
+            for (int j = 0; j < 16; ++j)
+              if (c0 + j < l) {
+                double* y = Y + row * l + c0 + j;
+                const double a = ((double)v[j] + (double)z[j]) + (double)w[j];
+                if (kc == 0) *y = cx ? a - cx[c0 + j] : a;
+                else *y += a;
+              }
+          }
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&acc_empty[u & 1]);
+      }
     }
   }
   __syncthreads();
   if (warp == 1) {
-    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(Cfg::kTmemCols));
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(Cfg::kCols));
   }
 }
 
 // ---------------------------------------------------------------- Z = Aᵀ·Y
-struct SplitF {
-  int64_t U, P, cpc;  // units, CTAs, 32-row chunks per 128-column block
-  __host__ __device__ int64_t u0(int64_t p) const { return p * U / P; }
+// Work plan: column blocks (128 columns) in groups of ≤ CBG; CTA p = g·Pg + r
+// owns group g and row chunks [r·R/Pg, (r+1)·R/Pg) (32-row chunks).
+struct AtyPlan {
+  int64_t nb, R;  // column blocks, 32-row chunks
+  int CBG, Gc, Pg;
+  __host__ __device__ int64_t rc0(int r) const { return (int64_t)r * R / Pg; }
 };
 
 template <int N>
-__global__ void __launch_bounds__(kThreads, 1)
+struct AtyCfg {
+  static constexpr int kX = N * 128;
+  static constexpr int kTN = N <= 32 ? 32 : 64;
+  static constexpr int kYS = 3;  // Yᵀ chunk buffers
+  static constexpr int kYBytes = kYS * 2 * kX;
+  static constexpr int kStages = (212 * 1024 - kYBytes) / kTileBytes > 8 ? 8 : (212 * 1024 - kYBytes) / kTileBytes;
+  static constexpr int kSmem = kStages * kTileBytes + kYBytes + 1024 + 512;
+  static constexpr int kSlot0 = 448;  // two 32-column A_lo slots after the accumulators
+  static constexpr int kMaxCB = kSlot0 / kTN;
+};
+
+// warps: 0 TMA producer, 1 hi-MMA issuer, 2 lo-MMA issuer, 3-6 split
+// (A_loᵀ → TMEM), 7-10 epilogue (fp64 flush per accumulation chunk)
+template <int N>
+__global__ void __launch_bounds__(kThreadsTC, 1)
     aty_f32_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmYh,
-                      const __grid_constant__ CUtensorMap tmYl, SplitF sp, int maxslots, int LP,
-                      double* __restrict__ part) {
-  using Cfg = F32Cfg<N, 2>;
-  constexpr int kStagesF = Cfg::kStages;
+                      const __grid_constant__ CUtensorMap tmYl, AtyPlan pl, double* __restrict__ part) {
+  using Cfg = AtyCfg<N>;
+  constexpr int S = Cfg::kStages, YS = Cfg::kYS;
+  constexpr int RC = kKChunk / 32;  // row chunks per fp32 accumulation
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kStagesF * Cfg::kStage);
-  uint64_t* lo_full = full + kStagesF;
-  uint64_t* empty = lo_full + kStagesF;
-  uint64_t* acc_full = empty + kStagesF;
+  uint8_t* ybuf = smem + S * kTileBytes;
+  uint64_t* full = reinterpret_cast<uint64_t*>(ybuf + Cfg::kYBytes);
+  uint64_t* empty = full + S;      // hi commit + lo commit
+  uint64_t* lo_full = empty + S;   // 4 split warps
+  uint64_t* tfree = lo_full + S;   // [2]
+  uint64_t* yfull = tfree + 2;     // [YS]
+  uint64_t* yempty = yfull + YS;   // [YS] hi commit + lo commit
+  uint64_t* hi_done = yempty + YS;  // [S] the stage's hi MMAs done (lo waits on it at chunk starts)
+  uint64_t* acc_full = hi_done + S;  // hi commit + lo commit
   uint64_t* acc_empty = acc_full + 1;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 1);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t p = blockIdx.x;
-  const int64_t ub = sp.u0(p), ue = sp.u0(p + 1);
+  const int p = blockIdx.x, g = p / pl.Pg, r = p - g * pl.Pg;
+  const int64_t cb0 = (int64_t)g * pl.CBG;
+  const int ncb = (int)imin64(pl.CBG, pl.nb - cb0);
+  const int64_t rb = pl.rc0(r), re = pl.rc0(r + 1);
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < kStagesF; ++s) {
+    for (int s = 0; s < S; ++s) {
       mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 2);
       mbar_init(&lo_full[s], 4);
-      mbar_init(&empty[s], 1);
     }
-    mbar_init(acc_full, 1);
+    for (int y = 0; y < YS; ++y) {
+      mbar_init(&yfull[y], 1);
+      mbar_init(&yempty[y], 2);
+    }
+    mbar_init(&tfree[0], 1);
+    mbar_init(&tfree[1], 1);
+    for (int s = 0; s < S; ++s) mbar_init(&hi_done[s], 1);
+    mbar_init(acc_full, 2);
     mbar_init(acc_empty, 4);
     fence_barrier_init();
   }
   if (warp == 1) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
-                 "n"(Cfg::kTmemCols));
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_slot)));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
-  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  tc_fence_before();
   __syncthreads();
-  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
-  if (warp == 0) {
-    if (lane == 0) {
-      prefetch_tmap(&tmA);
-      prefetch_tmap(&tmYh);
-      prefetch_tmap(&tmYl);
-      int s = 0;
-      uint32_t ph = 0;
-      for (int64_t u = ub; u < ue; ++u) {
-        const int64_t cb = u / sp.cpc, rc = u - cb * sp.cpc;
-        mbar_wait(&empty[s], ph ^ 1);
-        uint8_t* st = smem + s * Cfg::kStage;
-        mbar_arrive_expect_tx(&full[s], Cfg::kA + 2 * Cfg::kX);
-#pragma unroll
-        for (int b = 0; b < 4; ++b)  // four [32 rows × 32 cols] boxes = the 32×128 tile
-          tma_load_2d(st + b * 4096, &tmA, (int32_t)(cb * 128 + b * 32), (int32_t)(rc * 32), &full[s]);
-        tma_load_2d(st + Cfg::kXoff, &tmYh, (int32_t)(rc * 32), 0, &full[s]);
-        tma_load_2d(st + Cfg::kXoff + Cfg::kX, &tmYl, (int32_t)(rc * 32), 0, &full[s]);
-        if (++s == kStagesF) { s = 0; ph ^= 1; }
+  if (warp == 0) {  // ----------------------------------------------- producer
+    const bool leader = elect_one();
+    prefetch_tmap(&tmA);
+    prefetch_tmap(&tmYh);
+    prefetch_tmap(&tmYl);
+    Ring<S> rg;
+    Ring<YS> ry;
+    for (int64_t rc = rb; rc < re; ++rc, ry.next()) {
+      mbar_wait(&yempty[ry.s], ry.ph ^ 1u);
+      uint8_t* yb = ybuf + ry.s * 2 * Cfg::kX;
+      if (leader) {
+        mbar_arrive_expect_tx(&yfull[ry.s], 2 * Cfg::kX);
+        tma_load_2d(yb, &tmYh, (int32_t)(rc * 32), 0, &yfull[ry.s]);
+        tma_load_2d(yb + Cfg::kX, &tmYl, (int32_t)(rc * 32), 0, &yfull[ry.s]);
       }
-    }
-  } else if (warp == 1) {
-    if (lane == 0) {
-      constexpr uint32_t idesc = idesc_tf32(128, N);
-      int s = 0;
-      uint32_t ph = 0, aph = 0;
-      bool first = true;
-      for (int64_t u = ub; u < ue; ++u) {
-        const int64_t cb = u / sp.cpc;
-        if (first) {
-          mbar_wait(acc_empty, aph ^ 1);
-          aph ^= 1;
-          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        }
-        mbar_wait(&lo_full[s], ph);
-        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        const uint32_t th = smem_u32(smem + s * Cfg::kStage) + Cfg::kA;  // Aᵀ_hi (128 cols × 32 rows)
-        const uint32_t tl = th + Cfg::kAlo;                              // Aᵀ_lo
-        const uint32_t yh = smem_u32(smem + s * Cfg::kStage) + Cfg::kXoff, yl = yh + Cfg::kX;
-#pragma unroll
-        for (int ks = 0; ks < 4; ++ks) {
-          const uint32_t acc = (!first || ks) ? 1u : 0u;
-          mma_tf32(tmem, desc_sw128(th + ks * 32), desc_sw128(yh + ks * 32), idesc, acc);
-          mma_tf32(tmem, desc_sw128(th + ks * 32), desc_sw128(yl + ks * 32), idesc, 1);
-          mma_tf32(tmem, desc_sw128(tl + ks * 32), desc_sw128(yh + ks * 32), idesc, 1);
-        }
-        mma_commit(&empty[s]);
-        const bool last_of_cb = (u + 1 == ue) || ((u + 1) / sp.cpc != cb);
-        if (last_of_cb) mma_commit(acc_full);
-        first = last_of_cb;
-        if (++s == kStagesF) { s = 0; ph ^= 1; }
-      }
-    }
-  } else {
-    const int t = threadIdx.x - 64;  // column of the 128-column block, 0..127
-    const int q = warp & 3;
-    int s = 0;
-    uint32_t ph = 0, aph = 0;
-    const int64_t cb_first = ub / sp.cpc;
-    for (int64_t u = ub; u < ue; ++u) {
-      const int64_t cb = u / sp.cpc;
-      mbar_wait(&full[s], ph);
-      const uint8_t* a = smem + s * Cfg::kStage;
-      uint8_t* th = smem + s * Cfg::kStage + Cfg::kA;
-      uint8_t* tl = th + Cfg::kAlo;
-      const uint8_t* slab = a + (t >> 5) * 4096;
-      const int cc = t & 31;
-#pragma unroll
-      for (int g = 0; g < 8; ++g) {  // rows 4g..4g+3 of column t → one 16-byte chunk of row t of Aᵀ
-        float4 h, lo;
-        h.x = *reinterpret_cast<const float*>(slab + kmaj(4 * g + 0, cc));
-        h.y = *reinterpret_cast<const float*>(slab + kmaj(4 * g + 1, cc));
-        h.z = *reinterpret_cast<const float*>(slab + kmaj(4 * g + 2, cc));
-        h.w = *reinterpret_cast<const float*>(slab + kmaj(4 * g + 3, cc));
-        lo.x = lo_part(h.x);
-        lo.y = lo_part(h.y);
-        lo.z = lo_part(h.z);
-        lo.w = lo_part(h.w);
-        const uint32_t off = kmaj(t, 4 * g);
-        *reinterpret_cast<float4*>(th + off) = h;
-        *reinterpret_cast<float4*>(tl + off) = lo;
-      }
-      fence_proxy_async();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&lo_full[s]);
-      if (++s == kStagesF) { s = 0; ph ^= 1; }
-      const bool last_of_cb = (u + 1 == ue) || ((u + 1) / sp.cpc != cb);
-      if (last_of_cb) {  // flush: column 32q+lane of the block ← TMEM lane 32q+lane
-        mbar_wait(acc_full, aph);
-        aph ^= 1;
-        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        double* dst = part + ((p * maxslots + (cb - cb_first)) * 128 + 32 * q + lane) * LP;
+      for (int cbi = 0; cbi < ncb; ++cbi, rg.next()) {
+        mbar_wait(&empty[rg.s], rg.ph ^ 1u);
+        uint8_t* st = smem + rg.s * kTileBytes;
+        if (leader) {
+          mbar_arrive_expect_tx(&full[rg.s], kTileBytes);
+#pragma unroll
+          for (int b = 0; b < 4; ++b)  // four [32 rows × 32 cols] boxes (128B_ATOM_32B), MN chunks 4 KB apart
+            tma_load_2d(st + b * 4096, &tmA, (int32_t)((cb0 + cbi) * 128 + b * 32), (int32_t)(rc * 32), &full[rg.s]);
+        }
+        __syncwarp();
+      }
+    }
+  } else if (warp == 1) {  // ---------------------------------------- hi-MMA issuer
+    // D_cb += A·Y_hi + A·Y_lo, A read MN-major (bit 15 of the instruction descriptor)
+    const bool leader = elect_one();
+    constexpr uint32_t idesc = idesc_tf32(128, N) | (1u << 15);
+    Ring<S> rg;
+    Ring<YS> ry;
+    int kin = 0;        // row chunks into the current accumulation chunk
+    uint32_t chph = 0;  // acc_empty phase
+    for (int64_t rc = rb; rc < re; ++rc, ry.next()) {
+      if (kin == 0) {  // a new accumulation chunk: the flush of the last one must be done
+        mbar_wait(acc_empty, chph ^ 1u);
+        chph ^= 1u;
+        tc_fence_after();
+      }
+      const bool chunk_end = (kin == RC - 1) || (rc + 1 == re);
+      mbar_wait(&yfull[ry.s], ry.ph);
+      tc_fence_after();
+      const uint32_t yh = smem_u32(ybuf + ry.s * 2 * Cfg::kX);
+      const uint64_t dh = desc_sw128(yh), dl = desc_sw128(yh + Cfg::kX);
+      for (int cbi = 0; cbi < ncb; ++cbi, rg.next()) {
+        mbar_wait(&full[rg.s], rg.ph);
+        tc_fence_after();
+        const uint32_t d = tmem + (uint32_t)(cbi * Cfg::kTN);
+        const uint64_t da = desc_mn_sw128_32b(smem_u32(smem + rg.s * kTileBytes));
+        if (leader) {
+#pragma unroll
+          for (int ks = 0; ks < 4; ++ks) {
+            mma_tf32(d, da + 64 * ks, dh + 2 * ks, idesc, (kin != 0 || ks != 0) ? 1u : 0u);
+            mma_tf32(d, da + 64 * ks, dl + 2 * ks, idesc, 1u);
+          }
+          mma_commit(&empty[rg.s]);
+          mma_commit(&hi_done[rg.s]);
+          if (cbi == ncb - 1) {
+            mma_commit(&yempty[ry.s]);
+            if (chunk_end) mma_commit(acc_full);
+          }
+        }
+        __syncwarp();
+      }
+      if (++kin == RC) kin = 0;
+    }
+  } else if (warp == 2) {  // ---------------------------------------- lo-MMA issuer
+    // D_cb += A_lo·Y_hi with A_loᵀ read from TMEM (lane = column of A, column = row)
+    const bool leader = elect_one();
+    constexpr uint32_t idesc = idesc_tf32(128, N);
+    Ring<S> rg;
+    Ring<YS> ry;
+    Ring<2> rt;
+    int kin = 0;
+    for (int64_t rc = rb; rc < re; ++rc, ry.next()) {
+      const bool chunk_end = (kin == RC - 1) || (rc + 1 == re);
+      mbar_wait(&yfull[ry.s], ry.ph);
+      tc_fence_after();
+      const uint64_t dh = desc_sw128(smem_u32(ybuf + ry.s * 2 * Cfg::kX));
+      for (int cbi = 0; cbi < ncb; ++cbi, rg.next(), rt.next()) {
+        // at a chunk start the hi issuer's accumulate-off MMA for this block
+        // must have run first (its next hi_done phase needs this stage freed)
+        if (kin == 0) mbar_wait(&hi_done[rg.s], rg.ph);
+        mbar_wait(&lo_full[rg.s], rg.ph);
+        tc_fence_after();
+        const uint32_t d = tmem + (uint32_t)(cbi * Cfg::kTN);
+        const uint32_t at = tmem + (uint32_t)(Cfg::kSlot0 + 32 * rt.s);
+        if (leader) {
+#pragma unroll
+          for (int ks = 0; ks < 4; ++ks) mma_tf32_ts(d, at + 8 * ks, dh + 2 * ks, idesc, 1u);
+          mma_commit(&empty[rg.s]);
+          mma_commit(&tfree[rt.s]);
+          if (cbi == ncb - 1) {
+            mma_commit(&yempty[ry.s]);
+            if (chunk_end) mma_commit(acc_full);
+          }
+        }
+        __syncwarp();
+      }
+      if (++kin == RC) kin = 0;
+    }
+  } else if (warp < 7) {  // ---------------------------------------- split: A_loᵀ → TMEM
+    const int q = warp & 3;
+    const int t = 32 * q + lane;  // column of the block = TMEM lane
+    const int64_t total = (re - rb) * ncb;
+    // element (row ρ, column t) of the 128B_ATOM_32B tile: box t/32, 128-byte
+    // row ρ, 32-byte chunk ((t mod 32)/8) XOR (ρ mod 4)
+    const uint32_t cb_off = (uint32_t)((t >> 5) * 4096 + ((t & 7) << 2));
+    const int c8 = (t & 31) >> 3;
+    Ring<S> rg;
+    Ring<2> rt;
+    for (int64_t i = 0; i < total; ++i, rg.next(), rt.next()) {
+      mbar_wait(&full[rg.s], rg.ph);
+      mbar_wait(&tfree[rt.s], rt.ph ^ 1u);
+      tc_fence_after();
+      const uint8_t* tile = smem + rg.s * kTileBytes + cb_off;
+      float v[32];
+#pragma unroll
+      for (int rho = 0; rho < 32; ++rho)
+        v[rho] = lo_part(*reinterpret_cast<const float*>(tile + rho * 128 + ((c8 ^ (rho & 3)) << 5)));
+      tmem_st32(tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(Cfg::kSlot0 + 32 * rt.s), v);
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&lo_full[rg.s]);
+    }
+  } else {  // ---------------------------------------------------- epilogue: fp64 flush per chunk
+    const int q = warp & 3;
+    const int64_t nch = (re - rb + RC - 1) / RC;
+    for (int64_t ch = 0; ch < nch; ++ch) {
+      mbar_wait(acc_full, (uint32_t)(ch & 1));
+      tc_fence_after();
+      for (int cbi = 0; cbi < ncb; ++cbi) {
+        double* dst = part + (((int64_t)p * pl.CBG + cbi) * 128 + 32 * q + lane) * N;
+        const uint32_t d = tmem + (uint32_t)(cbi * Cfg::kTN) + ((uint32_t)(32 * q) << 16);
 #pragma unroll
         for (int c0 = 0; c0 < N; c0 += 16) {
           float v[16];
-          tmem_ld16(tmem + ((uint32_t)(32 * q) << 16) + c0, v);
+          tmem_ld16(d + c0, v);
 #pragma unroll
-          for (int j = 0; j < 16; ++j)
-            if (c0 + j < LP) dst[c0 + j] = (double)v[j];
+          for (int j = 0; j < 16; ++j) dst[c0 + j] = ch == 0 ? (double)v[j] : dst[c0 + j] + (double)v[j];
         }
-        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-        __syncwarp();
-        if (lane == 0) mbar_arrive(acc_empty);
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(acc_empty);
+    }
+    if (nch == 0) {  // no rows: zero partial
+      for (int cbi = 0; cbi < ncb; ++cbi) {
+        double* dst = part + (((int64_t)p * pl.CBG + cbi) * 128 + 32 * q + lane) * N;
+        for (int j = 0; j < N; ++j) dst[j] = 0.0;
       }
     }
   }
   __syncthreads();
   if (warp == 1) {
-    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(Cfg::kTmemCols));
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+  }
+}
+
+// Z[c][j] = Σ_{r ascending} part[g·Pg + r][c/128 − g·CBG][c mod 128][j] − cmean[c]·sy[j]
+// (g = ⌊c/128⌋ / CBG).  One warp per output: lane λ sums r ≡ λ (mod 32), then
+// a fixed shuffle tree — deterministic.
+__global__ void aty_f32_reduce_kernel(const double* __restrict__ part, AtyPlan pl, int LP, int64_t n, int l,
+                                      const double* __restrict__ cmean, const double* __restrict__ sy,
+                                      double* __restrict__ Z) {
+  const int64_t total = n * l;
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t idx = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); idx < total; idx += warps) {
+    const int64_t c = idx / l;
+    const int j = (int)(idx - c * l);
+    const int64_t cb = c >> 7;
+    const int g = (int)(cb / pl.CBG), cbi = (int)(cb - (int64_t)g * pl.CBG);
+    double s = 0.0;
+    for (int r = lane; r < pl.Pg; r += 32)
+      s += part[((((int64_t)g * pl.Pg + r) * pl.CBG + cbi) * 128 + (c & 127)) * LP + j];
+    s = warp_sum(s);
+    if (lane == 0) Z[idx] = cmean ? s - cmean[c] * sy[j] : s;
   }
 }
 
@@ -428,14 +649,15 @@ PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
   return fn;
 }
 
-CUtensorMap tmap_f32(const void* base, int64_t inner, int64_t outer, int64_t ld_elems, int box_inner, int box_outer) {
+CUtensorMap tmap_f32(const void* base, int64_t inner, int64_t outer, int64_t ld_elems, int box_inner, int box_outer,
+                     CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_128B) {
   CUtensorMap tm;
   cuuint64_t dims[2] = {(cuuint64_t)inner, (cuuint64_t)outer};
   cuuint64_t strides[1] = {(cuuint64_t)ld_elems * 4};
   cuuint32_t box[2] = {(cuuint32_t)box_inner, (cuuint32_t)box_outer};
   cuuint32_t estr[2] = {1, 1};
   CUresult r = get_encode()(&tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(base), dims, strides, box,
-                            estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                            estr, CU_TENSOR_MAP_INTERLEAVE_NONE, swz,
                             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   RPCA_REQUIRE(r == CUDA_SUCCESS, RPCA_E_CUDA, "cuTensorMapEncodeTiled(f32) failed (%d)", (int)r);
   return tm;
@@ -451,47 +673,56 @@ void split_transpose(Ctx& c, const double* X, int64_t K, int l, int Npad, int64_
 }
 
 template <int N>
-void launch_ax(Ctx& c, const DenseA& A, const float* hi, const float* lo, int64_t Kpad, int l, double* Y) {
-  using Cfg = F32Cfg<N, 1>;
+void launch_ax(Ctx& c, const DenseA& A, const float* hi, const float* lo, int64_t Kpad, int l, const double* cx,
+               double* Y) {
+  using Cfg = AxCfg<N>;
   const CUtensorMap tA = tmap_f32(A.a, A.n, A.m, A.lda, 32, 128);
   const CUtensorMap tH = tmap_f32(hi, Kpad, N, Kpad, 32, N);
   const CUtensorMap tL = tmap_f32(lo, Kpad, N, Kpad, 32, N);
   ensure_smem((const void*)ax_f32_tc_kernel<N>, Cfg::kSmem);
   const int64_t ntiles = cdiv(A.m, 128);
   const int grid = (int)std::min<int64_t>(ntiles, c.num_sms);
-  ax_f32_tc_kernel<N><<<grid, kThreads, Cfg::kSmem, c.stream>>>(tA, tH, tL, A.m, l, ntiles, (int)(Kpad / 32), Y);
+  ax_f32_tc_kernel<N><<<grid, kThreadsTC, Cfg::kSmem, c.stream>>>(tA, tH, tL, A.m, l, ntiles, (int)(Kpad / 32), cx,
+                                                                   Y);
   RPCA_CHECK_LAUNCH();
   count_launch(c, 1, c.tag ? c.tag : "ax_f32_tc");
 }
 
 template <int N>
-void launch_aty(Ctx& c, const DenseA& A, const float* hi, const float* lo, int64_t Kpad, const SplitF& sp,
-                int maxslots, double* part) {
-  using Cfg = F32Cfg<N, 2>;
-  const CUtensorMap tA = tmap_f32(A.a, A.n, A.m, A.lda, 32, 32);
+AtyPlan make_plan(Ctx& c, const DenseA& A) {
+  AtyPlan pl;
+  pl.nb = cdiv(A.n, 128);
+  pl.R = cdiv(A.m, 32);
+  pl.CBG = (int)std::min<int64_t>(pl.nb, AtyCfg<N>::kMaxCB);
+  pl.Gc = (int)cdiv(pl.nb, pl.CBG);
+  pl.Pg = (int)std::max<int64_t>(1, std::min<int64_t>(pl.R, c.num_sms / pl.Gc));
+  return pl;
+}
+
+template <int N>
+void launch_aty(Ctx& c, const DenseA& A, const float* hi, const float* lo, int64_t Kpad, const AtyPlan& pl,
+                double* part) {
+  using Cfg = AtyCfg<N>;
+  const CUtensorMap tA = tmap_f32(A.a, A.n, A.m, A.lda, 32, 32, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
   const CUtensorMap tH = tmap_f32(hi, Kpad, N, Kpad, 32, N);
   const CUtensorMap tL = tmap_f32(lo, Kpad, N, Kpad, 32, N);
   ensure_smem((const void*)aty_f32_tc_kernel<N>, Cfg::kSmem);
-  aty_f32_tc_kernel<N><<<(unsigned)sp.P, kThreads, Cfg::kSmem, c.stream>>>(tA, tH, tL, sp, maxslots, N, part);
+  aty_f32_tc_kernel<N><<<(unsigned)(pl.Gc * pl.Pg), kThreadsTC, Cfg::kSmem, c.stream>>>(tA, tH, tL, pl, part);
   RPCA_CHECK_LAUNCH();
   count_launch(c, 1, c.tag ? c.tag : "aty_f32_tc");
 }
 
-SplitF make_split(Ctx& c, const DenseA& A) {
-  SplitF sp;
-  sp.cpc = cdiv(A.m, 32);
-  sp.U = cdiv(A.n, 128) * sp.cpc;
-  sp.P = std::min<int64_t>(c.num_sms, sp.U);
-  return sp;
-}
-
-int max_slots(const SplitF& sp) {
-  int mx = 1;
-  for (int64_t p = 0; p < sp.P; ++p) {
-    const int64_t a = sp.u0(p), b = sp.u0(p + 1);
-    if (b > a) mx = std::max<int>(mx, (int)((b - 1) / sp.cpc - a / sp.cpc + 1));
-  }
-  return mx;
+template <int N>
+void aty_f32_run(Ctx& c, const DenseA& A, const float* hi, const float* lo, int64_t Kpad, int l,
+                 const double* cmean, const double* sy, double* Z, Arena& ar) {
+  const AtyPlan pl = make_plan<N>(c, A);
+  double* part = ar.get<double>((size_t)pl.Gc * pl.Pg * pl.CBG * 128 * N);
+  launch_aty<N>(c, A, hi, lo, Kpad, pl, part);
+  const int64_t total = A.n * l;
+  const unsigned grid = (unsigned)std::min<int64_t>(cdiv(total, 8), (int64_t)c.num_sms * 32);
+  aty_f32_reduce_kernel<<<grid, 256, 0, c.stream>>>(part, pl, N, A.n, l, cmean, sy, Z);
+  RPCA_CHECK_LAUNCH();
+  count_launch(c, 1, "aty_reduce");
 }
 
 }  // namespace
@@ -509,52 +740,50 @@ size_t ax_f32_ws_bytes(const DenseA& A, int l) {
   return s.total;
 }
 
-void dense_ax_f32(Ctx& c, const DenseA& A, const double* X, int l, double* Y, Arena& ar) {
+void dense_ax_f32(Ctx& c, const DenseA& A, const double* X, int l, const double* cx, double* Y, Arena& ar) {
   const int Np = npad_for(l);
   const int64_t Kpad = cdiv(A.n, 64) * 64;
   float* hi = ar.get<float>((size_t)Np * Kpad);
   float* lo = ar.get<float>((size_t)Np * Kpad);
   split_transpose(c, X, A.n, l, Np, Kpad, hi, lo);
   switch (Np) {
-    case 16: launch_ax<16>(c, A, hi, lo, Kpad, l, Y); break;
-    case 32: launch_ax<32>(c, A, hi, lo, Kpad, l, Y); break;
-    case 48: launch_ax<48>(c, A, hi, lo, Kpad, l, Y); break;
-    default: launch_ax<64>(c, A, hi, lo, Kpad, l, Y); break;
+    case 16: launch_ax<16>(c, A, hi, lo, Kpad, l, cx, Y); break;
+    case 32: launch_ax<32>(c, A, hi, lo, Kpad, l, cx, Y); break;
+    case 48: launch_ax<48>(c, A, hi, lo, Kpad, l, cx, Y); break;
+    default: launch_ax<64>(c, A, hi, lo, Kpad, l, cx, Y); break;
   }
 }
 
 size_t aty_f32_ws_bytes(Ctx& c, const DenseA& A, int l) {
-  const SplitF sp = make_split(c, A);
+  const int Np = npad_for(l);
   Sizer s;
   const int64_t Kpad = cdiv(A.m, 64) * 64;
-  s.add<float>((size_t)npad_for(l) * Kpad);
-  s.add<float>((size_t)npad_for(l) * Kpad);
-  s.add<double>((size_t)sp.P * max_slots(sp) * 128 * npad_for(l));
+  s.add<float>((size_t)Np * Kpad);
+  s.add<float>((size_t)Np * Kpad);
+  AtyPlan pl;
+  switch (Np) {
+    case 16: pl = make_plan<16>(c, A); break;
+    case 32: pl = make_plan<32>(c, A); break;
+    case 48: pl = make_plan<48>(c, A); break;
+    default: pl = make_plan<64>(c, A); break;
+  }
+  s.add<double>((size_t)pl.Gc * pl.Pg * pl.CBG * 128 * Np);
   return s.total;
 }
 
-// Z partials; the caller reduces them with aty_reduce (dense_aty.cu)
-void dense_aty_f32_partials(Ctx& c, const DenseA& A, const double* Y, int l, double** part_out, int64_t* P,
-                            int* maxslots, int64_t* cpc, int* LP, Arena& ar) {
+void dense_aty_f32(Ctx& c, const DenseA& A, const double* Y, int l, const double* cmean, const double* sy,
+                   double* Z, Arena& ar) {
   const int Np = npad_for(l);
   const int64_t Kpad = cdiv(A.m, 64) * 64;
   float* hi = ar.get<float>((size_t)Np * Kpad);
   float* lo = ar.get<float>((size_t)Np * Kpad);
   split_transpose(c, Y, A.m, l, Np, Kpad, hi, lo);
-  const SplitF sp = make_split(c, A);
-  const int ms = max_slots(sp);
-  double* part = ar.get<double>((size_t)sp.P * ms * 128 * Np);
-  *part_out = part;
   switch (Np) {
-    case 16: launch_aty<16>(c, A, hi, lo, Kpad, sp, ms, part); break;
-    case 32: launch_aty<32>(c, A, hi, lo, Kpad, sp, ms, part); break;
-    case 48: launch_aty<48>(c, A, hi, lo, Kpad, sp, ms, part); break;
-    default: launch_aty<64>(c, A, hi, lo, Kpad, sp, ms, part); break;
+    case 16: aty_f32_run<16>(c, A, hi, lo, Kpad, l, cmean, sy, Z, ar); break;
+    case 32: aty_f32_run<32>(c, A, hi, lo, Kpad, l, cmean, sy, Z, ar); break;
+    case 48: aty_f32_run<48>(c, A, hi, lo, Kpad, l, cmean, sy, Z, ar); break;
+    default: aty_f32_run<64>(c, A, hi, lo, Kpad, l, cmean, sy, Z, ar); break;
   }
-  *P = sp.P;
-  *maxslots = ms;
-  *cpc = sp.cpc;
-  *LP = Np;
 }
 
 }  // namespace rpca

@@ -315,12 +315,16 @@ struct Op {
 // Y = A·X [− 1·(c·X)]
 void apply_ax(Ctx& c, const MatV& A, const double* cmean, const double* X, int l, double* Y, Arena& ar) {
   const size_t mark = ar.off;
-  if (A.csr) csr_spmm(c, A.a, X, l, Y);
-  else dense_ax(c, A.d, X, l, Y, ar);
+  double* cx = nullptr;
   if (cmean) {
-    double* cx = ar.get<double>(kMaxL);
+    cx = ar.get<double>(kMaxL);
     weighted_colsum(c, cmean, X, A.n, l, cx, ar);
-    sub_rank1(c, Y, A.m, l, nullptr, cx);
+  }
+  if (A.csr) {
+    csr_spmm(c, A.a, X, l, Y);
+    if (cx) sub_rank1(c, Y, A.m, l, nullptr, cx);
+  } else {
+    dense_ax(c, A.d, X, l, Y, ar, cx);
   }
   ar.off = mark;
 }

@@ -158,7 +158,8 @@ struct DenseA {
   int64_t m, n, lda;  // m = local rows
 };
 size_t ax_ws_bytes(const DenseA& A, int l);
-void dense_ax(Ctx& c, const DenseA& A, const double* X, int l, double* Y, Arena& ar);
+// Y = A·X [− 1·cxᵀ]  (cx = c·X, the centring correction of PAPER.md:430; may be NULL)
+void dense_ax(Ctx& c, const DenseA& A, const double* X, int l, double* Y, Arena& ar, const double* cx = nullptr);
 size_t aty_ws_bytes(Ctx& c, const DenseA& A, int l);
 // Z (n×l) = Aᵀ·Y [− cmean ⊗ colsum(Y)] (cmean may be NULL)
 void dense_aty(Ctx& c, const DenseA& A, const double* Y, int l, const double* cmean, double* Z, Arena& ar);
@@ -175,10 +176,12 @@ void csr_colmeans(Ctx& c, const CsrA& T, int64_t m_total, double* cmean);
 // dense_f32_tc.cu — fp32 A on tcgen05 (3×TF32)
 bool f32_tc_ok(const DenseA& A);
 size_t ax_f32_ws_bytes(const DenseA& A, int l);
-void dense_ax_f32(Ctx& c, const DenseA& A, const double* X, int l, double* Y, Arena& ar);
+// Y = A·X [− 1·cxᵀ] (cx may be NULL)
+void dense_ax_f32(Ctx& c, const DenseA& A, const double* X, int l, const double* cx, double* Y, Arena& ar);
 size_t aty_f32_ws_bytes(Ctx& c, const DenseA& A, int l);
-void dense_aty_f32_partials(Ctx& c, const DenseA& A, const double* Y, int l, double** part, int64_t* P, int* maxslots,
-                            int64_t* cpc, int* LP, Arena& ar);
+// Z = Aᵀ·Y [− cmean·syᵀ]
+void dense_aty_f32(Ctx& c, const DenseA& A, const double* Y, int l, const double* cmean, const double* sy,
+                   double* Z, Arena& ar);
 void aty_reduce_partials(Ctx& c, const double* part, int64_t U, int64_t P, int64_t cpc, int maxslots, int64_t n,
                          int l, int LP, const double* cmean, const double* sy, double* Z);
 
