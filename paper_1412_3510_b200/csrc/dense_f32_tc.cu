@@ -134,6 +134,9 @@ __device__ __forceinline__ bool elect_one() {
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 
+#ifndef ATY_SLOTS
+#define ATY_SLOTS 2
+#endif
 constexpr int kThreadsTC = 352;  // 11 warps: producer, hi-MMA, lo-MMA, 4 split, 4 epilogue
 constexpr int kTileBytes = 128 * 128;  // 16 KB A tile
 constexpr int kKChunk = 4096;          // max products per fp32 accumulation (Q15)
@@ -160,6 +163,7 @@ struct AxCfg {
   static constexpr int kW = (3 * N + 31) / 32 * 32;
   static constexpr int kSlot0 = 2 * kW;
   static constexpr int kCols = kSlot0 + 64 <= 256 ? 256 : 512;
+  static constexpr int kNS = (kCols - kSlot0) / 32 >= 4 ? 4 : 2;  // A_lo slots
 };
 
 // ---------------------------------------------------------------- Y = A·X
@@ -178,8 +182,8 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + S * Cfg::kStage);
   uint64_t* empty = full + S;       // hi commit + lo commit
   uint64_t* lo_full = empty + S;    // 4 split warps (A_lo in TMEM)
-  uint64_t* tfree = lo_full + S;    // [2] A_lo slot free (lo commit)
-  uint64_t* ustart = tfree + 2;     // [2] first hi MMAs of unit u done (lo may accumulate), by u & 1
+  uint64_t* tfree = lo_full + S;    // [kNS] A_lo slot free (lo commit)
+  uint64_t* ustart = tfree + Cfg::kNS;     // [2] first hi MMAs of unit u done (lo may accumulate), by u & 1
   uint64_t* acc_full = ustart + 2;  // [2] hi commit + lo commit
   uint64_t* acc_empty = acc_full + 2;  // [2] 4 epilogue warps
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
@@ -192,8 +196,8 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
       mbar_init(&empty[s], 2);
       mbar_init(&lo_full[s], 4);
     }
+    for (int a = 0; a < Cfg::kNS; ++a) mbar_init(&tfree[a], 1);
     for (int a = 0; a < 2; ++a) {
-      mbar_init(&tfree[a], 1);
       mbar_init(&ustart[a], 1);
       mbar_init(&acc_full[a], 2);
       mbar_init(&acc_empty[a], 4);
@@ -262,7 +266,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
     const bool leader = elect_one();
     constexpr uint32_t idesc = idesc_tf32(128, N);
     Ring<S> rg;
-    Ring<2> rt;
+    Ring<Cfg::kNS> rt;
     int64_t u = -1;
     for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x)
       for (int kb = 0; kb < KB; ++kb, rg.next(), rt.next()) {
@@ -290,7 +294,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
     const int q = warp & 3;
     const int t = 32 * q + lane;  // tile row = TMEM lane
     Ring<S> rg;
-    Ring<2> rt;
+    Ring<Cfg::kNS> rt;
     for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x)
       for (int kb = 0; kb < KB; ++kb, rg.next(), rt.next()) {
         mbar_wait(&full[rg.s], rg.ph);
@@ -366,9 +370,10 @@ struct AtyCfg {
   static constexpr int kTN = N <= 32 ? 32 : 64;
   static constexpr int kYS = 3;  // Yᵀ chunk buffers
   static constexpr int kYBytes = kYS * 2 * kX;
-  static constexpr int kStages = (212 * 1024 - kYBytes) / kTileBytes > 8 ? 8 : (212 * 1024 - kYBytes) / kTileBytes;
+  static constexpr int kStages = (212 * 1024 - kYBytes) / kTileBytes > 10 ? 10 : (212 * 1024 - kYBytes) / kTileBytes;
   static constexpr int kSmem = kStages * kTileBytes + kYBytes + 1024 + 512;
-  static constexpr int kSlot0 = 448;  // two 32-column A_lo slots after the accumulators
+  static constexpr int kNS = ATY_SLOTS;                 // 32-column A_lo slots after the accumulators
+  static constexpr int kSlot0 = 512 - 32 * kNS;
   static constexpr int kMaxCB = kSlot0 / kTN;
 };
 
@@ -387,8 +392,8 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
   uint64_t* full = reinterpret_cast<uint64_t*>(ybuf + Cfg::kYBytes);
   uint64_t* empty = full + S;      // hi commit + lo commit
   uint64_t* lo_full = empty + S;   // 4 split warps
-  uint64_t* tfree = lo_full + S;   // [2]
-  uint64_t* yfull = tfree + 2;     // [YS]
+  uint64_t* tfree = lo_full + S;   // [kNS]
+  uint64_t* yfull = tfree + Cfg::kNS;  // [YS]
   uint64_t* yempty = yfull + YS;   // [YS] hi commit + lo commit
   uint64_t* hi_done = yempty + YS;  // [S] the stage's hi MMAs done (lo waits on it at chunk starts)
   uint64_t* acc_full = hi_done + S;  // hi commit + lo commit
@@ -410,8 +415,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
       mbar_init(&yfull[y], 1);
       mbar_init(&yempty[y], 2);
     }
-    mbar_init(&tfree[0], 1);
-    mbar_init(&tfree[1], 1);
+    for (int a = 0; a < Cfg::kNS; ++a) mbar_init(&tfree[a], 1);
     for (int s = 0; s < S; ++s) mbar_init(&hi_done[s], 1);
     mbar_init(acc_full, 2);
     mbar_init(acc_empty, 4);
@@ -501,7 +505,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
     constexpr uint32_t idesc = idesc_tf32(128, N);
     Ring<S> rg;
     Ring<YS> ry;
-    Ring<2> rt;
+    Ring<Cfg::kNS> rt;
     int kin = 0;
     for (int64_t rc = rb; rc < re; ++rc, ry.next()) {
       const bool chunk_end = (kin == RC - 1) || (rc + 1 == re);
@@ -539,7 +543,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
     const uint32_t cb_off = (uint32_t)((t >> 5) * 4096 + ((t & 7) << 2));
     const int c8 = (t & 31) >> 3;
     Ring<S> rg;
-    Ring<2> rt;
+    Ring<Cfg::kNS> rt;
     for (int64_t i = 0; i < total; ++i, rg.next(), rt.next()) {
       mbar_wait(&full[rg.s], rg.ph);
       mbar_wait(&tfree[rt.s], rt.ph ^ 1u);

@@ -305,12 +305,27 @@ size_t host_copy_bytes(const rpca_mat* A) {
 // With a multi-rank communicator A's rows are sharded: vectors of length m
 // are row shards, vectors of length n are replicated, and every Aᵀ·(·) —
 // a sum over rows — is all-reduced.
+// Implicit column centring as the projector P = I − 11ᵀ/m
+// on the m-long side: (A − 1c)·X = P·(A·X) and (A − 1c)ᵀ·Y = Aᵀ·(P·Y), since
+// c·X = 1ᵀ(A·X)/m.  Equal to the paper's rank-1 corrections in exact
+// arithmetic (reading Q8) and it needs no column-means pass over A.
 struct Op {
   MatV A;
-  const double* cmean;
+  bool centered;
+  int64_t m_total;  // global rows of A (the mean is over all ranks' rows)
   bool trans;
   bool sharded;
 };
+
+// Y ← P·Y for an m-long block (rows of this shard), column sums over the global rows
+void center_block(Ctx& c, double* Y, int64_t rows, int l, int64_t m_total, bool sharded, Arena& ar) {
+  const size_t mark = ar.off;
+  double* s = ar.get<double>(kMaxL);
+  weighted_colsum(c, nullptr, Y, rows, l, s, ar);
+  if (sharded) allreduce_sum(c, s, (size_t)l);
+  sub_rank1(c, Y, rows, l, nullptr, s, 1.0 / (double)m_total);
+  ar.off = mark;
+}
 
 // Y = A·X [− 1·(c·X)]
 void apply_ax(Ctx& c, const MatV& A, const double* cmean, const double* X, int l, double* Y, Arena& ar) {
@@ -354,19 +369,23 @@ void colmeans(Ctx& c, const MatV& A, int64_t m_total, double* cmean, Arena& ar, 
   if (sharded) allreduce_sum(c, cmean, A.n);
 }
 
-void fwd(Ctx& c, const Op& F, const double* X, int l, double* Y, Arena& ar) {
-  if (F.trans) {
-    apply_aty(c, F.A, F.cmean, X, l, Y, ar);
+void fwd(Ctx& c, const Op& F, double* X, int l, double* Y, Arena& ar) {
+  if (F.trans) {  // F = A_cᵀ: Y = Aᵀ·(P·X)
+    if (F.centered) center_block(c, X, F.A.m, l, F.m_total, F.sharded, ar);
+    apply_aty(c, F.A, nullptr, X, l, Y, ar);
     if (F.sharded) allreduce_sum(c, Y, (size_t)F.A.n * l);
-  } else {
-    apply_ax(c, F.A, F.cmean, X, l, Y, ar);
+  } else {  // Y = P·(A·X)
+    apply_ax(c, F.A, nullptr, X, l, Y, ar);
+    if (F.centered) center_block(c, Y, F.A.m, l, F.m_total, F.sharded, ar);
   }
 }
-void adj(Ctx& c, const Op& F, const double* Y, int l, double* Z, Arena& ar) {
-  if (F.trans) {
-    apply_ax(c, F.A, F.cmean, Y, l, Z, ar);
-  } else {
-    apply_aty(c, F.A, F.cmean, Y, l, Z, ar);
+void adj(Ctx& c, const Op& F, double* Y, int l, double* Z, Arena& ar) {
+  if (F.trans) {  // Z = P·(A·Y)
+    apply_ax(c, F.A, nullptr, Y, l, Z, ar);
+    if (F.centered) center_block(c, Z, F.A.m, l, F.m_total, F.sharded, ar);
+  } else {  // Z = Aᵀ·(P·Y)
+    if (F.centered) center_block(c, Y, F.A.m, l, F.m_total, F.sharded, ar);
+    apply_aty(c, F.A, nullptr, Y, l, Z, ar);
     if (F.sharded) allreduce_sum(c, Z, (size_t)F.A.n * l);
   }
 }
@@ -483,7 +502,6 @@ void pca(Ctx& c, const rpca_mat* Am, int64_t k, int raw, int its, int64_t l, uin
   sz.add<char>(host_copy_bytes(Am));
   sz.add<double>(nin * l);   // Zb
   sz.add<double>(nout * l);  // Yb
-  sz.add<double>(n);         // cmean
   sz.add<double>(4 * l * l + 4 * l);
   sz.add<double>(std::max(nin, nout) * k);  // V-side temp
   sz.add<double>(k);                        // signs
@@ -509,7 +527,6 @@ void pca(Ctx& c, const rpca_mat* Am, int64_t k, int raw, int its, int64_t l, uin
     const MatV dA = device_view(c, Am, ar);
     double* Zb = ar.get<double>(nin * l);
     double* Yb = ar.get<double>(nout * l);
-    double* cmean = ar.get<double>(n);
     double* R = ar.get<double>(l * l);
     double* W = ar.get<double>(l * l);
     double* Vr = ar.get<double>(l * l);
@@ -524,13 +541,7 @@ void pca(Ctx& c, const rpca_mat* Am, int64_t k, int raw, int its, int64_t l, uin
     }
     // the m-long block is the sharded one
     const Blk Y{Yb, nout, sh && !trans, r0}, Z{Zb, nin, sh && trans, r0};
-    Op F{dA, nullptr, trans, sh};
-    if (!raw) {
-      const size_t mark = ar.off;
-      colmeans(c, dA, m, cmean, ar, sh);
-      ar.off = mark;
-      F.cmean = cmean;
-    }
+    Op F{dA, !raw, m, trans, sh};
     // Ω (nin×l; for the sketched Aᵀ, this rank's rows of the m×l Ω); the fp32
     // path consumes fl32(Ω) exactly as the oracle does
     omega(c, seed, 0u, nin, l, dist, odt == RPCA_F32, Zb, trans ? r0 : 0);

@@ -127,7 +127,9 @@ void pack_y(Ctx& c, const double* Y, int64_t m, int l, double* Yp);
 // v[j] = Σ_k a[k]·X[k][j] (a may be NULL ⇒ all-ones), fixed-order reduction
 void weighted_colsum(Ctx& c, const double* a, const double* X, int64_t rows, int l, double* v, Arena& ar,
                      int64_t ldx = 0);
-void sub_rank1(Ctx& c, double* Y, int64_t rows, int l, const double* u /*rows or NULL=ones*/, const double* v);
+// Y −= α·u·vᵀ (u = NULL ⇒ ones)
+void sub_rank1(Ctx& c, double* Y, int64_t rows, int l, const double* u /*rows or NULL=ones*/, const double* v,
+               double alpha = 1.0);
 void colmeans_dense(Ctx& c, const void* A, int dtype, int64_t m, int64_t n, int64_t lda, int64_t m_total,
                     double* cmean, Arena& ar);
 // Out (rows×k, ld ldo, dtype out_dtype) = In (rows×l) · W[:, :k] (W l×l) · diag(sign)

@@ -87,13 +87,13 @@ __global__ void sum_partials_wide_kernel(const double* __restrict__ part, int64_
 }
 
 __global__ void sub_rank1_kernel(double* __restrict__ Y, int64_t rows, int l, const double* __restrict__ u,
-                                 const double* __restrict__ v) {
+                                 const double* __restrict__ v, double alpha) {
   const int64_t total = rows * l;
   for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
        idx += (int64_t)gridDim.x * blockDim.x) {
     const int64_t i = idx / l;
     const int j = (int)(idx - i * l);
-    Y[idx] -= (u ? u[i] : 1.0) * v[j];
+    Y[idx] -= (u ? u[i] : 1.0) * (alpha * v[j]);
   }
 }
 
@@ -340,8 +340,8 @@ void weighted_colsum(Ctx& c, const double* a, const double* X, int64_t rows, int
   count_launch(c, 2);
 }
 
-void sub_rank1(Ctx& c, double* Y, int64_t rows, int l, const double* u, const double* v) {
-  sub_rank1_kernel<<<grid_for(c, rows * l), 256, 0, c.stream>>>(Y, rows, l, u, v);
+void sub_rank1(Ctx& c, double* Y, int64_t rows, int l, const double* u, const double* v, double alpha) {
+  sub_rank1_kernel<<<grid_for(c, rows * l), 256, 0, c.stream>>>(Y, rows, l, u, v, alpha);
   RPCA_CHECK_LAUNCH();
   count_launch(c);
 }
