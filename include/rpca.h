@@ -111,6 +111,13 @@ rpca_status rpca_launch_count(rpca_ctx* ctx, int64_t* count);
  * (duration = gap to the previous event; launches are stream-serialised) into
  * buf (NUL-terminated, truncated to cap); *needed = full length.            */
 rpca_status rpca_profile_begin(rpca_ctx* ctx);
+/* mode RPCA_PROFILE_ALL (= rpca_profile_begin) or RPCA_PROFILE_PASSES: events
+ * only around the pass kernels that stream A (the other intervals are reported
+ * as "gap"), which keeps event overhead out of a timed region; RPCA_E_ARG for
+ * any other mode */
+#define RPCA_PROFILE_ALL 1
+#define RPCA_PROFILE_PASSES 2
+rpca_status rpca_profile_begin_mode(rpca_ctx* ctx, int mode);
 rpca_status rpca_profile_end(rpca_ctx* ctx, char* buf, size_t cap, size_t* needed);
 
 /* ---- multi-GPU (rows of A sharded across ranks) ---------

@@ -75,6 +75,7 @@ def _load():
             "rpca_launch_count": [vp, C.POINTER(i64)],
             "rpca_workspace_size": [vp, C.POINTER(C.c_size_t)],
             "rpca_profile_begin": [vp],
+            "rpca_profile_begin_mode": [vp, i32],
             "rpca_profile_end": [vp, C.c_char_p, C.c_size_t, C.POINTER(C.c_size_t)],
             "rpca_comm_unique_id": [vp, C.c_size_t],
             "rpca_comm_init": [vp, i32, i32, vp],
@@ -262,16 +263,19 @@ def launch_count(device=None) -> int:
 
 
 class profile:
-    """Context manager timing every library launch on the current stream:
-    ``with profile() as p: ...`` then ``p.records`` = [(kernel, ms), ...]."""
+    """Context manager timing library launches on the current stream:
+    ``with profile() as p: ...`` then ``p.records`` = [(kernel, ms), ...].
+    ``passes_only=True`` records events only around the pass kernels that
+    stream A (everything between them is reported as "gap")."""
 
-    def __init__(self, device=None):
+    def __init__(self, device=None, passes_only=False):
         self.device = torch.device("cuda", torch.cuda.current_device() if device is None else device)
         self.records = []
+        self.mode = 2 if passes_only else 1
 
     def __enter__(self):
         L, h = _ctx(self.device)
-        _check(L.rpca_profile_begin(h))
+        _check(L.rpca_profile_begin_mode(h, self.mode))
         return self
 
     def __exit__(self, *exc):

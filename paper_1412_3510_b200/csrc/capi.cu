@@ -128,18 +128,20 @@ rpca_status rpca_launch_count(rpca_ctx* c, int64_t* count) {
   return RPCA_OK;
 }
 
-rpca_status rpca_profile_begin(rpca_ctx* c) {
-  if (!c) return RPCA_E_ARG;
+rpca_status rpca_profile_begin(rpca_ctx* c) { return rpca_profile_begin_mode(c, RPCA_PROFILE_ALL); }
+
+rpca_status rpca_profile_begin_mode(rpca_ctx* c, int mode) {
+  if (!c || (mode != RPCA_PROFILE_ALL && mode != RPCA_PROFILE_PASSES)) return RPCA_E_ARG;
   return guard([&] {
     c->prof_out.clear();
-    c->prof = true;
+    c->prof = mode;
   });
 }
 
 rpca_status rpca_profile_end(rpca_ctx* c, char* buf, size_t cap, size_t* needed) {
   if (!c) return RPCA_E_ARG;
   return guard([&] {
-    c->prof = false;
+    c->prof = 0;
     RPCA_CUDA(cudaStreamSynchronize(c->stream));
     std::string out;
     char line[160];

@@ -137,6 +137,7 @@ void csr_spmm(Ctx& c, const CsrA& A, const double* X, int l, double* Y) {
   RPCA_REQUIRE(l >= 1 && l <= kMaxL, RPCA_E_SHAPE, "l out of range");
   if (A.rows == 0) return;
   const unsigned grid = grid_cap(c, A.rows, kThreads / 32);
+  prof_pre(c);
   if (A.dtype == RPCA_F64)
     csr_spmm_kernel<double><<<grid, kThreads, 0, c.stream>>>(A.ptr, A.idx, (const double*)A.vals, A.rows, X, l, Y);
   else

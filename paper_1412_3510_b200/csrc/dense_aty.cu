@@ -283,6 +283,7 @@ void launch_aty_tma(Ctx& c, const DenseA& A, const double* Yp, const Split& sp, 
                             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   RPCA_REQUIRE(r == CUDA_SUCCESS, RPCA_E_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
   ensure_smem((const void*)aty_f64_tma_kernel<NT>, Cfg::kSmem);
+  prof_pre(c);
   aty_f64_tma_kernel<NT><<<(unsigned)sp.P, kThreads, Cfg::kSmem, c.stream>>>(tm, Yp, sp, maxslots, part);
   RPCA_CHECK_LAUNCH();
   count_launch(c, 1, c.tag ? c.tag : "aty_f64_dmma");
@@ -361,6 +362,7 @@ void dense_aty(Ctx& c, const DenseA& A, const double* Y, int l, const double* cm
   double* part = ar.get<double>(splits * A.n * l);
   if (A.m > 0) {
     dim3 grid((unsigned)cdiv(A.n, 64), (unsigned)splits);
+    prof_pre(c);
     if (A.dtype == RPCA_F64)
       aty_generic_kernel<double><<<grid, 256, 0, c.stream>>>((const double*)A.a, A.m, A.n, A.lda, Y, l, rps, part);
     else

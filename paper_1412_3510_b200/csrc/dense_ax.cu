@@ -223,6 +223,7 @@ void launch_ax_tma(Ctx& c, const DenseA& A, const double* Xp, int l, double* Y) 
   const int64_t ntiles = cdiv(A.m, BM);
   const int KB = (int)cdiv(A.n, BK);
   const int grid = (int)std::min<int64_t>(ntiles, c.num_sms);
+  prof_pre(c);
   ax_f64_tma_kernel<NT><<<grid, kThreads, Cfg::kSmem, c.stream>>>(tm, Xp, A.m, l, ntiles, KB, Y);
   RPCA_CHECK_LAUNCH();
   count_launch(c, 1, c.tag ? c.tag : "ax_f64_dmma");
@@ -270,6 +271,7 @@ void dense_ax(Ctx& c, const DenseA& A, const double* X, int l, double* Y, Arena&
     return;
   }
   const unsigned grid = (unsigned)cdiv(A.m, 64);
+  prof_pre(c);
   if (A.dtype == RPCA_F64)
     ax_generic_kernel<double><<<grid, 256, 0, c.stream>>>((const double*)A.a, A.m, A.n, A.lda, X, l, Y);
   else

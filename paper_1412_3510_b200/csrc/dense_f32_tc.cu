@@ -686,6 +686,7 @@ void launch_ax(Ctx& c, const DenseA& A, const float* hi, const float* lo, int64_
   ensure_smem((const void*)ax_f32_tc_kernel<N>, Cfg::kSmem);
   const int64_t ntiles = cdiv(A.m, 128);
   const int grid = (int)std::min<int64_t>(ntiles, c.num_sms);
+  prof_pre(c);
   ax_f32_tc_kernel<N><<<grid, kThreadsTC, Cfg::kSmem, c.stream>>>(tA, tH, tL, A.m, l, ntiles, (int)(Kpad / 32), cx,
                                                                    Y);
   RPCA_CHECK_LAUNCH();
@@ -711,6 +712,7 @@ void launch_aty(Ctx& c, const DenseA& A, const float* hi, const float* lo, int64
   const CUtensorMap tH = tmap_f32(hi, Kpad, N, Kpad, 32, N);
   const CUtensorMap tL = tmap_f32(lo, Kpad, N, Kpad, 32, N);
   ensure_smem((const void*)aty_f32_tc_kernel<N>, Cfg::kSmem);
+  prof_pre(c);
   aty_f32_tc_kernel<N><<<(unsigned)(pl.Gc * pl.Pg), kThreadsTC, Cfg::kSmem, c.stream>>>(tA, tH, tL, pl, part);
   RPCA_CHECK_LAUNCH();
   count_launch(c, 1, c.tag ? c.tag : "aty_f32_tc");

@@ -76,7 +76,7 @@ struct Ctx {
   size_t ws_cap = 0;
   int64_t launches = 0;
   Comm* comm = nullptr;
-  bool prof = false;
+  int prof = 0;  // 0 off, 1 every launch, 2 the A-streaming pass kernels only
   const char* tag = nullptr;  // profile name for the pass kernels when used on thin blocks
   bool capturing = false;
   bool use_graphs = true;
@@ -107,9 +107,20 @@ struct TagScope {
   ~TagScope() { c.tag = prev; }
 };
 
+// the pass kernels over A (dense A·X / Aᵀ·Y on A itself, CSR SpMM) — the
+// ones profile mode 2 brackets with events
+inline bool is_pass_kernel(const char* name) {
+  return (name[0] == 'a' && name[1] == 'x' && name[2] == '_') ||
+         (name[0] == 'a' && name[1] == 't' && name[2] == 'y' && name[3] == '_' && name[4] != 'r') ||
+         (name[0] == 'c' && name[1] == 's' && name[2] == 'r' && name[3] == '_' && name[4] == 's');
+}
 inline void count_launch(Ctx& c, int n = 1, const char* name = "misc") {
   c.launches += n;
-  if (c.prof) prof_mark(c, name);
+  if (c.prof == 1 || (c.prof == 2 && !c.tag && is_pass_kernel(name))) prof_mark(c, name);
+}
+// before a pass-kernel launch: in mode 2 close the preceding interval ("gap")
+inline void prof_pre(Ctx& c) {
+  if (c.prof == 2 && !c.tag) prof_mark(c, "gap");
 }
 
 // ---------------------------------------------------------------- kernels
