@@ -93,6 +93,8 @@ rpca_status rpca_ctx_destroy(rpca_ctx* c) {
     }
     if (c->ws) cudaFree(c->ws);
     if (c->tcache.mem) cudaFree(c->tcache.mem);
+    if (c->tcache.plan_a) cudaFree(c->tcache.plan_a);
+    if (c->tcache.plan_t) cudaFree(c->tcache.plan_t);
     delete c;
   });
 }

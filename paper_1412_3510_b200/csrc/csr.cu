@@ -18,6 +18,8 @@
 //   * column means: per-column sums over CSR(Aᵀ) (ascending row order) / m.
 #include <cub/device/device_radix_sort.cuh>
 
+#include <vector>
+
 #include "internal.cuh"
 
 namespace rpca {
@@ -25,57 +27,101 @@ namespace {
 
 constexpr int kThreads = 256;
 
+// lane-owned output columns (lane, lane+32) of Σ_{t0 ≤ t < t1} vals[t]·X[colind[t]]
+template <class T>
+__device__ __forceinline__ void row_dot(const int32_t* __restrict__ colind, const T* __restrict__ vals, int64_t t0,
+                                        int64_t t1, const double* __restrict__ X, int l, int lane, double& a0,
+                                        double& a1) {
+  for (int64_t tb = t0; tb < t1; tb += 32) {
+    const int cnt = (int)imin64(32, t1 - tb);
+    int myc = 0;
+    double myv = 0.0;
+    if (lane < cnt) {
+      myc = colind[tb + lane];
+      myv = static_cast<double>(vals[tb + lane]);
+    }
+    int k = 0;
+    for (; k + 4 <= cnt; k += 4) {  // four gathers in flight
+      const int c0 = __shfl_sync(0xffffffffu, myc, k), c1 = __shfl_sync(0xffffffffu, myc, k + 1);
+      const int c2 = __shfl_sync(0xffffffffu, myc, k + 2), c3 = __shfl_sync(0xffffffffu, myc, k + 3);
+      const double v0 = __shfl_sync(0xffffffffu, myv, k), v1 = __shfl_sync(0xffffffffu, myv, k + 1);
+      const double v2 = __shfl_sync(0xffffffffu, myv, k + 2), v3 = __shfl_sync(0xffffffffu, myv, k + 3);
+      if (lane < l) {
+        const double x0 = X[(int64_t)c0 * l + lane], x1 = X[(int64_t)c1 * l + lane];
+        const double x2 = X[(int64_t)c2 * l + lane], x3 = X[(int64_t)c3 * l + lane];
+        a0 += v0 * x0;
+        a0 += v1 * x1;
+        a0 += v2 * x2;
+        a0 += v3 * x3;
+      }
+      if (lane + 32 < l) {
+        const double x0 = X[(int64_t)c0 * l + lane + 32], x1 = X[(int64_t)c1 * l + lane + 32];
+        const double x2 = X[(int64_t)c2 * l + lane + 32], x3 = X[(int64_t)c3 * l + lane + 32];
+        a1 += v0 * x0;
+        a1 += v1 * x1;
+        a1 += v2 * x2;
+        a1 += v3 * x3;
+      }
+    }
+    for (; k < cnt; ++k) {
+      const int cc = __shfl_sync(0xffffffffu, myc, k);
+      const double vv = __shfl_sync(0xffffffffu, myv, k);
+      if (lane < l) a0 += vv * X[(int64_t)cc * l + lane];
+      if (lane + 32 < l) a1 += vv * X[(int64_t)cc * l + lane + 32];
+    }
+  }
+}
+
+// warp per row; rows with more than `heavy` nonzeros are left to the chunk kernels
 template <class T>
 __global__ void __launch_bounds__(kThreads) csr_spmm_kernel(const int64_t* __restrict__ rowptr,
                                                             const int32_t* __restrict__ colind,
                                                             const T* __restrict__ vals, int64_t rows,
-                                                            const double* __restrict__ X, int l,
+                                                            const double* __restrict__ X, int l, int64_t heavy,
                                                             double* __restrict__ Y) {
   const int lane = threadIdx.x & 31;
   const int64_t warps = (int64_t)gridDim.x * (kThreads / 32);
   for (int64_t i = (int64_t)blockIdx.x * (kThreads / 32) + (threadIdx.x >> 5); i < rows; i += warps) {
     const int64_t t0 = rowptr[i], t1 = rowptr[i + 1];
+    if (t1 - t0 > heavy) continue;
     double a0 = 0.0, a1 = 0.0;
-    for (int64_t tb = t0; tb < t1; tb += 32) {
-      const int cnt = (int)imin64(32, t1 - tb);
-      int myc = 0;
-      double myv = 0.0;
-      if (lane < cnt) {
-        myc = colind[tb + lane];
-        myv = static_cast<double>(vals[tb + lane]);
-      }
-      int k = 0;
-      for (; k + 4 <= cnt; k += 4) {  // four gathers in flight
-        const int c0 = __shfl_sync(0xffffffffu, myc, k), c1 = __shfl_sync(0xffffffffu, myc, k + 1);
-        const int c2 = __shfl_sync(0xffffffffu, myc, k + 2), c3 = __shfl_sync(0xffffffffu, myc, k + 3);
-        const double v0 = __shfl_sync(0xffffffffu, myv, k), v1 = __shfl_sync(0xffffffffu, myv, k + 1);
-        const double v2 = __shfl_sync(0xffffffffu, myv, k + 2), v3 = __shfl_sync(0xffffffffu, myv, k + 3);
-        if (lane < l) {
-          const double x0 = X[(int64_t)c0 * l + lane], x1 = X[(int64_t)c1 * l + lane];
-          const double x2 = X[(int64_t)c2 * l + lane], x3 = X[(int64_t)c3 * l + lane];
-          a0 += v0 * x0;
-          a0 += v1 * x1;
-          a0 += v2 * x2;
-          a0 += v3 * x3;
-        }
-        if (lane + 32 < l) {
-          const double x0 = X[(int64_t)c0 * l + lane + 32], x1 = X[(int64_t)c1 * l + lane + 32];
-          const double x2 = X[(int64_t)c2 * l + lane + 32], x3 = X[(int64_t)c3 * l + lane + 32];
-          a1 += v0 * x0;
-          a1 += v1 * x1;
-          a1 += v2 * x2;
-          a1 += v3 * x3;
-        }
-      }
-      for (; k < cnt; ++k) {
-        const int cc = __shfl_sync(0xffffffffu, myc, k);
-        const double vv = __shfl_sync(0xffffffffu, myv, k);
-        if (lane < l) a0 += vv * X[(int64_t)cc * l + lane];
-        if (lane + 32 < l) a1 += vv * X[(int64_t)cc * l + lane + 32];
-      }
-    }
+    row_dot(colind, vals, t0, t1, X, l, lane, a0, a1);
     if (lane < l) Y[i * l + lane] = a0;
     if (lane + 32 < l) Y[i * l + lane + 32] = a1;
+  }
+}
+
+// warp per chunk of a heavy row → its partial row
+template <class T>
+__global__ void __launch_bounds__(kThreads) csr_chunk_kernel(const int32_t* __restrict__ colind,
+                                                             const T* __restrict__ vals,
+                                                             const int64_t* __restrict__ hc, int64_t nhc,
+                                                             const double* __restrict__ X, int l,
+                                                             double* __restrict__ hpart) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = (int64_t)gridDim.x * (kThreads / 32);
+  for (int64_t c = (int64_t)blockIdx.x * (kThreads / 32) + (threadIdx.x >> 5); c < nhc; c += warps) {
+    double a0 = 0.0, a1 = 0.0;
+    row_dot(colind, vals, hc[3 * c + 1], hc[3 * c + 2], X, l, lane, a0, a1);
+    hpart[c * kMaxL + lane] = a0;
+    hpart[c * kMaxL + lane + 32] = a1;
+  }
+}
+
+// warp per heavy row: Y[row] = Σ of its chunks' partials, ascending chunk order
+__global__ void csr_heavy_reduce_kernel(const int64_t* __restrict__ hr, int64_t nhr,
+                                        const double* __restrict__ hpart, int l, double* __restrict__ Y) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = (int64_t)gridDim.x * (blockDim.x / 32);
+  for (int64_t k = (int64_t)blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5); k < nhr; k += warps) {
+    const int64_t row = hr[2 * k], c0 = hr[2 * k + 1], c1 = hr[2 * k + 3];
+    double a0 = 0.0, a1 = 0.0;
+    for (int64_t c = c0; c < c1; ++c) {
+      a0 += hpart[c * kMaxL + lane];
+      a1 += hpart[c * kMaxL + lane + 32];
+    }
+    if (lane < l) Y[row * l + lane] = a0;
+    if (lane + 32 < l) Y[row * l + lane + 32] = a1;
   }
 }
 
@@ -137,13 +183,69 @@ void csr_spmm(Ctx& c, const CsrA& A, const double* X, int l, double* Y) {
   RPCA_REQUIRE(l >= 1 && l <= kMaxL, RPCA_E_SHAPE, "l out of range");
   if (A.rows == 0) return;
   const unsigned grid = grid_cap(c, A.rows, kThreads / 32);
+  const int64_t heavy = A.nhc ? kHeavyNnz : INT64_MAX;
   prof_pre(c);
   if (A.dtype == RPCA_F64)
-    csr_spmm_kernel<double><<<grid, kThreads, 0, c.stream>>>(A.ptr, A.idx, (const double*)A.vals, A.rows, X, l, Y);
+    csr_spmm_kernel<double><<<grid, kThreads, 0, c.stream>>>(A.ptr, A.idx, (const double*)A.vals, A.rows, X, l, heavy,
+                                                             Y);
   else
-    csr_spmm_kernel<float><<<grid, kThreads, 0, c.stream>>>(A.ptr, A.idx, (const float*)A.vals, A.rows, X, l, Y);
+    csr_spmm_kernel<float><<<grid, kThreads, 0, c.stream>>>(A.ptr, A.idx, (const float*)A.vals, A.rows, X, l, heavy,
+                                                            Y);
   RPCA_CHECK_LAUNCH();
   count_launch(c, 1, "csr_spmm");
+  if (A.nhc) {
+    const unsigned g2 = grid_cap(c, A.nhc, kThreads / 32);
+    if (A.dtype == RPCA_F64)
+      csr_chunk_kernel<double><<<g2, kThreads, 0, c.stream>>>(A.idx, (const double*)A.vals, A.hc, A.nhc, X, l,
+                                                              A.hpart);
+    else
+      csr_chunk_kernel<float><<<g2, kThreads, 0, c.stream>>>(A.idx, (const float*)A.vals, A.hc, A.nhc, X, l,
+                                                             A.hpart);
+    RPCA_CHECK_LAUNCH();
+    count_launch(c, 1, "csr_spmm_heavy");
+    csr_heavy_reduce_kernel<<<grid_cap(c, A.nhr, 8), 256, 0, c.stream>>>(A.hr, A.nhr, A.hpart, l, Y);
+    RPCA_CHECK_LAUNCH();
+    count_launch(c, 1, "csr_heavy_reduce");
+  }
+}
+
+void* csr_build_heavy_plan(Ctx& c, CsrA& A) {
+  A.hc = nullptr;
+  A.hr = nullptr;
+  A.nhc = A.nhr = 0;
+  A.hpart = nullptr;
+  if (A.rows == 0) return nullptr;
+  std::vector<int64_t> ptr((size_t)A.rows + 1);
+  RPCA_CUDA(cudaMemcpyAsync(ptr.data(), A.ptr, sizeof(int64_t) * ptr.size(), cudaMemcpyDeviceToHost, c.stream));
+  RPCA_CUDA(cudaStreamSynchronize(c.stream));
+  std::vector<int64_t> hc, hr;
+  for (int64_t i = 0; i < A.rows; ++i) {
+    const int64_t t0 = ptr[i], t1 = ptr[i + 1];
+    if (t1 - t0 <= kHeavyNnz) continue;
+    hr.push_back(i);
+    hr.push_back((int64_t)hc.size() / 3);
+    for (int64_t t = t0; t < t1; t += kHeavyNnz) {
+      hc.push_back(i);
+      hc.push_back(t);
+      hc.push_back(std::min(t1, t + kHeavyNnz));
+    }
+  }
+  if (hr.empty()) return nullptr;
+  const int64_t nhc = (int64_t)hc.size() / 3, nhr = (int64_t)hr.size() / 2;
+  hr.push_back(-1);
+  hr.push_back(nhc);
+  const size_t b_hc = Arena::align(hc.size() * 8), b_hr = Arena::align(hr.size() * 8);
+  const size_t b_part = Arena::align((size_t)nhc * kMaxL * 8);
+  char* mem = nullptr;
+  RPCA_CUDA(cudaMalloc(&mem, b_hc + b_hr + b_part));
+  RPCA_CUDA(cudaMemcpy(mem, hc.data(), hc.size() * 8, cudaMemcpyHostToDevice));
+  RPCA_CUDA(cudaMemcpy(mem + b_hc, hr.data(), hr.size() * 8, cudaMemcpyHostToDevice));
+  A.hc = reinterpret_cast<const int64_t*>(mem);
+  A.nhc = nhc;
+  A.hr = reinterpret_cast<const int64_t*>(mem + b_hc);
+  A.nhr = nhr;
+  A.hpart = reinterpret_cast<double*>(mem + b_hc + b_hr);
+  return mem;
 }
 
 size_t csr_transpose_ws_bytes(const CsrA& A) {

@@ -249,7 +249,14 @@ MatV probe_of(const rpca_mat* A) {
   return v;
 }
 
-// CSR(Aᵀ) is built once per sparse A (before any graph capture) and cached.
+void free_plans(Ctx& c) {
+  if (c.tcache.plan_a) cudaFree(c.tcache.plan_a);
+  if (c.tcache.plan_t) cudaFree(c.tcache.plan_t);
+  c.tcache.plan_a = c.tcache.plan_t = nullptr;
+}
+
+// CSR(Aᵀ) is built once per sparse A (before any graph capture) and cached,
+// with the heavy-row plans of A and Aᵀ.
 void ensure_transpose(Ctx& c, const rpca_mat* A) {
   if (A->kind != RPCA_CSR) return;
   KeyHasher kh;
@@ -259,6 +266,7 @@ void ensure_transpose(Ctx& c, const rpca_mat* A) {
     RPCA_CUDA(cudaStreamSynchronize(c.stream));
     RPCA_CUDA(cudaFree(c.tcache.mem));
     c.tcache.mem = nullptr;
+    free_plans(c);
   }
   const int es = elem_size(A->dtype);
   const size_t b_ptr = Arena::align((A->n + 1) * 8), b_idx = Arena::align(A->nnz * 4 + 4);
@@ -277,12 +285,16 @@ void ensure_transpose(Ctx& c, const rpca_mat* A) {
   RPCA_CUDA(cudaFree(scratch));
   c.tcache.mem = mem;
   c.tcache.key = kh.h;
+  c.tcache.plan_a = csr_build_heavy_plan(c, src);
+  c.tcache.plan_t = csr_build_heavy_plan(c, T);
+  c.tcache.A = src;
   c.tcache.T = T;
 }
 
 MatV device_view(Ctx& c, const rpca_mat* A, Arena& ar) {
   MatV v = probe_of(A);
   if (v.csr) {
+    v.a = c.tcache.A;
     v.at = c.tcache.T;
     return v;
   }
@@ -472,6 +484,7 @@ void clear_cache(Ctx& c) {
     RPCA_CUDA(cudaFree(c.tcache.mem));
     c.tcache.mem = nullptr;
     c.tcache.key = 0;
+    free_plans(c);
   }
   drop_graphs(c);
 }

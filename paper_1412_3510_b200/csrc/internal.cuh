@@ -48,7 +48,17 @@ struct CsrA {
   const void* vals;
   int dtype;
   int64_t rows, nnz;
+  // heavy-row plan (csr.cu, built once per matrix and cached): rows with more
+  // than kHeavyNnz nonzeros are cut into chunks, one warp each, whose partial
+  // rows are summed in ascending chunk order.  hc[c] = (row, t0, t1);
+  // hr[k] = (row, first chunk), hr[nhr] = (−1, nhc); hpart: nhc × kMaxL doubles
+  const int64_t* hc = nullptr;
+  int64_t nhc = 0;
+  const int64_t* hr = nullptr;
+  int64_t nhr = 0;
+  double* hpart = nullptr;
 };
+constexpr int64_t kHeavyNnz = 4096;
 
 
 // Optional per-launch timing (rpca_profile): an event is recorded on the
@@ -92,6 +102,9 @@ struct Ctx {
     uint64_t key = 0;
     void* mem = nullptr;
     CsrA T{};
+    CsrA A{};                   // the cached matrix itself, with its heavy-row plan
+    void* plan_a = nullptr;     // plan memory of A and of T
+    void* plan_t = nullptr;
   } tcache;
   cudaEvent_t fence_in = nullptr, fence_out = nullptr;
   Arena arena(size_t bytes);  // ensures capacity, returns an arena over the workspace
@@ -181,6 +194,9 @@ void dense_aty(Ctx& c, const DenseA& A, const double* Y, int l, const double* cm
 // Y (rows×l) = A·X   (X has as many rows as A has columns)
 void csr_spmm(Ctx& c, const CsrA& A, const double* X, int l, double* Y);
 size_t csr_transpose_ws_bytes(const CsrA& A);
+// device memory (caller frees with cudaFree) holding A's heavy-row plan; sets
+// the plan fields of A (synchronises the stream; nullptr if A has no heavy row)
+void* csr_build_heavy_plan(Ctx& c, CsrA& A);
 // T = CSR(Aᵀ) (n rows) into caller buffers T.ptr (n+1), T.idx, T.vals (nnz); stable in rows
 void csr_transpose(Ctx& c, const CsrA& A, int64_t n, CsrA& T, Arena& scratch);
 // cmean[j] = (Σ_i A_ij)/m_total from CSR(Aᵀ), rows ascending

@@ -348,3 +348,39 @@ def test_pca_csr_scaled_c5(m, n, raw):
     est = rp.diffsnorm(A, *res, raw=raw, its=20, seed=1)
     ref = oracle.diffsnorm(host, *[t.cpu().numpy() for t in res], raw=raw, its=20, seed=1)
     assert abs(est - ref) <= 1e-9 * ref
+
+
+def heavy_csr(m=12000, n=9000, seed=5):
+    """CSR with heavy rows in A (three dense rows, n > 4096 nonzeros) and in Aᵀ
+    (column 0 in every row): both directions take the chunked heavy-row path."""
+    rng = np.random.default_rng(seed)
+    rows = []
+    for i in range(m):
+        if i in (7, 5000, m - 1):
+            cols = np.arange(n)
+        else:
+            cols = np.unique(np.concatenate([[0], rng.choice(n, 6, replace=False)]))
+        rows.append(cols)
+    rp_ = np.zeros(m + 1, dtype=np.int64)
+    rp_[1:] = np.cumsum([len(c) for c in rows])
+    ci = np.concatenate(rows).astype(np.int32)
+    va = rng.standard_normal(len(ci))
+    A = rp.CSR(torch.tensor(rp_, device=dev()), torch.tensor(ci, device=dev()), torch.tensor(va, device=dev()), (m, n))
+    return A, (rp_, ci, va, (m, n))
+
+
+@pytest.mark.parametrize("l", [1, 32, 52])
+def test_csr_heavy_rows(l):
+    A, host = heavy_csr()
+    D = dense_of(host)
+    g = torch.Generator(device="cuda").manual_seed(12)
+    X = torch.randn(D.shape[1], l, generator=g, device=dev(), dtype=torch.float64)
+    Y = torch.randn(D.shape[0], l, generator=g, device=dev(), dtype=torch.float64)
+    Xn, Yn = X.cpu().numpy(), Y.cpu().numpy()
+    got = rp.apply(A, X).cpu().numpy()
+    assert np.all(np.abs(got - oracle.apply(host, Xn)) <= 2 * gamma(9000) * (np.abs(D) @ np.abs(Xn)) + 1e-300)
+    got2 = rp.apply(A, X).cpu().numpy()
+    assert np.array_equal(got, got2)  # deterministic chunk order
+    got = rp.apply(A, Y, adjoint=True).cpu().numpy()
+    assert np.all(np.abs(got - oracle.apply(host, Yn, adjoint=True)) <=
+                  2 * gamma(12000) * (np.abs(D).T @ np.abs(Yn)) + 1e-300)
