@@ -278,14 +278,15 @@ rpca_status rpca_small_svd(rpca_ctx* c, const double* G, int64_t n, int64_t l, d
     rpca::Sizer s;
     s.add<double>(n * l);
     s.add<double>(2 * l * l);
-    rpca::Arena ar = c->arena(s.total + rpca::orth_ws_bytes(*c, n, (int)l) + 65536);
+    rpca::Arena ar = c->arena(s.total + std::max(rpca::orth_ws_bytes(*c, n, (int)l),
+                                                 rpca::thin_gemm_ws_bytes(n, (int)l, (int)l)) + 65536);
     double* Qb = ar.get<double>(n * l);
     double* R = ar.get<double>(l * l);
     double* Vr = ar.get<double>(l * l);
     RPCA_CUDA(cudaMemcpyAsync(Qb, G, sizeof(double) * n * l, cudaMemcpyDeviceToDevice, c->stream));
     rpca::orthonormalize(*c, Qb, n, (int)l, R, ar);
     rpca::jacobi_svd_small(*c, R, (int)l, sigma, W, Vr);
-    rpca::thin_gemm(*c, Qb, n, (int)l, Vr, (int)l, nullptr, Vt, l, RPCA_F64);
+    rpca::thin_gemm(*c, Qb, n, (int)l, Vr, (int)l, nullptr, Vt, l, RPCA_F64, ar);
   });
 }
 

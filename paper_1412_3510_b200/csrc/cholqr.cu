@@ -12,7 +12,7 @@
 // Exact zero pivots (rank-deficient Y) make L's column a unit vector, so L —
 // and hence Q — stays full rank and orthonormal.
 // The two Grams (LᵀL, Q1ᵀQ1) run on the fp64 tensor-core adjoint pass
-// (dense_aty with A := Y) and the two triangular products on the A·X pass
+// (gram.cu) and the two triangular products on the A·X pass
 // (dense_ax, in place); only the l×l Cholesky/inverse is a one-CTA kernel.
 #include "comm.cuh"
 
@@ -108,10 +108,7 @@ size_t orth_ws_bytes(int64_t m, int l) {
   return s.total + lu_ws_bytes(m, l) + ax_ws_bytes(Y, l) + 4096;
 }
 
-size_t orth_ws_bytes(Ctx& c, int64_t m, int l) {
-  const DenseA Y{nullptr, RPCA_F64, m, l, l};
-  return orth_ws_bytes(m, l) + aty_ws_bytes(c, Y, l);
-}
+size_t orth_ws_bytes(Ctx& c, int64_t m, int l) { return orth_ws_bytes(m, l) + gram_ws_bytes(c, m, l); }
 
 void orthonormalize(Ctx& c, double* Y, int64_t m, int l, double* R_out, Arena& ar) {
   RPCA_REQUIRE(l >= 1 && l <= kMaxL && m >= l, RPCA_E_SHAPE, "orthonormalize: need 1 ≤ l ≤ %d, m ≥ l", kMaxL);
@@ -126,14 +123,14 @@ void orthonormalize(Ctx& c, double* Y, int64_t m, int l, double* R_out, Arena& a
   lu_renorm(c, Y, m, l, U, nullptr, ar);  // Y ← L
   ar.off = mark;
   TagScope ts(c, "cholqr_gram");
-  dense_aty(c, Yd, Y, l, nullptr, G, ar);  // G = LᵀL
+  gram(c, Y, Y, m, l, G, ar);              // G = LᵀL
   ar.off = mark;
   chol(c, G, l, U, 0, M1, R1);             // R1·U
   c.tag = "cholqr_trmm";
   dense_ax(c, Yd, M1, l, Y, ar);           // Q1 = L·R1⁻¹
   ar.off = mark;
   c.tag = "cholqr_gram";
-  dense_aty(c, Yd, Y, l, nullptr, G, ar);  // G = Q1ᵀQ1
+  gram(c, Y, Y, m, l, G, ar);              // G = Q1ᵀQ1
   ar.off = mark;
   chol(c, G, l, R1, 1, M2, R2);            // R = D·R2·R1·U
   c.tag = "cholqr_trmm";
@@ -158,10 +155,9 @@ void orthonormalize_sharded(Ctx& c, double* Y, int64_t m, int64_t row0, int l, d
   const size_t mark = ar.off;
   lu_renorm_sharded(c, Y, m, row0, l, U, ar);  // Y ← L (local rows)
   ar.off = mark;
-  auto gram = [&] {
+  auto gram_all = [&] {
     c.tag = "cholqr_gram";
-    if (m > 0) dense_aty(c, Yd, Y, l, nullptr, G, ar);
-    else RPCA_CUDA(cudaMemsetAsync(G, 0, sizeof(double) * l * l, c.stream));
+    gram(c, Y, Y, m, l, G, ar);  // zero when this shard has no rows
     ar.off = mark;
     allreduce_sum(c, G, (size_t)l * l);
   };
@@ -171,10 +167,10 @@ void orthonormalize_sharded(Ctx& c, double* Y, int64_t m, int64_t row0, int l, d
     ar.off = mark;
   };
   TagScope ts(c, "cholqr_gram");
-  gram();
+  gram_all();
   chol(c, G, l, U, 0, M1, R1);
   trmm(M1);
-  gram();
+  gram_all();
   chol(c, G, l, R1, 1, M2, R2);
   trmm(M2);
   if (R_out) RPCA_CUDA(cudaMemcpyAsync(R_out, R2, sizeof(double) * l * l, cudaMemcpyDeviceToDevice, c.stream));

@@ -528,6 +528,7 @@ void pca(Ctx& c, const rpca_mat* Am, int64_t k, int raw, int its, int64_t l, uin
   scratch = std::max(scratch, lu_ws_bytes(std::max(nin, nout), L));
   scratch = std::max(scratch, orth_ws_bytes(c, std::max(nin, nout), L));
   scratch = std::max(scratch, (size_t)(cdiv(std::max(ml, n), 8192) + 2) * (n + 2 * k) * 8 + 65536);
+  scratch = std::max(scratch, thin_gemm_ws_bytes(std::max(nin, nout), L, K) + 65536);
   ensure_transpose(c, Am);
   Arena ar = c.arena(fixed + scratch + 65536);
 
@@ -577,16 +578,16 @@ void pca(Ctx& c, const rpca_mat* Am, int64_t k, int raw, int its, int64_t l, uin
       // V (n×k, replicated) fixes the column signs; U is this rank's rows
       if (!trans) {
         // V = Q_B·Vr[:, :k] (n×k), U = Q·W[:, :k] (m×k)  (eq. i4)
-        thin_gemm(c, Zb, nin, L, Vr, K, nullptr, side, k, RPCA_F64);
+        thin_gemm(c, Zb, nin, L, Vr, K, nullptr, side, k, RPCA_F64, ar);
         column_signs(c, side, n, K, k, sign, ar);
         scale_cast(c, side, n, K, sign, Vd, ldv, odt);
-        thin_gemm(c, Yb, nout, L, W, K, sign, Ud, ldu, odt);
+        thin_gemm(c, Yb, nout, L, W, K, sign, Ud, ldu, odt, ar);
       } else {
         // sketched Aᵀ: its "U" = Q·W is A's V (n×k); its "V" = Q_B·Vr is A's U
-        thin_gemm(c, Yb, nout, L, W, K, nullptr, side, k, RPCA_F64);
+        thin_gemm(c, Yb, nout, L, W, K, nullptr, side, k, RPCA_F64, ar);
         column_signs(c, side, n, K, k, sign, ar);
         scale_cast(c, side, n, K, sign, Vd, ldv, odt);
-        thin_gemm(c, Zb, nin, L, Vr, K, sign, Ud, ldu, odt);
+        thin_gemm(c, Zb, nin, L, Vr, K, sign, Ud, ldu, odt, ar);
       }
       copy_cast(c, sig, Sd, k, odt);
       ar.off = mark;
@@ -639,6 +640,7 @@ void eigens(Ctx& c, const rpca_mat* Am, int64_t k, int its, int64_t l, uint64_t 
   scratch = std::max(scratch, lu_ws_bytes(ml, L));
   scratch = std::max(scratch, orth_ws_bytes(c, ml, L));
   scratch = std::max(scratch, (size_t)(cdiv(n, 8192) + 2) * l * l * 8 + 65536 + (size_t)P * 3 * l * 8);
+  scratch = std::max(scratch, thin_gemm_ws_bytes(ml, L, K) + gram_ws_bytes(c, ml, L) + 65536);
   Arena ar = c.arena(sz.total + scratch + 65536);
   if (!c.status_host) RPCA_CUDA(cudaMallocHost(&c.status_host, 64));
 
@@ -696,9 +698,9 @@ void eigens(Ctx& c, const rpca_mat* Am, int64_t k, int its, int64_t l, uint64_t 
     apply_ax(c, dA, nullptr, Qf, L, B1, ar);  // (start) B1 = A·Q (this rank's rows)
     {
       const size_t mark = ar.off;
-      // (second) B2 = QᵀB1 (symmetrised in the kernels below) — an "Aᵀ·Y" with
-      // A := Q (n×l), Y := B1, so it runs on the fp64 tensor-core adjoint kernel
-      dense_aty(c, DenseA{Qf + slot, RPCA_F64, ml, L, L}, B1, L, nullptr, G, ar);
+      // (second) B2 = QᵀB1 (symmetrised in the kernels below) on the fp64
+      // tensor-core Gram kernel
+      gram(c, Qf + slot, B1, ml, L, G, ar);
       if (sh) allreduce_sum(c, G, (size_t)l * l);
       if (variant == RPCA_SHIFT_CHOL) {
         weighted_colsum(c, B1, B1, ml * l, 1, scal, ar);  // ‖B1‖_F²
@@ -716,7 +718,7 @@ void eigens(Ctx& c, const rpca_mat* Am, int64_t k, int its, int64_t l, uint64_t 
     jacobi_svd_small(c, R, L, sig, W, Vr);
     {
       const size_t mark = ar.off;
-      thin_gemm(c, Fm, ml, L, Vr, K, nullptr, side, k, RPCA_F64);
+      thin_gemm(c, Fm, ml, L, Vr, K, nullptr, side, k, RPCA_F64, ar);
       signs(side, sign);
       scale_cast(c, side, ml, K, sign, Ud, ldu, odt);
       nystrom_lambda(c, sig, scal + 1, K, Ld, odt);

@@ -158,7 +158,8 @@ void colmeans_dense(Ctx& c, const void* A, int dtype, int64_t m, int64_t n, int6
                     double* cmean, Arena& ar);
 // Out (rows×k, ld ldo, dtype out_dtype) = In (rows×l) · W[:, :k] (W l×l) · diag(sign)
 void thin_gemm(Ctx& c, const double* In, int64_t rows, int l, const double* W, int k, const double* sign,
-               void* Out, int64_t ldo, int out_dtype);
+               void* Out, int64_t ldo, int out_dtype, Arena& ar);
+size_t thin_gemm_ws_bytes(int64_t rows, int l, int k);
 // sign[j] = sign of the largest-|·| entry of column j of V (rows×k), lowest index on ties
 void column_signs(Ctx& c, const double* V, int64_t rows, int k, int64_t ldv, double* sign, Arena& ar);
 // same rule over a V whose rows [row0, row0+rows) are this rank's shard
@@ -167,8 +168,9 @@ void column_signs_sharded(Ctx& c, const double* V, int64_t rows, int64_t row0, i
 void copy_cast(Ctx& c, const double* src, void* dst, int64_t count, int dtype);
 // dst (rows×k, ld ldd, dtype) = src (rows×k, ld k) · diag(sign)   (sign may be NULL)
 void scale_cast(Ctx& c, const double* src, int64_t rows, int k, const double* sign, void* dst, int64_t ldd, int dtype);
-// G (l×l) = Xᵀ·Y over rows (fixed-order two-stage reduction)
+// G (l×l) = Xᵀ·Y over rows (gram.cu: fp64 tensor cores, per-CTA partials summed in CTA order)
 void gram(Ctx& c, const double* X, const double* Y, int64_t rows, int l, double* G, Arena& ar);
+size_t gram_ws_bytes(Ctx& c, int64_t rows, int l);
 // Out (rows×l) = (In + ν·Q)·M, ν read from device (Q may be NULL ⇒ Out = In·M)
 void right_mult(Ctx& c, const double* In, const double* Q, const double* nu, const double* M, int64_t rows, int l,
                 double* Out);

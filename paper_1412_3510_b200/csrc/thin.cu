@@ -120,28 +120,12 @@ __global__ void colsum_dense_final(const double* __restrict__ part, int64_t npar
 template <class T>
 __device__ __forceinline__ T cast_out(double v) { return static_cast<T>(v); }
 
-// Out[i][j] = sign[j]·Σ_t In[i][t]·W[t][j], j < k; rows staged through smem.
-template <class T>
-__global__ void thin_gemm_kernel(const double* __restrict__ In, int64_t rows, int l, const double* __restrict__ W,
-                                 int k, const double* __restrict__ sign, T* __restrict__ Out, int64_t ldo) {
-  extern __shared__ double sm[];
-  double* Ws = sm;             // l×k
-  double* Is = sm + l * k;     // 64×l
+// Wk (l×k) = W[:, :k]·diag(sign)   (W l×l, sign may be NULL)
+__global__ void scale_cols_kernel(const double* __restrict__ W, int l, int k, const double* __restrict__ sign,
+                                  double* __restrict__ Wk) {
   for (int idx = threadIdx.x; idx < l * k; idx += blockDim.x) {
-    const int t = idx / k, j = idx % k;
-    Ws[idx] = W[t * l + j] * (sign ? sign[j] : 1.0);
-  }
-  for (int64_t r0 = (int64_t)blockIdx.x * 64; r0 < rows; r0 += (int64_t)gridDim.x * 64) {
-    __syncthreads();
-    const int nr = (int)imin64(64, rows - r0);
-    for (int idx = threadIdx.x; idx < nr * l; idx += blockDim.x) Is[idx] = In[r0 * l + idx];
-    __syncthreads();
-    for (int idx = threadIdx.x; idx < nr * k; idx += blockDim.x) {
-      const int r = idx / k, j = idx % k;
-      double s = 0.0;
-      for (int t = 0; t < l; ++t) s += Is[r * l + t] * Ws[t * k + j];
-      Out[(r0 + r) * ldo + j] = cast_out<T>(s);
-    }
+    const int t = idx / k, j = idx - t * k;
+    Wk[idx] = W[t * l + j] * (sign ? sign[j] : 1.0);
   }
 }
 
@@ -240,18 +224,6 @@ __global__ void scale_cast_kernel(const double* __restrict__ src, int64_t rows, 
     const int64_t i = idx / k;
     const int j = (int)(idx - i * k);
     dst[i * ldd + j] = static_cast<T>(src[idx] * (sign ? sign[j] : 1.0));
-  }
-}
-
-// partial[b][p][q] = Σ_{i in chunk b} X[i][p]·Y[i][q]   (X, Y rows×l)
-__global__ void gram_partial(const double* __restrict__ X, const double* __restrict__ Y, int64_t rows, int l,
-                             double* __restrict__ part) {
-  const int64_t r0 = (int64_t)blockIdx.x * kChunk, r1 = min(rows, r0 + kChunk);
-  for (int pq = threadIdx.x; pq < l * l; pq += blockDim.x) {
-    const int p = pq / l, q = pq % l;
-    double s = 0.0;
-    for (int64_t i = r0; i < r1; ++i) s += X[i * l + p] * Y[i * l + q];
-    part[(int64_t)blockIdx.x * l * l + pq] = s;
   }
 }
 
@@ -361,19 +333,36 @@ void colmeans_dense(Ctx& c, const void* A, int dtype, int64_t m, int64_t n, int6
   count_launch(c, 2, "colmeans");
 }
 
+size_t thin_gemm_ws_bytes(int64_t rows, int l, int k) {
+  Sizer s;
+  s.add<double>((size_t)l * k);
+  s.add<double>((size_t)rows * k);
+  s.add<char>(ax_ws_bytes(DenseA{nullptr, RPCA_F64, rows, l, l}, k));
+  return s.total + 4096;
+}
+
+// Out = In·W[:, :k]·diag(sign) on the fp64 tensor-core pass kernel (dense_ax
+// with the thin block as "A"): W' = W[:, :k]·diag(sign) is formed first; an fp64
+// output with ldo = k is written directly, otherwise through an fp64 temporary
+// and a casting copy
 void thin_gemm(Ctx& c, const double* In, int64_t rows, int l, const double* W, int k, const double* sign, void* Out,
-               int64_t ldo, int out_dtype) {
-  const size_t smem = (size_t)(l * k + 64 * l) * sizeof(double);
-  const unsigned grid = grid_for(c, rows, 64);
-  const int smax = (kMaxL * kMaxL + 64 * kMaxL) * (int)sizeof(double);
-  ensure_smem((const void*)thin_gemm_kernel<double>, smax);
-  ensure_smem((const void*)thin_gemm_kernel<float>, smax);
-  if (out_dtype == RPCA_F64)
-    thin_gemm_kernel<double><<<grid, 256, smem, c.stream>>>(In, rows, l, W, k, sign, (double*)Out, ldo);
-  else
-    thin_gemm_kernel<float><<<grid, 256, smem, c.stream>>>(In, rows, l, W, k, sign, (float*)Out, ldo);
+               int64_t ldo, int out_dtype, Arena& ar) {
+  if (rows == 0) return;
+  const size_t mark = ar.off;
+  double* Wk = ar.get<double>((size_t)l * k);
+  scale_cols_kernel<<<1, 256, 0, c.stream>>>(W, l, k, sign, Wk);
   RPCA_CHECK_LAUNCH();
-  count_launch(c, 1, "thin_gemm");
+  count_launch(c);
+  TagScope ts(c, "thin_gemm");
+  const DenseA A{In, RPCA_F64, rows, l, l};
+  if (out_dtype == RPCA_F64 && ldo == k) {
+    dense_ax(c, A, Wk, k, (double*)Out, ar);
+  } else {
+    double* tmp = ar.get<double>((size_t)rows * k);
+    dense_ax(c, A, Wk, k, tmp, ar);
+    scale_cast(c, tmp, rows, k, nullptr, Out, ldo, out_dtype);
+  }
+  ar.off = mark;
 }
 
 void column_signs(Ctx& c, const double* V, int64_t rows, int k, int64_t ldv, double* sign, Arena& ar) {
@@ -413,16 +402,6 @@ void scale_cast(Ctx& c, const double* src, int64_t rows, int k, const double* si
   else
     scale_cast_kernel<float><<<grid_for(c, rows * k), 256, 0, c.stream>>>(src, rows, k, sign, (float*)dst, ldd);
   RPCA_CHECK_LAUNCH();
-  count_launch(c);
-}
-
-void gram(Ctx& c, const double* X, const double* Y, int64_t rows, int l, double* G, Arena& ar) {
-  const int64_t nparts = std::max<int64_t>(1, cdiv(rows, kChunk));
-  double* part = ar.get<double>(nparts * l * l);
-  gram_partial<<<(unsigned)nparts, 256, 0, c.stream>>>(X, Y, rows, l, part);
-  RPCA_CHECK_LAUNCH();
-  // reuse sum_partials with "l" = l*l columns (≤ 4096): one thread per entry
-  sum_partials_wide(c, part, nparts, l * l, G);
   count_launch(c);
 }
 
