@@ -39,6 +39,28 @@ sys.path.insert(0, ROOT)
 import synth  # noqa: E402
 
 PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
+TRAFFIC_PATH = os.path.join(ROOT, "profiles", "traffic.json")  # written by tools/gpu/make_traffic.py from ncu
+NCU_NAME = {"ax_f64_dmma": "ax_f64_tma_kernel", "aty_f64_dmma": "aty_f64_tma_kernel", "ax_f32_tc": "ax_f32_tc_kernel",
+            "aty_f32_tc": "aty_f32_tc_kernel", "csr_spmm": "csr_spmm_kernel"}
+
+
+def ncu_traffic(config, kernel):
+    """dram read+write bytes per launch of `kernel` on `config` from the committed
+    ncu --set full capture (the A-streaming launches: the largest-traffic records;
+    CSR: the mean of its A·X and Aᵀ·Y launches), or None."""
+    try:
+        with open(TRAFFIC_PATH) as f:
+            d = json.load(f)[config]
+    except Exception:
+        return None
+    prefix = NCU_NAME.get(kernel, kernel)
+    recs = [r for k, v in d.items() if k.startswith(prefix) for r in v]
+    if not recs:
+        return None
+    if kernel == "csr_spmm":
+        return {"bytes": sum(r["traffic_bytes"] for r in recs) / len(recs), "source": recs[0]["source"]}
+    r = max(recs, key=lambda r: r["traffic_bytes"])
+    return {"bytes": r["traffic_bytes"], "source": r["source"]}
 FALLBACK_HBM = 6650.0  # B200_PROFILING.md fallback, GB/s
 
 
@@ -343,8 +365,12 @@ def main():
         avg_ms = tot / cnt
         achieved = pbytes / (avg_ms / 1e3) / 1e9
         achieved = max_over_ranks(-achieved, ws, dev) * -1.0  # slowest rank
+        tr = ncu_traffic(cfg.name, dom[0]) if ws == 1 else None
         roof = {"bound": "hbm", "kernel": dom[0], "achieved": round(achieved, 1), "peak": hbm, "unit": "GB/s",
-                "frac": round(achieved / hbm, 4), "traffic": None, "peak_source": peak_src,
+                "frac": round(achieved / hbm, 4), "traffic": round(tr["bytes"]) if tr else None,
+                "traffic_source": ("ncu --set full, dram__bytes_read.sum + dram__bytes_write.sum per launch: "
+                                   + os.path.relpath(tr["source"], ROOT)) if tr else None,
+                "peak_source": peak_src,
                 "algorithmic_bytes_per_launch": pbytes, "avg_launch_ms": round(avg_ms, 5),
                 "share_of_step": round(tot / args.steps / step_ms, 4)}
         all_pass_ms = sum(v[1] for v in passes_k.values()) / args.steps
