@@ -54,6 +54,15 @@ __device__ __forceinline__ uint32_t piv_key(double v) {
   return ((uint32_t)__double2hiint(v) & 0x7FFFFFFFu) + 1u;
 }
 
+// w[t−1] ← w[t] − mult·prow[t] for t < W (the live width), w[W−1.. ] ← 0
+template <int LP, int W>
+__device__ __forceinline__ void eliminate(double (&w)[LP], const double* prow, double mult) {
+#pragma unroll
+  for (int t = 1; t < W; ++t) w[t - 1] = fma(-mult, prow[t], w[t]);
+#pragma unroll
+  for (int t = W - 1; t < LP; ++t) w[t] = 0.0;
+}
+
 // One CTA: rows from Y (leaf: contiguous block; tree: a group of candidate
 // sets), GEPP, l nominated original rows → cand_out[blockIdx.x*l ...] (-1 pad).
 // If final, also U, Lp, the original pivot rows piv_out and M = U⁻¹.
@@ -168,9 +177,13 @@ __global__ void __launch_bounds__(kThreads, SelCfg<LP>::kMinBlocks)
           const double u = w[q][0];
           slot[j & 1][warp] = make_uint2(mk, (uint32_t)(tid * R + q));
           suinv[j & 1][warp] = (u != 0.0) ? __drcp_rn(u) : 0.0;
+          // only the LP − j live values (the shifted tail is zero); a single
+          // lane's shared stores are the costliest part of a step
           double2* dst = reinterpret_cast<double2*>(buf[j & 1][warp]);
+          const int npair = (LP - j + 1) >> 1;
 #pragma unroll
-          for (int t = 0; t < LP; t += 2) dst[t >> 1] = make_double2(w[q][t], w[q][t + 1]);
+          for (int t = 0; t < LP; t += 2)
+            if ((t >> 1) < npair) dst[t >> 1] = make_double2(w[q][t], w[q][t + 1]);
         }
     }
     __syncthreads();
@@ -198,9 +211,11 @@ __global__ void __launch_bounds__(kThreads, SelCfg<LP>::kMinBlocks)
       if (tid * R + q == p) { act[q] = false; continue; }
       const double mult = w[q][0] * uinv;
       if (final_) msm[j * CAP + tid * R + q] = mult;
-#pragma unroll
-      for (int t = 1; t < LP; ++t) w[q][t - 1] = fma(-mult, prow[t], w[q][t]);
-      w[q][LP - 1] = 0.0;
+      // only the live width: columns ≥ LP − j are zero (and stay zero)
+      if (j >= (3 * LP) / 4) eliminate<LP, LP / 4>(w[q], prow, mult);
+      else if (j >= LP / 2) eliminate<LP, LP / 2>(w[q], prow, mult);
+      else if (j >= LP / 4) eliminate<LP, (3 * LP) / 4>(w[q], prow, mult);
+      else eliminate<LP, LP>(w[q], prow, mult);
     }
   }
   __syncthreads();
