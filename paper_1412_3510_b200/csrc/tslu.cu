@@ -63,6 +63,26 @@ __device__ __forceinline__ void eliminate(double (&w)[LP], const double* prow, d
   for (int t = W - 1; t < LP; ++t) w[t] = 0.0;
 }
 
+// rank-ns update of the trailing columns then the shift to the next panel:
+// w[t] −= Σ_{s<ns} w[s]·U12[s][t−8] for 8 ≤ t < W, then w[t] ← w[t+8]
+template <int LP, int W>
+__device__ __forceinline__ void trail_update(double (&w)[LP], const double (*u12)[LP], int ns) {
+  double m[8];
+#pragma unroll
+  for (int s = 0; s < 8; ++s) m[s] = s < ns ? w[s] : 0.0;
+#pragma unroll
+  for (int t = 8; t < W; ++t) {
+    double v = w[t];
+#pragma unroll
+    for (int s = 0; s < 8; ++s) v = fma(-m[s], u12[s][t - 8], v);
+    w[t] = v;
+  }
+#pragma unroll
+  for (int t = 0; t + 8 < LP; ++t) w[t] = w[t + 8];
+#pragma unroll
+  for (int t = LP - 8; t < LP; ++t) w[t] = 0.0;
+}
+
 // One CTA: rows from Y (leaf: contiguous block; tree: a group of candidate
 // sets), GEPP, l nominated original rows → cand_out[blockIdx.x*l ...] (-1 pad).
 // If final, also U, Lp, the original pivot rows piv_out and M = U⁻¹.
@@ -81,7 +101,10 @@ __global__ void __launch_bounds__(kThreads, SelCfg<LP>::kMinBlocks)
   __shared__ int slot_of[CAP];
   __shared__ uint2 slot[2][kWarps];  // {pivot key, local row} of each warp's winner
   __shared__ double suinv[2][kWarps];
-  __shared__ __align__(16) double buf[2][kWarps][LP];
+  __shared__ __align__(16) double pbuf[2][kWarps][8];  // panel part of each warp winner's row
+  __shared__ double traw[8][LP];                         // raw trailing parts of the panel's pivot rows
+  __shared__ double l11[8][8];                           // the panel's unit-lower multipliers
+  __shared__ double u12[8][LP];                          // trailing rows of U
   __shared__ int piv[LP];
   __shared__ int nrows_s;
   __shared__ int setcnt[CAP + 1];
@@ -143,10 +166,12 @@ __global__ void __launch_bounds__(kThreads, SelCfg<LP>::kMinBlocks)
   // this thread's rows → registers (zero beyond l / beyond rows)
   double w[R][LP];
   bool act[R];
+  int pstep[R];  // ≥ 0: pivot step within the current panel (−1: not a pivot)
 #pragma unroll
   for (int q = 0; q < R; ++q) {
     const int r = tid * R + q;
     act[q] = r < rows;
+    pstep[q] = -1;
     const double* src = nullptr;
     if (act[q])
       src = leaf == 2 ? rows_in + ((int64_t)blockIdx.x * G * l + slot_of[r]) * l : Y + ids[r] * l;
@@ -154,68 +179,111 @@ __global__ void __launch_bounds__(kThreads, SelCfg<LP>::kMinBlocks)
     for (int t = 0; t < LP; ++t) w[q][t] = (act[q] && t < l) ? src[t] : 0.0;
   }
 
-  // Rolled column loop (a straight-line unroll over all columns overflows the
-  // instruction cache).  Registers hold the row SHIFTED: at step j, w[q][t] is
-  // column j+t (zero beyond LP−j); each elimination writes w[t−1] ← w[t] −
-  // mult·p[t].  Only the final level keeps the multipliers (msm, shared) and
-  // the published pivot rows (keep) for U and Lp.
-  for (int j = 0; j < steps; ++j) {
-    uint32_t best = 0;
-    int bq = 0;
+  // Blocked GEPP, panels of 8 columns.  Registers hold each row SHIFTED so
+  // the current panel is w[q][0..7] (static indices; the loop over panels is
+  // rolled — a straight-line unroll over all columns overflows the
+  // instruction cache).  Panel step s: argmax of column s, the warp winner
+  // publishes only the panel part of its row (≤ 8 values), one barrier, then
+  // each row eliminates the panel columns and keeps its multiplier in w[q][s].
+  // Panel end: the panel's pivot rows publish their raw trailing parts, the
+  // trailing rows of U are formed by forward substitution with the panel's
+  // unit-lower L11 (one thread per column), and every other row applies the
+  // rank-8 update w_trail −= Σ_s mult_s·U12[s] and shifts left by 8.  Same
+  // pivots as column-by-column GEPP; only the order of the trailing updates
+  // differs.  Final level: U rows go to `keep`, multipliers to `msm`.
+  for (int pb = 0; pb < steps; pb += 8) {
+    const int ns = min(8, steps - pb);
 #pragma unroll
-    for (int q = 0; q < R; ++q)
-      if (act[q]) {
-        const uint32_t k = piv_key(w[q][0]);
-        if (k > best) { best = k; bq = q; }
-      }
-    const uint32_t mk = __reduce_max_sync(0xffffffffu, best);
-    const int wl = __ffs(__ballot_sync(0xffffffffu, best == mk)) - 1;  // lowest lane = lowest row
-    if (lane == wl) {
+    for (int s = 0; s < 8; ++s) {
+      if (s >= ns) break;
+      const int j = pb + s;
+      uint32_t best = 0;
+      int bq = 0;
 #pragma unroll
       for (int q = 0; q < R; ++q)
-        if (q == bq) {
-          const double u = w[q][0];
-          slot[j & 1][warp] = make_uint2(mk, (uint32_t)(tid * R + q));
-          suinv[j & 1][warp] = (u != 0.0) ? __drcp_rn(u) : 0.0;
-          // only the LP − j live values (the shifted tail is zero); a single
-          // lane's shared stores are the costliest part of a step
-          double2* dst = reinterpret_cast<double2*>(buf[j & 1][warp]);
-          const int npair = (LP - j + 1) >> 1;
-#pragma unroll
-          for (int t = 0; t < LP; t += 2)
-            if ((t >> 1) < npair) dst[t >> 1] = make_double2(w[q][t], w[q][t + 1]);
+        if (act[q]) {
+          const uint32_t k = piv_key(w[q][s]);
+          if (k > best) { best = k; bq = q; }
         }
+      const uint32_t mk = __reduce_max_sync(0xffffffffu, best);
+      const int wl = __ffs(__ballot_sync(0xffffffffu, best == mk)) - 1;  // lowest lane = lowest row
+      if (lane == wl) {
+#pragma unroll
+        for (int q = 0; q < R; ++q)
+          if (q == bq) {
+            const double u = w[q][s];
+            slot[j & 1][warp] = make_uint2(mk, (uint32_t)(tid * R + q));
+            suinv[j & 1][warp] = (u != 0.0) ? __drcp_rn(u) : 0.0;
+#pragma unroll
+            for (int t = s; t < 8; ++t) pbuf[j & 1][warp][t] = w[q][t];
+          }
+      }
+      __syncthreads();
+      // max over the 8 warp winners in a fixed 3-level tree (lower warp on ties)
+      uint2 k[kWarps];
+      int wi[kWarps];
+#pragma unroll
+      for (int i = 0; i < kWarps; ++i) {
+        k[i] = slot[j & 1][i];
+        wi[i] = i;
+      }
+#pragma unroll
+      for (int st = 1; st < kWarps; st <<= 1)
+#pragma unroll
+        for (int i = 0; i < kWarps; i += 2 * st)
+          if (k[i + st].x > k[i].x) { k[i] = k[i + st]; wi[i] = wi[i + st]; }
+      const int p = (int)k[0].y;
+      const double uinv = suinv[j & 1][wi[0]];
+      const double* prow = pbuf[j & 1][wi[0]];
+      if (tid == 0) piv[j] = p;
+      if (final_ && tid < 8 - s) keep[j * LP + tid] = prow[s + tid];  // U[j][j .. pb+7]
+#pragma unroll
+      for (int q = 0; q < R; ++q) {
+        if (!act[q]) continue;
+        if (tid * R + q == p) {
+          act[q] = false;
+          pstep[q] = s;  // this row is the panel's s-th pivot
+          continue;
+        }
+        const double mult = w[q][s] * uinv;
+        w[q][s] = mult;
+        if (final_) msm[j * CAP + tid * R + q] = mult;
+#pragma unroll
+        for (int t = s + 1; t < 8; ++t) w[q][t] = fma(-mult, prow[t], w[q][t]);
+      }
+    }
+    if (pb + 8 >= LP) break;  // no trailing columns
+    // ---- panel end: U12 (rows of U right of the panel) by forward substitution
+#pragma unroll
+    for (int q = 0; q < R; ++q)
+      if (pstep[q] >= 0) {
+        const int sp = pstep[q];
+#pragma unroll
+        for (int t = 8; t < LP; ++t) traw[sp][t - 8] = w[q][t];
+#pragma unroll
+        for (int t = 0; t < 8; ++t) l11[sp][t] = t < sp ? w[q][t] : 0.0;
+        pstep[q] = -2;  // published; the row is done
+      }
+    __syncthreads();
+    if (tid < LP - 8) {
+      double u[8];
+#pragma unroll
+      for (int sp = 0; sp < 8; ++sp) {
+        double v = sp < ns ? traw[sp][tid] : 0.0;
+#pragma unroll
+        for (int s2 = 0; s2 < sp; ++s2) v = fma(-l11[sp][s2], u[s2], v);
+        u[sp] = v;
+        u12[sp][tid] = v;
+        if (final_ && sp < ns) keep[(pb + sp) * LP + (8 - sp) + tid] = v;  // U[j][pb+8+tid]
+      }
     }
     __syncthreads();
-    // max over the 8 warp winners in a fixed 3-level tree (lower warp on ties)
-    uint2 k[kWarps];
-    int wi[kWarps];
-#pragma unroll
-    for (int i = 0; i < kWarps; ++i) {
-      k[i] = slot[j & 1][i];
-      wi[i] = i;
-    }
-#pragma unroll
-    for (int st = 1; st < kWarps; st <<= 1)
-#pragma unroll
-      for (int i = 0; i < kWarps; i += 2 * st)
-        if (k[i + st].x > k[i].x) { k[i] = k[i + st]; wi[i] = wi[i + st]; }
-    const int p = (int)k[0].y;
-    const double uinv = suinv[j & 1][wi[0]];
-    const double* prow = buf[j & 1][wi[0]];
-    if (tid == 0) piv[j] = p;
-    if (final_ && tid < LP) keep[j * LP + tid] = prow[tid];
+    const int live = LP - pb;  // columns beyond are zero in every row
 #pragma unroll
     for (int q = 0; q < R; ++q) {
       if (!act[q]) continue;
-      if (tid * R + q == p) { act[q] = false; continue; }
-      const double mult = w[q][0] * uinv;
-      if (final_) msm[j * CAP + tid * R + q] = mult;
-      // only the live width: columns ≥ LP − j are zero (and stay zero)
-      if (j >= (3 * LP) / 4) eliminate<LP, LP / 4>(w[q], prow, mult);
-      else if (j >= LP / 2) eliminate<LP, LP / 2>(w[q], prow, mult);
-      else if (j >= LP / 4) eliminate<LP, (3 * LP) / 4>(w[q], prow, mult);
-      else eliminate<LP, LP>(w[q], prow, mult);
+      if (live > LP / 2) trail_update<LP, LP>(w[q], u12, ns);
+      else trail_update<LP, LP / 2>(w[q], u12, ns);
     }
   }
   __syncthreads();
