@@ -41,33 +41,29 @@ __global__ void __launch_bounds__(kThreads) chol_kernel(const double* __restrict
   __syncthreads();
   double gmax = 0.0;
   for (int j = 0; j < l; ++j) gmax = fmax(gmax, G[j * l + j]);
+  // right-looking: column j's pivot, then row j of R, then the rank-1 update
+  // of the trailing block of G — every step fully parallel
+  const double floor_ = 0x1p-104 * gmax;  // L (and Q1) are full rank; guard against roundoff only
   for (int j = 0; j < l; ++j) {
-    if (tid == 0) {
-      double dj = G[j * l + j];
-      for (int t = 0; t < j; ++t) dj -= R[t * l + j] * R[t * l + j];
-      // L (and Q1) are full rank by construction; guard against roundoff only
-      const double floor_ = 0x1p-104 * gmax;
-      R[j * l + j] = sqrt(dj > floor_ ? dj : (floor_ > 0.0 ? floor_ : 1.0));
-    }
+    const double dj = G[j * l + j];
+    const double rjj = sqrt(dj > floor_ ? dj : (floor_ > 0.0 ? floor_ : 1.0));
+    for (int i = j + tid; i < l; i += kThreads) R[j * l + i] = i == j ? rjj : G[j * l + i] / rjj;
     __syncthreads();
-    for (int i = j + 1 + tid; i < l; i += kThreads) {
-      double s = G[j * l + i];
-      for (int t = 0; t < j; ++t) s -= R[t * l + j] * R[t * l + i];
-      R[j * l + i] = s / R[j * l + j];
+    const int w = l - j - 1;
+    for (int idx = tid; idx < w * w; idx += kThreads) {
+      const int a = j + 1 + idx / w, b = j + 1 + idx % w;
+      G[a * l + b] -= R[j * l + a] * R[j * l + b];
     }
     __syncthreads();
   }
-  // X = R⁻¹ (upper): warp per column, M[i][j] = −(Σ_{t=i+1..j} R_it X_tj)/R_ii
-  const int lane = tid & 31, warp = tid >> 5;
-  for (int j = warp; j < l; j += kThreads / 32) {
-    for (int i = lane; i < l; i += 32) X[i * l + j] = 0.0;
-    __syncwarp();
-    for (int i = j; i >= 0; --i) {
+  // X = R⁻¹ (upper): thread j owns column j, back substitution with i
+  // descending in lock-step (R reads are broadcasts)
+  if (tid < l) {
+    const int j = tid;
+    for (int i = l - 1; i >= 0; --i) {
       double s = 0.0;
-      for (int t = i + 1 + lane; t <= j; t += 32) s += R[i * l + t] * X[t * l + j];
-      s = warp_sum(s);
-      if (lane == 0) X[i * l + j] = ((i == j ? 1.0 : 0.0) - s) / R[i * l + i];
-      __syncwarp();
+      for (int t = i + 1; t <= j; ++t) s += R[i * l + t] * X[t * l + j];
+      X[i * l + j] = i <= j ? ((i == j ? 1.0 : 0.0) - s) / R[i * l + i] : 0.0;
     }
   }
   __syncthreads();

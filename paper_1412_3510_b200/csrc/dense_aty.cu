@@ -141,33 +141,30 @@ __global__ void __launch_bounds__(kThreads, 1)
 }
 
 // Z[c][j] = Σ_{p covering cb(c), ascending} part[p][slot][c mod 128][j] − cmean[c]·sy[j]
-// Z[c][j] = Σ_{p covering cb(c), ascending} part[p][slot][c mod 128][j] − cmean[c]·sy[j]
-// One warp per output: lane λ sums the CTAs p ≡ λ (mod 32) of the covering
-// range in ascending order, then a fixed shuffle tree — deterministic.
+// One thread per output: the few CTAs covering column block cb(c) (stream-K
+// ranges) are summed in ascending order — deterministic.
 __global__ void aty_reduce_kernel(const double* __restrict__ part, Split sp, int maxslots, int64_t n, int l, int LP,
                                   const double* __restrict__ cmean, const double* __restrict__ sy,
                                   double* __restrict__ Z) {
   const int64_t total = n * l;
-  const int lane = threadIdx.x & 31;
-  const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
-  for (int64_t idx = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); idx < total; idx += warps) {
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
     const int64_t c = idx / l;
     const int j = (int)(idx - c * l);
     const int64_t cb = c / BN;
     const int cl = (int)(c - cb * BN);
     const int64_t ustart = cb * sp.cpc, uend = ustart + sp.cpc;
-    int64_t p0 = (ustart * sp.P) / sp.U;
-    if (p0 > 0) --p0;
-    while (p0 < sp.P && sp.u0(p0 + 1) <= ustart) ++p0;
+    int64_t p = (ustart * sp.P) / sp.U;  // first CTA whose range can reach ustart
+    if (p > 0) --p;
+    while (p < sp.P && sp.u0(p + 1) <= ustart) ++p;
     double s = 0.0;
-    for (int64_t p = p0 + lane; p < sp.P && sp.u0(p) < uend; p += 32) {
+    for (; p < sp.P && sp.u0(p) < uend; ++p) {
       const int64_t a = sp.u0(p), b = sp.u0(p + 1);
       if (b <= a) continue;
       const int64_t slot = cb - a / sp.cpc;
       s += part[((p * maxslots + slot) * BN + cl) * LP + j];
     }
-    s = warp_sum(s);
-    if (lane == 0) Z[idx] = cmean ? s - cmean[c] * sy[j] : s;
+    Z[idx] = cmean ? s - cmean[c] * sy[j] : s;
   }
 }
 
@@ -298,7 +295,7 @@ void aty_reduce_partials(Ctx& c, const double* part, int64_t U, int64_t P, int64
   sp.P = P;
   sp.cpc = cpc;
   const int64_t total = n * l;
-  const unsigned grid = (unsigned)std::min<int64_t>(cdiv(total, 8), (int64_t)c.num_sms * 32);
+  const unsigned grid = (unsigned)std::min<int64_t>(cdiv(total, 256), (int64_t)c.num_sms * 16);
   aty_reduce_kernel<<<grid, 256, 0, c.stream>>>(part, sp, maxslots, n, l, LP, cmean, sy, Z);
   RPCA_CHECK_LAUNCH();
   count_launch(c, 1, "aty_reduce");
@@ -351,7 +348,7 @@ void dense_aty(Ctx& c, const DenseA& A, const double* Y, int l, const double* cm
       default: launch_aty_tma<8>(c, A, Yp, sp, ms, part); break;
     }
     const int64_t total = A.n * l;
-    const unsigned grid = (unsigned)std::min<int64_t>(cdiv(total, 8), (int64_t)c.num_sms * 32);
+    const unsigned grid = (unsigned)std::min<int64_t>(cdiv(total, 256), (int64_t)c.num_sms * 16);
     aty_reduce_kernel<<<grid, 256, 0, c.stream>>>(part, sp, ms, A.n, l, NT * 8, cmean, sy, Z);
     RPCA_CHECK_LAUNCH();
     count_launch(c, 1, "aty_reduce");

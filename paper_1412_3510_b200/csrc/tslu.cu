@@ -39,11 +39,16 @@ namespace {
 constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
 
-template <int LP>
+// rows per thread: leaves favour occupancy, tree levels (few CTAs, latency-
+// bound) favour bigger groups so the tournament has fewer levels
+constexpr int leaf_rows_per_thread(int LP) { return LP <= 8 ? 4 : (LP <= 16 ? 2 : 1); }
+constexpr int tree_rows_per_thread(int LP) { return LP <= 8 ? 4 : (LP <= 32 ? 2 : 1); }
+
+template <int LP, int RR>
 struct SelCfg {
-  static constexpr int R = LP <= 8 ? 4 : (LP <= 16 ? 2 : 1);  // rows per thread
-  static constexpr int kCap = kThreads * R;                    // rows per CTA
-  static constexpr int kMinBlocks = LP <= 32 ? 2 : 1;
+  static constexpr int R = RR;
+  static constexpr int kCap = kThreads * R;  // rows per CTA
+  static constexpr int kMinBlocks = R * LP <= 32 ? 2 : 1;
 };
 
 // Pivot key of a value: the high word of |v| (11 exponent + 20 mantissa bits)
@@ -89,13 +94,13 @@ __device__ __forceinline__ void trail_update(double (&w)[LP], const double (*u12
 //   leaf: 1 = contiguous rows of Y; 0 = candidate ids into Y; 2 = candidate
 //   rows given directly (rows_in, one l-vector per slot; ids are global rows
 //   — the all-gathered local winners of a row-sharded LU)
-template <int LP>
-__global__ void __launch_bounds__(kThreads, SelCfg<LP>::kMinBlocks)
+template <int LP, int RR>
+__global__ void __launch_bounds__(kThreads, SelCfg<LP, RR>::kMinBlocks)
     lu_select_kernel(const double* __restrict__ Y, int64_t m, int l, int leaf, const int64_t* __restrict__ cand_in,
                      int64_t n_in, int G, int64_t* __restrict__ cand_out, int final_, double* __restrict__ U,
                      double* __restrict__ Lp, int64_t* __restrict__ piv_out, double* __restrict__ M,
                      const double* __restrict__ rows_in, double* __restrict__ rows_out) {
-  using Cfg = SelCfg<LP>;
+  using Cfg = SelCfg<LP, RR>;
   constexpr int R = Cfg::R, CAP = Cfg::kCap;
   __shared__ int64_t ids[CAP];
   __shared__ int slot_of[CAP];
@@ -349,24 +354,31 @@ __global__ void pack_candidates_kernel(const double* __restrict__ Y, int l, int6
 }
 
 int lp_of(int l) { return (l + 7) & ~7; }
-int cap_of(int l) {
-  switch (lp_of(l)) {
-    case 8: return SelCfg<8>::kCap;
-    case 16: return SelCfg<16>::kCap;
-    default: return kThreads;
-  }
-}
+int leaf_cap(int l) { return kThreads * leaf_rows_per_thread(lp_of(l)); }
+int tree_cap(int l) { return kThreads * tree_rows_per_thread(lp_of(l)); }
 // a tree group stacks G candidate sets of l rows into one CTA's rows
-int group_for(int l) { return std::max(2, cap_of(l) / l); }
+int group_for(int l) { return std::max(2, tree_cap(l) / l); }
+
+template <int LP, int R>
+void select_lpr(Ctx& c, unsigned grid, const double* Y, int64_t m, int l, int leaf, const int64_t* cin, int64_t n_in,
+                int G, int64_t* cout, int final_, double* U, double* Lp, int64_t* piv, double* M,
+                const double* rows_in, double* rows_out) {
+  const size_t smem = final_ ? (size_t)(LP * LP + l * l + (size_t)SelCfg<LP, R>::kCap * l) * 8 : 0;
+  if (smem) ensure_smem((const void*)lu_select_kernel<LP, R>, (int)smem);
+  lu_select_kernel<LP, R><<<grid, kThreads, smem, c.stream>>>(Y, m, l, leaf, cin, n_in, G, cout, final_, U, Lp, piv,
+                                                              M, rows_in, rows_out);
+}
 
 template <int LP>
 void select_lp(Ctx& c, unsigned grid, const double* Y, int64_t m, int l, int leaf, const int64_t* cin, int64_t n_in,
                int G, int64_t* cout, int final_, double* U, double* Lp, int64_t* piv, double* M,
                const double* rows_in, double* rows_out) {
-  const size_t smem = final_ ? (size_t)(LP * LP + l * l + (size_t)SelCfg<LP>::kCap * l) * 8 : 0;
-  if (smem) ensure_smem((const void*)lu_select_kernel<LP>, (int)smem);
-  lu_select_kernel<LP><<<grid, kThreads, smem, c.stream>>>(Y, m, l, leaf, cin, n_in, G, cout, final_, U, Lp, piv,
-                                                           M, rows_in, rows_out);
+  if (leaf == 1)
+    select_lpr<LP, leaf_rows_per_thread(LP)>(c, grid, Y, m, l, leaf, cin, n_in, G, cout, final_, U, Lp, piv, M,
+                                             rows_in, rows_out);
+  else
+    select_lpr<LP, tree_rows_per_thread(LP)>(c, grid, Y, m, l, leaf, cin, n_in, G, cout, final_, U, Lp, piv, M,
+                                             rows_in, rows_out);
 }
 
 void select(Ctx& c, unsigned grid, const double* Y, int64_t m, int l, int leaf, const int64_t* cin, int64_t n_in,
@@ -398,7 +410,7 @@ void select(Ctx& c, unsigned grid, const double* Y, int64_t m, int l, int leaf, 
 int64_t* tournament(Ctx& c, const double* Y, int64_t m, int l, bool finalize, double* U, double* Lp, int64_t* piv,
                     double* M, Arena& ar) {
   const int G = group_for(l);
-  const int64_t nblk = std::max<int64_t>(1, cdiv(m, cap_of(l)));
+  const int64_t nblk = std::max<int64_t>(1, cdiv(m, leaf_cap(l)));
   int64_t* ca = ar.get<int64_t>(nblk * l);
   int64_t* cb = ar.get<int64_t>(nblk * l);
   if (m == 0) {
