@@ -4,8 +4,10 @@
 // jacobi_svd_small: the SVD of eq. (i3), PAPER.md:133-139 ("W Σ V* = B"),
 // applied to the l×l triangular factor R of Bᵀ = Q_B·R (so B = Rᵀ Q_Bᵀ).
 // One-sided Hestenes Jacobi on the columns of R (readings Q9/Q18):
-// rotate a pair iff |γ| > 2^-52·sqrt(αβ), stop after a sweep without a
-// rotation or after 30 sweeps.  Pairs are scheduled in parallel rounds
+// rotate a pair iff |γ| > l·2^-52·sqrt(αβ) — the rounding level of an l-term
+// dot product (the oracle's 2^-52 is below it, so its cyclic sweeps keep
+// rotating on rounding noise until the 30-sweep cap) — stop after a sweep
+// without a rotation or after 30 sweeps.  Pairs are scheduled in parallel rounds
 // (round-robin tournament: l/2 disjoint pairs per round, one warp per pair);
 // the oracle sweeps cyclically — same fixed point up to rounding.
 // Result: R·W = Vr·diag(σ), σ sorted non-increasing (stable), zero-σ
@@ -39,7 +41,7 @@ __global__ void __launch_bounds__(kJThreads) jacobi_kernel(const double* __restr
   if (tid < 2) rotated[tid] = 0;
   __syncthreads();
   const int lp = (l + 1) & ~1;  // players (one dummy if l is odd)
-  const double eps = 0x1p-52;
+  const double eps = 0x1p-52 * (double)l;
   for (int sweep = 0; sweep < 30 && l > 1; ++sweep) {
     for (int round = 0; round < lp - 1; ++round) {
       const int k = warp;
