@@ -26,6 +26,7 @@ constexpr int BM = 128;          // rows per tile
 constexpr int BK = 32;           // k per stage (two TMA boxes of 16 doubles)
 constexpr int kConsumerWarps = 8;
 constexpr int kThreads = (kConsumerWarps + 1) * 32;
+constexpr int kMaxSms = 160;  // stream-K partial slots (≥ the SM count)
 
 template <int NT>
 struct AxCfg {
@@ -44,16 +45,32 @@ struct AxCfg {
 // as a double2.  Within each 8-lane LDS.128 phase (rows r, r+1) the swizzled
 // chunk positions (2c + (q&1)) ^ (r&7) are all distinct: conflict-free.
 // Packed X holds X[that same k][nt·8 + (lane>>2)] at Xp[kb][st][nt][lane].
+// Stream-K work split: unit u = tile·KB + kb; CTA p owns units
+// [p·U/P, (p+1)·U/P).  A tile the CTA covers whole is written to Y directly;
+// a tile cut by a CTA boundary leaves fp64 partial rows in part[p][slot]
+// (slot 0 = the CTA's first tile, 1 = its last) that ax_fixup_kernel sums in
+// ascending CTA order — every CTA gets the same number of k-blocks (no tail
+// wave: C2's 782 tiles on 148 SMs left 12% idle) and the result is
+// deterministic.
+struct AxSplit {
+  int64_t U, P;
+  int KB;
+  __host__ __device__ int64_t u0(int64_t p) const { return p * U / P; }
+};
+
 template <int NT>
 __global__ void __launch_bounds__(kThreads, 1)
     ax_f64_tma_kernel(const __grid_constant__ CUtensorMap tmA, const double* __restrict__ Xp, int64_t m, int l,
-                      int64_t ntiles, int KB, double* __restrict__ Y) {
+                      AxSplit sp, double* __restrict__ Y, double* __restrict__ part) {
   using Cfg = AxCfg<NT>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + Cfg::kStages * Cfg::kStageBytes);
   uint64_t* empty = full + Cfg::kStages;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int KB = sp.KB;
+  const int64_t ub = sp.u0(blockIdx.x), ue = sp.u0(blockIdx.x + 1);
+  const int64_t tile_first = ub / KB;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < Cfg::kStages; ++s) {
@@ -63,6 +80,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     fence_barrier_init();
   }
   __syncthreads();
+  if (ub >= ue) return;
 
   if (warp == kConsumerWarps) {
     // ------------------------------------------------------------ producer
@@ -70,16 +88,17 @@ __global__ void __launch_bounds__(kThreads, 1)
       prefetch_tmap(&tmA);
       int s = 0;
       uint32_t ph = 0;
-      for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-        for (int kb = 0; kb < KB; ++kb) {
-          mbar_wait(&empty[s], ph ^ 1);
-          uint8_t* st = smem + s * Cfg::kStageBytes;
-          mbar_arrive_expect_tx(&full[s], Cfg::kStageBytes);
-          tma_load_2d(st, &tmA, kb * BK, (int32_t)(tile * BM), &full[s]);
-          tma_load_2d(st + BM * 128, &tmA, kb * BK + 16, (int32_t)(tile * BM), &full[s]);
-          bulk_load(st + Cfg::kABytes, Xp + (int64_t)kb * 256 * NT, Cfg::kXBytes, &full[s]);
-          if (++s == Cfg::kStages) { s = 0; ph ^= 1; }
-        }
+      int64_t tile = tile_first;
+      int kb = (int)(ub - tile_first * KB);
+      for (int64_t u = ub; u < ue; ++u) {
+        mbar_wait(&empty[s], ph ^ 1);
+        uint8_t* st = smem + s * Cfg::kStageBytes;
+        mbar_arrive_expect_tx(&full[s], Cfg::kStageBytes);
+        tma_load_2d(st, &tmA, kb * BK, (int32_t)(tile * BM), &full[s]);
+        tma_load_2d(st + BM * 128, &tmA, kb * BK + 16, (int32_t)(tile * BM), &full[s]);
+        bulk_load(st + Cfg::kABytes, Xp + (int64_t)kb * 256 * NT, Cfg::kXBytes, &full[s]);
+        if (++s == Cfg::kStages) { s = 0; ph ^= 1; }
+        if (++kb == KB) { kb = 0; ++tile; }
       }
     }
     return;
@@ -89,14 +108,20 @@ __global__ void __launch_bounds__(kThreads, 1)
   int s = 0;
   uint32_t ph = 0;
   const int rsel = lane >> 2;
-  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+  int64_t tile = tile_first;
+  int kb = (int)(ub - tile_first * KB);
+  int64_t u = ub;
+  while (u < ue) {
+    const bool starts = (kb == 0);
+    const int kend = (int)imin64(KB, kb + (ue - u));  // this CTA's k-blocks of the tile: [kb, kend)
+    const bool whole = starts && kend == KB;
     double acc[2][NT][2];
 #pragma unroll
     for (int mt = 0; mt < 2; ++mt)
 #pragma unroll
       for (int nt = 0; nt < NT; ++nt) acc[mt][nt][0] = acc[mt][nt][1] = 0.0;
 
-    for (int kb = 0; kb < KB; ++kb) {
+    for (; kb < kend; ++kb, ++u) {
       mbar_wait(&full[s], ph);
       const uint8_t* As = smem + s * Cfg::kStageBytes;
       const double* Xs = reinterpret_cast<const double*>(As + Cfg::kABytes);
@@ -126,15 +151,25 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (++s == Cfg::kStages) { s = 0; ph ^= 1; }
     }
     // epilogue: D rows = lane>>2, cols 2·(lane&3) + {0,1}
+    double* dst = Y;
+    int64_t ld = l, rbase = tile * BM;
+    if (!whole) {  // partial rows of a split tile → this CTA's slot
+      dst = part + ((int64_t)blockIdx.x * 2 + (tile == tile_first ? 0 : 1)) * BM * (NT * 8);
+      ld = NT * 8;
+      rbase = 0;
+    }
 #pragma unroll
     for (int mt = 0; mt < 2; ++mt) {
-      const int64_t row = tile * BM + warp * 16 + mt * 8 + rsel;
-      if (row >= m) continue;
+      const int rt = warp * 16 + mt * 8 + rsel;
+      if (tile * BM + rt >= m) continue;
+      const int64_t row = rbase + rt;
 #pragma unroll
       for (int nt = 0; nt < NT; ++nt) {
         const int col = nt * 8 + 2 * (lane & 3);
-        double* y = Y + row * l + col;
-        if (col + 1 < l) {
+        double* y = dst + row * ld + col;
+        if (!whole) {
+          *reinterpret_cast<double2*>(y) = make_double2(acc[mt][nt][0], acc[mt][nt][1]);
+        } else if (col + 1 < l) {
           if ((l & 1) == 0)
             *reinterpret_cast<double2*>(y) = make_double2(acc[mt][nt][0], acc[mt][nt][1]);
           else {
@@ -146,7 +181,65 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
     }
+    if (kb == KB) { kb = 0; ++tile; }
   }
+}
+
+// Split tiles: block b looks at CTA boundary p = b+1; if it cuts a tile and is
+// the first boundary inside it, the block sums that tile's partials over the
+// covering CTAs in ascending order and writes its rows of Y.
+__global__ void ax_fixup_kernel(AxSplit sp, int64_t m, int l, int LP, const double* __restrict__ part,
+                                double* __restrict__ Y) {
+  __shared__ int64_t t_s, pa_s;
+  __shared__ int nq_s;
+  __shared__ const double* src[32];  // the covering CTAs' partial slots, ascending
+  if (threadIdx.x == 0) {
+    nq_s = 0;
+    const int64_t p = blockIdx.x + 1;
+    const int64_t KB = sp.KB;
+    const int64_t b = sp.u0(p);
+    const int64_t t = b / KB;
+    // act only for the first boundary strictly inside a tile
+    if (b % KB != 0 && b < sp.U && sp.u0(p - 1) <= t * KB) {
+      int64_t q = p - 1;  // CTA holding unit t·KB
+      int nq = 0;
+      for (; q < sp.P && sp.u0(q) < (t + 1) * KB && nq < 32; ++q, ++nq) {
+        const int slot = (sp.u0(q) / KB == t) ? 0 : 1;  // t is q's first tile, or its last
+        src[nq] = part + (q * 2 + slot) * BM * LP;
+      }
+      nq_s = nq;
+      t_s = t;
+    }
+  }
+  __syncthreads();
+  const int nq = nq_s;
+  if (nq == 0) return;
+  const int64_t t = t_s;
+  const int nrow = (int)imin64(BM, m - t * BM);
+  double* __restrict__ yt = Y + t * BM * l;
+  // four outputs per thread in flight (the loads do not alias the stores)
+  for (int idx0 = threadIdx.x; idx0 < nrow * l; idx0 += 4 * blockDim.x) {
+    double s[4] = {0.0, 0.0, 0.0, 0.0};
+    int off[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const int idx = idx0 + e * blockDim.x;
+      const int r = idx / l, j = idx - r * l;
+      off[e] = idx < nrow * l ? r * LP + j : -1;
+    }
+    for (int k = 0; k < nq; ++k) {
+      const double* __restrict__ sk = src[k];
+#pragma unroll
+      for (int e = 0; e < 4; ++e)
+        if (off[e] >= 0) s[e] += __ldg(sk + off[e]);
+    }
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const int idx = idx0 + e * blockDim.x;
+      if (idx < nrow * l) yt[idx] = s[e];
+    }
+  }
+  (void)pa_s;
 }
 
 // Generic CUDA-core fallback: 64-row tiles, X and A chunks staged in smem (fp64).
@@ -208,7 +301,7 @@ PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
 }
 
 template <int NT>
-void launch_ax_tma(Ctx& c, const DenseA& A, const double* Xp, int l, double* Y) {
+void launch_ax_tma(Ctx& c, const DenseA& A, const double* Xp, int l, double* Y, double* part) {
   using Cfg = AxCfg<NT>;
   CUtensorMap tm;
   cuuint64_t dims[2] = {(cuuint64_t)A.n, (cuuint64_t)A.m};
@@ -222,11 +315,24 @@ void launch_ax_tma(Ctx& c, const DenseA& A, const double* Xp, int l, double* Y) 
   ensure_smem((const void*)ax_f64_tma_kernel<NT>, Cfg::kSmem);
   const int64_t ntiles = cdiv(A.m, BM);
   const int KB = (int)cdiv(A.n, BK);
-  const int grid = (int)std::min<int64_t>(ntiles, c.num_sms);
+  AxSplit sp;
+  sp.KB = KB;
+  sp.U = ntiles * KB;
+  sp.P = std::min<int64_t>({sp.U, (int64_t)c.num_sms, ntiles * 16});  // a tile spans ≤ ~17 CTAs (fixup ≤ 32)
+  // whole tiles when they balance already or K is short (the thin-block
+  // products: K = l ≤ 64) — splitting those would only add fixup launches
+  if (ntiles % sp.P == 0 || KB < 8) sp.P = std::min<int64_t>(ntiles, c.num_sms);
+  bool split = false;  // does any CTA boundary cut a tile?
+  for (int64_t q = 1; q < sp.P && !split; ++q) split = sp.u0(q) % KB != 0;
   prof_pre(c);
-  ax_f64_tma_kernel<NT><<<grid, kThreads, Cfg::kSmem, c.stream>>>(tm, Xp, A.m, l, ntiles, KB, Y);
+  ax_f64_tma_kernel<NT><<<(unsigned)sp.P, kThreads, Cfg::kSmem, c.stream>>>(tm, Xp, A.m, l, sp, Y, part);
   RPCA_CHECK_LAUNCH();
   count_launch(c, 1, c.tag ? c.tag : "ax_f64_dmma");
+  if (split && sp.P > 1) {
+    ax_fixup_kernel<<<(unsigned)(sp.P - 1), 256, 0, c.stream>>>(sp, A.m, l, NT * 8, part, Y);
+    RPCA_CHECK_LAUNCH();
+    count_launch(c, 1, "stream_k_fixup");
+  }
 }
 
 bool tma_ok(const DenseA& A) {
@@ -240,6 +346,7 @@ size_t ax_ws_bytes(const DenseA& A, int l) {
   if (f32_tc_ok(A)) return ax_f32_ws_bytes(A, l);
   Sizer s;
   s.add<double>(packx_elems(A.n, l));
+  s.add<double>((size_t)kMaxSms * 2 * BM * ((l + 7) / 8 * 8));  // stream-K partial rows
   return s.total;
 }
 
@@ -257,16 +364,17 @@ void dense_ax(Ctx& c, const DenseA& A, const double* X, int l, double* Y, Arena&
   }
   if (tma_ok(A)) {
     double* Xp = ar.get<double>(packx_elems(A.n, l));
+    double* part = ar.get<double>((size_t)kMaxSms * 2 * BM * ((l + 7) / 8 * 8));
     pack_x(c, X, A.n, l, Xp);
     switch ((l + 7) / 8) {
-      case 1: launch_ax_tma<1>(c, A, Xp, l, Y); break;
-      case 2: launch_ax_tma<2>(c, A, Xp, l, Y); break;
-      case 3: launch_ax_tma<3>(c, A, Xp, l, Y); break;
-      case 4: launch_ax_tma<4>(c, A, Xp, l, Y); break;
-      case 5: launch_ax_tma<5>(c, A, Xp, l, Y); break;
-      case 6: launch_ax_tma<6>(c, A, Xp, l, Y); break;
-      case 7: launch_ax_tma<7>(c, A, Xp, l, Y); break;
-      default: launch_ax_tma<8>(c, A, Xp, l, Y); break;
+      case 1: launch_ax_tma<1>(c, A, Xp, l, Y, part); break;
+      case 2: launch_ax_tma<2>(c, A, Xp, l, Y, part); break;
+      case 3: launch_ax_tma<3>(c, A, Xp, l, Y, part); break;
+      case 4: launch_ax_tma<4>(c, A, Xp, l, Y, part); break;
+      case 5: launch_ax_tma<5>(c, A, Xp, l, Y, part); break;
+      case 6: launch_ax_tma<6>(c, A, Xp, l, Y, part); break;
+      case 7: launch_ax_tma<7>(c, A, Xp, l, Y, part); break;
+      default: launch_ax_tma<8>(c, A, Xp, l, Y, part); break;
     }
     return;
   }
