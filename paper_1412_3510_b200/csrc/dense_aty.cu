@@ -73,8 +73,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       prefetch_tmap(&tmA);
       int s = 0;
       uint32_t ph = 0;
-      for (int64_t u = ub; u < ue; ++u) {
-        const int64_t cb = u / sp.cpc, rc = u - cb * sp.cpc;
+      int64_t cb = ub / sp.cpc, rc = ub - cb * sp.cpc;
+      for (int64_t u = ub; u < ue; ++u, ++rc) {
+        if (rc == sp.cpc) { rc = 0; ++cb; }
         mbar_wait(&empty[s], ph ^ 1);
         uint8_t* st = smem + s * Cfg::kStageBytes;
         mbar_arrive_expect_tx(&full[s], Cfg::kStageBytes);
@@ -100,8 +101,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int nt = 0; nt < NT; ++nt) acc[mt][nt][0] = acc[mt][nt][1] = 0.0;
   };
   zero();
+  int64_t cb = cb_first, rc = ub - cb_first * sp.cpc;  // no 64-bit division per unit
   for (int64_t u = ub; u < ue; ++u) {
-    const int64_t cb = u / sp.cpc;
     mbar_wait(&full[s], ph);
     const uint8_t* box = smem + s * Cfg::kStageBytes + warp * (BR * 128);
     const double* Ys = reinterpret_cast<const double*>(smem + s * Cfg::kStageBytes + Cfg::kABytes);
@@ -123,7 +124,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[s]);
     if (++s == Cfg::kStages) { s = 0; ph ^= 1; }
-    const bool last_of_cb = (u + 1 == ue) || ((u + 1) / sp.cpc != cb);
+    const bool last_of_cb = (u + 1 == ue) || (rc + 1 == sp.cpc);
     if (last_of_cb) {
       double* dst = part + ((p * maxslots + (cb - cb_first)) * BN) * LP;
 #pragma unroll
@@ -137,6 +138,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       zero();
     }
+    if (++rc == sp.cpc) { rc = 0; ++cb; }
   }
 }
 
