@@ -126,18 +126,24 @@ class ClockSampler:
                 self.reasons |= nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
             except Exception:
                 pass
-            time.sleep(0.005)
+            time.sleep(0.001)
 
     def __enter__(self):
         if self.ok:
+            self._interval = sys.getswitchinterval()
+            sys.setswitchinterval(0.0005)  # let the sampler in between the (GIL-releasing) library calls
             self.t = threading.Thread(target=self._run, daemon=True)
             self.t.start()
+            t0 = time.perf_counter()
+            while not self.samples and time.perf_counter() - t0 < 0.5:
+                time.sleep(0.0005)
         return self
 
     def __exit__(self, *a):
         if self.ok:
             self._stop.set()
             self.t.join()
+            sys.setswitchinterval(self._interval)
 
     def summary(self):
         if not self.ok or not self.samples:
