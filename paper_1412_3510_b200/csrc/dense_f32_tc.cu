@@ -382,7 +382,7 @@ struct AtyCfg {
 template <int N>
 __global__ void __launch_bounds__(kThreadsTC, 1)
     aty_f32_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmYh,
-                      const __grid_constant__ CUtensorMap tmYl, AtyPlan pl, double* __restrict__ part) {
+                      const __grid_constant__ CUtensorMap tmYl, AtyPlan pl, int a3d, double* __restrict__ part) {
   using Cfg = AtyCfg<N>;
   constexpr int S = Cfg::kStages, YS = Cfg::kYS;
   constexpr int RC = kKChunk / 32;  // row chunks per fp32 accumulation
@@ -451,9 +451,14 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
         uint8_t* st = smem + rg.s * kTileBytes;
         if (leader) {
           mbar_arrive_expect_tx(&full[rg.s], kTileBytes);
+          if (a3d) {  // one 3-D box (32 cols × 32 rows × 4 column groups) = the four 4 KB MN chunks
+            tma_load_3d(st, &tmA, 0, (int32_t)(rc * 32), (int32_t)((cb0 + cbi) * 4), &full[rg.s]);
+          } else {
 #pragma unroll
-          for (int b = 0; b < 4; ++b)  // four [32 rows × 32 cols] boxes (128B_ATOM_32B), MN chunks 4 KB apart
-            tma_load_2d(st + b * 4096, &tmA, (int32_t)((cb0 + cbi) * 128 + b * 32), (int32_t)(rc * 32), &full[rg.s]);
+            for (int b = 0; b < 4; ++b)  // four [32 rows × 32 cols] boxes (128B_ATOM_32B), MN chunks 4 KB apart
+              tma_load_2d(st + b * 4096, &tmA, (int32_t)((cb0 + cbi) * 128 + b * 32), (int32_t)(rc * 32),
+                          &full[rg.s]);
+          }
         }
         __syncwarp();
       }
@@ -708,12 +713,27 @@ template <int N>
 void launch_aty(Ctx& c, const DenseA& A, const float* hi, const float* lo, int64_t Kpad, const AtyPlan& pl,
                 double* part) {
   using Cfg = AtyCfg<N>;
-  const CUtensorMap tA = tmap_f32(A.a, A.n, A.m, A.lda, 32, 32, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
+  // n ≡ 0 (mod 32): the tile is one 3-D box (dims: 32 columns, rows, column
+  // groups of 32) — no reads past a row's n columns; otherwise four 2-D boxes
+  const int a3d = (A.n % 32 == 0) ? 1 : 0;
+  CUtensorMap tA;
+  if (a3d) {
+    cuuint64_t dims[3] = {32, (cuuint64_t)A.m, (cuuint64_t)(A.n / 32)};
+    cuuint64_t strides[2] = {(cuuint64_t)A.lda * 4, 128};
+    cuuint32_t box[3] = {32, 32, 4};
+    cuuint32_t estr[3] = {1, 1, 1};
+    CUresult r = get_encode()(&tA, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<void*>(A.a), dims, strides, box,
+                              estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B,
+                              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    RPCA_REQUIRE(r == CUDA_SUCCESS, RPCA_E_CUDA, "cuTensorMapEncodeTiled(f32, 3-D) failed (%d)", (int)r);
+  } else {
+    tA = tmap_f32(A.a, A.n, A.m, A.lda, 32, 32, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
+  }
   const CUtensorMap tH = tmap_f32(hi, Kpad, N, Kpad, 32, N);
   const CUtensorMap tL = tmap_f32(lo, Kpad, N, Kpad, 32, N);
   ensure_smem((const void*)aty_f32_tc_kernel<N>, Cfg::kSmem);
   prof_pre(c);
-  aty_f32_tc_kernel<N><<<(unsigned)(pl.Gc * pl.Pg), kThreadsTC, Cfg::kSmem, c.stream>>>(tA, tH, tL, pl, part);
+  aty_f32_tc_kernel<N><<<(unsigned)(pl.Gc * pl.Pg), kThreadsTC, Cfg::kSmem, c.stream>>>(tA, tH, tL, pl, a3d, part);
   RPCA_CHECK_LAUNCH();
   count_launch(c, 1, c.tag ? c.tag : "aty_f32_tc");
 }
