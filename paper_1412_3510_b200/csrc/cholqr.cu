@@ -106,7 +106,7 @@ size_t orth_ws_bytes(int64_t m, int l) {
 
 size_t orth_ws_bytes(Ctx& c, int64_t m, int l) { return orth_ws_bytes(m, l) + gram_ws_bytes(c, m, l); }
 
-void orthonormalize(Ctx& c, double* Y, int64_t m, int l, double* R_out, Arena& ar) {
+void orthonormalize(Ctx& c, double* Y, int64_t m, int l, double* R_out, Arena& ar, const double* mu) {
   RPCA_REQUIRE(l >= 1 && l <= kMaxL && m >= l, RPCA_E_SHAPE, "orthonormalize: need 1 ≤ l ≤ %d, m ≥ l", kMaxL);
   double* U = ar.get<double>((size_t)l * l);
   double* G = ar.get<double>((size_t)l * l);
@@ -116,7 +116,7 @@ void orthonormalize(Ctx& c, double* Y, int64_t m, int l, double* R_out, Arena& a
   double* R2 = ar.get<double>((size_t)l * l);
   const DenseA Yd{Y, RPCA_F64, m, l, l};
   const size_t mark = ar.off;
-  lu_renorm(c, Y, m, l, U, nullptr, ar);  // Y ← L
+  lu_renorm(c, Y, m, l, U, nullptr, ar, mu);  // Y ← L (of Y − 1·mu when centring is pending)
   ar.off = mark;
   TagScope ts(c, "cholqr_gram");
   gram(c, Y, Y, m, l, G, ar);              // G = LᵀL
@@ -139,7 +139,8 @@ void orthonormalize(Ctx& c, double* Y, int64_t m, int l, double* R_out, Arena& a
 // each Gram is the all-reduced sum of the per-shard Grams (fixed rank order),
 // the l×l Cholesky runs redundantly on every rank and the triangular products
 // stay local.
-void orthonormalize_sharded(Ctx& c, double* Y, int64_t m, int64_t row0, int l, double* R_out, Arena& ar) {
+void orthonormalize_sharded(Ctx& c, double* Y, int64_t m, int64_t row0, int l, double* R_out, Arena& ar,
+                            const double* mu) {
   RPCA_REQUIRE(l >= 1 && l <= kMaxL && m >= 0, RPCA_E_SHAPE, "orthonormalize: need 1 ≤ l ≤ %d", kMaxL);
   double* U = ar.get<double>((size_t)l * l);
   double* G = ar.get<double>((size_t)l * l);
@@ -149,7 +150,7 @@ void orthonormalize_sharded(Ctx& c, double* Y, int64_t m, int64_t row0, int l, d
   double* R2 = ar.get<double>((size_t)l * l);
   const DenseA Yd{Y, RPCA_F64, m, l, l};
   const size_t mark = ar.off;
-  lu_renorm_sharded(c, Y, m, row0, l, U, ar);  // Y ← L (local rows)
+  lu_renorm_sharded(c, Y, m, row0, l, U, ar, mu);  // Y ← L (local rows)
   ar.off = mark;
   auto gram_all = [&] {
     c.tag = "cholqr_gram";

@@ -31,7 +31,7 @@ constexpr int kThreads = 256;
 template <class T>
 __device__ __forceinline__ void row_dot(const int32_t* __restrict__ colind, const T* __restrict__ vals, int64_t t0,
                                         int64_t t1, const double* __restrict__ X, int l, int lane, double& a0,
-                                        double& a1) {
+                                        double& a1, double& vsum) {
   for (int64_t tb = t0; tb < t1; tb += 32) {
     const int cnt = (int)imin64(32, t1 - tb);
     int myc = 0;
@@ -40,6 +40,7 @@ __device__ __forceinline__ void row_dot(const int32_t* __restrict__ colind, cons
       myc = colind[tb + lane];
       myv = static_cast<double>(vals[tb + lane]);
     }
+    vsum += myv;  // per-lane partial Σ vals (for a centred operand)
     int k = 0;
     for (; k + 4 <= cnt; k += 4) {  // four gathers in flight
       const int c0 = __shfl_sync(0xffffffffu, myc, k), c1 = __shfl_sync(0xffffffffu, myc, k + 1);
@@ -78,14 +79,20 @@ __global__ void __launch_bounds__(kThreads) csr_spmm_kernel(const int64_t* __res
                                                             const int32_t* __restrict__ colind,
                                                             const T* __restrict__ vals, int64_t rows,
                                                             const double* __restrict__ X, int l, int64_t heavy,
+                                                            const double* __restrict__ xmean,
                                                             double* __restrict__ Y) {
   const int lane = threadIdx.x & 31;
   const int64_t warps = (int64_t)gridDim.x * (kThreads / 32);
   for (int64_t i = (int64_t)blockIdx.x * (kThreads / 32) + (threadIdx.x >> 5); i < rows; i += warps) {
     const int64_t t0 = rowptr[i], t1 = rowptr[i + 1];
     if (t1 - t0 > heavy) continue;
-    double a0 = 0.0, a1 = 0.0;
-    row_dot(colind, vals, t0, t1, X, l, lane, a0, a1);
+    double a0 = 0.0, a1 = 0.0, vs = 0.0;
+    row_dot(colind, vals, t0, t1, X, l, lane, a0, a1, vs);
+    if (xmean) {  // Σ v·(x − x̄) = Σ v·x − x̄·Σ v
+      vs = warp_sum(vs);
+      if (lane < l) a0 -= xmean[lane] * vs;
+      if (lane + 32 < l) a1 -= xmean[lane + 32] * vs;
+    }
     if (lane < l) Y[i * l + lane] = a0;
     if (lane + 32 < l) Y[i * l + lane + 32] = a1;
   }
@@ -97,12 +104,18 @@ __global__ void __launch_bounds__(kThreads) csr_chunk_kernel(const int32_t* __re
                                                              const T* __restrict__ vals,
                                                              const int64_t* __restrict__ hc, int64_t nhc,
                                                              const double* __restrict__ X, int l,
+                                                             const double* __restrict__ xmean,
                                                              double* __restrict__ hpart) {
   const int lane = threadIdx.x & 31;
   const int64_t warps = (int64_t)gridDim.x * (kThreads / 32);
   for (int64_t c = (int64_t)blockIdx.x * (kThreads / 32) + (threadIdx.x >> 5); c < nhc; c += warps) {
-    double a0 = 0.0, a1 = 0.0;
-    row_dot(colind, vals, hc[3 * c + 1], hc[3 * c + 2], X, l, lane, a0, a1);
+    double a0 = 0.0, a1 = 0.0, vs = 0.0;
+    row_dot(colind, vals, hc[3 * c + 1], hc[3 * c + 2], X, l, lane, a0, a1, vs);
+    if (xmean) {
+      vs = warp_sum(vs);
+      if (lane < l) a0 -= xmean[lane] * vs;
+      if (lane + 32 < l) a1 -= xmean[lane + 32] * vs;
+    }
     hpart[c * kMaxL + lane] = a0;
     hpart[c * kMaxL + lane + 32] = a1;
   }
@@ -179,7 +192,7 @@ unsigned grid_cap(Ctx& c, int64_t work, int per) {
 
 }  // namespace
 
-void csr_spmm(Ctx& c, const CsrA& A, const double* X, int l, double* Y) {
+void csr_spmm(Ctx& c, const CsrA& A, const double* X, int l, double* Y, const double* xmean) {
   RPCA_REQUIRE(l >= 1 && l <= kMaxL, RPCA_E_SHAPE, "l out of range");
   if (A.rows == 0) return;
   const unsigned grid = grid_cap(c, A.rows, kThreads / 32);
@@ -187,20 +200,20 @@ void csr_spmm(Ctx& c, const CsrA& A, const double* X, int l, double* Y) {
   prof_pre(c);
   if (A.dtype == RPCA_F64)
     csr_spmm_kernel<double><<<grid, kThreads, 0, c.stream>>>(A.ptr, A.idx, (const double*)A.vals, A.rows, X, l, heavy,
-                                                             Y);
+                                                             xmean, Y);
   else
     csr_spmm_kernel<float><<<grid, kThreads, 0, c.stream>>>(A.ptr, A.idx, (const float*)A.vals, A.rows, X, l, heavy,
-                                                            Y);
+                                                            xmean, Y);
   RPCA_CHECK_LAUNCH();
   count_launch(c, 1, "csr_spmm");
   if (A.nhc) {
     const unsigned g2 = grid_cap(c, A.nhc, kThreads / 32);
     if (A.dtype == RPCA_F64)
       csr_chunk_kernel<double><<<g2, kThreads, 0, c.stream>>>(A.idx, (const double*)A.vals, A.hc, A.nhc, X, l,
-                                                              A.hpart);
+                                                              xmean, A.hpart);
     else
       csr_chunk_kernel<float><<<g2, kThreads, 0, c.stream>>>(A.idx, (const float*)A.vals, A.hc, A.nhc, X, l,
-                                                             A.hpart);
+                                                             xmean, A.hpart);
     RPCA_CHECK_LAUNCH();
     count_launch(c, 1, "csr_spmm_heavy");
     csr_heavy_reduce_kernel<<<grid_cap(c, A.nhr, 8), 256, 0, c.stream>>>(A.hr, A.nhr, A.hpart, l, Y);

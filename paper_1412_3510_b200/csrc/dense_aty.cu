@@ -306,7 +306,7 @@ void aty_reduce_partials(Ctx& c, const double* part, int64_t U, int64_t P, int64
 size_t aty_ws_bytes(Ctx& c, const DenseA& A, int l) {
   Sizer s;
   s.add<double>(kMaxL);                                            // sy
-  s.add<double>(std::max<int64_t>(1, cdiv(A.m, 8192)) * kMaxL);    // colsum partials
+  s.add<double>(std::max<int64_t>(1, cdiv(A.m, 2048)) * kMaxL);    // colsum partials
   if (f32_tc_ok(A)) {
     s.add<char>(aty_f32_ws_bytes(c, A, l));
   } else if (tma_ok(A)) {
@@ -315,11 +315,13 @@ size_t aty_ws_bytes(Ctx& c, const DenseA& A, int l) {
     s.add<double>(sp.P * (int64_t)max_slots(sp) * BN * cdiv(l, 8) * 8);
   } else {
     s.add<double>(generic_splits(c, A) * A.n * l);
+    s.add<double>((size_t)A.m * l);  // centred copy of Y
   }
   return s.total;
 }
 
-void dense_aty(Ctx& c, const DenseA& A, const double* Y, int l, const double* cmean, double* Z, Arena& ar) {
+void dense_aty(Ctx& c, const DenseA& A, const double* Y, int l, const double* cmean, double* Z, Arena& ar,
+               const double* ymean) {
   RPCA_REQUIRE(l >= 1 && l <= kMaxL, RPCA_E_SHAPE, "l=%d out of range [1,%d]", l, kMaxL);
   double* sy = nullptr;
   if (cmean) {
@@ -328,7 +330,7 @@ void dense_aty(Ctx& c, const DenseA& A, const double* Y, int l, const double* cm
   }
   if (f32_tc_ok(A) && A.m > 0) {
     const size_t mark = ar.off;
-    dense_aty_f32(c, A, Y, l, cmean, sy, Z, ar);
+    dense_aty_f32(c, A, Y, l, cmean, sy, Z, ar, ymean);
     ar.off = mark;
     return;
   }
@@ -338,7 +340,7 @@ void dense_aty(Ctx& c, const DenseA& A, const double* Y, int l, const double* cm
     const int NT = (int)cdiv(l, 8);
     double* Yp = ar.get<double>(packy_elems(A.m, l));
     double* part = ar.get<double>(sp.P * (int64_t)ms * BN * NT * 8);
-    pack_y(c, Y, A.m, l, Yp);
+    pack_y(c, Y, A.m, l, Yp, ymean);
     switch (NT) {
       case 1: launch_aty_tma<1>(c, A, Yp, sp, ms, part); break;
       case 2: launch_aty_tma<2>(c, A, Yp, sp, ms, part); break;
@@ -355,6 +357,12 @@ void dense_aty(Ctx& c, const DenseA& A, const double* Y, int l, const double* cm
     RPCA_CHECK_LAUNCH();
     count_launch(c, 1, "aty_reduce");
     return;
+  }
+  if (ymean && A.m > 0) {  // generic kernel: centre a copy of Y first
+    double* Yc = ar.get<double>((size_t)A.m * l);
+    RPCA_CUDA(cudaMemcpyAsync(Yc, Y, sizeof(double) * A.m * l, cudaMemcpyDeviceToDevice, c.stream));
+    sub_rank1(c, Yc, A.m, l, nullptr, ymean);
+    Y = Yc;
   }
   const int64_t splits = A.m > 0 ? generic_splits(c, A) : 1;
   const int64_t rps = std::max<int64_t>(1, cdiv(A.m, splits));

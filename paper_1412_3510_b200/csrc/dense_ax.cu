@@ -61,7 +61,7 @@ struct AxSplit {
 template <int NT>
 __global__ void __launch_bounds__(kThreads, 1)
     ax_f64_tma_kernel(const __grid_constant__ CUtensorMap tmA, const double* __restrict__ Xp, int64_t m, int l,
-                      AxSplit sp, double* __restrict__ Y, double* __restrict__ part) {
+                      AxSplit sp, const double* __restrict__ cx, double* __restrict__ Y, double* __restrict__ part) {
   using Cfg = AxCfg<NT>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
@@ -169,15 +169,20 @@ __global__ void __launch_bounds__(kThreads, 1)
         double* y = dst + row * ld + col;
         if (!whole) {
           *reinterpret_cast<double2*>(y) = make_double2(acc[mt][nt][0], acc[mt][nt][1]);
-        } else if (col + 1 < l) {
-          if ((l & 1) == 0)
-            *reinterpret_cast<double2*>(y) = make_double2(acc[mt][nt][0], acc[mt][nt][1]);
-          else {
-            y[0] = acc[mt][nt][0];
-            y[1] = acc[mt][nt][1];
+        } else {
+          // the centring correction Y −= 1·cxᵀ folded into the store
+          const double v0 = acc[mt][nt][0] - (cx && col < l ? cx[col] : 0.0);
+          const double v1 = acc[mt][nt][1] - (cx && col + 1 < l ? cx[col + 1] : 0.0);
+          if (col + 1 < l) {
+            if ((l & 1) == 0)
+              *reinterpret_cast<double2*>(y) = make_double2(v0, v1);
+            else {
+              y[0] = v0;
+              y[1] = v1;
+            }
+          } else if (col < l) {
+            y[0] = v0;
           }
-        } else if (col < l) {
-          y[0] = acc[mt][nt][0];
         }
       }
     }
@@ -189,7 +194,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 // the first boundary inside it, the block sums that tile's partials over the
 // covering CTAs in ascending order and writes its rows of Y.
 __global__ void ax_fixup_kernel(AxSplit sp, int64_t m, int l, int LP, const double* __restrict__ part,
-                                double* __restrict__ Y) {
+                                const double* __restrict__ cx, double* __restrict__ Y) {
   __shared__ int64_t t_s, pa_s;
   __shared__ int nq_s;
   __shared__ const double* src[32];  // the covering CTAs' partial slots, ascending
@@ -236,7 +241,7 @@ __global__ void ax_fixup_kernel(AxSplit sp, int64_t m, int l, int LP, const doub
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
       const int idx = idx0 + e * blockDim.x;
-      if (idx < nrow * l) yt[idx] = s[e];
+      if (idx < nrow * l) yt[idx] = cx ? s[e] - cx[idx % l] : s[e];
     }
   }
   (void)pa_s;
@@ -301,7 +306,7 @@ PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
 }
 
 template <int NT>
-void launch_ax_tma(Ctx& c, const DenseA& A, const double* Xp, int l, double* Y, double* part) {
+void launch_ax_tma(Ctx& c, const DenseA& A, const double* Xp, int l, const double* cx, double* Y, double* part) {
   using Cfg = AxCfg<NT>;
   CUtensorMap tm;
   cuuint64_t dims[2] = {(cuuint64_t)A.n, (cuuint64_t)A.m};
@@ -325,11 +330,11 @@ void launch_ax_tma(Ctx& c, const DenseA& A, const double* Xp, int l, double* Y, 
   bool split = false;  // does any CTA boundary cut a tile?
   for (int64_t q = 1; q < sp.P && !split; ++q) split = sp.u0(q) % KB != 0;
   prof_pre(c);
-  ax_f64_tma_kernel<NT><<<(unsigned)sp.P, kThreads, Cfg::kSmem, c.stream>>>(tm, Xp, A.m, l, sp, Y, part);
+  ax_f64_tma_kernel<NT><<<(unsigned)sp.P, kThreads, Cfg::kSmem, c.stream>>>(tm, Xp, A.m, l, sp, cx, Y, part);
   RPCA_CHECK_LAUNCH();
   count_launch(c, 1, c.tag ? c.tag : "ax_f64_dmma");
   if (split && sp.P > 1) {
-    ax_fixup_kernel<<<(unsigned)(sp.P - 1), 256, 0, c.stream>>>(sp, A.m, l, NT * 8, part, Y);
+    ax_fixup_kernel<<<(unsigned)(sp.P - 1), 256, 0, c.stream>>>(sp, A.m, l, NT * 8, part, cx, Y);
     RPCA_CHECK_LAUNCH();
     count_launch(c, 1, "stream_k_fixup");
   }
@@ -357,7 +362,7 @@ void dense_ax(Ctx& c, const DenseA& A, const double* X, int l, double* Y, Arena&
     dense_ax_f32(c, A, X, l, cx, Y, ar);  // centring folded into the epilogue
     return;
   }
-  if (cx) {  // fp64 / generic kernels: the rank-1 correction as a separate thin pass
+  if (cx && !tma_ok(A)) {  // generic kernel: the rank-1 correction as a separate thin pass
     dense_ax(c, A, X, l, Y, ar, nullptr);
     sub_rank1(c, Y, A.m, l, nullptr, cx);
     return;
@@ -367,14 +372,14 @@ void dense_ax(Ctx& c, const DenseA& A, const double* X, int l, double* Y, Arena&
     double* part = ar.get<double>((size_t)kMaxSms * 2 * BM * ((l + 7) / 8 * 8));
     pack_x(c, X, A.n, l, Xp);
     switch ((l + 7) / 8) {
-      case 1: launch_ax_tma<1>(c, A, Xp, l, Y, part); break;
-      case 2: launch_ax_tma<2>(c, A, Xp, l, Y, part); break;
-      case 3: launch_ax_tma<3>(c, A, Xp, l, Y, part); break;
-      case 4: launch_ax_tma<4>(c, A, Xp, l, Y, part); break;
-      case 5: launch_ax_tma<5>(c, A, Xp, l, Y, part); break;
-      case 6: launch_ax_tma<6>(c, A, Xp, l, Y, part); break;
-      case 7: launch_ax_tma<7>(c, A, Xp, l, Y, part); break;
-      default: launch_ax_tma<8>(c, A, Xp, l, Y, part); break;
+      case 1: launch_ax_tma<1>(c, A, Xp, l, cx, Y, part); break;
+      case 2: launch_ax_tma<2>(c, A, Xp, l, cx, Y, part); break;
+      case 3: launch_ax_tma<3>(c, A, Xp, l, cx, Y, part); break;
+      case 4: launch_ax_tma<4>(c, A, Xp, l, cx, Y, part); break;
+      case 5: launch_ax_tma<5>(c, A, Xp, l, cx, Y, part); break;
+      case 6: launch_ax_tma<6>(c, A, Xp, l, cx, Y, part); break;
+      case 7: launch_ax_tma<7>(c, A, Xp, l, cx, Y, part); break;
+      default: launch_ax_tma<8>(c, A, Xp, l, cx, Y, part); break;
     }
     return;
   }

@@ -625,15 +625,15 @@ __global__ void aty_f32_reduce_kernel(const double* __restrict__ part, AtyPlan p
 // 64-row tiles go through shared memory so both the read of X (rows of l
 // doubles) and the writes of Xᵀ (runs of 64 k) are coalesced.
 __global__ void __launch_bounds__(256) split_transpose_kernel(const double* __restrict__ X, int64_t K, int l, int Npad,
-                                                              int64_t Kpad, float* __restrict__ hi,
-                                                              float* __restrict__ lo) {
+                                                              int64_t Kpad, const double* __restrict__ xmean,
+                                                              float* __restrict__ hi, float* __restrict__ lo) {
   __shared__ double tile[64][kMaxL + 1];
   for (int64_t k0 = (int64_t)blockIdx.x * 64; k0 < Kpad; k0 += (int64_t)gridDim.x * 64) {
     __syncthreads();
     for (int idx = threadIdx.x; idx < 64 * l; idx += 256) {
       const int r = idx / l, j = idx - r * l;
       const int64_t k = k0 + r;
-      tile[r][j] = k < K ? X[k * l + j] : 0.0;
+      tile[r][j] = k < K ? X[k * l + j] - (xmean ? xmean[j] : 0.0) : 0.0;
     }
     __syncthreads();
     for (int idx = threadIdx.x; idx < 64 * Npad; idx += 256) {
@@ -674,9 +674,10 @@ CUtensorMap tmap_f32(const void* base, int64_t inner, int64_t outer, int64_t ld_
 
 int npad_for(int l) { return l <= 16 ? 16 : (l <= 32 ? 32 : (l <= 48 ? 48 : 64)); }
 
-void split_transpose(Ctx& c, const double* X, int64_t K, int l, int Npad, int64_t Kpad, float* hi, float* lo) {
+void split_transpose(Ctx& c, const double* X, int64_t K, int l, int Npad, int64_t Kpad, float* hi, float* lo,
+                     const double* xmean = nullptr) {
   const unsigned grid = (unsigned)std::min<int64_t>(cdiv(Kpad, 64), (int64_t)c.num_sms * 8);
-  split_transpose_kernel<<<grid, 256, 0, c.stream>>>(X, K, l, Npad, Kpad, hi, lo);
+  split_transpose_kernel<<<grid, 256, 0, c.stream>>>(X, K, l, Npad, Kpad, xmean, hi, lo);
   RPCA_CHECK_LAUNCH();
   count_launch(c, 1, "split_tf32");
 }
@@ -798,12 +799,12 @@ size_t aty_f32_ws_bytes(Ctx& c, const DenseA& A, int l) {
 }
 
 void dense_aty_f32(Ctx& c, const DenseA& A, const double* Y, int l, const double* cmean, const double* sy,
-                   double* Z, Arena& ar) {
+                   double* Z, Arena& ar, const double* ymean) {
   const int Np = npad_for(l);
   const int64_t Kpad = cdiv(A.m, 64) * 64;
   float* hi = ar.get<float>((size_t)Np * Kpad);
   float* lo = ar.get<float>((size_t)Np * Kpad);
-  split_transpose(c, Y, A.m, l, Np, Kpad, hi, lo);
+  split_transpose(c, Y, A.m, l, Np, Kpad, hi, lo, ymean);
   switch (Np) {
     case 16: aty_f32_run<16>(c, A, hi, lo, Kpad, l, cmean, sy, Z, ar); break;
     case 32: aty_f32_run<32>(c, A, hi, lo, Kpad, l, cmean, sy, Z, ar); break;

@@ -329,13 +329,14 @@ struct Op {
   bool sharded;
 };
 
-// Y ← P·Y for an m-long block (rows of this shard), column sums over the global rows
-void center_block(Ctx& c, double* Y, int64_t rows, int l, int64_t m_total, bool sharded, Arena& ar) {
+// mu = the column means of an m-long block over the global rows (this shard's
+// sums, all-reduced, ÷ m_total).  P·Y = Y − 1·muᵀ is never formed: the mean
+// is subtracted on load by the block's consumer (the LU renormalisation, the
+// Aᵀ·Y operand preparation).
+void column_mean(Ctx& c, const double* Y, int64_t rows, int l, int64_t m_total, bool sharded, double* mu, Arena& ar) {
   const size_t mark = ar.off;
-  double* s = ar.get<double>(kMaxL);
-  weighted_colsum(c, nullptr, Y, rows, l, s, ar);
-  if (sharded) allreduce_sum(c, s, (size_t)l);
-  sub_rank1(c, Y, rows, l, nullptr, s, 1.0 / (double)m_total);
+  weighted_colsum(c, nullptr, Y, rows, l, mu, ar, 0, 1.0 / (double)m_total);
+  if (sharded) allreduce_sum(c, mu, (size_t)l);
   ar.off = mark;
 }
 
@@ -356,18 +357,19 @@ void apply_ax(Ctx& c, const MatV& A, const double* cmean, const double* X, int l
   ar.off = mark;
 }
 
-// Z = Aᵀ·Y [− cᵀ·(1ᵀY)] — this shard's rows only
-void apply_aty(Ctx& c, const MatV& A, const double* cmean, const double* Y, int l, double* Z, Arena& ar) {
+// Z = Aᵀ·(Y − 1·ymeanᵀ) [− cᵀ·(1ᵀY)] — this shard's rows only
+void apply_aty(Ctx& c, const MatV& A, const double* cmean, const double* Y, int l, double* Z, Arena& ar,
+               const double* ymean = nullptr) {
   const size_t mark = ar.off;
   if (A.csr) {
-    csr_spmm(c, A.at, Y, l, Z);
+    csr_spmm(c, A.at, Y, l, Z, ymean);
     if (cmean) {
       double* sy = ar.get<double>(kMaxL);
       weighted_colsum(c, nullptr, Y, A.m, l, sy, ar);
       sub_rank1(c, Z, A.n, l, cmean, sy);
     }
   } else {
-    dense_aty(c, A.d, Y, l, cmean, Z, ar);
+    dense_aty(c, A.d, Y, l, cmean, Z, ar, ymean);
   }
   ar.off = mark;
 }
@@ -381,29 +383,46 @@ void colmeans(Ctx& c, const MatV& A, int64_t m_total, double* cmean, Arena& ar, 
   if (sharded) allreduce_sum(c, cmean, A.n);
 }
 
-void fwd(Ctx& c, const Op& F, double* X, int l, double* Y, Arena& ar) {
+// F·X and F*·Y with the centring projector on the m-long side.  An m-long
+// OUTPUT is returned uncentred together with its pending column means (in
+// `mu`, the return value; NULL when nothing is pending) for the renormalisation
+// that consumes it; an m-long INPUT is centred on load (its means are taken
+// into `tmp`).
+const double* fwd(Ctx& c, const Op& F, const double* X, int l, double* Y, double* mu, double* tmp, Arena& ar) {
   if (F.trans) {  // F = A_cᵀ: Y = Aᵀ·(P·X)
-    if (F.centered) center_block(c, X, F.A.m, l, F.m_total, F.sharded, ar);
-    apply_aty(c, F.A, nullptr, X, l, Y, ar);
+    const double* xm = nullptr;
+    if (F.centered) {
+      column_mean(c, X, F.A.m, l, F.m_total, F.sharded, tmp, ar);
+      xm = tmp;
+    }
+    apply_aty(c, F.A, nullptr, X, l, Y, ar, xm);
     if (F.sharded) allreduce_sum(c, Y, (size_t)F.A.n * l);
-  } else {  // Y = P·(A·X)
-    apply_ax(c, F.A, nullptr, X, l, Y, ar);
-    if (F.centered) center_block(c, Y, F.A.m, l, F.m_total, F.sharded, ar);
+    return nullptr;
   }
+  apply_ax(c, F.A, nullptr, X, l, Y, ar);  // Y = P·(A·X), P pending
+  if (!F.centered) return nullptr;
+  column_mean(c, Y, F.A.m, l, F.m_total, F.sharded, mu, ar);
+  return mu;
 }
-void adj(Ctx& c, const Op& F, double* Y, int l, double* Z, Arena& ar) {
-  if (F.trans) {  // Z = P·(A·Y)
+const double* adj(Ctx& c, const Op& F, const double* Y, int l, double* Z, double* mu, double* tmp, Arena& ar) {
+  if (F.trans) {  // Z = P·(A·Y), P pending
     apply_ax(c, F.A, nullptr, Y, l, Z, ar);
-    if (F.centered) center_block(c, Z, F.A.m, l, F.m_total, F.sharded, ar);
-  } else {  // Z = Aᵀ·(P·Y)
-    if (F.centered) center_block(c, Y, F.A.m, l, F.m_total, F.sharded, ar);
-    apply_aty(c, F.A, nullptr, Y, l, Z, ar);
-    if (F.sharded) allreduce_sum(c, Z, (size_t)F.A.n * l);
+    if (!F.centered) return nullptr;
+    column_mean(c, Z, F.A.m, l, F.m_total, F.sharded, mu, ar);
+    return mu;
   }
+  const double* ym = nullptr;  // Z = Aᵀ·(P·Y)
+  if (F.centered) {
+    column_mean(c, Y, F.A.m, l, F.m_total, F.sharded, tmp, ar);
+    ym = tmp;
+  }
+  apply_aty(c, F.A, nullptr, Y, l, Z, ar, ym);
+  if (F.sharded) allreduce_sum(c, Z, (size_t)F.A.n * l);
+  return nullptr;
 }
 
 size_t op_ws(Ctx& c, const MatV& A, int l) {
-  const size_t small = (size_t)(cdiv(std::max(A.m, A.n), 8192) + 4) * kMaxL * 8 * 2 + 65536;
+  const size_t small = (size_t)(cdiv(std::max(A.m, A.n), 2048) + 4) * kMaxL * 8 * 2 + 65536;
   if (A.csr) return small;
   return std::max(ax_ws_bytes(A.d, l) + 4096 * 4, aty_ws_bytes(c, A.d, l)) + small;
 }
@@ -417,17 +436,18 @@ struct Blk {
   int64_t row0;
 };
 
-void renorm_lu(Ctx& c, const Blk& Y, int l, Arena& ar) {
+// (mu: the block's pending column means, or NULL)
+void renorm_lu(Ctx& c, const Blk& Y, int l, Arena& ar, const double* mu = nullptr) {
   const size_t mark = ar.off;
-  if (Y.sharded) lu_renorm_sharded(c, Y.p, Y.rows, Y.row0, l, nullptr, ar);
-  else lu_renorm(c, Y.p, Y.rows, l, nullptr, nullptr, ar);
+  if (Y.sharded) lu_renorm_sharded(c, Y.p, Y.rows, Y.row0, l, nullptr, ar, mu);
+  else lu_renorm(c, Y.p, Y.rows, l, nullptr, nullptr, ar, mu);
   ar.off = mark;
 }
 // the last renormalisation and the QR of Bᵀ: LU-Cholesky-QR
-void renorm_qr(Ctx& c, const Blk& Y, int l, double* R, Arena& ar) {
+void renorm_qr(Ctx& c, const Blk& Y, int l, double* R, Arena& ar, const double* mu = nullptr) {
   const size_t mark = ar.off;
-  if (Y.sharded) orthonormalize_sharded(c, Y.p, Y.rows, Y.row0, l, R, ar);
-  else orthonormalize(c, Y.p, Y.rows, l, R, ar);
+  if (Y.sharded) orthonormalize_sharded(c, Y.p, Y.rows, Y.row0, l, R, ar, mu);
+  else orthonormalize(c, Y.p, Y.rows, l, R, ar, mu);
   ar.off = mark;
 }
 
@@ -516,6 +536,7 @@ void pca(Ctx& c, const rpca_mat* Am, int64_t k, int raw, int its, int64_t l, uin
   sz.add<double>(nin * l);   // Zb
   sz.add<double>(nout * l);  // Yb
   sz.add<double>(4 * l * l + 4 * l);
+  sz.add<double>(2 * kMaxL);  // column means
   sz.add<double>(std::max(nin, nout) * k);  // V-side temp
   sz.add<double>(k);                        // signs
   if (out_host) {
@@ -527,7 +548,7 @@ void pca(Ctx& c, const rpca_mat* Am, int64_t k, int raw, int its, int64_t l, uin
   size_t scratch = op_ws(c, probe, L);
   scratch = std::max(scratch, lu_ws_bytes(std::max(nin, nout), L));
   scratch = std::max(scratch, orth_ws_bytes(c, std::max(nin, nout), L));
-  scratch = std::max(scratch, (size_t)(cdiv(std::max(ml, n), 8192) + 2) * (n + 2 * k) * 8 + 65536);
+  scratch = std::max(scratch, (size_t)(cdiv(std::max(ml, n), 2048) + 2) * (n + 2 * k) * 8 + 65536);
   scratch = std::max(scratch, thin_gemm_ws_bytes(std::max(nin, nout), L, K) + 65536);
   ensure_transpose(c, Am);
   Arena ar = c.arena(fixed + scratch + 65536);
@@ -553,25 +574,26 @@ void pca(Ctx& c, const rpca_mat* Am, int64_t k, int raw, int its, int64_t l, uin
       Vd = ar.get<char>((size_t)n * ldv * osz);
       Sd = ar.get<char>((size_t)k * osz);
     }
+    double* mub = ar.get<double>(2 * kMaxL);  // pending column means / input means
     // the m-long block is the sharded one
     const Blk Y{Yb, nout, sh && !trans, r0}, Z{Zb, nin, sh && trans, r0};
     Op F{dA, !raw, m, trans, sh};
     // Ω (nin×l; for the sketched Aᵀ, this rank's rows of the m×l Ω); the fp32
     // path consumes fl32(Ω) exactly as the oracle does
     omega(c, seed, 0u, nin, l, dist, odt == RPCA_F32, Zb, trans ? r0 : 0);
-    fwd(c, F, Zb, L, Yb, ar);
-    if (its == 0) renorm_qr(c, Y, L, nullptr, ar);
-    else renorm_lu(c, Y, L, ar);
+    const double* mu = fwd(c, F, Zb, L, Yb, mub, mub + kMaxL, ar);  // mu: Y's pending centring
+    if (its == 0) renorm_qr(c, Y, L, nullptr, ar, mu);
+    else renorm_lu(c, Y, L, ar, mu);
     for (int it = 1; it <= its; ++it) {
-      adj(c, F, Yb, L, Zb, ar);
-      renorm_lu(c, Z, L, ar);
-      fwd(c, F, Zb, L, Yb, ar);
-      if (it < its) renorm_lu(c, Y, L, ar);
-      else renorm_qr(c, Y, L, nullptr, ar);
+      mu = adj(c, F, Yb, L, Zb, mub, mub + kMaxL, ar);
+      renorm_lu(c, Z, L, ar, mu);
+      mu = fwd(c, F, Zb, L, Yb, mub, mub + kMaxL, ar);
+      if (it < its) renorm_lu(c, Y, L, ar, mu);
+      else renorm_qr(c, Y, L, nullptr, ar, mu);
     }
     // Bᵀ = F*·Q (eq. i2), Bᵀ = Q_B·R, R = Vr·Σ·Wᵀ ⇒ B = W Σ (Q_B Vr)ᵀ (eq. i3)
-    adj(c, F, Yb, L, Zb, ar);
-    renorm_qr(c, Z, L, R, ar);
+    mu = adj(c, F, Yb, L, Zb, mub, mub + kMaxL, ar);
+    renorm_qr(c, Z, L, R, ar, mu);
     jacobi_svd_small(c, R, L, sig, W, Vr);
     {
       const size_t mark = ar.off;
@@ -639,7 +661,7 @@ void eigens(Ctx& c, const rpca_mat* Am, int64_t k, int its, int64_t l, uint64_t 
   size_t scratch = op_ws(c, probe, L);
   scratch = std::max(scratch, lu_ws_bytes(ml, L));
   scratch = std::max(scratch, orth_ws_bytes(c, ml, L));
-  scratch = std::max(scratch, (size_t)(cdiv(n, 8192) + 2) * l * l * 8 + 65536 + (size_t)P * 3 * l * 8);
+  scratch = std::max(scratch, (size_t)(cdiv(n, 2048) + 2) * l * l * 8 + 65536 + (size_t)P * 3 * l * 8);
   scratch = std::max(scratch, thin_gemm_ws_bytes(ml, L, K) + gram_ws_bytes(c, ml, L) + 65536);
   Arena ar = c.arena(sz.total + scratch + 65536);
   if (!c.status_host) RPCA_CUDA(cudaMallocHost(&c.status_host, 64));
@@ -760,7 +782,7 @@ void diffsnorm(Ctx& c, const rpca_mat* Am, int raw, const double* U, int64_t ldu
   Sizer sz;
   sz.add<char>(host_copy_bytes(Am));
   sz.add<double>(2 * n + ml + n + k + 64);
-  size_t scratch = op_ws(c, probe, 1) + (size_t)(cdiv(std::max(ml, n), 8192) + 2) * (n + 64) * 8;
+  size_t scratch = op_ws(c, probe, 1) + (size_t)(cdiv(std::max(ml, n), 2048) + 2) * (n + 64) * 8;
   ensure_transpose(c, Am);
   Arena ar = c.arena(sz.total + scratch + 65536);
   if (!c.status_host) RPCA_CUDA(cudaMallocHost(&c.status_host, 64));

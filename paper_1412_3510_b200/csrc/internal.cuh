@@ -147,10 +147,10 @@ void omega(Ctx& c, uint64_t seed, uint32_t sid, int64_t rows, int64_t cols, int 
 int64_t packx_elems(int64_t n, int l);   // doubles in the packed X of an n×l block
 int64_t packy_elems(int64_t m, int l);   // doubles in the packed Y of an m×l block
 void pack_x(Ctx& c, const double* X, int64_t n, int l, double* Xp);
-void pack_y(Ctx& c, const double* Y, int64_t m, int l, double* Yp);
+void pack_y(Ctx& c, const double* Y, int64_t m, int l, double* Yp, const double* ymean = nullptr);
 // v[j] = Σ_k a[k]·X[k][j] (a may be NULL ⇒ all-ones), fixed-order reduction
 void weighted_colsum(Ctx& c, const double* a, const double* X, int64_t rows, int l, double* v, Arena& ar,
-                     int64_t ldx = 0);
+                     int64_t ldx = 0, double scale = 1.0);
 // Y −= α·u·vᵀ (u = NULL ⇒ ones)
 void sub_rank1(Ctx& c, double* Y, int64_t rows, int l, const double* u /*rows or NULL=ones*/, const double* v,
                double alpha = 1.0);
@@ -189,12 +189,13 @@ size_t ax_ws_bytes(const DenseA& A, int l);
 // Y = A·X [− 1·cxᵀ]  (cx = c·X, the centring correction of PAPER.md:430; may be NULL)
 void dense_ax(Ctx& c, const DenseA& A, const double* X, int l, double* Y, Arena& ar, const double* cx = nullptr);
 size_t aty_ws_bytes(Ctx& c, const DenseA& A, int l);
-// Z (n×l) = Aᵀ·Y [− cmean ⊗ colsum(Y)] (cmean may be NULL)
-void dense_aty(Ctx& c, const DenseA& A, const double* Y, int l, const double* cmean, double* Z, Arena& ar);
+// Z (n×l) = Aᵀ·(Y − 1·ymeanᵀ) [− cmean ⊗ colsum(Y)] (cmean, ymean may be NULL)
+void dense_aty(Ctx& c, const DenseA& A, const double* Y, int l, const double* cmean, double* Z, Arena& ar,
+               const double* ymean = nullptr);
 
 // csr.cu — sparse A (row-major CSR, int64 row pointers, int32 sorted column indices)
-// Y (rows×l) = A·X   (X has as many rows as A has columns)
-void csr_spmm(Ctx& c, const CsrA& A, const double* X, int l, double* Y);
+// Y (rows×l) = A·(X − 1·xmeanᵀ)   (X has as many rows as A has columns; xmean may be NULL)
+void csr_spmm(Ctx& c, const CsrA& A, const double* X, int l, double* Y, const double* xmean = nullptr);
 size_t csr_transpose_ws_bytes(const CsrA& A);
 // device memory (caller frees with cudaFree) holding A's heavy-row plan; sets
 // the plan fields of A (synchronises the stream; nullptr if A has no heavy row)
@@ -212,15 +213,18 @@ void dense_ax_f32(Ctx& c, const DenseA& A, const double* X, int l, const double*
 size_t aty_f32_ws_bytes(Ctx& c, const DenseA& A, int l);
 // Z = Aᵀ·Y [− cmean·syᵀ]
 void dense_aty_f32(Ctx& c, const DenseA& A, const double* Y, int l, const double* cmean, const double* sy,
-                   double* Z, Arena& ar);
+                   double* Z, Arena& ar, const double* ymean = nullptr);
 void aty_reduce_partials(Ctx& c, const double* part, int64_t U, int64_t P, int64_t cpc, int maxslots, int64_t n,
                          int l, int LP, const double* cmean, const double* sy, double* Z);
 
 // tslu.cu
 size_t lu_ws_bytes(int64_t m, int l);
-void lu_renorm(Ctx& c, double* Y, int64_t m, int l, double* U_out, int64_t* piv_out, Arena& ar);
+// LU renormalisation of (Y − 1·muᵀ) when mu ≠ NULL (a pending centring, reading Q8)
+void lu_renorm(Ctx& c, double* Y, int64_t m, int l, double* U_out, int64_t* piv_out, Arena& ar,
+               const double* mu = nullptr);
 // row shard [row0, row0+m) of a matrix distributed over the context's communicator
-void lu_renorm_sharded(Ctx& c, double* Y, int64_t m, int64_t row0, int l, double* U_out, Arena& ar);
+void lu_renorm_sharded(Ctx& c, double* Y, int64_t m, int64_t row0, int l, double* U_out, Arena& ar,
+                       const double* mu = nullptr);
 
 // tsqr.cu
 size_t qr_ws_bytes(int64_t m, int l);
@@ -229,8 +233,9 @@ void qr(Ctx& c, double* Y, int64_t m, int l, double* R_out, Arena& ar);
 // cholqr.cu — LU-Cholesky-QR: Y ← Q (orthonormal, span Y), R (l×l upper, diag ≥ 0, Y = Q·R)
 size_t orth_ws_bytes(int64_t m, int l);
 size_t orth_ws_bytes(Ctx& c, int64_t m, int l);
-void orthonormalize(Ctx& c, double* Y, int64_t m, int l, double* R_out, Arena& ar);
-void orthonormalize_sharded(Ctx& c, double* Y, int64_t m, int64_t row0, int l, double* R_out, Arena& ar);
+void orthonormalize(Ctx& c, double* Y, int64_t m, int l, double* R_out, Arena& ar, const double* mu = nullptr);
+void orthonormalize_sharded(Ctx& c, double* Y, int64_t m, int64_t row0, int l, double* R_out, Arena& ar,
+                            const double* mu = nullptr);
 
 // small.cu — one-CTA l×l kernels
 // R (l×l) → Jacobi: R·W = Vr·diag(sigma); sigma sorted, Vr completed.

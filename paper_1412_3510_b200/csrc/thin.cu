@@ -31,7 +31,7 @@ __global__ void pack_x_kernel(const double* __restrict__ X, int64_t n, int l, in
 
 // Packed Y for dense_aty: Yp[g][s][nt][lane] = Y[8g + 2*(lane&3) + s][nt*8 + (lane>>2)]
 __global__ void pack_y_kernel(const double* __restrict__ Y, int64_t m, int l, int NT, int64_t total,
-                              double* __restrict__ Yp) {
+                              const double* __restrict__ ymean, double* __restrict__ Yp) {
   for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
        idx += (int64_t)gridDim.x * blockDim.x) {
     const int lane = (int)(idx & 31);
@@ -42,28 +42,58 @@ __global__ void pack_y_kernel(const double* __restrict__ Y, int64_t m, int l, in
     const int64_t g = t >> 1;
     const int64_t i = 8 * g + 2 * (lane & 3) + s;
     const int j = nt * 8 + (lane >> 2);
-    Yp[idx] = (i < m && j < l) ? Y[i * l + j] : 0.0;
+    Yp[idx] = (i < m && j < l) ? Y[i * l + j] - (ymean ? ymean[j] : 0.0) : 0.0;
   }
 }
 
-// partial[b][j] = Σ_{i in chunk b} a[i]·X[i][j]  (a == NULL ⇒ 1)
-__global__ void wcolsum_partial(const double* __restrict__ a, const double* __restrict__ X, int64_t rows, int l,
-                                int64_t ldx, double* __restrict__ part) {
+// partial[b][j] = Σ_{i in chunk b} a[i]·X[i][j]  (a == NULL ⇒ 1); chunks of
+// kColChunk rows, threads (phase, column) read whole rows (coalesced), four
+// independent accumulators per thread, fixed order
+constexpr int kColChunk = 2048;
+__global__ void __launch_bounds__(256) wcolsum_partial(const double* __restrict__ a, const double* __restrict__ X,
+                                                      int64_t rows, int l, int64_t ldx, double* __restrict__ part) {
   __shared__ double red[256];
-  const int64_t r0 = (int64_t)blockIdx.x * kChunk;
-  const int64_t r1 = min(rows, r0 + kChunk);
+  const int64_t r0 = (int64_t)blockIdx.x * kColChunk;
+  const int64_t r1 = min(rows, r0 + kColChunk);
   const int phases = 256 / l;  // l ≤ 64 ⇒ ≥ 4 phases
   const int ph = threadIdx.x / l, j = threadIdx.x % l;
-  double s = 0.0;
+  double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
   if (ph < phases) {
-    for (int64_t i = r0 + ph; i < r1; i += phases) s += (a ? a[i] : 1.0) * X[i * ldx + j];
+    int64_t i = r0 + ph;
+    for (; i + 3 * phases < r1; i += 4 * phases) {
+      s0 += (a ? a[i] : 1.0) * X[i * ldx + j];
+      s1 += (a ? a[i + phases] : 1.0) * X[(i + phases) * ldx + j];
+      s2 += (a ? a[i + 2 * phases] : 1.0) * X[(i + 2 * phases) * ldx + j];
+      s3 += (a ? a[i + 3 * phases] : 1.0) * X[(i + 3 * phases) * ldx + j];
+    }
+    for (; i < r1; i += phases) s0 += (a ? a[i] : 1.0) * X[i * ldx + j];
   }
-  red[threadIdx.x] = s;
+  red[threadIdx.x] = (s0 + s1) + (s2 + s3);
   __syncthreads();
   if (threadIdx.x < l) {
     double t = 0.0;
     for (int p = 0; p < phases; ++p) t += red[p * l + threadIdx.x];
     part[(int64_t)blockIdx.x * l + threadIdx.x] = t;
+  }
+}
+
+// v[j] = scale·Σ_b part[b][j]: warp w sums the partials b ≡ w (mod 8) in
+// ascending order, then the eight warp sums are added in order
+__global__ void sum_partials_8w(const double* __restrict__ part, int64_t nparts, int l, double scale,
+                                double* __restrict__ v) {
+  __shared__ double red[8][kMaxL];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int j = lane; j < l; j += 32) {
+    double s = 0.0;
+    for (int64_t b = warp; b < nparts; b += 8) s += part[b * l + j];
+    red[warp][j] = s;
+  }
+  __syncthreads();
+  if (threadIdx.x < l) {
+    double t = 0.0;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) t += red[w][threadIdx.x];
+    v[threadIdx.x] = t * scale;
   }
 }
 
@@ -292,22 +322,22 @@ void pack_x(Ctx& c, const double* X, int64_t n, int l, double* Xp) {
   count_launch(c, 1, "pack_x");
 }
 
-void pack_y(Ctx& c, const double* Y, int64_t m, int l, double* Yp) {
+void pack_y(Ctx& c, const double* Y, int64_t m, int l, double* Yp, const double* ymean) {
   const int NT = (int)cdiv(l, 8);
   const int64_t total = packy_elems(m, l);
-  pack_y_kernel<<<grid_for(c, total), 256, 0, c.stream>>>(Y, m, l, NT, total, Yp);
+  pack_y_kernel<<<grid_for(c, total), 256, 0, c.stream>>>(Y, m, l, NT, total, ymean, Yp);
   RPCA_CHECK_LAUNCH();
   count_launch(c, 1, "pack_y");
 }
 
 void weighted_colsum(Ctx& c, const double* a, const double* X, int64_t rows, int l, double* v, Arena& ar,
-                     int64_t ldx) {
+                     int64_t ldx, double scale) {
   if (ldx <= 0) ldx = l;
-  const int64_t nparts = std::max<int64_t>(1, cdiv(rows, kChunk));
+  const int64_t nparts = std::max<int64_t>(1, cdiv(rows, kColChunk));
   double* part = ar.get<double>(nparts * l);
   wcolsum_partial<<<(unsigned)nparts, 256, 0, c.stream>>>(a, X, rows, l, ldx, part);
   RPCA_CHECK_LAUNCH();
-  sum_partials<<<1, 64, 0, c.stream>>>(part, nparts, l, 1.0, v);
+  sum_partials_8w<<<1, 256, 0, c.stream>>>(part, nparts, l, scale, v);
   RPCA_CHECK_LAUNCH();
   count_launch(c, 2);
 }

@@ -99,7 +99,8 @@ __global__ void __launch_bounds__(kThreads, SelCfg<LP, RR>::kMinBlocks)
     lu_select_kernel(const double* __restrict__ Y, int64_t m, int l, int leaf, const int64_t* __restrict__ cand_in,
                      int64_t n_in, int G, int64_t* __restrict__ cand_out, int final_, double* __restrict__ U,
                      double* __restrict__ Lp, int64_t* __restrict__ piv_out, double* __restrict__ M,
-                     const double* __restrict__ rows_in, double* __restrict__ rows_out) {
+                     const double* __restrict__ rows_in, double* __restrict__ rows_out,
+                     const double* __restrict__ mu) {
   using Cfg = SelCfg<LP, RR>;
   constexpr int R = Cfg::R, CAP = Cfg::kCap;
   __shared__ int64_t ids[CAP];
@@ -180,8 +181,11 @@ __global__ void __launch_bounds__(kThreads, SelCfg<LP, RR>::kMinBlocks)
     const double* src = nullptr;
     if (act[q])
       src = leaf == 2 ? rows_in + ((int64_t)blockIdx.x * G * l + slot_of[r]) * l : Y + ids[r] * l;
+    // a pending centring of Y (the projector P of DESIGN.md reading Q8) is
+    // applied on load; direct rows (leaf 2) arrive centred
+    const bool sub = mu != nullptr && leaf != 2;
 #pragma unroll
-    for (int t = 0; t < LP; ++t) w[q][t] = (act[q] && t < l) ? src[t] : 0.0;
+    for (int t = 0; t < LP; ++t) w[q][t] = (act[q] && t < l) ? src[t] - (sub ? mu[t] : 0.0) : 0.0;
   }
 
   // Blocked GEPP, panels of 8 columns.  Registers hold each row SHIFTED so
@@ -343,12 +347,12 @@ __global__ void pivot_rows_kernel(double* __restrict__ Y, int64_t m, int64_t row
 // rows_out[j] = Y[cand[j]] (l-vectors), gid[j] = row0 + cand[j] (−1 kept) — the
 // local tournament winners packaged for the all-gather of a sharded LU
 __global__ void pack_candidates_kernel(const double* __restrict__ Y, int l, int64_t row0,
-                                       const int64_t* __restrict__ cand, double* __restrict__ rows_out,
-                                       int64_t* __restrict__ gid) {
+                                       const int64_t* __restrict__ cand, const double* __restrict__ mu,
+                                       double* __restrict__ rows_out, int64_t* __restrict__ gid) {
   for (int idx = threadIdx.x; idx < l * l; idx += blockDim.x) {
     const int j = idx / l, t = idx - j * l;
     const int64_t r = cand[j];
-    rows_out[idx] = r >= 0 ? Y[r * l + t] : 0.0;
+    rows_out[idx] = r >= 0 ? Y[r * l + t] - (mu ? mu[t] : 0.0) : 0.0;
     if (t == 0) gid[j] = r >= 0 ? row0 + r : -1;
   }
 }
@@ -362,31 +366,31 @@ int group_for(int l) { return std::max(2, tree_cap(l) / l); }
 template <int LP, int R>
 void select_lpr(Ctx& c, unsigned grid, const double* Y, int64_t m, int l, int leaf, const int64_t* cin, int64_t n_in,
                 int G, int64_t* cout, int final_, double* U, double* Lp, int64_t* piv, double* M,
-                const double* rows_in, double* rows_out) {
+                const double* rows_in, double* rows_out, const double* mu) {
   const size_t smem = final_ ? (size_t)(LP * LP + l * l + (size_t)SelCfg<LP, R>::kCap * l) * 8 : 0;
   if (smem) ensure_smem((const void*)lu_select_kernel<LP, R>, (int)smem);
   lu_select_kernel<LP, R><<<grid, kThreads, smem, c.stream>>>(Y, m, l, leaf, cin, n_in, G, cout, final_, U, Lp, piv,
-                                                              M, rows_in, rows_out);
+                                                              M, rows_in, rows_out, mu);
 }
 
 template <int LP>
 void select_lp(Ctx& c, unsigned grid, const double* Y, int64_t m, int l, int leaf, const int64_t* cin, int64_t n_in,
                int G, int64_t* cout, int final_, double* U, double* Lp, int64_t* piv, double* M,
-               const double* rows_in, double* rows_out) {
+               const double* rows_in, double* rows_out, const double* mu) {
   if (leaf == 1)
     select_lpr<LP, leaf_rows_per_thread(LP)>(c, grid, Y, m, l, leaf, cin, n_in, G, cout, final_, U, Lp, piv, M,
-                                             rows_in, rows_out);
+                                             rows_in, rows_out, mu);
   else
     select_lpr<LP, tree_rows_per_thread(LP)>(c, grid, Y, m, l, leaf, cin, n_in, G, cout, final_, U, Lp, piv, M,
-                                             rows_in, rows_out);
+                                             rows_in, rows_out, mu);
 }
 
 void select(Ctx& c, unsigned grid, const double* Y, int64_t m, int l, int leaf, const int64_t* cin, int64_t n_in,
             int G, int64_t* cout, int final_, double* U, double* Lp, int64_t* piv, double* M,
-            const double* rows_in = nullptr, double* rows_out = nullptr) {
-#define RPCA_SEL(LPV)                                                                                 \
-  case LPV:                                                                                           \
-    select_lp<LPV>(c, grid, Y, m, l, leaf, cin, n_in, G, cout, final_, U, Lp, piv, M, rows_in, rows_out); \
+            const double* rows_in = nullptr, double* rows_out = nullptr, const double* mu = nullptr) {
+#define RPCA_SEL(LPV)                                                                                      \
+  case LPV:                                                                                                \
+    select_lp<LPV>(c, grid, Y, m, l, leaf, cin, n_in, G, cout, final_, U, Lp, piv, M, rows_in, rows_out, mu); \
     break;
   switch (lp_of(l)) {
     RPCA_SEL(8)
@@ -408,7 +412,7 @@ void select(Ctx& c, unsigned grid, const double* Y, int64_t m, int l, int leaf, 
 // (l entries, local row indices, −1 padded).  If `finalize`, the last level
 // also writes U, Lp, piv and M.
 int64_t* tournament(Ctx& c, const double* Y, int64_t m, int l, bool finalize, double* U, double* Lp, int64_t* piv,
-                    double* M, Arena& ar) {
+                    double* M, Arena& ar, const double* mu) {
   const int G = group_for(l);
   const int64_t nblk = std::max<int64_t>(1, cdiv(m, leaf_cap(l)));
   int64_t* ca = ar.get<int64_t>(nblk * l);
@@ -417,11 +421,12 @@ int64_t* tournament(Ctx& c, const double* Y, int64_t m, int l, bool finalize, do
     RPCA_CUDA(cudaMemsetAsync(ca, 0xFF, sizeof(int64_t) * l, c.stream));  // no local rows: all −1
     return ca;
   }
-  select(c, (unsigned)nblk, Y, m, l, 1, nullptr, 0, G, ca, finalize && nblk == 1, U, Lp, piv, M);
+  select(c, (unsigned)nblk, Y, m, l, 1, nullptr, 0, G, ca, finalize && nblk == 1, U, Lp, piv, M, nullptr, nullptr,
+         mu);
   int64_t n = nblk;
   while (n > 1) {
     const int64_t ng = cdiv(n, G);
-    select(c, (unsigned)ng, Y, m, l, 0, ca, n, G, cb, finalize && ng == 1, U, Lp, piv, M);
+    select(c, (unsigned)ng, Y, m, l, 0, ca, n, G, cb, finalize && ng == 1, U, Lp, piv, M, nullptr, nullptr, mu);
     std::swap(ca, cb);
     n = ng;
   }
@@ -431,11 +436,30 @@ int64_t* tournament(Ctx& c, const double* Y, int64_t m, int l, bool finalize, do
 // L = Y·M on the fp64 tensor-core pass kernel (in place: every output row is
 // written only after all of its own K-chunks were read), then the pivot rows
 // this shard holds get their exact unit-lower rows
+// cx_j = Σ_t mu_t·M_tj: (Y − 1·mu)·M = Y·M − 1·cx
+__global__ void mu_times_m_kernel(const double* __restrict__ mu, const double* __restrict__ M, int l,
+                                  double* __restrict__ cx) {
+  const int j = threadIdx.x;
+  if (j >= l) return;
+  double s = 0.0;
+  for (int t = 0; t < l; ++t) s += mu[t] * M[t * l + j];
+  cx[j] = s;
+}
+
 void apply_l(Ctx& c, double* Y, int64_t m, int64_t row0, int l, const double* M, const double* Lp,
-             const int64_t* piv, Arena& ar) {
+             const int64_t* piv, Arena& ar, const double* mu) {
   if (m > 0) {
+    const size_t mark = ar.off;
+    double* cx = nullptr;
+    if (mu) {  // L = (Y − 1·mu)·M: the pending centring enters the epilogue
+      cx = ar.get<double>(kMaxL);
+      mu_times_m_kernel<<<1, 64, 0, c.stream>>>(mu, M, l, cx);
+      RPCA_CHECK_LAUNCH();
+      count_launch(c, 1, "misc");
+    }
     TagScope ts(c, "lu_apply");
-    dense_ax(c, DenseA{Y, RPCA_F64, m, l, l}, M, l, Y, ar);
+    dense_ax(c, DenseA{Y, RPCA_F64, m, l, l}, M, l, Y, ar, cx);
+    ar.off = mark;
   }
   pivot_rows_kernel<<<1, 256, 0, c.stream>>>(Y, m, row0, l, Lp, piv);
   RPCA_CHECK_LAUNCH();
@@ -453,19 +477,20 @@ size_t lu_ws_bytes(int64_t m, int l) {
   s.add<double>(4 * (size_t)l * l);
   s.add<int64_t>(l);
   s.add<double>((size_t)2 * kMaxL * (size_t)(kMaxL + 1) * 64 + 2 * kMaxL * kMaxL);  // sharded: gathered rows + ids
+  s.add<double>(kMaxL);                                                                 // mu·M
   return s.total;
 }
 
-void lu_renorm(Ctx& c, double* Y, int64_t m, int l, double* U_out, int64_t* piv_out, Arena& ar) {
+void lu_renorm(Ctx& c, double* Y, int64_t m, int l, double* U_out, int64_t* piv_out, Arena& ar, const double* mu) {
   RPCA_REQUIRE(l >= 1 && l <= kMaxL && m >= l, RPCA_E_SHAPE, "lu_renorm: need 1 ≤ l ≤ %d and m ≥ l", kMaxL);
   double* U = U_out ? U_out : ar.get<double>((size_t)l * l);
   double* Lp = ar.get<double>((size_t)l * l);
   int64_t* piv = ar.get<int64_t>(l);
   double* M = ar.get<double>((size_t)l * l);
   const size_t mark = ar.off;
-  tournament(c, Y, m, l, true, U, Lp, piv, M, ar);
+  tournament(c, Y, m, l, true, U, Lp, piv, M, ar, mu);
   ar.off = mark;
-  apply_l(c, Y, m, 0, l, M, Lp, piv, ar);
+  apply_l(c, Y, m, 0, l, M, Lp, piv, ar, mu);
   if (piv_out) RPCA_CUDA(cudaMemcpyAsync(piv_out, piv, sizeof(int64_t) * l, cudaMemcpyDeviceToDevice, c.stream));
 }
 
@@ -473,7 +498,8 @@ void lu_renorm(Ctx& c, double* Y, int64_t m, int l, double* U_out, int64_t* piv_
 // [row0, row0+m); the winners (l rows + their global ids) are all-gathered and
 // every rank runs the final GEPP on the same P·l rows — identical U, pivots and
 // M everywhere — then applies L = Y·M to its own rows.
-void lu_renorm_sharded(Ctx& c, double* Y, int64_t m, int64_t row0, int l, double* U_out, Arena& ar) {
+void lu_renorm_sharded(Ctx& c, double* Y, int64_t m, int64_t row0, int l, double* U_out, Arena& ar,
+                       const double* mu) {
   RPCA_REQUIRE(l >= 1 && l <= kMaxL && m >= 0, RPCA_E_SHAPE, "lu_renorm: need 1 ≤ l ≤ %d", kMaxL);
   const int P = comm_size(c);
   RPCA_REQUIRE(P <= 64, RPCA_E_ARG, "at most 64 ranks");
@@ -488,8 +514,8 @@ void lu_renorm_sharded(Ctx& c, double* Y, int64_t m, int64_t row0, int l, double
   int64_t* ids_a = ar.get<int64_t>((size_t)l * P);
   int64_t* ids_b = ar.get<int64_t>((size_t)l * P);
   const size_t mark = ar.off;
-  const int64_t* cand = tournament(c, Y, m, l, false, nullptr, nullptr, nullptr, nullptr, ar);
-  pack_candidates_kernel<<<1, 256, 0, c.stream>>>(Y, l, row0, cand, rows_send, ids_send);
+  const int64_t* cand = tournament(c, Y, m, l, false, nullptr, nullptr, nullptr, nullptr, ar, mu);
+  pack_candidates_kernel<<<1, 256, 0, c.stream>>>(Y, l, row0, cand, mu, rows_send, ids_send);
   RPCA_CHECK_LAUNCH();
   count_launch(c, 1, "lu_pack");
   ar.off = mark;
@@ -508,7 +534,7 @@ void lu_renorm_sharded(Ctx& c, double* Y, int64_t m, int64_t row0, int l, double
     std::swap(ids_a, ids_b);
     n = ng;
   }
-  apply_l(c, Y, m, row0, l, M, Lp, piv, ar);
+  apply_l(c, Y, m, row0, l, M, Lp, piv, ar, mu);
 }
 
 }  // namespace rpca
