@@ -31,39 +31,69 @@ __global__ void __launch_bounds__(kThreads) chol_kernel(const double* __restrict
   double* G = sm;              // l×l
   double* R = sm + l * l;      // l×l
   double* X = sm + 2 * l * l;  // l×l (inverse)
+  double* P = sm + 3 * l * l;  // l×l (Rprev)
   __shared__ double d[kMaxL];
-  const int tid = threadIdx.x;
-  for (int idx = tid; idx < l * l; idx += kThreads) {
-    const int p = idx / l, q = idx - p * l;
-    G[idx] = 0.5 * (Gin[idx] + Gin[q * l + p]);
-    R[idx] = 0.0;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  constexpr int kPer = kMaxL * kMaxL / kThreads;
+  {  // every global read issued before the first use (one round trip)
+    double g0[kPer], g1[kPer], pr[kPer];
+#pragma unroll
+    for (int k = 0; k < kPer; ++k) {
+      const int idx = tid + k * kThreads;
+      const int p = idx / l, q = idx - p * l;
+      const bool in = idx < l * l;
+      g0[k] = in ? Gin[idx] : 0.0;
+      g1[k] = in ? Gin[q * l + p] : 0.0;
+      pr[k] = in && Rprev ? Rprev[idx] : 0.0;
+    }
+#pragma unroll
+    for (int k = 0; k < kPer; ++k) {
+      const int idx = tid + k * kThreads;
+      if (idx < l * l) {
+        G[idx] = 0.5 * (g0[k] + g1[k]);
+        R[idx] = 0.0;
+        P[idx] = pr[k];
+      }
+    }
   }
   __syncthreads();
   double gmax = 0.0;
   for (int j = 0; j < l; ++j) gmax = fmax(gmax, G[j * l + j]);
-  // right-looking: column j's pivot, then row j of R, then the rank-1 update
-  // of the trailing block of G — every step fully parallel
+  // right-looking, one barrier per column: every thread forms the pivot's
+  // reciprocal square root itself (same bits everywhere), then row j of R and
+  // the rank-1 update of the trailing block of G, G_ab −= G_ja·G_jb / G_jj
+  // (row j of G is not written in step j)
   const double floor_ = 0x1p-104 * gmax;  // L (and Q1) are full rank; guard against roundoff only
   for (int j = 0; j < l; ++j) {
     const double dj = G[j * l + j];
-    const double rjj = sqrt(dj > floor_ ? dj : (floor_ > 0.0 ? floor_ : 1.0));
-    for (int i = j + tid; i < l; i += kThreads) R[j * l + i] = i == j ? rjj : G[j * l + i] / rjj;
-    __syncthreads();
-    const int w = l - j - 1;
-    for (int idx = tid; idx < w * w; idx += kThreads) {
-      const int a = j + 1 + idx / w, b = j + 1 + idx % w;
-      G[a * l + b] -= R[j * l + a] * R[j * l + b];
+    const double dc = dj > floor_ ? dj : (floor_ > 0.0 ? floor_ : 1.0);
+    const double ri = rsqrt(dc);  // 1/R_jj
+    for (int i = j + tid; i < l; i += kThreads) R[j * l + i] = i == j ? dc * ri : G[j * l + i] * ri;
+    if (tid == 0) d[j] = ri;
+    const double ri2 = ri * ri;
+    for (int a = j + 1 + warp; a < l; a += kThreads / 32) {
+      const double ga = G[j * l + a] * ri2;
+      for (int b = j + 1 + lane; b < l; b += 32) G[a * l + b] = fma(-ga, G[j * l + b], G[a * l + b]);
     }
     __syncthreads();
   }
   // X = R⁻¹ (upper): thread j owns column j, back substitution with i
-  // descending in lock-step (R reads are broadcasts)
+  // descending (R reads are broadcasts), four partial sums per dot product
   if (tid < l) {
     const int j = tid;
-    for (int i = l - 1; i >= 0; --i) {
-      double s = 0.0;
-      for (int t = i + 1; t <= j; ++t) s += R[i * l + t] * X[t * l + j];
-      X[i * l + j] = i <= j ? ((i == j ? 1.0 : 0.0) - s) / R[i * l + i] : 0.0;
+    for (int i = l - 1; i > j; --i) X[i * l + j] = 0.0;
+    for (int i = j; i >= 0; --i) {
+      double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+      const double* ri = R + i * l;
+      int t = i + 1;
+      for (; t + 3 <= j; t += 4) {
+        a0 = fma(ri[t], X[t * l + j], a0);
+        a1 = fma(ri[t + 1], X[(t + 1) * l + j], a1);
+        a2 = fma(ri[t + 2], X[(t + 2) * l + j], a2);
+        a3 = fma(ri[t + 3], X[(t + 3) * l + j], a3);
+      }
+      for (; t <= j; ++t) a0 = fma(ri[t], X[t * l + j], a0);
+      X[i * l + j] = ((i == j ? 1.0 : 0.0) - ((a0 + a1) + (a2 + a3))) * d[i];
     }
   }
   __syncthreads();
@@ -74,7 +104,7 @@ __global__ void __launch_bounds__(kThreads) chol_kernel(const double* __restrict
     if (!Rprev) s = R[idx];
     else {
       s = 0.0;
-      for (int t = i; t <= j; ++t) s += R[i * l + t] * Rprev[t * l + j];
+      for (int t = i; t <= j; ++t) s = fma(R[i * l + t], P[t * l + j], s);
     }
     G[idx] = s;  // reuse G for Rtot
   }
@@ -88,9 +118,96 @@ __global__ void __launch_bounds__(kThreads) chol_kernel(const double* __restrict
   }
 }
 
+// The same contract for l ≤ 32 in ONE warp, no shared memory and no
+// barriers: lane b holds column b of G, then of R (and of Rprev), in
+// registers (LP = l rounded up to 8, static indices); the values of other
+// columns arrive by broadcast shuffles.  Order: Cholesky (right-looking), then
+// Rtot = R·Rprev and its row signs, then X = R⁻¹ written with the column signs.
+template <int LP>
+__global__ void __launch_bounds__(32) chol_warp_kernel(const double* __restrict__ Gin, int l,
+                                                       const double* __restrict__ Rprev, int signfix,
+                                                       double* __restrict__ Minv, double* __restrict__ Rtot) {
+  constexpr unsigned FULL = 0xffffffffu;
+  const int lane = threadIdx.x;
+  const bool own = lane < l;
+  double g[LP], r[LP], pc[LP], d[LP];
+#pragma unroll
+  for (int i = 0; i < LP; ++i) {
+    const bool in = own && i < l;
+    g[i] = in ? 0.5 * (Gin[i * l + lane] + Gin[lane * l + i]) : 0.0;
+    pc[i] = in && Rprev ? Rprev[i * l + lane] : 0.0;
+    r[i] = 0.0;
+  }
+  double gmax = 0.0;
+#pragma unroll
+  for (int j = 0; j < LP; ++j) gmax = fmax(gmax, __shfl_sync(FULL, g[j], j));  // lanes ≥ l hold 0
+  const double floor_ = 0x1p-104 * gmax;
+#pragma unroll
+  for (int j = 0; j < LP; ++j) {
+    if (j >= l) break;
+    const double dj = __shfl_sync(FULL, g[j], j);
+    const double dc = dj > floor_ ? dj : (floor_ > 0.0 ? floor_ : 1.0);
+    const double ri = rsqrt(dc);
+    d[j] = ri;
+    const double rjb = lane == j ? dc * ri : (lane > j ? g[j] * ri : 0.0);  // R[j][lane]
+    r[j] = rjb;
+#pragma unroll
+    for (int a = j + 1; a < LP; ++a) {
+      const double rja = __shfl_sync(FULL, rjb, a);
+      g[a] = fma(-rja, rjb, g[a]);
+    }
+  }
+  // Rtot = R·Rprev (column `lane`), reusing g; row signs from its diagonal
+#pragma unroll
+  for (int i = 0; i < LP; ++i) {
+    double s = 0.0;
+    if (!Rprev) {
+      s = r[i];
+    } else {
+#pragma unroll
+      for (int t = i; t < LP; ++t) s = fma(__shfl_sync(FULL, r[i], t), pc[t], s);
+    }
+    g[i] = s;
+  }
+  double sg[LP];
+#pragma unroll
+  for (int i = 0; i < LP; ++i) sg[i] = (signfix && __shfl_sync(FULL, g[i], i) < 0.0) ? -1.0 : 1.0;
+  if (own)
+#pragma unroll
+    for (int i = 0; i < LP; ++i)
+      if (i < l) Rtot[i * l + lane] = g[i] * sg[i];
+  // X = R⁻¹, column `lane` (upper), back substitution; reuse pc
+  double dl = 1.0;  // this column's sign
+#pragma unroll
+  for (int i = 0; i < LP; ++i)
+    if (i == lane) dl = sg[i];
+#pragma unroll
+  for (int i = LP - 1; i >= 0; --i) {
+    double a0 = 0.0, a1 = 0.0;
+#pragma unroll
+    for (int t = i + 1; t < LP; ++t) {
+      const double rit = __shfl_sync(FULL, r[i], t);
+      if ((t - i) & 1) a0 = fma(rit, pc[t], a0);
+      else a1 = fma(rit, pc[t], a1);
+    }
+    pc[i] = i < l && i <= lane ? ((i == lane ? 1.0 : 0.0) - (a0 + a1)) * d[i] : 0.0;
+  }
+  if (own)
+#pragma unroll
+    for (int i = 0; i < LP; ++i)
+      if (i < l) Minv[i * l + lane] = pc[i] * dl;
+}
+
 void chol(Ctx& c, const double* G, int l, const double* Rprev, int signfix, double* Minv, double* Rtot) {
-  ensure_smem((const void*)chol_kernel, 3 * kMaxL * kMaxL * 8);
-  chol_kernel<<<1, kThreads, 3 * l * l * 8, c.stream>>>(G, l, Rprev, signfix, Minv, Rtot);
+  switch ((l + 7) & ~7) {
+    case 8: chol_warp_kernel<8><<<1, 32, 0, c.stream>>>(G, l, Rprev, signfix, Minv, Rtot); break;
+    case 16: chol_warp_kernel<16><<<1, 32, 0, c.stream>>>(G, l, Rprev, signfix, Minv, Rtot); break;
+    case 24: chol_warp_kernel<24><<<1, 32, 0, c.stream>>>(G, l, Rprev, signfix, Minv, Rtot); break;
+    case 32: chol_warp_kernel<32><<<1, 32, 0, c.stream>>>(G, l, Rprev, signfix, Minv, Rtot); break;
+    default:
+      ensure_smem((const void*)chol_kernel, 4 * kMaxL * kMaxL * 8);
+      chol_kernel<<<1, kThreads, 4 * l * l * 8, c.stream>>>(G, l, Rprev, signfix, Minv, Rtot);
+  }
   RPCA_CHECK_LAUNCH();
   count_launch(c, 1, "cholqr_chol");
 }

@@ -124,6 +124,18 @@ __device__ __forceinline__ void dmma(double (&d)[2], double a, double b) {
                : "d"(a), "d"(b));
 }
 
+// 1/u: MUFU seed + two Newton steps (≤ 1 ulp); 0 for u = 0, the exact
+// reciprocal for |u| < 2^-1000 (where the flush-to-zero seed is not usable)
+__device__ __forceinline__ double rcp_nr(double u) {
+  if (fabs(u) < 0x1p-1000) return u != 0.0 ? 1.0 / u : 0.0;
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(u));
+  double e = fma(-u, r, 1.0);
+  r = fma(r, e, r);
+  e = fma(-u, r, 1.0);
+  return fma(r, e, r);
+}
+
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);

@@ -30,10 +30,12 @@ __global__ void __launch_bounds__(kJThreads) jacobi_kernel(const double* __restr
   double* Mc = sm;
   double* Wc = sm + l * l;
   __shared__ double nrm[kMaxL];
+  __shared__ double nrm2[kMaxL];  // ‖M[:, p]‖², refreshed every sweep, updated by each rotation
   __shared__ int rank_[kMaxL];
   __shared__ int rotated[2];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  for (int idx = tid; idx < l * l; idx += kJThreads) {
+  const int nthr = blockDim.x, nwarp = nthr >> 5;  // one warp per pair of a round
+  for (int idx = tid; idx < l * l; idx += nthr) {
     const int i = idx / l, p = idx % l;
     Mc[p * l + i] = R[idx];
     Wc[p * l + i] = (i == p) ? 1.0 : 0.0;
@@ -41,12 +43,22 @@ __global__ void __launch_bounds__(kJThreads) jacobi_kernel(const double* __restr
   if (tid < 2) rotated[tid] = 0;
   __syncthreads();
   const int lp = (l + 1) & ~1;  // players (one dummy if l is odd)
-  const double eps = 0x1p-52 * (double)l;
+  const double eps = 0x1p-52 * (double)l, eps2 = eps * eps;
   for (int sweep = 0; sweep < 30 && l > 1; ++sweep) {
+    for (int p = warp; p < l; p += nwarp) {
+      double s = 0.0;
+      for (int i = lane; i < l; i += 32) s = fma(Mc[p * l + i], Mc[p * l + i], s);
+      s = warp_sum(s);
+      if (lane == 0) nrm2[p] = s;
+    }
+    __syncthreads();
     for (int round = 0; round < lp - 1; ++round) {
       const int k = warp;
       if (k < lp / 2) {
-        auto player = [&](int i) { return i == 0 ? 0 : 1 + ((i - 1 + round) % (lp - 1)); };
+        auto player = [&](int i) {  // 1 + (i − 1 + round) mod (lp − 1), both terms < lp − 1
+          const int v = i - 1 + round;
+          return i == 0 ? 0 : 1 + (v >= lp - 1 ? v - (lp - 1) : v);
+        };
         int p = player(k), q = player(lp - 1 - k);
         if (p > q) { const int t = p; p = q; q = t; }
         if (q < l) {
@@ -54,18 +66,21 @@ __global__ void __launch_bounds__(kJThreads) jacobi_kernel(const double* __restr
           const double x0 = lane < l ? Mc[p * l + lane] : 0.0, y0 = lane < l ? Mc[q * l + lane] : 0.0;
           const double x1 = lane + 32 < l ? Mc[p * l + lane + 32] : 0.0;
           const double y1 = lane + 32 < l ? Mc[q * l + lane + 32] : 0.0;
-          double a = x0 * x0 + x1 * x1, b = y0 * y0 + y1 * y1, g = x0 * y0 + x1 * y1;
-#pragma unroll
-          for (int o = 16; o > 0; o >>= 1) {
-            a += __shfl_xor_sync(0xffffffffu, a, o);
-            b += __shfl_xor_sync(0xffffffffu, b, o);
-            g += __shfl_xor_sync(0xffffffffu, g, o);
-          }
-          if (fabs(g) > eps * sqrt(a * b)) {
-            if (lane == 0) rotated[sweep & 1] = 1;
-            const double zeta = (b - a) / (2.0 * g);
-            const double t = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
-            const double cs = 1.0 / sqrt(1.0 + t * t), sn = cs * t;
+          // only γ is reduced; α, β follow the rotations exactly in exact
+          // arithmetic (α' = α − tγ, β' = β + tγ) and are recomputed per sweep
+          const double g = warp_sum(fma(x0, y0, x1 * y1));
+          const double a = nrm2[p], b = nrm2[q];
+          if (g * g > eps2 * (a * b)) {
+            // t = tan θ = sign(ζ)/(|ζ| + √(1+ζ²)), ζ = (β−α)/(2γ), written as
+            // sign(β−α)·2γ / (|β−α| + hypot(β−α, 2γ)): one hypot, one reciprocal
+            const double tau = b - a, sig = 2.0 * g;
+            const double t = (tau >= 0.0 ? sig : -sig) * rcp_nr(fabs(tau) + hypot(tau, sig));
+            const double cs = rsqrt(fma(t, t, 1.0)), sn = cs * t;
+            if (lane == 0) {
+              rotated[sweep & 1] = 1;
+              nrm2[p] = fma(-t, g, a);
+              nrm2[q] = fma(t, g, b);
+            }
             if (lane < l) {
               Mc[p * l + lane] = cs * x0 - sn * y0;
               Mc[q * l + lane] = sn * x0 + cs * y0;
@@ -91,7 +106,7 @@ __global__ void __launch_bounds__(kJThreads) jacobi_kernel(const double* __restr
     if (!any) break;
   }
   // σ_p = ‖M[:, p]‖
-  for (int p = warp; p < l; p += (kJThreads / 32)) {
+  for (int p = warp; p < l; p += nwarp) {
     double s = 0.0;
     for (int i = lane; i < l; i += 32) s += Mc[p * l + i] * Mc[p * l + i];
     s = warp_sum(s);
@@ -104,7 +119,7 @@ __global__ void __launch_bounds__(kJThreads) jacobi_kernel(const double* __restr
     rank_[tid] = r;
   }
   __syncthreads();
-  for (int idx = tid; idx < l * l; idx += kJThreads) {
+  for (int idx = tid; idx < l * l; idx += nthr) {
     const int p = idx / l, i = idx % l;
     const int rp = rank_[p];
     Wout[i * l + rp] = Wc[p * l + i];
@@ -246,7 +261,10 @@ __global__ void __launch_bounds__(kThreads) sqrt_inv_kernel(const double* __rest
     __syncthreads();
     for (int round = 0; round < lp - 1; ++round) {
       for (int k = tid; k < lp / 2; k += kThreads) {
-        auto player = [&](int i) { return i == 0 ? 0 : 1 + ((i - 1 + round) % (lp - 1)); };
+        auto player = [&](int i) {  // 1 + (i − 1 + round) mod (lp − 1), both terms < lp − 1
+          const int v = i - 1 + round;
+          return i == 0 ? 0 : 1 + (v >= lp - 1 ? v - (lp - 1) : v);
+        };
         int p = player(k), q = player(lp - 1 - k);
         if (p > q) { const int t = p; p = q; q = t; }
         double c = 1.0, s = 0.0;
@@ -359,7 +377,8 @@ void jacobi_svd_small(Ctx& c, const double* R, int l, double* sigma, double* W, 
   RPCA_REQUIRE(l >= 1 && l <= kMaxL, RPCA_E_SHAPE, "jacobi: l=%d", l);
   const int smem = 2 * l * l * 8;
   ensure_smem((const void*)jacobi_kernel, 2 * kMaxL * kMaxL * 8);
-  jacobi_kernel<<<1, kJThreads, smem, c.stream>>>(R, l, sigma, W, Vr);
+  const int threads = 32 * std::max(1, ((l + 1) & ~1) / 2);  // one warp per pair of a round
+  jacobi_kernel<<<1, threads, smem, c.stream>>>(R, l, sigma, W, Vr);
   RPCA_CHECK_LAUNCH();
   count_launch(c, 1, "jacobi");
 }

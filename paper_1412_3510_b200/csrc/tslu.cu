@@ -6,8 +6,9 @@
 // L with Y = L·U (MATLAB's two-output lu; reading Q3).
 //
 // B200 design — tournament pivoting (CALU):
-//   1. leaf kernel: one CTA per block of R·256 rows runs GEPP and nominates l
-//      candidate pivot rows (original rows);
+//   1. leaf kernel: a persistent CTA walks blocks of R·256 rows (the next
+//      block bulk-copied into shared memory meanwhile), runs GEPP on each and
+//      nominates l candidate pivot rows (original rows);
 //   2. tree kernel: groups of G candidate sets are stacked (original values
 //      gathered from Y) and reduced by GEPP again, until one set is left; the
 //      last GEPP gives the pivot order, U (l×l) and the multipliers of the pivot
@@ -21,9 +22,10 @@
 // all register indices are static).  Per column: the argmax over the warp is
 // two redux.sync.max on the bits of |v| (a non-negative double orders like its
 // bit pattern) plus a ballot for the lowest lane on ties; each warp's winner
-// lane publishes its (key, row) and its whole row to shared memory; ONE
-// __syncthreads; every warp then reduces the 8 warp winners the same way and
-// reads the pivot row with broadcast loads.  Local row order = original row
+// lane publishes its (key, row), its reciprocal and the panel part of its row
+// to shared memory; ONE __syncthreads; every warp then reduces the 8 warp winners the
+// same way (lanes 0-7 hold the keys) and reads the pivot row with broadcast
+// loads.  Local row order = original row
 // order (leaves are contiguous; tree candidates are sorted by id within each
 // set and sets cover ascending row ranges), so "lowest local row" is the
 // lowest-original-row tie rule.  Tournament pivots differ from plain GEPP, so
@@ -100,7 +102,7 @@ __global__ void __launch_bounds__(kThreads, SelCfg<LP, RR>::kMinBlocks)
                      int64_t n_in, int G, int64_t* __restrict__ cand_out, int final_, double* __restrict__ U,
                      double* __restrict__ Lp, int64_t* __restrict__ piv_out, double* __restrict__ M,
                      const double* __restrict__ rows_in, double* __restrict__ rows_out,
-                     const double* __restrict__ mu) {
+                     const double* __restrict__ mu, int bulk) {
   using Cfg = SelCfg<LP, RR>;
   constexpr int R = Cfg::R, CAP = Cfg::kCap;
   __shared__ int64_t ids[CAP];
@@ -114,18 +116,41 @@ __global__ void __launch_bounds__(kThreads, SelCfg<LP, RR>::kMinBlocks)
   __shared__ int piv[LP];
   __shared__ int nrows_s;
   __shared__ int setcnt[CAP + 1];
-  extern __shared__ double keep[];  // final only: LP × LP published pivot rows, U, M, multipliers
+  __shared__ uint64_t full_bar;
+  __shared__ double udr[LP];
+  // final: LP × LP published pivot rows, U, M, multipliers; bulk: the staged
+  // rows of the next leaf (CAP × l, row-major as in Y)
+  extern __shared__ double keep[];
   double* msm = keep + LP * LP + l * l;  // final only: multiplier of (step j, row r) at j·CAP + r
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
 
+  // bulk (leaves only, never final): a persistent CTA walks leaves b, b+grid, …
+  // and a 1-D bulk copy stages the next leaf's rows (contiguous in Y) in
+  // shared memory while the current leaf runs its GEPP on registers
+  const int64_t nleaf = (leaf == 1 && bulk) ? (m + CAP - 1) / CAP : (int64_t)blockIdx.x + 1;
+  auto leaf_bytes = [&](int64_t b) -> uint32_t {
+    return (uint32_t)(imin64(CAP, m - b * CAP) * l * 8) & ~15u;  // an odd last double is read from Y
+  };
+  if (leaf == 1 && bulk) {
+    if (tid == 0) {
+      mbar_init(&full_bar, 1);
+      fence_barrier_init();
+      const int64_t b = blockIdx.x;
+      mbar_arrive_expect_tx(&full_bar, leaf_bytes(b));
+      if (leaf_bytes(b)) bulk_load(keep, Y + b * CAP * l, leaf_bytes(b), &full_bar);
+    }
+    __syncthreads();
+  }
+  uint32_t it = 0;
+  for (int64_t blk = blockIdx.x; blk < nleaf; blk += gridDim.x, ++it) {
   if (leaf == 1) {
-    const int64_t r0 = (int64_t)blockIdx.x * CAP;
+    const int64_t r0 = blk * CAP;
     if (tid == 0) nrows_s = (int)imin64(CAP, m - r0);
     for (int r = tid; r < CAP; r += kThreads) ids[r] = r0 + r;
   } else {
     // compact the valid candidates of this group: sets in ascending order,
     // each set's ids sorted ascending (rank = #smaller valid ids in the set)
-    const int64_t s0 = (int64_t)blockIdx.x * G * l, s1 = imin64(n_in * l, s0 + (int64_t)G * l);
+    const int64_t s0 = blk * G * l, s1 = imin64(n_in * l, s0 + (int64_t)G * l);
     const int nslots = (int)(s1 - s0), nsets = (nslots + l - 1) / l;
     for (int s = tid; s < nslots; s += kThreads) ids[s] = cand_in[s0 + s];
     __syncthreads();
@@ -173,6 +198,9 @@ __global__ void __launch_bounds__(kThreads, SelCfg<LP, RR>::kMinBlocks)
   double w[R][LP];
   bool act[R];
   int pstep[R];  // ≥ 0: pivot step within the current panel (−1: not a pivot)
+  const bool staged = leaf == 1 && bulk;
+  if (staged) mbar_wait(&full_bar, it & 1u);
+  const uint32_t nstaged = staged ? leaf_bytes(blk) / 8 : 0u;
 #pragma unroll
   for (int q = 0; q < R; ++q) {
     const int r = tid * R + q;
@@ -180,12 +208,23 @@ __global__ void __launch_bounds__(kThreads, SelCfg<LP, RR>::kMinBlocks)
     pstep[q] = -1;
     const double* src = nullptr;
     if (act[q])
-      src = leaf == 2 ? rows_in + ((int64_t)blockIdx.x * G * l + slot_of[r]) * l : Y + ids[r] * l;
+      src = leaf == 2                             ? rows_in + (blk * G * l + slot_of[r]) * l
+            : (uint32_t)((r + 1) * l) <= nstaged ? keep + r * l
+                                                  : Y + ids[r] * l;
     // a pending centring of Y (the projector P of DESIGN.md reading Q8) is
     // applied on load; direct rows (leaf 2) arrive centred
     const bool sub = mu != nullptr && leaf != 2;
 #pragma unroll
     for (int t = 0; t < LP; ++t) w[q][t] = (act[q] && t < l) ? src[t] - (sub ? mu[t] : 0.0) : 0.0;
+  }
+  if (staged) {
+    __syncthreads();  // every row is in registers: the buffer takes the next leaf
+    const int64_t nb = blk + gridDim.x;
+    if (tid == 0 && nb < nleaf) {
+      fence_proxy_async();
+      mbar_arrive_expect_tx(&full_bar, leaf_bytes(nb));
+      if (leaf_bytes(nb)) bulk_load(keep, Y + nb * CAP * l, leaf_bytes(nb), &full_bar);
+    }
   }
 
   // Blocked GEPP, panels of 8 columns.  Registers hold each row SHIFTED so
@@ -220,30 +259,21 @@ __global__ void __launch_bounds__(kThreads, SelCfg<LP, RR>::kMinBlocks)
 #pragma unroll
         for (int q = 0; q < R; ++q)
           if (q == bq) {
-            const double u = w[q][s];
             slot[j & 1][warp] = make_uint2(mk, (uint32_t)(tid * R + q));
-            suinv[j & 1][warp] = (u != 0.0) ? __drcp_rn(u) : 0.0;
+            suinv[j & 1][warp] = rcp_nr(w[q][s]);
 #pragma unroll
             for (int t = s; t < 8; ++t) pbuf[j & 1][warp][t] = w[q][t];
           }
       }
       __syncthreads();
-      // max over the 8 warp winners in a fixed 3-level tree (lower warp on ties)
-      uint2 k[kWarps];
-      int wi[kWarps];
-#pragma unroll
-      for (int i = 0; i < kWarps; ++i) {
-        k[i] = slot[j & 1][i];
-        wi[i] = i;
-      }
-#pragma unroll
-      for (int st = 1; st < kWarps; st <<= 1)
-#pragma unroll
-        for (int i = 0; i < kWarps; i += 2 * st)
-          if (k[i + st].x > k[i].x) { k[i] = k[i + st]; wi[i] = wi[i + st]; }
-      const int p = (int)k[0].y;
-      const double uinv = suinv[j & 1][wi[0]];
-      const double* prow = pbuf[j & 1][wi[0]];
+      // max over the 8 warp winners: lanes 0-7 hold their keys, one redux and
+      // a ballot (lowest warp = lowest rows on ties)
+      const uint32_t kv = lane < kWarps ? slot[j & 1][lane].x : 0u;
+      const uint32_t gk = __reduce_max_sync(0xffffffffu, kv);
+      const int ww = __ffs(__ballot_sync(0xffffffffu, kv == gk)) - 1;
+      const int p = (int)slot[j & 1][ww].y;
+      const double uinv = suinv[j & 1][ww];
+      const double* prow = pbuf[j & 1][ww];
       if (tid == 0) piv[j] = p;
       if (final_ && tid < 8 - s) keep[j * LP + tid] = prow[s + tid];  // U[j][j .. pb+7]
 #pragma unroll
@@ -296,15 +326,17 @@ __global__ void __launch_bounds__(kThreads, SelCfg<LP, RR>::kMinBlocks)
     }
   }
   __syncthreads();
-  for (int j = tid; j < l; j += kThreads) cand_out[(int64_t)blockIdx.x * l + j] = j < steps ? ids[piv[j]] : -1;
+  for (int j = tid; j < l; j += kThreads) cand_out[blk * l + j] = j < steps ? ids[piv[j]] : -1;
   if (rows_out) {  // direct mode: forward the winners' original rows to the next level
     for (int idx = tid; idx < l * l; idx += kThreads) {
       const int j = idx / l, t = idx - j * l;
-      rows_out[(int64_t)blockIdx.x * l * l + idx] =
-          j < steps ? rows_in[((int64_t)blockIdx.x * G * l + slot_of[piv[j]]) * l + t] : 0.0;
+      rows_out[blk * l * l + idx] = j < steps ? rows_in[(blk * G * l + slot_of[piv[j]]) * l + t] : 0.0;
     }
   }
-  if (!final_) return;
+  if (!final_) {
+    __syncthreads();  // ids / piv are rewritten by the next leaf
+    continue;
+  }
   // keep[j] = pivot row j as published (columns j.. at 0..LP−j−1); its
   // multiplier of step s < j is msm[s·CAP + piv[j]]
   double* Ms = keep + LP * LP;  // l×l M = U⁻¹ (U_ic = keep[i·LP + c − i])
@@ -314,23 +346,36 @@ __global__ void __launch_bounds__(kThreads, SelCfg<LP, RR>::kMinBlocks)
     U[idx] = u;
     Lp[idx] = c < j ? msm[c * CAP + piv[j]] : (c == j ? 1.0 : 0.0);
   }
-  for (int j = tid; j < l; j += kThreads) piv_out[j] = ids[piv[j]];
+  for (int j = tid; j < l; j += kThreads) {
+    piv_out[j] = ids[piv[j]];
+    const double uii = keep[j * LP];
+    udr[j] = uii != 0.0 ? 1.0 / uii : 0.0;
+  }
   __syncthreads();
   // M = U⁻¹ with the zero-pivot rule (a zero U_ii zeroes row i of M: x_i = 0
   // for every input of the row substitution x·U = y, reading Q3).  Thread j
-  // owns column j: back substitution M[i][j] = (δ_ij − Σ_{t=i+1..j} U_it M_tj)/U_ii
-  // with i descending in lock-step over all threads (U reads are broadcasts).
+  // owns column j: back substitution M[i][j] = (δ_ij − Σ_{t=i+1..j} U_it M_tj)/U_ii,
+  // four partial sums per dot product (U reads are broadcasts).
   if (tid < l) {
     const int j = tid;
-    for (int i = l - 1; i >= 0; --i) {
-      double acc = 0.0;
-      for (int t = i + 1; t <= j; ++t) acc += keep[i * LP + t - i] * Ms[t * l + j];
-      const double uii = keep[i * LP];
-      Ms[i * l + j] = (i <= j && uii != 0.0) ? ((i == j ? 1.0 : 0.0) - acc) / uii : 0.0;
+    for (int i = l - 1; i > j; --i) Ms[i * l + j] = 0.0;
+    for (int i = j; i >= 0; --i) {
+      double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+      const double* ui = keep + i * LP - i;  // U_it = ui[t]
+      int t = i + 1;
+      for (; t + 3 <= j; t += 4) {
+        a0 = fma(ui[t], Ms[t * l + j], a0);
+        a1 = fma(ui[t + 1], Ms[(t + 1) * l + j], a1);
+        a2 = fma(ui[t + 2], Ms[(t + 2) * l + j], a2);
+        a3 = fma(ui[t + 3], Ms[(t + 3) * l + j], a3);
+      }
+      for (; t <= j; ++t) a0 = fma(ui[t], Ms[t * l + j], a0);
+      Ms[i * l + j] = ((i == j ? 1.0 : 0.0) - ((a0 + a1) + (a2 + a3))) * udr[i];
     }
   }
   __syncthreads();
   for (int idx = tid; idx < l * l; idx += kThreads) M[idx] = Ms[idx];
+  }  // leaves
 }
 
 // Y[piv[j] − row0] ← Lp[j] for the pivot rows this shard holds (their exact
@@ -367,10 +412,19 @@ template <int LP, int R>
 void select_lpr(Ctx& c, unsigned grid, const double* Y, int64_t m, int l, int leaf, const int64_t* cin, int64_t n_in,
                 int G, int64_t* cout, int final_, double* U, double* Lp, int64_t* piv, double* M,
                 const double* rows_in, double* rows_out, const double* mu) {
-  const size_t smem = final_ ? (size_t)(LP * LP + l * l + (size_t)SelCfg<LP, R>::kCap * l) * 8 : 0;
-  if (smem) ensure_smem((const void*)lu_select_kernel<LP, R>, (int)smem);
+  constexpr int CAP = SelCfg<LP, R>::kCap;
+  // leaves that are not the last level run persistent with bulk-staged rows
+  const int bulk = leaf == 1 && !final_ && (reinterpret_cast<uintptr_t>(Y) & 15) == 0;
+  const size_t smem = final_ ? (size_t)(LP * LP + l * l + (size_t)CAP * l) * 8 : bulk ? (size_t)CAP * l * 8 : 0;
+  const void* fn = (const void*)lu_select_kernel<LP, R>;
+  if (smem) ensure_smem(fn, (int)smem);
+  if (bulk) {
+    int occ = 0;
+    RPCA_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, kThreads, smem));
+    grid = (unsigned)std::min<int64_t>(grid, (int64_t)c.num_sms * std::max(1, occ));
+  }
   lu_select_kernel<LP, R><<<grid, kThreads, smem, c.stream>>>(Y, m, l, leaf, cin, n_in, G, cout, final_, U, Lp, piv,
-                                                              M, rows_in, rows_out, mu);
+                                                              M, rows_in, rows_out, mu, bulk);
 }
 
 template <int LP>
