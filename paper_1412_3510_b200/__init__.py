@@ -22,7 +22,8 @@ __all__ = ["pca", "eigens", "diffsnorm", "omega", "apply", "colmeans", "lu_renor
            "comm_init", "comm_init_torch", "VirtualGroup", "uniform_shard"]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-_LIB_PATH = os.path.join(_HERE, "librpca.so")
+# RPCA_LIB_PATH: an alternative build of the same library (tuning experiments)
+_LIB_PATH = os.environ.get("RPCA_LIB_PATH") or os.path.join(_HERE, "librpca.so")
 
 OK, E_ARG, E_SHAPE, E_NONFINITE, E_NOTPSD, E_CUDA, E_NCCL, E_WORKSPACE, E_NOTIMPL, E_NOMEM = range(10)
 DENSE, CSR_KIND = 0, 1

@@ -73,14 +73,17 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t by
                : "memory");
 }
 
+// Wait for the phase with parity `parity` to complete.  The suspend-time hint
+// lets the waiting warp sleep in hardware until the phase flips instead of
+// spinning: a spinning warp costs issue slots the working warps need.
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   uint32_t addr = smem_u32(bar);
   asm volatile(
       "{\n\t.reg .pred p;\n"
       "WAIT_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n\t"
       "@!p bra WAIT_%=;\n\t}" ::"r"(addr),
-      "r"(parity)
+      "r"(parity), "r"(0x989680u)
       : "memory");
 }
 

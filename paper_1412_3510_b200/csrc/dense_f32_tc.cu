@@ -25,9 +25,10 @@
 //   alternate so the epilogue of unit u overlaps the MMAs of unit u+1; the
 //   epilogue writes (first chunk) or adds (later chunks) fp64 into Y and
 //   folds the centring correction −1·(c·X) of PAPER.md:430.
-// Aᵀ·Y (D[128 cols × N] += Aᵀ[128 cols × K rows] · Y[K × N]): the A tile is
-//   read as an MN-major operand straight from the TMA layout (no transpose;
-//   tf32 MN-major requires the 128B_ATOM_32B swizzle).
+// Aᵀ·Y (D[128 cols × N] += Aᵀ[128 cols × K rows] · Y[K × N]): the split
+//   warps read the row-major A tile (thread = column) and store A_hi and A_lo
+//   into TMEM (lane = column of A, one TMEM column per row), so all three
+//   products take their A operand from TMEM and only Yᵀ from shared memory.
 //   A CTA owns a group of ≤ 512/N column blocks (all accumulators live in
 //   TMEM) and a contiguous row range; each 32-row chunk of Yᵀ_hi/lo is loaded
 //   once and used for every column block of the group, so Y is read
@@ -61,21 +62,9 @@ __device__ __forceinline__ float lo_part(float a) {
   return a - __uint_as_float(__float_as_uint(a) & 0xFFFFE000u);
 }
 
-// MN-major tf32 operand: the only smem layout the tensor core takes for it is
-// SWIZZLE_128B_BASE32B (descriptor layout type 1; TMA mode 128B_ATOM_32B:
-// 32-byte chunks of each 128-byte MN row XOR-ed with the row index mod 4).
-// 128-byte MN rows (32 fp32), 4 K-rows per 512-byte atom (SBO), 32-wide MN
-// chunks 4096 bytes apart (LBO).
-__device__ __forceinline__ uint64_t desc_mn_sw128_32b(uint32_t saddr) {
-  uint64_t d = 0;
-  d |= (uint64_t)((saddr >> 4) & 0x3FFF);
-  d |= (uint64_t)(4096 >> 4) << 16;  // LBO: next 32 MN elements
-  d |= (uint64_t)(512 >> 4) << 32;   // SBO: next 4 K rows
-  d |= (uint64_t)1 << 46;
-  d |= (uint64_t)1 << 61;            // SWIZZLE_128B_BASE32B
-  return d;
-}
-
+// (An MN-major tf32 shared-memory operand would need SWIZZLE_128B_BASE32B —
+// descriptor layout type 1, TMA mode 128B_ATOM_32B, LBO 4096 / SBO 512; the
+// Aᵀ·Y kernel avoids it by moving A through TMEM.)
 __device__ __forceinline__ void mma_tf32(uint32_t tmem, uint64_t da, uint64_t db, uint32_t idesc, uint32_t acc) {
   asm volatile(
       "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
@@ -135,7 +124,7 @@ __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 
 #ifndef ATY_SLOTS
-#define ATY_SLOTS 2
+#define ATY_SLOTS 4
 #endif
 constexpr int kThreadsTC = 352;  // 11 warps: producer, hi-MMA, lo-MMA, 4 split, 4 epilogue
 constexpr int kTileBytes = 128 * 128;  // 16 KB A tile
@@ -366,39 +355,43 @@ struct AtyPlan {
 
 template <int N>
 struct AtyCfg {
-  static constexpr int kX = N * 128;
-  static constexpr int kTN = N <= 32 ? 32 : 64;
+  static constexpr int kX = N * 128;  // one Yᵀ chunk: N rows × 32 fp32
+  static constexpr int kTN = N <= 32 ? 32 : 64;  // TMEM columns per column-block accumulator
   static constexpr int kYS = 3;  // Yᵀ chunk buffers
   static constexpr int kYBytes = kYS * 2 * kX;
-  static constexpr int kStages = (212 * 1024 - kYBytes) / kTileBytes > 10 ? 10 : (212 * 1024 - kYBytes) / kTileBytes;
+  static constexpr int kStages = (212 * 1024 - kYBytes) / kTileBytes > 8 ? 8 : (212 * 1024 - kYBytes) / kTileBytes;
   static constexpr int kSmem = kStages * kTileBytes + kYBytes + 1024 + 512;
-  static constexpr int kNS = ATY_SLOTS;                 // 32-column A_lo slots after the accumulators
-  static constexpr int kSlot0 = 512 - 32 * kNS;
+  static constexpr int kNS = ATY_SLOTS;  // A slots after the accumulators: 32 columns A_hi + 32 columns A_lo
+  static constexpr int kSlot0 = 512 - 64 * kNS;
   static constexpr int kMaxCB = kSlot0 / kTN;
 };
+constexpr int kThreadsAty = 320;  // 10 warps: producer, MMA, 4 split, 4 epilogue
 
-// warps: 0 TMA producer, 1 hi-MMA issuer, 2 lo-MMA issuer, 3-6 split
-// (A_loᵀ → TMEM), 7-10 epilogue (fp64 flush per accumulation chunk)
+// warps: 0 TMA producer, 1 MMA issuer, 2-5 split (A → A_hi, A_lo in TMEM),
+// 6-9 epilogue (fp64 flush per accumulation chunk).  Every product reads its
+// A operand from TMEM (the "TS" form) and only Yᵀ from shared memory: per
+// 16 KB A tile the SM moves 16 KB (TMA) + 16 KB (split reads) + 24 KB (three
+// N-wide Yᵀ operands per k-step) through shared memory, not 88 KB as with the
+// MN-major shared-memory A operand read twice.
 template <int N>
-__global__ void __launch_bounds__(kThreadsTC, 1)
+__global__ void __launch_bounds__(kThreadsAty, 1)
     aty_f32_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmYh,
-                      const __grid_constant__ CUtensorMap tmYl, AtyPlan pl, int a3d, double* __restrict__ part) {
+                      const __grid_constant__ CUtensorMap tmYl, AtyPlan pl, double* __restrict__ part) {
   using Cfg = AtyCfg<N>;
-  constexpr int S = Cfg::kStages, YS = Cfg::kYS;
+  constexpr int S = Cfg::kStages, YS = Cfg::kYS, NS = Cfg::kNS;
   constexpr int RC = kKChunk / 32;  // row chunks per fp32 accumulation
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
   uint8_t* ybuf = smem + S * kTileBytes;
   uint64_t* full = reinterpret_cast<uint64_t*>(ybuf + Cfg::kYBytes);
-  uint64_t* empty = full + S;      // hi commit + lo commit
-  uint64_t* lo_full = empty + S;   // 4 split warps
-  uint64_t* tfree = lo_full + S;   // [kNS]
-  uint64_t* yfull = tfree + Cfg::kNS;  // [YS]
-  uint64_t* yempty = yfull + YS;   // [YS] hi commit + lo commit
-  uint64_t* hi_done = yempty + YS;  // [S] the stage's hi MMAs done (lo waits on it at chunk starts)
-  uint64_t* acc_full = hi_done + S;  // hi commit + lo commit
-  uint64_t* acc_empty = acc_full + 1;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 1);
+  uint64_t* empty = full + S;        // 4 split warps (tile read into registers)
+  uint64_t* yfull = empty + S;       // [YS]
+  uint64_t* yempty = yfull + YS;     // [YS] MMA commit
+  uint64_t* afull = yempty + YS;     // [NS] 4 split warps (A_hi, A_lo in TMEM)
+  uint64_t* tfree = afull + NS;      // [NS] MMA commit
+  uint64_t* acc_full = tfree + NS;   // MMA commit
+  uint64_t* acc_empty = acc_full + 1;  // [kMaxCB] 4 epilogue warps (that block's accumulator read out)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + Cfg::kMaxCB);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int p = blockIdx.x, g = p / pl.Pg, r = p - g * pl.Pg;
   const int64_t cb0 = (int64_t)g * pl.CBG;
@@ -408,17 +401,18 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
   if (threadIdx.x == 0) {
     for (int s = 0; s < S; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 2);
-      mbar_init(&lo_full[s], 4);
+      mbar_init(&empty[s], 4);
     }
     for (int y = 0; y < YS; ++y) {
       mbar_init(&yfull[y], 1);
-      mbar_init(&yempty[y], 2);
+      mbar_init(&yempty[y], 1);
     }
-    for (int a = 0; a < Cfg::kNS; ++a) mbar_init(&tfree[a], 1);
-    for (int s = 0; s < S; ++s) mbar_init(&hi_done[s], 1);
-    mbar_init(acc_full, 2);
-    mbar_init(acc_empty, 4);
+    for (int a = 0; a < NS; ++a) {
+      mbar_init(&afull[a], 4);
+      mbar_init(&tfree[a], 1);
+    }
+    mbar_init(acc_full, 1);
+    for (int cb = 0; cb < Cfg::kMaxCB; ++cb) mbar_init(&acc_empty[cb], 4);
     fence_barrier_init();
   }
   if (warp == 1) {
@@ -448,87 +442,44 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
       __syncwarp();
       for (int cbi = 0; cbi < ncb; ++cbi, rg.next()) {
         mbar_wait(&empty[rg.s], rg.ph ^ 1u);
-        uint8_t* st = smem + rg.s * kTileBytes;
-        if (leader) {
+        if (leader) {  // one box: 32 rows × 128 columns, row-major, no swizzle
           mbar_arrive_expect_tx(&full[rg.s], kTileBytes);
-          if (a3d) {  // one 3-D box (32 cols × 32 rows × 4 column groups) = the four 4 KB MN chunks
-            tma_load_3d(st, &tmA, 0, (int32_t)(rc * 32), (int32_t)((cb0 + cbi) * 4), &full[rg.s]);
-          } else {
-#pragma unroll
-            for (int b = 0; b < 4; ++b)  // four [32 rows × 32 cols] boxes (128B_ATOM_32B), MN chunks 4 KB apart
-              tma_load_2d(st + b * 4096, &tmA, (int32_t)((cb0 + cbi) * 128 + b * 32), (int32_t)(rc * 32),
-                          &full[rg.s]);
-          }
+          tma_load_2d(smem + rg.s * kTileBytes, &tmA, (int32_t)((cb0 + cbi) * 128), (int32_t)(rc * 32), &full[rg.s]);
         }
         __syncwarp();
       }
     }
-  } else if (warp == 1) {  // ---------------------------------------- hi-MMA issuer
-    // D_cb += A·Y_hi + A·Y_lo, A read MN-major (bit 15 of the instruction descriptor)
+  } else if (warp == 1) {  // ------------------------------------------- MMA issuer
+    // D_cb += A_hi·Y_hi + A_hi·Y_lo + A_lo·Y_hi, A_hi/A_lo from TMEM (lane =
+    // column of A, one TMEM column per row of A)
     const bool leader = elect_one();
-    constexpr uint32_t idesc = idesc_tf32(128, N) | (1u << 15);
-    Ring<S> rg;
+    constexpr uint32_t idesc = idesc_tf32(128, N);
     Ring<YS> ry;
+    Ring<NS> rt;
     int kin = 0;        // row chunks into the current accumulation chunk
     uint32_t chph = 0;  // acc_empty phase
     for (int64_t rc = rb; rc < re; ++rc, ry.next()) {
-      if (kin == 0) {  // a new accumulation chunk: the flush of the last one must be done
-        mbar_wait(acc_empty, chph ^ 1u);
-        chph ^= 1u;
-        tc_fence_after();
-      }
       const bool chunk_end = (kin == RC - 1) || (rc + 1 == re);
       mbar_wait(&yfull[ry.s], ry.ph);
       tc_fence_after();
       const uint32_t yh = smem_u32(ybuf + ry.s * 2 * Cfg::kX);
       const uint64_t dh = desc_sw128(yh), dl = desc_sw128(yh + Cfg::kX);
-      for (int cbi = 0; cbi < ncb; ++cbi, rg.next()) {
-        mbar_wait(&full[rg.s], rg.ph);
+      for (int cbi = 0; cbi < ncb; ++cbi, rt.next()) {
+        // a new accumulation chunk overwrites block cbi: its previous sums
+        // must have been read out (per block, so the flush of the last blocks
+        // overlaps the first MMAs of the next chunk)
+        if (kin == 0) mbar_wait(&acc_empty[cbi], chph ^ 1u);
+        mbar_wait(&afull[rt.s], rt.ph);
         tc_fence_after();
         const uint32_t d = tmem + (uint32_t)(cbi * Cfg::kTN);
-        const uint64_t da = desc_mn_sw128_32b(smem_u32(smem + rg.s * kTileBytes));
+        const uint32_t ah = tmem + (uint32_t)(Cfg::kSlot0 + 64 * rt.s), al = ah + 32;
         if (leader) {
 #pragma unroll
           for (int ks = 0; ks < 4; ++ks) {
-            mma_tf32(d, da + 64 * ks, dh + 2 * ks, idesc, (kin != 0 || ks != 0) ? 1u : 0u);
-            mma_tf32(d, da + 64 * ks, dl + 2 * ks, idesc, 1u);
+            mma_tf32_ts(d, ah + 8 * ks, dh + 2 * ks, idesc, (kin != 0 || ks != 0) ? 1u : 0u);
+            mma_tf32_ts(d, ah + 8 * ks, dl + 2 * ks, idesc, 1u);
+            mma_tf32_ts(d, al + 8 * ks, dh + 2 * ks, idesc, 1u);
           }
-          mma_commit(&empty[rg.s]);
-          mma_commit(&hi_done[rg.s]);
-          if (cbi == ncb - 1) {
-            mma_commit(&yempty[ry.s]);
-            if (chunk_end) mma_commit(acc_full);
-          }
-        }
-        __syncwarp();
-      }
-      if (++kin == RC) kin = 0;
-    }
-  } else if (warp == 2) {  // ---------------------------------------- lo-MMA issuer
-    // D_cb += A_lo·Y_hi with A_loᵀ read from TMEM (lane = column of A, column = row)
-    const bool leader = elect_one();
-    constexpr uint32_t idesc = idesc_tf32(128, N);
-    Ring<S> rg;
-    Ring<YS> ry;
-    Ring<Cfg::kNS> rt;
-    int kin = 0;
-    for (int64_t rc = rb; rc < re; ++rc, ry.next()) {
-      const bool chunk_end = (kin == RC - 1) || (rc + 1 == re);
-      mbar_wait(&yfull[ry.s], ry.ph);
-      tc_fence_after();
-      const uint64_t dh = desc_sw128(smem_u32(ybuf + ry.s * 2 * Cfg::kX));
-      for (int cbi = 0; cbi < ncb; ++cbi, rg.next(), rt.next()) {
-        // at a chunk start the hi issuer's accumulate-off MMA for this block
-        // must have run first (its next hi_done phase needs this stage freed)
-        if (kin == 0) mbar_wait(&hi_done[rg.s], rg.ph);
-        mbar_wait(&lo_full[rg.s], rg.ph);
-        tc_fence_after();
-        const uint32_t d = tmem + (uint32_t)(cbi * Cfg::kTN);
-        const uint32_t at = tmem + (uint32_t)(Cfg::kSlot0 + 32 * rt.s);
-        if (leader) {
-#pragma unroll
-          for (int ks = 0; ks < 4; ++ks) mma_tf32_ts(d, at + 8 * ks, dh + 2 * ks, idesc, 1u);
-          mma_commit(&empty[rg.s]);
           mma_commit(&tfree[rt.s]);
           if (cbi == ncb - 1) {
             mma_commit(&yempty[ry.s]);
@@ -537,31 +488,38 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
         }
         __syncwarp();
       }
+      if (kin == 0) chph ^= 1u;
       if (++kin == RC) kin = 0;
     }
-  } else if (warp < 7) {  // ---------------------------------------- split: A_loᵀ → TMEM
-    const int q = warp & 3;
-    const int t = 32 * q + lane;  // column of the block = TMEM lane
+  } else if (warp < 6) {  // ---------------------------------------- split: A → A_hi, A_lo in TMEM
+    const int q = warp & 3;        // this warp's TMEM lane quarter
+    const int t = 32 * q + lane;   // column of the block = TMEM lane
     const int64_t total = (re - rb) * ncb;
-    // element (row ρ, column t) of the 128B_ATOM_32B tile: box t/32, 128-byte
-    // row ρ, 32-byte chunk ((t mod 32)/8) XOR (ρ mod 4)
-    const uint32_t cb_off = (uint32_t)((t >> 5) * 4096 + ((t & 7) << 2));
-    const int c8 = (t & 31) >> 3;
+    const uint32_t lane_off = (uint32_t)(32 * q) << 16;
     Ring<S> rg;
-    Ring<Cfg::kNS> rt;
+    Ring<NS> rt;
     for (int64_t i = 0; i < total; ++i, rg.next(), rt.next()) {
       mbar_wait(&full[rg.s], rg.ph);
+      const float* tile = reinterpret_cast<const float*>(smem + rg.s * kTileBytes) + t;
+      float hi[32], lo[32];
+#pragma unroll
+      for (int rho = 0; rho < 32; ++rho) hi[rho] = tile[rho * 128];  // a warp reads 128 contiguous bytes
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[rg.s]);  // the tile is in registers: the stage is free
+#pragma unroll
+      for (int rho = 0; rho < 32; ++rho) {
+        const float a = hi[rho];
+        hi[rho] = __uint_as_float(__float_as_uint(a) & 0xFFFFE000u);
+        lo[rho] = a - hi[rho];
+      }
       mbar_wait(&tfree[rt.s], rt.ph ^ 1u);
       tc_fence_after();
-      const uint8_t* tile = smem + rg.s * kTileBytes + cb_off;
-      float v[32];
-#pragma unroll
-      for (int rho = 0; rho < 32; ++rho)
-        v[rho] = lo_part(*reinterpret_cast<const float*>(tile + rho * 128 + ((c8 ^ (rho & 3)) << 5)));
-      tmem_st32(tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(Cfg::kSlot0 + 32 * rt.s), v);
+      const uint32_t at = tmem + lane_off + (uint32_t)(Cfg::kSlot0 + 64 * rt.s);
+      tmem_st32(at, hi);
+      tmem_st32(at + 32, lo);
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&lo_full[rg.s]);
+      if (lane == 0) mbar_arrive(&afull[rt.s]);
     }
   } else {  // ---------------------------------------------------- epilogue: fp64 flush per chunk
     const int q = warp & 3;
@@ -572,17 +530,15 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
       for (int cbi = 0; cbi < ncb; ++cbi) {
         double* dst = part + (((int64_t)p * pl.CBG + cbi) * 128 + 32 * q + lane) * N;
         const uint32_t d = tmem + (uint32_t)(cbi * Cfg::kTN) + ((uint32_t)(32 * q) << 16);
+        float v[N];
 #pragma unroll
-        for (int c0 = 0; c0 < N; c0 += 16) {
-          float v[16];
-          tmem_ld16(d + c0, v);
+        for (int c0 = 0; c0 < N; c0 += 16) tmem_ld16(d + c0, *reinterpret_cast<float(*)[16]>(v + c0));
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&acc_empty[cbi]);  // block cbi may take the next chunk
 #pragma unroll
-          for (int j = 0; j < 16; ++j) dst[c0 + j] = ch == 0 ? (double)v[j] : dst[c0 + j] + (double)v[j];
-        }
+        for (int j = 0; j < N; ++j) dst[j] = ch == 0 ? (double)v[j] : dst[j] + (double)v[j];
       }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(acc_empty);
     }
     if (nch == 0) {  // no rows: zero partial
       for (int cbi = 0; cbi < ncb; ++cbi) {
@@ -714,27 +670,12 @@ template <int N>
 void launch_aty(Ctx& c, const DenseA& A, const float* hi, const float* lo, int64_t Kpad, const AtyPlan& pl,
                 double* part) {
   using Cfg = AtyCfg<N>;
-  // n ≡ 0 (mod 32): the tile is one 3-D box (dims: 32 columns, rows, column
-  // groups of 32) — no reads past a row's n columns; otherwise four 2-D boxes
-  const int a3d = (A.n % 32 == 0) ? 1 : 0;
-  CUtensorMap tA;
-  if (a3d) {
-    cuuint64_t dims[3] = {32, (cuuint64_t)A.m, (cuuint64_t)(A.n / 32)};
-    cuuint64_t strides[2] = {(cuuint64_t)A.lda * 4, 128};
-    cuuint32_t box[3] = {32, 32, 4};
-    cuuint32_t estr[3] = {1, 1, 1};
-    CUresult r = get_encode()(&tA, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<void*>(A.a), dims, strides, box,
-                              estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B,
-                              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    RPCA_REQUIRE(r == CUDA_SUCCESS, RPCA_E_CUDA, "cuTensorMapEncodeTiled(f32, 3-D) failed (%d)", (int)r);
-  } else {
-    tA = tmap_f32(A.a, A.n, A.m, A.lda, 32, 32, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
-  }
+  const CUtensorMap tA = tmap_f32(A.a, A.n, A.m, A.lda, 128, 32, CU_TENSOR_MAP_SWIZZLE_NONE);
   const CUtensorMap tH = tmap_f32(hi, Kpad, N, Kpad, 32, N);
   const CUtensorMap tL = tmap_f32(lo, Kpad, N, Kpad, 32, N);
   ensure_smem((const void*)aty_f32_tc_kernel<N>, Cfg::kSmem);
   prof_pre(c);
-  aty_f32_tc_kernel<N><<<(unsigned)(pl.Gc * pl.Pg), kThreadsTC, Cfg::kSmem, c.stream>>>(tA, tH, tL, pl, a3d, part);
+  aty_f32_tc_kernel<N><<<(unsigned)(pl.Gc * pl.Pg), kThreadsAty, Cfg::kSmem, c.stream>>>(tA, tH, tL, pl, part);
   RPCA_CHECK_LAUNCH();
   count_launch(c, 1, c.tag ? c.tag : "aty_f32_tc");
 }
