@@ -249,7 +249,9 @@ Split make_split(Ctx& c, const DenseA& A) {
   Split sp;
   sp.cpc = cdiv(A.m, BR);
   sp.U = cdiv(A.n, BN) * sp.cpc;
-  sp.P = std::min<int64_t>(c.num_sms, sp.U);
+  // ≥ 16 units (512 KB of A) per CTA: small passes would otherwise spend
+  // more in the reduction of many partials than in the pass
+  sp.P = std::min<int64_t>({(int64_t)c.num_sms, sp.U, std::max<int64_t>(1, cdiv(sp.U, 16))});
   return sp;
 }
 

@@ -324,6 +324,9 @@ void launch_ax_tma(Ctx& c, const DenseA& A, const double* Xp, int l, const doubl
   sp.KB = KB;
   sp.U = ntiles * KB;
   sp.P = std::min<int64_t>({sp.U, (int64_t)c.num_sms, ntiles * 16});  // a tile spans ≤ ~17 CTAs (fixup ≤ 32)
+  // small passes (A mostly L2-resident, microseconds of work): ≥ 16 units
+  // (512 KB of A) per CTA, so the fixup does not cost more than it saves
+  sp.P = std::min<int64_t>(sp.P, std::max<int64_t>(1, cdiv(sp.U, 16)));
   // whole tiles when they balance already or K is short (the thin-block
   // products: K = l ≤ 64) — splitting those would only add fixup launches
   if (ntiles % sp.P == 0 || KB < 8) sp.P = std::min<int64_t>(ntiles, c.num_sms);
