@@ -94,6 +94,16 @@ __device__ __forceinline__ void tmem_st32(uint32_t addr, const float (&v)[32]) {
   asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
 }
 
+// this thread's 16 consecutive TMEM columns of its lane ← v (no wait)
+__device__ __forceinline__ void tmem_st16_nowait(uint32_t addr, const float (&v)[16]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(
+          addr),
+      "f"(v[0]), "f"(v[1]), "f"(v[2]), "f"(v[3]), "f"(v[4]), "f"(v[5]), "f"(v[6]), "f"(v[7]), "f"(v[8]), "f"(v[9]),
+      "f"(v[10]), "f"(v[11]), "f"(v[12]), "f"(v[13]), "f"(v[14]), "f"(v[15])
+      : "memory");
+}
+
 __device__ __forceinline__ void mma_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
                : "memory");
@@ -365,10 +375,12 @@ struct AtyCfg {
   static constexpr int kSlot0 = 512 - 64 * kNS;
   static constexpr int kMaxCB = kSlot0 / kTN;
 };
-constexpr int kThreadsAty = 320;  // 10 warps: producer, MMA, 4 split, 4 epilogue
+constexpr int kSplitWarps = 8;    // two per TMEM lane quarter, 16 rows of the tile each
+constexpr int kThreadsAty = 32 * (2 + kSplitWarps + 4);  // producer, MMA, split, 4 epilogue
 
-// warps: 0 TMA producer, 1 MMA issuer, 2-5 split (A → A_hi, A_lo in TMEM),
-// 6-9 epilogue (fp64 flush per accumulation chunk).  Every product reads its
+// warps: 0 TMA producer, 1 MMA issuer, 2-9 split (A → A_hi, A_lo in TMEM;
+// warps w and w+4 share a TMEM lane quarter and take 16 rows each), 10-13
+// epilogue (fp64 flush per accumulation chunk).  Every product reads its
 // A operand from TMEM (the "TS" form) and only Yᵀ from shared memory: per
 // 16 KB A tile the SM moves 16 KB (TMA) + 16 KB (split reads) + 24 KB (three
 // N-wide Yᵀ operands per k-step) through shared memory, not 88 KB as with the
@@ -384,10 +396,10 @@ __global__ void __launch_bounds__(kThreadsAty, 1)
   uint8_t* smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
   uint8_t* ybuf = smem + S * kTileBytes;
   uint64_t* full = reinterpret_cast<uint64_t*>(ybuf + Cfg::kYBytes);
-  uint64_t* empty = full + S;        // 4 split warps (tile read into registers)
+  uint64_t* empty = full + S;        // kSplitWarps (tile read into registers)
   uint64_t* yfull = empty + S;       // [YS]
   uint64_t* yempty = yfull + YS;     // [YS] MMA commit
-  uint64_t* afull = yempty + YS;     // [NS] 4 split warps (A_hi, A_lo in TMEM)
+  uint64_t* afull = yempty + YS;     // [NS] kSplitWarps (A_hi, A_lo in TMEM)
   uint64_t* tfree = afull + NS;      // [NS] MMA commit
   uint64_t* acc_full = tfree + NS;   // MMA commit
   uint64_t* acc_empty = acc_full + 1;  // [kMaxCB] 4 epilogue warps (that block's accumulator read out)
@@ -401,14 +413,14 @@ __global__ void __launch_bounds__(kThreadsAty, 1)
   if (threadIdx.x == 0) {
     for (int s = 0; s < S; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 4);
+      mbar_init(&empty[s], kSplitWarps);
     }
     for (int y = 0; y < YS; ++y) {
       mbar_init(&yfull[y], 1);
       mbar_init(&yempty[y], 1);
     }
     for (int a = 0; a < NS; ++a) {
-      mbar_init(&afull[a], 4);
+      mbar_init(&afull[a], kSplitWarps);
       mbar_init(&tfree[a], 1);
     }
     mbar_init(acc_full, 1);
@@ -431,20 +443,24 @@ __global__ void __launch_bounds__(kThreadsAty, 1)
     prefetch_tmap(&tmYl);
     Ring<S> rg;
     Ring<YS> ry;
+    // A is streamed once: evict-first, so it does not push out the Yᵀ chunks
+    // the other column-block groups re-read from L2 (evict-last)
+    const uint64_t pol_a = policy_evict_first(), pol_y = policy_evict_last();
     for (int64_t rc = rb; rc < re; ++rc, ry.next()) {
       mbar_wait(&yempty[ry.s], ry.ph ^ 1u);
       uint8_t* yb = ybuf + ry.s * 2 * Cfg::kX;
       if (leader) {
         mbar_arrive_expect_tx(&yfull[ry.s], 2 * Cfg::kX);
-        tma_load_2d(yb, &tmYh, (int32_t)(rc * 32), 0, &yfull[ry.s]);
-        tma_load_2d(yb + Cfg::kX, &tmYl, (int32_t)(rc * 32), 0, &yfull[ry.s]);
+        tma_load_2d_hint(yb, &tmYh, (int32_t)(rc * 32), 0, &yfull[ry.s], pol_y);
+        tma_load_2d_hint(yb + Cfg::kX, &tmYl, (int32_t)(rc * 32), 0, &yfull[ry.s], pol_y);
       }
       __syncwarp();
       for (int cbi = 0; cbi < ncb; ++cbi, rg.next()) {
         mbar_wait(&empty[rg.s], rg.ph ^ 1u);
         if (leader) {  // one box: 32 rows × 128 columns, row-major, no swizzle
           mbar_arrive_expect_tx(&full[rg.s], kTileBytes);
-          tma_load_2d(smem + rg.s * kTileBytes, &tmA, (int32_t)((cb0 + cbi) * 128), (int32_t)(rc * 32), &full[rg.s]);
+          tma_load_2d_hint(smem + rg.s * kTileBytes, &tmA, (int32_t)((cb0 + cbi) * 128), (int32_t)(rc * 32),
+                           &full[rg.s], pol_a);
         }
         __syncwarp();
       }
@@ -491,8 +507,9 @@ __global__ void __launch_bounds__(kThreadsAty, 1)
       if (kin == 0) chph ^= 1u;
       if (++kin == RC) kin = 0;
     }
-  } else if (warp < 6) {  // ---------------------------------------- split: A → A_hi, A_lo in TMEM
+  } else if (warp < 2 + kSplitWarps) {  // ------------------------- split: A → A_hi, A_lo in TMEM
     const int q = warp & 3;        // this warp's TMEM lane quarter
+    const int h = (warp - 2) >> 2;  // which 16 rows of the tile
     const int t = 32 * q + lane;   // column of the block = TMEM lane
     const int64_t total = (re - rb) * ncb;
     const uint32_t lane_off = (uint32_t)(32 * q) << 16;
@@ -500,23 +517,24 @@ __global__ void __launch_bounds__(kThreadsAty, 1)
     Ring<NS> rt;
     for (int64_t i = 0; i < total; ++i, rg.next(), rt.next()) {
       mbar_wait(&full[rg.s], rg.ph);
-      const float* tile = reinterpret_cast<const float*>(smem + rg.s * kTileBytes) + t;
-      float hi[32], lo[32];
+      const float* tile = reinterpret_cast<const float*>(smem + rg.s * kTileBytes) + 16 * h * 128 + t;
+      float hi[16], lo[16];
 #pragma unroll
-      for (int rho = 0; rho < 32; ++rho) hi[rho] = tile[rho * 128];  // a warp reads 128 contiguous bytes
+      for (int rho = 0; rho < 16; ++rho) hi[rho] = tile[rho * 128];  // a warp reads 128 contiguous bytes
       __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[rg.s]);  // the tile is in registers: the stage is free
+      if (lane == 0) mbar_arrive(&empty[rg.s]);  // the rows are in registers: the stage may be refilled
 #pragma unroll
-      for (int rho = 0; rho < 32; ++rho) {
+      for (int rho = 0; rho < 16; ++rho) {
         const float a = hi[rho];
         hi[rho] = __uint_as_float(__float_as_uint(a) & 0xFFFFE000u);
         lo[rho] = a - hi[rho];
       }
       mbar_wait(&tfree[rt.s], rt.ph ^ 1u);
       tc_fence_after();
-      const uint32_t at = tmem + lane_off + (uint32_t)(Cfg::kSlot0 + 64 * rt.s);
-      tmem_st32(at, hi);
-      tmem_st32(at + 32, lo);
+      const uint32_t at = tmem + lane_off + (uint32_t)(Cfg::kSlot0 + 64 * rt.s + 16 * h);
+      tmem_st16_nowait(at, hi);
+      tmem_st16_nowait(at + 32, lo);
+      asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&afull[rt.s]);

@@ -46,11 +46,16 @@ constexpr int kWarps = kThreads / 32;
 constexpr int leaf_rows_per_thread(int LP) { return LP <= 8 ? 4 : (LP <= 16 ? 2 : 1); }
 constexpr int tree_rows_per_thread(int LP) { return LP <= 8 ? 4 : (LP <= 32 ? 2 : 1); }
 
+// two CTAs per SM (registers capped at 128) while a thread's rows fit
+#ifndef LU_TWO_BLOCK_MAX
+#define LU_TWO_BLOCK_MAX 32
+#endif
+
 template <int LP, int RR>
 struct SelCfg {
   static constexpr int R = RR;
   static constexpr int kCap = kThreads * R;  // rows per CTA
-  static constexpr int kMinBlocks = R * LP <= 32 ? 2 : 1;
+  static constexpr int kMinBlocks = R * LP <= LU_TWO_BLOCK_MAX ? 2 : 1;
 };
 
 // Pivot key of a value: the high word of |v| (11 exponent + 20 mantissa bits)
