@@ -7,5 +7,3 @@ import json,sys
 d=json.loads(sys.stdin.read()); print(d['config']['workload'][:3], 'ms', round(d['ms_per_step'],3), 'roof', d['roofline']['kernel'], d['roofline']['achieved'], d['roofline']['frac'], 'cpu', d.get('cpu_baseline'))"
 done
 timeout 600 python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/bench_ref.log 2>&1; echo "ref rc=$?"; tail -1 gpurun_out/bench_ref.log
-timeout 900 ncu --set full --import-source on --clock-control none -k regex:"aty_f64_tma" -c 1 -o gpurun_out/prof/C2_aty python bench.py --config C2 --steps 1 --warmup 0 --no-e2e --no-cpu-baseline > gpurun_out/ncu_C2aty.log 2>&1; echo "ncu aty rc=$?"
-timeout 900 ncu --set full --import-source on --clock-control none -k regex:"ax_f64_tma" -c 1 -o gpurun_out/prof/C2_ax python bench.py --config C2 --steps 1 --warmup 0 --no-e2e --no-cpu-baseline > gpurun_out/ncu_C2ax.log 2>&1; echo "ncu ax rc=$?"
