@@ -355,7 +355,7 @@ size_t ax_ws_bytes(const DenseA& A, int l) {
   Sizer s;
   s.add<double>(packx_elems(A.n, l));
   s.add<double>((size_t)kMaxSms * 2 * BM * ((l + 7) / 8 * 8));  // stream-K partial rows
-  return s.total;
+  return std::max(s.total, emu_eligible(A, l) ? emu_ws_bytes(A, l) : (size_t)0);
 }
 
 void dense_ax(Ctx& c, const DenseA& A, const double* X, int l, double* Y, Arena& ar, const double* cx) {
@@ -363,6 +363,10 @@ void dense_ax(Ctx& c, const DenseA& A, const double* X, int l, double* Y, Arena&
   if (A.m == 0) return;
   if (f32_tc_ok(A)) {
     dense_ax_f32(c, A, X, l, cx, Y, ar);  // centring folded into the epilogue
+    return;
+  }
+  if (!cx && c.emu_E && A.a == c.emu_A && emu_eligible(A, l)) {  // the driver's A, row exponents known
+    dense_ax_emu(c, A, c.emu_E, X, l, Y, ar);
     return;
   }
   if (cx && !tma_ok(A)) {  // generic kernel: the rank-1 correction as a separate thin pass

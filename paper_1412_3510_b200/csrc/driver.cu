@@ -421,6 +421,26 @@ const double* adj(Ctx& c, const Op& F, const double* Y, int l, double* Z, double
   return nullptr;
 }
 
+// For the duration of a driver call: the row exponents of a dense fp64 A
+// whose A·X passes go to the int8-digit emulation (dense_ax_emu.cu) — one
+// extra read of A, worth it from two A·X passes on.  RPCA_NO_EMU=1 keeps the
+// fp64 tensor-core passes.
+struct EmuScope {
+  Ctx& c;
+  EmuScope(Ctx& c_, const MatV& A, int l, int ax_passes, Arena& ar) : c(c_) {
+    static const bool off = getenv("RPCA_NO_EMU") != nullptr;
+    if (off || A.csr || ax_passes < 2 || !emu_eligible(A.d, l)) return;
+    int* E = ar.get<int>(A.d.m);
+    row_exponents(c, A.d, E);
+    c.emu_E = E;
+    c.emu_A = A.d.a;
+  }
+  ~EmuScope() {
+    c.emu_E = nullptr;
+    c.emu_A = nullptr;
+  }
+};
+
 size_t op_ws(Ctx& c, const MatV& A, int l) {
   const size_t small = (size_t)(cdiv(std::max(A.m, A.n), 2048) + 4) * kMaxL * 8 * 2 + 65536;
   if (A.csr) return small;
@@ -539,6 +559,7 @@ void pca(Ctx& c, const rpca_mat* Am, int64_t k, int raw, int its, int64_t l, uin
   sz.add<double>(2 * kMaxL);  // column means
   sz.add<double>(std::max(nin, nout) * k);  // V-side temp
   sz.add<double>(k);                        // signs
+  sz.add<int>(ml + 16);                     // row exponents (EmuScope)
   if (out_host) {
     sz.add<char>((size_t)ml * ldu * osz);
     sz.add<char>((size_t)n * ldv * osz);
@@ -560,6 +581,7 @@ void pca(Ctx& c, const rpca_mat* Am, int64_t k, int raw, int its, int64_t l, uin
 
   execute(c, kh.h, graphable, [&] {
     const MatV dA = device_view(c, Am, ar);
+    EmuScope emu(c, dA, L, trans ? its + 2 : its + 1, ar);
     double* Zb = ar.get<double>(nin * l);
     double* Yb = ar.get<double>(nout * l);
     double* R = ar.get<double>(l * l);
@@ -654,6 +676,7 @@ void eigens(Ctx& c, const rpca_mat* Am, int64_t k, int its, int64_t l, uint64_t 
   sz.add<double>(2 * P * pad * l + 2 * ml * l);
   sz.add<double>(6 * l * l + 8 * l + 16);
   sz.add<double>(ml * k + k);
+  sz.add<int>(ml + 16);  // row exponents (EmuScope)
   if (out_host) {
     sz.add<char>((size_t)ml * ldu * osz);
     sz.add<char>((size_t)k * osz);
@@ -697,6 +720,7 @@ void eigens(Ctx& c, const rpca_mat* Am, int64_t k, int its, int64_t l, uint64_t 
   double* Qfin = ((its & 1) ? Qb : Qa) + slot;  // this rank's final Q after the loop's swaps
   execute(c, kh.h, graphable, [&] {
     const MatV dA = device_view(c, Am, ar);
+    EmuScope emu(c, dA, L, its + 2, ar);
     double* Qf = Qa;  // gathered Q
     double* Qo = Qb;  // the other gather buffer
     double* side = ar.get<double>(ml * k);

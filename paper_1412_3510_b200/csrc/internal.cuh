@@ -107,6 +107,10 @@ struct Ctx {
     void* plan_t = nullptr;
   } tcache;
   cudaEvent_t fence_in = nullptr, fence_out = nullptr;
+  // fp64 A·X on the int8 tensor cores (dense_ax_emu.cu): the row exponents of
+  // the driver call's A, valid while that call runs (EmuScope)
+  const int* emu_E = nullptr;
+  const void* emu_A = nullptr;
   Arena arena(size_t bytes);  // ensures capacity, returns an arena over the workspace
 };
 
@@ -188,6 +192,11 @@ struct DenseA {
 size_t ax_ws_bytes(const DenseA& A, int l);
 // Y = A·X [− 1·cxᵀ]  (cx = c·X, the centring correction of PAPER.md:430; may be NULL)
 void dense_ax(Ctx& c, const DenseA& A, const double* X, int l, double* Y, Arena& ar, const double* cx = nullptr);
+// dense_ax_emu.cu — fp64 A·X as int8-digit products on tcgen05 (Ozaki scheme I)
+bool emu_eligible(const DenseA& A, int l);
+void row_exponents(Ctx& c, const DenseA& A, int* E);
+size_t emu_ws_bytes(const DenseA& A, int l);
+void dense_ax_emu(Ctx& c, const DenseA& A, const int* E, const double* X, int l, double* Y, Arena& ar);
 size_t aty_ws_bytes(Ctx& c, const DenseA& A, int l);
 // Z (n×l) = Aᵀ·(Y − 1·ymeanᵀ) [− cmean ⊗ colsum(Y)] (cmean, ymean may be NULL)
 void dense_aty(Ctx& c, const DenseA& A, const double* Y, int l, const double* cmean, double* Z, Arena& ar,
