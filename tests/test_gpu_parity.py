@@ -220,6 +220,28 @@ def test_pca_shapes(m, n, k, l, its, raw):
     compare(res, oracle.pca(An, k, raw=raw, its=its, l=l, seed=3), k)
 
 
+# fp64 dense with l > 24 takes the int8-digit emulation of A·X (dense_ax_emu.cu):
+# ragged m and n (not multiples of 128 / 32), centring, the transposed path
+# (m < n), and rows whose magnitudes span 10^±150 plus a zero row (the per-row
+# exponent of the digit planes)
+@pytest.mark.parametrize("m,n,k,l,its,raw,spread", [(3001, 777, 28, 30, 2, True, False),
+                                                    (2500, 1200, 40, 48, 1, False, False),
+                                                    (1000, 3001, 25, 27, 2, True, False),
+                                                    (2049, 513, 30, 32, 2, True, True)])
+def test_pca_emu_path(m, n, k, l, its, raw, spread):
+    g = torch.Generator(device="cuda").manual_seed(m * 3 + n)
+    sig = torch.exp(-torch.arange(min(m, n), dtype=torch.float64) / 6.0)
+    A = synth.synth_dense(m, n, sig, seed=m * 5 + n, device=dev()).contiguous()
+    if not raw:
+        A += torch.rand(n, generator=g, device=dev(), dtype=torch.float64) * 10 - 5
+    if spread:
+        A *= 10.0 ** torch.linspace(-150, 150, m, device=dev(), dtype=torch.float64)[:, None]
+        A[m // 3] = 0.0
+    An = A.cpu().numpy()
+    res = rp.pca(A, k, raw=raw, its=its, l=l, seed=5)
+    compare(res, oracle.pca(An, k, raw=raw, its=its, l=l, seed=5), k)
+
+
 def test_pca_propack_diagonal():
     """the matrices PROPACK gets wrong; zero pivots on the GPU too."""
     A = synth.propack_diag(30).to(dev())
