@@ -55,8 +55,9 @@ struct EmuCfg {
   static constexpr int kStage = kATile + kB;
   static constexpr int kStages = (212 * 1024) / kStage > 6 ? 6 : (212 * 1024) / kStage;
   static constexpr int kSmem = kStages * kStage + 1024 + 512;
-  static constexpr int kSlot0 = kNc;             // then two digit sets of 8·kDigits columns
+  static constexpr int kSlot0 = kNc;             // then kSets digit sets of 8·kDigits columns
   static constexpr int kSet = 8 * kDigits;
+  static constexpr int kSets = (512 - kNc) / kSet >= 3 ? 3 : 2;
   static_assert(kNc + 2 * kSet <= 512, "TMEM: levels + two digit sets");
 };
 
@@ -211,7 +212,7 @@ template <int LPn>
 __global__ void __launch_bounds__(kThreadsEmu, 1)
     ax_f64_emu_kernel(const __grid_constant__ CUtensorMap tmA, const int8_t* __restrict__ Xs,
                       const int* __restrict__ E, const int* __restrict__ Gf, int64_t m, int l, int64_t ntiles,
-                      int KB, double* __restrict__ Y) {
+                      int KB, double* __restrict__ Y, double* __restrict__ part) {
   using Cfg = EmuCfg<LPn>;
   constexpr int S = Cfg::kStages;
   constexpr int KCH = kKChunkEmu / 32;  // k-blocks per int32 accumulation
@@ -219,20 +220,24 @@ __global__ void __launch_bounds__(kThreadsEmu, 1)
   uint8_t* smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + S * Cfg::kStage);
   uint64_t* empty = full + S;       // split warps (A read) + MMA commit (X digits read)
-  uint64_t* sfull = empty + S;      // [2] split warps (digits in TMEM)
-  uint64_t* sfree = sfull + 2;      // [2] MMA commit
-  uint64_t* acc_full = sfree + 2;   // MMA commit
+  uint64_t* sfull = empty + S;      // [kSets] split warps (digits in TMEM)
+  uint64_t* sfree = sfull + Cfg::kSets;  // [kSets] MMA commit
+  uint64_t* acc_full = sfree + Cfg::kSets;  // MMA commit
   uint64_t* acc_empty = acc_full + 1;  // 4 epilogue warps
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 1);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // units (tile, K-chunk of KCH k-blocks), dealt round-robin over the CTAs:
+  // with several K-chunks per tile every unit writes its own partial (part,
+  // 128 × l fp64) and ax_emu_reduce_kernel sums them in chunk order
   const int nkc = (KB + KCH - 1) / KCH;
+  const int64_t nunits = ntiles * nkc;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < S; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], kSplitW + 1);
     }
-    for (int b = 0; b < 2; ++b) {
+    for (int b = 0; b < Cfg::kSets; ++b) {
       mbar_init(&sfull[b], kSplitW);
       mbar_init(&sfree[b], 1);
     }
@@ -253,8 +258,10 @@ __global__ void __launch_bounds__(kThreadsEmu, 1)
     const bool leader = elect();
     prefetch_tmap(&tmA);
     Ring<S> rg;
-    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x)
-      for (int kb = 0; kb < KB; ++kb, rg.next()) {
+    for (int64_t un = blockIdx.x; un < nunits; un += gridDim.x) {
+      const int64_t tile = un / nkc;
+      const int kc = (int)(un - tile * nkc);
+      for (int kb = kc * KCH; kb < KB && kb < (kc + 1) * KCH; ++kb, rg.next()) {
         mbar_wait(&empty[rg.s], rg.ph ^ 1u);
         uint8_t* st = smem + rg.s * Cfg::kStage;
         if (leader) {
@@ -265,14 +272,18 @@ __global__ void __launch_bounds__(kThreadsEmu, 1)
         }
         __syncwarp();
       }
+    }
   } else if (warp == 1) {  // ------------------------------------------- MMA issuer
     const bool leader = elect();
     Ring<S> rg;
-    Ring<2> rb;
+    Ring<Cfg::kSets> rb;
     int64_t u = 0;  // units issued
-    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x)
-      for (int kb = 0; kb < KB; ++kb, rg.next(), rb.next()) {
-        const int kin = kb % KCH;
+    for (int64_t un = blockIdx.x; un < nunits; un += gridDim.x, ++u) {
+      const int64_t tile = un / nkc;
+      const int kc = (int)(un - tile * nkc);
+      const int kb0 = kc * KCH, kb1 = KB < kb0 + KCH ? KB : kb0 + KCH;
+      for (int kb = kb0; kb < kb1; ++kb, rg.next(), rb.next()) {
+        const int kin = kb - kb0;
         if (kin == 0) {  // the level accumulators of the last unit must have been read out
           mbar_wait(acc_empty, (uint32_t)(u & 1) ^ 1u);
           fence_after();
@@ -295,22 +306,24 @@ __global__ void __launch_bounds__(kThreadsEmu, 1)
           }
           commit(&sfree[rb.s]);
           commit(&empty[rg.s]);
-          if (kin == KCH - 1 || kb == KB - 1) commit(acc_full);
+          if (kb == kb1 - 1) commit(acc_full);
         }
         __syncwarp();
-        if (kin == KCH - 1 || kb == KB - 1) ++u;
       }
+    }
   } else if (warp < 2 + kSplitW) {  // -------------------------------- split: digits → TMEM
     const int q = warp & 3;
     const int h = (warp - 2) >> 2;  // which 16 k of the 32 (box h of the stage)
     const int t = 32 * q + lane;    // tile row = TMEM lane
     const uint32_t lane_off = (uint32_t)(32 * q) << 16;
     Ring<S> rg;
-    Ring<2> rb;
-    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    Ring<Cfg::kSets> rb;
+    for (int64_t un = blockIdx.x; un < nunits; un += gridDim.x) {
+      const int64_t tile = un / nkc;
+      const int kc = (int)(un - tile * nkc);
       const int64_t row = tile * 128 + t;
       const double scale = scale_of(row < m ? E[row] : 0);
-      for (int kb = 0; kb < KB; ++kb, rg.next(), rb.next()) {
+      for (int kb = kc * KCH; kb < KB && kb < (kc + 1) * KCH; ++kb, rg.next(), rb.next()) {
         mbar_wait(&full[rg.s], rg.ph);
         const uint8_t* st = smem + rg.s * Cfg::kStage + h * 16384 + t * 128;
         uint32_t w[4][kDigits];  // 4-element group g (k = 16h + 4g .. +3), plane s
@@ -346,10 +359,11 @@ __global__ void __launch_bounds__(kThreadsEmu, 1)
     const int q = warp & 3;
     const int t = 32 * q + lane;
     int64_t u = 0;
-    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    for (int64_t un = blockIdx.x; un < nunits; un += gridDim.x, ++u) {
+      const int64_t tile = un / nkc;
       const int64_t row = tile * 128 + t;
       const int Er = row < m ? E[row] : 0;
-      for (int kc = 0; kc < nkc; ++kc, ++u) {
+      {
         mbar_wait(acc_full, (uint32_t)(u & 1));
         fence_after();
 #pragma unroll
@@ -371,7 +385,7 @@ __global__ void __launch_bounds__(kThreadsEmu, 1)
             for (int j = 0; j < 16; ++j) s[j] = fma(s[j], 0x1p-8, (double)(int)v[j]);
           }
           if (row < m) {
-            double* y = Y + row * l;
+            double* y = nkc == 1 ? Y + row * l : part + (un * 128 + t) * l;
 #pragma unroll
             for (int j = 0; j < 16; ++j)
               if (c0 + j < l) {
@@ -379,8 +393,7 @@ __global__ void __launch_bounds__(kThreadsEmu, 1)
                 const int e = Er + Gj - 12;
                 double v = (e >= -1022 && e <= 1023) ? s[j] * pow2(e) : ldexp(s[j], e);
                 if (Er >= kNonFinite || Gj >= kNonFinite) v = __longlong_as_double(0x7FF8000000000000LL);
-                if (kc == 0) y[c0 + j] = v;
-                else y[c0 + j] += v;
+                y[c0 + j] = v;
               }
           }
         }
@@ -394,6 +407,20 @@ __global__ void __launch_bounds__(kThreadsEmu, 1)
   if (warp == 1) {
     fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+  }
+}
+
+// Y[row][j] = Σ_{kc ascending} part[tile·nkc + kc][row mod 128][j]
+__global__ void ax_emu_reduce_kernel(const double* __restrict__ part, int64_t m, int l, int nkc,
+                                     double* __restrict__ Y) {
+  const int64_t total = m * l;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t row = idx / l, tile = row >> 7;
+    const int64_t off = ((row & 127) * l) + (idx - row * l);
+    double s = 0.0;
+    for (int kc = 0; kc < nkc; ++kc) s += part[(tile * nkc + kc) * 128 * l + off];
+    Y[idx] = s;
   }
 }
 
@@ -412,7 +439,8 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 int lpn_of(int l) { return (l + 15) / 16 * 16; }
 
 template <int LPn>
-void launch_emu(Ctx& c, const DenseA& A, const int8_t* Xs, const int* E, const int* Gf, int l, int KB, double* Y) {
+void launch_emu(Ctx& c, const DenseA& A, const int8_t* Xs, const int* E, const int* Gf, int l, int KB, double* Y,
+                double* part) {
   using Cfg = EmuCfg<LPn>;
   CUtensorMap tm;
   cuuint64_t dims[2] = {(cuuint64_t)A.n, (cuuint64_t)A.m};
@@ -425,11 +453,18 @@ void launch_emu(Ctx& c, const DenseA& A, const int8_t* Xs, const int* E, const i
   RPCA_REQUIRE(r == CUDA_SUCCESS, RPCA_E_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
   ensure_smem((const void*)ax_f64_emu_kernel<LPn>, Cfg::kSmem);
   const int64_t ntiles = cdiv(A.m, 128);
-  const int grid = (int)std::min<int64_t>(ntiles, c.num_sms);
+  const int nkc = (int)cdiv(KB, kKChunkEmu / 32);
+  const int grid = (int)std::min<int64_t>(ntiles * nkc, c.num_sms);
   prof_pre(c);
-  ax_f64_emu_kernel<LPn><<<grid, kThreadsEmu, Cfg::kSmem, c.stream>>>(tm, Xs, E, Gf, A.m, l, ntiles, KB, Y);
+  ax_f64_emu_kernel<LPn><<<grid, kThreadsEmu, Cfg::kSmem, c.stream>>>(tm, Xs, E, Gf, A.m, l, ntiles, KB, Y, part);
   RPCA_CHECK_LAUNCH();
   count_launch(c, 1, c.tag ? c.tag : "ax_f64_emu");
+  if (nkc > 1) {
+    const unsigned g2 = (unsigned)std::min<int64_t>(cdiv(A.m * l, 256), (int64_t)c.num_sms * 8);
+    ax_emu_reduce_kernel<<<g2, 256, 0, c.stream>>>(part, A.m, l, nkc, Y);
+    RPCA_CHECK_LAUNCH();
+    count_launch(c, 1, "emu_reduce");
+  }
 }
 
 }  // namespace
@@ -453,6 +488,7 @@ size_t emu_ws_bytes(const DenseA& A, int l) {
   Sizer s;
   s.add<int>(64);
   s.add<int8_t>((size_t)cdiv(A.n, 32) * (lpn_of(l) == 32 ? EmuCfg<32>::kB : EmuCfg<48>::kB));
+  s.add<double>((size_t)cdiv(A.m, 128) * cdiv(A.n, kKChunkEmu) * 128 * l);  // per-unit partials
   return s.total;
 }
 
@@ -462,6 +498,8 @@ void dense_ax_emu(Ctx& c, const DenseA& A, const int* E, const double* X, int l,
   int* Gf = ar.get<int>(64);
   const int kB = LPn == 32 ? EmuCfg<32>::kB : EmuCfg<48>::kB;
   int8_t* Xs = ar.get<int8_t>((size_t)KB * kB);
+  const int64_t nkc = cdiv(KB, kKChunkEmu / 32);
+  double* part = nkc > 1 ? ar.get<double>((size_t)cdiv(A.m, 128) * nkc * 128 * l) : nullptr;
   RPCA_CUDA(cudaMemsetAsync(Gf, 0, sizeof(int) * 64, c.stream));
   {
     const int64_t total = A.n * (int64_t)l;
@@ -478,8 +516,8 @@ void dense_ax_emu(Ctx& c, const DenseA& A, const int* E, const double* X, int l,
     count_launch(c, 1, "emu_x_slices");
   }
   switch (LPn) {
-    case 32: launch_emu<32>(c, A, Xs, E, Gf, l, KB, Y); break;
-    default: launch_emu<48>(c, A, Xs, E, Gf, l, KB, Y); break;
+    case 32: launch_emu<32>(c, A, Xs, E, Gf, l, KB, Y, part); break;
+    default: launch_emu<48>(c, A, Xs, E, Gf, l, KB, Y, part); break;
   }
 }
 
