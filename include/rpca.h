@@ -167,6 +167,15 @@ rpca_status rpca_colmeans(rpca_ctx* ctx, const rpca_mat* A, double* c);
 rpca_status rpca_apply(rpca_ctx* ctx, const rpca_mat* A, const double* c, int adjoint, const double* X,
                        int64_t l, double* Y);
 
+/* ---- step a2 on the int8 tensor cores: Y (m_local×l) = A·X for a dense fp64
+ * A whose A·X passes rpca_pca / rpca_eigens emulate (24 < l ≤ 48, m ≥ 128,
+ * n ≥ 32): A and X split into 7 balanced base-256 digit planes with per-row /
+ * per-column exponents, 28 exact int8 products (Ozaki scheme I); error
+ * ≲ 2^-55·2^E_i·2^G_j per term, relative to the row / column maxima of A and
+ * X.  Reads A twice (row exponents, then the pass).  Non-finite
+ * entries give NaN rows / columns.  RPCA_E_NOTIMPL for other A or l.        */
+rpca_status rpca_apply_int8emu(rpca_ctx* ctx, const rpca_mat* A, const double* X, int64_t l, double* Y);
+
 /* ---- §8(a) step a3: LU renormalisation ("[Q,R]=lu(Q)") ---
  * In place: Y (m×l, m ≥ l) ← L with Y = L·U, L in the ORIGINAL row order
  * (unit lower triangular in the pivot rows, reading Q3).  Pivot rows are

@@ -17,7 +17,7 @@ import threading
 
 import torch
 
-__all__ = ["pca", "eigens", "diffsnorm", "omega", "apply", "colmeans", "lu_renorm", "qr", "small_svd",
+__all__ = ["pca", "eigens", "diffsnorm", "omega", "apply", "apply_int8emu", "colmeans", "lu_renorm", "qr", "small_svd",
            "launch_count", "library_path", "RPCAError", "CSR", "profile", "clear_cache", "comm_unique_id",
            "comm_init", "comm_init_torch", "VirtualGroup", "uniform_shard"]
 
@@ -86,6 +86,7 @@ def _load():
             "rpca_omega": [vp, u64, u32, i64, i64, i32, i32, dp],
             "rpca_colmeans": [vp, pm, dp],
             "rpca_apply": [vp, pm, dp, i32, dp, i64, dp],
+            "rpca_apply_int8emu": [vp, pm, dp, i64, dp],
             "rpca_lu_renorm": [vp, dp, i64, i64, dp, vp],
             "rpca_qr": [vp, dp, i64, i64, dp],
             "rpca_small_svd": [vp, dp, i64, i64, dp, dp, dp],
@@ -326,6 +327,19 @@ def apply(A: torch.Tensor, X: torch.Tensor, adjoint: bool = False, cmean: torch.
     Y = torch.empty(rows, l, dtype=torch.float64, device=A.device)
     mat, keep = _as_mat(A, m_total=m_total, row0=row0)
     _check(L.rpca_apply(h, C.byref(mat), _ptr(cmean), int(adjoint), _ptr(X), l, _ptr(Y)))
+    return Y
+
+
+def apply_int8emu(A: torch.Tensor, X: torch.Tensor, m_total=None, row0=0):
+    """Y = A·X through the int8-digit emulation of the fp64 product (the path
+    pca/eigens take for dense fp64 A with 24 < l ≤ 48); for tests and benches."""
+    L, h = _ctx(A.device)
+    X = X.contiguous()
+    assert X.dtype == torch.float64
+    l = X.shape[1]
+    Y = torch.empty(A.shape[0], l, dtype=torch.float64, device=A.device)
+    mat, keep = _as_mat(A, m_total=m_total, row0=row0)
+    _check(L.rpca_apply_int8emu(h, C.byref(mat), _ptr(X), l, _ptr(Y)))
     return Y
 
 

@@ -16,6 +16,7 @@ void diffsnorm(Ctx&, const rpca_mat*, int, const double*, int64_t, const double*
                int, uint64_t, double*);
 const char* last_error_cstr();
 void apply_step(Ctx&, const rpca_mat*, const double*, int, const double*, int64_t, double*);
+void apply_emu_step(Ctx&, const rpca_mat*, const double*, int64_t, double*);
 void colmeans_step(Ctx&, const rpca_mat*, double*);
 void clear_cache(Ctx&);
 }  // namespace rpca
@@ -238,6 +239,14 @@ rpca_status rpca_apply(rpca_ctx* c, const rpca_mat* A, const double* cm, int adj
   return guard([&] {
     DeviceScope ds(c->device);
     rpca::apply_step(*c, A, cm, adjoint, X, l, Y);
+  });
+}
+
+rpca_status rpca_apply_int8emu(rpca_ctx* c, const rpca_mat* A, const double* X, int64_t l, double* Y) {
+  if (!c || !A || !X || !Y) return RPCA_E_ARG;
+  return guard([&] {
+    DeviceScope ds(c->device);
+    rpca::apply_emu_step(*c, A, X, l, Y);
   });
 }
 

@@ -36,6 +36,8 @@
 // of every K-chunk, scale by 2^(E_i+G_j−12) and write / add Y.
 #include <cudaTypedefs.h>
 
+#include <type_traits>
+
 #include "internal.cuh"
 
 namespace rpca {
@@ -43,7 +45,11 @@ namespace {
 
 constexpr int kDigits = 7;                // digit planes per operand = levels kept
 constexpr int kKChunkEmu = 8192;          // products per int32 level sum
-constexpr int kSplitW = 8;                // split warps: two per TMEM lane quarter
+#ifndef EMU_SPLIT_WARPS
+#define EMU_SPLIT_WARPS 16
+#endif
+constexpr int kSplitW = EMU_SPLIT_WARPS;   // split warps: kSplitW/4 per TMEM lane quarter
+constexpr int kGroups = 32 / kSplitW;      // 4-element k groups per split warp and stage
 constexpr int kThreadsEmu = 32 * (2 + kSplitW + 4);  // producer, MMA, split, 4 epilogue
 constexpr int kATile = 128 * 32 * 8;      // fp64 A stage: 128 rows × 32 k
 
@@ -52,9 +58,14 @@ struct EmuCfg {
   static constexpr int kNc = kDigits * LPn;      // level accumulator columns
   static constexpr int kBraw = kDigits * LPn * 32;  // X planes of one 32-k block: 7·LPn rows × 32 B
   static constexpr int kB = (kBraw + 1023) / 1024 * 1024;  // stages stay 1024-aligned (SW128 TMA)
-  static constexpr int kStage = kATile + kB;
-  static constexpr int kStages = (212 * 1024) / kStage > 6 ? 6 : (212 * 1024) / kStage;
-  static constexpr int kSmem = kStages * kStage + 1024 + 512;
+  // separate rings: A tiles (released by the split warps once in registers)
+  // and X planes (released by the MMA commit), so A streams ahead of the MMAs
+#ifndef EMU_SB
+#define EMU_SB 8
+#endif
+  static constexpr int kStagesB = EMU_SB;
+  static constexpr int kStages = (210 * 1024 - kStagesB * kB) / kATile;  // A ring
+  static constexpr int kSmem = kStages * kATile + kStagesB * kB + 1024 + 512;
   static constexpr int kSlot0 = kNc;             // then kSets digit sets of 8·kDigits columns
   static constexpr int kSet = 8 * kDigits;
   static constexpr int kSets = (512 - kNc) / kSet >= 3 ? 3 : 2;
@@ -115,10 +126,10 @@ __device__ __forceinline__ double pow2(int e) { return __longlong_as_double((lon
 constexpr int kNonFinite = 4096;
 __host__ __device__ __forceinline__ int exp_of_field(int f) {
   if (f >= 2047) return kNonFinite;
-  const int e = f - 1022;
-  return e < -960 ? -960 : e;  // keeps 2^(62−E) a normal double; tinier values flush to digit 0
+  return f ? f - 1022 : -1021;  // f = 0: zeros and subnormals, all below 2^-1021
 }
-__device__ __forceinline__ double scale_of(int E) { return E >= kNonFinite ? 0.0 : pow2(62 - E); }
+// 2^(62−E), capped at 2^1022 (E < −960 needs the pre-scale 2^(−960−E) too)
+__device__ __forceinline__ double scale_of(int E) { return E >= kNonFinite ? 0.0 : pow2(E < -960 ? 1022 : 62 - E); }
 
 // U = trunc(a·scale) + 0x8080…80 (two 32-bit halves): byte p of U, top bit
 // flipped, is the balanced base-256 digit of weight 256^p
@@ -194,7 +205,8 @@ __global__ void x_slices_kernel(const double* __restrict__ X, int64_t K, int l, 
     const int64_t k = idx / LPn;
     const double x = (k < K && j < l) ? X[k * l + j] : 0.0;
     uint32_t lo, hi;
-    biased(x, scale_of(exp_of_field(j < l ? Gf[j] : 0)), lo, hi);
+    const int G = exp_of_field(j < l ? Gf[j] : 0);
+    biased(G < -960 ? x * pow2(-960 - G) : x, scale_of(G), lo, hi);
     const unsigned long long U = ((unsigned long long)hi << 32) | lo;
     const int64_t b = k >> 5;
     const int kk = (int)(k & 31);
@@ -214,13 +226,16 @@ __global__ void __launch_bounds__(kThreadsEmu, 1)
                       const int* __restrict__ E, const int* __restrict__ Gf, int64_t m, int l, int64_t ntiles,
                       int KB, double* __restrict__ Y, double* __restrict__ part) {
   using Cfg = EmuCfg<LPn>;
-  constexpr int S = Cfg::kStages;
+  constexpr int S = Cfg::kStages, SB = Cfg::kStagesB;
   constexpr int KCH = kKChunkEmu / 32;  // k-blocks per int32 accumulation
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + S * Cfg::kStage);
-  uint64_t* empty = full + S;       // split warps (A read) + MMA commit (X digits read)
-  uint64_t* sfull = empty + S;      // [kSets] split warps (digits in TMEM)
+  uint8_t* bring = smem + S * kATile;  // X-plane ring
+  uint64_t* full = reinterpret_cast<uint64_t*>(bring + SB * Cfg::kB);
+  uint64_t* empty = full + S;       // split warps (A read into registers)
+  uint64_t* bfull = empty + S;      // [SB] X planes landed
+  uint64_t* bempty = bfull + SB;    // [SB] MMA commit
+  uint64_t* sfull = bempty + SB;    // [kSets] split warps (digits in TMEM)
   uint64_t* sfree = sfull + Cfg::kSets;  // [kSets] MMA commit
   uint64_t* acc_full = sfree + Cfg::kSets;  // MMA commit
   uint64_t* acc_empty = acc_full + 1;  // 4 epilogue warps
@@ -235,7 +250,11 @@ __global__ void __launch_bounds__(kThreadsEmu, 1)
   if (threadIdx.x == 0) {
     for (int s = 0; s < S; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], kSplitW + 1);
+      mbar_init(&empty[s], kSplitW);
+    }
+    for (int s = 0; s < SB; ++s) {
+      mbar_init(&bfull[s], 1);
+      mbar_init(&bempty[s], 1);
     }
     for (int b = 0; b < Cfg::kSets; ++b) {
       mbar_init(&sfull[b], kSplitW);
@@ -258,24 +277,30 @@ __global__ void __launch_bounds__(kThreadsEmu, 1)
     const bool leader = elect();
     prefetch_tmap(&tmA);
     Ring<S> rg;
+    Ring<SB> rx;
     for (int64_t un = blockIdx.x; un < nunits; un += gridDim.x) {
       const int64_t tile = un / nkc;
       const int kc = (int)(un - tile * nkc);
-      for (int kb = kc * KCH; kb < KB && kb < (kc + 1) * KCH; ++kb, rg.next()) {
+      for (int kb = kc * KCH; kb < KB && kb < (kc + 1) * KCH; ++kb, rg.next(), rx.next()) {
         mbar_wait(&empty[rg.s], rg.ph ^ 1u);
-        uint8_t* st = smem + rg.s * Cfg::kStage;
+        uint8_t* st = smem + rg.s * kATile;
         if (leader) {
-          mbar_arrive_expect_tx(&full[rg.s], kATile + Cfg::kBraw);
+          mbar_arrive_expect_tx(&full[rg.s], kATile);
           tma_load_2d(st, &tmA, kb * 32, (int32_t)(tile * 128), &full[rg.s]);
           tma_load_2d(st + 16384, &tmA, kb * 32 + 16, (int32_t)(tile * 128), &full[rg.s]);
-          bulk_load(st + kATile, Xs + (int64_t)kb * Cfg::kB, Cfg::kBraw, &full[rg.s]);
+        }
+        __syncwarp();
+        mbar_wait(&bempty[rx.s], rx.ph ^ 1u);
+        if (leader) {
+          mbar_arrive_expect_tx(&bfull[rx.s], Cfg::kBraw);
+          bulk_load(bring + rx.s * Cfg::kB, Xs + (int64_t)kb * Cfg::kB, Cfg::kBraw, &bfull[rx.s]);
         }
         __syncwarp();
       }
     }
   } else if (warp == 1) {  // ------------------------------------------- MMA issuer
     const bool leader = elect();
-    Ring<S> rg;
+    Ring<SB> rg;
     Ring<Cfg::kSets> rb;
     int64_t u = 0;  // units issued
     for (int64_t un = blockIdx.x; un < nunits; un += gridDim.x, ++u) {
@@ -289,11 +314,12 @@ __global__ void __launch_bounds__(kThreadsEmu, 1)
           fence_after();
         }
         mbar_wait(&sfull[rb.s], rb.ph);
-        mbar_wait(&full[rg.s], rg.ph);
+        mbar_wait(&bfull[rg.s], rg.ph);
         fence_after();
-        const uint32_t xb = smem_u32(smem + rg.s * Cfg::kStage + kATile);
+        const uint32_t xb = smem_u32(bring + rg.s * Cfg::kB);
         const uint32_t ad = tmem + (uint32_t)(Cfg::kSlot0 + Cfg::kSet * rb.s);
         if (leader) {
+#ifndef EMU_NO_MMA
 #pragma unroll
           for (int p = 0; p < kDigits; ++p) {
             const int np = (kDigits - p) * LPn;  // X planes t = 0..6−p, levels p..6
@@ -304,8 +330,9 @@ __global__ void __launch_bounds__(kThreadsEmu, 1)
                         (kin != 0 || p != 0) ? 1u : 0u);
             }
           }
+#endif
           commit(&sfree[rb.s]);
-          commit(&empty[rg.s]);
+          commit(&bempty[rg.s]);
           if (kb == kb1 - 1) commit(acc_full);
         }
         __syncwarp();
@@ -313,7 +340,7 @@ __global__ void __launch_bounds__(kThreadsEmu, 1)
     }
   } else if (warp < 2 + kSplitW) {  // -------------------------------- split: digits → TMEM
     const int q = warp & 3;
-    const int h = (warp - 2) >> 2;  // which 16 k of the 32 (box h of the stage)
+    const int h = (warp - 2) >> 2;  // k = 4·kGroups·h .. of the stage's 32
     const int t = 32 * q + lane;    // tile row = TMEM lane
     const uint32_t lane_off = (uint32_t)(32 * q) << 16;
     Ring<S> rg;
@@ -322,38 +349,67 @@ __global__ void __launch_bounds__(kThreadsEmu, 1)
       const int64_t tile = un / nkc;
       const int kc = (int)(un - tile * nkc);
       const int64_t row = tile * 128 + t;
-      const double scale = scale_of(row < m ? E[row] : 0);
+      const int Erow = row < m ? E[row] : 0;
+      const double scale = scale_of(Erow);
+      // rows below 2^-960: 2^(62−E) is not a double — pre-scale by 2^(−960−E)
+      const bool tiny = Erow < -960;
+      const double pre = tiny ? pow2(-960 - Erow) : 1.0;
+      // two instantiations of the k loop: rows below 2^-960 in this warp need
+      // the extra pre-scale (warp-uniform choice, once per unit)
+      auto kloop = [&](auto tiny_tag) {
+      constexpr bool kTiny = decltype(tiny_tag)::value;
       for (int kb = kc * KCH; kb < KB && kb < (kc + 1) * KCH; ++kb, rg.next(), rb.next()) {
         mbar_wait(&full[rg.s], rg.ph);
-        const uint8_t* st = smem + rg.s * Cfg::kStage + h * 16384 + t * 128;
-        uint32_t w[4][kDigits];  // 4-element group g (k = 16h + 4g .. +3), plane s
+        const uint8_t* st = smem + rg.s * kATile + t * 128;
+        uint32_t w[kGroups][kDigits];  // group g (k = 4·(kGroups·h + g) .. +3), plane s
 #pragma unroll
-        for (int g = 0; g < 4; ++g) {
+        for (int g = 0; g < kGroups; ++g) {
           uint32_t lo[4], hi[4];
+          const int k0 = 4 * (kGroups * h + g);  // box k0/16, logical chunks (k0 mod 16)/2 + cc
 #pragma unroll
-          for (int cc = 0; cc < 2; ++cc) {  // logical 16-byte chunk c = 2g + cc sits at c ^ (t mod 8)
-            const int c = 2 * g + cc;
-            const double2 v = *reinterpret_cast<const double2*>(st + ((c ^ (t & 7)) << 4));
-            biased(v.x, scale, lo[2 * cc], hi[2 * cc]);
-            biased(v.y, scale, lo[2 * cc + 1], hi[2 * cc + 1]);
+          for (int cc = 0; cc < 2; ++cc) {  // logical 16-byte chunk c sits at c ^ (t mod 8)
+            const int c = ((k0 & 15) >> 1) + cc;
+            const double2 v = *reinterpret_cast<const double2*>(st + (k0 >> 4) * 16384 + ((c ^ (t & 7)) << 4));
+#ifdef EMU_NO_SPLIT
+            lo[2 * cc] = __double2loint(v.x); hi[2 * cc] = __double2hiint(v.x);
+            lo[2 * cc + 1] = __double2loint(v.y); hi[2 * cc + 1] = __double2hiint(v.y);
+          }
+#pragma unroll
+          for (int p = 0; p < kDigits; ++p) w[g][p] = lo[p & 3] ^ hi[(p + 1) & 3];
+#else
+            biased(kTiny ? v.x * pre : v.x, scale, lo[2 * cc], hi[2 * cc]);
+            biased(kTiny ? v.y * pre : v.y, scale, lo[2 * cc + 1], hi[2 * cc + 1]);
           }
           planes4(lo, hi, w[g]);
+#endif
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[rg.s]);  // the row is in registers
         mbar_wait(&sfree[rb.s], rb.ph ^ 1u);
         fence_after();
-        const uint32_t at = tmem + lane_off + (uint32_t)(Cfg::kSlot0 + Cfg::kSet * rb.s + 4 * h);
+        const uint32_t at = tmem + lane_off + (uint32_t)(Cfg::kSlot0 + Cfg::kSet * rb.s + kGroups * h);
 #pragma unroll
-        for (int p = 0; p < kDigits; ++p)
-          asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1,%2,%3,%4};" ::"r"(at + 8 * p),
-                       "r"(w[0][p]), "r"(w[1][p]), "r"(w[2][p]), "r"(w[3][p])
-                       : "memory");
+        for (int p = 0; p < kDigits; ++p) {
+          if constexpr (kGroups == 4)
+            asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1,%2,%3,%4};" ::"r"(at + 8 * p),
+                         "r"(w[0][p]), "r"(w[1][p]), "r"(w[2][p]), "r"(w[3][p])
+                         : "memory");
+          else if constexpr (kGroups == 2)
+            asm volatile("tcgen05.st.sync.aligned.32x32b.x2.b32 [%0], {%1,%2};" ::"r"(at + 8 * p), "r"(w[0][p]),
+                         "r"(w[1][p])
+                         : "memory");
+          else
+            asm volatile("tcgen05.st.sync.aligned.32x32b.x1.b32 [%0], {%1};" ::"r"(at + 8 * p), "r"(w[0][p])
+                         : "memory");
+        }
         asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
         fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&sfull[rb.s]);
       }
+      };
+      if (__any_sync(0xffffffffu, tiny)) kloop(std::true_type{});
+      else kloop(std::false_type{});
     }
   } else {  // ---------------------------------------------------- epilogue
     const int q = warp & 3;

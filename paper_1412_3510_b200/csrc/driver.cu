@@ -508,6 +508,23 @@ void apply_step(Ctx& c, const rpca_mat* Am, const double* cm, int adjoint, const
   }
 }
 
+// Y = A·X through the int8-digit emulation (dense fp64 A, 24 < l ≤ 48): the
+// path rpca_pca / rpca_eigens take for such A, exposed for tests and benches
+void apply_emu_step(Ctx& c, const rpca_mat* Am, const double* X, int64_t l, double* Y) {
+  validate_mat(Am);
+  RPCA_REQUIRE(Am->location == RPCA_DEVICE, RPCA_E_ARG, "apply_int8emu: device A only");
+  RPCA_REQUIRE(l >= 1 && l <= kMaxL && X && Y, RPCA_E_SHAPE, "apply_int8emu: bad l / NULL X, Y");
+  const MatV probe = probe_of(Am);
+  RPCA_REQUIRE(!probe.csr && emu_eligible(probe.d, (int)l), RPCA_E_NOTIMPL,
+               "apply_int8emu: needs a dense fp64 A (m ≥ 128, n ≥ 32) and 24 < l ≤ 48");
+  Arena ar = c.arena(op_ws(c, probe, (int)l) + (size_t)probe.m * 4 + 65536);
+  const MatV A = device_view(c, Am, ar);
+  profiled_step(c, [&] {
+    EmuScope emu(c, A, (int)l, 2, ar);
+    dense_ax(c, A.d, X, (int)l, Y, ar, nullptr);
+  });
+}
+
 void colmeans_step(Ctx& c, const rpca_mat* Am, double* cm) {
   validate_mat(Am);
   RPCA_REQUIRE(Am->location == RPCA_DEVICE && cm, RPCA_E_ARG, "colmeans: device A and c only");

@@ -106,6 +106,49 @@ def test_apply_f32_input(m, n, l):
     assert np.all(np.abs(got - ref) <= bound * (np.abs(An).T @ np.abs(Y.cpu().numpy())) + 1e-300)
 
 
+# ----------------------------------------------------------------- a2: int8 emulation
+# The fp64 A·X of pca/eigens for 24 < l ≤ 48 (dense_ax_emu.cu): against the
+# oracle's product, within the scheme's bound — each of the n terms is exact
+# to 2^-55·2^E_i·2^G_j (E_i, G_j the row / column exponents, 2^E > max|·|)
+@pytest.mark.parametrize("m,n,l", [(1000, 700, 42), (257, 1026, 25), (3001, 96, 48), (128, 32, 30)])
+def test_apply_int8emu_vs_oracle(m, n, l):
+    g = torch.Generator(device="cuda").manual_seed(m * 11 + n + l)
+    A = torch.randn(m, n, generator=g, device=dev(), dtype=torch.float64)
+    A *= 10.0 ** torch.randint(-30, 30, (m, 1), generator=g, device=dev()).double()  # rows of any scale
+    X = torch.randn(n, l, generator=g, device=dev(), dtype=torch.float64)
+    X[:, 3] *= 1e-80
+    Y = rp.apply_int8emu(A, X).cpu().numpy()
+    An, Xn = A.cpu().numpy(), X.cpu().numpy()
+    ref = oracle.apply(An, Xn)
+    rmax = 2.0 ** np.ceil(np.log2(np.abs(An).max(1) * (1 + 2**-52)))
+    cmax = 2.0 ** np.ceil(np.log2(np.abs(Xn).max(0) * (1 + 2**-52)))
+    bound = n * 2.0**-54 * np.outer(rmax, cmax) + 2.0**-52 * np.abs(ref)
+    assert np.all(np.abs(Y - ref) <= bound)
+    assert np.max(np.abs(Y - ref) / (np.abs(An) @ np.abs(Xn))) < 1e-13
+
+
+def test_apply_int8emu_special_values():
+    m, n, l = 300, 200, 40
+    g = torch.Generator(device="cuda").manual_seed(7)
+    A = torch.randn(m, n, generator=g, device=dev(), dtype=torch.float64)
+    X = torch.randn(n, l, generator=g, device=dev(), dtype=torch.float64)
+    A[5] = 0.0                      # zero row → zero output row
+    A[9, 17] = float("nan")         # non-finite row → NaN output row
+    X[:, 2] = 0.0                   # zero column → zero output column
+    A[40] *= 1e300                  # near the top of the range
+    A[41] *= 1e-300                 # and near the bottom
+    Y = rp.apply_int8emu(A, X)
+    assert bool((Y[5] == 0).all()) and bool(Y[9].isnan().all())
+    assert bool((torch.cat([Y[:9], Y[10:]])[:, 2] == 0).all())
+    ok = torch.ones(m, dtype=torch.bool, device=dev())
+    ok[9] = False
+    ref = torch.tensor(oracle.apply(torch.nan_to_num(A).cpu().numpy(), X.cpu().numpy()), device=dev())
+    rel = ((Y - ref).abs() / (A.abs() @ X.abs())).nan_to_num(0.0)[ok]
+    assert float(rel.max()) < 1e-13
+    with pytest.raises(rp.RPCAError):
+        rp.apply_int8emu(A, X[:, :20])  # l ≤ 24: not an emulated shape
+
+
 # ----------------------------------------------------------------- a3: LU
 # the last three run persistent leaves (more leaves than resident CTAs) whose
 # last leaf has an odd number of doubles (the bulk copy's 16-byte tail)
