@@ -139,6 +139,18 @@ __device__ __forceinline__ void biased(double a, double scale, uint32_t& lo, uin
   hi = (uint32_t)(U >> 32);
 }
 
+// biased() with a·2^(62−E) formed by adding dexp = (62−E)<<20 to the high
+// word (a normal, E ≥ −960): fields below flo = E − 61 give 0
+__device__ __forceinline__ void biased_exp(double a, uint32_t dexp, int flo, uint32_t& lo, uint32_t& hi) {
+  const uint32_t h = (uint32_t)__double2hiint(a);
+  const int f = (int)((h >> 20) & 0x7FFu);
+  const bool keep = f >= flo && f != 0;
+  const double t = __hiloint2double(keep ? (int)(h + dexp) : 0, keep ? __double2loint(a) : 0);
+  const unsigned long long U = (unsigned long long)__double2ll_rz(t) + 0x8080808080808080ull;
+  lo = (uint32_t)U;
+  hi = (uint32_t)(U >> 32);
+}
+
 // plane words of four consecutive elements (U halves lo[e], hi[e]): w[s] holds
 // digit s (byte 7 − s of U) of elements 0..3 in bytes 0..3, as int8
 __device__ __forceinline__ void planes4(const uint32_t (&lo)[4], const uint32_t (&hi)[4], uint32_t (&w)[kDigits]) {
@@ -354,6 +366,8 @@ __global__ void __launch_bounds__(kThreadsEmu, 1)
       // rows below 2^-960: 2^(62−E) is not a double — pre-scale by 2^(−960−E)
       const bool tiny = Erow < -960;
       const double pre = tiny ? pow2(-960 - Erow) : 1.0;
+      const uint32_t dexp = (uint32_t)(62 - Erow) << 20;  // exponent-field increment of 2^(62−E)
+      const int flo = Erow - 61;                            // smallest field kept
       // two instantiations of the k loop: rows below 2^-960 in this warp need
       // the extra pre-scale (warp-uniform choice, once per unit)
       auto kloop = [&](auto tiny_tag) {
@@ -377,8 +391,25 @@ __global__ void __launch_bounds__(kThreadsEmu, 1)
 #pragma unroll
           for (int p = 0; p < kDigits; ++p) w[g][p] = lo[p & 3] ^ hi[(p + 1) & 3];
 #else
+#if !defined(EMU_NO_FP64) && !defined(EMU_DMUL)
+            // the power-of-two scaling as an integer add to the exponent field
+            // (exact: the field stays in [1, 1084]; elements below 2^(E−1083)
+            // would give T = 0 and are zeroed) — the fp64 pipe, shared with
+            // the tensor cores, then runs only the conversion
+            if constexpr (kTiny) {
+              biased(v.x * pre, scale, lo[2 * cc], hi[2 * cc]);
+              biased(v.y * pre, scale, lo[2 * cc + 1], hi[2 * cc + 1]);
+            } else {
+              biased_exp(v.x, dexp, flo, lo[2 * cc], hi[2 * cc]);
+              biased_exp(v.y, dexp, flo, lo[2 * cc + 1], hi[2 * cc + 1]);
+            }
+#elif defined(EMU_NO_FP64)  // ablation: the digit arithmetic without its fp64-pipe instructions
+            lo[2 * cc] = __double2loint(v.x) + 0x80808080u; hi[2 * cc] = __double2hiint(v.x) + 0x80808080u;
+            lo[2 * cc + 1] = __double2loint(v.y) + 0x80808080u; hi[2 * cc + 1] = __double2hiint(v.y) + 0x80808080u;
+#else
             biased(kTiny ? v.x * pre : v.x, scale, lo[2 * cc], hi[2 * cc]);
             biased(kTiny ? v.y * pre : v.y, scale, lo[2 * cc + 1], hi[2 * cc + 1]);
+#endif
           }
           planes4(lo, hi, w[g]);
 #endif
