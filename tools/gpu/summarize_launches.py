@@ -5,6 +5,8 @@ hi = [i for i, r in enumerate(rows) if r and r[0] == "ID"][0]
 h = rows[hi]
 ks = [(r[h.index("Kernel Name")], float(r[h.index("Metric Value")])) for r in rows[hi + 1:]]
 start = [i for i, (k, v) in enumerate(ks) if "omega_kernel" in k][-1]
+if start > 0 and "row_exp_kernel" in ks[start - 1][0]:  # the emulated path's exponent read opens the step
+    start -= 1
 last = ks[start:]
 agg = collections.OrderedDict()
 for k, v in last:
