@@ -101,7 +101,7 @@ __device__ __forceinline__ void trail_update(double (&w)[LP], const double (*u12
 //   leaf: 1 = contiguous rows of Y; 0 = candidate ids into Y; 2 = candidate
 //   rows given directly (rows_in, one l-vector per slot; ids are global rows
 //   — the all-gathered local winners of a row-sharded LU)
-template <int LP, int RR>
+template <int LP, int RR, bool BULK>
 __global__ void __launch_bounds__(kThreads, SelCfg<LP, RR>::kMinBlocks)
     lu_select_kernel(const double* __restrict__ Y, int64_t m, int l, int leaf, const int64_t* __restrict__ cand_in,
                      int64_t n_in, int G, int64_t* __restrict__ cand_out, int final_, double* __restrict__ U,
@@ -132,6 +132,7 @@ __global__ void __launch_bounds__(kThreads, SelCfg<LP, RR>::kMinBlocks)
   // bulk (leaves only, never final): a persistent CTA walks leaves b, b+grid, …
   // and a 1-D bulk copy stages the next leaf's rows (contiguous in Y) in
   // shared memory while the current leaf runs its GEPP on registers
+  bulk = BULK && bulk;  // the staging code exists in the BULK instantiation only
   const int64_t nleaf = (leaf == 1 && bulk) ? (m + CAP - 1) / CAP : (int64_t)blockIdx.x + 1;
   auto leaf_bytes = [&](int64_t b) -> uint32_t {
     return (uint32_t)(imin64(CAP, m - b * CAP) * l * 8) & ~15u;  // an odd last double is read from Y
@@ -418,18 +419,26 @@ void select_lpr(Ctx& c, unsigned grid, const double* Y, int64_t m, int l, int le
                 int G, int64_t* cout, int final_, double* U, double* Lp, int64_t* piv, double* M,
                 const double* rows_in, double* rows_out, const double* mu) {
   constexpr int CAP = SelCfg<LP, R>::kCap;
-  // leaves that are not the last level run persistent with bulk-staged rows
-  const int bulk = leaf == 1 && !final_ && (reinterpret_cast<uintptr_t>(Y) & 15) == 0;
+  // leaves that are not the last level run persistent with bulk-staged rows —
+  // in the one-CTA-per-SM configurations (with two CTAs per SM the second one
+  // already hides the row loads, and the 128-register cap has no room for
+  // the staging state)
+  constexpr bool kBulkOK = SelCfg<LP, R>::kMinBlocks == 1;
+  const int bulk = kBulkOK && leaf == 1 && !final_ && (reinterpret_cast<uintptr_t>(Y) & 15) == 0;
   const size_t smem = final_ ? (size_t)(LP * LP + l * l + (size_t)CAP * l) * 8 : bulk ? (size_t)CAP * l * 8 : 0;
-  const void* fn = (const void*)lu_select_kernel<LP, R>;
+  const void* fn = bulk ? (const void*)lu_select_kernel<LP, R, kBulkOK> : (const void*)lu_select_kernel<LP, R, false>;
   if (smem) ensure_smem(fn, (int)smem);
   if (bulk) {
     int occ = 0;
     RPCA_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, kThreads, smem));
     grid = (unsigned)std::min<int64_t>(grid, (int64_t)c.num_sms * std::max(1, occ));
   }
-  lu_select_kernel<LP, R><<<grid, kThreads, smem, c.stream>>>(Y, m, l, leaf, cin, n_in, G, cout, final_, U, Lp, piv,
-                                                              M, rows_in, rows_out, mu, bulk);
+  if (bulk)
+    lu_select_kernel<LP, R, kBulkOK><<<grid, kThreads, smem, c.stream>>>(Y, m, l, leaf, cin, n_in, G, cout, final_, U,
+                                                                         Lp, piv, M, rows_in, rows_out, mu, bulk);
+  else
+    lu_select_kernel<LP, R, false><<<grid, kThreads, smem, c.stream>>>(Y, m, l, leaf, cin, n_in, G, cout, final_, U,
+                                                                       Lp, piv, M, rows_in, rows_out, mu, 0);
 }
 
 template <int LP>
