@@ -98,6 +98,77 @@ __global__ void __launch_bounds__(kThreads) csr_spmm_kernel(const int64_t* __res
   }
 }
 
+// Half-warp per row for even l ≤ 32 (C5's A·X: ~10 nonzeros per row, where a
+// warp per row leaves most of the memory parallelism unused): sub-lane s owns
+// columns 2s, 2s+1 (one 16-byte gather per nonzero), eight gathers in flight
+// per half-warp, two rows per warp.  Same summation order per output as
+// csr_spmm_kernel (ascending t).
+template <class T>
+__global__ void __launch_bounds__(kThreads) csr_spmm_pair_kernel(const int64_t* __restrict__ rowptr,
+                                                                 const int32_t* __restrict__ colind,
+                                                                 const T* __restrict__ vals, int64_t rows,
+                                                                 const double* __restrict__ X, int l, int64_t heavy,
+                                                                 const double* __restrict__ xmean,
+                                                                 double* __restrict__ Y) {
+  const int lane = threadIdx.x & 31, half = lane >> 4, s = lane & 15;
+  const unsigned hm = 0xFFFFu << (16 * half);
+  const bool act = 2 * s < l;
+  const int64_t stride = (int64_t)gridDim.x * (kThreads / 16);
+  for (int64_t i = ((int64_t)blockIdx.x * (kThreads / 32) + (threadIdx.x >> 5)) * 2 + half; i < rows; i += stride) {
+    const int64_t t0 = rowptr[i], t1 = rowptr[i + 1];
+    if (t1 - t0 > heavy) continue;
+    double ax = 0.0, ay = 0.0, vs = 0.0;
+    for (int64_t tb = t0; tb < t1; tb += 16) {
+      const int cnt = (int)imin64(16, t1 - tb);
+      int myc = 0;
+      double myv = 0.0;
+      if (s < cnt) {
+        myc = colind[tb + s];
+        myv = static_cast<double>(vals[tb + s]);
+      }
+      vs += myv;
+      int k = 0;
+      for (; k + 8 <= cnt; k += 8) {
+        int c[8];
+        double v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          c[u] = __shfl_sync(hm, myc, k + u, 16);
+          v[u] = __shfl_sync(hm, myv, k + u, 16);
+        }
+        if (act) {
+          double2 x[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) x[u] = *reinterpret_cast<const double2*>(X + (int64_t)c[u] * l + 2 * s);
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            ax += v[u] * x[u].x;
+            ay += v[u] * x[u].y;
+          }
+        }
+      }
+      for (; k < cnt; ++k) {
+        const int cc = __shfl_sync(hm, myc, k, 16);
+        const double vv = __shfl_sync(hm, myv, k, 16);
+        if (act) {
+          const double2 x = *reinterpret_cast<const double2*>(X + (int64_t)cc * l + 2 * s);
+          ax += vv * x.x;
+          ay += vv * x.y;
+        }
+      }
+    }
+    if (xmean) {  // Σ v·(x − x̄) = Σ v·x − x̄·Σ v
+#pragma unroll
+      for (int o = 8; o > 0; o >>= 1) vs += __shfl_xor_sync(hm, vs, o, 16);
+      if (act) {
+        ax -= xmean[2 * s] * vs;
+        ay -= xmean[2 * s + 1] * vs;
+      }
+    }
+    if (act) *reinterpret_cast<double2*>(Y + i * l + 2 * s) = make_double2(ax, ay);
+  }
+}
+
 // warp per chunk of a heavy row → its partial row
 template <class T>
 __global__ void __launch_bounds__(kThreads) csr_chunk_kernel(const int32_t* __restrict__ colind,
@@ -198,7 +269,17 @@ void csr_spmm(Ctx& c, const CsrA& A, const double* X, int l, double* Y, const do
   const unsigned grid = grid_cap(c, A.rows, kThreads / 32);
   const int64_t heavy = A.nhc ? kHeavyNnz : INT64_MAX;
   prof_pre(c);
-  if (A.dtype == RPCA_F64)
+  const bool pair = l % 2 == 0 && l <= 32 && (reinterpret_cast<uintptr_t>(X) & 15) == 0 &&
+                    (reinterpret_cast<uintptr_t>(Y) & 15) == 0;
+  if (pair) {
+    const unsigned gp = grid_cap(c, A.rows, kThreads / 16);
+    if (A.dtype == RPCA_F64)
+      csr_spmm_pair_kernel<double><<<gp, kThreads, 0, c.stream>>>(A.ptr, A.idx, (const double*)A.vals, A.rows, X, l,
+                                                                  heavy, xmean, Y);
+    else
+      csr_spmm_pair_kernel<float><<<gp, kThreads, 0, c.stream>>>(A.ptr, A.idx, (const float*)A.vals, A.rows, X, l,
+                                                                 heavy, xmean, Y);
+  } else if (A.dtype == RPCA_F64)
     csr_spmm_kernel<double><<<grid, kThreads, 0, c.stream>>>(A.ptr, A.idx, (const double*)A.vals, A.rows, X, l, heavy,
                                                              xmean, Y);
   else
