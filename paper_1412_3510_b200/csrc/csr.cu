@@ -98,28 +98,34 @@ __global__ void __launch_bounds__(kThreads) csr_spmm_kernel(const int64_t* __res
   }
 }
 
-// Half-warp per row for even l ≤ 32 (C5's A·X: ~10 nonzeros per row, where a
-// warp per row leaves most of the memory parallelism unused): sub-lane s owns
-// columns 2s, 2s+1 (one 16-byte gather per nonzero), eight gathers in flight
-// per half-warp, two rows per warp.  Same summation order per output as
-// csr_spmm_kernel (ascending t).
-template <class T>
+// W lanes per row (W = 16 or 8) for l ≤ 2W·… even, l ≤ 32: C5's A·X has ~10
+// nonzeros per row, where a warp per row leaves most of the memory
+// parallelism unused.  Sub-lane s owns columns C·s … C·s+C−1 (C = 32/W, one
+// or two 16-byte gathers per nonzero), eight nonzeros in flight per row,
+// 32/W rows per warp.  Same summation order per output as csr_spmm_kernel
+// (ascending t).
+template <class T, int W>
 __global__ void __launch_bounds__(kThreads) csr_spmm_pair_kernel(const int64_t* __restrict__ rowptr,
                                                                  const int32_t* __restrict__ colind,
                                                                  const T* __restrict__ vals, int64_t rows,
                                                                  const double* __restrict__ X, int l, int64_t heavy,
                                                                  const double* __restrict__ xmean,
                                                                  double* __restrict__ Y) {
-  const int lane = threadIdx.x & 31, half = lane >> 4, s = lane & 15;
-  const unsigned hm = 0xFFFFu << (16 * half);
-  const bool act = 2 * s < l;
-  const int64_t stride = (int64_t)gridDim.x * (kThreads / 16);
-  for (int64_t i = ((int64_t)blockIdx.x * (kThreads / 32) + (threadIdx.x >> 5)) * 2 + half; i < rows; i += stride) {
+  constexpr int C = 32 / W;  // columns per sub-lane (2 or 4)
+  const int lane = threadIdx.x & 31, grp = lane / W, s = lane % W;
+  const unsigned hm = (W == 32 ? 0xFFFFFFFFu : ((1u << W) - 1u)) << (W * grp);
+  const bool act = C * s < l;
+  const int64_t stride = (int64_t)gridDim.x * (kThreads / W);
+  for (int64_t i = ((int64_t)blockIdx.x * (kThreads / 32) + (threadIdx.x >> 5)) * (32 / W) + grp; i < rows;
+       i += stride) {
     const int64_t t0 = rowptr[i], t1 = rowptr[i + 1];
     if (t1 - t0 > heavy) continue;
-    double ax = 0.0, ay = 0.0, vs = 0.0;
-    for (int64_t tb = t0; tb < t1; tb += 16) {
-      const int cnt = (int)imin64(16, t1 - tb);
+    double a[C];
+#pragma unroll
+    for (int q = 0; q < C; ++q) a[q] = 0.0;
+    double vs = 0.0;
+    for (int64_t tb = t0; tb < t1; tb += W) {
+      const int cnt = (int)imin64(W, t1 - tb);
       int myc = 0;
       double myv = 0.0;
       if (s < cnt) {
@@ -133,39 +139,48 @@ __global__ void __launch_bounds__(kThreads) csr_spmm_pair_kernel(const int64_t* 
         double v[8];
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
-          c[u] = __shfl_sync(hm, myc, k + u, 16);
-          v[u] = __shfl_sync(hm, myv, k + u, 16);
+          c[u] = __shfl_sync(hm, myc, k + u, W);
+          v[u] = __shfl_sync(hm, myv, k + u, W);
         }
         if (act) {
-          double2 x[8];
+          double2 x[8][C / 2];
 #pragma unroll
-          for (int u = 0; u < 8; ++u) x[u] = *reinterpret_cast<const double2*>(X + (int64_t)c[u] * l + 2 * s);
+          for (int u = 0; u < 8; ++u)
 #pragma unroll
-          for (int u = 0; u < 8; ++u) {
-            ax += v[u] * x[u].x;
-            ay += v[u] * x[u].y;
-          }
+            for (int h = 0; h < C / 2; ++h)
+              x[u][h] = *reinterpret_cast<const double2*>(X + (int64_t)c[u] * l + C * s + 2 * h);
+#pragma unroll
+          for (int u = 0; u < 8; ++u)
+#pragma unroll
+            for (int h = 0; h < C / 2; ++h) {
+              a[2 * h] += v[u] * x[u][h].x;
+              a[2 * h + 1] += v[u] * x[u][h].y;
+            }
         }
       }
       for (; k < cnt; ++k) {
-        const int cc = __shfl_sync(hm, myc, k, 16);
-        const double vv = __shfl_sync(hm, myv, k, 16);
-        if (act) {
-          const double2 x = *reinterpret_cast<const double2*>(X + (int64_t)cc * l + 2 * s);
-          ax += vv * x.x;
-          ay += vv * x.y;
-        }
+        const int cc = __shfl_sync(hm, myc, k, W);
+        const double vv = __shfl_sync(hm, myv, k, W);
+        if (act)
+#pragma unroll
+          for (int h = 0; h < C / 2; ++h) {
+            const double2 x = *reinterpret_cast<const double2*>(X + (int64_t)cc * l + C * s + 2 * h);
+            a[2 * h] += vv * x.x;
+            a[2 * h + 1] += vv * x.y;
+          }
       }
     }
     if (xmean) {  // Σ v·(x − x̄) = Σ v·x − x̄·Σ v
 #pragma unroll
-      for (int o = 8; o > 0; o >>= 1) vs += __shfl_xor_sync(hm, vs, o, 16);
-      if (act) {
-        ax -= xmean[2 * s] * vs;
-        ay -= xmean[2 * s + 1] * vs;
-      }
+      for (int o = W / 2; o > 0; o >>= 1) vs += __shfl_xor_sync(hm, vs, o, W);
+      if (act)
+#pragma unroll
+        for (int q = 0; q < C; ++q) a[q] -= xmean[C * s + q] * vs;
     }
-    if (act) *reinterpret_cast<double2*>(Y + i * l + 2 * s) = make_double2(ax, ay);
+    if (act)
+#pragma unroll
+      for (int h = 0; h < C / 2; ++h)
+        *reinterpret_cast<double2*>(Y + i * l + C * s + 2 * h) = make_double2(a[2 * h], a[2 * h + 1]);
   }
 }
 
@@ -269,16 +284,30 @@ void csr_spmm(Ctx& c, const CsrA& A, const double* X, int l, double* Y, const do
   const unsigned grid = grid_cap(c, A.rows, kThreads / 32);
   const int64_t heavy = A.nhc ? kHeavyNnz : INT64_MAX;
   prof_pre(c);
-  const bool pair = l % 2 == 0 && l <= 32 && (reinterpret_cast<uintptr_t>(X) & 15) == 0 &&
-                    (reinterpret_cast<uintptr_t>(Y) & 15) == 0;
-  if (pair) {
+#ifndef CSR_LANES
+#define CSR_LANES 16
+#endif
+  // lanes per row: 16 × 2 columns (measured best on C5; 8 × 4 with CSR_LANES=8)
+  const bool al = (reinterpret_cast<uintptr_t>(X) & 15) == 0 && (reinterpret_cast<uintptr_t>(Y) & 15) == 0;
+  const int avg = (int)std::min<int64_t>(1 << 20, A.nnz / std::max<int64_t>(1, A.rows));
+  const int W = (CSR_LANES == 8 && l % 4 == 0 && avg < 64) ? 8 : 16;
+  const bool pair = al && l % 2 == 0 && l <= 32;
+  if (pair && W == 8) {
+    const unsigned gp = grid_cap(c, A.rows, kThreads / 8);
+    if (A.dtype == RPCA_F64)
+      csr_spmm_pair_kernel<double, 8><<<gp, kThreads, 0, c.stream>>>(A.ptr, A.idx, (const double*)A.vals, A.rows, X,
+                                                                     l, heavy, xmean, Y);
+    else
+      csr_spmm_pair_kernel<float, 8><<<gp, kThreads, 0, c.stream>>>(A.ptr, A.idx, (const float*)A.vals, A.rows, X, l,
+                                                                    heavy, xmean, Y);
+  } else if (pair) {
     const unsigned gp = grid_cap(c, A.rows, kThreads / 16);
     if (A.dtype == RPCA_F64)
-      csr_spmm_pair_kernel<double><<<gp, kThreads, 0, c.stream>>>(A.ptr, A.idx, (const double*)A.vals, A.rows, X, l,
-                                                                  heavy, xmean, Y);
+      csr_spmm_pair_kernel<double, 16><<<gp, kThreads, 0, c.stream>>>(A.ptr, A.idx, (const double*)A.vals, A.rows, X,
+                                                                      l, heavy, xmean, Y);
     else
-      csr_spmm_pair_kernel<float><<<gp, kThreads, 0, c.stream>>>(A.ptr, A.idx, (const float*)A.vals, A.rows, X, l,
-                                                                 heavy, xmean, Y);
+      csr_spmm_pair_kernel<float, 16><<<gp, kThreads, 0, c.stream>>>(A.ptr, A.idx, (const float*)A.vals, A.rows, X,
+                                                                     l, heavy, xmean, Y);
   } else if (A.dtype == RPCA_F64)
     csr_spmm_kernel<double><<<grid, kThreads, 0, c.stream>>>(A.ptr, A.idx, (const double*)A.vals, A.rows, X, l, heavy,
                                                              xmean, Y);
