@@ -227,15 +227,36 @@ def run_step(rp, cfg, A, plan=None):
 
 
 # ------------------------------------------------------------------ CPU oracle
+def host_of(A):
+    """A as the oracle takes it: a dense ndarray, or the CSR triple + shape."""
+    if isinstance(A, torch.Tensor):
+        return A.cpu().numpy()
+    if isinstance(A, (tuple, list)):
+        rp_, ci, va = A[:3]
+        m = rp_.numel() - 1
+        return (rp_.cpu().numpy(), ci.cpu().numpy(), va.cpu().numpy(), (m, None))
+    return (A.rowptr.cpu().numpy(), A.colind.cpu().numpy(), A.vals.cpu().numpy(), tuple(A.shape))
+
+
+def leading_rows(A_host, ms, n):
+    """The leading ms rows of a dense or CSR host matrix."""
+    if isinstance(A_host, np.ndarray):
+        return np.ascontiguousarray(A_host[:ms])
+    rp_, ci, va, _ = A_host
+    nz = int(rp_[ms])
+    return (np.ascontiguousarray(rp_[:ms + 1]), ci[:nz], va[:nz], (ms, n))
+
+
 def oracle_sample(cfg, A_host, target_s):
     """Time the oracle (as it stands) on a leading-row sample of the workload,
-    growing the sample until one run takes ≥ target_s / 4; extrapolate to full m."""
+    growing the sample until one run takes ≥ target_s / 4; extrapolate to full m.
+    CSR samples start at n rows so that the sample keeps the m ≥ n orientation."""
     import oracle
 
-    m = A_host.shape[0]
-    ms = min(m, max(cfg.l * 4, 2000))
+    m = cfg.m
+    ms = min(m, max(cfg.l * 4, 2000, 0 if isinstance(A_host, np.ndarray) else cfg.n))
     while True:
-        As = np.ascontiguousarray(A_host[:ms])
+        As = leading_rows(A_host, ms, cfg.n)
         t0 = time.perf_counter()
         if cfg.op == "eigens":
             # the Nyström path needs a square matrix: sample its leading ms×ms block
@@ -256,6 +277,8 @@ def cpu_baseline(cfg, A_host, target_s):
 
     ms, dt, scale = oracle_sample(cfg, A_host, target_s)
     what = (f"leading {ms}x{ms} block" if cfg.op == "eigens" else f"leading {ms} of {cfg.m} rows")
+    if not isinstance(A_host, np.ndarray):
+        what += " (CSR; the n-side work does not grow with m, so linear extrapolation overstates it slightly)"
     return {"value": dt * scale, "unit": "s", "cores": oracle.num_threads(), "kind": "oracle",
             "sample": f"oracle on the {what} ({dt:.2f} s), extrapolated "
                       f"{'quadratically in n' if cfg.op == 'eigens' else 'linearly in m'} (x{scale:.1f})"}
@@ -269,12 +292,12 @@ def reference_arm(args):
     import oracle
 
     A = synth.make(cfg.name, device="cuda" if torch.cuda.is_available() else "cpu")
-    A_host = A.cpu().numpy()
+    A_host = host_of(A)
     del A
     ms, dt, scale = oracle_sample(cfg, A_host, args.cpu_seconds)
     times = []
     for it in range(args.warmup + args.steps):
-        As = np.ascontiguousarray(A_host[:ms, :ms] if cfg.op == "eigens" else A_host[:ms])
+        As = np.ascontiguousarray(A_host[:ms, :ms]) if cfg.op == "eigens" else leading_rows(A_host, ms, cfg.n)
         t0 = time.perf_counter()
         if cfg.op == "eigens":
             oracle.eigens(As, cfg.k, its=cfg.its, l=cfg.l, seed=0)
@@ -407,8 +430,8 @@ def main():
         del Ah
 
     cpu = None
-    if rank == 0 and ws == 1 and not args.no_cpu_baseline and isinstance(A, torch.Tensor):
-        cpu = cpu_baseline(cfg, A.cpu().numpy(), args.cpu_seconds)
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(cfg, host_of(A), args.cpu_seconds)
 
     if rank == 0:
         line = {"metric": "rank-k PCA wall time (s)", "value": t_step, "unit": "s", "n_gpus": ws,
