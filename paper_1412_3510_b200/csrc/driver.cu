@@ -500,12 +500,14 @@ void apply_step(Ctx& c, const rpca_mat* Am, const double* cm, int adjoint, const
   Arena ar = c.arena(op_ws(c, probe, (int)l) + 65536);
   const MatV A = device_view(c, Am, ar);
   const bool sh = check_shard(c, Am);
-  if (adjoint) {
-    apply_aty(c, A, cm, X, (int)l, Y, ar);
-    if (sh) allreduce_sum(c, Y, (size_t)A.n * l);
-  } else {
-    apply_ax(c, A, cm, X, (int)l, Y, ar);
-  }
+  profiled_step(c, [&] {
+    if (adjoint) {
+      apply_aty(c, A, cm, X, (int)l, Y, ar);
+      if (sh) allreduce_sum(c, Y, (size_t)A.n * l);
+    } else {
+      apply_ax(c, A, cm, X, (int)l, Y, ar);
+    }
+  });
 }
 
 // Y = A·X through the int8-digit emulation (dense fp64 A, 24 < l ≤ 48): the

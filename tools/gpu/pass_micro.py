@@ -28,3 +28,14 @@ for name, fn in (("A·X", lambda: rp.apply(A, X)), ("Aᵀ·Y", lambda: rp.apply(
     torch.cuda.synchronize()
     per = e0.elapsed_time(e1) / reps
     print(f"{name:6s} {per:8.3f} ms/call (split + pass + reduce)  {gb / per:6.2f} TB/s of A", flush=True)
+with rp.profile() as p:
+    for _ in range(reps):
+        rp.apply(A, X)
+        rp.apply(A, Q, adjoint=True)
+    torch.cuda.synchronize()
+agg = {}
+for k, ms in p.records:
+    c, s_ = agg.get(k, (0, 0.0))
+    agg[k] = (c + 1, s_ + ms)
+for k, (c, s_) in agg.items():
+    print(f"  {k:16s} {c // reps}x {s_ / c:8.3f} ms/launch" + (f"  {gb / (s_ / c):6.2f} TB/s" if "f32_tc" in k else ""))
