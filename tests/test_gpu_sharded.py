@@ -99,7 +99,8 @@ def test_sharded_pca_c1(P):
                                                (3001, 257, 20, 22, 3, False, 3),   # centred, ragged
                                                (513, 1025, 5, 12, 1, False, 2),
                                                (4000, 64, 40, 64, 2, True, 2),     # l = 64, P·l = 128
-                                               (2000, 700, 8, 10, 0, True, 3)])    # its = 0: QR only
+                                               (2000, 700, 8, 10, 0, True, 3),     # its = 0: QR only
+                                               (3001, 258, 20, 30, 2, False, 3)])  # l = 30: int8-emulated A·X
 def test_sharded_pca_shapes(m, n, k, l, its, raw, P):
     g = torch.Generator(device="cuda").manual_seed(m + n)
     sig = torch.exp(-torch.arange(min(m, n), dtype=torch.float64) / 4.0)
