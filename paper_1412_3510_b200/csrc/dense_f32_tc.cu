@@ -10,16 +10,17 @@
 // tools/microbench/tc_tf32_probe.cu), so the raw fp32 tile is the "hi"
 // operand as loaded and only A_lo = A − trunc13(A) has to be formed.
 //
-// In-place split: a stage holds ONE copy of the A tile.  The MMA warp first
-// issues the two "hi" products (A·X_hi, A·X_lo) and commits them to the
-// stage's hi_done barrier; the split warps then overwrite the tile with A_lo
-// in place (the transform is elementwise, so any layout works) and the MMA
-// warp issues A_lo·X_hi two stages later (fixed lag), whose commit frees the
-// stage.  One copy per stage buys 6-8 stages of A in flight per SM.
+// Both kernels move A through TMEM: split warps read the A tile from shared
+// memory once, store A_hi = trunc13(A) and A_lo = A − A_hi to TMEM (one
+// 32-bit TMEM column per k, lane = the M index), and every product reads its
+// A operand from TMEM (tcgen05.mma TS form) — shared memory carries the tile
+// once plus the thin operand (ablations: both passes were shared-memory
+// bound with the A_hi operand read from shared memory).
 //
 // A·X  (D[128 rows × N] += A[128 × K] · Xᵀ[N × K]ᵀ, both K-major):
 //   warp 0 producer (TMA A box [128 rows × 32 fp32] + Xᵀ_hi/lo chunks),
-//   warp 1 MMA issuer, warps 2-5 split, warps 6-9 epilogue.  Units are
+//   warp 1 MMA issuer (A_hi·[X_hi | X_lo] as one N = 2N MMA, A_lo·X_hi into
+//   the first N columns), warps 2-5 split, warps 6-9 epilogue.  Units are
 //   (128-row tile, ≤ 4096-wide K chunk) — fp32 accumulation never runs over
 //   more than 4096 products; two TMEM accumulators
 //   alternate so the epilogue of unit u overlaps the MMAs of unit u+1; the
@@ -58,19 +59,10 @@ __host__ __device__ constexpr uint32_t idesc_tf32(int M, int N) {
   return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
 }
 
-__device__ __forceinline__ float lo_part(float a) {
-  return a - __uint_as_float(__float_as_uint(a) & 0xFFFFE000u);
-}
 
 // (An MN-major tf32 shared-memory operand would need SWIZZLE_128B_BASE32B —
 // descriptor layout type 1, TMA mode 128B_ATOM_32B, LBO 4096 / SBO 512; the
 // Aᵀ·Y kernel avoids it by moving A through TMEM.)
-__device__ __forceinline__ void mma_tf32(uint32_t tmem, uint64_t da, uint64_t db, uint32_t idesc, uint32_t acc) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem),
-      "l"(da), "l"(db), "r"(idesc), "r"(acc));
-}
 
 // D[tmem] (+)= A[tmem] · B[smem]: the A operand read from TMEM (lane = M row,
 // one 32-bit column per K element)
@@ -136,7 +128,6 @@ __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence:
 #ifndef ATY_SLOTS
 #define ATY_SLOTS 4
 #endif
-constexpr int kThreadsTC = 352;  // 11 warps: producer, hi-MMA, lo-MMA, 4 split, 4 epilogue
 constexpr int kTileBytes = 128 * 128;  // 16 KB A tile
 constexpr int kKChunk = 4096;          // max products per fp32 accumulation (Q15)
 
@@ -156,34 +147,37 @@ struct AxCfg {
   static constexpr int kStage = kTileBytes + 2 * kX;
   static constexpr int kStages = (212 * 1024) / kStage > 8 ? 8 : (212 * 1024) / kStage;
   static constexpr int kSmem = kStages * kStage + 1024 + 512;
-  // TMEM per accumulator: [0, N) A·X_hi, [N, 2N) A·X_lo (one N = 2N MMA),
-  // [2N, 3N) A_lo·X_hi (the lo issuer's own columns); two accumulators, then
-  // two 32-column A_lo slots
-  static constexpr int kW = (3 * N + 31) / 32 * 32;
+  // TMEM per accumulator: [0, N) A_hi·X_hi + A_lo·X_hi, [N, 2N) A_hi·X_lo
+  // (one N = 2N MMA over the adjacent X_hi, X_lo chunks); two accumulators,
+  // then 64-column A slots (32 columns A_hi, 32 columns A_lo)
+  static constexpr int kW = (2 * N + 31) / 32 * 32;
   static constexpr int kSlot0 = 2 * kW;
-  static constexpr int kCols = kSlot0 + 64 <= 256 ? 256 : 512;
-  static constexpr int kNS = (kCols - kSlot0) / 32 >= 4 ? 4 : 2;  // A_lo slots
+  static constexpr int kNS = (512 - kSlot0) / 64 >= 4 ? 4 : 2;
 };
+constexpr int kThreadsAx = 320;  // 10 warps: producer, MMA, 4 split, 4 epilogue
 
 // ---------------------------------------------------------------- Y = A·X
-// warps: 0 TMA producer, 1 hi-MMA issuer, 2 lo-MMA issuer, 3-6 split
-// (A_lo → TMEM), 7-10 epilogue
+// warps: 0 TMA producer, 1 MMA issuer, 2-5 split (A → A_hi, A_lo in TMEM,
+// thread = row = TMEM lane), 6-9 epilogue.  Both products of A take their
+// A operand from TMEM (TS form), so shared memory carries the A tile once
+// (TMA write, split read) plus the Xᵀ operand reads — 56 KB per 16 KB tile
+// instead of 72 KB with the A_hi MMA reading A from shared memory (the
+// ablation showed the pass shared-memory bound there).
 template <int N>
-__global__ void __launch_bounds__(kThreadsTC, 1)
+__global__ void __launch_bounds__(kThreadsAx, 1)
     ax_f32_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmXh,
                      const __grid_constant__ CUtensorMap tmXl, int64_t m, int l, int64_t ntiles, int KB,
                      const double* __restrict__ cx, double* __restrict__ Y) {
   using Cfg = AxCfg<N>;
-  constexpr int S = Cfg::kStages;
+  constexpr int S = Cfg::kStages, NS = Cfg::kNS;
   constexpr int KC = kKChunk / 32;  // k-blocks per unit
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + S * Cfg::kStage);
-  uint64_t* empty = full + S;       // hi commit + lo commit
-  uint64_t* lo_full = empty + S;    // 4 split warps (A_lo in TMEM)
-  uint64_t* tfree = lo_full + S;    // [kNS] A_lo slot free (lo commit)
-  uint64_t* ustart = tfree + Cfg::kNS;     // [2] first hi MMAs of unit u done (lo may accumulate), by u & 1
-  uint64_t* acc_full = ustart + 2;  // [2] hi commit + lo commit
+  uint64_t* empty = full + S;        // 4 split warps (A read) + MMA commit (Xᵀ read)
+  uint64_t* afull = empty + S;       // [NS] 4 split warps (A_hi, A_lo in TMEM)
+  uint64_t* tfree = afull + NS;      // [NS] MMA commit
+  uint64_t* acc_full = tfree + NS;   // [2] MMA commit
   uint64_t* acc_empty = acc_full + 2;  // [2] 4 epilogue warps
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -192,20 +186,20 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
   if (threadIdx.x == 0) {
     for (int s = 0; s < S; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 2);
-      mbar_init(&lo_full[s], 4);
+      mbar_init(&empty[s], 5);
     }
-    for (int a = 0; a < Cfg::kNS; ++a) mbar_init(&tfree[a], 1);
+    for (int a = 0; a < NS; ++a) {
+      mbar_init(&afull[a], 4);
+      mbar_init(&tfree[a], 1);
+    }
     for (int a = 0; a < 2; ++a) {
-      mbar_init(&ustart[a], 1);
-      mbar_init(&acc_full[a], 2);
+      mbar_init(&acc_full[a], 1);
       mbar_init(&acc_empty[a], 4);
     }
     fence_barrier_init();
   }
   if (warp == 1) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
-                 "n"(Cfg::kCols));
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_slot)));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   tc_fence_before();
@@ -231,88 +225,74 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
         }
         __syncwarp();
       }
-  } else if (warp == 1) {  // ---------------------------------------- hi-MMA issuer
-    // D[:, 0:2N] += A·[X_hi | X_lo] — one N = 2N MMA per k-step (the two Xᵀ
-    // chunks are adjacent in the stage: a 2N-row K-major operand)
+  } else if (warp == 1) {  // ------------------------------------------- MMA issuer
+    // D[:, 0:2N] += A_hi·[X_hi | X_lo]; D[:, 0:N] += A_lo·X_hi (A from TMEM)
     const bool leader = elect_one();
-    constexpr uint32_t idesc = idesc_tf32(128, 2 * N);
+    constexpr uint32_t idesc2 = idesc_tf32(128, 2 * N), idesc1 = idesc_tf32(128, N);
     Ring<S> rg;
+    Ring<NS> rt;
     int64_t u = -1;
     for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x)
-      for (int kb = 0; kb < KB; ++kb, rg.next()) {
+      for (int kb = 0; kb < KB; ++kb, rg.next(), rt.next()) {
         const int kin = kb & (KC - 1);
         if (kin == 0) {  // first stage of a unit: its accumulator must have been drained
           ++u;
           mbar_wait(&acc_empty[u & 1], (uint32_t)((u >> 1) & 1) ^ 1u);
           tc_fence_after();
         }
+        mbar_wait(&afull[rt.s], rt.ph);
         mbar_wait(&full[rg.s], rg.ph);
         tc_fence_after();
         const uint32_t d = tmem + (uint32_t)((u & 1) * Cfg::kW);
-        const uint32_t a0 = smem_u32(smem + rg.s * Cfg::kStage);
-        const uint64_t da = desc_sw128(a0), dx = desc_sw128(a0 + kTileBytes);
-        if (leader) {
-#pragma unroll
-          for (int ks = 0; ks < 4; ++ks) mma_tf32(d, da + 2 * ks, dx + 2 * ks, idesc, (kin != 0 || ks != 0) ? 1u : 0u);
-          mma_commit(&empty[rg.s]);
-          if (kin == 0) mma_commit(&ustart[u & 1]);
-          if (kb == KB - 1 || kin == KC - 1) mma_commit(&acc_full[u & 1]);
-        }
-        __syncwarp();
-      }
-  } else if (warp == 2) {  // ---------------------------------------- lo-MMA issuer
-    // D[:, 2N:3N] (+)= A_lo·X_hi with A_lo read from TMEM
-    const bool leader = elect_one();
-    constexpr uint32_t idesc = idesc_tf32(128, N);
-    Ring<S> rg;
-    Ring<Cfg::kNS> rt;
-    int64_t u = -1;
-    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x)
-      for (int kb = 0; kb < KB; ++kb, rg.next(), rt.next()) {
-        const int kin = kb & (KC - 1);
-        if (kin == 0) {  // the unit's accumulator was drained once the hi issuer started it
-          ++u;
-          mbar_wait(&ustart[u & 1], (uint32_t)((u >> 1) & 1));
-          tc_fence_after();
-        }
-        mbar_wait(&lo_full[rg.s], rg.ph);
-        tc_fence_after();
-        const uint32_t d = tmem + (uint32_t)((u & 1) * Cfg::kW + 2 * N);
-        const uint32_t at = tmem + (uint32_t)(Cfg::kSlot0 + 32 * rt.s);
+        const uint32_t ah = tmem + (uint32_t)(Cfg::kSlot0 + 64 * rt.s), al = ah + 32;
         const uint64_t dx = desc_sw128(smem_u32(smem + rg.s * Cfg::kStage) + kTileBytes);
         if (leader) {
 #pragma unroll
-          for (int ks = 0; ks < 4; ++ks) mma_tf32_ts(d, at + 8 * ks, dx + 2 * ks, idesc, (kin != 0 || ks != 0) ? 1u : 0u);
-          mma_commit(&empty[rg.s]);
+          for (int ks = 0; ks < 4; ++ks) {
+            mma_tf32_ts(d, ah + 8 * ks, dx + 2 * ks, idesc2, (kin != 0 || ks != 0) ? 1u : 0u);
+            mma_tf32_ts(d, al + 8 * ks, dx + 2 * ks, idesc1, 1u);
+          }
           mma_commit(&tfree[rt.s]);
+          mma_commit(&empty[rg.s]);
           if (kb == KB - 1 || kin == KC - 1) mma_commit(&acc_full[u & 1]);
         }
         __syncwarp();
       }
-  } else if (warp < 7) {  // ---------------------------------------- split: A_lo → TMEM
+  } else if (warp < 6) {  // ---------------------------------------- split: A → A_hi, A_lo in TMEM
     const int q = warp & 3;
     const int t = 32 * q + lane;  // tile row = TMEM lane
+    const uint32_t lane_off = (uint32_t)(32 * q) << 16;
     Ring<S> rg;
-    Ring<Cfg::kNS> rt;
+    Ring<NS> rt;
     for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x)
       for (int kb = 0; kb < KB; ++kb, rg.next(), rt.next()) {
         mbar_wait(&full[rg.s], rg.ph);
-        mbar_wait(&tfree[rt.s], rt.ph ^ 1u);
-        tc_fence_after();
         const uint8_t* row = smem + rg.s * Cfg::kStage + t * 128;
-        float v[32];
+        float hi[32], lo[32];
 #pragma unroll
         for (int c = 0; c < 8; ++c) {  // logical 16-byte chunk c (k = 4c..4c+3) sits at c ^ (t mod 8)
           const float4 x = *reinterpret_cast<const float4*>(row + ((c ^ (t & 7)) << 4));
-          v[4 * c] = lo_part(x.x);
-          v[4 * c + 1] = lo_part(x.y);
-          v[4 * c + 2] = lo_part(x.z);
-          v[4 * c + 3] = lo_part(x.w);
+          hi[4 * c] = x.x;
+          hi[4 * c + 1] = x.y;
+          hi[4 * c + 2] = x.z;
+          hi[4 * c + 3] = x.w;
         }
-        tmem_st32(tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(Cfg::kSlot0 + 32 * rt.s), v);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[rg.s]);  // the row is in registers
+#pragma unroll
+        for (int k = 0; k < 32; ++k) {
+          const float a = hi[k];
+          hi[k] = __uint_as_float(__float_as_uint(a) & 0xFFFFE000u);
+          lo[k] = a - hi[k];
+        }
+        mbar_wait(&tfree[rt.s], rt.ph ^ 1u);
+        tc_fence_after();
+        const uint32_t at = tmem + lane_off + (uint32_t)(Cfg::kSlot0 + 64 * rt.s);
+        tmem_st32(at, hi);
+        tmem_st32(at + 32, lo);
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(&lo_full[rg.s]);
+        if (lane == 0) mbar_arrive(&afull[rt.s]);
       }
   } else {  // ---------------------------------------------------- epilogue
     const int q = warp & 3;  // TMEM lane quarter this warp may access
@@ -326,16 +306,15 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
         const uint32_t d = tmem + (uint32_t)((u & 1) * Cfg::kW) + ((uint32_t)(32 * q) << 16);
 #pragma unroll
         for (int c0 = 0; c0 < N; c0 += 16) {
-          float v[16], w[16], z[16];
+          float v[16], w[16];
           tmem_ld16(d + c0, v);
           tmem_ld16(d + N + c0, w);
-          tmem_ld16(d + 2 * N + c0, z);
           if (row < m) {
 #pragma unroll
             for (int j = 0; j < 16; ++j)
               if (c0 + j < l) {
                 double* y = Y + row * l + c0 + j;
-                const double a = ((double)v[j] + (double)z[j]) + (double)w[j];
+                const double a = (double)v[j] + (double)w[j];
                 if (kc == 0) *y = cx ? a - cx[c0 + j] : a;
                 else *y += a;
               }
@@ -350,7 +329,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
   __syncthreads();
   if (warp == 1) {
     tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(Cfg::kCols));
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
   }
 }
 
@@ -667,7 +646,7 @@ void launch_ax(Ctx& c, const DenseA& A, const float* hi, const float* lo, int64_
   const int64_t ntiles = cdiv(A.m, 128);
   const int grid = (int)std::min<int64_t>(ntiles, c.num_sms);
   prof_pre(c);
-  ax_f32_tc_kernel<N><<<grid, kThreadsTC, Cfg::kSmem, c.stream>>>(tA, tH, tL, A.m, l, ntiles, (int)(Kpad / 32), cx,
+  ax_f32_tc_kernel<N><<<grid, kThreadsAx, Cfg::kSmem, c.stream>>>(tA, tH, tL, A.m, l, ntiles, (int)(Kpad / 32), cx,
                                                                    Y);
   RPCA_CHECK_LAUNCH();
   count_launch(c, 1, c.tag ? c.tag : "ax_f32_tc");
