@@ -42,7 +42,7 @@ PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
 TRAFFIC_PATH = os.path.join(ROOT, "profiles", "traffic.json")  # written by tools/gpu/make_traffic.py from ncu
 NCU_NAME = {"ax_f64_dmma": "ax_f64_tma_kernel", "aty_f64_dmma": "aty_f64_tma_kernel", "ax_f32_tc": "ax_f32_tc_kernel",
             "ax_f64_emu": "ax_f64_emu_kernel",
-            "aty_f32_tc": "aty_f32_tc_kernel", "csr_spmm": "csr_spmm_kernel"}
+            "aty_f32_tc": "aty_f32_tc_kernel", "csr_spmm": "csr_spmm"}
 
 
 def ncu_traffic(config, kernel):
