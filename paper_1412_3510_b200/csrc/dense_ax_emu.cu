@@ -207,27 +207,39 @@ __global__ void col_field_kernel(const double* __restrict__ X, int64_t K, int l,
 
 // X digit planes, block b of 32 k (kB bytes apart): rows n' = t·LPn + j
 // (plane t, column j), K-major core-matrix layout of desc_core; zero past K
-// and past l
+// and past l.  Thread = (column j, 16-k half c of block b): it digitises 16
+// elements of column j and writes one 16-byte core-matrix row per plane.
 __global__ void x_slices_kernel(const double* __restrict__ X, int64_t K, int l, int LPn, int64_t KB, int kB,
                                 const int* __restrict__ Gf, int8_t* __restrict__ Xs) {
-  const int64_t total = KB * 32 * LPn;
+  const int64_t total = KB * 2 * LPn;
   for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
        idx += (int64_t)gridDim.x * blockDim.x) {
     const int j = (int)(idx % LPn);
-    const int64_t k = idx / LPn;
-    const double x = (k < K && j < l) ? X[k * l + j] : 0.0;
-    uint32_t lo, hi;
+    const int64_t bc = idx / LPn, b = bc >> 1;
+    const int c = (int)(bc & 1);
     const int G = exp_of_field(j < l ? Gf[j] : 0);
-    biased(G < -960 ? x * pow2(-960 - G) : x, scale_of(G), lo, hi);
-    const unsigned long long U = ((unsigned long long)hi << 32) | lo;
-    const int64_t b = k >> 5;
-    const int kk = (int)(k & 31);
+    const double pre = G < -960 ? pow2(-960 - G) : 1.0, scale = scale_of(G);
+    uint32_t w[kDigits][4];
+#pragma unroll
+    for (int g = 0; g < 4; ++g) {
+      uint32_t lo[4], hi[4];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int64_t k = b * 32 + c * 16 + 4 * g + e;
+        const double x = (k < K && j < l) ? X[k * l + j] : 0.0;
+        biased(x * pre, scale, lo[e], hi[e]);
+      }
+      uint32_t pw[kDigits];
+      planes4(lo, hi, pw);
+#pragma unroll
+      for (int t = 0; t < kDigits; ++t) w[t][g] = pw[t];
+    }
     int8_t* blk = Xs + b * (int64_t)kB;
 #pragma unroll
     for (int t = 0; t < kDigits; ++t) {
       const int np = t * LPn + j;
-      blk[((np >> 3) * 2 + (kk >> 4)) * 128 + (np & 7) * 16 + (kk & 15)] =
-          (int8_t)(((U >> (8 * (7 - t))) & 0xFF) ^ 0x80);
+      *reinterpret_cast<uint4*>(blk + ((np >> 3) * 2 + c) * 128 + (np & 7) * 16) =
+          make_uint4(w[t][0], w[t][1], w[t][2], w[t][3]);
     }
   }
 }
@@ -596,7 +608,7 @@ void dense_ax_emu(Ctx& c, const DenseA& A, const int* E, const double* X, int l,
     count_launch(c, 1, "emu_x_exp");
   }
   {
-    const int64_t total = (int64_t)KB * 32 * LPn;
+    const int64_t total = (int64_t)KB * 2 * LPn;
     const unsigned grid = (unsigned)std::min<int64_t>(cdiv(total, 256), (int64_t)c.num_sms * 8);
     x_slices_kernel<<<grid, 256, 0, c.stream>>>(X, A.n, l, LPn, KB, kB, Gf, Xs);
     RPCA_CHECK_LAUNCH();
