@@ -126,7 +126,7 @@ __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 
 #ifndef ATY_SLOTS
-#define ATY_SLOTS 4
+#define ATY_SLOTS 2
 #endif
 constexpr int kTileBytes = 128 * 128;  // 16 KB A tile
 constexpr int kKChunk = 4096;          // max products per fp32 accumulation (Q15)
@@ -345,7 +345,8 @@ struct AtyPlan {
 template <int N>
 struct AtyCfg {
   static constexpr int kX = N * 128;  // one Yᵀ chunk: N rows × 32 fp32
-  static constexpr int kTN = N <= 32 ? 32 : 64;  // TMEM columns per column-block accumulator
+  // [0, N) A_hi·Y_hi + A_lo·Y_hi, [N, 2N) A_hi·Y_lo (one N = 2N MMA)
+  static constexpr int kTN = 2 * N <= 32 ? 32 : (2 * N <= 64 ? 64 : 128);
   static constexpr int kYS = 3;  // Yᵀ chunk buffers
   static constexpr int kYBytes = kYS * 2 * kX;
   static constexpr int kStages = (212 * 1024 - kYBytes) / kTileBytes > 8 ? 8 : (212 * 1024 - kYBytes) / kTileBytes;
@@ -448,7 +449,7 @@ __global__ void __launch_bounds__(kThreadsAty, 1)
     // D_cb += A_hi·Y_hi + A_hi·Y_lo + A_lo·Y_hi, A_hi/A_lo from TMEM (lane =
     // column of A, one TMEM column per row of A)
     const bool leader = elect_one();
-    constexpr uint32_t idesc = idesc_tf32(128, N);
+    constexpr uint32_t idesc = idesc_tf32(128, N), idesc2 = idesc_tf32(128, 2 * N);
     Ring<YS> ry;
     Ring<NS> rt;
     int kin = 0;        // row chunks into the current accumulation chunk
@@ -458,7 +459,7 @@ __global__ void __launch_bounds__(kThreadsAty, 1)
       mbar_wait(&yfull[ry.s], ry.ph);
       tc_fence_after();
       const uint32_t yh = smem_u32(ybuf + ry.s * 2 * Cfg::kX);
-      const uint64_t dh = desc_sw128(yh), dl = desc_sw128(yh + Cfg::kX);
+      const uint64_t dh = desc_sw128(yh);  // Y_hi rows [0, N) then Y_lo rows [N, 2N): one 2N-row operand
       for (int cbi = 0; cbi < ncb; ++cbi, rt.next()) {
         // a new accumulation chunk overwrites block cbi: its previous sums
         // must have been read out (per block, so the flush of the last blocks
@@ -471,8 +472,7 @@ __global__ void __launch_bounds__(kThreadsAty, 1)
         if (leader) {
 #pragma unroll
           for (int ks = 0; ks < 4; ++ks) {
-            mma_tf32_ts(d, ah + 8 * ks, dh + 2 * ks, idesc, (kin != 0 || ks != 0) ? 1u : 0u);
-            mma_tf32_ts(d, ah + 8 * ks, dl + 2 * ks, idesc, 1u);
+            mma_tf32_ts(d, ah + 8 * ks, dh + 2 * ks, idesc2, (kin != 0 || ks != 0) ? 1u : 0u);
             mma_tf32_ts(d, al + 8 * ks, dh + 2 * ks, idesc, 1u);
           }
           mma_commit(&tfree[rt.s]);
@@ -527,14 +527,20 @@ __global__ void __launch_bounds__(kThreadsAty, 1)
       for (int cbi = 0; cbi < ncb; ++cbi) {
         double* dst = part + (((int64_t)p * pl.CBG + cbi) * 128 + 32 * q + lane) * N;
         const uint32_t d = tmem + (uint32_t)(cbi * Cfg::kTN) + ((uint32_t)(32 * q) << 16);
-        float v[N];
 #pragma unroll
-        for (int c0 = 0; c0 < N; c0 += 16) tmem_ld16(d + c0, *reinterpret_cast<float(*)[16]>(v + c0));
+        for (int c0 = 0; c0 < N; c0 += 16) {
+          float v[16], w[16];
+          tmem_ld16(d + c0, v);
+          tmem_ld16(d + N + c0, w);
+#pragma unroll
+          for (int j = 0; j < 16; ++j) {
+            const double a = (double)v[j] + (double)w[j];
+            dst[c0 + j] = ch == 0 ? a : dst[c0 + j] + a;
+          }
+        }
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(&acc_empty[cbi]);  // block cbi may take the next chunk
-#pragma unroll
-        for (int j = 0; j < N; ++j) dst[j] = ch == 0 ? (double)v[j] : dst[j] + (double)v[j];
+        if (lane == 0) mbar_arrive(&acc_empty[cbi]);
       }
     }
     if (nch == 0) {  // no rows: zero partial
