@@ -23,6 +23,9 @@ constexpr int kWarps = 8;
 __device__ __forceinline__ void cp_async8(double* dst, const double* src) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
 }
+__device__ __forceinline__ void cp_async16(double* dst, const double* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void cp_async_wait() {
@@ -35,11 +38,22 @@ int stride_for(int LP) {
   return s;
 }
 
-// stage rows [r0, r0+64) of X (l columns) into T (128 × s); zeros past rows /
-// past l (the padded columns up to LP are read by the fragments)
+// stage rows [r0, r0+64) of X (l columns) into T (64 × s); zeros past rows /
+// past l (the padded columns up to LP are read by the fragments).  vec: l even
+// and X 16-byte aligned — 16-byte copies (s is even, so T's rows stay aligned)
 __device__ __forceinline__ void stage(double* T, const double* __restrict__ X, int64_t rows, int l, int LP, int s,
-                                      int64_t r0) {
+                                      int64_t r0, bool vec) {
   const int nr = (int)imin64(kRows, rows - r0);
+  if (vec) {
+    const int hp = LP / 2;
+    for (int idx = threadIdx.x; idx < kRows * hp; idx += blockDim.x) {
+      const int r = idx / hp, cc = 2 * (idx - r * hp);
+      double* d = T + r * s + cc;
+      if (r < nr && cc < l) cp_async16(d, X + (r0 + r) * l + cc);
+      else d[0] = d[1] = 0.0;
+    }
+    return;
+  }
   for (int idx = threadIdx.x; idx < kRows * LP; idx += blockDim.x) {
     const int r = idx / LP, cc = idx - r * LP;
     double* d = T + r * s + cc;
@@ -48,89 +62,120 @@ __device__ __forceinline__ void stage(double* T, const double* __restrict__ X, i
   }
 }
 
-template <int NB>
+__device__ __forceinline__ void cp_async_wait_dyn(int n) {
+  if (n <= 0) cp_async_wait<0>();
+  else if (n == 1) cp_async_wait<1>();
+  else cp_async_wait<2>();
+}
+
+// The 8×8 blocks of G (bi ≤ bj when Y = X) are split over BG warp groups
+// (block q·BG + g to group g) and the 16 four-row k-steps of a tile over the
+// KS = 8/BG warps of a group, so every warp issues the same number of DMMAs
+// and one fragment load per block row serves all of its blocks.
+template <int NB, bool SAME>
+struct GramCfg {
+  static constexpr int kPairs = SAME ? NB * (NB + 1) / 2 : NB * NB;
+  static constexpr int BG = kPairs <= 18 ? 1 : (kPairs <= 36 ? 2 : 4);
+  static constexpr int KS = kWarps / BG;
+  static constexpr int kAcc = (kPairs + BG - 1) / BG;
+};
+
+template <int NB, bool SAME>
+size_t gram_red_bytes() {
+  using C = GramCfg<NB, SAME>;
+  return (size_t)C::KS * C::kPairs * 64 * sizeof(double);
+}
+
+template <int NB, bool SAME>
 __global__ void __launch_bounds__(256) gram_dmma_kernel(const double* __restrict__ X, const double* __restrict__ Y,
-                                                        int64_t rows, int l, int s, int64_t ntiles,
+                                                        int64_t rows, int l, int s, int64_t ntiles, int nst, int vec,
                                                         double* __restrict__ part) {
+  using C = GramCfg<NB, SAME>;
   constexpr int LP = 8 * NB;
-  constexpr int kMaxPairs = (NB * NB + kWarps - 1) / kWarps;
-  extern __shared__ double sm[];
-  const bool same = (X == Y);
+  extern __shared__ __align__(16) double sm[];
   const int tile_elems = kRows * s;
-  double* ybase = same ? sm : sm + 2 * tile_elems;  // buffers b at +b·tile_elems
+  const int buf_elems = (SAME ? 1 : 2) * tile_elems;  // X tile, then Y tile
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = warp % C::BG, ksl = warp / C::BG;
   const int64_t t0 = ntiles * blockIdx.x / gridDim.x, t1 = ntiles * (blockIdx.x + 1) / gridDim.x;
-
-  // this warp's blocks of G: pairs p = warp, warp+8, … of the (bi, bj) list
-  const int npairs = same ? NB * (NB + 1) / 2 : NB * NB;
-  int bi[kMaxPairs], bj[kMaxPairs];
-  int np = 0;
+  auto stage_tile = [&](int b, int64_t t) {
+    stage(sm + b * buf_elems, X, rows, l, LP, s, t * kRows, vec);
+    if (!SAME) stage(sm + b * buf_elems + tile_elems, Y, rows, l, LP, s, t * kRows, vec);
+  };
+  double acc[C::kAcc][2];
 #pragma unroll
-  for (int q = 0; q < kMaxPairs; ++q) {
-    const int p = warp + q * kWarps;
-    bi[q] = bj[q] = 0;
-    if (p < npairs) {
-      ++np;
-      if (same) {  // row-major upper triangle
-        int a = 0, rem = p;
-        while (rem >= NB - a) { rem -= NB - a; ++a; }
-        bi[q] = a;
-        bj[q] = a + rem;
-      } else {
-        bi[q] = p / NB;
-        bj[q] = p % NB;
-      }
-    }
-  }
-  double acc[kMaxPairs][2];
-#pragma unroll
-  for (int q = 0; q < kMaxPairs; ++q) acc[q][0] = acc[q][1] = 0.0;
+  for (int q = 0; q < C::kAcc; ++q) acc[q][0] = acc[q][1] = 0.0;
 
-  if (t0 < t1) {
-    stage(sm, X, rows, l, LP, s, t0 * kRows);
-    if (!same) stage(ybase, Y, rows, l, LP, s, t0 * kRows);
+  // ring of nst tiles: tile t's copy group is complete once at most nst − 2
+  // younger groups are pending (one group is committed per tile, empty or not)
+  for (int i = 0; i < nst - 1; ++i) {
+    if (t0 + i < t1) stage_tile(i, t0 + i);
     cp_async_commit();
   }
   const int kr = lane & 3, kc = lane >> 2;
   for (int64_t t = t0; t < t1; ++t) {
-    const int b = (int)((t - t0) & 1);
-    if (t + 1 < t1) {
-      stage(sm + (b ^ 1) * tile_elems, X, rows, l, LP, s, (t + 1) * kRows);
-      if (!same) stage(ybase + (b ^ 1) * tile_elems, Y, rows, l, LP, s, (t + 1) * kRows);
-      cp_async_commit();
-      cp_async_wait<1>();
-    } else {
-      cp_async_wait<0>();
-    }
-    __syncthreads();
-    const double* xs = sm + b * tile_elems;
-    const double* ys = ybase + b * tile_elems;
-#pragma unroll 4
-    for (int k4 = 0; k4 < kRows; k4 += 4) {
+    const int b = (int)((t - t0) % nst);
+    cp_async_wait_dyn(nst - 2);
+    __syncthreads();  // tile t visible; every warp is done with tile t − 1's buffer
+    if (t + nst - 1 < t1) stage_tile((b + nst - 1) % nst, t + nst - 1);
+    cp_async_commit();
+    const double* xs = sm + b * buf_elems;
+    const double* ys = SAME ? xs : xs + tile_elems;
+#pragma unroll
+    for (int kk = 0; kk < 16 / C::KS; ++kk) {
+      const int k4 = 4 * (ksl + C::KS * kk);
       const double* xr = xs + (k4 + kr) * s + kc;
       const double* yr = ys + (k4 + kr) * s + kc;
+      double fx[NB], fy[NB];
 #pragma unroll
-      for (int q = 0; q < kMaxPairs; ++q)
-        if (q < np) dmma(acc[q], xr[bi[q] * 8], yr[bj[q] * 8]);
+      for (int a = 0; a < NB; ++a) {
+        fx[a] = xr[a * 8];
+        fy[a] = SAME ? fx[a] : yr[a * 8];
+      }
+      int idx = 0;
+#pragma unroll
+      for (int a = 0; a < NB; ++a)
+#pragma unroll
+        for (int bb = SAME ? a : 0; bb < NB; ++bb, ++idx)
+          if (idx % C::BG == g) dmma(acc[idx / C::BG], fx[a], fy[bb]);
     }
-    __syncthreads();
   }
+  cp_async_wait<0>();
+  __syncthreads();
+  // fixed-order sum of the KS k-slices: red[(ksl·kPairs + p)·64 + lane·2 + e]
+  double* red = sm;
+#pragma unroll
+  for (int q = 0; q < C::kAcc; ++q) {
+    const int p = q * C::BG + g;
+    if (p < C::kPairs) {
+      red[(ksl * C::kPairs + p) * 64 + lane * 2] = acc[q][0];
+      red[(ksl * C::kPairs + p) * 64 + lane * 2 + 1] = acc[q][1];
+    }
+  }
+  __syncthreads();
   // partial G of this CTA (d = {D[kc][2kr], D[kc][2kr+1]}); mirrored when Y = X
   double* G = part + (int64_t)blockIdx.x * l * l;
+  for (int idx = threadIdx.x; idx < C::kPairs * 64; idx += blockDim.x) {
+    const int p = idx >> 6, ln = (idx >> 1) & 31, e = idx & 1;
+    double v = 0.0;
 #pragma unroll
-  for (int q = 0; q < kMaxPairs; ++q) {
-    if (q >= np) continue;
-    const int i = bi[q] * 8 + kc;
-#pragma unroll
-    for (int e = 0; e < 2; ++e) {
-      const int j = bj[q] * 8 + 2 * kr + e;
-      if (i < l && j < l) {
-        G[i * l + j] = acc[q][e];
-        if (same && bi[q] != bj[q]) G[j * l + i] = acc[q][e];
-      }
+    for (int k = 0; k < C::KS; ++k) v += red[(k * C::kPairs + p) * 64 + ln * 2 + e];
+    int bi, bj;
+    if (SAME) {  // row-major upper triangle
+      int a = 0, rem = p;
+      while (rem >= NB - a) { rem -= NB - a; ++a; }
+      bi = a;
+      bj = a + rem;
+    } else {
+      bi = p / NB;
+      bj = p % NB;
+    }
+    const int i = bi * 8 + (ln >> 2), j = bj * 8 + 2 * (ln & 3) + e;
+    if (i < l && j < l) {
+      G[i * l + j] = v;
+      if (SAME && bi != bj) G[j * l + i] = v;
     }
   }
-  (void)LP;
 }
 
 // v[j] = Σ_b part[b][j]: 32 entries per CTA, the 8 warps take partials
@@ -157,6 +202,48 @@ int gram_ctas(Ctx& c, int64_t rows) {
   return (int)std::min<int64_t>(ntiles, (int64_t)c.num_sms * 2);
 }
 
+template <int NB, bool SAME>
+void launch_gram_nb(Ctx& c, const double* X, const double* Y, int64_t rows, int l, int s, int64_t ntiles, int& grid,
+                    double* part) {
+  const size_t buf = (size_t)(SAME ? 1 : 2) * kRows * s * sizeof(double);
+  // deepest ring (≤ 4 tiles) that leaves two CTAs per SM, else one
+  int nst = 4;
+  while (nst > 2 && nst * buf > 110 * 1024) --nst;
+  if (nst == 2 && 3 * buf <= 220 * 1024) nst = 3;
+  const size_t smem = std::max(nst * buf, gram_red_bytes<NB, SAME>());
+  const void* fn = (const void*)gram_dmma_kernel<NB, SAME>;
+  ensure_smem(fn, (int)smem);
+  int occ = 1;
+  RPCA_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, 256, smem));
+  grid = (int)std::min<int64_t>(grid, (int64_t)c.num_sms * std::max(1, occ));  // one wave: fixed tile ranges
+  const int vec = (l % 2 == 0) && (reinterpret_cast<uintptr_t>(X) & 15) == 0 &&
+                  (reinterpret_cast<uintptr_t>(Y) & 15) == 0;
+  gram_dmma_kernel<NB, SAME><<<grid, 256, smem, c.stream>>>(X, Y, rows, l, s, ntiles, nst, vec, part);
+}
+
+// the partial count is returned through `grid` (≤ gram_ctas)
+void launch_gram(Ctx& c, const double* X, const double* Y, int64_t rows, int l, int LP, int s, int64_t ntiles,
+                 int& grid, double* part) {
+  const bool same = X == Y;
+#define RPCA_GRAM(NBV)                                                                            \
+  case NBV:                                                                                       \
+    if (same) launch_gram_nb<NBV, true>(c, X, Y, rows, l, s, ntiles, grid, part);                 \
+    else launch_gram_nb<NBV, false>(c, X, Y, rows, l, s, ntiles, grid, part);                     \
+    break;
+  switch (LP / 8) {
+    RPCA_GRAM(1)
+    RPCA_GRAM(2)
+    RPCA_GRAM(3)
+    RPCA_GRAM(4)
+    RPCA_GRAM(5)
+    RPCA_GRAM(6)
+    RPCA_GRAM(7)
+    RPCA_GRAM(8)
+    default: RPCA_REQUIRE(false, RPCA_E_SHAPE, "gram: l=%d", l);
+  }
+#undef RPCA_GRAM
+}
+
 }  // namespace
 
 size_t gram_ws_bytes(Ctx& c, int64_t rows, int l) {
@@ -173,27 +260,9 @@ void gram(Ctx& c, const double* X, const double* Y, int64_t rows, int l, double*
   }
   const int LP = (l + 7) / 8 * 8, s = stride_for(LP);
   const int64_t ntiles = cdiv(rows, kRows);
-  const int grid = gram_ctas(c, rows);
+  int grid = gram_ctas(c, rows);
   double* part = ar.get<double>((size_t)grid * l * l);
-  const size_t smem = (size_t)(X == Y ? 2 : 4) * kRows * s * sizeof(double);
-#define RPCA_GRAM(NBV)                                                                                    \
-  case NBV:                                                                                               \
-    ensure_smem((const void*)gram_dmma_kernel<NBV>, 4 * kRows * 68 * 8);                                  \
-    gram_dmma_kernel<NBV><<<grid, 256, smem, c.stream>>>(X, Y, rows, l, s, ntiles, part);                 \
-    break;
-  switch (LP / 8) {
-    RPCA_GRAM(1)
-    RPCA_GRAM(2)
-    RPCA_GRAM(3)
-    RPCA_GRAM(4)
-    RPCA_GRAM(5)
-    RPCA_GRAM(6)
-    RPCA_GRAM(7)
-    default: ensure_smem((const void*)gram_dmma_kernel<8>, 4 * kRows * 68 * 8);
-      gram_dmma_kernel<8><<<grid, 256, smem, c.stream>>>(X, Y, rows, l, s, ntiles, part);
-      break;
-  }
-#undef RPCA_GRAM
+  launch_gram(c, X, Y, rows, l, LP, s, ntiles, grid, part);
   RPCA_CHECK_LAUNCH();
   count_launch(c, 1, c.tag ? c.tag : "gram");
   sum_parts_kernel<<<(unsigned)cdiv(l * l, 32), 256, 0, c.stream>>>(part, grid, l * l, G);
