@@ -431,10 +431,13 @@ int oracle_jacobi_svd(double* G, int64_t n, int64_t l, double* sigma, double* W)
       for (int64_t q = p + 1; q < l; ++q) {
         double a, b, g;
         colpair_dots(G, n, l, p, q, &a, &b, &g);
-        if (!(fabs(g) > eps * sqrt(a * b))) continue;
+        /* √a·√b and hypot(1, ζ), not √(ab) and √(1+ζ²): the products
+           overflow for columns of norm above 2^256 (a rotation test that is
+           never true there would return the column norms of G as σ) */
+        if (!(fabs(g) > eps * sqrt(a) * sqrt(b))) continue;
         rotated = 1;
         double zeta = (b - a) / (2.0 * g);
-        double t = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
+        double t = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + hypot(1.0, zeta));
         double cs = 1.0 / sqrt(1.0 + t * t), sn = cs * t;
 #pragma omp parallel for schedule(static)
         for (int64_t i = 0; i < n; ++i) {
@@ -498,10 +501,10 @@ int oracle_jacobi_eig(double* S, int64_t l, double* mu, double* E) {
     for (int64_t p = 0; p < l - 1; ++p)
       for (int64_t q = p + 1; q < l; ++q) {
         double apq = S[p * l + q], app = S[p * l + p], aqq = S[q * l + q];
-        if (!(fabs(apq) > eps * sqrt(fabs(app * aqq)))) continue;
+        if (!(fabs(apq) > eps * sqrt(fabs(app)) * sqrt(fabs(aqq)))) continue; /* no overflow of app·aqq */
         rotated = 1;
         double zeta = (aqq - app) / (2.0 * apq);
-        double t = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
+        double t = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + hypot(1.0, zeta));
         double c = 1.0 / sqrt(1.0 + t * t), s = c * t;
         for (int64_t r = 0; r < l; ++r) { /* S ← S J (columns p,q) */
           double x = S[r * l + p], y = S[r * l + q];

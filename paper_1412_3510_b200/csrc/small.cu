@@ -20,6 +20,61 @@ namespace {
 constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
 
+// Zero-σ completion (rare): column col of Vout (l×l row-major) with σ = 0 is
+// replaced by the Gram–Schmidt residual of the first e_t that keeps a norm
+// ≥ 1/2 against the other columns (the largest residual if none does).
+__device__ void complete_zero_sigma(const double* sigma, double* Vout, int l) {
+  for (int col = 0; col < l; ++col) {
+    if (sigma[col] > 0.0) continue;
+    double best = -1.0;
+    double v[kMaxL], bv[kMaxL];
+    for (int t = 0; t < l; ++t) {
+      for (int i = 0; i < l; ++i) v[i] = (i == t) ? 1.0 : 0.0;
+      for (int pass = 0; pass < 2; ++pass)
+        for (int s = 0; s < l; ++s) {
+          if (s == col || (sigma[s] == 0.0 && s > col)) continue;
+          double d = 0.0;
+          for (int i = 0; i < l; ++i) d += Vout[i * l + s] * v[i];
+          for (int i = 0; i < l; ++i) v[i] -= d * Vout[i * l + s];
+        }
+      double nv = 0.0;
+      for (int i = 0; i < l; ++i) nv += v[i] * v[i];
+      nv = sqrt(nv);
+      if (nv > best) {
+        best = nv;
+        for (int i = 0; i < l; ++i) bv[i] = v[i];
+      }
+      if (nv >= 0.5) break;
+    }
+    for (int i = 0; i < l; ++i) Vout[i * l + col] = bv[i] / best;
+  }
+}
+
+// Jacobi rotation zeroing γ between columns of squared norms α (lower index)
+// and β: t = tan θ = sign(β−α)·2γ / (|β−α| + h), h = √((β−α)² + 4γ²), and
+// since 1 + t² = 2h·d / d² with d = |β−α| + h:  cs = d/√(2hd), sn = ±2γ/√(2hd).
+// One square root and one reciprocal square root on the dependent chain (the
+// reciprocal of d, for tγ = the norm update, runs beside the latter).  The
+// operands are O(l) after the 2^-E prescale of R, so no hypot scaling.
+__device__ __forceinline__ void jacobi_rotation(double al, double be, double g, double& cs, double& sn,
+                                                double& tg) {
+  const double tau = be - al, sig = tau >= 0.0 ? 2.0 * g : -2.0 * g;
+  const double h = sqrt(fma(tau, tau, sig * sig));
+  const double d = fabs(tau) + h;
+  const double r = rsqrt(2.0 * h * d);
+  cs = d * r;
+  sn = sig * r;
+  tg = sig * g * rcp_nr(d);
+}
+
+// 2^-E with 2^E ≥ max |x| (the exponent field of the max |x|, clamped so both
+// 2^±E are normal): applied to R it is exact and bounds every norm by O(l)
+__device__ __forceinline__ int scale_exp_of(unsigned hi_max) {
+  const int f = (int)(hi_max >> 20);  // biased exponent of the largest |R_ij|
+  return f == 0 ? 0 : max(-1000, min(1000, f - 1022));
+}
+__device__ __forceinline__ double pow2(int e) { return __hiloint2double((1023 + e) << 20, 0); }
+
 constexpr int kJThreads = 1024;  // one warp per column pair: l/2 ≤ 32 pairs in flight
 
 __global__ void __launch_bounds__(kJThreads) jacobi_kernel(const double* __restrict__ R, int l,
@@ -33,11 +88,21 @@ __global__ void __launch_bounds__(kJThreads) jacobi_kernel(const double* __restr
   __shared__ double nrm2[kMaxL];  // ‖M[:, p]‖², refreshed every sweep, updated by each rotation
   __shared__ int rank_[kMaxL];
   __shared__ int rotated[2];
+  __shared__ unsigned hmax;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int nthr = blockDim.x, nwarp = nthr >> 5;  // one warp per pair of a round
+  if (tid == 0) hmax = 0u;
+  __syncthreads();
+  unsigned hm = 0u;
+  for (int idx = tid; idx < l * l; idx += nthr) hm = max(hm, (unsigned)__double2hiint(R[idx]) & 0x7FFFFFFFu);
+  hm = __reduce_max_sync(0xffffffffu, hm);
+  if (lane == 0) atomicMax(&hmax, hm);
+  __syncthreads();
+  const int E = scale_exp_of(hmax);
+  const double down = pow2(-E);
   for (int idx = tid; idx < l * l; idx += nthr) {
     const int i = idx / l, p = idx % l;
-    Mc[p * l + i] = R[idx];
+    Mc[p * l + i] = R[idx] * down;
     Wc[p * l + i] = (i == p) ? 1.0 : 0.0;
   }
   if (tid < 2) rotated[tid] = 0;
@@ -71,15 +136,12 @@ __global__ void __launch_bounds__(kJThreads) jacobi_kernel(const double* __restr
           const double g = warp_sum(fma(x0, y0, x1 * y1));
           const double a = nrm2[p], b = nrm2[q];
           if (g * g > eps2 * (a * b)) {
-            // t = tan θ = sign(ζ)/(|ζ| + √(1+ζ²)), ζ = (β−α)/(2γ), written as
-            // sign(β−α)·2γ / (|β−α| + hypot(β−α, 2γ)): one hypot, one reciprocal
-            const double tau = b - a, sig = 2.0 * g;
-            const double t = (tau >= 0.0 ? sig : -sig) * rcp_nr(fabs(tau) + hypot(tau, sig));
-            const double cs = rsqrt(fma(t, t, 1.0)), sn = cs * t;
+            double cs, sn, tg;
+            jacobi_rotation(a, b, g, cs, sn, tg);
             if (lane == 0) {
               rotated[sweep & 1] = 1;
-              nrm2[p] = fma(-t, g, a);
-              nrm2[q] = fma(t, g, b);
+              nrm2[p] = a - tg;
+              nrm2[q] = b + tg;
             }
             if (lane < l) {
               Mc[p * l + lane] = cs * x0 - sn * y0;
@@ -125,36 +187,104 @@ __global__ void __launch_bounds__(kJThreads) jacobi_kernel(const double* __restr
     Wout[i * l + rp] = Wc[p * l + i];
     Vout[i * l + rp] = nrm[p] > 0.0 ? Mc[p * l + i] / nrm[p] : 0.0;
   }
-  if (tid < l) sigma[rank_[tid]] = nrm[tid];
+  if (tid < l) sigma[rank_[tid]] = nrm[tid] * pow2(E);
   __syncthreads();
   __threadfence_block();
-  // zero-σ completion (rare): Gram–Schmidt of e_t against the other columns
-  if (tid == 0) {
-    for (int col = 0; col < l; ++col) {
-      if (sigma[col] > 0.0) continue;
-      double best = -1.0;
-      double v[kMaxL], bv[kMaxL];
-      for (int t = 0; t < l; ++t) {
-        for (int i = 0; i < l; ++i) v[i] = (i == t) ? 1.0 : 0.0;
-        for (int pass = 0; pass < 2; ++pass)
-          for (int s = 0; s < l; ++s) {
-            if (s == col || (sigma[s] == 0.0 && s > col)) continue;
-            double d = 0.0;
-            for (int i = 0; i < l; ++i) d += Vout[i * l + s] * v[i];
-            for (int i = 0; i < l; ++i) v[i] -= d * Vout[i * l + s];
-          }
-        double nv = 0.0;
-        for (int i = 0; i < l; ++i) nv += v[i] * v[i];
-        nv = sqrt(nv);
-        if (nv > best) {
-          best = nv;
-          for (int i = 0; i < l; ++i) bv[i] = v[i];
-        }
-        if (nv >= 0.5) break;
-      }
-      for (int i = 0; i < l; ++i) Vout[i * l + col] = bv[i] / best;
-    }
+  if (tid == 0) complete_zero_sigma(sigma, Vout, l);
+}
+
+// The same sweeps for l ≤ 32 in one warp, lane p owning column p of M and of
+// W in registers: a round exchanges the partner's column by shuffles, both
+// lanes of a pair compute the identical γ (same products, same order) and
+// hence the identical rotation, and no barrier separates the rounds.
+template <int LP>
+__global__ void __launch_bounds__(32) jacobi_warp_kernel(const double* __restrict__ R, int l,
+                                                         double* __restrict__ sigma, double* __restrict__ Wout,
+                                                         double* __restrict__ Vout) {
+  const unsigned full = 0xffffffffu;
+  const int p = threadIdx.x;
+  double m[LP], w[LP], y[LP];
+  unsigned hm = 0u;
+#pragma unroll
+  for (int i = 0; i < LP; ++i) {
+    m[i] = (i < l && p < l) ? R[i * l + p] : 0.0;
+    w[i] = (i == p) ? 1.0 : 0.0;
+    hm = max(hm, (unsigned)__double2hiint(m[i]) & 0x7FFFFFFFu);
   }
+  const int E = scale_exp_of(__reduce_max_sync(full, hm));
+  const double down = pow2(-E);
+#pragma unroll
+  for (int i = 0; i < LP; ++i) m[i] *= down;
+  const int lp = (l + 1) & ~1;
+  const double eps = 0x1p-52 * (double)l, eps2 = eps * eps;
+  for (int sweep = 0; sweep < 30 && l > 1; ++sweep) {
+    double a = 0.0;
+#pragma unroll
+    for (int i = 0; i < LP; ++i) a = fma(m[i], m[i], a);
+    bool any = false;
+    for (int round = 0; round < lp - 1; ++round) {
+      // position of player p (inverse of player() in jacobi_kernel), its partner
+      int q;
+      if (p >= lp) q = p;
+      else {
+        int pos = 0;
+        if (p > 0) { const int v = p - 1 - round; pos = 1 + (v < 0 ? v + (lp - 1) : v); }
+        const int k = lp - 1 - pos;
+        const int v = k - 1 + round;
+        q = k == 0 ? 0 : 1 + (v >= lp - 1 ? v - (lp - 1) : v);
+      }
+      const bool pair = p < l && q < l;
+      const int src = pair ? q : p;
+      double g0 = 0.0, g1 = 0.0;
+#pragma unroll
+      for (int i = 0; i < LP; ++i) {
+        y[i] = __shfl_sync(full, m[i], src);
+        if (i & 1) g1 = fma(m[i], y[i], g1); else g0 = fma(m[i], y[i], g0);
+      }
+      const double g = g0 + g1;
+      const double b = __shfl_sync(full, a, src);
+      const bool lo = p < q;
+      const double al = lo ? a : b, be = lo ? b : a;
+      const bool act = pair && g * g > eps2 * (al * be);
+      if (!__any_sync(full, act)) continue;
+      any |= act;
+      double cs = 1.0, sn = 0.0;
+      if (act) {
+        double tg;
+        jacobi_rotation(al, be, g, cs, sn, tg);
+        a = lo ? al - tg : be + tg;
+        if (!lo) sn = -sn;  // hi column: sn·x + cs·y = cs·own − (−sn)·partner
+      }
+#pragma unroll
+      for (int i = 0; i < LP; ++i) {
+        const double wq = __shfl_sync(full, w[i], src);
+        m[i] = cs * m[i] - sn * y[i];
+        w[i] = cs * w[i] - sn * wq;
+      }
+    }
+    if (!__any_sync(full, any)) break;
+  }
+  double s = 0.0;
+#pragma unroll
+  for (int i = 0; i < LP; ++i) s += m[i] * m[i];
+  const double nrm = sqrt(s);
+  int r = 0;
+  for (int i = 0; i < l; ++i) {
+    const double ni = __shfl_sync(full, nrm, i);
+    r += (ni > nrm) || (ni == nrm && i < p);
+  }
+  if (p < l) {
+#pragma unroll
+    for (int i = 0; i < LP; ++i)
+      if (i < l) {
+        Wout[i * l + r] = w[i];
+        Vout[i * l + r] = nrm > 0.0 ? m[i] / nrm : 0.0;
+      }
+    sigma[r] = nrm * pow2(E);
+  }
+  __syncwarp();
+  __threadfence_block();
+  if (p == 0) complete_zero_sigma(sigma, Vout, l);
 }
 
 
@@ -270,9 +400,9 @@ __global__ void __launch_bounds__(kThreads) sqrt_inv_kernel(const double* __rest
         double c = 1.0, s = 0.0;
         if (q < l) {
           const double apq = A[p * l + q], app = A[p * l + p], aqq = A[q * l + q];
-          if (fabs(apq) > eps * sqrt(fabs(app * aqq))) {
+          if (fabs(apq) > eps * sqrt(fabs(app)) * sqrt(fabs(aqq))) {  // no overflow of app·aqq
             const double zeta = (aqq - app) / (2.0 * apq);
-            const double t = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
+            const double t = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + hypot(1.0, zeta));
             c = 1.0 / sqrt(1.0 + t * t);
             s = c * t;
             rotated = 1;
@@ -375,6 +505,16 @@ __global__ void power_step_kernel(const double* __restrict__ nz2, double* __rest
 
 void jacobi_svd_small(Ctx& c, const double* R, int l, double* sigma, double* W, double* Vr) {
   RPCA_REQUIRE(l >= 1 && l <= kMaxL, RPCA_E_SHAPE, "jacobi: l=%d", l);
+#ifndef JACOBI_NO_WARP  // ablation: the shared-memory kernel for every l
+  if (l <= 32) {
+    auto k = l <= 8 ? jacobi_warp_kernel<8> : l <= 16 ? jacobi_warp_kernel<16>
+           : l <= 24 ? jacobi_warp_kernel<24> : jacobi_warp_kernel<32>;
+    k<<<1, 32, 0, c.stream>>>(R, l, sigma, W, Vr);
+    RPCA_CHECK_LAUNCH();
+    count_launch(c, 1, "jacobi");
+    return;
+  }
+#endif
   const int smem = 2 * l * l * 8;
   ensure_smem((const void*)jacobi_kernel, 2 * kMaxL * kMaxL * 8);
   const int threads = 32 * std::max(1, ((l + 1) & ~1) / 2);  // one warp per pair of a round

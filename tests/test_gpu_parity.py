@@ -213,7 +213,8 @@ def test_qr_rank_deficient():
 
 
 # ----------------------------------------------------------------- a7: small SVD
-@pytest.mark.parametrize("n,l", [(500, 12), (4000, 22), (32768, 42), (64, 64)])
+@pytest.mark.parametrize("n,l", [(500, 12), (4000, 22), (32768, 42), (64, 64), (300, 1), (300, 7), (900, 31),
+                                 (900, 32), (900, 33)])
 def test_small_svd(n, l):
     g = torch.Generator(device="cuda").manual_seed(n + l)
     G = torch.randn(n, l, generator=g, device=dev(), dtype=torch.float64) * torch.logspace(
@@ -227,6 +228,42 @@ def test_small_svd(n, l):
     assert np.linalg.norm(Vn * sn @ Wn.T - Gn) < 1e-13 * np.linalg.norm(Gn)
     assert np.linalg.norm(Vn.T @ Vn - np.eye(l)) < 1e-13 * l
     assert cluster_sin_angle(Vo, Vn, so, l) < 1e-9
+
+
+@pytest.mark.parametrize("l", [22, 42])
+@pytest.mark.parametrize("scale", [2.0 ** 500, 2.0 ** -500, 1e288])
+def test_small_svd_extreme_scale(l, scale):
+    """σ(c·G) = c·σ(G) where the column norms² over- or underflow fp64 (the
+    one-warp kernel at l = 22, the shared-memory one at l = 42)."""
+    rng = np.random.default_rng(l)
+    Gn = rng.standard_normal((600, l)) * np.exp(-np.arange(l) / 4.0)
+    sn = np.linalg.svd(Gn, compute_uv=False)
+    Vt, s, W = rp.small_svd(torch.tensor(Gn * scale, device=dev()))
+    assert np.allclose(s.cpu().numpy() / scale, sn, rtol=1e-12)
+    Vn = Vt.cpu().numpy()
+    assert np.linalg.norm(Vn.T @ Vn - np.eye(l)) < 1e-13 * l
+
+
+@pytest.mark.parametrize("l", [9, 24, 40])
+def test_small_svd_rank_deficient(l):
+    """Repeated and zero columns: σ = 0 for l − r of them; the zero-σ columns
+    of Vt are completed to an orthonormal basis (Gram–Schmidt of e_t)."""
+    rng = np.random.default_rng(l)
+    r = l // 3
+    Gn = np.zeros((700, l))
+    Gn[:, :r] = rng.standard_normal((700, r))
+    Gn[:, r:2 * r] = Gn[:, :r] * 2.0
+    Vt, s, W = rp.small_svd(torch.tensor(Gn, device=dev()))
+    sn, Vn, Wn = s.cpu().numpy(), Vt.cpu().numpy(), W.cpu().numpy()
+    so = np.linalg.svd(Gn, compute_uv=False)
+    assert np.allclose(sn[:r], so[:r], rtol=1e-12)
+    assert np.all(sn[r:] <= 1e-13 * so[0])
+    assert np.all(np.diff(sn) <= 0)
+    assert np.linalg.norm(Vn[:, :r] * sn[:r] @ Wn[:, :r].T - Gn) < 1e-13 * np.linalg.norm(Gn)
+    assert np.linalg.norm(Wn.T @ Wn - np.eye(l)) < 1e-13 * l
+    # the σ > 0 columns are orthonormal; completed ones are unit vectors
+    # orthogonal to them and to each other (when G has l ≤ n rows)
+    assert np.linalg.norm(Vn.T @ Vn - np.eye(l)) < 1e-12 * l
 
 
 # ----------------------------------------------------------------- whole pca

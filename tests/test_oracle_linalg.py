@@ -127,6 +127,23 @@ def test_jacobi_rank_deficient_completion():
     assert np.linalg.norm(V * s @ W.T - G) < 1e-13 * np.linalg.norm(G)
 
 
+@pytest.mark.parametrize("scale", [2.0 ** 500, 2.0 ** -500, 1e150])
+def test_jacobi_extreme_scales(scale):
+    """σ(c·G) = c·σ(G) at magnitudes where a·b and 1 + ζ² overflow or
+    underflow in fp64 (column norms 2^±500): the rotation test and tan θ must
+    not be formed from those products."""
+    G = rand(300, 16, 7) * np.logspace(0, -5, 16)
+    sn = np.linalg.svd(G, compute_uv=False)
+    V, s, W = oracle.jacobi_svd(G * scale)
+    assert np.allclose(s / scale, sn, rtol=1e-12)
+    assert np.linalg.norm(V.T @ V - np.eye(16)) < 1e-13 * 16
+    M = rand(12, 12, 8)
+    S = M @ M.T - np.eye(12)
+    mu, E = oracle.jacobi_eig(S * scale)
+    ev = np.linalg.eigvalsh(S)[::-1]
+    assert np.allclose(mu / scale, ev, rtol=1e-12, atol=1e-12 * np.abs(ev).max())
+
+
 def test_jacobi_eig_matches_lapack():
     M = rand(30, 30, 5)
     S = M @ M.T - 3 * np.eye(30)
