@@ -558,24 +558,32 @@ __global__ void __launch_bounds__(kThreadsAty, 1)
 }
 
 // Z[c][j] = Σ_{r ascending} part[g·Pg + r][c/128 − g·CBG][c mod 128][j] − cmean[c]·sy[j]
-// (g = ⌊c/128⌋ / CBG).  One warp per output: lane λ sums r ≡ λ (mod 32), then
-// a fixed shuffle tree — deterministic.
+// (g = ⌊c/128⌋ / CBG), in ascending r — deterministic.
 __global__ void aty_f32_reduce_kernel(const double* __restrict__ part, AtyPlan pl, int LP, int64_t n, int l,
                                       const double* __restrict__ cmean, const double* __restrict__ sy,
                                       double* __restrict__ Z) {
+  // one thread per output (adjacent threads: adjacent j, coalesced reads),
+  // eight loads in flight
   const int64_t total = n * l;
-  const int lane = threadIdx.x & 31;
-  const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
-  for (int64_t idx = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); idx < total; idx += warps) {
+  const int64_t stride = (int64_t)pl.CBG * 128 * LP;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
     const int64_t c = idx / l;
     const int j = (int)(idx - c * l);
     const int64_t cb = c >> 7;
     const int g = (int)(cb / pl.CBG), cbi = (int)(cb - (int64_t)g * pl.CBG);
+    const double* p = part + ((((int64_t)g * pl.Pg) * pl.CBG + cbi) * 128 + (c & 127)) * LP + j;
     double s = 0.0;
-    for (int r = lane; r < pl.Pg; r += 32)
-      s += part[((((int64_t)g * pl.Pg + r) * pl.CBG + cbi) * 128 + (c & 127)) * LP + j];
-    s = warp_sum(s);
-    if (lane == 0) Z[idx] = cmean ? s - cmean[c] * sy[j] : s;
+    int r = 0;
+    for (; r + 8 <= pl.Pg; r += 8) {
+      double v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) v[u] = p[(r + u) * stride];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) s += v[u];
+    }
+    for (; r < pl.Pg; ++r) s += p[r * stride];
+    Z[idx] = cmean ? s - cmean[c] * sy[j] : s;
   }
 }
 
@@ -690,7 +698,7 @@ void aty_f32_run(Ctx& c, const DenseA& A, const float* hi, const float* lo, int6
   double* part = ar.get<double>((size_t)pl.Gc * pl.Pg * pl.CBG * 128 * N);
   launch_aty<N>(c, A, hi, lo, Kpad, pl, part);
   const int64_t total = A.n * l;
-  const unsigned grid = (unsigned)std::min<int64_t>(cdiv(total, 8), (int64_t)c.num_sms * 32);
+  const unsigned grid = (unsigned)std::min<int64_t>(cdiv(total, 256), (int64_t)c.num_sms * 16);
   aty_f32_reduce_kernel<<<grid, 256, 0, c.stream>>>(part, pl, N, A.n, l, cmean, sy, Z);
   RPCA_CHECK_LAUNCH();
   count_launch(c, 1, "aty_reduce");

@@ -185,8 +185,17 @@ __global__ void sum_parts_kernel(const double* __restrict__ part, int64_t nparts
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int j = blockIdx.x * 32 + lane;
   double s = 0.0;
-  if (j < w)
-    for (int64_t b = warp; b < nparts; b += 8) s += part[b * w + j];
+  if (j < w) {
+    int64_t b = warp;
+    for (; b + 56 < nparts; b += 64) {  // eight loads in flight, added in the same order
+      double v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) v[u] = part[(b + 8 * u) * w + j];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) s += v[u];
+    }
+    for (; b < nparts; b += 8) s += part[b * w + j];
+  }
   red[warp][lane] = s;
   __syncthreads();
   if (warp == 0 && j < w) {

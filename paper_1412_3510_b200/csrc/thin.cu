@@ -85,7 +85,15 @@ __global__ void sum_partials_8w(const double* __restrict__ part, int64_t nparts,
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   for (int j = lane; j < l; j += 32) {
     double s = 0.0;
-    for (int64_t b = warp; b < nparts; b += 8) s += part[b * l + j];
+    int64_t b = warp;
+    for (; b + 56 < nparts; b += 64) {  // eight loads in flight, added in the same order
+      double v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) v[u] = part[(b + 8 * u) * l + j];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) s += v[u];
+    }
+    for (; b < nparts; b += 8) s += part[b * l + j];
     red[warp][j] = s;
   }
   __syncthreads();
@@ -97,24 +105,6 @@ __global__ void sum_partials_8w(const double* __restrict__ part, int64_t nparts,
   }
 }
 
-__global__ void sum_partials(const double* __restrict__ part, int64_t nparts, int l, double scale,
-                             double* __restrict__ v) {
-  const int j = threadIdx.x;
-  if (j >= l) return;
-  double s = 0.0;
-  for (int64_t b = 0; b < nparts; ++b) s += part[b * l + j];
-  v[j] = s * scale;
-}
-
-
-__global__ void sum_partials_wide_kernel(const double* __restrict__ part, int64_t nparts, int w,
-                                         double* __restrict__ v) {
-  const int j = blockIdx.x * blockDim.x + threadIdx.x;
-  if (j >= w) return;
-  double s = 0.0;
-  for (int64_t b = 0; b < nparts; ++b) s += part[b * w + j];
-  v[j] = s;
-}
 
 __global__ void sub_rank1_kernel(double* __restrict__ Y, int64_t rows, int l, const double* __restrict__ u,
                                  const double* __restrict__ v, double alpha) {
@@ -304,10 +294,6 @@ unsigned grid_for(Ctx& c, int64_t work, int per = 256) {
   return (unsigned)b;
 }
 
-void sum_partials_wide(Ctx& c, const double* part, int64_t nparts, int w, double* v) {
-  sum_partials_wide_kernel<<<(unsigned)cdiv(w, 256), 256, 0, c.stream>>>(part, nparts, w, v);
-  RPCA_CHECK_LAUNCH();
-}
 
 }  // namespace
 
