@@ -43,7 +43,15 @@ constexpr int kWarps = kThreads / 32;
 
 // rows per thread: leaves favour occupancy, tree levels (few CTAs, latency-
 // bound) favour bigger groups so the tournament has fewer levels
-constexpr int leaf_rows_per_thread(int LP) { return LP <= 8 ? 4 : (LP <= 16 ? 2 : 1); }
+#ifndef LU_LEAF_R24
+#define LU_LEAF_R24 1  // rows per thread of the leaves for 16 < LP ≤ 24
+#endif
+#ifndef LU_LEAF_R32
+#define LU_LEAF_R32 2  // … for 24 < LP ≤ 32 (C5: leaves +0.8 ms, tree −1.0 ms)
+#endif
+constexpr int leaf_rows_per_thread(int LP) {
+  return LP <= 8 ? 4 : (LP <= 16 ? 2 : (LP <= 24 ? LU_LEAF_R24 : (LP <= 32 ? LU_LEAF_R32 : 1)));
+}
 constexpr int tree_rows_per_thread(int LP) { return LP <= 8 ? 4 : (LP <= 32 ? 2 : 1); }
 
 // two CTAs per SM (registers capped at 128) while a thread's rows fit
