@@ -47,7 +47,7 @@ __global__ void pack_y_kernel(const double* __restrict__ Y, int64_t m, int l, in
 }
 
 // partial[b][j] = Σ_{i in chunk b} a[i]·X[i][j]  (a == NULL ⇒ 1); chunks of
-// kColChunk rows, threads (phase, column) read whole rows (coalesced), four
+// kColChunk rows, threads (phase, column) read whole rows (coalesced), eight
 // independent accumulators per thread, fixed order
 constexpr int kColChunk = 2048;
 __global__ void __launch_bounds__(256) wcolsum_partial(const double* __restrict__ a, const double* __restrict__ X,
@@ -57,18 +57,21 @@ __global__ void __launch_bounds__(256) wcolsum_partial(const double* __restrict_
   const int64_t r1 = min(rows, r0 + kColChunk);
   const int phases = 256 / l;  // l ≤ 64 ⇒ ≥ 4 phases
   const int ph = threadIdx.x / l, j = threadIdx.x % l;
-  double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+  double s[8];
+#pragma unroll
+  for (int u = 0; u < 8; ++u) s[u] = 0.0;
   if (ph < phases) {
     int64_t i = r0 + ph;
-    for (; i + 3 * phases < r1; i += 4 * phases) {
-      s0 += (a ? a[i] : 1.0) * X[i * ldx + j];
-      s1 += (a ? a[i + phases] : 1.0) * X[(i + phases) * ldx + j];
-      s2 += (a ? a[i + 2 * phases] : 1.0) * X[(i + 2 * phases) * ldx + j];
-      s3 += (a ? a[i + 3 * phases] : 1.0) * X[(i + 3 * phases) * ldx + j];
+    for (; i + 7 * phases < r1; i += 8 * phases) {  // eight loads in flight per thread
+      double x[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) x[u] = X[(i + u * phases) * ldx + j];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) s[u] += (a ? a[i + u * phases] : 1.0) * x[u];
     }
-    for (; i < r1; i += phases) s0 += (a ? a[i] : 1.0) * X[i * ldx + j];
+    for (; i < r1; i += phases) s[0] += (a ? a[i] : 1.0) * X[i * ldx + j];
   }
-  red[threadIdx.x] = (s0 + s1) + (s2 + s3);
+  red[threadIdx.x] = ((s[0] + s[1]) + (s[2] + s[3])) + ((s[4] + s[5]) + (s[6] + s[7]));
   __syncthreads();
   if (threadIdx.x < l) {
     double t = 0.0;
