@@ -153,7 +153,7 @@ def test_apply_int8emu_special_values():
 # the last three run persistent leaves (more leaves than resident CTAs) whose
 # last leaf has an odd number of doubles (the bulk copy's 16-byte tail)
 @pytest.mark.parametrize("m,l", [(100, 12), (1000, 22), (100000, 22), (70000, 42), (4096, 64), (257, 64), (22, 22),
-                                 (300001, 13), (200003, 41), (1000003, 53)])
+                                 (300001, 13), (200003, 41), (1000003, 53), (600007, 29), (300005, 32)])
 def test_lu_span_and_factorisation(m, l):
     g = torch.Generator(device="cuda").manual_seed(m + l)
     Y = torch.randn(m, l, generator=g, device=dev(), dtype=torch.float64)
