@@ -167,7 +167,7 @@ template <int N>
 __global__ void __launch_bounds__(kThreadsAx, 1)
     ax_f32_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmXh,
                      const __grid_constant__ CUtensorMap tmXl, int64_t m, int l, int64_t ntiles, int KB,
-                     const double* __restrict__ cx, double* __restrict__ Y) {
+                     const double* __restrict__ cx, double* __restrict__ Y, double* __restrict__ colpart) {
   using Cfg = AxCfg<N>;
   constexpr int S = Cfg::kStages, NS = Cfg::kNS;
   constexpr int KC = kKChunk / 32;  // k-blocks per unit
@@ -307,17 +307,25 @@ __global__ void __launch_bounds__(kThreadsAx, 1)
 #pragma unroll
         for (int c0 = 0; c0 < N; c0 += 16) {
           float v[16], w[16];
+          double fin[16];  // the values stored (final after the last chunk)
           tmem_ld16(d + c0, v);
           tmem_ld16(d + N + c0, w);
-          if (row < m) {
 #pragma unroll
-            for (int j = 0; j < 16; ++j)
-              if (c0 + j < l) {
-                double* y = Y + row * l + c0 + j;
-                const double a = (double)v[j] + (double)w[j];
-                if (kc == 0) *y = cx ? a - cx[c0 + j] : a;
-                else *y += a;
-              }
+          for (int j = 0; j < 16; ++j) {
+            fin[j] = 0.0;
+            if (row < m && c0 + j < l) {
+              double* y = Y + row * l + c0 + j;
+              const double a = (double)v[j] + (double)w[j];
+              fin[j] = kc == 0 ? (cx ? a - cx[c0 + j] : a) : *y + a;
+              *y = fin[j];
+            }
+          }
+          if (colpart && kc == nkc - 1) {  // column sums of this quarter's 32 rows
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
+              const double sv = warp_sum(fin[j]);
+              if (lane == 0 && c0 + j < l) colpart[(tile * 4 + q) * l + c0 + j] = sv;
+            }
           }
         }
         tc_fence_before();
@@ -661,7 +669,8 @@ void launch_ax(Ctx& c, const DenseA& A, const float* hi, const float* lo, int64_
   const int grid = (int)std::min<int64_t>(ntiles, c.num_sms);
   prof_pre(c);
   ax_f32_tc_kernel<N><<<grid, kThreadsAx, Cfg::kSmem, c.stream>>>(tA, tH, tL, A.m, l, ntiles, (int)(Kpad / 32), cx,
-                                                                   Y);
+                                                                   Y, c.ax_colpart);
+  if (c.ax_colpart) c.ax_colpart_n = ntiles * 4;
   RPCA_CHECK_LAUNCH();
   count_launch(c, 1, c.tag ? c.tag : "ax_f32_tc");
 }

@@ -388,6 +388,31 @@ void colmeans(Ctx& c, const MatV& A, int64_t m_total, double* cmean, Arena& ar, 
 // `mu`, the return value; NULL when nothing is pending) for the renormalisation
 // that consumes it; an m-long INPUT is centred on load (its means are taken
 // into `tmp`).
+// Y = A·X (this shard's rows) and, centred, Y's column means over the global
+// rows: from the pass epilogue's column sums where the pass writes them (the
+// fp32 tcgen05 pass), else from one more read of Y
+const double* ax_and_mean(Ctx& c, const Op& F, const double* X, int l, double* Y, double* mu, Arena& ar) {
+  const size_t mark = ar.off;
+  c.ax_colpart_n = 0;
+  c.ax_colpart = (F.centered && !F.A.csr) ? ar.get<double>(ax_colpart_elems(F.A.m, l)) : nullptr;
+  apply_ax(c, F.A, nullptr, X, l, Y, ar);
+  const double* part = c.ax_colpart;
+  const int64_t np = c.ax_colpart_n;
+  c.ax_colpart = nullptr;
+  c.ax_colpart_n = 0;
+  if (F.centered) {
+    if (np > 0) {
+      // the partials are an np × l row-major block: its column sums, fixed order
+      weighted_colsum(c, nullptr, part, np, l, mu, ar, 0, 1.0 / (double)F.m_total);
+      if (F.sharded) allreduce_sum(c, mu, (size_t)l);
+    } else {
+      column_mean(c, Y, F.A.m, l, F.m_total, F.sharded, mu, ar);
+    }
+  }
+  ar.off = mark;
+  return F.centered ? mu : nullptr;
+}
+
 const double* fwd(Ctx& c, const Op& F, const double* X, int l, double* Y, double* mu, double* tmp, Arena& ar) {
   if (F.trans) {  // F = A_cᵀ: Y = Aᵀ·(P·X)
     const double* xm = nullptr;
@@ -399,18 +424,10 @@ const double* fwd(Ctx& c, const Op& F, const double* X, int l, double* Y, double
     if (F.sharded) allreduce_sum(c, Y, (size_t)F.A.n * l);
     return nullptr;
   }
-  apply_ax(c, F.A, nullptr, X, l, Y, ar);  // Y = P·(A·X), P pending
-  if (!F.centered) return nullptr;
-  column_mean(c, Y, F.A.m, l, F.m_total, F.sharded, mu, ar);
-  return mu;
+  return ax_and_mean(c, F, X, l, Y, mu, ar);  // Y = P·(A·X), P pending
 }
 const double* adj(Ctx& c, const Op& F, const double* Y, int l, double* Z, double* mu, double* tmp, Arena& ar) {
-  if (F.trans) {  // Z = P·(A·Y), P pending
-    apply_ax(c, F.A, nullptr, Y, l, Z, ar);
-    if (!F.centered) return nullptr;
-    column_mean(c, Z, F.A.m, l, F.m_total, F.sharded, mu, ar);
-    return mu;
-  }
+  if (F.trans) return ax_and_mean(c, F, Y, l, Z, mu, ar);  // Z = P·(A·Y), P pending
   const double* ym = nullptr;  // Z = Aᵀ·(P·Y)
   if (F.centered) {
     column_mean(c, Y, F.A.m, l, F.m_total, F.sharded, tmp, ar);
@@ -444,7 +461,8 @@ struct EmuScope {
 size_t op_ws(Ctx& c, const MatV& A, int l) {
   const size_t small = (size_t)(cdiv(std::max(A.m, A.n), 2048) + 4) * kMaxL * 8 * 2 + 65536;
   if (A.csr) return small;
-  return std::max(ax_ws_bytes(A.d, l) + 4096 * 4, aty_ws_bytes(c, A.d, l)) + small;
+  const size_t colpart = (size_t)ax_colpart_elems(A.m, kMaxL) * 8 + 256;  // centred A·X epilogue sums
+  return std::max(ax_ws_bytes(A.d, l) + 4096 * 4 + colpart, aty_ws_bytes(c, A.d, l)) + small;
 }
 
 // A block of `rows` rows that is either whole (replicated) or this rank's

@@ -111,6 +111,11 @@ struct Ctx {
   // the driver call's A, valid while that call runs (EmuScope)
   const int* emu_E = nullptr;
   const void* emu_A = nullptr;
+  // centred A·X: where the pass kernel can, its epilogue writes the column
+  // sums of Y per (128-row tile, 32-row quarter) here (the driver sets the
+  // buffer, the fp32 pass sets the count) — no second read of Y for its mean
+  double* ax_colpart = nullptr;
+  int64_t ax_colpart_n = 0;
   Arena arena(size_t bytes);  // ensures capacity, returns an arena over the workspace
 };
 
@@ -219,6 +224,8 @@ bool f32_tc_ok(const DenseA& A);
 size_t ax_f32_ws_bytes(const DenseA& A, int l);
 // Y = A·X [− 1·cxᵀ] (cx may be NULL)
 void dense_ax_f32(Ctx& c, const DenseA& A, const double* X, int l, const double* cx, double* Y, Arena& ar);
+inline int64_t ax_colpart_elems(int64_t m, int l) { return ((m + 127) / 128) * 4 * (int64_t)l; }
+
 size_t aty_f32_ws_bytes(Ctx& c, const DenseA& A, int l);
 // Z = Aᵀ·Y [− cmean·syᵀ]
 void dense_aty_f32(Ctx& c, const DenseA& A, const double* Y, int l, const double* cmean, const double* sy,
