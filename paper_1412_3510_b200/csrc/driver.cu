@@ -393,6 +393,10 @@ void colmeans(Ctx& c, const MatV& A, int64_t m_total, double* cmean, Arena& ar, 
 // fp32 tcgen05 pass), else from one more read of Y
 const double* ax_and_mean(Ctx& c, const Op& F, const double* X, int l, double* Y, double* mu, Arena& ar) {
   const size_t mark = ar.off;
+  struct Reset {  // the request never outlives this pass, error or not
+    Ctx& c;
+    ~Reset() { c.ax_colpart = nullptr; c.ax_colpart_n = 0; }
+  } reset{c};
   c.ax_colpart_n = 0;
   c.ax_colpart = (F.centered && !F.A.csr) ? ar.get<double>(ax_colpart_elems(F.A.m, l)) : nullptr;
   apply_ax(c, F.A, nullptr, X, l, Y, ar);
