@@ -478,11 +478,13 @@ __global__ void __launch_bounds__(kThreadsAty, 1)
         const uint32_t d = tmem + (uint32_t)(cbi * Cfg::kTN);
         const uint32_t ah = tmem + (uint32_t)(Cfg::kSlot0 + 64 * rt.s), al = ah + 32;
         if (leader) {
+#ifndef ATY_NO_MMA  // ablation: the pipeline without the tensor-core products
 #pragma unroll
           for (int ks = 0; ks < 4; ++ks) {
             mma_tf32_ts(d, ah + 8 * ks, dh + 2 * ks, idesc2, (kin != 0 || ks != 0) ? 1u : 0u);
             mma_tf32_ts(d, al + 8 * ks, dh + 2 * ks, idesc, 1u);
           }
+#endif
           mma_commit(&tfree[rt.s]);
           if (cbi == ncb - 1) {
             mma_commit(&yempty[ry.s]);
@@ -519,9 +521,14 @@ __global__ void __launch_bounds__(kThreadsAty, 1)
       mbar_wait(&tfree[rt.s], rt.ph ^ 1u);
       tc_fence_after();
       const uint32_t at = tmem + lane_off + (uint32_t)(Cfg::kSlot0 + 64 * rt.s + 16 * h);
+#ifndef ATY_NO_TMEM_ST  // ablation: the split without its TMEM stores
       tmem_st16_nowait(at, hi);
       tmem_st16_nowait(at + 32, lo);
       asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+#else
+      if (hi[0] == 12345.0f && lo[0] == 1.0f) asm volatile("trap;");  // keep the split live
+      (void)at;
+#endif
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&afull[rt.s]);
