@@ -80,30 +80,33 @@ __global__ void __launch_bounds__(256) wcolsum_partial(const double* __restrict_
   }
 }
 
-// v[j] = scale·Σ_b part[b][j]: warp w sums the partials b ≡ w (mod 8) in
-// ascending order, then the eight warp sums are added in order
-__global__ void sum_partials_8w(const double* __restrict__ part, int64_t nparts, int l, double scale,
-                                double* __restrict__ v) {
-  __shared__ double red[8][kMaxL];
+// v[j] = scale·Σ_b part[b][j]: warp w of the 32 sums the partials
+// b ≡ w (mod 32) in ascending order (eight loads in flight), then the 32
+// warp sums are added in order — fixed order, one CTA
+constexpr int kSumWarps = 32;
+__global__ void __launch_bounds__(32 * kSumWarps) sum_partials_8w(const double* __restrict__ part, int64_t nparts,
+                                                                 int l, double scale, double* __restrict__ v) {
+  __shared__ double red[kSumWarps][kMaxL];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  constexpr int W = kSumWarps;
   for (int j = lane; j < l; j += 32) {
     double s = 0.0;
     int64_t b = warp;
-    for (; b + 56 < nparts; b += 64) {  // eight loads in flight, added in the same order
-      double v[8];
+    for (; b + 7 * W < nparts; b += 8 * W) {
+      double x[8];
 #pragma unroll
-      for (int u = 0; u < 8; ++u) v[u] = part[(b + 8 * u) * l + j];
+      for (int u = 0; u < 8; ++u) x[u] = part[(b + W * u) * l + j];
 #pragma unroll
-      for (int u = 0; u < 8; ++u) s += v[u];
+      for (int u = 0; u < 8; ++u) s += x[u];
     }
-    for (; b < nparts; b += 8) s += part[b * l + j];
+    for (; b < nparts; b += W) s += part[b * l + j];
     red[warp][j] = s;
   }
   __syncthreads();
   if (threadIdx.x < l) {
     double t = 0.0;
 #pragma unroll
-    for (int w = 0; w < 8; ++w) t += red[w][threadIdx.x];
+    for (int w = 0; w < W; ++w) t += red[w][threadIdx.x];
     v[threadIdx.x] = t * scale;
   }
 }
@@ -326,7 +329,7 @@ void weighted_colsum(Ctx& c, const double* a, const double* X, int64_t rows, int
   double* part = ar.get<double>(nparts * l);
   wcolsum_partial<<<(unsigned)nparts, 256, 0, c.stream>>>(a, X, rows, l, ldx, part);
   RPCA_CHECK_LAUNCH();
-  sum_partials_8w<<<1, 256, 0, c.stream>>>(part, nparts, l, scale, v);
+  sum_partials_8w<<<1, 32 * kSumWarps, 0, c.stream>>>(part, nparts, l, scale, v);
   RPCA_CHECK_LAUNCH();
   count_launch(c, 2);
 }
