@@ -16,11 +16,11 @@ a bounded row sample of the same workload, extrapolated linearly in m.
 --impl reference times that oracle as the reference arm.
 
 Multi-GPU (torchrun, one rank per GPU, NCCL): A is sharded by rows
-(SURVEY.md §8(e)).  The dense-PCA and CSR configs scale WEAKLY — every rank
-holds one full per-GPU instance of the config as its row block (seed offset
-by rank), so global m = N·m — and `value` stays the whole-job step time (max
-over ranks).  The Nyström config C3 scales STRONGLY: the same n×n matrix, rows
-split uniformly.
+ and every config scales STRONGLY, as SURVEY §8(d) fixes it:
+the same global matrix at every N, rank r holding the uniform row block
+[r·⌈m/N⌉, min(m, (r+1)·⌈m/N⌉)) (C4: 250,000 rows per GPU at N = 8; C5:
+1.25e6).  `value` stays the whole-job PCA time (max over ranks) and
+`roofline.aggregate` the whole-job A-streaming rate against N × the peak.
 """
 import argparse
 import json
@@ -155,17 +155,11 @@ class ClockSampler:
 
 
 def plan_shard(cfg, ws, rank):
-    """How rank `rank` of `ws` holds the workload: weak scaling stacks ws
-    per-GPU instances (rank r's seed = base + r) into an (ws·m)-row A; strong
-    scaling (the square Nyström config) splits one matrix's rows uniformly."""
-    if ws == 1:
-        return {"scaling": "weak", "m_total": cfg.m, "row0": 0, "m_local": cfg.m, "seed_offset": 0}
-    if cfg.op == "eigens":
-        pad = -(-cfg.m // ws)
-        row0 = min(cfg.m, rank * pad)
-        return {"scaling": "strong", "m_total": cfg.m, "row0": row0, "m_local": min(pad, cfg.m - row0),
-                "seed_offset": 0}
-    return {"scaling": "weak", "m_total": ws * cfg.m, "row0": rank * cfg.m, "m_local": cfg.m, "seed_offset": rank}
+    """How rank `rank` of `ws` holds the workload: strong scaling — one global
+    matrix, rows split uniformly (the partition rpca_eigens requires)."""
+    pad = -(-cfg.m // ws)
+    row0 = min(cfg.m, rank * pad)
+    return {"scaling": "strong", "m_total": cfg.m, "row0": row0, "m_local": min(pad, cfg.m - row0)}
 
 
 def max_over_ranks(x, ws, device):
@@ -188,17 +182,21 @@ def workload(name):
 
 
 def make_input(cfg, device, rp=None, plan=None):
-    plan = plan or {"seed_offset": 0, "row0": 0, "m_local": cfg.m, "scaling": "weak"}
-    kw = {}
-    if plan["seed_offset"]:
-        kw["seed"] = synth.GEN_SEEDS[cfg.name] + plan["seed_offset"]
-    A = synth.make(cfg.name, device=device, **kw)
-    if plan["scaling"] == "strong" and plan["m_local"] != cfg.m:
-        A = A[plan["row0"]:plan["row0"] + plan["m_local"]].clone()
-    torch.cuda.synchronize()
+    """This rank's rows of the config's (global, seeded) matrix."""
+    plan = plan or {"row0": 0, "m_local": cfg.m}
+    r0, r1 = plan["row0"], plan["row0"] + plan["m_local"]
+    A = synth.make(cfg.name, device=device)
     if cfg.kind == "csr":
         rowptr, colind, vals = A
-        return rp.CSR(rowptr, colind, vals, (cfg.m, cfg.n))
+        if (r0, r1) != (0, cfg.m):
+            t0, t1 = int(rowptr[r0]), int(rowptr[r1])
+            rowptr = (rowptr[r0:r1 + 1] - t0).contiguous()
+            colind, vals = colind[t0:t1].clone(), vals[t0:t1].clone()
+        torch.cuda.synchronize()
+        return rp.CSR(rowptr, colind, vals, (r1 - r0, cfg.n))
+    if (r0, r1) != (0, cfg.m):
+        A = A[r0:r1].clone()
+    torch.cuda.synchronize()
     return A
 
 
@@ -272,6 +270,19 @@ def oracle_sample(cfg, A_host, target_s):
     return ms, dt, scale
 
 
+def cpu_model():
+    """The host CPU model (lscpu), for cpu_baseline."""
+    try:
+        import subprocess
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for line in out.splitlines():
+            if line.startswith("Model name:"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return None
+
+
 def cpu_baseline(cfg, A_host, target_s):
     import oracle
 
@@ -279,8 +290,8 @@ def cpu_baseline(cfg, A_host, target_s):
     what = (f"leading {ms}x{ms} block" if cfg.op == "eigens" else f"leading {ms} of {cfg.m} rows")
     if not isinstance(A_host, np.ndarray):
         what += " (CSR; the n-side work does not grow with m, so linear extrapolation overstates it slightly)"
-    return {"value": dt * scale, "unit": "s", "cores": oracle.num_threads(), "kind": "oracle",
-            "sample": f"oracle on the {what} ({dt:.2f} s), extrapolated "
+    return {"value": dt * scale, "unit": "s", "cores": oracle.num_threads(), "cpu_model": cpu_model(),
+            "kind": "oracle", "sample": f"oracle on the {what} ({dt:.2f} s), extrapolated "
                       f"{'quadratically in n' if cfg.op == 'eigens' else 'linearly in m'} (x{scale:.1f})"}
 
 
@@ -311,7 +322,8 @@ def reference_arm(args):
             "n_gpus": ws, "steps": args.steps, "warmup": args.warmup, "ms_per_step": v * 1e3,
             "higher_is_better": False, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic", "config": conf,
-            "cpu_baseline": {"value": v, "unit": "s", "cores": oracle.num_threads(), "kind": "oracle",
+            "cpu_baseline": {"value": v, "unit": "s", "cores": oracle.num_threads(), "cpu_model": cpu_model(),
+                             "kind": "oracle",
                              "sample": f"oracle on the {what} per step, extrapolated x{scale:.1f}"},
             "e2e": {"value": v, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -338,10 +350,15 @@ def main():
     pbytes = pass_bytes(A, cfg)
     passes = conf["passes_over_A"]
     conf.update({"l2": f"A ({abytes / 1e9:.2f} GB per GPU) > L2 (126 MB): no flush needed",
-                 "parallelism": f"row-sharded dp{ws} ({plan['scaling']} scaling, m_total={plan['m_total']})"
-                 if ws > 1 else "single GPU"})
+                 "parallelism": f"row-sharded dp{ws} ({plan['scaling']} scaling, m_total={plan['m_total']}, "
+                                f"{plan['m_local']} rows on rank 0)" if ws > 1 else "single GPU"})
 
     for _ in range(args.warmup):
+        run_step(rp, cfg, A, plan)
+    # one more warm-up step in the timed region's profile mode: the library
+    # captures a separate CUDA graph per profile mode, so this keeps the
+    # capture and instantiation out of the timed steps
+    with rp.profile(passes_only=True):
         run_step(rp, cfg, A, plan)
     torch.cuda.synchronize()
 
@@ -403,6 +420,13 @@ def main():
                 "peak_source": peak_src,
                 "algorithmic_bytes_per_launch": pbytes, "avg_launch_ms": round(avg_ms, 5),
                 "share_of_step": round(tot / args.steps / step_ms, 4)}
+        if tr and not isinstance(A, torch.Tensor):
+            # CSR: the gather-inclusive algorithmic bytes count every gathered
+            # operand row as DRAM traffic while part of X hits L2; the fraction
+            # from ncu's measured DRAM bytes per launch is reported beside it
+            roof["dram_based"] = {"achieved": round(tr["bytes"] / (avg_ms / 1e3) / 1e9, 1),
+                                  "frac": round(tr["bytes"] / (avg_ms / 1e3) / 1e9 / hbm, 4),
+                                  "note": "ncu dram bytes per launch / live launch time"}
         all_pass_ms = sum(v[1] for v in passes_k.values()) / args.steps
         roof["all_passes"] = {"launches_per_step": sum(v[0] for v in passes_k.values()) // args.steps,
                               "gbs_per_pass": round(abytes * passes / (all_pass_ms / 1e3) / 1e9, 1)}
@@ -413,8 +437,12 @@ def main():
                  for k, v in sorted(kern_all.items(), key=lambda kv: -kv[1][1])}
 
     e2e = None
-    if not args.no_e2e and isinstance(A, torch.Tensor):  # every rank (the call has collectives)
-        Ah = A.cpu().pin_memory()
+    if not args.no_e2e:  # every rank (the call has collectives)
+        if isinstance(A, torch.Tensor):
+            Ah = A.cpu().pin_memory()
+        else:  # host CSR: the three arrays are copied (and CSR(Aᵀ) rebuilt) inside each call
+            Ah = rp.CSR(A.rowptr.cpu().pin_memory(), A.colind.cpu().pin_memory(), A.vals.cpu().pin_memory(),
+                        A.shape)
         run_step(rp, cfg, Ah, plan)  # warm
         torch.cuda.synchronize()
         barrier()
@@ -425,8 +453,9 @@ def main():
         te = max_over_ranks((time.perf_counter() - t0) / ne, ws, dev)
         d2h = sum(o.numel() * o.element_size() for o in out)
         e2e = {"value": te, "unit": "s", "h2d_bytes_per_step": abytes * ws, "d2h_bytes_per_step": d2h * ws,
-               "note": "host-pinned A (shard) copied H2D and the factors copied D2H inside each library call; "
-                       "host wall clock, max over ranks"}
+               "note": "host-pinned A (shard) copied H2D and the factors copied D2H inside each library call"
+                       + ("" if isinstance(A, torch.Tensor) else "; CSR(A^T) rebuilt on the device per call")
+                       + "; host wall clock, max over ranks"}
         del Ah
 
     cpu = None

@@ -7,7 +7,8 @@
  * otherwise, matrices are ROW-MAJOR, thin blocks (m×l, n×l, l×l) are fp64
  * with leading dimension = number of columns, and all buffers are DEVICE
  * memory of the context's GPU owned by the caller.  The library keeps no
- * pointer past the return of a call (its workspace is context-owned).
+ * pointer to caller data past the return of a call, except the workspace
+ * given to rpca_set_workspace (the cached CSR(Aᵀ) lives in the workspace).
  * Calls enqueue on the context's stream; calls that return host scalars or
  * statuses computed on the device synchronise that stream (noted per call).
  *
@@ -53,8 +54,15 @@ enum { RPCA_SHIFT_CHOL = 0, RPCA_SQRT = 1 };
 /* flags for rpca_ctx_create / the drivers */
 #define RPCA_FLAG_UNIFORM_OMEGA 0x1u  /* draw Ω from U[-1,1] instead of N(0,1) */
 #define RPCA_FLAG_OUTPUTS_HOST 0x2u   /* U, S, V / lam are HOST buffers (copied back inside the call) */
-#define RPCA_FLAG_CHECK_FINITE 0x4u   /* validate A during pass 1 → RPCA_E_NONFINITE */
+#define RPCA_FLAG_CHECK_FINITE 0x4u   /* non-finite input → RPCA_E_NONFINITE: detected from the
+                                         first thin block (A·Ω; a NaN/Inf entry of A makes its row
+                                         non-finite since Ω is finite and nonzero; an overflow in A·Ω
+                                         reports the same), no extra pass over A; diffsnorm also
+                                         checks the factors through y = A·x − U·(S⊙Vᵀx) */
 #define RPCA_FLAG_NO_GRAPH 0x8u       /* do not capture/replay driver calls as CUDA graphs */
+
+/* ops for rpca_workspace_query */
+enum { RPCA_OP_PCA = 1, RPCA_OP_EIGENS = 2, RPCA_OP_DIFFSNORM = 3, RPCA_OP_APPLY = 4, RPCA_OP_REIG = 5 };
 
 /*
  * The matrix A (§2 l.107-114: m×n, k ≪ min(m,n)).
@@ -65,7 +73,13 @@ enum { RPCA_SHIFT_CHOL = 0, RPCA_SQRT = 1 };
  *   with fp32 products (dense: 3×TF32 tensor-core split) and fp64 reductions.
  *   m, n: GLOBAL shape.  row0, m_local: the rows [row0, row0+m_local) this
  *   rank holds (single GPU: 0, m).  location: RPCA_DEVICE or RPCA_HOST (host
- *   A is copied to the device inside the call — the end-to-end mode).
+ *   A — dense, or all three CSR arrays — is copied to the device inside each
+ *   call, the end-to-end mode; a host CSR's transpose is rebuilt per call).
+ *   A device CSR's transpose CSR(Aᵀ) is
+ *   cached in the workspace across calls, keyed by the pointers, the shape
+ *   and a 64-bit fingerprint of the three arrays' contents recomputed on
+ *   every call (one read of the CSR, ≈ 0.5% of a C5 PCA), so a different
+ *   matrix at recycled addresses or an in-place edit rebuilds it.
  */
 typedef struct {
   int32_t kind;
@@ -87,9 +101,11 @@ typedef struct rpca_ctx rpca_ctx;
 /* ---- context ------------------------------------------------------------
  * rpca_ctx_create: binds to CUDA `device` and `stream` (a cudaStream_t; NULL
  * = the legacy default stream).  flags: default driver flags (RPCA_FLAG_*).
- * The context owns a growable device workspace; the first call of a given
- * size allocates (cudaMalloc), later calls of the same or smaller size do
- * not, so steady-state calls are CUDA-graph capturable.                    */
+ * Allocates 64 bytes of pinned host and 256 bytes of device scratch.  By
+ * default the context owns a growable device workspace: the first call of a
+ * given size allocates (cudaMalloc, outside any capture), later calls of the
+ * same or smaller size do not, so steady-state calls are CUDA-graph captured
+ * and replayed.  See rpca_set_workspace for a caller-owned workspace.      */
 rpca_status rpca_ctx_create(rpca_ctx** ctx, int device, void* stream, uint32_t flags);
 rpca_status rpca_ctx_destroy(rpca_ctx* ctx);
 rpca_status rpca_ctx_set_stream(rpca_ctx* ctx, void* stream);
@@ -101,6 +117,25 @@ rpca_status rpca_ctx_sync(rpca_ctx* ctx);
 rpca_status rpca_ctx_clear_cache(rpca_ctx* ctx);
 /* bytes of workspace currently held by the context */
 rpca_status rpca_workspace_size(rpca_ctx* ctx, size_t* bytes);
+/* Caller-owned workspace.
+ * rpca_workspace_query: *bytes = device workspace one call of `op` needs for
+ * A (RPCA_OP_PCA / _EIGENS: k, l (≤ 0 ⇒ k+2), its; RPCA_OP_DIFFSNORM: k = the
+ * factors' rank; RPCA_OP_APPLY: l = the thin block's width, covers
+ * rpca_apply / rpca_apply_int8emu / rpca_colmeans), with the context's
+ * current flags (RPCA_FLAG_OUTPUTS_HOST adds staging) and communicator, and
+ * outputs with ld = k.  For a device CSR A it includes the cached CSR(Aᵀ) and
+ * the heavy-row plans.  Reads no matrix data; RPCA_E_SHAPE / RPCA_E_ARG as the
+ * op would.
+ * rpca_set_workspace: the context uses [dptr, dptr + bytes) (device memory of
+ * its GPU, 256-byte aligned, owned by the caller, not touched after the
+ * context is destroyed or another workspace is set) and never calls
+ * cudaMalloc for calls again; a call needing more returns RPCA_E_WORKSPACE
+ * before launching anything.  dptr = NULL returns to a context-owned
+ * workspace.  Either way the cached CSR(Aᵀ) and captured graphs are dropped.
+ * Synchronises the context stream.                                         */
+rpca_status rpca_workspace_query(rpca_ctx* ctx, int op, const rpca_mat* A, int64_t k, int64_t l, int its,
+                                 size_t* bytes);
+rpca_status rpca_set_workspace(rpca_ctx* ctx, void* dptr, size_t bytes);
 const char* rpca_strerror(rpca_status s);
 const char* rpca_last_error(void);
 /* number of kernels this library launched since the context was created */
@@ -185,6 +220,17 @@ rpca_status rpca_apply_int8emu(rpca_ctx* ctx, const rpca_mat* A, const double* X
  * device) may be NULL.                                                     */
 rpca_status rpca_lu_renorm(rpca_ctx* ctx, double* Y, int64_t m, int64_t l, double* U, int64_t* piv);
 
+/* ---- §8(a) step a5: the pipeline's orthonormalisation --
+ * In place: Y (m×l, m ≥ l) ← Q, Y = Q·R, R upper (l×l, device, may be NULL),
+ * diag(R) ≥ 0 — exactly the kernels rpca_pca / rpca_eigens run for their last
+ * renormalisation and the QR of Bᵀ: tournament LU (Y = L·U), then two
+ * Cholesky-QR steps on L (LU-Cholesky-QR2).  A Cholesky pivot of LᵀL below
+ * 2^-40 of its largest (κ(L) ≳ 1e6) is a breakdown: the call then redoes the
+ * block with Householder TSQR (as rpca_qr) — the drivers re-run the whole
+ * call that way.  *used_householder (host, may be NULL) reports it.
+ * Synchronises the stream.                                                 */
+rpca_status rpca_orthonormalize(rpca_ctx* ctx, double* Y, int64_t m, int64_t l, double* R, int* used_householder);
+
 /* ---- §8(a) steps a5/a7: Householder QR --------
  * In place: Y (m×l, m ≥ l) ← Q with orthonormal columns, Y = Q·R, R upper
  * triangular with diag(R) ≥ 0 (R: l×l device, may be NULL).  Tall-skinny
@@ -224,6 +270,20 @@ rpca_status rpca_pca(rpca_ctx* ctx, const rpca_mat* A, int64_t k, int raw, int i
  * RPCA_E_SHAPE.  Synchronises the stream.                                   */
 rpca_status rpca_eigens(rpca_ctx* ctx, const rpca_mat* A, int64_t k, int its, int64_t l, uint64_t seed,
                         int variant, void* U, int64_t ldu, void* lam);
+
+/* ---- self-adjoint, possibly indefinite A (§8(f) N1) ------------------------
+ * PAPER.md:183-184 ("Further accelerations are possible when A is
+ * self-adjoint").  A square and symmetric (the caller's
+ * promise, not checked).  Q from the self-adjoint loop of PAPER.md:386-412
+ * (as rpca_eigens: its+1 applications, LU inside, QR last); B1 = A·Q (one
+ * more pass); T = (QᵀB1 + B1ᵀQ)/2 = E·Λ·Eᵀ by Jacobi; U = Q·E truncated to
+ * the k eigenvalues of largest |λ| (ties: the larger λ, then the lower index).
+ * its + 2 passes over A.  Outputs in A's dtype: U (m_local×k, ld ldu; the
+ * largest-|·| entry of each column positive), lam (k, signed, |lam|
+ * non-increasing).  Sharding as rpca_eigens (uniform row partition).
+ * Synchronises the stream.                                                 */
+rpca_status rpca_reig(rpca_ctx* ctx, const rpca_mat* A, int64_t k, int its, int64_t l, uint64_t seed, void* U,
+                      int64_t ldu, void* lam);
 
 /* ---- accuracy: ‖A − U·diag(S)·Vᵀ‖ by the randomized power method ----------
  * PAPER.md §4 l.362-371.  x = stream-1 Gaussian n-vector (seed), normalised;

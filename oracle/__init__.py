@@ -62,6 +62,7 @@ def lib():
             L.oracle_pca.argtypes = mat + [i64, i32, i32, i64, u64, i32, dp, dp, dp]
             L.oracle_eigens.argtypes = [i32, i32, i64, vp, i64, vp, vp, vp, i64, i32, i64, u64, i32, i32, dp, dp]
             L.oracle_diffsnorm.argtypes = mat + [i32, dp, dp, dp, i64, i32, u64, dp]
+            L.oracle_reig.argtypes = [i32, i32, i64, vp, i64, vp, vp, vp, i64, i32, i64, u64, i32, dp, dp]
             L.oracle_apply.argtypes = mat + [i32, i32, dp, i64, dp]
             L.oracle_colmeans.argtypes = mat + [dp]
             L.oracle_num_threads.argtypes = []
@@ -198,6 +199,20 @@ def eigens(A, k: int, its: int = 2, l: int | None = None, seed: int = 0, dist: i
     a = [args[0], args[1], n, args[4], args[5], args[6], args[7], args[8]]
     _check(lib().oracle_eigens(*a, k, its, -1 if l is None else l, seed, dist, variant, _p(U), _p(lam)),
            "eigens")
+    return U, lam
+
+
+def reig(A, k: int, its: int = 2, l: int | None = None, seed: int = 0, dist: int = GAUSSIAN):
+    """(U n×k, lam k) — self-adjoint eigendecomposition, PAPER.md:183-184 / SPEC.md:229-237
+    (|lam| non-increasing, signed)."""
+    keep, args = _mat_args(A)
+    n = args[2]
+    if args[2] != args[3]:
+        raise ValueError("reig needs a square matrix")
+    U = np.empty((n, k))
+    lam = np.empty(k)
+    a = [args[0], args[1], n, args[4], args[5], args[6], args[7], args[8]]
+    _check(lib().oracle_reig(*a, k, its, -1 if l is None else l, seed, dist, _p(U), _p(lam)), "reig")
     return U, lam
 
 

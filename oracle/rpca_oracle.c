@@ -805,6 +805,78 @@ done:
 }
 
 /* ------------------------------------------------------------------------
+ * oracle_reig — the self-adjoint (possibly indefinite) eigendecomposition:
+ * PAPER.md:183-184 (§2, "Further accelerations are possible when A is
+ * self-adjoint"), the self-adjoint range finder of §5 PAPER.md:386-416 (the
+ * loop of oracle_eigens: LU in interior rounds, QR at the last), then
+ * T = QᵀAQ (one more application of A: B1 = A·Q,
+ * T = QᵀB1), symmetrised (T + Tᵀ)/2, its dense eigendecomposition (the
+ * cyclic Jacobi of oracle_jacobi_eig), U = Q·E, truncated to the k
+ * eigenvalues of largest |λ| (ties: the larger λ, then the lower index;
+ * SPEC.md "Open Questions": truncation by |λ|).  its + 2 applications of A.
+ * Outputs: U n×k (largest-|·| entry of each column positive), lam k (signed,
+ * |lam| non-increasing).
+ * ---------------------------------------------------------------------- */
+int oracle_reig(int kind, int dtype, int64_t n, const void* a, int64_t lda,
+                const int64_t* rowptr, const int32_t* colind, const void* vals,
+                int64_t k, int its, int64_t l, uint64_t seed, int dist, double* U, double* lam) {
+  omat A;
+  int st = make_omat(&A, kind, dtype, n, n, a, lda, rowptr, colind, vals);
+  if (st) return st;
+  if (l <= 0) l = k + 2;
+  if (k < 1 || l < k || l > n || l > 512 || its < 0) return ORC_E_SHAPE;
+  double* Om = (double*)malloc((size_t)(n * l) * sizeof(double));
+  double* Q = (double*)malloc((size_t)(n * l) * sizeof(double));
+  double* B1 = (double*)malloc((size_t)(n * l) * sizeof(double));
+  double* T = (double*)malloc((size_t)(l * l) * sizeof(double));
+  double* E = (double*)malloc((size_t)(l * l) * sizeof(double));
+  double* mu = (double*)malloc((size_t)l * sizeof(double));
+  int64_t* ord = (int64_t*)malloc((size_t)l * sizeof(int64_t));
+  oracle_omega(seed, 0u, n, l, dist, Om);
+  if (dtype == 1) round_to_f32(Om, n * l);
+  apply_A(&A, NULL, Om, l, Q);
+  st = (its == 0) ? oracle_house_qr(Q, n, l, NULL) : oracle_lu_renorm(Q, n, l, NULL, NULL);
+  if (st) goto done;
+  for (int it = 1; it <= its; ++it) {
+    apply_A(&A, NULL, Q, l, B1);
+    memcpy(Q, B1, (size_t)(n * l) * sizeof(double));
+    st = (it < its) ? oracle_lu_renorm(Q, n, l, NULL, NULL) : oracle_house_qr(Q, n, l, NULL);
+    if (st) goto done;
+  }
+  apply_A(&A, NULL, Q, l, B1);
+  for (int64_t p = 0; p < l; ++p) /* T = QᵀAQ */
+    for (int64_t q = 0; q < l; ++q) T[p * l + q] = dot_rows(Q + p, l, B1 + q, l, 0, n);
+  for (int64_t p = 0; p < l; ++p) /* (T + Tᵀ)/2 */
+    for (int64_t q = p + 1; q < l; ++q) {
+      double s = 0.5 * (T[p * l + q] + T[q * l + p]);
+      T[p * l + q] = T[q * l + p] = s;
+    }
+  oracle_jacobi_eig(T, l, mu, E); /* mu non-increasing, E's columns the eigenvectors */
+  for (int64_t j = 0; j < l; ++j) ord[j] = j; /* stable insertion sort by |mu| desc, ties: larger mu first */
+  for (int64_t i = 1; i < l; ++i) {
+    int64_t o = ord[i], j = i;
+    while (j > 0 && (fabs(mu[ord[j - 1]]) < fabs(mu[o]) ||
+                     (fabs(mu[ord[j - 1]]) == fabs(mu[o]) && mu[ord[j - 1]] < mu[o]))) {
+      ord[j] = ord[j - 1];
+      --j;
+    }
+    ord[j] = o;
+  }
+#pragma omp parallel for schedule(static)
+  for (int64_t i = 0; i < n; ++i) /* U = Q·E[:, ord[:k]] */
+    for (int64_t j = 0; j < k; ++j) {
+      double s = 0.0;
+      for (int64_t t = 0; t < l; ++t) s += Q[i * l + t] * E[t * l + ord[j]];
+      U[i * k + j] = s;
+    }
+  for (int64_t j = 0; j < k; ++j) lam[j] = mu[ord[j]];
+  sign_normalize(NULL, 0, U, n, k);
+done:
+  free(Om); free(Q); free(B1); free(T); free(E); free(mu); free(ord);
+  return st;
+}
+
+/* ------------------------------------------------------------------------
  * oracle_diffsnorm — §4: the spectral norm of the
  * discrepancy ‖A − UΣV*‖ by the power method with a random start
  * (Kuczyński–Woźniakowski, within a factor of two w.h.p.).  Reading Q13:

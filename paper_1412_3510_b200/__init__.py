@@ -17,9 +17,10 @@ import threading
 
 import torch
 
-__all__ = ["pca", "eigens", "diffsnorm", "omega", "apply", "apply_int8emu", "colmeans", "lu_renorm", "qr", "small_svd",
-           "launch_count", "library_path", "RPCAError", "CSR", "profile", "clear_cache", "comm_unique_id",
-           "comm_init", "comm_init_torch", "VirtualGroup", "uniform_shard"]
+__all__ = ["pca", "eigens", "reig", "diffsnorm", "omega", "apply", "apply_int8emu", "colmeans", "lu_renorm", "qr",
+           "orthonormalize", "small_svd", "launch_count", "library_path", "RPCAError", "CSR", "profile", "clear_cache",
+           "comm_unique_id", "comm_init", "comm_init_torch", "VirtualGroup", "uniform_shard", "workspace_query",
+           "set_workspace"]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 # RPCA_LIB_PATH: an alternative build of the same library (tuning experiments)
@@ -32,6 +33,7 @@ DEVICE, HOST = 0, 1
 GAUSSIAN, UNIFORM = 0, 1
 SHIFT_CHOL, SQRT = 0, 1
 FLAG_UNIFORM_OMEGA, FLAG_OUTPUTS_HOST, FLAG_CHECK_FINITE = 0x1, 0x2, 0x4
+OP_PCA, OP_EIGENS, OP_DIFFSNORM, OP_APPLY, OP_REIG = 1, 2, 3, 4, 5
 
 
 class RPCAError(RuntimeError):
@@ -75,6 +77,9 @@ def _load():
             "rpca_ctx_clear_cache": [vp],
             "rpca_launch_count": [vp, C.POINTER(i64)],
             "rpca_workspace_size": [vp, C.POINTER(C.c_size_t)],
+            "rpca_workspace_query": [vp, i32, pm, i64, i64, i32, C.POINTER(C.c_size_t)],
+            "rpca_set_workspace": [vp, vp, C.c_size_t],
+            "rpca_orthonormalize": [vp, dp, i64, i64, dp, C.POINTER(C.c_int)],
             "rpca_profile_begin": [vp],
             "rpca_profile_begin_mode": [vp, i32],
             "rpca_profile_end": [vp, C.c_char_p, C.c_size_t, C.POINTER(C.c_size_t)],
@@ -92,6 +97,7 @@ def _load():
             "rpca_small_svd": [vp, dp, i64, i64, dp, dp, dp],
             "rpca_pca": [vp, pm, i64, i32, i32, i64, u64, vp, i64, vp, vp, i64],
             "rpca_eigens": [vp, pm, i64, i32, i64, u64, i32, vp, i64, vp],
+            "rpca_reig": [vp, pm, i64, i32, i64, u64, vp, i64, vp],
             "rpca_diffsnorm": [vp, pm, i32, dp, i64, dp, dp, i64, i64, i32, u64, C.POINTER(C.c_double)],
         }
         for name, args in sig.items():
@@ -163,7 +169,9 @@ def _dense(A: torch.Tensor, host=False, m_total=None, row0=0) -> rpca_mat:
 
 class CSR:
     """A sparse row-major matrix for the library: rowptr (int64, m+1), colind
-    (int32, sorted within rows), vals (float64/float32), shape (m, n), on one GPU."""
+    (int32, sorted within rows), vals (float64/float32), shape (m, n), on one
+    GPU — or in (pinned) host memory: pca / eigens / diffsnorm then copy it to
+    the device inside the call (the end-to-end mode)."""
 
     def __init__(self, rowptr, colind, vals, shape):
         self.rowptr = rowptr.to(torch.int64).contiguous()
@@ -187,8 +195,9 @@ def _as_mat(A, host=False, m_total=None, row0=0):
     if isinstance(A, CSR):
         ml, n = A.shape
         m = ml if m_total is None else int(m_total)
+        loc = HOST if A.device.type == "cpu" else DEVICE
         mat = rpca_mat(CSR_KIND, _dtype_code(A.dtype), m, n, int(row0), ml, None, n, A.rowptr.data_ptr(),
-                       A.colind.data_ptr(), A.vals.data_ptr(), A.vals.numel(), DEVICE, 0)
+                       A.colind.data_ptr(), A.vals.data_ptr(), A.vals.numel(), loc, 0)
         return mat, A
     return _dense(A, host=host, m_total=m_total, row0=row0), A
 
@@ -247,6 +256,28 @@ class VirtualGroup:
         if self.h:
             _check(_load().rpca_virtual_group_destroy(self.h))
             self.h = C.c_void_p()
+
+
+def workspace_query(op: int, A, k: int = 1, l: int | None = None, its: int = 2, m_total=None, row0=0) -> int:
+    """Device bytes one call of `op` (OP_PCA, OP_EIGENS, OP_DIFFSNORM, OP_APPLY) needs for A."""
+    dev = A.device if isinstance(A, torch.Tensor) and A.device.type == "cuda" else torch.device(
+        "cuda", torch.cuda.current_device())
+    L, h = _ctx(dev)
+    mat, keep = _as_mat(A, host=isinstance(A, torch.Tensor) and A.device.type == "cpu", m_total=m_total, row0=row0)
+    out = C.c_size_t(0)
+    _check(L.rpca_workspace_query(h, op, C.byref(mat), k, -1 if l is None else l, its, C.byref(out)))
+    return out.value
+
+
+def set_workspace(buf: torch.Tensor | None, device=None):
+    """Use `buf` (a device tensor, 256-byte aligned, kept alive by the caller)
+    as this thread's context workspace; None returns to a context-owned one."""
+    dev = torch.device("cuda", torch.cuda.current_device() if device is None else device)
+    L, h = _ctx(buf.device if buf is not None else dev)
+    if buf is None:
+        _check(L.rpca_set_workspace(h, None, 0))
+    else:
+        _check(L.rpca_set_workspace(h, C.c_void_p(buf.data_ptr()), buf.numel() * buf.element_size()))
 
 
 def clear_cache(device=None):
@@ -364,6 +395,18 @@ def qr(Y: torch.Tensor):
     return Q, R
 
 
+def orthonormalize(Y: torch.Tensor):
+    """(Q, R, used_householder): the pipeline's final orthonormalisation
+    (LU-Cholesky-QR2, Householder TSQR after a breakdown), diag(R) ≥ 0."""
+    L_, h = _ctx(Y.device)
+    Q = Y.contiguous().clone()
+    m, l = Q.shape
+    R = torch.zeros(l, l, dtype=torch.float64, device=Y.device)
+    used = C.c_int(0)
+    _check(L_.rpca_orthonormalize(h, _ptr(Q), m, l, _ptr(R), C.byref(used)))
+    return Q, R, bool(used.value)
+
+
 def small_svd(G: torch.Tensor):
     """G = Vt·diag(s)·Wᵀ (eq. i3 applied to Bᵀ)."""
     L_, h = _ctx(G.device)
@@ -377,7 +420,7 @@ def small_svd(G: torch.Tensor):
 
 
 def pca(A: torch.Tensor, k: int, raw: bool = True, its: int = 2, l: int | None = None, seed: int = 0,
-        uniform_omega: bool = False, m_total: int | None = None, row0: int = 0):
+        uniform_omega: bool = False, m_total: int | None = None, row0: int = 0, check_finite: bool = False):
     """Rank-k PCA / SVD of A (§2 eqs. i1-i4, §5): returns (U m×k, S k, V n×k) on A's device.
 
     raw=False centres the columns implicitly.  A may also be
@@ -390,7 +433,8 @@ def pca(A: torch.Tensor, k: int, raw: bool = True, its: int = 2, l: int | None =
     dev = torch.device("cuda", torch.cuda.current_device()) if host else A.device
     L_, h = _ctx(dev)
     m, n = A.shape  # m: local rows
-    flags = (FLAG_UNIFORM_OMEGA if uniform_omega else 0) | (FLAG_OUTPUTS_HOST if host else 0)
+    flags = ((FLAG_UNIFORM_OMEGA if uniform_omega else 0) | (FLAG_OUTPUTS_HOST if host else 0) |
+             (FLAG_CHECK_FINITE if check_finite else 0))
     _ctx_flags(h, flags)
     outdev = torch.device("cpu") if host else dev
     pin = host
@@ -407,7 +451,8 @@ def pca(A: torch.Tensor, k: int, raw: bool = True, its: int = 2, l: int | None =
 
 
 def eigens(A: torch.Tensor, k: int, its: int = 2, l: int | None = None, seed: int = 0,
-           variant: str = "shift_chol", uniform_omega: bool = False, m_total: int | None = None, row0: int = 0):
+           variant: str = "shift_chol", uniform_omega: bool = False, m_total: int | None = None, row0: int = 0,
+           check_finite: bool = False):
     """Stabilised Nyström (§3) of a PSD A: returns (U n×k, lam k).
     Sharded: A holds rows uniform_shard(n, P, rank) and U comes back for them."""
     host = A.device.type == "cpu"
@@ -415,7 +460,8 @@ def eigens(A: torch.Tensor, k: int, its: int = 2, l: int | None = None, seed: in
     L_, h = _ctx(dev)
     n = A.shape[0]  # local rows
     v = {"shift_chol": SHIFT_CHOL, "sqrt": SQRT}[variant]
-    _ctx_flags(h, (FLAG_UNIFORM_OMEGA if uniform_omega else 0) | (FLAG_OUTPUTS_HOST if host else 0))
+    _ctx_flags(h, (FLAG_UNIFORM_OMEGA if uniform_omega else 0) | (FLAG_OUTPUTS_HOST if host else 0) |
+               (FLAG_CHECK_FINITE if check_finite else 0))
     outdev = torch.device("cpu") if host else dev
     U = torch.empty(n, k, dtype=A.dtype, device=outdev, pin_memory=host)
     lam = torch.empty(k, dtype=A.dtype, device=outdev, pin_memory=host)
@@ -427,17 +473,45 @@ def eigens(A: torch.Tensor, k: int, its: int = 2, l: int | None = None, seed: in
     return U, lam
 
 
+def reig(A: torch.Tensor, k: int, its: int = 2, l: int | None = None, seed: int = 0, uniform_omega: bool = False,
+         m_total: int | None = None, row0: int = 0, check_finite: bool = False):
+    """Eigendecomposition of a symmetric (possibly indefinite) A (PAPER.md:183-184,
+    SPEC.md:229-237): returns (U n×k, lam k) with lam signed, |lam| non-increasing.
+    Sharded: A holds rows uniform_shard(n, P, rank) and U comes back for them."""
+    host = A.device.type == "cpu"
+    dev = torch.device("cuda", torch.cuda.current_device()) if host else A.device
+    L_, h = _ctx(dev)
+    n = A.shape[0]
+    _ctx_flags(h, (FLAG_UNIFORM_OMEGA if uniform_omega else 0) | (FLAG_OUTPUTS_HOST if host else 0) |
+               (FLAG_CHECK_FINITE if check_finite else 0))
+    outdev = torch.device("cpu") if host else dev
+    U = torch.empty(n, k, dtype=A.dtype, device=outdev, pin_memory=host)
+    lam = torch.empty(k, dtype=A.dtype, device=outdev, pin_memory=host)
+    mat, keep = _as_mat(A, host=host, m_total=m_total, row0=row0)
+    try:
+        _check(L_.rpca_reig(h, C.byref(mat), k, its, -1 if l is None else l, seed, _ptr(U), k, _ptr(lam)))
+    finally:
+        _ctx_flags(h, 0)
+    return U, lam
+
+
 def diffsnorm(A: torch.Tensor, U: torch.Tensor, S: torch.Tensor, V: torch.Tensor, raw: bool = True, its: int = 20,
-              seed: int = 1, m_total: int | None = None, row0: int = 0) -> float:
+              seed: int = 1, m_total: int | None = None, row0: int = 0, check_finite: bool = False) -> float:
     """Power-method estimate of ‖A − U·diag(S)·Vᵀ‖ (§4 l.362-371).
     Sharded: A and U are this rank's rows, V replicated."""
-    L_, h = _ctx(A.device)
+    host = isinstance(A, torch.Tensor) and A.device.type == "cpu" or isinstance(A, CSR) and A.device.type == "cpu"
+    dev = torch.device("cuda", torch.cuda.current_device()) if host else A.device
+    L_, h = _ctx(dev)
     U = U.to(torch.float64).contiguous()
     V = V.to(torch.float64).contiguous()
     S = S.to(torch.float64).contiguous()
     k = S.shape[0]
     out = C.c_double(0.0)
-    mat, keep = _as_mat(A, m_total=m_total, row0=row0)
-    _check(L_.rpca_diffsnorm(h, C.byref(mat), int(bool(raw)), _ptr(U), max(k, 1), _ptr(S), _ptr(V), max(k, 1), k,
-                             its, seed, C.byref(out)))
+    mat, keep = _as_mat(A, host=host, m_total=m_total, row0=row0)
+    _ctx_flags(h, FLAG_CHECK_FINITE if check_finite else 0)
+    try:
+        _check(L_.rpca_diffsnorm(h, C.byref(mat), int(bool(raw)), _ptr(U), max(k, 1), _ptr(S), _ptr(V), max(k, 1),
+                                 k, its, seed, C.byref(out)))
+    finally:
+        _ctx_flags(h, 0)
     return out.value

@@ -19,6 +19,8 @@ void apply_step(Ctx&, const rpca_mat*, const double*, int, const double*, int64_
 void apply_emu_step(Ctx&, const rpca_mat*, const double*, int64_t, double*);
 void colmeans_step(Ctx&, const rpca_mat*, double*);
 void clear_cache(Ctx&);
+size_t workspace_query(Ctx&, int, const rpca_mat*, int64_t, int64_t, int);
+void set_workspace(Ctx&, void*, size_t);
 }  // namespace rpca
 
 namespace {
@@ -73,6 +75,13 @@ rpca_status rpca_ctx_create(rpca_ctx** out, int device, void* stream, uint32_t f
     c->stream = static_cast<cudaStream_t>(stream);
     c->flags = flags;
     c->num_sms = prop.multiProcessorCount;
+    if (cudaMallocHost(&c->status_host, 64) != cudaSuccess || cudaMalloc(&c->dscratch, 256) != cudaSuccess) {
+      (void)cudaGetLastError();
+      if (c->status_host) cudaFreeHost(c->status_host);
+      delete c;
+      rpca::set_last_error("context scratch allocation failed");
+      throw rpca::Error{RPCA_E_NOMEM};
+    }
     *out = c;
   });
 }
@@ -86,16 +95,19 @@ rpca_status rpca_ctx_destroy(rpca_ctx* c) {
     for (auto& g : c->graphs) cudaGraphExecDestroy(g.second.exec);
     for (auto e : c->prof_pool) cudaEventDestroy(e);
     if (c->status_host) cudaFreeHost(c->status_host);
+    if (c->side) {
+      cudaStreamSynchronize(c->side);
+      cudaStreamDestroy(c->side);
+    }
+    for (auto e : c->side_ev) cudaEventDestroy(e);
     if (c->work) {
       cudaStreamSynchronize(c->work);
       cudaStreamDestroy(c->work);
       cudaEventDestroy(c->fence_in);
       cudaEventDestroy(c->fence_out);
     }
-    if (c->ws) cudaFree(c->ws);
-    if (c->tcache.mem) cudaFree(c->tcache.mem);
-    if (c->tcache.plan_a) cudaFree(c->tcache.plan_a);
-    if (c->tcache.plan_t) cudaFree(c->tcache.plan_t);
+    if (c->ws && !c->ws_user) cudaFree(c->ws);
+    if (c->dscratch) cudaFree(c->dscratch);
     delete c;
   });
 }
@@ -123,6 +135,23 @@ rpca_status rpca_workspace_size(rpca_ctx* c, size_t* bytes) {
   if (!c || !bytes) return RPCA_E_ARG;
   *bytes = c->ws_cap;
   return RPCA_OK;
+}
+
+rpca_status rpca_workspace_query(rpca_ctx* c, int op, const rpca_mat* A, int64_t k, int64_t l, int its,
+                                 size_t* bytes) {
+  if (!c || !A || !bytes) return RPCA_E_ARG;
+  return guard([&] {
+    DeviceScope ds(c->device);
+    *bytes = rpca::workspace_query(*c, op, A, k, l, its);
+  });
+}
+
+rpca_status rpca_set_workspace(rpca_ctx* c, void* dptr, size_t bytes) {
+  if (!c) return RPCA_E_ARG;
+  return guard([&] {
+    DeviceScope ds(c->device);
+    rpca::set_workspace(*c, dptr, bytes);
+  });
 }
 
 rpca_status rpca_launch_count(rpca_ctx* c, int64_t* count) {
@@ -278,6 +307,29 @@ rpca_status rpca_qr(rpca_ctx* c, double* Y, int64_t m, int64_t l, double* R) {
   });
 }
 
+rpca_status rpca_orthonormalize(rpca_ctx* c, double* Y, int64_t m, int64_t l, double* R, int* used_householder) {
+  if (!c || !Y) return RPCA_E_ARG;
+  return guard([&] {
+    RPCA_REQUIRE(l >= 1 && l <= rpca::kMaxL && m >= l, RPCA_E_SHAPE, "need 1 ≤ l ≤ 64, m ≥ l");
+    DeviceScope ds(c->device);
+    const size_t need = std::max(rpca::orth_ws_bytes(*c, m, (int)l), rpca::orth_house_ws_bytes(m, (int)l, 1));
+    rpca::Arena ar = c->arena(need + (size_t)m * l * 8 + 65536);
+    double* Yin = ar.get<double>((size_t)m * l);  // the input, for the fallback
+    RPCA_CUDA(cudaMemcpyAsync(Yin, Y, (size_t)m * l * 8, cudaMemcpyDeviceToDevice, c->stream));
+    RPCA_CUDA(cudaMemsetAsync(rpca::breakdown_flag(*c), 0, 4, c->stream));
+    rpca::profiled_step(*c, [&] { rpca::orthonormalize(*c, Y, m, (int)l, R, ar); });
+    RPCA_CUDA(cudaMemcpyAsync(c->status_host, rpca::breakdown_flag(*c), 4, cudaMemcpyDeviceToHost, c->stream));
+    RPCA_CUDA(cudaStreamSynchronize(c->stream));
+    const int broke = c->status_host[0];
+    if (used_householder) *used_householder = broke;
+    if (broke) {
+      RPCA_CUDA(cudaMemcpyAsync(Y, Yin, (size_t)m * l * 8, cudaMemcpyDeviceToDevice, c->stream));
+      rpca::profiled_step(*c, [&] { rpca::orthonormalize_house(*c, Y, m, (int)l, R, ar); });
+      RPCA_CUDA(cudaStreamSynchronize(c->stream));
+    }
+  });
+}
+
 rpca_status rpca_small_svd(rpca_ctx* c, const double* G, int64_t n, int64_t l, double* Vt, double* sigma,
                            double* W) {
   if (!c || !G || !Vt || !sigma || !W) return RPCA_E_ARG;
@@ -314,6 +366,15 @@ rpca_status rpca_eigens(rpca_ctx* c, const rpca_mat* A, int64_t k, int its, int6
   return guard([&] {
     DeviceScope ds(c->device);
     rpca::eigens(*c, A, k, its, l, seed, variant, U, ldu, lam);
+  });
+}
+
+rpca_status rpca_reig(rpca_ctx* c, const rpca_mat* A, int64_t k, int its, int64_t l, uint64_t seed, void* U,
+                      int64_t ldu, void* lam) {
+  if (!c) return RPCA_E_ARG;
+  return guard([&] {
+    DeviceScope ds(c->device);
+    rpca::eigens(*c, A, k, its, l, seed, 2 /* kReig */, U, ldu, lam);
   });
 }
 

@@ -20,13 +20,19 @@ namespace rpca {
 namespace {
 
 constexpr int kThreads = 256;
+// A Cholesky pivot of LᵀL below 2^-40 of its largest diagonal (κ(L) ≳ 1e6,
+// far from CholeskyQR2's failure at κ ≈ u^-1/2 ≈ 7e7, which LU's bounded
+// multipliers make rare) flags a breakdown: the driver then re-runs the call
+// with Householder TSQR for every final orthonormalisation.
+constexpr double kBreakdown = 0x1p-40;
 
 // One CTA: R = chol(G) (upper, RᵀR = G, G full l×l) → X = R⁻¹ (upper);
 // Rtot = R·Rprev (Rprev upper or NULL); if `signfix`, D = sign(diag(Rtot)):
 // Minv = X·D, Rtot ← D·Rtot.
 __global__ void __launch_bounds__(kThreads) chol_kernel(const double* __restrict__ Gin, int l,
                                                         const double* __restrict__ Rprev, int signfix,
-                                                        double* __restrict__ Minv, double* __restrict__ Rtot) {
+                                                        double* __restrict__ Minv, double* __restrict__ Rtot,
+                                                        int* __restrict__ breakdown) {
   extern __shared__ double sm[];
   double* G = sm;              // l×l
   double* R = sm + l * l;      // l×l
@@ -66,6 +72,7 @@ __global__ void __launch_bounds__(kThreads) chol_kernel(const double* __restrict
   const double floor_ = 0x1p-104 * gmax;  // L (and Q1) are full rank; guard against roundoff only
   for (int j = 0; j < l; ++j) {
     const double dj = G[j * l + j];
+    if (breakdown && tid == 0 && !(dj > kBreakdown * gmax)) *breakdown = 1;
     const double dc = dj > floor_ ? dj : (floor_ > 0.0 ? floor_ : 1.0);
     const double ri = rsqrt(dc);  // 1/R_jj
     for (int i = j + tid; i < l; i += kThreads) R[j * l + i] = i == j ? dc * ri : G[j * l + i] * ri;
@@ -126,7 +133,8 @@ __global__ void __launch_bounds__(kThreads) chol_kernel(const double* __restrict
 template <int LP>
 __global__ void __launch_bounds__(32) chol_warp_kernel(const double* __restrict__ Gin, int l,
                                                        const double* __restrict__ Rprev, int signfix,
-                                                       double* __restrict__ Minv, double* __restrict__ Rtot) {
+                                                       double* __restrict__ Minv, double* __restrict__ Rtot,
+                                                       int* __restrict__ breakdown) {
   constexpr unsigned FULL = 0xffffffffu;
   const int lane = threadIdx.x;
   const bool own = lane < l;
@@ -146,6 +154,7 @@ __global__ void __launch_bounds__(32) chol_warp_kernel(const double* __restrict_
   for (int j = 0; j < LP; ++j) {
     if (j >= l) break;
     const double dj = __shfl_sync(FULL, g[j], j);
+    if (breakdown && lane == 0 && !(dj > kBreakdown * gmax)) *breakdown = 1;
     const double dc = dj > floor_ ? dj : (floor_ > 0.0 ? floor_ : 1.0);
     const double ri = rsqrt(dc);
     d[j] = ri;
@@ -198,15 +207,16 @@ __global__ void __launch_bounds__(32) chol_warp_kernel(const double* __restrict_
       if (i < l) Minv[i * l + lane] = pc[i] * dl;
 }
 
-void chol(Ctx& c, const double* G, int l, const double* Rprev, int signfix, double* Minv, double* Rtot) {
+void chol(Ctx& c, const double* G, int l, const double* Rprev, int signfix, double* Minv, double* Rtot,
+          int* bd = nullptr) {
   switch ((l + 7) & ~7) {
-    case 8: chol_warp_kernel<8><<<1, 32, 0, c.stream>>>(G, l, Rprev, signfix, Minv, Rtot); break;
-    case 16: chol_warp_kernel<16><<<1, 32, 0, c.stream>>>(G, l, Rprev, signfix, Minv, Rtot); break;
-    case 24: chol_warp_kernel<24><<<1, 32, 0, c.stream>>>(G, l, Rprev, signfix, Minv, Rtot); break;
-    case 32: chol_warp_kernel<32><<<1, 32, 0, c.stream>>>(G, l, Rprev, signfix, Minv, Rtot); break;
+    case 8: chol_warp_kernel<8><<<1, 32, 0, c.stream>>>(G, l, Rprev, signfix, Minv, Rtot, bd); break;
+    case 16: chol_warp_kernel<16><<<1, 32, 0, c.stream>>>(G, l, Rprev, signfix, Minv, Rtot, bd); break;
+    case 24: chol_warp_kernel<24><<<1, 32, 0, c.stream>>>(G, l, Rprev, signfix, Minv, Rtot, bd); break;
+    case 32: chol_warp_kernel<32><<<1, 32, 0, c.stream>>>(G, l, Rprev, signfix, Minv, Rtot, bd); break;
     default:
       ensure_smem((const void*)chol_kernel, 4 * kMaxL * kMaxL * 8);
-      chol_kernel<<<1, kThreads, 4 * l * l * 8, c.stream>>>(G, l, Rprev, signfix, Minv, Rtot);
+      chol_kernel<<<1, kThreads, 4 * l * l * 8, c.stream>>>(G, l, Rprev, signfix, Minv, Rtot, bd);
   }
   RPCA_CHECK_LAUNCH();
   count_launch(c, 1, "cholqr_chol");
@@ -238,7 +248,7 @@ void orthonormalize(Ctx& c, double* Y, int64_t m, int l, double* R_out, Arena& a
   TagScope ts(c, "cholqr_gram");
   gram(c, Y, Y, m, l, G, ar);              // G = LᵀL
   ar.off = mark;
-  chol(c, G, l, U, 0, M1, R1);             // R1·U
+  chol(c, G, l, U, 0, M1, R1, breakdown_flag(c));  // R1·U
   c.tag = "cholqr_trmm";
   dense_ax(c, Yd, M1, l, Y, ar);           // Q1 = L·R1⁻¹
   ar.off = mark;
@@ -282,12 +292,75 @@ void orthonormalize_sharded(Ctx& c, double* Y, int64_t m, int64_t row0, int l, d
   };
   TagScope ts(c, "cholqr_gram");
   gram_all();
-  chol(c, G, l, U, 0, M1, R1);
+  chol(c, G, l, U, 0, M1, R1, breakdown_flag(c));
   trmm(M1);
   gram_all();
   chol(c, G, l, R1, 1, M2, R2);
   trmm(M2);
   if (R_out) RPCA_CUDA(cudaMemcpyAsync(R_out, R2, sizeof(double) * l * l, cudaMemcpyDeviceToDevice, c.stream));
+}
+
+// ---------------------------------------------------------------- fallback
+// Householder TSQR (tsqr.cu) for the final orthonormalisation when the
+// LU-Cholesky-QR2 above flagged a breakdown (kBreakdown): unconditionally
+// backward stable, slower (≈ 4 block passes, one CTA per leaf).
+
+namespace {
+// out (l×l) = the rows × l block `in` zero-padded to l rows
+__global__ void pad_rows_kernel(const double* __restrict__ in, int64_t rows, int l, double* __restrict__ out) {
+  for (int idx = threadIdx.x; idx < l * l; idx += blockDim.x) out[idx] = idx / l < rows ? in[idx] : 0.0;
+}
+}  // namespace
+
+size_t orth_house_ws_bytes(int64_t m, int l, int nranks) {
+  Sizer s;
+  s.add<double>((size_t)nranks * l * l * 2 + 2 * (size_t)l * l);
+  s.add<double>((size_t)std::max<int64_t>(m, 1) * l);
+  const int64_t stack = std::max<int64_t>((int64_t)nranks * l, l);
+  return s.total + std::max(qr_ws_bytes(std::max<int64_t>(m, l), l), qr_ws_bytes(stack, l)) +
+         thin_gemm_ws_bytes(std::max<int64_t>(m, 1), l, l) + 65536;
+}
+
+void orthonormalize_house(Ctx& c, double* Y, int64_t m, int l, double* R_out, Arena& ar, const double* mu) {
+  if (mu) sub_rank1(c, Y, m, l, nullptr, mu);
+  qr(c, Y, m, l, R_out, ar);
+}
+
+// Rows [row0, row0+m) of a row-sharded block: local QR (Y_p = Q_p·R_p; a shard
+// of fewer than l rows is its own R, zero-padded, with Q_p = I), the l×l R_p
+// all-gathered in rank order, QR of the stack (the same bytes on every rank ⇒
+// the same Q_s, R), Y_p ← Q_p·Q_s[rank].  diag(R) ≥ 0 from the stack's QR.
+void orthonormalize_house_sharded(Ctx& c, double* Y, int64_t m, int l, double* R_out, Arena& ar,
+                                  const double* mu) {
+  const int P = comm_size(c), rank = c.comm ? c.comm->rank : 0;
+  const size_t ll = (size_t)l * l;
+  double* Rp = ar.get<double>(ll);
+  double* stack = ar.get<double>((size_t)P * ll);
+  double* Rs = ar.get<double>(ll);
+  double* tmp = ar.get<double>((size_t)std::max<int64_t>(m, 1) * l);
+  const size_t mark = ar.off;
+  if (mu && m > 0) sub_rank1(c, Y, m, l, nullptr, mu);
+  const bool local_qr = m >= l;
+  if (local_qr) {
+    qr(c, Y, m, l, Rp, ar);  // Y ← Q_p
+    ar.off = mark;
+  } else {
+    pad_rows_kernel<<<1, 256, 0, c.stream>>>(Y, m, l, Rp);
+    RPCA_CHECK_LAUNCH();
+    count_launch(c);
+  }
+  allgather_bytes(c, Rp, stack, ll * sizeof(double));
+  qr(c, stack, (int64_t)P * l, l, Rs, ar);  // stack ← Q_s (P·l × l)
+  ar.off = mark;
+  const double* slice = stack + (size_t)rank * ll;
+  if (local_qr) {
+    thin_gemm(c, Y, m, l, slice, l, nullptr, tmp, l, RPCA_F64, ar);
+    RPCA_CUDA(cudaMemcpyAsync(Y, tmp, (size_t)m * l * 8, cudaMemcpyDeviceToDevice, c.stream));
+  } else if (m > 0) {
+    RPCA_CUDA(cudaMemcpyAsync(Y, slice, (size_t)m * l * 8, cudaMemcpyDeviceToDevice, c.stream));
+  }
+  ar.off = mark;
+  if (R_out) RPCA_CUDA(cudaMemcpyAsync(R_out, Rs, ll * sizeof(double), cudaMemcpyDeviceToDevice, c.stream));
 }
 
 }  // namespace rpca

@@ -77,9 +77,11 @@ constexpr int kNcclSum = 0;      // ncclSum
 
 struct NcclComm : Comm {
   void* handle = nullptr;
-  // NCCL collectives can be stream-captured, but that path cannot be exercised
-  // on a one-GPU test box; it stays opt-in (RPCA_NCCL_GRAPH=1) until measured.
-  bool graph = false;
+  // NCCL collectives are stream-captured into the driver call's CUDA graph
+  // (one graph launch per PCA at N > 1 too); RPCA_NCCL_GRAPH=0 launches the
+  // call eagerly instead.  A 1-rank communicator exercises the captured path
+  // on one GPU (tests/test_gpu_sharded.py).
+  bool graph = true;
   bool graphable() const override { return graph; }
   void allreduce_sum(Ctx& c, double* buf, size_t count) override {
     check(nccl().allreduce(buf, buf, count, kNcclFloat64, kNcclSum, handle, c.stream), "ncclAllReduce");
@@ -176,7 +178,7 @@ void comm_init(Ctx& c, int nranks, int rank, const void* id) {
   if (c.comm) comm_destroy(c);
   NcclComm* cm = new NcclComm();
   const char* g = getenv("RPCA_NCCL_GRAPH");
-  cm->graph = g && g[0] == '1';
+  cm->graph = !(g && g[0] == '0');  // captured by default; RPCA_NCCL_GRAPH=0 opts out
   cm->nranks = nranks;
   cm->rank = rank;
   NcclUniqueId u;

@@ -279,8 +279,19 @@ unsigned grid_cap(Ctx& c, int64_t work, int per) {
 }  // namespace
 
 void csr_spmm(Ctx& c, const CsrA& A, const double* X, int l, double* Y, const double* xmean) {
+  csr_spmm_rows(c, A, 0, A.rows, X, l, Y, xmean);
+  csr_spmm_heavy(c, A, X, l, Y, xmean);
+}
+
+// rows [r0, r1) of A·X, heavy rows (> kHeavyNnz nonzeros, when A has a plan) excluded
+void csr_spmm_rows(Ctx& c, const CsrA& Afull, int64_t r0, int64_t r1, const double* X, int l, double* Yfull,
+                   const double* xmean) {
   RPCA_REQUIRE(l >= 1 && l <= kMaxL, RPCA_E_SHAPE, "l out of range");
-  if (A.rows == 0) return;
+  if (r1 <= r0) return;
+  CsrA A = Afull;  // the row range as a CSR of its own (row pointers stay absolute)
+  A.ptr = Afull.ptr + r0;
+  A.rows = r1 - r0;
+  double* Y = Yfull + r0 * l;
   const unsigned grid = grid_cap(c, A.rows, kThreads / 32);
   const int64_t heavy = A.nhc ? kHeavyNnz : INT64_MAX;
   prof_pre(c);
@@ -316,6 +327,10 @@ void csr_spmm(Ctx& c, const CsrA& A, const double* X, int l, double* Y, const do
                                                             xmean, Y);
   RPCA_CHECK_LAUNCH();
   count_launch(c, 1, "csr_spmm");
+}
+
+// the heavy rows of A·X: one warp per 4096-nonzero chunk, chunks summed in order
+void csr_spmm_heavy(Ctx& c, const CsrA& A, const double* X, int l, double* Y, const double* xmean) {
   if (A.nhc) {
     const unsigned g2 = grid_cap(c, A.nhc, kThreads / 32);
     if (A.dtype == RPCA_F64)
@@ -332,15 +347,26 @@ void csr_spmm(Ctx& c, const CsrA& A, const double* X, int l, double* Y, const do
   }
 }
 
-void* csr_build_heavy_plan(Ctx& c, CsrA& A) {
+// at most 2·nnz/kHeavyNnz + 1 chunks over at most nnz/kHeavyNnz + 1 heavy rows
+size_t csr_heavy_plan_bytes(const CsrA& A) {
+  const int64_t C = 2 * (A.nnz / kHeavyNnz) + 1, H = A.nnz / kHeavyNnz + 2;
+  return Arena::align((size_t)C * 3 * 8) + Arena::align((size_t)H * 2 * 8) + Arena::align((size_t)C * kMaxL * 8);
+}
+
+void csr_build_heavy_plan(Ctx& c, CsrA& A, char* mem, const int64_t* host_ptr) {
   A.hc = nullptr;
   A.hr = nullptr;
   A.nhc = A.nhr = 0;
   A.hpart = nullptr;
-  if (A.rows == 0) return nullptr;
-  std::vector<int64_t> ptr((size_t)A.rows + 1);
-  RPCA_CUDA(cudaMemcpyAsync(ptr.data(), A.ptr, sizeof(int64_t) * ptr.size(), cudaMemcpyDeviceToHost, c.stream));
-  RPCA_CUDA(cudaStreamSynchronize(c.stream));
+  if (A.rows == 0) return;
+  std::vector<int64_t> buf;
+  const int64_t* ptr = host_ptr;
+  if (!ptr) {
+    buf.resize((size_t)A.rows + 1);
+    RPCA_CUDA(cudaMemcpyAsync(buf.data(), A.ptr, sizeof(int64_t) * buf.size(), cudaMemcpyDeviceToHost, c.stream));
+    RPCA_CUDA(cudaStreamSynchronize(c.stream));
+    ptr = buf.data();
+  }
   std::vector<int64_t> hc, hr;
   for (int64_t i = 0; i < A.rows; ++i) {
     const int64_t t0 = ptr[i], t1 = ptr[i + 1];
@@ -353,22 +379,65 @@ void* csr_build_heavy_plan(Ctx& c, CsrA& A) {
       hc.push_back(std::min(t1, t + kHeavyNnz));
     }
   }
-  if (hr.empty()) return nullptr;
+  if (hr.empty()) return;
   const int64_t nhc = (int64_t)hc.size() / 3, nhr = (int64_t)hr.size() / 2;
   hr.push_back(-1);
   hr.push_back(nhc);
   const size_t b_hc = Arena::align(hc.size() * 8), b_hr = Arena::align(hr.size() * 8);
-  const size_t b_part = Arena::align((size_t)nhc * kMaxL * 8);
-  char* mem = nullptr;
-  RPCA_CUDA(cudaMalloc(&mem, b_hc + b_hr + b_part));
-  RPCA_CUDA(cudaMemcpy(mem, hc.data(), hc.size() * 8, cudaMemcpyHostToDevice));
-  RPCA_CUDA(cudaMemcpy(mem + b_hc, hr.data(), hr.size() * 8, cudaMemcpyHostToDevice));
+  RPCA_REQUIRE(b_hc + b_hr + Arena::align((size_t)nhc * kMaxL * 8) <= csr_heavy_plan_bytes(A), RPCA_E_WORKSPACE,
+               "heavy-row plan exceeds its bound");
+  RPCA_CUDA(cudaMemcpyAsync(mem, hc.data(), hc.size() * 8, cudaMemcpyHostToDevice, c.stream));
+  RPCA_CUDA(cudaMemcpyAsync(mem + b_hc, hr.data(), hr.size() * 8, cudaMemcpyHostToDevice, c.stream));
+  RPCA_CUDA(cudaStreamSynchronize(c.stream));  // hc / hr are host temporaries
   A.hc = reinterpret_cast<const int64_t*>(mem);
   A.nhc = nhc;
   A.hr = reinterpret_cast<const int64_t*>(mem + b_hc);
   A.nhr = nhr;
   A.hpart = reinterpret_cast<double*>(mem + b_hc + b_hr);
-  return mem;
+}
+
+namespace {
+__device__ __forceinline__ uint64_t mix64(uint64_t z) {  // splitmix64 finaliser
+  z += 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+// Σ_i mix(word_i, i, salt) mod 2^64 over the 4-byte words of an array:
+// integer sums commute, so the result does not depend on the grid.  (Row
+// shards of a CSR are often views at 4-byte offsets, so no wider alignment is
+// assumed.)
+__global__ void fingerprint_kernel(const uint32_t* __restrict__ w, int64_t nw, uint64_t salt,
+                                   unsigned long long* __restrict__ out) {
+  uint64_t acc = 0;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nw; i += stride)
+    acc += mix64((uint64_t)w[i] ^ mix64((uint64_t)i + salt));
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if ((threadIdx.x & 31) == 0) atomicAdd(out, (unsigned long long)acc);
+}
+}  // namespace
+
+uint64_t csr_fingerprint(Ctx& c, const CsrA& A) {
+  unsigned long long* d = reinterpret_cast<unsigned long long*>(c.dscratch + 64);
+  RPCA_CUDA(cudaMemsetAsync(d, 0, 8, c.stream));
+  const int es = A.dtype == RPCA_F64 ? 8 : 4;
+  const void* arrs[3] = {A.ptr, A.idx, A.vals};
+  const size_t bytes[3] = {(size_t)(A.rows + 1) * 8, (size_t)A.nnz * 4, (size_t)A.nnz * es};
+  for (int a = 0; a < 3; ++a) {
+    if (bytes[a] == 0) continue;
+    RPCA_REQUIRE((reinterpret_cast<uintptr_t>(arrs[a]) & 3) == 0, RPCA_E_ARG, "CSR arrays must be 4-byte aligned");
+    const int64_t nw = (int64_t)(bytes[a] / 4);
+    fingerprint_kernel<<<grid_cap(c, nw, 2048), 256, 0, c.stream>>>(reinterpret_cast<const uint32_t*>(arrs[a]), nw,
+                                                                    0x51ED27ull * (a + 1), d);
+    RPCA_CHECK_LAUNCH();
+    count_launch(c, 1, "csr_fingerprint");
+  }
+  uint64_t h = 0;
+  RPCA_CUDA(cudaMemcpyAsync(&h, d, 8, cudaMemcpyDeviceToHost, c.stream));
+  RPCA_CUDA(cudaStreamSynchronize(c.stream));
+  return h;
 }
 
 size_t csr_transpose_ws_bytes(const CsrA& A) {

@@ -173,17 +173,46 @@ __device__ __forceinline__ void planes4(const uint32_t (&lo)[4], const uint32_t 
   w[6] = __byte_perm(l01b, l23b, 0x5410) ^ 0x80808080u;  // byte 1
 }
 
-// E[i] = exponent of row i's largest |a_ik| (+1): one warp per row
-__global__ void row_exp_kernel(const double* __restrict__ A, int64_t m, int64_t n, int64_t lda, int* __restrict__ E) {
+// E[i] = exponent of row i's largest |a_ik| (+1): one warp per row.  With
+// `wide` given, the same read also sets *wide = 1 for a row whose largest
+// |a_ik| exceeds 1/8 of Σ_k |a_ik| (emulation guard): such a row
+// would meet the emulation's row-max-relative truncation (≈ 2^-55·2^E per
+// term) on terms far below its maximum, so the call keeps the fp64 DMMA pass.
+__global__ void row_exp_kernel(const double* __restrict__ A, int64_t m, int64_t n, int64_t lda, int* __restrict__ E,
+                               int* __restrict__ wide) {
   const int lane = threadIdx.x & 31;
   const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
   for (int64_t i = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); i < m; i += warps) {
     const double* row = A + i * lda;
     unsigned f = 0;
-    for (int64_t k = lane; k < n; k += 32)
-      f = max(f, (unsigned)(__double_as_longlong(row[k]) >> 52) & 0x7FFu);
+    double amax = 0.0, s0 = 0.0, s1 = 0.0;
+    int64_t k = lane;
+    for (; k + 32 < n; k += 64) {
+      const double a0 = row[k], a1 = row[k + 32];
+      f = max(f, max((unsigned)(__double_as_longlong(a0) >> 52) & 0x7FFu,
+                     (unsigned)(__double_as_longlong(a1) >> 52) & 0x7FFu));
+      if (wide) {
+        amax = fmax(amax, fmax(fabs(a0), fabs(a1)));
+        s0 += fabs(a0);
+        s1 += fabs(a1);
+      }
+    }
+    for (; k < n; k += 32) {
+      const double a0 = row[k];
+      f = max(f, (unsigned)(__double_as_longlong(a0) >> 52) & 0x7FFu);
+      if (wide) {
+        amax = fmax(amax, fabs(a0));
+        s0 += fabs(a0);
+      }
+    }
     f = __reduce_max_sync(0xffffffffu, f);
     if (lane == 0) E[i] = exp_of_field((int)f);
+    if (wide) {
+      double s = warp_sum(s0 + s1);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) amax = fmax(amax, __shfl_xor_sync(0xffffffffu, amax, o));
+      if (lane == 0 && 8.0 * amax > s) *wide = 1;
+    }
   }
 }
 
@@ -575,10 +604,10 @@ bool emu_eligible(const DenseA& A, int l) {
          lpn_of(l) <= 48 && A.m >= 128 && A.n >= 32;
 }
 
-void row_exponents(Ctx& c, const DenseA& A, int* E) {
+void row_exponents(Ctx& c, const DenseA& A, int* E, int* wide) {
   if (A.m == 0) return;
   const unsigned grid = (unsigned)std::min<int64_t>(cdiv(A.m, 8), (int64_t)c.num_sms * 16);
-  row_exp_kernel<<<grid, 256, 0, c.stream>>>(static_cast<const double*>(A.a), A.m, A.n, A.lda, E);
+  row_exp_kernel<<<grid, 256, 0, c.stream>>>(static_cast<const double*>(A.a), A.m, A.n, A.lda, E, wide);
   RPCA_CHECK_LAUNCH();
   count_launch(c, 1, "emu_row_exp");
 }

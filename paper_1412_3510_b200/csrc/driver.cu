@@ -15,6 +15,7 @@
 #include <map>
 #include <mutex>
 #include <string>
+#include <type_traits>
 
 #include "comm.cuh"
 
@@ -182,28 +183,50 @@ void drop_graphs(Ctx& c) {
   c.graphs.clear();
 }
 
-Arena Ctx::arena(size_t bytes) {
-  if (bytes > ws_cap) {
-    if (ws) {
-      RPCA_CUDA(cudaStreamSynchronize(stream));
-      for (auto& g : graphs) cudaGraphExecDestroy(g.second.exec);
-      graphs.clear();
-      RPCA_CUDA(cudaFree(ws));
-      ws = nullptr;
-      ws_cap = 0;
-    }
-    const size_t want = bytes + (bytes >> 4) + (1 << 20);
-    cudaError_t e = cudaMalloc(&ws, want);
-    if (e != cudaSuccess) {
-      (void)cudaGetLastError();
-      set_last_error("workspace cudaMalloc(%zu) failed: %s", want, cudaGetErrorString(e));
-      throw Error{RPCA_E_NOMEM};
-    }
-    ws_cap = want;
+void Ctx::rebase(char* old_base, char* new_base) {
+  auto mv = [&](auto& p) {
+    if (p) p = reinterpret_cast<std::remove_reference_t<decltype(p)>>(
+               new_base + (reinterpret_cast<const char*>(p) - old_base));
+  };
+  for (CsrA* a : {&tcache.A, &tcache.T}) {
+    mv(a->hc);
+    mv(a->hr);
+    mv(a->hpart);
   }
+  mv(tcache.T.ptr);
+  mv(tcache.T.idx);
+  mv(tcache.T.vals);
+}
+
+void Ctx::reserve(size_t total) {
+  if (total <= ws_cap) return;
+  RPCA_REQUIRE(!ws_user, RPCA_E_WORKSPACE,
+               "caller workspace too small: %zu bytes needed, %zu given (rpca_workspace_query)", total, ws_cap);
+  const size_t want = total + (total >> 4) + (1 << 20);
+  char* nws = nullptr;
+  RPCA_CUDA(cudaStreamSynchronize(stream));
+  for (auto& g : graphs) cudaGraphExecDestroy(g.second.exec);
+  graphs.clear();
+  const cudaError_t e = cudaMalloc(&nws, want);
+  if (e != cudaSuccess) {
+    (void)cudaGetLastError();
+    set_last_error("workspace cudaMalloc(%zu) failed: %s", want, cudaGetErrorString(e));
+    throw Error{RPCA_E_NOMEM};
+  }
+  if (ws) {
+    if (persist) RPCA_CUDA(cudaMemcpy(nws, ws, persist, cudaMemcpyDeviceToDevice));
+    rebase(ws, nws);
+    RPCA_CUDA(cudaFree(ws));
+  }
+  ws = nws;
+  ws_cap = want;
+}
+
+Arena Ctx::arena(size_t bytes) {
+  reserve(persist + bytes);
   Arena a;
-  a.base = ws;
-  a.cap = ws_cap;
+  a.base = ws + persist;
+  a.cap = ws_cap - persist;
   a.off = 0;
   return a;
 }
@@ -225,7 +248,6 @@ void validate_mat(const rpca_mat* A) {
   } else {
     RPCA_REQUIRE(A->rowptr && (A->nnz == 0 || (A->colind && A->vals)), RPCA_E_ARG, "CSR arrays are NULL");
     RPCA_REQUIRE(A->nnz >= 0 && A->n <= INT32_MAX, RPCA_E_SHAPE, "bad nnz / n > 2^31-1");
-    RPCA_REQUIRE(A->location == RPCA_DEVICE, RPCA_E_NOTIMPL, "host CSR inputs are not supported");
   }
 }
 
@@ -249,53 +271,86 @@ MatV probe_of(const rpca_mat* A) {
   return v;
 }
 
-void free_plans(Ctx& c) {
-  if (c.tcache.plan_a) cudaFree(c.tcache.plan_a);
-  if (c.tcache.plan_t) cudaFree(c.tcache.plan_t);
-  c.tcache.plan_a = c.tcache.plan_t = nullptr;
+// Device bytes of CSR(Aᵀ) (n+1 row pointers, nnz indices and values) plus the
+// heavy-row plans of A and Aᵀ: the persistent prefix a sparse A keeps in the
+// workspace, and the scratch its construction needs (above the prefix).
+struct CsrLayout {
+  size_t b_ptr, b_idx, b_val, b_plan_a, b_plan_t;
+  size_t persist() const { return b_ptr + b_idx + b_val + b_plan_a + b_plan_t; }
+};
+CsrLayout csr_layout(const rpca_mat* A) {
+  const CsrA probe{nullptr, nullptr, nullptr, A->dtype, A->m_local, A->nnz};
+  return CsrLayout{Arena::align((A->n + 1) * 8), Arena::align(A->nnz * 4 + 4),
+                   Arena::align(A->nnz * elem_size(A->dtype) + 8), csr_heavy_plan_bytes(probe),
+                   csr_heavy_plan_bytes(probe)};
+}
+size_t csr_build_scratch(const rpca_mat* A) {
+  const CsrA probe{nullptr, nullptr, nullptr, A->dtype, A->m_local, A->nnz};
+  return csr_transpose_ws_bytes(probe) + 65536;
 }
 
-// CSR(Aᵀ) is built once per sparse A (before any graph capture) and cached,
-// with the heavy-row plans of A and Aᵀ.
-void ensure_transpose(Ctx& c, const rpca_mat* A) {
-  if (A->kind != RPCA_CSR) return;
-  KeyHasher kh;
-  kh << A->rowptr << A->colind << A->vals << A->m_local << A->n << A->nnz << A->dtype;
-  if (c.tcache.mem && c.tcache.key == kh.h) return;
-  if (c.tcache.mem) {
-    RPCA_CUDA(cudaStreamSynchronize(c.stream));
-    RPCA_CUDA(cudaFree(c.tcache.mem));
-    c.tcache.mem = nullptr;
-    free_plans(c);
-  }
-  const int es = elem_size(A->dtype);
-  const size_t b_ptr = Arena::align((A->n + 1) * 8), b_idx = Arena::align(A->nnz * 4 + 4);
-  const size_t b_val = Arena::align(A->nnz * es + 8);
-  char* mem = nullptr;
-  RPCA_CUDA(cudaMalloc(&mem, b_ptr + b_idx + b_val));
+// Lay CSR(Aᵀ) and both plans out in `mem` (a CsrLayout's worth of bytes) and
+// build them, using `scratch` for the transpose.  host_ptr: A's row pointers
+// on the host when A was copied from there.
+void build_transpose(Ctx& c, CsrA& src, int64_t n, char* mem, Arena& scratch, CsrA& T, const int64_t* host_ptr,
+                     const CsrLayout& L) {
+  T = CsrA{reinterpret_cast<int64_t*>(mem), reinterpret_cast<int32_t*>(mem + L.b_ptr), mem + L.b_ptr + L.b_idx,
+           src.dtype, n, src.nnz};
+  csr_transpose(c, src, n, T, scratch);
+  char* plans = mem + L.b_ptr + L.b_idx + L.b_val;
+  csr_build_heavy_plan(c, src, plans, host_ptr);
+  csr_build_heavy_plan(c, T, plans + L.b_plan_a);
+}
+
+// A device CSR A's transpose is built once per matrix (before any graph
+// capture) and cached at the start of the workspace, keyed by the pointers,
+// shape and a fingerprint of the contents (pointers alone are
+// recycled by allocators).  Host CSR inputs are copied and transposed inside
+// each call instead (device_view).  Returns the fingerprint (0 for dense A).
+uint64_t ensure_transpose(Ctx& c, const rpca_mat* A) {
+  if (A->kind != RPCA_CSR || A->location != RPCA_DEVICE) return 0;
   CsrA src{A->rowptr, A->colind, A->vals, A->dtype, A->m_local, A->nnz};
-  CsrA T{reinterpret_cast<int64_t*>(mem), reinterpret_cast<int32_t*>(mem + b_ptr), mem + b_ptr + b_idx, A->dtype,
-         A->n, A->nnz};
-  const size_t sb = csr_transpose_ws_bytes(src) + 65536;
-  char* scratch = nullptr;
-  RPCA_CUDA(cudaMalloc(&scratch, sb));
-  Arena ar{scratch, sb, 0};
-  csr_transpose(c, src, A->n, T, ar);
+  const uint64_t fp = csr_fingerprint(c, src);
+  KeyHasher kh;
+  kh << A->rowptr << A->colind << A->vals << A->m_local << A->n << A->nnz << A->dtype << fp;
+  if (c.tcache.valid && c.tcache.key == kh.h) return fp;
   RPCA_CUDA(cudaStreamSynchronize(c.stream));
-  RPCA_CUDA(cudaFree(scratch));
-  c.tcache.mem = mem;
-  c.tcache.key = kh.h;
-  c.tcache.plan_a = csr_build_heavy_plan(c, src);
-  c.tcache.plan_t = csr_build_heavy_plan(c, T);
+  drop_graphs(c);
+  c.tcache.valid = false;
+  c.persist = 0;
+  const CsrLayout L = csr_layout(A);
+  c.reserve(L.persist() + csr_build_scratch(A));
+  Arena scratch{c.ws + L.persist(), c.ws_cap - L.persist(), 0};
+  build_transpose(c, src, A->n, c.ws, scratch, c.tcache.T, nullptr, L);
+  RPCA_CUDA(cudaStreamSynchronize(c.stream));
   c.tcache.A = src;
-  c.tcache.T = T;
+  c.tcache.key = kh.h;
+  c.tcache.valid = true;
+  c.persist = L.persist();
+  return fp;
 }
 
 MatV device_view(Ctx& c, const rpca_mat* A, Arena& ar) {
   MatV v = probe_of(A);
-  if (v.csr) {
+  if (v.csr && A->location == RPCA_DEVICE) {
     v.a = c.tcache.A;
     v.at = c.tcache.T;
+    return v;
+  }
+  if (v.csr) {  // host CSR: copy the three arrays, then transpose and plan in the arena
+    const int es = elem_size(A->dtype);
+    int64_t* ptr = ar.get<int64_t>(A->m_local + 1);
+    int32_t* idx = ar.get<int32_t>(A->nnz + 1);
+    char* vals = ar.get<char>((size_t)A->nnz * es + 8);
+    RPCA_CUDA(cudaMemcpyAsync(ptr, A->rowptr, (A->m_local + 1) * 8, cudaMemcpyHostToDevice, c.stream));
+    RPCA_CUDA(cudaMemcpyAsync(idx, A->colind, (size_t)A->nnz * 4, cudaMemcpyHostToDevice, c.stream));
+    RPCA_CUDA(cudaMemcpyAsync(vals, A->vals, (size_t)A->nnz * es, cudaMemcpyHostToDevice, c.stream));
+    const CsrLayout L = csr_layout(A);
+    char* mem = ar.get<char>(L.persist());
+    const size_t mark = ar.off;
+    v.a = CsrA{ptr, idx, vals, A->dtype, A->m_local, A->nnz};
+    build_transpose(c, v.a, A->n, mem, ar, v.at, A->rowptr, L);
+    ar.off = mark;
     return v;
   }
   if (A->location == RPCA_HOST && A->m_local > 0) {
@@ -307,10 +362,16 @@ MatV device_view(Ctx& c, const rpca_mat* A, Arena& ar) {
   return v;
 }
 
+// arena bytes device_view takes for a host A (+ the transpose scratch of a host CSR)
 size_t host_copy_bytes(const rpca_mat* A) {
-  return (A->kind == RPCA_DENSE && A->location == RPCA_HOST)
-             ? (size_t)A->m_local * A->lda * elem_size(A->dtype) + 256
-             : 0;
+  if (A->location != RPCA_HOST) return 0;
+  if (A->kind == RPCA_DENSE) return (size_t)A->m_local * A->lda * elem_size(A->dtype) + 256;
+  Sizer s;
+  s.add<int64_t>(A->m_local + 1);
+  s.add<int32_t>(A->nnz + 1);
+  s.add<char>((size_t)A->nnz * elem_size(A->dtype) + 8);
+  s.add<char>(csr_layout(A).persist());
+  return s.total + csr_build_scratch(A);
 }
 
 // The operator the range finder sketches (reading Q6): F = A, or Aᵀ if m < n.
@@ -430,6 +491,42 @@ const double* fwd(Ctx& c, const Op& F, const double* X, int l, double* Y, double
   }
   return ax_and_mean(c, F, X, l, Y, mu, ar);  // Y = P·(A·X), P pending
 }
+// Sharded sparse Z = Aᵀ·(P·Y) with its all-reduce (C5's n×l
+// reduction is 256 MB, comparable to the SpMM itself): the heavy rows of
+// CSR(Aᵀ) first, then the light rows in tiles of n/kTiles output rows, each
+// tile's all-reduce issued on the context's second stream as soon as the tile
+// is written, so the NCCL transfer of tile t overlaps the SpMM of tile t+1.
+// Inside a captured call the fork/join events become graph edges.
+constexpr int kAllreduceTiles = 8;
+
+void csr_aty_allreduce_overlapped(Ctx& c, const CsrA& T, const double* Y, int l, double* Z, const double* ymean) {
+  const int64_t n = T.rows;
+  if (!c.side) RPCA_CUDA(cudaStreamCreateWithFlags(&c.side, cudaStreamNonBlocking));
+  while ((int)c.side_ev.size() < kAllreduceTiles + 1) {
+    cudaEvent_t e;
+    RPCA_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    c.side_ev.push_back(e);
+  }
+  csr_spmm_heavy(c, T, Y, l, Z, ymean);
+  const cudaStream_t main = c.stream;
+  for (int t = 0; t < kAllreduceTiles; ++t) {
+    const int64_t j0 = n * t / kAllreduceTiles, j1 = n * (t + 1) / kAllreduceTiles;
+    csr_spmm_rows(c, T, j0, j1, Y, l, Z, ymean);
+    RPCA_CUDA(cudaEventRecord(c.side_ev[t], main));
+    RPCA_CUDA(cudaStreamWaitEvent(c.side, c.side_ev[t], 0));
+    c.stream = c.side;
+    try {
+      allreduce_sum(c, Z + j0 * l, (size_t)(j1 - j0) * l);
+    } catch (...) {
+      c.stream = main;
+      throw;
+    }
+    c.stream = main;
+  }
+  RPCA_CUDA(cudaEventRecord(c.side_ev[kAllreduceTiles], c.side));
+  RPCA_CUDA(cudaStreamWaitEvent(main, c.side_ev[kAllreduceTiles], 0));
+}
+
 const double* adj(Ctx& c, const Op& F, const double* Y, int l, double* Z, double* mu, double* tmp, Arena& ar) {
   if (F.trans) return ax_and_mean(c, F, Y, l, Z, mu, ar);  // Z = P·(A·Y), P pending
   const double* ym = nullptr;  // Z = Aᵀ·(P·Y)
@@ -437,24 +534,51 @@ const double* adj(Ctx& c, const Op& F, const double* Y, int l, double* Z, double
     column_mean(c, Y, F.A.m, l, F.m_total, F.sharded, tmp, ar);
     ym = tmp;
   }
+  if (F.sharded && F.A.csr && (size_t)F.A.n * l * 8 >= ((size_t)32 << 20)) {
+    csr_aty_allreduce_overlapped(c, F.A.at, Y, l, Z, ym);
+    return nullptr;
+  }
   apply_aty(c, F.A, nullptr, Y, l, Z, ar, ym);
   if (F.sharded) allreduce_sum(c, Z, (size_t)F.A.n * l);
   return nullptr;
 }
 
-// For the duration of a driver call: the row exponents of a dense fp64 A
-// whose A·X passes go to the int8-digit emulation (dense_ax_emu.cu) — one
-// extra read of A, worth it from two A·X passes on.  RPCA_NO_EMU=1 keeps the
-// fp64 tensor-core passes.
+// The int8-digit emulation of a driver call's A·X passes (dense_ax_emu.cu):
+// decided BEFORE the call's graph runs, from one read of A that yields the
+// row exponents and the dynamic-range guard (row_exp_kernel; a synchronising
+// read of one flag) — worth it from two A·X passes on.  A row whose largest
+// |a| exceeds 1/8 of its Σ|a| keeps the call on the fp64 DMMA passes (ADVICE
+// r1).  Device-resident dense fp64 A only (a host A is staged
+// inside the call).  RPCA_NO_EMU=1 disables it.
+struct EmuPlan {
+  const int* E = nullptr;
+  const void* A = nullptr;
+  bool on() const { return E != nullptr; }
+};
+
+EmuPlan emu_prepare(Ctx& c, const rpca_mat* Am, int l, int ax_passes, Arena& ar) {
+  static const bool off = getenv("RPCA_NO_EMU") != nullptr;
+  EmuPlan p;
+  const MatV A = probe_of(Am);
+  if (off || A.csr || Am->location != RPCA_DEVICE || ax_passes < 2 || !emu_eligible(A.d, l)) return p;
+  int* E = ar.get<int>(A.d.m);
+  int* wide = reinterpret_cast<int*>(c.dscratch + 8);
+  RPCA_CUDA(cudaMemsetAsync(wide, 0, 4, c.stream));
+  row_exponents(c, A.d, E, wide);
+  RPCA_CUDA(cudaMemcpyAsync(c.status_host + 2, wide, 4, cudaMemcpyDeviceToHost, c.stream));
+  RPCA_CUDA(cudaStreamSynchronize(c.stream));
+  if (c.status_host[2]) return p;
+  p.E = E;
+  p.A = A.d.a;
+  return p;
+}
+
+// For the duration of a driver call's body: the emulation's row exponents
 struct EmuScope {
   Ctx& c;
-  EmuScope(Ctx& c_, const MatV& A, int l, int ax_passes, Arena& ar) : c(c_) {
-    static const bool off = getenv("RPCA_NO_EMU") != nullptr;
-    if (off || A.csr || ax_passes < 2 || !emu_eligible(A.d, l)) return;
-    int* E = ar.get<int>(A.d.m);
-    row_exponents(c, A.d, E);
-    c.emu_E = E;
-    c.emu_A = A.d.a;
+  EmuScope(Ctx& c_, const EmuPlan& p) : c(c_) {
+    c.emu_E = p.E;
+    c.emu_A = p.A;
   }
   ~EmuScope() {
     c.emu_E = nullptr;
@@ -486,11 +610,47 @@ void renorm_lu(Ctx& c, const Blk& Y, int l, Arena& ar, const double* mu = nullpt
   ar.off = mark;
 }
 // the last renormalisation and the QR of Bᵀ: LU-Cholesky-QR
+// (Householder TSQR instead when the call is re-run after a breakdown)
 void renorm_qr(Ctx& c, const Blk& Y, int l, double* R, Arena& ar, const double* mu = nullptr) {
   const size_t mark = ar.off;
-  if (Y.sharded) orthonormalize_sharded(c, Y.p, Y.rows, Y.row0, l, R, ar, mu);
-  else orthonormalize(c, Y.p, Y.rows, l, R, ar, mu);
+  if (c.force_house) {
+    if (Y.sharded) orthonormalize_house_sharded(c, Y.p, Y.rows, l, R, ar, mu);
+    else orthonormalize_house(c, Y.p, Y.rows, l, R, ar, mu);
+  } else if (Y.sharded) {
+    orthonormalize_sharded(c, Y.p, Y.rows, Y.row0, l, R, ar, mu);
+  } else {
+    orthonormalize(c, Y.p, Y.rows, l, R, ar, mu);
+  }
   ar.off = mark;
+}
+
+// Run a driver body (execute()) with the device status words reset, then read
+// them: RPCA_FLAG_CHECK_FINITE + a non-finite value seen ⇒ RPCA_E_NONFINITE;
+// a Cholesky-QR breakdown (cholqr.cu) ⇒ the whole call runs once more with
+// Householder TSQR for its final orthonormalisations.  The body must carve its
+// buffers from `ar` (rewound for the second run).
+template <class F>
+void run_checked(Ctx& c, uint64_t key, bool graphable, Arena& ar, F&& body) {
+  const size_t mark = ar.off;
+  for (int attempt = 0; attempt < 2; ++attempt) {
+    ar.off = mark;
+    c.force_house = attempt == 1;
+    try {
+      execute(c, key ^ (attempt ? 0x5BD1E9955BD1E995ull : 0ull), graphable, [&] {
+        RPCA_CUDA(cudaMemsetAsync(c.dscratch, 0, 8, c.stream));
+        body();
+      });
+    } catch (...) {
+      c.force_house = false;
+      throw;
+    }
+    c.force_house = false;
+    RPCA_CUDA(cudaMemcpyAsync(c.status_host, c.dscratch, 8, cudaMemcpyDeviceToHost, c.work));
+    RPCA_CUDA(cudaStreamSynchronize(c.work));
+    RPCA_REQUIRE(!((c.flags & RPCA_FLAG_CHECK_FINITE) && c.status_host[0]), RPCA_E_NONFINITE,
+                 "non-finite value in A (or an overflow in A·Ω) — RPCA_FLAG_CHECK_FINITE");
+    if (!c.status_host[1]) return;
+  }
 }
 
 // Without a communicator A must be whole; with one (any size), every rank
@@ -541,10 +701,12 @@ void apply_emu_step(Ctx& c, const rpca_mat* Am, const double* X, int64_t l, doub
   const MatV probe = probe_of(Am);
   RPCA_REQUIRE(!probe.csr && emu_eligible(probe.d, (int)l), RPCA_E_NOTIMPL,
                "apply_int8emu: needs a dense fp64 A (m ≥ 128, n ≥ 32) and 24 < l ≤ 48");
-  Arena ar = c.arena(op_ws(c, probe, (int)l) + (size_t)probe.m * 4 + 65536);
+  Arena ar = c.arena(op_ws(c, probe, (int)l) + (size_t)probe.m * 4 + 65536);  // = the RPCA_OP_APPLY query
   const MatV A = device_view(c, Am, ar);
+  int* E = ar.get<int>(A.d.m);
   profiled_step(c, [&] {
-    EmuScope emu(c, A, (int)l, 2, ar);
+    row_exponents(c, A.d, E);  // the caller asked for the emulation: no dynamic-range guard
+    EmuScope emu(c, EmuPlan{E, A.d.a});
     dense_ax(c, A.d, X, (int)l, Y, ar, nullptr);
   });
 }
@@ -560,14 +722,44 @@ void colmeans_step(Ctx& c, const rpca_mat* Am, double* cm) {
 }
 
 void clear_cache(Ctx& c) {
-  if (c.tcache.mem) {
-    RPCA_CUDA(cudaStreamSynchronize(c.stream));
-    RPCA_CUDA(cudaFree(c.tcache.mem));
-    c.tcache.mem = nullptr;
-    c.tcache.key = 0;
-    free_plans(c);
-  }
+  RPCA_CUDA(cudaStreamSynchronize(c.stream));
+  c.tcache.valid = false;
+  c.tcache.key = 0;
+  c.persist = 0;
   drop_graphs(c);
+}
+
+// Arena bytes of one rpca_pca call (the workspace plan; vectors of length m are
+// this rank's rows).  Used by the driver and by rpca_workspace_query.
+size_t pca_arena_bytes(Ctx& c, const rpca_mat* Am, int64_t k, int64_t l, int64_t ldu, int64_t ldv) {
+  const bool out_host = (c.flags & RPCA_FLAG_OUTPUTS_HOST) != 0;
+  const int osz = elem_size(Am->dtype);
+  const int64_t m = Am->m, n = Am->n, ml = Am->m_local;
+  const int L = (int)l, K = (int)k;
+  const MatV probe = probe_of(Am);
+  const bool trans = m < n;
+  const int64_t nin = trans ? ml : n, nout = trans ? n : ml;
+  Sizer sz;
+  sz.add<char>(host_copy_bytes(Am));
+  sz.add<double>(nin * l);   // Zb
+  sz.add<double>(nout * l);  // Yb
+  sz.add<double>(4 * l * l + 4 * l);
+  sz.add<double>(2 * kMaxL);  // column means
+  sz.add<double>(std::max(nin, nout) * k);  // V-side temp
+  sz.add<double>(k);                        // signs
+  sz.add<int>(ml + 16);                     // row exponents (EmuScope)
+  if (out_host) {
+    sz.add<char>((size_t)ml * ldu * osz);
+    sz.add<char>((size_t)n * ldv * osz);
+    sz.add<char>((size_t)k * osz);
+  }
+  size_t scratch = op_ws(c, probe, L);
+  scratch = std::max(scratch, lu_ws_bytes(std::max(nin, nout), L));
+  scratch = std::max(scratch, orth_ws_bytes(c, std::max(nin, nout), L));
+  scratch = std::max(scratch, qr_ws_bytes(std::max(nin, nout), L) + (size_t)4 * l * l * 8);  // Householder fallback
+  scratch = std::max(scratch, (size_t)(cdiv(std::max(ml, n), 2048) + 2) * (n + 2 * k) * 8 + 65536);
+  scratch = std::max(scratch, thin_gemm_ws_bytes(std::max(nin, nout), L, K) + 65536);
+  return sz.total + scratch + 65536;
 }
 
 // ============================================================ rpca_pca
@@ -587,42 +779,21 @@ void pca(Ctx& c, const rpca_mat* Am, int64_t k, int raw, int its, int64_t l, uin
   const int odt = Am->dtype, osz = elem_size(odt);
   const int64_t m = Am->m, n = Am->n, ml = Am->m_local, r0 = Am->row0;
 
-  // ---- workspace plan (allocation happens before any capture).  Vectors of
-  // length m are this rank's rows (ml of them); U is returned for those rows.
-  const MatV probe = probe_of(Am);
   const bool trans = m < n;
   const int64_t nin = trans ? ml : n, nout = trans ? n : ml;
-  Sizer sz;
-  sz.add<char>(host_copy_bytes(Am));
-  sz.add<double>(nin * l);   // Zb
-  sz.add<double>(nout * l);  // Yb
-  sz.add<double>(4 * l * l + 4 * l);
-  sz.add<double>(2 * kMaxL);  // column means
-  sz.add<double>(std::max(nin, nout) * k);  // V-side temp
-  sz.add<double>(k);                        // signs
-  sz.add<int>(ml + 16);                     // row exponents (EmuScope)
-  if (out_host) {
-    sz.add<char>((size_t)ml * ldu * osz);
-    sz.add<char>((size_t)n * ldv * osz);
-    sz.add<char>((size_t)k * osz);
-  }
-  const size_t fixed = sz.total;
-  size_t scratch = op_ws(c, probe, L);
-  scratch = std::max(scratch, lu_ws_bytes(std::max(nin, nout), L));
-  scratch = std::max(scratch, orth_ws_bytes(c, std::max(nin, nout), L));
-  scratch = std::max(scratch, (size_t)(cdiv(std::max(ml, n), 2048) + 2) * (n + 2 * k) * 8 + 65536);
-  scratch = std::max(scratch, thin_gemm_ws_bytes(std::max(nin, nout), L, K) + 65536);
-  ensure_transpose(c, Am);
-  Arena ar = c.arena(fixed + scratch + 65536);
+  const size_t need = pca_arena_bytes(c, Am, k, l, ldu, ldv);  // allocation happens before any capture
+  const uint64_t fp = ensure_transpose(c, Am);
+  Arena ar = c.arena(need);
 
+  const EmuPlan ep = emu_prepare(c, Am, L, trans ? its + 2 : its + 1, ar);
   KeyHasher kh;
-  kh << 1 << *Am << k << raw << its << l << seed << U << ldu << S << V << ldv << c.flags << c.ws << c.tcache.mem
-     << c.comm;
+  kh << 1 << *Am << k << raw << its << l << seed << U << ldu << S << V << ldv << c.flags << c.ws << c.persist << fp
+     << c.comm << ep.on();
   const bool graphable = Am->location == RPCA_DEVICE && !out_host && graphable_comm(c);
 
-  execute(c, kh.h, graphable, [&] {
+  run_checked(c, kh.h, graphable, ar, [&] {
     const MatV dA = device_view(c, Am, ar);
-    EmuScope emu(c, dA, L, trans ? its + 2 : its + 1, ar);
+    EmuScope emu(c, ep);
     double* Zb = ar.get<double>(nin * l);
     double* Yb = ar.get<double>(nout * l);
     double* R = ar.get<double>(l * l);
@@ -645,6 +816,9 @@ void pca(Ctx& c, const rpca_mat* Am, int64_t k, int raw, int its, int64_t l, uin
     // path consumes fl32(Ω) exactly as the oracle does
     omega(c, seed, 0u, nin, l, dist, odt == RPCA_F32, Zb, trans ? r0 : 0);
     const double* mu = fwd(c, F, Zb, L, Yb, mub, mub + kMaxL, ar);  // mu: Y's pending centring
+    // a non-finite entry of A makes its row of A·Ω non-finite (Ω is finite and
+    // nonzero): the check reads Y, not A
+    if (c.flags & RPCA_FLAG_CHECK_FINITE) finite_check(c, Yb, nout * l, finite_flag(c));
     if (its == 0) renorm_qr(c, Y, L, nullptr, ar, mu);
     else renorm_lu(c, Y, L, ar, mu);
     for (int it = 1; it <= its; ++it) {
@@ -685,6 +859,37 @@ void pca(Ctx& c, const rpca_mat* Am, int64_t k, int raw, int its, int64_t l, uin
   });
 }
 
+// the self-adjoint indefinite eigendecomposition (rpca_reig) runs the eigens
+// driver up to B2 = QᵀAQ, then a Jacobi eigendecomposition of it
+constexpr int kReig = 2;
+
+size_t eigens_arena_bytes(Ctx& c, const rpca_mat* Am, int64_t k, int64_t l, int64_t ldu) {
+  const bool out_host = (c.flags & RPCA_FLAG_OUTPUTS_HOST) != 0;
+  const int osz = elem_size(Am->dtype);
+  const int64_t n = Am->n, ml = Am->m_local;
+  const int P = comm_size(c);
+  const int64_t pad = c.comm ? cdiv(n, P) : n;
+  const int L = (int)l, K = (int)k;
+  const MatV probe = probe_of(Am);
+  Sizer sz;
+  sz.add<char>(host_copy_bytes(Am));
+  sz.add<double>(2 * P * pad * l + 2 * ml * l);
+  sz.add<double>(6 * l * l + 8 * l + 16);
+  sz.add<double>(ml * k + k);
+  sz.add<int>(ml + 16);  // row exponents (EmuScope)
+  if (out_host) {
+    sz.add<char>((size_t)ml * ldu * osz);
+    sz.add<char>((size_t)k * osz);
+  }
+  size_t scratch = op_ws(c, probe, L);
+  scratch = std::max(scratch, lu_ws_bytes(ml, L));
+  scratch = std::max(scratch, orth_ws_bytes(c, ml, L));
+  scratch = std::max(scratch, qr_ws_bytes(ml, L) + (size_t)4 * l * l * 8);  // Householder fallback
+  scratch = std::max(scratch, (size_t)(cdiv(n, 2048) + 2) * l * l * 8 + 65536 + (size_t)P * 3 * l * 8);
+  scratch = std::max(scratch, thin_gemm_ws_bytes(ml, L, K) + gram_ws_bytes(c, ml, L) + 65536);
+  return sz.total + scratch + 65536;
+}
+
 // ============================================================ rpca_eigens
 // Row-sharded: the shards must be the uniform partition
 // (rank r holds rows [r·⌈n/P⌉, min(n, (r+1)·⌈n/P⌉))) so that Q can be
@@ -695,7 +900,7 @@ void eigens(Ctx& c, const rpca_mat* Am, int64_t k, int its, int64_t l, uint64_t 
   validate_mat(Am);
   const bool sh = check_shard(c, Am);
   RPCA_REQUIRE(Am->m == Am->n, RPCA_E_SHAPE, "eigens needs a square A");
-  RPCA_REQUIRE(variant == RPCA_SHIFT_CHOL || variant == RPCA_SQRT, RPCA_E_ARG, "bad variant");
+  RPCA_REQUIRE(variant == RPCA_SHIFT_CHOL || variant == RPCA_SQRT || variant == kReig, RPCA_E_ARG, "bad variant");
   if (l <= 0) l = k + 2;
   const int64_t n = Am->n, ml = Am->m_local, r0 = Am->row0;
   RPCA_REQUIRE(k >= 1 && l >= k && l <= n && its >= 0 && l <= kMaxL, RPCA_E_SHAPE, "bad k/l/its");
@@ -711,27 +916,14 @@ void eigens(Ctx& c, const rpca_mat* Am, int64_t k, int its, int64_t l, uint64_t 
   const int dist = (c.flags & RPCA_FLAG_UNIFORM_OMEGA) ? RPCA_UNIFORM : RPCA_GAUSSIAN;
   const int odt = Am->dtype, osz = elem_size(odt);
 
-  const MatV probe = probe_of(Am);
-  Sizer sz;
-  sz.add<char>(host_copy_bytes(Am));
-  sz.add<double>(2 * P * pad * l + 2 * ml * l);
-  sz.add<double>(6 * l * l + 8 * l + 16);
-  sz.add<double>(ml * k + k);
-  sz.add<int>(ml + 16);  // row exponents (EmuScope)
-  if (out_host) {
-    sz.add<char>((size_t)ml * ldu * osz);
-    sz.add<char>((size_t)k * osz);
-  }
-  size_t scratch = op_ws(c, probe, L);
-  scratch = std::max(scratch, lu_ws_bytes(ml, L));
-  scratch = std::max(scratch, orth_ws_bytes(c, ml, L));
-  scratch = std::max(scratch, (size_t)(cdiv(n, 2048) + 2) * l * l * 8 + 65536 + (size_t)P * 3 * l * 8);
-  scratch = std::max(scratch, thin_gemm_ws_bytes(ml, L, K) + gram_ws_bytes(c, ml, L) + 65536);
-  Arena ar = c.arena(sz.total + scratch + 65536);
-  if (!c.status_host) RPCA_CUDA(cudaMallocHost(&c.status_host, 64));
+  const size_t need = eigens_arena_bytes(c, Am, k, l, ldu);
+  const uint64_t fp = ensure_transpose(c, Am);
+  Arena ar = c.arena(need);
 
+  const EmuPlan ep = emu_prepare(c, Am, L, its + 2, ar);
   KeyHasher kh;
-  kh << 2 << *Am << k << its << l << seed << variant << U << ldu << lam << c.flags << c.ws << c.comm;
+  kh << 2 << *Am << k << its << l << seed << variant << U << ldu << lam << c.flags << c.ws << c.persist << fp
+     << c.comm << ep.on();
   const bool graphable = Am->location == RPCA_DEVICE && !out_host && graphable_comm(c);
   // fixed buffers are carved before execute() so that graph replays (which do
   // not run the lambda) see the same pointers
@@ -759,17 +951,19 @@ void eigens(Ctx& c, const rpca_mat* Am, int64_t k, int its, int64_t l, uint64_t 
     else column_signs(c, X, ml, K, k, sign, ar);
   };
   double* Qfin = ((its & 1) ? Qb : Qa) + slot;  // this rank's final Q after the loop's swaps
-  execute(c, kh.h, graphable, [&] {
+  run_checked(c, kh.h, graphable, ar, [&] {
     const MatV dA = device_view(c, Am, ar);
-    EmuScope emu(c, dA, L, its + 2, ar);
+    EmuScope emu(c, ep);
     double* Qf = Qa;  // gathered Q
     double* Qo = Qb;  // the other gather buffer
     double* side = ar.get<double>(ml * k);
     double* sign = ar.get<double>(k);
     auto gather = [&] { allgather_bytes(c, Qf + slot, Qf, sizeof(double) * pad * l); };
+    RPCA_CUDA(cudaMemsetAsync(status, 0, sizeof(int), c.stream));
     // self-adjoint loop: Y = AΩ, then its × (Q = A·Q)
     omega(c, seed, 0u, n, l, dist, odt == RPCA_F32, Qo);  // the whole n×l Ω on every rank
     apply_ax(c, dA, nullptr, Qo, L, Qf + slot, ar);
+    if (c.flags & RPCA_FLAG_CHECK_FINITE) finite_check(c, Qf + slot, ml * l, finite_flag(c));
     const Blk Q0{Qf + slot, ml, sh, r0};
     if (its == 0) renorm_qr(c, Q0, L, nullptr, ar);
     else renorm_lu(c, Q0, L, ar);
@@ -789,6 +983,17 @@ void eigens(Ctx& c, const rpca_mat* Am, int64_t k, int its, int64_t l, uint64_t 
       // tensor-core Gram kernel
       gram(c, Qf + slot, B1, ml, L, G, ar);
       if (sh) allreduce_sum(c, G, (size_t)l * l);
+      if (variant == kReig) {
+        // reig: T = sym(QᵀAQ) = E·Λ·Eᵀ,
+        // U = Q·E[:, :k], λ signed, ordered by |λ| — Rayleigh–Ritz, no shift
+        sym_eig_abs(c, G, L, sig, W);
+        thin_gemm(c, Qf + slot, ml, L, W, K, nullptr, side, k, RPCA_F64, ar);
+        signs(side, sign);
+        scale_cast(c, side, ml, K, sign, Ud, ldu, odt);
+        copy_cast(c, sig, Ld, k, odt);
+        ar.off = mark;
+        return;
+      }
       if (variant == RPCA_SHIFT_CHOL) {
         weighted_colsum(c, B1, B1, ml * l, 1, scal, ar);  // ‖B1‖_F²
         if (sh) allreduce_sum(c, scal, 1);
@@ -836,6 +1041,15 @@ void eigens(Ctx& c, const rpca_mat* Am, int64_t k, int its, int64_t l, uint64_t 
 // ============================================================ rpca_diffsnorm
 // Row-sharded: x, z (length n) are replicated, y (length m) and U are this
 // rank's rows; z — linear in y — is all-reduced once per iteration.
+size_t diffsnorm_arena_bytes(Ctx& c, const rpca_mat* Am, int64_t k) {
+  const int64_t n = Am->n, ml = Am->m_local;
+  Sizer sz;
+  sz.add<char>(host_copy_bytes(Am));
+  sz.add<double>(2 * n + ml + n + k + 64);
+  const size_t scratch = op_ws(c, probe_of(Am), 1) + (size_t)(cdiv(std::max(ml, n), 2048) + 2) * (n + 64) * 8;
+  return sz.total + scratch + 65536;
+}
+
 void diffsnorm(Ctx& c, const rpca_mat* Am, int raw, const double* U, int64_t ldu, const double* S, const double* V,
                int64_t ldv, int64_t k, int its, uint64_t seed, double* out) {
   validate_mat(Am);
@@ -843,16 +1057,11 @@ void diffsnorm(Ctx& c, const rpca_mat* Am, int raw, const double* U, int64_t ldu
   RPCA_REQUIRE(k >= 0 && its >= 1 && out, RPCA_E_SHAPE, "bad k/its/out");
   RPCA_REQUIRE(k == 0 || (U && S && V && ldu >= k && ldv >= k), RPCA_E_ARG, "bad factors");
   const int64_t m = Am->m, n = Am->n, ml = Am->m_local;
-  const MatV probe = probe_of(Am);
-  Sizer sz;
-  sz.add<char>(host_copy_bytes(Am));
-  sz.add<double>(2 * n + ml + n + k + 64);
-  size_t scratch = op_ws(c, probe, 1) + (size_t)(cdiv(std::max(ml, n), 2048) + 2) * (n + 64) * 8;
-  ensure_transpose(c, Am);
-  Arena ar = c.arena(sz.total + scratch + 65536);
-  if (!c.status_host) RPCA_CUDA(cudaMallocHost(&c.status_host, 64));
+  const size_t need = diffsnorm_arena_bytes(c, Am, k);
+  const uint64_t fp = ensure_transpose(c, Am);
+  Arena ar = c.arena(need);
   KeyHasher kh;
-  kh << 3 << *Am << raw << U << ldu << S << V << ldv << k << its << seed << c.ws << c.tcache.mem << c.comm;
+  kh << 3 << *Am << raw << U << ldu << S << V << ldv << k << its << seed << c.ws << c.persist << fp << c.comm;
   double* x = ar.get<double>(n);
   double* z = ar.get<double>(n);
   double* y = ar.get<double>(ml);
@@ -860,7 +1069,8 @@ void diffsnorm(Ctx& c, const rpca_mat* Am, int raw, const double* U, int64_t ldu
   double* t = ar.get<double>(std::max<int64_t>(k, 1));
   double* sc = ar.get<double>(8);  // [0] nz2, [1] est, [2] scratch
   int* done = ar.get<int>(4);
-  execute(c, kh.h, Am->location == RPCA_DEVICE && graphable_comm(c), [&] {
+  kh << c.flags;
+  run_checked(c, kh.h, Am->location == RPCA_DEVICE && graphable_comm(c), ar, [&] {
     const MatV dA = device_view(c, Am, ar);
     if (!raw) {
       const size_t mark = ar.off;
@@ -886,6 +1096,7 @@ void diffsnorm(Ctx& c, const rpca_mat* Am, int raw, const double* U, int64_t ldu
         hadamard(c, t, S, (int)k);
         rank_k_sub(c, y, U, ldu, t, ml, (int)k);
       }
+      if (it == 0 && (c.flags & RPCA_FLAG_CHECK_FINITE)) finite_check(c, y, ml, finite_flag(c));
       apply_aty(c, dA, cm, y, 1, z, ar);  // z = Aᵀ y [− cᵀ (1ᵀy)]
       if (k > 0) {                        // z −= V (S ⊙ (Uᵀy))
         weighted_colsum(c, y, U, ml, (int)k, t, ar, ldu);
@@ -901,6 +1112,53 @@ void diffsnorm(Ctx& c, const rpca_mat* Am, int raw, const double* U, int64_t ldu
   RPCA_CUDA(cudaMemcpyAsync(c.status_host, sc + 1, sizeof(double), cudaMemcpyDeviceToHost, c.stream));
   sync_status(c);
   memcpy(out, c.status_host, sizeof(double));
+}
+
+// ============================================================ workspace API
+// Bytes a call needs: a device CSR's persistent CSR(Aᵀ) prefix plus the larger
+// of its construction scratch and the call's arena (include/rpca.h).
+size_t workspace_query(Ctx& c, int op, const rpca_mat* Am, int64_t k, int64_t l, int its) {
+  validate_mat(Am);
+  RPCA_REQUIRE(its >= 0, RPCA_E_SHAPE, "its < 0");
+  if (l <= 0) l = k + 2;
+  size_t arena = 0;
+  switch (op) {
+    case RPCA_OP_PCA:
+      RPCA_REQUIRE(k >= 1 && l >= k && l <= kMaxL, RPCA_E_SHAPE, "bad k / l");
+      arena = pca_arena_bytes(c, Am, k, l, k, k);
+      break;
+    case RPCA_OP_EIGENS:
+    case RPCA_OP_REIG:
+      RPCA_REQUIRE(k >= 1 && l >= k && l <= kMaxL, RPCA_E_SHAPE, "bad k / l");
+      arena = eigens_arena_bytes(c, Am, k, l, k);
+      break;
+    case RPCA_OP_DIFFSNORM:
+      RPCA_REQUIRE(k >= 0, RPCA_E_SHAPE, "bad k");
+      arena = diffsnorm_arena_bytes(c, Am, k);
+      break;
+    case RPCA_OP_APPLY:
+      RPCA_REQUIRE(l >= 1 && l <= kMaxL, RPCA_E_SHAPE, "bad l");
+      arena = std::max(op_ws(c, probe_of(Am), (int)l) + (size_t)Am->m_local * 4,
+                       (size_t)(cdiv(Am->m_local, 8192) + 2) * Am->n * 8) + 65536;
+      break;
+    default: RPCA_REQUIRE(false, RPCA_E_ARG, "bad op %d", op);
+  }
+  if (Am->kind == RPCA_CSR && Am->location == RPCA_DEVICE)
+    return csr_layout(Am).persist() + std::max(csr_build_scratch(Am), arena);
+  return arena;
+}
+
+void set_workspace(Ctx& c, void* ptr, size_t bytes) {
+  RPCA_REQUIRE(!ptr || (reinterpret_cast<uintptr_t>(ptr) & 255) == 0, RPCA_E_ARG,
+               "workspace must be 256-byte aligned");
+  RPCA_CUDA(cudaStreamSynchronize(c.stream));
+  drop_graphs(c);
+  c.tcache.valid = false;
+  c.persist = 0;
+  if (c.ws && !c.ws_user) RPCA_CUDA(cudaFree(c.ws));
+  c.ws = static_cast<char*>(ptr);
+  c.ws_cap = ptr ? bytes : 0;
+  c.ws_user = ptr != nullptr;
 }
 
 }  // namespace rpca

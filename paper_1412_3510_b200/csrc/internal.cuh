@@ -82,8 +82,17 @@ struct Ctx {
   cudaStream_t stream = nullptr;
   uint32_t flags = 0;
   int num_sms = 148;
+  // Workspace: context-owned (grown by cudaMalloc before a call when needed)
+  // or caller-owned (rpca_set_workspace: never reallocated; too small ⇒
+  // RPCA_E_WORKSPACE).  Its first `persist` bytes hold the cached CSR(Aᵀ)
+  // and heavy-row plans of the last sparse A; call arenas start after them.
   char* ws = nullptr;
   size_t ws_cap = 0;
+  bool ws_user = false;
+  size_t persist = 0;
+  // 256 bytes of device scratch allocated with the context: status words
+  // (finite check, QR breakdown) and the CSR fingerprint
+  char* dscratch = nullptr;
   int64_t launches = 0;
   Comm* comm = nullptr;
   int prof = 0;  // 0 off, 1 every launch, 2 the A-streaming pass kernels only
@@ -97,16 +106,25 @@ struct Ctx {
   std::vector<std::pair<uint64_t, CachedGraph>> graphs;
   int* status_host = nullptr;  // pinned scratch for device status words
   cudaStream_t work = nullptr;   // private stream the drivers run (and capture) on
-  // cached CSR(Aᵀ) of the last sparse A (keyed by its pointers and shape)
+  // cached CSR(Aᵀ) of the last sparse A, at the start of the workspace; keyed
+  // by the CSR pointers, shape AND a fingerprint of the arrays' contents
+  // (csr_fingerprint, one read of the CSR per call), so a different matrix
+  // at recycled addresses — or an in-place edit — rebuilds it
   struct TransposeCache {
+    bool valid = false;
     uint64_t key = 0;
-    void* mem = nullptr;
     CsrA T{};
     CsrA A{};                   // the cached matrix itself, with its heavy-row plan
-    void* plan_a = nullptr;     // plan memory of A and of T
-    void* plan_t = nullptr;
   } tcache;
+  // pointers into [ws, ws + persist) move with the workspace
+  void rebase(char* old_base, char* new_base);
+  // the workspace holds ≥ total bytes (keeping the persistent prefix)
+  void reserve(size_t total);
   cudaEvent_t fence_in = nullptr, fence_out = nullptr;
+  // second stream + events for collectives overlapped with compute (the tiled
+  // sparse Aᵀ·Y all-reduce of driver.cu)
+  cudaStream_t side = nullptr;
+  std::vector<cudaEvent_t> side_ev;
   // fp64 A·X on the int8 tensor cores (dense_ax_emu.cu): the row exponents of
   // the driver call's A, valid while that call runs (EmuScope)
   const int* emu_E = nullptr;
@@ -116,8 +134,15 @@ struct Ctx {
   // buffer, the fp32 pass sets the count) — no second read of Y for its mean
   double* ax_colpart = nullptr;
   int64_t ax_colpart_n = 0;
+  // set by the driver when a call is re-run after a Cholesky-QR breakdown:
+  // the final orthonormalisations use Householder TSQR (tsqr.cu)
+  bool force_house = false;
   Arena arena(size_t bytes);  // ensures capacity, returns an arena over the workspace
 };
+
+// device status words in the context's scratch (reset by the drivers)
+inline int* finite_flag(Ctx& c) { return reinterpret_cast<int*>(c.dscratch); }        // non-finite seen
+inline int* breakdown_flag(Ctx& c) { return reinterpret_cast<int*>(c.dscratch + 4); }  // Cholesky-QR breakdown
 
 void prof_mark(Ctx& c, const char* name);
 // run a step-API body; with profiling on, harvest its launch marks
@@ -187,6 +212,8 @@ void right_mult(Ctx& c, const double* In, const double* Q, const double* nu, con
 void rank_k_sub(Ctx& c, double* y, const double* U, int64_t ldu, const double* t, int64_t rows, int k);
 // t ← t ⊙ S
 void hadamard(Ctx& c, double* t, const double* S, int k);
+// *flag = 1 if any of x[0..count) is NaN or ±Inf (flag untouched otherwise)
+void finite_check(Ctx& c, const double* x, int64_t count, int* flag);
 
 // dense_ax.cu / dense_aty.cu
 struct DenseA {
@@ -199,7 +226,9 @@ size_t ax_ws_bytes(const DenseA& A, int l);
 void dense_ax(Ctx& c, const DenseA& A, const double* X, int l, double* Y, Arena& ar, const double* cx = nullptr);
 // dense_ax_emu.cu — fp64 A·X as int8-digit products on tcgen05 (Ozaki scheme I)
 bool emu_eligible(const DenseA& A, int l);
-void row_exponents(Ctx& c, const DenseA& A, int* E);
+// E[i] = row i's exponent; wide (may be NULL, not cleared here) set to 1 if a
+// row's largest |a| exceeds 1/8 of its Σ|a| (the emulation guard)
+void row_exponents(Ctx& c, const DenseA& A, int* E, int* wide = nullptr);
 size_t emu_ws_bytes(const DenseA& A, int l);
 void dense_ax_emu(Ctx& c, const DenseA& A, const int* E, const double* X, int l, double* Y, Arena& ar);
 size_t aty_ws_bytes(Ctx& c, const DenseA& A, int l);
@@ -210,10 +239,20 @@ void dense_aty(Ctx& c, const DenseA& A, const double* Y, int l, const double* cm
 // csr.cu — sparse A (row-major CSR, int64 row pointers, int32 sorted column indices)
 // Y (rows×l) = A·(X − 1·xmeanᵀ)   (X has as many rows as A has columns; xmean may be NULL)
 void csr_spmm(Ctx& c, const CsrA& A, const double* X, int l, double* Y, const double* xmean = nullptr);
+// the two halves of csr_spmm: rows [r0, r1) except heavy ones, and the heavy rows
+void csr_spmm_rows(Ctx& c, const CsrA& A, int64_t r0, int64_t r1, const double* X, int l, double* Y,
+                   const double* xmean = nullptr);
+void csr_spmm_heavy(Ctx& c, const CsrA& A, const double* X, int l, double* Y, const double* xmean = nullptr);
 size_t csr_transpose_ws_bytes(const CsrA& A);
-// device memory (caller frees with cudaFree) holding A's heavy-row plan; sets
-// the plan fields of A (synchronises the stream; nullptr if A has no heavy row)
-void* csr_build_heavy_plan(Ctx& c, CsrA& A);
+// upper bound of the device bytes csr_build_heavy_plan writes for A
+size_t csr_heavy_plan_bytes(const CsrA& A);
+// A's heavy-row plan built into mem (≥ csr_heavy_plan_bytes(A)); sets the plan
+// fields of A.  host_ptr: A's row pointers on the host (else read from the
+// device — synchronises the stream)
+void csr_build_heavy_plan(Ctx& c, CsrA& A, char* mem, const int64_t* host_ptr = nullptr);
+// order-independent 64-bit hash of A's row pointers, column indices and
+// values (one read of the CSR; synchronises the stream)
+uint64_t csr_fingerprint(Ctx& c, const CsrA& A);
 // T = CSR(Aᵀ) (n rows) into caller buffers T.ptr (n+1), T.idx, T.vals (nnz); stable in rows
 void csr_transpose(Ctx& c, const CsrA& A, int64_t n, CsrA& T, Arena& scratch);
 // cmean[j] = (Σ_i A_ij)/m_total from CSR(Aᵀ), rows ascending
@@ -252,6 +291,13 @@ size_t orth_ws_bytes(Ctx& c, int64_t m, int l);
 void orthonormalize(Ctx& c, double* Y, int64_t m, int l, double* R_out, Arena& ar, const double* mu = nullptr);
 void orthonormalize_sharded(Ctx& c, double* Y, int64_t m, int64_t row0, int l, double* R_out, Arena& ar,
                             const double* mu = nullptr);
+// the Householder fallback of the two above (Y − 1·muᵀ when mu ≠ NULL); the
+// sharded form factors the local block, all-gathers the l×l R's, factors the
+// stack redundantly and applies this rank's slice of its Q
+size_t orth_house_ws_bytes(int64_t m, int l, int nranks);
+void orthonormalize_house(Ctx& c, double* Y, int64_t m, int l, double* R_out, Arena& ar, const double* mu = nullptr);
+void orthonormalize_house_sharded(Ctx& c, double* Y, int64_t m, int l, double* R_out, Arena& ar,
+                                  const double* mu = nullptr);
 
 // small.cu — one-CTA l×l kernels
 // R (l×l) → Jacobi: R·W = Vr·diag(sigma); sigma sorted, Vr completed.
@@ -264,6 +310,8 @@ void nystrom_shift_chol(Ctx& c, const double* G, const double* fro2, int l, int6
 // Nyström SQRT: B2 = sym(G) = E·diag(μ)·Eᵀ (Jacobi), Minv =
 // E·diag(μ^-1/2 or 0)·Eᵀ (cut-off 1e-12·sqrt(max μ)); status 1 if min μ < -1e-6·max|μ|.
 void nystrom_sqrt(Ctx& c, const double* G, int l, double* Minv, double* nu, int* status);
+// reig: sym(G) = E·diag(λ)·Eᵀ by Jacobi; lam (l) ordered by |λ| descending, signed; E (l×l) its columns
+void sym_eig_abs(Ctx& c, const double* G, int l, double* lam, double* E);
 // lam[j] = max(σ_j² − ν, 0)   (eq. finish), cast to dtype
 void nystrom_lambda(Ctx& c, const double* sigma, const double* nu, int k, void* lam, int dtype);
 // power-method scalar step: nz = sqrt(nz2); est = done ? est : (nz == 0 ? 0 : sqrt(nz));

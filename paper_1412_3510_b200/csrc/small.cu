@@ -364,25 +364,16 @@ __global__ void __launch_bounds__(kThreads) shift_chol_kernel(const double* __re
   if (tid == 0) { *nu_out = nu_s; *status = 0; }
 }
 
-// Parallel (Brent–Luk) two-sided Jacobi on the symmetric l×l B2; then the
-// regularised inverse square root Minv = E·diag(d)·Eᵀ.
-__global__ void __launch_bounds__(kThreads) sqrt_inv_kernel(const double* __restrict__ G, int l,
-                                                            double* __restrict__ Minv, double* __restrict__ nu_out,
-                                                            int* __restrict__ status) {
-  extern __shared__ double sm[];
-  double* A = sm;          // l×l row-major
-  double* E = sm + l * l;  // eigenvectors (columns)
+// Parallel (Brent–Luk) two-sided Jacobi on a symmetric l×l matrix in shared
+// memory: on return A is diagonal (its eigenvalues) and E (initialised here)
+// holds the eigenvectors as columns.  Rotate iff |a_pq| > 2^-52·√|a_pp|·√|a_qq|,
+// ≤ 30 sweeps (the oracle's rule, reading Q18).
+__device__ void sym_jacobi(double* A, double* E, int l) {
   __shared__ double cs_[kMaxL / 2], sn_[kMaxL / 2];
   __shared__ int pp_[kMaxL / 2], qq_[kMaxL / 2];
   __shared__ int rotated;
-  __shared__ double mu[kMaxL], dd[kMaxL];
-  __shared__ int rk[kMaxL];
   const int tid = threadIdx.x;
-  for (int idx = tid; idx < l * l; idx += kThreads) {
-    const int p = idx / l, q = idx % l;
-    A[idx] = 0.5 * (G[p * l + q] + G[q * l + p]);
-    E[idx] = (p == q) ? 1.0 : 0.0;
-  }
+  for (int idx = tid; idx < l * l; idx += blockDim.x) E[idx] = (idx / l == idx % l) ? 1.0 : 0.0;
   __syncthreads();
   const int lp = (l + 1) & ~1;
   const double eps = 0x1p-52;
@@ -390,7 +381,7 @@ __global__ void __launch_bounds__(kThreads) sqrt_inv_kernel(const double* __rest
     if (tid == 0) rotated = 0;
     __syncthreads();
     for (int round = 0; round < lp - 1; ++round) {
-      for (int k = tid; k < lp / 2; k += kThreads) {
+      for (int k = tid; k < lp / 2; k += blockDim.x) {
         auto player = [&](int i) {  // 1 + (i − 1 + round) mod (lp − 1), both terms < lp − 1
           const int v = i - 1 + round;
           return i == 0 ? 0 : 1 + (v >= lp - 1 ? v - (lp - 1) : v);
@@ -412,7 +403,7 @@ __global__ void __launch_bounds__(kThreads) sqrt_inv_kernel(const double* __rest
       }
       __syncthreads();
       // columns: A ← A·J, E ← E·J
-      for (int idx = tid; idx < (lp / 2) * l; idx += kThreads) {
+      for (int idx = tid; idx < (lp / 2) * l; idx += blockDim.x) {
         const int k = idx / l, r = idx % l;
         const int p = pp_[k], q = qq_[k];
         if (q >= l || sn_[k] == 0.0) continue;
@@ -426,7 +417,7 @@ __global__ void __launch_bounds__(kThreads) sqrt_inv_kernel(const double* __rest
       }
       __syncthreads();
       // rows: A ← Jᵀ·A
-      for (int idx = tid; idx < (lp / 2) * l; idx += kThreads) {
+      for (int idx = tid; idx < (lp / 2) * l; idx += blockDim.x) {
         const int k = idx / l, r = idx % l;
         const int p = pp_[k], q = qq_[k];
         if (q >= l || sn_[k] == 0.0) continue;
@@ -436,13 +427,31 @@ __global__ void __launch_bounds__(kThreads) sqrt_inv_kernel(const double* __rest
         A[q * l + r] = s * x + c * y;
       }
       __syncthreads();
-      for (int k = tid; k < lp / 2; k += kThreads)
+      for (int k = tid; k < lp / 2; k += blockDim.x)
         if (qq_[k] < l && sn_[k] != 0.0) A[pp_[k] * l + qq_[k]] = A[qq_[k] * l + pp_[k]] = 0.0;
       __syncthreads();
     }
     if (!rotated) break;
     __syncthreads();
   }
+}
+
+// Regularised inverse square root of the symmetric B2: Minv = E·diag(d)·Eᵀ.
+__global__ void __launch_bounds__(kThreads) sqrt_inv_kernel(const double* __restrict__ G, int l,
+                                                            double* __restrict__ Minv, double* __restrict__ nu_out,
+                                                            int* __restrict__ status) {
+  extern __shared__ double sm[];
+  double* A = sm;          // l×l row-major
+  double* E = sm + l * l;  // eigenvectors (columns)
+  __shared__ double mu[kMaxL], dd[kMaxL];
+  __shared__ int rk[kMaxL];
+  const int tid = threadIdx.x;
+  for (int idx = tid; idx < l * l; idx += kThreads) {
+    const int p = idx / l, q = idx % l;
+    A[idx] = 0.5 * (G[p * l + q] + G[q * l + p]);
+  }
+  __syncthreads();
+  sym_jacobi(A, E, l);
   if (tid < l) {
     int r = 0;
     const double v = A[tid * l + tid];
@@ -474,6 +483,44 @@ __global__ void __launch_bounds__(kThreads) sqrt_inv_kernel(const double* __rest
     double s = 0.0;
     for (int t = 0; t < l; ++t) s += E[p * l + t] * dd[rk[t]] * E[q * l + t];
     Minv[idx] = s;
+  }
+}
+
+// reig: T = sym(G) = E·diag(λ)·Eᵀ; the
+// eigenvalues ordered by |λ| descending (ties: the larger λ, then the lower
+// index — the oracle's order), lam[j] = λ of rank j (signed), Eo[:, j] its
+// eigenvector.
+__global__ void __launch_bounds__(kThreads) sym_eig_abs_kernel(const double* __restrict__ G, int l,
+                                                               double* __restrict__ lam, double* __restrict__ Eo) {
+  extern __shared__ double sm[];
+  double* A = sm;
+  double* E = sm + l * l;
+  __shared__ int col_of[kMaxL];
+  const int tid = threadIdx.x;
+  for (int idx = tid; idx < l * l; idx += kThreads) {
+    const int p = idx / l, q = idx % l;
+    A[idx] = 0.5 * (G[p * l + q] + G[q * l + p]);
+  }
+  __syncthreads();
+  sym_jacobi(A, E, l);
+  // rank among the eigenvalues in the oracle's order: oracle_jacobi_eig sorts
+  // λ non-increasing (stable in index), then reig stable-sorts by |λ| with the
+  // larger λ first on |λ| ties — both tie-breaks reduce to the lower index
+  if (tid < l) {
+    const double v = A[tid * l + tid];
+    int r = 0;
+    for (int i = 0; i < l; ++i) {
+      const double w = A[i * l + i];
+      const bool before = fabs(w) > fabs(v) || (fabs(w) == fabs(v) && (w > v || (w == v && i < tid)));
+      r += before;
+    }
+    col_of[r] = tid;
+  }
+  __syncthreads();
+  for (int j = tid; j < l; j += kThreads) lam[j] = A[col_of[j] * l + col_of[j]];
+  for (int idx = tid; idx < l * l; idx += kThreads) {
+    const int p = idx / l, j = idx % l;
+    Eo[idx] = E[p * l + col_of[j]];
   }
 }
 
@@ -538,6 +585,14 @@ void nystrom_sqrt(Ctx& c, const double* G, int l, double* Minv, double* nu, int*
   sqrt_inv_kernel<<<1, kThreads, 2 * l * l * 8, c.stream>>>(G, l, Minv, nu, status);
   RPCA_CHECK_LAUNCH();
   count_launch(c);
+}
+
+void sym_eig_abs(Ctx& c, const double* G, int l, double* lam, double* E) {
+  const int smem = 2 * l * l * 8;
+  ensure_smem((const void*)sym_eig_abs_kernel, 2 * kMaxL * kMaxL * 8);
+  sym_eig_abs_kernel<<<1, kThreads, smem, c.stream>>>(G, l, lam, E);
+  RPCA_CHECK_LAUNCH();
+  count_launch(c, 1, "jacobi");
 }
 
 void nystrom_lambda(Ctx& c, const double* sigma, const double* nu, int k, void* lam, int dtype) {

@@ -292,6 +292,13 @@ __global__ void hadamard_kernel(double* __restrict__ t, const double* __restrict
   if (j < k) t[j] *= S[j];
 }
 
+__global__ void finite_check_kernel(const double* __restrict__ x, int64_t count, int* __restrict__ flag) {
+  bool bad = false;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count; i += (int64_t)gridDim.x * blockDim.x)
+    bad |= !isfinite(x[i]);
+  if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) *flag = 1;
+}
+
 unsigned grid_for(Ctx& c, int64_t work, int per = 256) {
   int64_t b = cdiv(work, per);
   const int64_t cap = (int64_t)c.num_sms * 16;
@@ -441,6 +448,13 @@ void rank_k_sub(Ctx& c, double* y, const double* U, int64_t ldu, const double* t
   rank_k_sub_kernel<<<grid_for(c, rows), 256, 0, c.stream>>>(y, U, ldu, t, rows, k);
   RPCA_CHECK_LAUNCH();
   count_launch(c);
+}
+
+void finite_check(Ctx& c, const double* x, int64_t count, int* flag) {
+  if (count == 0) return;
+  finite_check_kernel<<<grid_for(c, count, 1024), 256, 0, c.stream>>>(x, count, flag);
+  RPCA_CHECK_LAUNCH();
+  count_launch(c, 1, "finite_check");
 }
 
 void hadamard(Ctx& c, double* t, const double* S, int k) {

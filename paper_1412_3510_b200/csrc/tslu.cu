@@ -392,6 +392,215 @@ __global__ void __launch_bounds__(kThreads, SelCfg<LP, RR>::kMinBlocks)
   }  // leaves
 }
 
+// ---------------------------------------------------------------------------
+// Nomination levels in fp32 (every tournament level but the last).  A level
+// only NOMINATES l candidate rows of its block — the last level re-reads the
+// candidates' original fp64 rows and runs the exact fp64 GEPP that fixes the
+// pivots, U and M, so L = Y·U⁻¹ stays an exact factorisation whatever was
+// nominated (reading Q3).  fp32 halves the registers a row
+// takes (two CTAs per SM instead of one) and the FFMA / MUFU latencies of the
+// step chain.  Each column is scaled by an exact power of two so that its
+// largest |value| in the block is in [1, 2) — column scaling leaves GEPP's
+// pivot choices unchanged, and the fp32 range then covers every column
+// whatever the fp64 magnitudes.  A column whose remaining values are all
+// below 2^-100 of its block maximum counts as zero (no elimination).
+
+__device__ __forceinline__ uint32_t piv_key32(float v) { return (__float_as_uint(v) & 0x7FFFFFFFu) >> 3; }
+
+template <int LP, int W>
+__device__ __forceinline__ void trail_update32(float (&w)[LP], const float (*u12)[LP], int ns) {
+  float mm[8];
+#pragma unroll
+  for (int s = 0; s < 8; ++s) mm[s] = s < ns ? w[s] : 0.f;
+#pragma unroll
+  for (int t = 8; t < W; ++t) {
+    float v = w[t];
+#pragma unroll
+    for (int s = 0; s < 8; ++s) v = fmaf(-mm[s], u12[s][t - 8], v);
+    w[t] = v;
+  }
+#pragma unroll
+  for (int t = 0; t + 8 < LP; ++t) w[t] = w[t + 8];
+#pragma unroll
+  for (int t = LP - 8; t < LP; ++t) w[t] = 0.f;
+}
+
+template <int LP, int R>
+__global__ void __launch_bounds__(kThreads, 2)
+    lu_nominate_kernel(const double* __restrict__ Y, int64_t m, int l, int leaf, const int64_t* __restrict__ cand_in,
+                       int64_t n_in, int G, int64_t* __restrict__ cand_out, const double* __restrict__ mu) {
+  constexpr int CAP = kThreads * R;
+  __shared__ int64_t ids[CAP];
+  __shared__ int setcnt[CAP + 1];
+  __shared__ uint2 slot[2][kWarps];
+  __shared__ float suinv[2][kWarps];
+  __shared__ __align__(16) float pbuf[2][kWarps][8];
+  __shared__ float traw[8][LP];
+  __shared__ float l11[8][8];
+  __shared__ float u12[8][LP];
+  __shared__ int piv[LP];
+  __shared__ int colexp[LP];
+  __shared__ int nrows_s;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t blk = blockIdx.x;
+  for (int t = tid; t < LP; t += kThreads) colexp[t] = 0;
+  if (leaf == 1) {
+    const int64_t r0 = blk * CAP;
+    if (tid == 0) nrows_s = (int)imin64(CAP, m - r0);
+    for (int r = tid; r < CAP; r += kThreads) ids[r] = r0 + r;
+  } else {
+    // valid candidates of this group in ascending id order within each set
+    // (sets cover ascending row ranges, so ascending overall)
+    const int64_t s0 = blk * G * l, s1 = imin64(n_in * l, s0 + (int64_t)G * l);
+    const int nslots = (int)(s1 - s0), nsets = (nslots + l - 1) / l;
+    for (int st = tid; st < nsets; st += kThreads) {
+      int cnt = 0;
+      for (int t = st * l; t < min(nslots, st * l + l); ++t) cnt += cand_in[s0 + t] >= 0;
+      setcnt[st + 1] = cnt;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      setcnt[0] = 0;
+      for (int st = 0; st < nsets; ++st) setcnt[st + 1] += setcnt[st];
+      nrows_s = setcnt[nsets];
+    }
+    __syncthreads();
+    for (int s = tid; s < nslots; s += kThreads) {
+      const int64_t id = cand_in[s0 + s];
+      if (id < 0) continue;
+      const int st = s / l;
+      int rank = 0;
+      for (int t = st * l; t < min(nslots, st * l + l); ++t) {
+        const int64_t o = cand_in[s0 + t];
+        rank += (o >= 0 && o < id);
+      }
+      ids[setcnt[st] + rank] = id;
+    }
+  }
+  __syncthreads();
+  const int rows = nrows_s;
+  const int steps = min(rows, l);
+  bool act[R];
+  int pstep[R];
+  const double* src[R];
+#pragma unroll
+  for (int q = 0; q < R; ++q) {
+    const int r = tid * R + q;
+    act[q] = r < rows;
+    pstep[q] = -1;
+    src[q] = act[q] ? Y + ids[r] * l : Y;
+  }
+  // pass 1: per-column exponent maxima of the block (pending centring on load)
+#pragma unroll 4
+  for (int t = 0; t < LP; ++t) {
+    if (t >= l) break;
+    const double mt = mu ? mu[t] : 0.0;
+    unsigned f = 0;
+#pragma unroll
+    for (int q = 0; q < R; ++q)
+      if (act[q]) f = max(f, (unsigned)(__double_as_longlong(src[q][t] - mt) >> 52) & 0x7FFu);
+    f = __reduce_max_sync(0xffffffffu, f);
+    if (lane == 0 && f) atomicMax(&colexp[t], (int)f);
+  }
+  __syncthreads();
+  // pass 2 (L1-resident): scaled fp32 rows in registers
+  float w[R][LP];
+#pragma unroll
+  for (int t = 0; t < LP; ++t) {
+    const int f = t < l ? colexp[t] : 0;
+    // 2^(1023 − f) (field f ≥ 1): the column maximum lands in [1, 2) ([2, 4)
+    // for the top binade, whose 2^-1023 would be subnormal)
+    const double sc = f ? __longlong_as_double((long long)(2046 - min(f, 2045)) << 52) : 0.0;
+    const double mt = (mu && t < l) ? mu[t] : 0.0;
+#pragma unroll
+    for (int q = 0; q < R; ++q) w[q][t] = (act[q] && t < l && f) ? (float)((src[q][t] - mt) * sc) : 0.f;
+  }
+  // blocked GEPP in 8-column panels — the fp64 kernel's scheme (lu_select_kernel)
+  for (int pb = 0; pb < steps; pb += 8) {
+    const int ns = min(8, steps - pb);
+#pragma unroll
+    for (int s = 0; s < 8; ++s) {
+      if (s >= ns) break;
+      const int j = pb + s;
+      uint32_t best = 0;
+      int bq = 0;
+#pragma unroll
+      for (int q = 0; q < R; ++q)
+        if (act[q]) {
+          const uint32_t k = piv_key32(w[q][s]) + 1u;
+          if (k > best) { best = k; bq = q; }
+        }
+      const uint32_t mk = __reduce_max_sync(0xffffffffu, best);
+      const int wl = __ffs(__ballot_sync(0xffffffffu, best == mk)) - 1;
+      if (lane == wl) {
+#pragma unroll
+        for (int q = 0; q < R; ++q)
+          if (q == bq) {
+            slot[j & 1][warp] = make_uint2(mk, (uint32_t)(tid * R + q));
+            const float pv = w[q][s];
+            suinv[j & 1][warp] = fabsf(pv) >= 0x1p-100f ? __frcp_rn(pv) : 0.f;  // tiny: a zero column
+#pragma unroll
+            for (int t = s; t < 8; ++t) pbuf[j & 1][warp][t] = w[q][t];
+          }
+      }
+      __syncthreads();
+      const uint32_t kv = lane < kWarps ? slot[j & 1][lane].x : 0u;
+      const uint32_t gk = __reduce_max_sync(0xffffffffu, kv);
+      const int ww = __ffs(__ballot_sync(0xffffffffu, kv == gk)) - 1;
+      const int p = (int)slot[j & 1][ww].y;
+      const float uinv = suinv[j & 1][ww];
+      const float* prow = pbuf[j & 1][ww];
+      if (tid == 0) piv[j] = p;
+#pragma unroll
+      for (int q = 0; q < R; ++q) {
+        if (!act[q]) continue;
+        if (tid * R + q == p) {
+          act[q] = false;
+          pstep[q] = s;
+          continue;
+        }
+        const float mult = w[q][s] * uinv;
+        w[q][s] = mult;
+#pragma unroll
+        for (int t = s + 1; t < 8; ++t) w[q][t] = fmaf(-mult, prow[t], w[q][t]);
+      }
+    }
+    if (pb + 8 >= LP) break;
+#pragma unroll
+    for (int q = 0; q < R; ++q)
+      if (pstep[q] >= 0) {
+        const int sp = pstep[q];
+#pragma unroll
+        for (int t = 8; t < LP; ++t) traw[sp][t - 8] = w[q][t];
+#pragma unroll
+        for (int t = 0; t < 8; ++t) l11[sp][t] = t < sp ? w[q][t] : 0.f;
+        pstep[q] = -2;
+      }
+    __syncthreads();
+    if (tid < LP - 8) {
+      float u[8];
+#pragma unroll
+      for (int sp = 0; sp < 8; ++sp) {
+        float v = sp < ns ? traw[sp][tid] : 0.f;
+#pragma unroll
+        for (int s2 = 0; s2 < sp; ++s2) v = fmaf(-l11[sp][s2], u[s2], v);
+        u[sp] = v;
+        u12[sp][tid] = v;
+      }
+    }
+    __syncthreads();
+    const int live = LP - pb;
+#pragma unroll
+    for (int q = 0; q < R; ++q) {
+      if (!act[q]) continue;
+      if (live > LP / 2) trail_update32<LP, LP>(w[q], u12, ns);
+      else trail_update32<LP, LP / 2>(w[q], u12, ns);
+    }
+  }
+  __syncthreads();
+  for (int j = tid; j < l; j += kThreads) cand_out[blk * l + j] = j < steps ? ids[piv[j]] : -1;
+}
+
 // Y[piv[j] − row0] ← Lp[j] for the pivot rows this shard holds (their exact
 // unit-lower rows)
 __global__ void pivot_rows_kernel(double* __restrict__ Y, int64_t m, int64_t row0, int l,
@@ -484,27 +693,72 @@ void select(Ctx& c, unsigned grid, const double* Y, int64_t m, int l, int leaf, 
   count_launch(c, 1, leaf == 1 ? "lu_leaf" : "lu_tree");
 }
 
+constexpr int nominate_rows_per_thread(int LP) { return LP <= 16 ? 4 : (LP <= 32 ? 2 : 1); }
+int nominate_cap(int l) { return kThreads * nominate_rows_per_thread(lp_of(l)); }
+
+template <int LP>
+void nominate_lp(Ctx& c, unsigned grid, const double* Y, int64_t m, int l, int leaf, const int64_t* cin,
+                 int64_t n_in, int G, int64_t* cout, const double* mu) {
+  lu_nominate_kernel<LP, nominate_rows_per_thread(LP)><<<grid, kThreads, 0, c.stream>>>(Y, m, l, leaf, cin, n_in, G,
+                                                                                          cout, mu);
+}
+
+void nominate(Ctx& c, unsigned grid, const double* Y, int64_t m, int l, int leaf, const int64_t* cin, int64_t n_in,
+              int G, int64_t* cout, const double* mu) {
+  switch (lp_of(l)) {
+    case 8: nominate_lp<8>(c, grid, Y, m, l, leaf, cin, n_in, G, cout, mu); break;
+    case 16: nominate_lp<16>(c, grid, Y, m, l, leaf, cin, n_in, G, cout, mu); break;
+    case 24: nominate_lp<24>(c, grid, Y, m, l, leaf, cin, n_in, G, cout, mu); break;
+    case 32: nominate_lp<32>(c, grid, Y, m, l, leaf, cin, n_in, G, cout, mu); break;
+    case 40: nominate_lp<40>(c, grid, Y, m, l, leaf, cin, n_in, G, cout, mu); break;
+    case 48: nominate_lp<48>(c, grid, Y, m, l, leaf, cin, n_in, G, cout, mu); break;
+    case 56: nominate_lp<56>(c, grid, Y, m, l, leaf, cin, n_in, G, cout, mu); break;
+    case 64: nominate_lp<64>(c, grid, Y, m, l, leaf, cin, n_in, G, cout, mu); break;
+    default: RPCA_REQUIRE(false, RPCA_E_SHAPE, "lu: l=%d > %d", l, kMaxL);
+  }
+  RPCA_CHECK_LAUNCH();
+  count_launch(c, 1, leaf == 1 ? "lu_leaf" : "lu_tree");
+}
+
+bool lu_f64_nomination() {
+  static const bool v = getenv("RPCA_LU_F64_LEAF") != nullptr;  // ablation: the round-1 fp64 nomination
+  return v;
+}
+
 // Tournament over rows [0, m) of Y down to one candidate set; returns the set
 // (l entries, local row indices, −1 padded).  If `finalize`, the last level
-// also writes U, Lp, piv and M.
+// (fp64 GEPP on the candidates' original rows) also writes U, Lp, piv and M;
+// every other level nominates in fp32 (lu_nominate_kernel).
 int64_t* tournament(Ctx& c, const double* Y, int64_t m, int l, bool finalize, double* U, double* Lp, int64_t* piv,
                     double* M, Arena& ar, const double* mu) {
-  const int G = group_for(l);
-  const int64_t nblk = std::max<int64_t>(1, cdiv(m, leaf_cap(l)));
+  const bool f64 = lu_f64_nomination();
+  const int G64 = group_for(l);
+  const int Gn = f64 ? G64 : std::max(2, nominate_cap(l) / l);
+  const int64_t leafcap = f64 ? leaf_cap(l) : nominate_cap(l);
+  const int64_t nblk = std::max<int64_t>(1, cdiv(m, leafcap));
   int64_t* ca = ar.get<int64_t>(nblk * l);
   int64_t* cb = ar.get<int64_t>(nblk * l);
   if (m == 0) {
     RPCA_CUDA(cudaMemsetAsync(ca, 0xFF, sizeof(int64_t) * l, c.stream));  // no local rows: all −1
     return ca;
   }
-  select(c, (unsigned)nblk, Y, m, l, 1, nullptr, 0, G, ca, finalize && nblk == 1, U, Lp, piv, M, nullptr, nullptr,
-         mu);
+  if (finalize && m <= leaf_cap(l)) {  // one block: the exact GEPP directly
+    select(c, 1u, Y, m, l, 1, nullptr, 0, G64, ca, 1, U, Lp, piv, M, nullptr, nullptr, mu);
+    return ca;
+  }
+  if (f64) select(c, (unsigned)nblk, Y, m, l, 1, nullptr, 0, G64, ca, 0, U, Lp, piv, M, nullptr, nullptr, mu);
+  else nominate(c, (unsigned)nblk, Y, m, l, 1, nullptr, 0, Gn, ca, mu);
   int64_t n = nblk;
-  while (n > 1) {
+  for (;;) {
+    const bool last = finalize && n <= G64;
+    if (!last && n <= 1) break;
+    const int G = last ? G64 : Gn;
     const int64_t ng = cdiv(n, G);
-    select(c, (unsigned)ng, Y, m, l, 0, ca, n, G, cb, finalize && ng == 1, U, Lp, piv, M, nullptr, nullptr, mu);
+    if (last || f64) select(c, (unsigned)ng, Y, m, l, 0, ca, n, G, cb, last ? 1 : 0, U, Lp, piv, M, nullptr, nullptr, mu);
+    else nominate(c, (unsigned)ng, Y, m, l, 0, ca, n, G, cb, mu);
     std::swap(ca, cb);
     n = ng;
+    if (last) break;
   }
   return ca;
 }

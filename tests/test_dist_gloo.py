@@ -53,12 +53,14 @@ def test_plan_shard_partitions_rows(name, ws):
     assert cover[0][0] == 0 and cover[-1][1] == m_total
     assert all(a[1] == b[0] for a, b in zip(cover, cover[1:]))  # disjoint, contiguous
     assert all(p["m_local"] >= 1 for p in plans)
-    if cfg.op == "eigens":  # strong scaling on the uniform partition the library requires
-        assert m_total == cfg.m
-        assert all((p["row0"], p["m_local"]) == rp.uniform_shard(cfg.m, ws, r) for r, p in enumerate(plans))
-    else:  # weak scaling: one full per-GPU instance per rank, distinct seeds
-        assert m_total == ws * cfg.m and all(p["m_local"] == cfg.m for p in plans)
-        assert len({p["seed_offset"] for p in plans}) == ws
+    # strong scaling: one global matrix on the uniform
+    # partition (the one rpca_eigens requires) — C4 at 8: 250,000 rows per GPU
+    assert m_total == cfg.m and all(p["scaling"] == "strong" for p in plans)
+    assert all((p["row0"], p["m_local"]) == rp.uniform_shard(cfg.m, ws, r) for r, p in enumerate(plans))
+    if name == "C4" and ws == 8:
+        assert all(p["m_local"] == 250000 for p in plans)
+    if name == "C5" and ws == 8:
+        assert all(p["m_local"] == 1250000 for p in plans)
 
 
 def _max_rank(rank, ws):

@@ -1,15 +1,17 @@
 """Parity at BASELINE.json's full sizes, in the launch configuration bench.py
-times.
+times, against the oracle on the same
+bytes with BASELINE north_star's tolerances: leading-k σ relative 1e-10 (fp64)
+/ 1e-4 (fp32), largest principal angle (sine form, per σ cluster) < 1e-8 /
+1e-3, and diffsnorm within 1% of the oracle's.
 
-* C3 (Nyström, fp64 32768²): the whole `eigens` against the oracle on the same
-  bytes (λ rel 1e-10, principal angles < 1e-8 per cluster).
-* C4 (centred fp32 2e6×4096) and C5 (CSR 1e7×1e6): the oracle cannot run the
-  whole pipeline in test time, so (a) the pass kernels are checked on sampled
-  output rows that are recomputed exactly (fp64, one row at a time), and (b)
-  the returned factors are checked against properties that hold at any size:
-  orthonormal U and V, the SVD identity A_cᵀU = V·diag(S) (B = Qᵀ A_c = W S Vᵀ
-  ⇒ A_cᵀ U = V S exactly), and Rayleigh–Ritz interlacing S_j ≤ σ_j(A_c) with
-  the exact σ from the fp64 Gram (C4).
+* C2 (fp64 100000×4000) is in test_gpu_parity.py (plus its diffsnorm here).
+* C3 (Nyström, fp64 32768²): `eigens` and its diffsnorm (V = U, S = λ).
+* C4 (centred fp32 2e6×4096): the whole `pca` and diffsnorm against the oracle
+  (≈ 4 min of oracle time on 16 cores), plus the pass kernels on sampled rows
+  and the properties that hold at any size (orthonormality, A_cᵀU = V·S,
+  Rayleigh–Ritz interlacing against the exact σ of the fp64 Gram).
+* C5 (CSR 1e7×1e6): the whole `pca` and diffsnorm against the oracle, plus the
+  SpMM passes on sampled rows and against cuSPARSE.
 """
 import numpy as np
 import pytest
@@ -27,14 +29,73 @@ def dev():
     return torch.device("cuda", 0)
 
 
+def diffsnorm_pair(A, A_host, res_g, res_o, raw, same_factors=True):
+    """GPU diffsnorm of the GPU factors vs the oracle's of its own factors (≤ 1%,
+    BASELINE), and both estimators on the SAME factors (same algorithm, same
+    start vector: agreement to rounding)."""
+    est = rp.diffsnorm(A, *res_g, raw=raw, its=20, seed=1)
+    ref = oracle.diffsnorm(A_host, *res_o, raw=raw, its=20, seed=1)
+    assert abs(est - ref) <= 0.01 * ref, (est, ref)
+    if same_factors:  # fp64 A: the two estimators differ by rounding only
+        same = oracle.diffsnorm(A_host, *[t.cpu().numpy() for t in res_g], raw=raw, its=20, seed=1)
+        assert abs(est - same) <= 1e-9 * same, (est, same)
+    return est, ref
+
+
 def test_c3_full_vs_oracle():
     cfg = synth.CONFIGS["C3"]
     A = synth.make_c3(device=dev())
     U, lam = rp.eigens(A, cfg.k, its=cfg.its, l=cfg.l, seed=0)
-    Uo, lo = oracle.eigens(A.cpu().numpy(), cfg.k, its=cfg.its, l=cfg.l, seed=0)
+    Ah = A.cpu().numpy()
+    Uo, lo = oracle.eigens(Ah, cfg.k, its=cfg.its, l=cfg.l, seed=0)
     lg = lam.cpu().numpy()
     assert np.max(np.abs(lg - lo) / lo) < 1e-10
     assert cluster_sin_angle(Uo, U.cpu().numpy(), lo, cfg.k) < 1e-8
+    # Nyström factors: V = U, S = λ (include/rpca.h)
+    est = rp.diffsnorm(A, U, lam, U, its=20, seed=1)
+    ref = oracle.diffsnorm(Ah, Uo, lo, Uo, its=20, seed=1)
+    assert abs(est - ref) <= 0.01 * ref, (est, ref)
+    assert est >= 1.0 / (cfg.k + 1) ** 2 * (1 - 1e-6)  # ≥ λ_{k+1} (Eckart–Young, exact spectrum j^-2)
+
+
+def test_c2_full_diffsnorm():
+    cfg = synth.CONFIGS["C2"]
+    A = synth.make_c2(device=dev())
+    res = rp.pca(A, cfg.k, raw=True, its=cfg.its, l=cfg.l, seed=0)
+    Ah = A.cpu().numpy()
+    o = oracle.pca(Ah, cfg.k, its=cfg.its, l=cfg.l, seed=0)
+    diffsnorm_pair(A, Ah, res, o, True)
+
+
+def test_c4_full_vs_oracle():
+    """C4 at full size: 2e6×4096 fp32, centred, k=50, l=52, its=4 — the whole
+    pipeline against the oracle (fp32 tolerances of BASELINE)."""
+    cfg = synth.CONFIGS["C4"]
+    A = synth.make_c4(device=dev())
+    res = rp.pca(A, cfg.k, raw=False, its=cfg.its, l=cfg.l, seed=0)
+    Ah = A.cpu().numpy()
+    o = oracle.pca(Ah, cfg.k, raw=False, its=cfg.its, l=cfg.l, seed=0)
+    Sg = res[1].cpu().numpy().astype(np.float64)
+    assert np.max(np.abs(Sg - o[1]) / o[1]) < 1e-4
+    assert cluster_sin_angle(o[0], res[0].cpu().numpy().astype(np.float64), o[1], cfg.k) < 1e-3
+    assert cluster_sin_angle(o[2], res[2].cpu().numpy().astype(np.float64), o[1], cfg.k) < 1e-3
+    diffsnorm_pair(A, Ah, res, o, False, same_factors=False)  # (≈ 90 s of oracle time per estimate)
+
+
+def test_c5_full_vs_oracle():
+    """C5 at full size: CSR 1e7×1e6 (≈1.2e8 nonzeros), k=30, l=32, its=2 — the whole
+    pipeline against the oracle (fp64 tolerances)."""
+    cfg = synth.CONFIGS["C5"]
+    rowptr, colind, vals = synth.make_c5(device=dev())
+    A = rp.CSR(rowptr, colind, vals, (cfg.m, cfg.n))
+    res = rp.pca(A, cfg.k, raw=True, its=cfg.its, l=cfg.l, seed=0)
+    host = (rowptr.cpu().numpy(), colind.cpu().numpy(), vals.cpu().numpy(), (cfg.m, cfg.n))
+    o = oracle.pca(host, cfg.k, raw=True, its=cfg.its, l=cfg.l, seed=0)
+    Sg = res[1].cpu().numpy()
+    assert np.max(np.abs(Sg - o[1]) / o[1]) < 1e-10
+    assert cluster_sin_angle(o[0], res[0].cpu().numpy(), o[1], cfg.k) < 1e-8
+    assert cluster_sin_angle(o[2], res[2].cpu().numpy(), o[1], cfg.k) < 1e-8
+    diffsnorm_pair(A, host, res, o, True)
 
 
 def _chunks(m, size=1 << 17):

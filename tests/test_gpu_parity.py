@@ -489,3 +489,35 @@ def test_csr_heavy_rows(l):
     got = rp.apply(A, Y, adjoint=True).cpu().numpy()
     assert np.all(np.abs(got - oracle.apply(host, Yn, adjoint=True)) <=
                   2 * gamma(12000) * (np.abs(D).T @ np.abs(Yn)) + 1e-300)
+
+
+# ----------------------------------------------------------------- reig (§8(f) N1)
+@pytest.mark.parametrize("n,k,l,its", [(2048, 20, 22, 2), (3001, 8, 12, 1), (1500, 30, 42, 3)])
+def test_reig_indefinite_vs_oracle(n, k, l, its):
+    """Symmetric indefinite A = V·diag(λ)·Vᵀ, λ_j = ±j^-1.5 alternating: reig
+    against the oracle on the same bits (λ rel 1e-10, angles 1e-8), and
+    against the known spectrum (the leading |λ| converge)."""
+    lam_t = (-1.0) ** torch.arange(n, dtype=torch.float64) * torch.arange(1, n + 1, dtype=torch.float64) ** -1.5
+    V = synth.haar_columns(n, n, n + k, device=dev())
+    A = (V * lam_t.to(dev())) @ V.T
+    A = 0.5 * (A + A.T)
+    U, lam = rp.reig(A, k, its=its, l=l, seed=0)
+    Uo, lo = oracle.reig(A.cpu().numpy(), k, its=its, l=l, seed=0)
+    lg = lam.cpu().numpy()
+    assert np.all(np.sign(lg) == np.sign(lo))
+    assert np.max(np.abs(lg - lo) / np.abs(lo)) < 1e-10
+    assert cluster_sin_angle(Uo, U.cpu().numpy(), np.abs(lo), k) < 1e-8
+    assert abs(lg[0] - 1.0) < 1e-6 and abs(lg[1] + 2.0**-1.5) < 1e-6
+    # the error estimate of the rank-k eigen-approximation: ≥ |λ_{k+1}| (Eckart–Young)
+    est = rp.diffsnorm(A, U, lam, U, its=20, seed=1)
+    ref = oracle.diffsnorm(A.cpu().numpy(), Uo, lo, Uo, its=20, seed=1)
+    assert abs(est - ref) <= 1e-2 * ref and est >= (k + 1) ** -1.5 * (1 - 1e-6)
+
+
+def test_reig_spec_examples_gpu():
+    """SPEC.md:233-235 on the GPU: diag(3, −2, 1, 0, …) → (3, −2); identity → 1."""
+    A = torch.diag(torch.tensor([3.0, -2.0, 1.0] + [0.0] * 61, dtype=torch.float64)).to(dev())
+    U, lam = rp.reig(A, 2, its=2, l=4, seed=0)
+    assert np.allclose(lam.cpu().numpy(), [3.0, -2.0], atol=1e-12, rtol=0)
+    U, lam = rp.reig(torch.eye(40, dtype=torch.float64, device=dev()), 1, its=1, l=3)
+    assert abs(float(lam[0]) - 1.0) < 1e-13

@@ -159,6 +159,58 @@ def test_sharded_csr_pca_and_diffsnorm():
     assert all(abs(x[3] - ref) <= 1e-9 * ref for x in res)
 
 
+@pytest.mark.parametrize("comm", ["virtual", "nccl"])
+def test_sharded_csr_overlapped_allreduce(comm):
+    """n·l·8 ≥ 32 MB: the sharded sparse Aᵀ·Y all-reduces CSR(Aᵀ)'s output in 8
+    row tiles on a second stream, each overlapping the next tile's SpMM
+    (driver.cu csr_aty_allreduce_overlapped) — on virtual ranks (host-barrier
+    collectives) and through a 1-rank NCCL communicator inside the captured
+    graph (replayed on the second call)."""
+    m, n, k, l = 300000, 140000, 30, 32
+    rp_, ci, va = synth.make_c5(m=m, n=n, seed=11, device=dev(), planted_rows=m // 100, planted_cols=200)
+    host = (rp_.cpu().numpy(), ci.cpu().numpy(), va.cpu().numpy(), (m, n))
+    o = oracle.pca(host, k, raw=False, its=2, l=l, seed=0)
+    if comm == "virtual":
+        P = 2
+        sp = splits_of(m, P)
+
+        def fn(r):
+            r0, ml = sp[r]
+            a, b = int(rp_[r0]), int(rp_[r0 + ml])
+            Ar = rp.CSR(rp_[r0:r0 + ml + 1] - a, ci[a:b], va[a:b], (ml, n))
+            U, S, V = rp.pca(Ar, k, raw=False, its=2, l=l, seed=0, m_total=m, row0=r0)
+            return U.cpu().numpy(), S.cpu().numpy(), V.cpu().numpy()
+
+        res = run_ranks(P, fn)
+        U = np.concatenate([x[0] for x in res])
+        compare(U, res[0][1], res[0][2], o, k)
+        return
+    out = {}
+
+    def body():
+        try:
+            torch.cuda.set_device(0)
+            rp.comm_init(1, 0, rp.comm_unique_id())
+            A = rp.CSR(rp_, ci, va, (m, n))
+            r1 = rp.pca(A, k, raw=False, its=2, l=l, seed=0, m_total=m, row0=0)
+            r2 = rp.pca(A, k, raw=False, its=2, l=l, seed=0, m_total=m, row0=0)
+            torch.cuda.synchronize()
+            out.update(r1=r1, r2=r2)
+        except BaseException as e:  # noqa: BLE001 - re-raised below
+            out["err"] = e
+        finally:
+            rp.release_context()
+
+    th = threading.Thread(target=body, daemon=True)
+    th.start()
+    th.join(300)
+    assert not th.is_alive()
+    if out.get("err") is not None:
+        raise out["err"]
+    compare(*[t.cpu().numpy() for t in out["r1"]], o, k)
+    assert all(torch.equal(a, b) for a, b in zip(out["r1"], out["r2"]))
+
+
 @pytest.mark.parametrize("raw", [True, False])
 def test_sharded_diffsnorm(raw):
     A = synth.make_c1(device=dev()) + (0.0 if raw else 2.0)
@@ -242,7 +294,7 @@ def test_shard_errors():
     assert run_ranks(2, bad_eigens) == [rp.E_SHAPE, rp.E_SHAPE]
 
 
-@pytest.mark.parametrize("graph", ["0", "1"])
+@pytest.mark.parametrize("graph", ["0", "1"])  # captured by default; "0" opts out
 def test_nccl_single_rank_runs_sharded_schedule(graph, monkeypatch):
     """A 1-rank NCCL communicator drives the whole sharded schedule through real
     ncclAllReduce / ncclAllGather calls (with RPCA_NCCL_GRAPH=1 also inside the

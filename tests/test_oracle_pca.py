@@ -326,3 +326,62 @@ def test_diffsnorm_centered_and_pca_residual():
     est = oracle.diffsnorm(A, U, S, V, raw=False, its=60, seed=1)
     assert exact / 2 <= est <= exact * (1 + 1e-10)
     assert abs(est - exact) < 0.02 * exact
+
+
+# ----------------------------------------------------------------- reig (§8(f) N1)
+def test_reig_spec_examples():
+    """SPEC.md:233-236: diag(3, −2, 1, 0, …) 10×10, k = 2 → (3, −2) with signs
+    kept and eigenvectors e₀, e₁; the identity with k = 1 → 1."""
+    A = np.diag([3.0, -2.0, 1.0] + [0.0] * 7)
+    U, lam = oracle.reig(A, 2, its=2, l=4, seed=0)
+    assert np.allclose(lam, [3.0, -2.0], atol=1e-10, rtol=0)
+    assert np.allclose(np.abs(U[:2, :]), np.eye(2), atol=1e-10) and np.allclose(U[2:], 0, atol=1e-10)
+    U, lam = oracle.reig(np.eye(20), 1, its=1, l=3, seed=1)
+    assert abs(lam[0] - 1.0) < 1e-12 and abs(np.linalg.norm(U[:, 0]) - 1.0) < 1e-12
+
+
+def test_reig_full_width_is_lapack_eigh():
+    """l = n: Q spans everything, so reig is the exact eigendecomposition —
+    LAPACK's (numpy eigh) ordered by |λ| (SPEC.md:236's random symmetric 40×40)."""
+    rng = np.random.default_rng(40)
+    G = rng.standard_normal((40, 40))
+    A = (G + G.T) / 2
+    U, lam = oracle.reig(A, 6, its=4, l=40, seed=0)
+    w, V = np.linalg.eigh(A)
+    o = np.argsort(-np.abs(w), kind="stable")[:6]
+    assert np.max(np.abs(lam - w[o]) / np.abs(w[o])) < 1e-12
+    for j in range(6):  # simple eigenvalues: vectors equal up to sign
+        assert min(np.linalg.norm(U[:, j] - V[:, o[j]]), np.linalg.norm(U[:, j] + V[:, o[j]])) < 1e-10
+    assert np.linalg.norm(U.T @ U - np.eye(6)) < 1e-13
+
+
+@pytest.mark.parametrize("n,r,k,l", [(300, 8, 8, 10), (500, 12, 6, 12)])
+def test_reig_exact_rank_indefinite(n, r, k, l):
+    """A = V diag(λ) Vᵀ of rank r ≤ l with mixed signs: reig recovers the
+    eigenpairs of largest |λ| exactly (Q spans range(A) after one application)."""
+    rng = np.random.default_rng(n + r)
+    V = np.linalg.qr(rng.standard_normal((n, r)))[0]
+    lam_true = np.array([(-1.0) ** j * 10.0 * 0.7 ** j for j in range(r)])
+    A = (V * lam_true) @ V.T
+    A = (A + A.T) / 2
+    U, lam = oracle.reig(A, k, its=1, l=l, seed=2)
+    o = np.argsort(-np.abs(lam_true), kind="stable")[:k]
+    assert np.max(np.abs(lam - lam_true[o]) / np.abs(lam_true[o])) < 1e-11
+    assert np.all(np.sign(lam) == np.sign(lam_true[o]))
+    assert sin_angle(V[:, o], U) < 1e-10
+    Ak = (U * lam) @ U.T
+    if k == r:
+        assert np.linalg.norm(A - Ak) < 1e-10 * np.linalg.norm(A)
+
+
+def test_reig_psd_matches_nystrom_and_is_nonnegative():
+    """SPEC.md invariants: a nonnegative-definite A gives lam ≥ −1e-10·‖A‖, and
+    Rayleigh–Ritz (reig) interlaces below the true λ (λ̂_j ≤ λ_j)."""
+    A = synth.make_c3(n=1024).numpy()
+    U, lam = oracle.reig(A, 20, its=2, l=22, seed=0)
+    true = 1.0 / np.arange(1, 21) ** 2
+    assert np.all(lam >= -1e-10 * true[0])
+    assert np.all(lam <= true * (1 + 1e-12))
+    assert np.max(np.abs(lam[:5] - true[:5]) / true[:5]) < 1e-7  # (λ₂₃/λ_j)^(2·its+2) convergence
+    Un, ln = oracle.eigens(A, 20, its=2, l=22, seed=0)
+    assert np.max(np.abs(lam[:5] - ln[:5]) / ln[:5]) < 1e-7
