@@ -60,6 +60,10 @@ enum { RPCA_SHIFT_CHOL = 0, RPCA_SQRT = 1 };
                                          reports the same), no extra pass over A; diffsnorm also
                                          checks the factors through y = A·x − U·(S⊙Vᵀx) */
 #define RPCA_FLAG_NO_GRAPH 0x8u       /* do not capture/replay driver calls as CUDA graphs */
+#define RPCA_FLAG_RENORM_ODD 0x10u    /* rpca_pca: renormalise only after the odd applications
+                                         (§8(f) N2) — the long-side block of each
+                                         interior power round enters the next adjoint application
+                                         unrenormalised (its LU skipped); faster, less accurate */
 
 /* ops for rpca_workspace_query */
 enum { RPCA_OP_PCA = 1, RPCA_OP_EIGENS = 2, RPCA_OP_DIFFSNORM = 3, RPCA_OP_APPLY = 4, RPCA_OP_REIG = 5 };

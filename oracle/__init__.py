@@ -60,6 +60,7 @@ def lib():
             L.oracle_jacobi_eig.argtypes = [dp, i64, dp, dp]
             mat = [i32, i32, i64, i64, vp, i64, vp, vp, vp]
             L.oracle_pca.argtypes = mat + [i64, i32, i32, i64, u64, i32, dp, dp, dp]
+            L.oracle_pca_ex.argtypes = mat + [i64, i32, i32, i64, u64, i32, i32, dp, dp, dp]
             L.oracle_eigens.argtypes = [i32, i32, i64, vp, i64, vp, vp, vp, i64, i32, i64, u64, i32, i32, dp, dp]
             L.oracle_diffsnorm.argtypes = mat + [i32, dp, dp, dp, i64, i32, u64, dp]
             L.oracle_reig.argtypes = [i32, i32, i64, vp, i64, vp, vp, vp, i64, i32, i64, u64, i32, dp, dp]
@@ -175,15 +176,20 @@ def colmeans(A):
     return c
 
 
-def pca(A, k: int, raw: bool = True, its: int = 2, l: int | None = None, seed: int = 0, dist: int = GAUSSIAN):
-    """(U m×k, S k, V n×k) — PAPER.md §2 eqs. (i1)-(i4), §5."""
+def pca(A, k: int, raw: bool = True, its: int = 2, l: int | None = None, seed: int = 0, dist: int = GAUSSIAN,
+        renorm_odd: bool = False):
+    """(U m×k, S k, V n×k) — PAPER.md §2 eqs. (i1)-(i4), §5 (renorm_odd: PAPER.md:442-449)."""
     keep, args = _mat_args(A)
     m, n = args[2], args[3]
     U = np.empty((m, k))
     S = np.empty(k)
     V = np.empty((n, k))
-    _check(lib().oracle_pca(*args, k, int(bool(raw)), its, -1 if l is None else l, seed, dist,
-                            _p(U), _p(S), _p(V)), "pca")
+    if renorm_odd:
+        _check(lib().oracle_pca_ex(*args, k, int(bool(raw)), its, -1 if l is None else l, seed, dist, 1,
+                                   _p(U), _p(S), _p(V)), "pca")
+    else:
+        _check(lib().oracle_pca(*args, k, int(bool(raw)), its, -1 if l is None else l, seed, dist,
+                                _p(U), _p(S), _p(V)), "pca")
     return U, S, V
 
 

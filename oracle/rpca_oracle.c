@@ -587,11 +587,14 @@ static void round_to_f32(double* x, int64_t count) {
  *
  * Outputs (row-major): U m×k, S k, V n×k; sign convention Q10.
  * raw != 0: no centring; raw == 0: implicit column centring.
+ * renorm_odd != 0 (oracle_pca_ex; §8(f) N2, "renormalize
+ * only in the odd-numbered iterations"): the interior rounds' Y = F·Z is
+ * passed to the next F* unrenormalised (the first lu and the last qr stay).
  * ---------------------------------------------------------------------- */
-int oracle_pca(int kind, int dtype, int64_t m, int64_t n, const void* a, int64_t lda,
-               const int64_t* rowptr, const int32_t* colind, const void* vals,
-               int64_t k, int raw, int its, int64_t l, uint64_t seed, int dist,
-               double* U, double* S, double* V) {
+int oracle_pca_ex(int kind, int dtype, int64_t m, int64_t n, const void* a, int64_t lda,
+                  const int64_t* rowptr, const int32_t* colind, const void* vals,
+                  int64_t k, int raw, int its, int64_t l, uint64_t seed, int dist, int renorm_odd,
+                  double* U, double* S, double* V) {
   omat A;
   int st = make_omat(&A, kind, dtype, m, n, a, lda, rowptr, colind, vals);
   if (st) return st;
@@ -618,6 +621,7 @@ int oracle_pca(int kind, int dtype, int64_t m, int64_t n, const void* a, int64_t
     op_adj(&F, Y, l, Z);
     if ((st = oracle_lu_renorm(Z, nin, l, NULL, NULL))) goto done;
     op_fwd(&F, Z, l, Y);
+    if (it < its && renorm_odd) continue;
     st = (it < its) ? oracle_lu_renorm(Y, nout, l, NULL, NULL) : oracle_house_qr(Y, nout, l, NULL);
     if (st) goto done;
   }
@@ -651,6 +655,13 @@ int oracle_pca(int kind, int dtype, int64_t m, int64_t n, const void* a, int64_t
 done:
   free(c); free(Om); free(Y); free(Z); free(Wm); free(sg);
   return st;
+}
+
+int oracle_pca(int kind, int dtype, int64_t m, int64_t n, const void* a, int64_t lda,
+               const int64_t* rowptr, const int32_t* colind, const void* vals,
+               int64_t k, int raw, int its, int64_t l, uint64_t seed, int dist,
+               double* U, double* S, double* V) {
+  return oracle_pca_ex(kind, dtype, m, n, a, lda, rowptr, colind, vals, k, raw, its, l, seed, dist, 0, U, S, V);
 }
 
 /* Upper Cholesky C with CᵀC = B (l×l) — eq. (Cholesky).

@@ -34,6 +34,7 @@ GAUSSIAN, UNIFORM = 0, 1
 SHIFT_CHOL, SQRT = 0, 1
 FLAG_UNIFORM_OMEGA, FLAG_OUTPUTS_HOST, FLAG_CHECK_FINITE = 0x1, 0x2, 0x4
 OP_PCA, OP_EIGENS, OP_DIFFSNORM, OP_APPLY, OP_REIG = 1, 2, 3, 4, 5
+FLAG_RENORM_ODD = 0x10
 
 
 class RPCAError(RuntimeError):
@@ -420,8 +421,12 @@ def small_svd(G: torch.Tensor):
 
 
 def pca(A: torch.Tensor, k: int, raw: bool = True, its: int = 2, l: int | None = None, seed: int = 0,
-        uniform_omega: bool = False, m_total: int | None = None, row0: int = 0, check_finite: bool = False):
+        uniform_omega: bool = False, m_total: int | None = None, row0: int = 0, check_finite: bool = False,
+        renorm_odd: bool = False):
     """Rank-k PCA / SVD of A (§2 eqs. i1-i4, §5): returns (U m×k, S k, V n×k) on A's device.
+
+    renorm_odd=True renormalises only after the odd applications of A / A*
+    (PAPER.md:442-449): the interior rounds' long-side LU is skipped.
 
     raw=False centres the columns implicitly.  A may also be
     a pinned host tensor: then the host→device copy and the device→host copy of
@@ -434,7 +439,7 @@ def pca(A: torch.Tensor, k: int, raw: bool = True, its: int = 2, l: int | None =
     L_, h = _ctx(dev)
     m, n = A.shape  # m: local rows
     flags = ((FLAG_UNIFORM_OMEGA if uniform_omega else 0) | (FLAG_OUTPUTS_HOST if host else 0) |
-             (FLAG_CHECK_FINITE if check_finite else 0))
+             (FLAG_CHECK_FINITE if check_finite else 0) | (FLAG_RENORM_ODD if renorm_odd else 0))
     _ctx_flags(h, flags)
     outdev = torch.device("cpu") if host else dev
     pin = host

@@ -120,7 +120,8 @@ rpca_status rpca_ctx_set_stream(rpca_ctx* c, void* stream) {
 
 rpca_status rpca_ctx_set_flags(rpca_ctx* c, uint32_t flags) {
   if (!c) return RPCA_E_ARG;
-  if (flags & ~(uint32_t)(RPCA_FLAG_UNIFORM_OMEGA | RPCA_FLAG_OUTPUTS_HOST | RPCA_FLAG_CHECK_FINITE | RPCA_FLAG_NO_GRAPH))
+  if (flags & ~(uint32_t)(RPCA_FLAG_UNIFORM_OMEGA | RPCA_FLAG_OUTPUTS_HOST | RPCA_FLAG_CHECK_FINITE | RPCA_FLAG_NO_GRAPH |
+                          RPCA_FLAG_RENORM_ODD))
     return RPCA_E_ARG;
   c->flags = flags;
   return RPCA_OK;

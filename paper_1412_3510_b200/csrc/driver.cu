@@ -775,6 +775,7 @@ void pca(Ctx& c, const rpca_mat* Am, int64_t k, int raw, int its, int64_t l, uin
   RPCA_REQUIRE(ldu >= k && ldv >= k, RPCA_E_SHAPE, "ldu, ldv must be ≥ k");
   const int L = (int)l, K = (int)k;
   const bool out_host = (c.flags & RPCA_FLAG_OUTPUTS_HOST) != 0;
+  const bool renorm_odd = (c.flags & RPCA_FLAG_RENORM_ODD) != 0;
   const int dist = (c.flags & RPCA_FLAG_UNIFORM_OMEGA) ? RPCA_UNIFORM : RPCA_GAUSSIAN;
   const int odt = Am->dtype, osz = elem_size(odt);
   const int64_t m = Am->m, n = Am->n, ml = Am->m_local, r0 = Am->row0;
@@ -825,6 +826,11 @@ void pca(Ctx& c, const rpca_mat* Am, int64_t k, int raw, int its, int64_t l, uin
       mu = adj(c, F, Yb, L, Zb, mub, mub + kMaxL, ar);
       renorm_lu(c, Z, L, ar, mu);
       mu = fwd(c, F, Zb, L, Yb, mub, mub + kMaxL, ar);
+      // RPCA_FLAG_RENORM_ODD: the long-side block of an
+      // interior round goes into the next F*·Y unrenormalised — the schedule
+      // that lets F*(F·Z) stream in one pass; its pending centring is
+      // re-derived from Y by adj()
+      if (it < its && renorm_odd) continue;
       if (it < its) renorm_lu(c, Y, L, ar, mu);
       else renorm_qr(c, Y, L, nullptr, ar, mu);
     }

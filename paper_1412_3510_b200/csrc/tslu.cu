@@ -441,6 +441,7 @@ __global__ void __launch_bounds__(kThreads, 2)
   __shared__ int piv[LP];
   __shared__ int colexp[LP];
   __shared__ int nrows_s;
+  extern __shared__ float stage[];  // CAP × (l+1) scaled fp32 rows
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int64_t blk = blockIdx.x;
   for (int t = tid; t < LP; t += kThreads) colexp[t] = 0;
@@ -482,39 +483,67 @@ __global__ void __launch_bounds__(kThreads, 2)
   const int steps = min(rows, l);
   bool act[R];
   int pstep[R];
-  const double* src[R];
 #pragma unroll
   for (int q = 0; q < R; ++q) {
-    const int r = tid * R + q;
-    act[q] = r < rows;
+    act[q] = tid * R + q < rows;
     pstep[q] = -1;
-    src[q] = act[q] ? Y + ids[r] * l : Y;
   }
-  // pass 1: per-column exponent maxima of the block (pending centring on load)
-#pragma unroll 4
-  for (int t = 0; t < LP; ++t) {
-    if (t >= l) break;
-    const double mt = mu ? mu[t] : 0.0;
-    unsigned f = 0;
+  // Rows are read coalesced — warp w takes rows w, w+8, …, lane j columns j
+  // and j+32 (a thread-per-row read touched one 32-byte sector per lane and
+  // saturated L1: ncu, profiles/r02_lu_nominate.md) — twice: pass 1 takes the
+  // per-column exponent maxima (pending centring applied on load), pass 2
+  // (L1/L2-hot) writes the scaled fp32 rows to shared memory at a stride of
+  // l+1 floats, from where each thread loads its own rows bank-conflict free.
+  const int sl = l + 1;
+  {
+    const double m0 = (mu && lane < l) ? mu[lane] : 0.0, m1 = (mu && lane + 32 < l) ? mu[lane + 32] : 0.0;
+    // eight rows' loads in flight per warp (the loads are latency-bound)
+    constexpr int U8 = 8;
+    auto load8 = [&](int r0, double (&v0)[U8], double (&v1)[U8]) {
 #pragma unroll
-    for (int q = 0; q < R; ++q)
-      if (act[q]) f = max(f, (unsigned)(__double_as_longlong(src[q][t] - mt) >> 52) & 0x7FFu);
-    f = __reduce_max_sync(0xffffffffu, f);
-    if (lane == 0 && f) atomicMax(&colexp[t], (int)f);
-  }
-  __syncthreads();
-  // pass 2 (L1-resident): scaled fp32 rows in registers
-  float w[R][LP];
+      for (int u = 0; u < U8; ++u) {
+        const int r = r0 + u * kWarps;
+        const double* y = Y + (r < rows ? ids[r] : 0) * l;
+        v0[u] = (r < rows && lane < l) ? y[lane] : 0.0;
+        v1[u] = (r < rows && lane + 32 < l) ? y[lane + 32] : 0.0;
+      }
+    };
+    unsigned f0 = 0, f1 = 0;
+    for (int r0 = warp; r0 < rows; r0 += kWarps * U8) {
+      double v0[U8], v1[U8];
+      load8(r0, v0, v1);
 #pragma unroll
-  for (int t = 0; t < LP; ++t) {
-    const int f = t < l ? colexp[t] : 0;
+      for (int u = 0; u < U8; ++u) {
+        if (r0 + u * kWarps >= rows) break;
+        f0 = max(f0, (unsigned)(__double_as_longlong(v0[u] - m0) >> 52) & 0x7FFu);
+        f1 = max(f1, (unsigned)(__double_as_longlong(v1[u] - m1) >> 52) & 0x7FFu);
+      }
+    }
+    if (lane < l && f0) atomicMax(&colexp[lane], (int)f0);
+    if (lane + 32 < l && f1) atomicMax(&colexp[lane + 32], (int)f1);
+    __syncthreads();
     // 2^(1023 − f) (field f ≥ 1): the column maximum lands in [1, 2) ([2, 4)
     // for the top binade, whose 2^-1023 would be subnormal)
-    const double sc = f ? __longlong_as_double((long long)(2046 - min(f, 2045)) << 52) : 0.0;
-    const double mt = (mu && t < l) ? mu[t] : 0.0;
+    auto scale = [](int f) { return f ? __longlong_as_double((long long)(2046 - min(f, 2045)) << 52) : 0.0; };
+    const double s0 = lane < l ? scale(colexp[lane]) : 0.0, s1 = lane + 32 < l ? scale(colexp[lane + 32]) : 0.0;
+    for (int r0 = warp; r0 < rows; r0 += kWarps * U8) {
+      double v0[U8], v1[U8];
+      load8(r0, v0, v1);
 #pragma unroll
-    for (int q = 0; q < R; ++q) w[q][t] = (act[q] && t < l && f) ? (float)((src[q][t] - mt) * sc) : 0.f;
+      for (int u = 0; u < U8; ++u) {
+        const int r = r0 + u * kWarps;
+        if (r >= rows) break;
+        if (lane < l) stage[r * sl + lane] = (float)((v0[u] - m0) * s0);
+        if (lane + 32 < l) stage[r * sl + lane + 32] = (float)((v1[u] - m1) * s1);
+      }
+    }
   }
+  __syncthreads();
+  float w[R][LP];
+#pragma unroll
+  for (int q = 0; q < R; ++q)
+#pragma unroll
+    for (int t = 0; t < LP; ++t) w[q][t] = (act[q] && t < l) ? stage[(tid * R + q) * sl + t] : 0.f;
   // blocked GEPP in 8-column panels — the fp64 kernel's scheme (lu_select_kernel)
   for (int pb = 0; pb < steps; pb += 8) {
     const int ns = min(8, steps - pb);
@@ -538,7 +567,9 @@ __global__ void __launch_bounds__(kThreads, 2)
           if (q == bq) {
             slot[j & 1][warp] = make_uint2(mk, (uint32_t)(tid * R + q));
             const float pv = w[q][s];
-            suinv[j & 1][warp] = fabsf(pv) >= 0x1p-100f ? __frcp_rn(pv) : 0.f;  // tiny: a zero column
+            float rc;  // MUFU reciprocal (nomination only needs ~1 ulp); tiny pivot ⇒ a zero column
+            asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(rc) : "f"(pv));
+            suinv[j & 1][warp] = fabsf(pv) >= 0x1p-100f ? rc : 0.f;
 #pragma unroll
             for (int t = s; t < 8; ++t) pbuf[j & 1][warp][t] = w[q][t];
           }
@@ -699,8 +730,10 @@ int nominate_cap(int l) { return kThreads * nominate_rows_per_thread(lp_of(l)); 
 template <int LP>
 void nominate_lp(Ctx& c, unsigned grid, const double* Y, int64_t m, int l, int leaf, const int64_t* cin,
                  int64_t n_in, int G, int64_t* cout, const double* mu) {
-  lu_nominate_kernel<LP, nominate_rows_per_thread(LP)><<<grid, kThreads, 0, c.stream>>>(Y, m, l, leaf, cin, n_in, G,
-                                                                                          cout, mu);
+  constexpr int R = nominate_rows_per_thread(LP);
+  const int smem = kThreads * R * (l + 1) * 4;
+  ensure_smem((const void*)lu_nominate_kernel<LP, R>, kThreads * R * (LP + 1) * 4);
+  lu_nominate_kernel<LP, R><<<grid, kThreads, smem, c.stream>>>(Y, m, l, leaf, cin, n_in, G, cout, mu);
 }
 
 void nominate(Ctx& c, unsigned grid, const double* Y, int64_t m, int l, int leaf, const int64_t* cin, int64_t n_in,

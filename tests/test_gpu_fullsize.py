@@ -55,7 +55,7 @@ def test_c3_full_vs_oracle():
     est = rp.diffsnorm(A, U, lam, U, its=20, seed=1)
     ref = oracle.diffsnorm(Ah, Uo, lo, Uo, its=20, seed=1)
     assert abs(est - ref) <= 0.01 * ref, (est, ref)
-    assert est >= 1.0 / (cfg.k + 1) ** 2 * (1 - 1e-6)  # ≥ λ_{k+1} (Eckart–Young, exact spectrum j^-2)
+    assert est >= 1.0 / (cfg.k + 1) ** 2 * (1 - 1e-2)  # ≥ λ_{k+1} (power method: from below) (Eckart–Young, exact spectrum j^-2)
 
 
 def test_c2_full_diffsnorm():

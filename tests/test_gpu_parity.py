@@ -507,11 +507,12 @@ def test_reig_indefinite_vs_oracle(n, k, l, its):
     assert np.all(np.sign(lg) == np.sign(lo))
     assert np.max(np.abs(lg - lo) / np.abs(lo)) < 1e-10
     assert cluster_sin_angle(Uo, U.cpu().numpy(), np.abs(lo), k) < 1e-8
-    assert abs(lg[0] - 1.0) < 1e-6 and abs(lg[1] + 2.0**-1.5) < 1e-6
+    assert abs(lg[0] - 1.0) < 1e-4 and abs(lg[1] + 2.0**-1.5) < 1e-3 * 2.0**-1.5  # (|λ_{l+1}|/|λ_j|)^(2its+2)
     # the error estimate of the rank-k eigen-approximation: ≥ |λ_{k+1}| (Eckart–Young)
     est = rp.diffsnorm(A, U, lam, U, its=20, seed=1)
     ref = oracle.diffsnorm(A.cpu().numpy(), Uo, lo, Uo, its=20, seed=1)
-    assert abs(est - ref) <= 1e-2 * ref and est >= (k + 1) ** -1.5 * (1 - 1e-6)
+    # (the power method approaches ‖E‖ from below: 1% slack)
+    assert abs(est - ref) <= 1e-2 * ref and est >= (k + 1) ** -1.5 * (1 - 1e-2)
 
 
 def test_reig_spec_examples_gpu():
@@ -521,3 +522,30 @@ def test_reig_spec_examples_gpu():
     assert np.allclose(lam.cpu().numpy(), [3.0, -2.0], atol=1e-12, rtol=0)
     U, lam = rp.reig(torch.eye(40, dtype=torch.float64, device=dev()), 1, its=1, l=3)
     assert abs(float(lam[0]) - 1.0) < 1e-13
+
+
+# ----------------------------------------------------------------- renorm_odd (§8(f) N2)
+@pytest.mark.parametrize("m,n,k,l,its,raw", [(20000, 1000, 20, 22, 3, True), (3001, 257, 20, 22, 4, False),
+                                             (700, 2000, 8, 10, 3, True)])
+def test_pca_renorm_odd_vs_oracle(m, n, k, l, its, raw):
+    """RPCA_FLAG_RENORM_ODD: the interior long-side LUs are
+    skipped on both sides; parity at the fp64 tolerances on spectra where the
+    unrenormalised block stays well conditioned (σ_j = 1/j)."""
+    g = torch.Generator(device="cuda").manual_seed(m + its)
+    sig = 1.0 / torch.arange(1, min(m, n) + 1, dtype=torch.float64)
+    A = synth.synth_dense(m, n, sig, seed=m + n, device=dev()).contiguous()
+    if not raw:
+        A += torch.rand(n, generator=g, device=dev(), dtype=torch.float64) * 10 - 5
+    res = rp.pca(A, k, raw=raw, its=its, l=l, seed=4, renorm_odd=True)
+    # unrenormalised blocks amplify the two sides' different rounding (the
+    # accuracy the paper says this variant gives up): 10× the fp64 tolerances
+    compare(res, oracle.pca(A.cpu().numpy(), k, raw=raw, its=its, l=l, seed=4, renorm_odd=True), k,
+            tol_s=1e-9, tol_a=1e-7)
+    # and it launches fewer LU leaves than the default schedule
+    with rp.profile() as p1:
+        rp.pca(A, k, raw=raw, its=its, l=l, seed=4)
+        torch.cuda.synchronize()
+    with rp.profile() as p2:
+        rp.pca(A, k, raw=raw, its=its, l=l, seed=4, renorm_odd=True)
+        torch.cuda.synchronize()
+    assert p2.total("lu_leaf")[0] < p1.total("lu_leaf")[0]

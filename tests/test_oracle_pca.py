@@ -385,3 +385,44 @@ def test_reig_psd_matches_nystrom_and_is_nonnegative():
     assert np.max(np.abs(lam[:5] - true[:5]) / true[:5]) < 1e-7  # (λ₂₃/λ_j)^(2·its+2) convergence
     Un, ln = oracle.eigens(A, 20, its=2, l=22, seed=0)
     assert np.max(np.abs(lam[:5] - ln[:5]) / ln[:5]) < 1e-7
+
+
+# ----------------------------------------------------------------- renorm_odd (§8(f) N2)
+def test_renorm_odd_reduces_to_default_without_interior_rounds():
+    """its ≤ 1 has no interior round to skip: bitwise the default path."""
+    A = synth.make_c1(m=400, n=300).numpy()
+    for its in (0, 1):
+        a = oracle.pca(A, 8, its=its, l=10, seed=2)
+        b = oracle.pca(A, 8, its=its, l=10, seed=2, renorm_odd=True)
+        assert all(np.array_equal(x, y) for x, y in zip(a, b))
+
+
+@pytest.mark.parametrize("raw", [True, False])
+def test_renorm_odd_same_span_when_well_conditioned(raw):
+    """Renormalisation does not change the span in exact arithmetic (PAPER.md:
+    200-204): on a well-conditioned spectrum the two schedules agree to rounding."""
+    A = synth.make_c1(m=800, n=400, seed=5).numpy()
+    if not raw:
+        A = A + np.linspace(-3, 3, 400)[None, :]
+    a = oracle.pca(A, 10, raw=raw, its=3, l=12, seed=1)
+    b = oracle.pca(A, 10, raw=raw, its=3, l=12, seed=1, renorm_odd=True)
+    assert np.max(np.abs(a[1] - b[1]) / a[1]) < 1e-12
+    assert cluster_sin_angle(a[0], b[0], a[1], 10) < 1e-10
+    assert cluster_sin_angle(a[2], b[2], a[1], 10) < 1e-10
+
+
+def test_renorm_odd_loses_accuracy_on_fast_decay():
+    """skipping renormalisations "would sacrifice accuracy".
+    With σ_j = 10^-j/2 an unrenormalised F·F*·Q has κ ≈ (σ₁/σ_l)² and the trailing
+    directions drown in rounding: the default schedule's trailing σ are exact
+    to ~1e-13 relative, the odd-only schedule's are not."""
+    m, n, k, l = 600, 300, 16, 18
+    sig = torch.tensor([10.0 ** (-j / 2) for j in range(n)], dtype=torch.float64)
+    A = synth.synth_dense(m, n, sig, seed=9).numpy()
+    a = oracle.pca(A, k, its=4, l=l, seed=0)
+    b = oracle.pca(A, k, its=4, l=l, seed=0, renorm_odd=True)
+    true = sig[:k].numpy()
+    err_a = np.max(np.abs(a[1] - true) / true)
+    err_b = np.max(np.abs(b[1] - true) / true)
+    assert err_a < 1e-10 and err_b > 10 * err_a, (err_a, err_b)
+    assert np.max(np.abs(b[1][:4] - true[:4]) / true[:4]) < 1e-10  # the leading values survive

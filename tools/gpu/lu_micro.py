@@ -34,9 +34,12 @@ for m, l in shapes:
         c, s = agg.get(name, (0, 0.0))
         agg[name] = (c + 1, s + ms)
     L = Ys[0]
-    Q = torch.linalg.qr(L)[0]
-    Qy = torch.linalg.qr(Y)[0]
-    sin = float(torch.linalg.matrix_norm(Qy - Q @ (Q.T @ Qy), 2))
+    if m * l > 1e8:  # torch.linalg on 10M-row blocks: skip the span check
+        sin = float("nan")
+    else:
+        Q = torch.linalg.qr(L)[0]
+        Qy = torch.linalg.qr(Y)[0]
+        sin = float(torch.linalg.matrix_norm(Qy - Q @ (Q.T @ Qy), 2))
     tot = sum(v[1] for v in agg.values()) / 5
     print(f"m={m:9d} l={l:2d} total {1e3 * tot:8.1f}us  maxL {float(L.abs().max()):.3g} sin(Y,L) {sin:.1e}  " +
           " ".join(f"{k}:{v[0] // 5}x{1e3 * v[1] / 5:.1f}us" for k, v in agg.items()), flush=True)
