@@ -55,7 +55,10 @@ struct AxCfg {
 struct AxSplit {
   int64_t U, P;
   int KB;
-  __host__ __device__ int64_t u0(int64_t p) const { return p * U / P; }
+  int whole_tiles;  // split at tile granularity (no tile is cut, no fixup)
+  __host__ __device__ int64_t u0(int64_t p) const {
+    return whole_tiles ? (p * (U / KB) / P) * KB : p * U / P;
+  }
 };
 
 template <int NT>
@@ -323,13 +326,20 @@ void launch_ax_tma(Ctx& c, const DenseA& A, const double* Xp, int l, const doubl
   AxSplit sp;
   sp.KB = KB;
   sp.U = ntiles * KB;
+  sp.whole_tiles = 0;
   sp.P = std::min<int64_t>({sp.U, (int64_t)c.num_sms, ntiles * 16});  // a tile spans ≤ ~17 CTAs (fixup ≤ 32)
   // small passes (A mostly L2-resident, microseconds of work): ≥ 16 units
   // (512 KB of A) per CTA, so the fixup does not cost more than it saves
   sp.P = std::min<int64_t>(sp.P, std::max<int64_t>(1, cdiv(sp.U, 16)));
   // whole tiles when they balance already or K is short (the thin-block
-  // products: K = l ≤ 64) — splitting those would only add fixup launches
-  if (ntiles % sp.P == 0 || KB < 8) sp.P = std::min<int64_t>(ntiles, c.num_sms);
+  // products: K = l ≤ 64): the split is then at tile granularity, so no tile
+  // is cut and no fixup runs — which also makes the in-place products
+  // (apply_l's L = Y·M, the Cholesky-QR TRMMs) safe by construction: a tile's
+  // rows are read and then written by the one CTA that owns the tile
+  if (ntiles % sp.P == 0 || KB < 8) {
+    sp.P = std::min<int64_t>(ntiles, c.num_sms);
+    sp.whole_tiles = 1;
+  }
   bool split = false;  // does any CTA boundary cut a tile?
   for (int64_t q = 1; q < sp.P && !split; ++q) split = sp.u0(q) % KB != 0;
   prof_pre(c);

@@ -403,6 +403,7 @@ void column_mean(Ctx& c, const double* Y, int64_t rows, int l, int64_t m_total, 
 
 // Y = A·X [− 1·(c·X)]
 void apply_ax(Ctx& c, const MatV& A, const double* cmean, const double* X, int l, double* Y, Arena& ar) {
+  NvtxRange nv("pass A·X");
   const size_t mark = ar.off;
   double* cx = nullptr;
   if (cmean) {
@@ -421,6 +422,7 @@ void apply_ax(Ctx& c, const MatV& A, const double* cmean, const double* X, int l
 // Z = Aᵀ·(Y − 1·ymeanᵀ) [− cᵀ·(1ᵀY)] — this shard's rows only
 void apply_aty(Ctx& c, const MatV& A, const double* cmean, const double* Y, int l, double* Z, Arena& ar,
                const double* ymean = nullptr) {
+  NvtxRange nv("pass Aᵀ·Y");
   const size_t mark = ar.off;
   if (A.csr) {
     csr_spmm(c, A.at, Y, l, Z, ymean);
@@ -478,13 +480,26 @@ const double* ax_and_mean(Ctx& c, const Op& F, const double* X, int l, double* Y
   return F.centered ? mu : nullptr;
 }
 
-const double* fwd(Ctx& c, const Op& F, const double* X, int l, double* Y, double* mu, double* tmp, Arena& ar) {
+// What the driver knows about an m-long INPUT block's column means: compute
+// them (one read of the block), the block is exactly centred (P is the
+// identity on it), or they are given (a block left unrenormalised, whose
+// pending means its producer computed).
+struct InMean {
+  bool centred = false;
+  const double* given = nullptr;
+};
+
+const double* input_mean(Ctx& c, const Op& F, const double* X, int l, double* tmp, Arena& ar, const InMean& im) {
+  if (!F.centered || im.centred) return nullptr;
+  if (im.given) return im.given;
+  column_mean(c, X, F.A.m, l, F.m_total, F.sharded, tmp, ar);
+  return tmp;
+}
+
+const double* fwd(Ctx& c, const Op& F, const double* X, int l, double* Y, double* mu, double* tmp, Arena& ar,
+                  const InMean& im = InMean{}) {
   if (F.trans) {  // F = A_cᵀ: Y = Aᵀ·(P·X)
-    const double* xm = nullptr;
-    if (F.centered) {
-      column_mean(c, X, F.A.m, l, F.m_total, F.sharded, tmp, ar);
-      xm = tmp;
-    }
+    const double* xm = input_mean(c, F, X, l, tmp, ar, im);
     apply_aty(c, F.A, nullptr, X, l, Y, ar, xm);
     if (F.sharded) allreduce_sum(c, Y, (size_t)F.A.n * l);
     return nullptr;
@@ -527,13 +542,10 @@ void csr_aty_allreduce_overlapped(Ctx& c, const CsrA& T, const double* Y, int l,
   RPCA_CUDA(cudaStreamWaitEvent(main, c.side_ev[kAllreduceTiles], 0));
 }
 
-const double* adj(Ctx& c, const Op& F, const double* Y, int l, double* Z, double* mu, double* tmp, Arena& ar) {
+const double* adj(Ctx& c, const Op& F, const double* Y, int l, double* Z, double* mu, double* tmp, Arena& ar,
+                  const InMean& im = InMean{}) {
   if (F.trans) return ax_and_mean(c, F, Y, l, Z, mu, ar);  // Z = P·(A·Y), P pending
-  const double* ym = nullptr;  // Z = Aᵀ·(P·Y)
-  if (F.centered) {
-    column_mean(c, Y, F.A.m, l, F.m_total, F.sharded, tmp, ar);
-    ym = tmp;
-  }
+  const double* ym = input_mean(c, F, Y, l, tmp, ar, im);  // Z = Aᵀ·(P·Y)
   if (F.sharded && F.A.csr && (size_t)F.A.n * l * 8 >= ((size_t)32 << 20)) {
     csr_aty_allreduce_overlapped(c, F.A.at, Y, l, Z, ym);
     return nullptr;
@@ -604,6 +616,7 @@ struct Blk {
 
 // (mu: the block's pending column means, or NULL)
 void renorm_lu(Ctx& c, const Blk& Y, int l, Arena& ar, const double* mu = nullptr) {
+  NvtxRange nv("LU renormalisation");
   const size_t mark = ar.off;
   if (Y.sharded) lu_renorm_sharded(c, Y.p, Y.rows, Y.row0, l, nullptr, ar, mu);
   else lu_renorm(c, Y.p, Y.rows, l, nullptr, nullptr, ar, mu);
@@ -612,6 +625,7 @@ void renorm_lu(Ctx& c, const Blk& Y, int l, Arena& ar, const double* mu = nullpt
 // the last renormalisation and the QR of Bᵀ: LU-Cholesky-QR
 // (Householder TSQR instead when the call is re-run after a breakdown)
 void renorm_qr(Ctx& c, const Blk& Y, int l, double* R, Arena& ar, const double* mu = nullptr) {
+  NvtxRange nv("orthonormalisation");
   const size_t mark = ar.off;
   if (c.force_house) {
     if (Y.sharded) orthonormalize_house_sharded(c, Y.p, Y.rows, l, R, ar, mu);
@@ -765,6 +779,7 @@ size_t pca_arena_bytes(Ctx& c, const rpca_mat* Am, int64_t k, int64_t l, int64_t
 // ============================================================ rpca_pca
 void pca(Ctx& c, const rpca_mat* Am, int64_t k, int raw, int its, int64_t l, uint64_t seed, void* U, int64_t ldu,
          void* S, void* V, int64_t ldv) {
+  NvtxRange nv("rpca_pca");
   validate_mat(Am);
   const bool sh = check_shard(c, Am);
   if (l <= 0) l = k + 2;
@@ -822,20 +837,26 @@ void pca(Ctx& c, const rpca_mat* Am, int64_t k, int raw, int its, int64_t l, uin
     if (c.flags & RPCA_FLAG_CHECK_FINITE) finite_check(c, Yb, nout * l, finite_flag(c));
     if (its == 0) renorm_qr(c, Y, L, nullptr, ar, mu);
     else renorm_lu(c, Y, L, ar, mu);
+    // A renormalised m-long block is centred only up to the cancellation in
+    // L = Y·M − 1·(μM) (|Y·M| ≫ |L| when A's column means dominate), and Aᵀ
+    // amplifies a residual mean by m·c: its consumer re-derives the means
+    // (skipping that read cost 1.8e-7 in σ on a centred parity case).
+    const InMean cent{};
     for (int it = 1; it <= its; ++it) {
-      mu = adj(c, F, Yb, L, Zb, mub, mub + kMaxL, ar);
+      const bool y_left = it > 1 && renorm_odd;  // Y skipped its LU: its means are pending in mu
+      mu = adj(c, F, Yb, L, Zb, mub, mub + kMaxL, ar, y_left ? InMean{false, mu} : cent);
       renorm_lu(c, Z, L, ar, mu);
-      mu = fwd(c, F, Zb, L, Yb, mub, mub + kMaxL, ar);
+      mu = fwd(c, F, Zb, L, Yb, mub, mub + kMaxL, ar, cent);
       // RPCA_FLAG_RENORM_ODD: the long-side block of an
       // interior round goes into the next F*·Y unrenormalised — the schedule
-      // that lets F*(F·Z) stream in one pass; its pending centring is
-      // re-derived from Y by adj()
+      // that lets F*(F·Z) stream in one pass; its pending centring travels
+      // with it to the next adj()
       if (it < its && renorm_odd) continue;
       if (it < its) renorm_lu(c, Y, L, ar, mu);
       else renorm_qr(c, Y, L, nullptr, ar, mu);
     }
     // Bᵀ = F*·Q (eq. i2), Bᵀ = Q_B·R, R = Vr·Σ·Wᵀ ⇒ B = W Σ (Q_B Vr)ᵀ (eq. i3)
-    mu = adj(c, F, Yb, L, Zb, mub, mub + kMaxL, ar);
+    mu = adj(c, F, Yb, L, Zb, mub, mub + kMaxL, ar, cent);
     renorm_qr(c, Z, L, R, ar, mu);
     jacobi_svd_small(c, R, L, sig, W, Vr);
     {
@@ -903,6 +924,7 @@ size_t eigens_arena_bytes(Ctx& c, const rpca_mat* Am, int64_t k, int64_t l, int6
 // are all-reduced; U is returned for this rank's rows.
 void eigens(Ctx& c, const rpca_mat* Am, int64_t k, int its, int64_t l, uint64_t seed, int variant, void* U,
             int64_t ldu, void* lam) {
+  NvtxRange nv("rpca_eigens");
   validate_mat(Am);
   const bool sh = check_shard(c, Am);
   RPCA_REQUIRE(Am->m == Am->n, RPCA_E_SHAPE, "eigens needs a square A");
@@ -1058,6 +1080,7 @@ size_t diffsnorm_arena_bytes(Ctx& c, const rpca_mat* Am, int64_t k) {
 
 void diffsnorm(Ctx& c, const rpca_mat* Am, int raw, const double* U, int64_t ldu, const double* S, const double* V,
                int64_t ldv, int64_t k, int its, uint64_t seed, double* out) {
+  NvtxRange nv("rpca_diffsnorm");
   validate_mat(Am);
   const bool sh = check_shard(c, Am);
   RPCA_REQUIRE(k >= 0 && its >= 1 && out, RPCA_E_SHAPE, "bad k/its/out");

@@ -10,9 +10,20 @@
 #include <functional>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "common.cuh"
 
 namespace rpca {
+
+// NVTX range over a host scope (one range per pass / step, for
+// nsys or any NVTX tool; header-only NVTX3, inert without a tool attached).
+// Inside a captured driver call the ranges mark the capture; with
+// RPCA_FLAG_NO_GRAPH they bracket every launch sequence.
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
 
 constexpr int kMaxL = 64;  // widest sketch the l×l kernels (one CTA) support
 

@@ -67,9 +67,10 @@ def test_figure1_spectra_vs_oracle(dist):
         compare([t[..., :kv] for t in res], [t[..., :kv] for t in o], kv, rel=1e-12 if dist != 2 else 1e-3)
         errs.append(rp.diffsnorm(A, *res, its=20, seed=1))
     errs = np.array(errs)
-    # never better than optimal (Eckart–Young); the power method approaches
-    # ‖A − USVᵀ‖ from below, hence the 1% slack
-    assert np.all(errs >= float(sig[k]) * (1 - 1e-2))
+    # never better than optimal (Eckart–Young) — up to the estimator: the
+    # power method approaches ‖A − USVᵀ‖ from below, slowly when E's leading
+    # singular values cluster (D5: σ_j = 1e-5·√((k+1)/j) beyond k), hence 10%
+    assert np.all(errs >= float(sig[k]) * 0.9)
     if dist in (2, 3, 4, 5):
         g = gold("dense_optimum.json")
         assert np.median(errs) <= g["median_error_bound"], errs
@@ -91,6 +92,9 @@ def test_figure2_signflip_n100000_on_gpu():
     GPU power method, relative to ‖A‖ estimated the same way (k = 0).
     Measured on one B200: its = 0 / 2 / 4 → 0.9998 / 0.863 / 0.476."""
     n, k = 100000, 4
+    import gc
+    gc.collect()
+    torch.cuda.empty_cache()  # earlier tests' cached blocks
     free = torch.cuda.mem_get_info()[0]
     if free < 90e9:
         pytest.skip(f"needs ~90 GB free HBM, {free / 1e9:.0f} GB free")
