@@ -60,6 +60,13 @@ enum { RPCA_SHIFT_CHOL = 0, RPCA_SQRT = 1 };
                                          reports the same), no extra pass over A; diffsnorm also
                                          checks the factors through y = A·x − U·(S⊙Vᵀx) */
 #define RPCA_FLAG_NO_GRAPH 0x8u       /* do not capture/replay driver calls as CUDA graphs */
+#define RPCA_FLAG_STREAM_A 0x20u     /* out-of-core A (§8(f) N4): a HOST dense A is not
+                                         staged whole; every pass streams it through two device
+                                         buffers of $RPCA_STREAM_CHUNK_MB (default 256) MB, the
+                                         H2D copy of chunk c+1 overlapping the pass on chunk c
+                                         (pin the host A for overlap).  With RPCA_FLAG_RENORM_ODD
+                                         each interior round F*(F·Z) streams A ONCE (its + 2 streams
+                                         instead of 2·its + 2) */
 #define RPCA_FLAG_RENORM_ODD 0x10u    /* rpca_pca: renormalise only after the odd applications
                                          (§8(f) N2) — the long-side block of each
                                          interior power round enters the next adjoint application

@@ -34,7 +34,7 @@ GAUSSIAN, UNIFORM = 0, 1
 SHIFT_CHOL, SQRT = 0, 1
 FLAG_UNIFORM_OMEGA, FLAG_OUTPUTS_HOST, FLAG_CHECK_FINITE = 0x1, 0x2, 0x4
 OP_PCA, OP_EIGENS, OP_DIFFSNORM, OP_APPLY, OP_REIG = 1, 2, 3, 4, 5
-FLAG_RENORM_ODD = 0x10
+FLAG_RENORM_ODD, FLAG_STREAM_A = 0x10, 0x20
 
 
 class RPCAError(RuntimeError):
@@ -422,11 +422,13 @@ def small_svd(G: torch.Tensor):
 
 def pca(A: torch.Tensor, k: int, raw: bool = True, its: int = 2, l: int | None = None, seed: int = 0,
         uniform_omega: bool = False, m_total: int | None = None, row0: int = 0, check_finite: bool = False,
-        renorm_odd: bool = False):
+        renorm_odd: bool = False, stream_a: bool = False):
     """Rank-k PCA / SVD of A (§2 eqs. i1-i4, §5): returns (U m×k, S k, V n×k) on A's device.
 
     renorm_odd=True renormalises only after the odd applications of A / A*
     (PAPER.md:442-449): the interior rounds' long-side LU is skipped.
+    stream_a=True (host A only) keeps A out of core: every pass streams it
+    through two device chunk buffers (with renorm_odd, one stream per round).
 
     raw=False centres the columns implicitly.  A may also be
     a pinned host tensor: then the host→device copy and the device→host copy of
@@ -439,7 +441,8 @@ def pca(A: torch.Tensor, k: int, raw: bool = True, its: int = 2, l: int | None =
     L_, h = _ctx(dev)
     m, n = A.shape  # m: local rows
     flags = ((FLAG_UNIFORM_OMEGA if uniform_omega else 0) | (FLAG_OUTPUTS_HOST if host else 0) |
-             (FLAG_CHECK_FINITE if check_finite else 0) | (FLAG_RENORM_ODD if renorm_odd else 0))
+             (FLAG_CHECK_FINITE if check_finite else 0) | (FLAG_RENORM_ODD if renorm_odd else 0) |
+             (FLAG_STREAM_A if stream_a else 0))
     _ctx_flags(h, flags)
     outdev = torch.device("cpu") if host else dev
     pin = host
@@ -457,7 +460,7 @@ def pca(A: torch.Tensor, k: int, raw: bool = True, its: int = 2, l: int | None =
 
 def eigens(A: torch.Tensor, k: int, its: int = 2, l: int | None = None, seed: int = 0,
            variant: str = "shift_chol", uniform_omega: bool = False, m_total: int | None = None, row0: int = 0,
-           check_finite: bool = False):
+           check_finite: bool = False, stream_a: bool = False):
     """Stabilised Nyström (§3) of a PSD A: returns (U n×k, lam k).
     Sharded: A holds rows uniform_shard(n, P, rank) and U comes back for them."""
     host = A.device.type == "cpu"
@@ -466,7 +469,7 @@ def eigens(A: torch.Tensor, k: int, its: int = 2, l: int | None = None, seed: in
     n = A.shape[0]  # local rows
     v = {"shift_chol": SHIFT_CHOL, "sqrt": SQRT}[variant]
     _ctx_flags(h, (FLAG_UNIFORM_OMEGA if uniform_omega else 0) | (FLAG_OUTPUTS_HOST if host else 0) |
-               (FLAG_CHECK_FINITE if check_finite else 0))
+               (FLAG_CHECK_FINITE if check_finite else 0) | (FLAG_STREAM_A if stream_a else 0))
     outdev = torch.device("cpu") if host else dev
     U = torch.empty(n, k, dtype=A.dtype, device=outdev, pin_memory=host)
     lam = torch.empty(k, dtype=A.dtype, device=outdev, pin_memory=host)
@@ -501,7 +504,8 @@ def reig(A: torch.Tensor, k: int, its: int = 2, l: int | None = None, seed: int 
 
 
 def diffsnorm(A: torch.Tensor, U: torch.Tensor, S: torch.Tensor, V: torch.Tensor, raw: bool = True, its: int = 20,
-              seed: int = 1, m_total: int | None = None, row0: int = 0, check_finite: bool = False) -> float:
+              seed: int = 1, m_total: int | None = None, row0: int = 0, check_finite: bool = False,
+              stream_a: bool = False) -> float:
     """Power-method estimate of ‖A − U·diag(S)·Vᵀ‖ (§4 l.362-371).
     Sharded: A and U are this rank's rows, V replicated."""
     host = isinstance(A, torch.Tensor) and A.device.type == "cpu" or isinstance(A, CSR) and A.device.type == "cpu"
@@ -513,7 +517,7 @@ def diffsnorm(A: torch.Tensor, U: torch.Tensor, S: torch.Tensor, V: torch.Tensor
     k = S.shape[0]
     out = C.c_double(0.0)
     mat, keep = _as_mat(A, host=host, m_total=m_total, row0=row0)
-    _ctx_flags(h, FLAG_CHECK_FINITE if check_finite else 0)
+    _ctx_flags(h, (FLAG_CHECK_FINITE if check_finite else 0) | (FLAG_STREAM_A if stream_a else 0))
     try:
         _check(L_.rpca_diffsnorm(h, C.byref(mat), int(bool(raw)), _ptr(U), max(k, 1), _ptr(S), _ptr(V), max(k, 1),
                                  k, its, seed, C.byref(out)))

@@ -100,6 +100,11 @@ rpca_status rpca_ctx_destroy(rpca_ctx* c) {
       cudaStreamDestroy(c->side);
     }
     for (auto e : c->side_ev) cudaEventDestroy(e);
+    if (c->h2d) {
+      cudaStreamSynchronize(c->h2d);
+      cudaStreamDestroy(c->h2d);
+      for (auto e : c->h2d_ev) cudaEventDestroy(e);
+    }
     if (c->work) {
       cudaStreamSynchronize(c->work);
       cudaStreamDestroy(c->work);
@@ -121,7 +126,7 @@ rpca_status rpca_ctx_set_stream(rpca_ctx* c, void* stream) {
 rpca_status rpca_ctx_set_flags(rpca_ctx* c, uint32_t flags) {
   if (!c) return RPCA_E_ARG;
   if (flags & ~(uint32_t)(RPCA_FLAG_UNIFORM_OMEGA | RPCA_FLAG_OUTPUTS_HOST | RPCA_FLAG_CHECK_FINITE | RPCA_FLAG_NO_GRAPH |
-                          RPCA_FLAG_RENORM_ODD))
+                          RPCA_FLAG_RENORM_ODD | RPCA_FLAG_STREAM_A))
     return RPCA_E_ARG;
   c->flags = flags;
   return RPCA_OK;

@@ -251,13 +251,58 @@ void validate_mat(const rpca_mat* A) {
   }
 }
 
-// Device view of A's local shard (dense or CSR + cached CSR(Aᵀ)).
+// Out-of-core A (§8(f) N4, RPCA_FLAG_STREAM_A; "a matrix A
+// stored on disk"): a host dense A is streamed through two device buffers of
+// `chunk` rows per pass.  stage() issues the H2D copy of a chunk on the copy
+// stream once the buffer's previous user has finished (event `freed`) and
+// makes the compute stream wait for it (event `ready`); release() marks the
+// buffer free after the kernels enqueued on it.  Because the copy of chunk
+// c+1 is enqueued before the compute stream reaches it, it overlaps the pass
+// kernels on chunk c.
+struct Streamer {
+  const char* host = nullptr;
+  int es = 8, dtype = RPCA_F64;
+  int64_t lda = 0, m = 0, n = 0, chunk = 0;
+  char* buf[2] = {nullptr, nullptr};
+  int64_t q = 0;  // chunks staged so far in this call
+  int64_t nchunks() const { return cdiv(m, chunk); }
+  DenseA stage(Ctx& c, int64_t ci, int64_t* r0_out) {
+    const int b = (int)(q & 1);
+    if (q >= 2) RPCA_CUDA(cudaStreamWaitEvent(c.h2d, c.h2d_ev[2 + b], 0));
+    const int64_t r0 = ci * chunk, rows = std::min(chunk, m - r0);
+    RPCA_CUDA(cudaMemcpyAsync(buf[b], host + r0 * lda * es, (size_t)rows * lda * es, cudaMemcpyHostToDevice, c.h2d));
+    RPCA_CUDA(cudaEventRecord(c.h2d_ev[b], c.h2d));
+    RPCA_CUDA(cudaStreamWaitEvent(c.stream, c.h2d_ev[b], 0));
+    if (c.prof == 1) prof_mark(c, "h2d_chunk");  // (profiling only: one record per staged chunk)
+    *r0_out = r0;
+    return DenseA{buf[b], dtype, rows, n, lda};
+  }
+  void release(Ctx& c) {
+    RPCA_CUDA(cudaEventRecord(c.h2d_ev[2 + (q & 1)], c.stream));
+    ++q;
+  }
+};
+
+int64_t stream_chunk_rows(const rpca_mat* A) {
+  const char* e = getenv("RPCA_STREAM_CHUNK_MB");
+  const int64_t mb = e ? std::max<int64_t>(1, atoll(e)) : int64_t(256);
+  const int64_t row_bytes = A->lda * (A->dtype == RPCA_F64 ? 8 : 4);
+  return std::max<int64_t>(128, (mb << 20) / std::max<int64_t>(1, row_bytes) / 128 * 128);
+}
+
+bool streamed(const Ctx& c, const rpca_mat* A) {
+  return (c.flags & RPCA_FLAG_STREAM_A) && A->location == RPCA_HOST && A->kind == RPCA_DENSE && A->m_local > 0;
+}
+
+// Device view of A's local shard (dense or CSR + cached CSR(Aᵀ), or a
+// streamed host dense A).
 struct MatV {
   bool csr = false;
   DenseA d{};
   CsrA a{}, at{};
   int64_t m = 0, n = 0;  // local rows, columns
   int dtype = RPCA_F64;
+  Streamer* st = nullptr;
 };
 
 MatV probe_of(const rpca_mat* A) {
@@ -330,8 +375,27 @@ uint64_t ensure_transpose(Ctx& c, const rpca_mat* A) {
   return fp;
 }
 
-MatV device_view(Ctx& c, const rpca_mat* A, Arena& ar) {
+MatV device_view(Ctx& c, const rpca_mat* A, Arena& ar, Streamer* st = nullptr) {
   MatV v = probe_of(A);
+  if (st && streamed(c, A)) {
+    if (!c.h2d) {
+      RPCA_CUDA(cudaStreamCreateWithFlags(&c.h2d, cudaStreamNonBlocking));
+      for (auto& e : c.h2d_ev) RPCA_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    }
+    const int es = elem_size(A->dtype);
+    st->host = static_cast<const char*>(A->a);
+    st->es = es;
+    st->dtype = A->dtype;
+    st->lda = A->lda;
+    st->m = A->m_local;
+    st->n = A->n;
+    st->chunk = std::min<int64_t>(A->m_local, stream_chunk_rows(A));
+    st->q = 0;
+    for (auto& b : st->buf) b = ar.get<char>((size_t)st->chunk * A->lda * es);
+    v.st = st;
+    v.d.a = nullptr;
+    return v;
+  }
   if (v.csr && A->location == RPCA_DEVICE) {
     v.a = c.tcache.A;
     v.at = c.tcache.T;
@@ -363,8 +427,11 @@ MatV device_view(Ctx& c, const rpca_mat* A, Arena& ar) {
 }
 
 // arena bytes device_view takes for a host A (+ the transpose scratch of a host CSR)
-size_t host_copy_bytes(const rpca_mat* A) {
+size_t host_copy_bytes(const Ctx& c, const rpca_mat* A) {
   if (A->location != RPCA_HOST) return 0;
+  if (streamed(c, A))
+    return 2 * Arena::align((size_t)std::min<int64_t>(A->m_local, stream_chunk_rows(A)) * A->lda *
+                            elem_size(A->dtype)) + 512;
   if (A->kind == RPCA_DENSE) return (size_t)A->m_local * A->lda * elem_size(A->dtype) + 256;
   Sizer s;
   s.add<int64_t>(A->m_local + 1);
@@ -410,7 +477,16 @@ void apply_ax(Ctx& c, const MatV& A, const double* cmean, const double* X, int l
     cx = ar.get<double>(kMaxL);
     weighted_colsum(c, cmean, X, A.n, l, cx, ar);
   }
-  if (A.csr) {
+  if (A.st) {  // out-of-core: row chunks are independent
+    for (int64_t ci = 0; ci < A.st->nchunks(); ++ci) {
+      int64_t r0 = 0;
+      const DenseA Ac = A.st->stage(c, ci, &r0);
+      const size_t m2 = ar.off;
+      dense_ax(c, Ac, X, l, Y + r0 * l, ar, cx);
+      ar.off = m2;
+      A.st->release(c);
+    }
+  } else if (A.csr) {
     csr_spmm(c, A.a, X, l, Y);
     if (cx) sub_rank1(c, Y, A.m, l, nullptr, cx);
   } else {
@@ -424,7 +500,18 @@ void apply_aty(Ctx& c, const MatV& A, const double* cmean, const double* Y, int 
                const double* ymean = nullptr) {
   NvtxRange nv("pass Aᵀ·Y");
   const size_t mark = ar.off;
-  if (A.csr) {
+  if (A.st) {  // out-of-core: Z = Σ_chunks A_cᵀ·Y_c, added in chunk order
+    double* Zc = ar.get<double>((size_t)A.n * l);
+    for (int64_t ci = 0; ci < A.st->nchunks(); ++ci) {
+      int64_t r0 = 0;
+      const DenseA Ac = A.st->stage(c, ci, &r0);
+      const size_t m2 = ar.off;
+      dense_aty(c, Ac, Y + r0 * l, l, cmean, ci == 0 ? Z : Zc, ar, ymean);
+      ar.off = m2;
+      A.st->release(c);
+      if (ci > 0) add_into(c, Z, Zc, A.n * l);
+    }
+  } else if (A.csr) {
     csr_spmm(c, A.at, Y, l, Z, ymean);
     if (cmean) {
       double* sy = ar.get<double>(kMaxL);
@@ -440,8 +527,22 @@ void apply_aty(Ctx& c, const MatV& A, const double* cmean, const double* Y, int 
 // cmean = column means of the whole A (local sums ÷ m_total, all-reduced)
 void colmeans(Ctx& c, const MatV& A, int64_t m_total, double* cmean, Arena& ar, bool sharded = false) {
   const size_t mark = ar.off;
-  if (A.csr) csr_colmeans(c, A.at, m_total, cmean);
-  else colmeans_dense(c, A.d.a, A.d.dtype, A.d.m, A.d.n, A.d.lda, m_total, cmean, ar);
+  if (A.st) {
+    double* cc = ar.get<double>(A.n);
+    for (int64_t ci = 0; ci < A.st->nchunks(); ++ci) {
+      int64_t r0 = 0;
+      const DenseA Ac = A.st->stage(c, ci, &r0);
+      const size_t m2 = ar.off;
+      colmeans_dense(c, Ac.a, Ac.dtype, Ac.m, Ac.n, Ac.lda, m_total, ci == 0 ? cmean : cc, ar);
+      ar.off = m2;
+      A.st->release(c);
+      if (ci > 0) add_into(c, cmean, cc, A.n);
+    }
+  } else if (A.csr) {
+    csr_colmeans(c, A.at, m_total, cmean);
+  } else {
+    colmeans_dense(c, A.d.a, A.d.dtype, A.d.m, A.d.n, A.d.lda, m_total, cmean, ar);
+  }
   ar.off = mark;
   if (sharded) allreduce_sum(c, cmean, A.n);
 }
@@ -461,7 +562,7 @@ const double* ax_and_mean(Ctx& c, const Op& F, const double* X, int l, double* Y
     ~Reset() { c.ax_colpart = nullptr; c.ax_colpart_n = 0; }
   } reset{c};
   c.ax_colpart_n = 0;
-  c.ax_colpart = (F.centered && !F.A.csr) ? ar.get<double>(ax_colpart_elems(F.A.m, l)) : nullptr;
+  c.ax_colpart = (F.centered && !F.A.csr && !F.A.st) ? ar.get<double>(ax_colpart_elems(F.A.m, l)) : nullptr;
   apply_ax(c, F.A, nullptr, X, l, Y, ar);
   const double* part = c.ax_colpart;
   const int64_t np = c.ax_colpart_n;
@@ -553,6 +654,48 @@ const double* adj(Ctx& c, const Op& F, const double* Y, int l, double* Z, double
   apply_aty(c, F.A, nullptr, Y, l, Z, ar, ym);
   if (F.sharded) allreduce_sum(c, Z, (size_t)F.A.n * l);
   return nullptr;
+}
+
+// §8(f) N2 on an out-of-core A: one interior power round of the
+// RENORM_ODD schedule, Y = A·Z and Z' = Aᵀ·(P·Y), from ONE stream of A — the
+// "halve the number of disk accesses" of PAPER.md:442-449: every chunk's
+// Y_c = A_c·Z is followed at once by Z' += A_cᵀ·Y_c while A_c is resident.
+// Centred, P·Y needs Y's global column means μ, known only after the last
+// chunk, so the correction is applied in the paper's rank-1 form (PAPER.md:
+// 430-435): Z' −= (Aᵀ1)·μᵀ = m·c_A·μᵀ, with A's column means c_A summed
+// from the resident chunks of the first fused round.  Single-rank only.
+void fused_round(Ctx& c, const Op& F, const double* Z, int l, double* Y, double* Zn, double* cA, bool have_cA,
+                 double* mu, Arena& ar) {
+  NvtxRange nv("fused pass Aᵀ(A·Z)");
+  const MatV& A = F.A;
+  const size_t mark = ar.off;
+  double* Zc = ar.get<double>((size_t)A.n * l);
+  double* cc = ar.get<double>(A.n);
+  double* Zacc = Zn == Z ? ar.get<double>((size_t)A.n * l) : Zn;  // Z is read by every chunk's A·Z
+  for (int64_t ci = 0; ci < A.st->nchunks(); ++ci) {
+    int64_t r0 = 0;
+    const DenseA Ac = A.st->stage(c, ci, &r0);
+    const size_t m2 = ar.off;
+    dense_ax(c, Ac, Z, l, Y + r0 * l, ar, nullptr);
+    ar.off = m2;
+    dense_aty(c, Ac, Y + r0 * l, l, nullptr, ci == 0 ? Zacc : Zc, ar, nullptr);
+    ar.off = m2;
+    if (F.centered && !have_cA) {
+      colmeans_dense(c, Ac.a, Ac.dtype, Ac.m, Ac.n, Ac.lda, F.m_total, ci == 0 ? cA : cc, ar);
+      ar.off = m2;
+    }
+    A.st->release(c);
+    if (ci > 0) {
+      add_into(c, Zacc, Zc, A.n * l);
+      if (F.centered && !have_cA) add_into(c, cA, cc, A.n);
+    }
+  }
+  if (F.centered) {
+    column_mean(c, Y, A.m, l, F.m_total, false, mu, ar);
+    sub_rank1(c, Zacc, A.n, l, cA, mu, (double)F.m_total);
+  }
+  if (Zacc != Zn) RPCA_CUDA(cudaMemcpyAsync(Zn, Zacc, sizeof(double) * A.n * l, cudaMemcpyDeviceToDevice, c.stream));
+  ar.off = mark;
 }
 
 // The int8-digit emulation of a driver call's A·X passes (dense_ax_emu.cu):
@@ -754,7 +897,7 @@ size_t pca_arena_bytes(Ctx& c, const rpca_mat* Am, int64_t k, int64_t l, int64_t
   const bool trans = m < n;
   const int64_t nin = trans ? ml : n, nout = trans ? n : ml;
   Sizer sz;
-  sz.add<char>(host_copy_bytes(Am));
+  sz.add<char>(host_copy_bytes(c, Am));
   sz.add<double>(nin * l);   // Zb
   sz.add<double>(nout * l);  // Yb
   sz.add<double>(4 * l * l + 4 * l);
@@ -766,6 +909,10 @@ size_t pca_arena_bytes(Ctx& c, const rpca_mat* Am, int64_t k, int64_t l, int64_t
     sz.add<char>((size_t)ml * ldu * osz);
     sz.add<char>((size_t)n * ldv * osz);
     sz.add<char>((size_t)k * osz);
+  }
+  if (streamed(c, Am)) {  // chunk accumulators, A's column means, the fused round's buffers
+    sz.add<double>(n);
+    sz.add<double>(3 * n * l + 2 * n);
   }
   size_t scratch = op_ws(c, probe, L);
   scratch = std::max(scratch, lu_ws_bytes(std::max(nin, nout), L));
@@ -807,8 +954,9 @@ void pca(Ctx& c, const rpca_mat* Am, int64_t k, int raw, int its, int64_t l, uin
      << c.comm << ep.on();
   const bool graphable = Am->location == RPCA_DEVICE && !out_host && graphable_comm(c);
 
+  Streamer stm;
   run_checked(c, kh.h, graphable, ar, [&] {
-    const MatV dA = device_view(c, Am, ar);
+    const MatV dA = device_view(c, Am, ar, &stm);
     EmuScope emu(c, ep);
     double* Zb = ar.get<double>(nin * l);
     double* Yb = ar.get<double>(nout * l);
@@ -842,10 +990,22 @@ void pca(Ctx& c, const rpca_mat* Am, int64_t k, int raw, int its, int64_t l, uin
     // amplifies a residual mean by m·c: its consumer re-derives the means
     // (skipping that read cost 1.8e-7 in σ on a centred parity case).
     const InMean cent{};
+    // RENORM_ODD on an out-of-core A, one rank, m ≥ n: the interior rounds
+    // are fused into one stream of A each (fused_round)
+    const bool fuse = renorm_odd && dA.st && !trans && !sh && its >= 2;
+    double* cA = fuse && F.centered ? ar.get<double>(n) : nullptr;
     for (int it = 1; it <= its; ++it) {
-      const bool y_left = it > 1 && renorm_odd;  // Y skipped its LU: its means are pending in mu
-      mu = adj(c, F, Yb, L, Zb, mub, mub + kMaxL, ar, y_left ? InMean{false, mu} : cent);
-      renorm_lu(c, Z, L, ar, mu);
+      if (fuse && it >= 2) {
+        // the previous round's Y = A·Z was not formed separately: this pass
+        // forms it and Z = Aᵀ·(P·Y) together
+        fused_round(c, F, Zb, L, Yb, Zb, cA, it > 2, mub, ar);
+        renorm_lu(c, Z, L, ar, nullptr);
+      } else {
+        const bool y_left = it > 1 && renorm_odd;  // Y skipped its LU: its means are pending in mu
+        mu = adj(c, F, Yb, L, Zb, mub, mub + kMaxL, ar, y_left ? InMean{false, mu} : cent);
+        renorm_lu(c, Z, L, ar, mu);
+      }
+      if (fuse && it < its) continue;  // Y = A·Z happens inside the next fused pass
       mu = fwd(c, F, Zb, L, Yb, mub, mub + kMaxL, ar, cent);
       // RPCA_FLAG_RENORM_ODD: the long-side block of an
       // interior round goes into the next F*·Y unrenormalised — the schedule
@@ -899,7 +1059,7 @@ size_t eigens_arena_bytes(Ctx& c, const rpca_mat* Am, int64_t k, int64_t l, int6
   const int L = (int)l, K = (int)k;
   const MatV probe = probe_of(Am);
   Sizer sz;
-  sz.add<char>(host_copy_bytes(Am));
+  sz.add<char>(host_copy_bytes(c, Am));
   sz.add<double>(2 * P * pad * l + 2 * ml * l);
   sz.add<double>(6 * l * l + 8 * l + 16);
   sz.add<double>(ml * k + k);
@@ -979,8 +1139,9 @@ void eigens(Ctx& c, const rpca_mat* Am, int64_t k, int its, int64_t l, uint64_t 
     else column_signs(c, X, ml, K, k, sign, ar);
   };
   double* Qfin = ((its & 1) ? Qb : Qa) + slot;  // this rank's final Q after the loop's swaps
+  Streamer stm;
   run_checked(c, kh.h, graphable, ar, [&] {
-    const MatV dA = device_view(c, Am, ar);
+    const MatV dA = device_view(c, Am, ar, &stm);
     EmuScope emu(c, ep);
     double* Qf = Qa;  // gathered Q
     double* Qo = Qb;  // the other gather buffer
@@ -1072,7 +1233,7 @@ void eigens(Ctx& c, const rpca_mat* Am, int64_t k, int its, int64_t l, uint64_t 
 size_t diffsnorm_arena_bytes(Ctx& c, const rpca_mat* Am, int64_t k) {
   const int64_t n = Am->n, ml = Am->m_local;
   Sizer sz;
-  sz.add<char>(host_copy_bytes(Am));
+  sz.add<char>(host_copy_bytes(c, Am));
   sz.add<double>(2 * n + ml + n + k + 64);
   const size_t scratch = op_ws(c, probe_of(Am), 1) + (size_t)(cdiv(std::max(ml, n), 2048) + 2) * (n + 64) * 8;
   return sz.total + scratch + 65536;
@@ -1099,8 +1260,9 @@ void diffsnorm(Ctx& c, const rpca_mat* Am, int raw, const double* U, int64_t ldu
   double* sc = ar.get<double>(8);  // [0] nz2, [1] est, [2] scratch
   int* done = ar.get<int>(4);
   kh << c.flags;
+  Streamer stm;
   run_checked(c, kh.h, Am->location == RPCA_DEVICE && graphable_comm(c), ar, [&] {
-    const MatV dA = device_view(c, Am, ar);
+    const MatV dA = device_view(c, Am, ar, &stm);
     if (!raw) {
       const size_t mark = ar.off;
       colmeans(c, dA, m, cmean, ar, sh);

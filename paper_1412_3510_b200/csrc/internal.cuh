@@ -136,6 +136,10 @@ struct Ctx {
   // sparse Aᵀ·Y all-reduce of driver.cu)
   cudaStream_t side = nullptr;
   std::vector<cudaEvent_t> side_ev;
+  // out-of-core A (RPCA_FLAG_STREAM_A): host→device copy stream and the
+  // ready / freed events of its two chunk buffers
+  cudaStream_t h2d = nullptr;
+  cudaEvent_t h2d_ev[4] = {nullptr, nullptr, nullptr, nullptr};
   // fp64 A·X on the int8 tensor cores (dense_ax_emu.cu): the row exponents of
   // the driver call's A, valid while that call runs (EmuScope)
   const int* emu_E = nullptr;
@@ -223,6 +227,8 @@ void right_mult(Ctx& c, const double* In, const double* Q, const double* nu, con
 void rank_k_sub(Ctx& c, double* y, const double* U, int64_t ldu, const double* t, int64_t rows, int k);
 // t ← t ⊙ S
 void hadamard(Ctx& c, double* t, const double* S, int k);
+// Z[i] += W[i]
+void add_into(Ctx& c, double* Z, const double* W, int64_t count);
 // *flag = 1 if any of x[0..count) is NaN or ±Inf (flag untouched otherwise)
 void finite_check(Ctx& c, const double* x, int64_t count, int* flag);
 

@@ -341,6 +341,18 @@ void weighted_colsum(Ctx& c, const double* a, const double* X, int64_t rows, int
   count_launch(c, 2);
 }
 
+__global__ void add_into_kernel(double* __restrict__ Z, const double* __restrict__ W, int64_t count) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count; i += (int64_t)gridDim.x * blockDim.x)
+    Z[i] += W[i];
+}
+
+void add_into(Ctx& c, double* Z, const double* W, int64_t count) {
+  if (count == 0) return;
+  add_into_kernel<<<grid_for(c, count), 256, 0, c.stream>>>(Z, W, count);
+  RPCA_CHECK_LAUNCH();
+  count_launch(c, 1, "stream_accumulate");
+}
+
 void sub_rank1(Ctx& c, double* Y, int64_t rows, int l, const double* u, const double* v, double alpha) {
   sub_rank1_kernel<<<grid_for(c, rows * l), 256, 0, c.stream>>>(Y, rows, l, u, v, alpha);
   RPCA_CHECK_LAUNCH();
