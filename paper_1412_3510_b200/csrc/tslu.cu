@@ -632,206 +632,6 @@ __global__ void __launch_bounds__(kThreads, 2)
   for (int j = tid; j < l; j += kThreads) cand_out[blk * l + j] = j < steps ? ids[piv[j]] : -1;
 }
 
-// ---------------------------------------------------------------------------
-// Warp-level nomination for l ≤ 32: every WARP runs its own GEPP on a block
-// of 32·R rows (lane owns rows lane, lane+32, …, in registers) — no CTA
-// barrier per step: the column argmax is two redux.sync (max key, then the
-// lowest row among the ties), the pivot row's panel values and reciprocal are
-// broadcast by shuffles, and the panel-end U12 goes through the warp's own
-// slice of shared memory under __syncwarp.  A block of 32·R rows nominates l
-// of them (C2's l = 22: 128 → 22; C5's l = 32: 96 → 32), so the tournament
-// has more levels than with CTA-wide leaves, each far cheaper: the
-// CTA-barrier chain of the step was the bottleneck of lu_nominate_kernel
-// (ncu: 48% issue, stalls on barriers and short scoreboards).  Scaling and
-// the fp32 / final-fp64 contract as lu_nominate_kernel.
-constexpr int kNomWarps = 4;  // 4 independent warps per CTA, 3 CTAs per SM (≤ 170 registers)
-
-template <int LP>
-struct WNomCfg {
-  static constexpr int R = LP <= 8 ? 4 : (LP <= 16 ? 4 : (LP <= 24 ? 4 : 3));  // rows per lane
-  static constexpr int kRows = 32 * R;
-};
-
-template <int LP>
-__global__ void __launch_bounds__(32 * kNomWarps, 3)
-    lu_nominate_warp_kernel(const double* __restrict__ Y, int64_t m, int l, int leaf,
-                            const int64_t* __restrict__ cand_in, int64_t n_in, int G, int64_t nblk,
-                            int64_t* __restrict__ cand_out, const double* __restrict__ mu) {
-  using Cfg = WNomCfg<LP>;
-  constexpr int R = Cfg::R, ROWS = Cfg::kRows;
-  struct WarpSm {
-    int64_t ids[ROWS];
-    float stage[ROWS * 33];
-    float traw[8][LP];
-    float l11[8][8];
-    float u12[8][LP];
-    int piv[LP];
-  };
-  extern __shared__ __align__(16) unsigned char wsm_raw[];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  WarpSm& S = reinterpret_cast<WarpSm*>(wsm_raw)[warp];
-  const int64_t blk = (int64_t)blockIdx.x * kNomWarps + warp;
-  if (blk >= nblk) return;  // (no CTA-wide barrier below)
-  constexpr unsigned FULL = 0xffffffffu;
-  // ---- this block's rows: contiguous, or the valid candidates of G sets
-  int rows;
-  if (leaf == 1) {
-    const int64_t r0 = blk * ROWS;
-    rows = (int)imin64(ROWS, m - r0);
-    for (int r = lane; r < ROWS; r += 32) S.ids[r] = r0 + r;
-  } else {
-    const int64_t s0 = blk * G * l, s1 = imin64(n_in * l, s0 + (int64_t)G * l);
-    const int nslots = (int)(s1 - s0);
-    // sets cover ascending row ranges and each set's valid ids are kept in
-    // ascending order: a prefix count over the slots (valid ids first within
-    // a set after sorting) — slots are few (≤ ROWS), one lane per slot
-    int total = 0;
-    for (int base = 0; base < nslots; base += 32) {
-      const int sl = base + lane;
-      int64_t id = sl < nslots ? cand_in[s0 + sl] : -1;
-      int rank = 0;
-      if (id >= 0) {  // rank among the set's valid ids
-        const int st = sl / l;
-        for (int t = st * l; t < min(nslots, st * l + l); ++t) {
-          const int64_t o = cand_in[s0 + t];
-          rank += (o >= 0 && o < id);
-        }
-      }
-      // set offset: valid ids of the earlier sets (whole sets before this one)
-      int before = 0;
-      if (id >= 0) {
-        const int st = sl / l;
-        for (int t = 0; t < st * l; ++t) before += cand_in[s0 + t] >= 0;
-      }
-      if (id >= 0) S.ids[before + rank] = id;
-      total += __popc(__ballot_sync(FULL, id >= 0));
-    }
-    rows = total;
-  }
-  __syncwarp();
-  const int steps = min(rows, l);
-  // ---- coalesced loads, lane = column (l ≤ 32): pass 1 exponent maxima,
-  // pass 2 scaled fp32 rows into the warp's stage at a stride of 33 floats
-  const double mt = (mu && lane < l) ? mu[lane] : 0.0;
-  unsigned f = 0;
-  for (int r0 = 0; r0 < rows; r0 += 8) {
-    double v[8];
-#pragma unroll
-    for (int u = 0; u < 8; ++u) {
-      const int r = r0 + u;
-      v[u] = (r < rows && lane < l) ? Y[S.ids[r] * l + lane] : 0.0;
-    }
-#pragma unroll
-    for (int u = 0; u < 8; ++u)
-      if (r0 + u < rows) f = max(f, (unsigned)(__double_as_longlong(v[u] - mt) >> 52) & 0x7FFu);
-  }
-  const double sc = f ? __longlong_as_double((long long)(2046 - min((int)f, 2045)) << 52) : 0.0;
-  for (int r0 = 0; r0 < rows; r0 += 8) {
-    double v[8];
-#pragma unroll
-    for (int u = 0; u < 8; ++u) {
-      const int r = r0 + u;
-      v[u] = (r < rows && lane < l) ? Y[S.ids[r] * l + lane] : 0.0;
-    }
-#pragma unroll
-    for (int u = 0; u < 8; ++u)
-      if (r0 + u < rows) S.stage[(r0 + u) * 33 + lane] = lane < l ? (float)((v[u] - mt) * sc) : 0.f;
-  }
-  __syncwarp();
-  // lane's rows: q·32 + lane (conflict-free: bank (lane + q + t) mod 32)
-  float w[R][LP];
-  bool act[R];
-  int pstep[R];
-#pragma unroll
-  for (int q = 0; q < R; ++q) {
-    const int r = q * 32 + lane;
-    act[q] = r < rows;
-    pstep[q] = -1;
-#pragma unroll
-    for (int t = 0; t < LP; ++t) w[q][t] = (act[q] && t < l) ? S.stage[r * 33 + t] : 0.f;
-  }
-  // ---- GEPP in 8-column panels, warp-synchronous
-  for (int pb = 0; pb < steps; pb += 8) {
-    const int ns = min(8, steps - pb);
-#pragma unroll
-    for (int s = 0; s < 8; ++s) {
-      if (s >= ns) break;
-      uint32_t best = 0;
-      int bq = 0;
-#pragma unroll
-      for (int q = 0; q < R; ++q)
-        if (act[q]) {
-          const uint32_t k = piv_key32(w[q][s]) + 1u;
-          if (k > best) { best = k; bq = q; }
-        }
-      const uint32_t mk = __reduce_max_sync(FULL, best);
-      const uint32_t prow_id = __reduce_min_sync(FULL, best == mk ? (uint32_t)(bq * 32 + lane) : 0xFFFFFFFFu);
-      const int wl = (int)(prow_id & 31u), wq = (int)(prow_id >> 5);
-      // the winner's panel values (s … 7) and reciprocal, by shuffles
-      float pv[8];
-#pragma unroll
-      for (int t = 0; t < 8; ++t) {
-        float mine = 0.f;
-#pragma unroll
-        for (int q = 0; q < R; ++q)
-          if (q == wq) mine = w[q][t];
-        pv[t] = t >= s ? __shfl_sync(FULL, mine, wl) : 0.f;
-      }
-      float rc;
-      asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(rc) : "f"(pv[s]));
-      const float uinv = fabsf(pv[s]) >= 0x1p-100f ? rc : 0.f;  // tiny: a zero column
-      if (lane == 0) S.piv[pb + s] = (int)prow_id;  // local row = q·32 + lane
-#pragma unroll
-      for (int q = 0; q < R; ++q) {
-        if (!act[q]) continue;
-        if (lane == wl && q == wq) {
-          act[q] = false;
-          pstep[q] = s;
-          continue;
-        }
-        const float mult = w[q][s] * uinv;
-        w[q][s] = mult;
-#pragma unroll
-        for (int t = s + 1; t < 8; ++t) w[q][t] = fmaf(-mult, pv[t], w[q][t]);
-      }
-    }
-    if (pb + 8 >= LP) break;
-#pragma unroll
-    for (int q = 0; q < R; ++q)
-      if (pstep[q] >= 0) {
-        const int sp = pstep[q];
-#pragma unroll
-        for (int t = 8; t < LP; ++t) S.traw[sp][t - 8] = w[q][t];
-#pragma unroll
-        for (int t = 0; t < 8; ++t) S.l11[sp][t] = t < sp ? w[q][t] : 0.f;
-        pstep[q] = -2;
-      }
-    __syncwarp();
-    if (lane < LP - 8) {
-      float u[8];
-#pragma unroll
-      for (int sp = 0; sp < 8; ++sp) {
-        float v = sp < ns ? S.traw[sp][lane] : 0.f;
-#pragma unroll
-        for (int s2 = 0; s2 < sp; ++s2) v = fmaf(-S.l11[sp][s2], u[s2], v);
-        u[sp] = v;
-        S.u12[sp][lane] = v;
-      }
-    }
-    __syncwarp();
-    const int live = LP - pb;
-#pragma unroll
-    for (int q = 0; q < R; ++q) {
-      if (!act[q]) continue;
-      if (live > LP / 2) trail_update32<LP, LP>(w[q], S.u12, ns);
-      else trail_update32<LP, LP / 2>(w[q], S.u12, ns);
-    }
-    __syncwarp();  // u12 / traw are rewritten by the next panel
-  }
-  __syncwarp();
-  for (int j = lane; j < l; j += 32) cand_out[blk * l + j] = j < steps ? S.ids[S.piv[j]] : -1;
-}
-
 // Y[piv[j] − row0] ← Lp[j] for the pivot rows this shard holds (their exact
 // unit-lower rows)
 __global__ void pivot_rows_kernel(double* __restrict__ Y, int64_t m, int64_t row0, int l,
@@ -953,49 +753,6 @@ void nominate(Ctx& c, unsigned grid, const double* Y, int64_t m, int l, int leaf
   count_launch(c, 1, leaf == 1 ? "lu_leaf" : "lu_tree");
 }
 
-template <int LP>
-void nominate_warp_lp(Ctx& c, const double* Y, int64_t m, int l, int leaf, const int64_t* cin, int64_t n_in, int G,
-                      int64_t nblk, int64_t* cout, const double* mu) {
-  struct WarpSmSize {
-    int64_t ids[WNomCfg<LP>::kRows];
-    float stage[WNomCfg<LP>::kRows * 33];
-    float traw[8][LP];
-    float l11[8][8];
-    float u12[8][LP];
-    int piv[LP];
-  };
-  const int smem = (int)sizeof(WarpSmSize) * kNomWarps;
-  ensure_smem((const void*)lu_nominate_warp_kernel<LP>, smem);
-  const unsigned grid = (unsigned)cdiv(nblk, kNomWarps);
-  lu_nominate_warp_kernel<LP><<<grid, 32 * kNomWarps, smem, c.stream>>>(Y, m, l, leaf, cin, n_in, G, nblk, cout, mu);
-}
-
-int warp_nom_rows(int l) {
-  switch (lp_of(l)) {
-    case 8: return WNomCfg<8>::kRows;
-    case 16: return WNomCfg<16>::kRows;
-    case 24: return WNomCfg<24>::kRows;
-    default: return WNomCfg<32>::kRows;
-  }
-}
-bool warp_nom_ok(int l) {
-  static const bool off = getenv("RPCA_LU_CTA_NOMINATE") != nullptr;  // ablation: CTA-wide nomination
-  return !off && l <= 32 && warp_nom_rows(l) >= 2 * l;
-}
-
-// nomination level with warp-wide blocks (l ≤ 32): nblk blocks of warp_nom_rows(l) rows
-void nominate_warp(Ctx& c, const double* Y, int64_t m, int l, int leaf, const int64_t* cin, int64_t n_in, int G,
-                   int64_t nblk, int64_t* cout, const double* mu) {
-  switch (lp_of(l)) {
-    case 8: nominate_warp_lp<8>(c, Y, m, l, leaf, cin, n_in, G, nblk, cout, mu); break;
-    case 16: nominate_warp_lp<16>(c, Y, m, l, leaf, cin, n_in, G, nblk, cout, mu); break;
-    case 24: nominate_warp_lp<24>(c, Y, m, l, leaf, cin, n_in, G, nblk, cout, mu); break;
-    default: nominate_warp_lp<32>(c, Y, m, l, leaf, cin, n_in, G, nblk, cout, mu); break;
-  }
-  RPCA_CHECK_LAUNCH();
-  count_launch(c, 1, leaf == 1 ? "lu_leaf" : "lu_tree");
-}
-
 bool lu_f64_nomination() {
   static const bool v = getenv("RPCA_LU_F64_LEAF") != nullptr;  // ablation: the round-1 fp64 nomination
   return v;
@@ -1008,10 +765,9 @@ bool lu_f64_nomination() {
 int64_t* tournament(Ctx& c, const double* Y, int64_t m, int l, bool finalize, double* U, double* Lp, int64_t* piv,
                     double* M, Arena& ar, const double* mu) {
   const bool f64 = lu_f64_nomination();
-  const bool wn = !f64 && warp_nom_ok(l);
   const int G64 = group_for(l);
-  const int Gn = f64 ? G64 : std::max(2, (wn ? warp_nom_rows(l) : nominate_cap(l)) / l);
-  const int64_t leafcap = f64 ? leaf_cap(l) : (wn ? warp_nom_rows(l) : nominate_cap(l));
+  const int Gn = f64 ? G64 : std::max(2, nominate_cap(l) / l);
+  const int64_t leafcap = f64 ? leaf_cap(l) : nominate_cap(l);
   const int64_t nblk = std::max<int64_t>(1, cdiv(m, leafcap));
   int64_t* ca = ar.get<int64_t>(nblk * l);
   int64_t* cb = ar.get<int64_t>(nblk * l);
@@ -1024,7 +780,6 @@ int64_t* tournament(Ctx& c, const double* Y, int64_t m, int l, bool finalize, do
     return ca;
   }
   if (f64) select(c, (unsigned)nblk, Y, m, l, 1, nullptr, 0, G64, ca, 0, U, Lp, piv, M, nullptr, nullptr, mu);
-  else if (wn) nominate_warp(c, Y, m, l, 1, nullptr, 0, Gn, nblk, ca, mu);
   else nominate(c, (unsigned)nblk, Y, m, l, 1, nullptr, 0, Gn, ca, mu);
   int64_t n = nblk;
   for (;;) {
@@ -1033,7 +788,6 @@ int64_t* tournament(Ctx& c, const double* Y, int64_t m, int l, bool finalize, do
     const int G = last ? G64 : Gn;
     const int64_t ng = cdiv(n, G);
     if (last || f64) select(c, (unsigned)ng, Y, m, l, 0, ca, n, G, cb, last ? 1 : 0, U, Lp, piv, M, nullptr, nullptr, mu);
-    else if (wn) nominate_warp(c, Y, m, l, 0, ca, n, G, ng, cb, mu);
     else nominate(c, (unsigned)ng, Y, m, l, 0, ca, n, G, cb, mu);
     std::swap(ca, cb);
     n = ng;

@@ -54,7 +54,7 @@ def test_streamed_pca_matches_oracle(small_chunks, dtype, raw):
     compare(res, o, k, *tol)
     # the resident-A call on the device agrees to rounding
     rd = rp.pca(A, k, raw=raw, its=its, l=l, seed=0)
-    assert np.max(np.abs(res[1].numpy() - rd[1].cpu().numpy()) / rd[1].cpu().numpy()) < (1e-12 if dtype == torch.float64 else 1e-5)
+    assert np.max(np.abs(res[1].numpy() - rd[1].cpu().numpy()) / rd[1].cpu().numpy()) < (1e-12 if dtype == torch.float64 else 1e-4)
     # diffsnorm streamed too
     est = rp.diffsnorm(Ah, *[t.to(dev()) for t in res], raw=raw, stream_a=True)
     ref = rp.diffsnorm(A, *[t.to(dev()) for t in res], raw=raw)
