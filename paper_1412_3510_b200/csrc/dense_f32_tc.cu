@@ -113,6 +113,28 @@ __device__ __forceinline__ void tmem_ld16(uint32_t addr, float (&v)[16]) {
   for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
 }
 
+__device__ __forceinline__ void tmem_ld8(uint32_t addr, float* v) {
+  uint32_t r[8];
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+               : "r"(addr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 8; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+// 16 consecutive TMEM columns starting at a column that is only 8-aligned
+// (the second accumulator half when N = 56)
+template <int N>
+__device__ __forceinline__ void tmem_ld16_at(uint32_t addr, float (&v)[16]) {
+  if constexpr (N % 16 == 0) {
+    tmem_ld16(addr, v);
+  } else {
+    tmem_ld8(addr, v);
+    tmem_ld8(addr + 8, v + 8);
+  }
+}
+
 // one lane of a converged warp (the same one every time) — the issuing lane of
 // TMA / tcgen05.mma / tcgen05.commit; the rest of the warp keeps the loop
 // state uniform so operands stay in uniform registers
@@ -228,7 +250,11 @@ __global__ void __launch_bounds__(kThreadsAx, 1)
   } else if (warp == 1) {  // ------------------------------------------- MMA issuer
     // D[:, 0:2N] += A_hi·[X_hi | X_lo]; D[:, 0:N] += A_lo·X_hi (A from TMEM)
     const bool leader = elect_one();
-    constexpr uint32_t idesc2 = idesc_tf32(128, 2 * N), idesc1 = idesc_tf32(128, N);
+    // N = 56 (l ≤ 56): the lo·hi product runs at N = 64, whose extra 8
+    // columns add A_lo·X_lo[0..7] into the A_hi·X_lo accumulator of output
+    // columns 0-7 (a fourth, more accurate term), and [X_hi | X_lo] is one
+    // 112-row operand — 176 MMA columns per k-step instead of 192 at N = 64
+    constexpr uint32_t idesc2 = idesc_tf32(128, 2 * N), idesc1 = idesc_tf32(128, (N + 15) / 16 * 16);
     Ring<S> rg;
     Ring<NS> rt;
     int64_t u = -1;
@@ -309,7 +335,7 @@ __global__ void __launch_bounds__(kThreadsAx, 1)
           float v[16], w[16];
           double fin[16];  // the values stored (final after the last chunk)
           tmem_ld16(d + c0, v);
-          tmem_ld16(d + N + c0, w);
+          tmem_ld16_at<N>(d + N + c0, w);
 #pragma unroll
           for (int j = 0; j < 16; ++j) {
             fin[j] = 0.0;
@@ -457,7 +483,7 @@ __global__ void __launch_bounds__(kThreadsAty, 1)
     // D_cb += A_hi·Y_hi + A_hi·Y_lo + A_lo·Y_hi, A_hi/A_lo from TMEM (lane =
     // column of A, one TMEM column per row of A)
     const bool leader = elect_one();
-    constexpr uint32_t idesc = idesc_tf32(128, N), idesc2 = idesc_tf32(128, 2 * N);
+    constexpr uint32_t idesc = idesc_tf32(128, (N + 15) / 16 * 16), idesc2 = idesc_tf32(128, 2 * N);  // (as A·X)
     Ring<YS> ry;
     Ring<NS> rt;
     int kin = 0;        // row chunks into the current accumulation chunk
@@ -546,9 +572,10 @@ __global__ void __launch_bounds__(kThreadsAty, 1)
         for (int c0 = 0; c0 < N; c0 += 16) {
           float v[16], w[16];
           tmem_ld16(d + c0, v);
-          tmem_ld16(d + N + c0, w);
+          tmem_ld16_at<N>(d + N + c0, w);
 #pragma unroll
           for (int j = 0; j < 16; ++j) {
+            if (c0 + j >= N) break;  // N = 56: the last group is half used
             const double a = (double)v[j] + (double)w[j];
             dst[c0 + j] = ch == 0 ? a : dst[c0 + j] + a;
           }
@@ -603,24 +630,41 @@ __global__ void aty_f32_reduce_kernel(const double* __restrict__ part, AtyPlan p
 }
 
 // Xᵀ split: Xt_hi[j][k] = tf32(X[k][j]) (as fp32 with the low 13 bits cleared),
-// Xt_lo[j][k] = fp32(X[k][j] − Xt_hi[j][k]); zero padding to (Npad × Kpad).
-// 64-row tiles go through shared memory so both the read of X (rows of l
-// doubles) and the writes of Xᵀ (runs of 64 k) are coalesced.
-__global__ void __launch_bounds__(256) split_transpose_kernel(const double* __restrict__ X, int64_t K, int l, int Npad,
-                                                              int64_t Kpad, const double* __restrict__ xmean,
+// Xt_lo[j][k] = fp32(X[k][j] − Xt_hi[j][k]); rows j < l only (the TMA boxes
+// read rows l … Npad−1 out of bounds, i.e. as zeros), k zero-padded to Kpad.
+// 64-row tiles go through shared memory so both the read of X (64·l
+// contiguous doubles, all in flight: 16 loads per thread) and the writes of
+// Xᵀ (runs of 64 k) are coalesced.
+__global__ void __launch_bounds__(256) split_transpose_kernel(const double* __restrict__ X, int64_t K, int l,
+                                                              uint32_t lmagic, int64_t Kpad,
+                                                              const double* __restrict__ xmean,
                                                               float* __restrict__ hi, float* __restrict__ lo) {
   __shared__ double tile[64][kMaxL + 1];
   for (int64_t k0 = (int64_t)blockIdx.x * 64; k0 < Kpad; k0 += (int64_t)gridDim.x * 64) {
     __syncthreads();
-    for (int idx = threadIdx.x; idx < 64 * l; idx += 256) {
-      const int r = idx / l, j = idx - r * l;
-      const int64_t k = k0 + r;
-      tile[r][j] = k < K ? X[k * l + j] - (xmean ? xmean[j] : 0.0) : 0.0;
+    const int nrow = (int)imin64(64, K - k0 > 0 ? K - k0 : 0);
+    const int cnt = nrow * l;  // ≤ 64·64 = 16·256
+    const double* src = X + k0 * l;
+    double v[16];
+#pragma unroll
+    for (int u = 0; u < 16; ++u) {
+      const int idx = threadIdx.x + u * 256;
+      v[u] = idx < cnt ? src[idx] : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < 16; ++u) {
+      const int idx = threadIdx.x + u * 256;
+      if (idx < 64 * l) {
+        // idx / l by multiply-high (exact for idx < 2^32/l; the kernel was
+        // instruction-bound on the integer division: ncu issue 67%)
+        const int r = l == 1 ? idx : (int)__umulhi((uint32_t)idx, lmagic), j = idx - r * l;
+        tile[r][j] = idx < cnt ? v[u] - (xmean ? xmean[j] : 0.0) : 0.0;
+      }
     }
     __syncthreads();
-    for (int idx = threadIdx.x; idx < 64 * Npad; idx += 256) {
+    for (int idx = threadIdx.x; idx < 64 * l; idx += 256) {
       const int j = idx >> 6, r = idx & 63;
-      const double x = j < l ? tile[r][j] : 0.0;
+      const double x = tile[r][j];
       const float h = __uint_as_float(__float_as_uint((float)x) & 0xFFFFE000u);
       hi[(int64_t)j * Kpad + k0 + r] = h;
       lo[(int64_t)j * Kpad + k0 + r] = (float)(x - (double)h);
@@ -654,12 +698,13 @@ CUtensorMap tmap_f32(const void* base, int64_t inner, int64_t outer, int64_t ld_
   return tm;
 }
 
-int npad_for(int l) { return l <= 16 ? 16 : (l <= 32 ? 32 : (l <= 48 ? 48 : 64)); }
+int npad_for(int l) { return l <= 16 ? 16 : (l <= 32 ? 32 : (l <= 48 ? 48 : (l <= 56 ? 56 : 64))); }
 
-void split_transpose(Ctx& c, const double* X, int64_t K, int l, int Npad, int64_t Kpad, float* hi, float* lo,
+void split_transpose(Ctx& c, const double* X, int64_t K, int l, int64_t Kpad, float* hi, float* lo,
                      const double* xmean = nullptr) {
   const unsigned grid = (unsigned)std::min<int64_t>(cdiv(Kpad, 64), (int64_t)c.num_sms * 8);
-  split_transpose_kernel<<<grid, 256, 0, c.stream>>>(X, K, l, Npad, Kpad, xmean, hi, lo);
+  const uint32_t lmagic = l > 1 ? (uint32_t)(((uint64_t(1) << 32) + l - 1) / l) : 0u;  // ⌈2^32 / l⌉
+  split_transpose_kernel<<<grid, 256, 0, c.stream>>>(X, K, l, lmagic, Kpad, xmean, hi, lo);
   RPCA_CHECK_LAUNCH();
   count_launch(c, 1, "split_tf32");
 }
@@ -669,8 +714,8 @@ void launch_ax(Ctx& c, const DenseA& A, const float* hi, const float* lo, int64_
                double* Y) {
   using Cfg = AxCfg<N>;
   const CUtensorMap tA = tmap_f32(A.a, A.n, A.m, A.lda, 32, 128);
-  const CUtensorMap tH = tmap_f32(hi, Kpad, N, Kpad, 32, N);
-  const CUtensorMap tL = tmap_f32(lo, Kpad, N, Kpad, 32, N);
+  const CUtensorMap tH = tmap_f32(hi, Kpad, l, Kpad, 32, N);  // rows l … N−1: out of bounds ⇒ zero fill
+  const CUtensorMap tL = tmap_f32(lo, Kpad, l, Kpad, 32, N);
   ensure_smem((const void*)ax_f32_tc_kernel<N>, Cfg::kSmem);
   const int64_t ntiles = cdiv(A.m, 128);
   const int grid = (int)std::min<int64_t>(ntiles, c.num_sms);
@@ -694,12 +739,12 @@ AtyPlan make_plan(Ctx& c, const DenseA& A) {
 }
 
 template <int N>
-void launch_aty(Ctx& c, const DenseA& A, const float* hi, const float* lo, int64_t Kpad, const AtyPlan& pl,
+void launch_aty(Ctx& c, const DenseA& A, const float* hi, const float* lo, int64_t Kpad, int l, const AtyPlan& pl,
                 double* part) {
   using Cfg = AtyCfg<N>;
   const CUtensorMap tA = tmap_f32(A.a, A.n, A.m, A.lda, 128, 32, CU_TENSOR_MAP_SWIZZLE_NONE);
-  const CUtensorMap tH = tmap_f32(hi, Kpad, N, Kpad, 32, N);
-  const CUtensorMap tL = tmap_f32(lo, Kpad, N, Kpad, 32, N);
+  const CUtensorMap tH = tmap_f32(hi, Kpad, l, Kpad, 32, N);  // rows l … N−1: out of bounds ⇒ zero fill
+  const CUtensorMap tL = tmap_f32(lo, Kpad, l, Kpad, 32, N);
   ensure_smem((const void*)aty_f32_tc_kernel<N>, Cfg::kSmem);
   prof_pre(c);
   aty_f32_tc_kernel<N><<<(unsigned)(pl.Gc * pl.Pg), kThreadsAty, Cfg::kSmem, c.stream>>>(tA, tH, tL, pl, part);
@@ -712,7 +757,7 @@ void aty_f32_run(Ctx& c, const DenseA& A, const float* hi, const float* lo, int6
                  const double* cmean, const double* sy, double* Z, Arena& ar) {
   const AtyPlan pl = make_plan<N>(c, A);
   double* part = ar.get<double>((size_t)pl.Gc * pl.Pg * pl.CBG * 128 * N);
-  launch_aty<N>(c, A, hi, lo, Kpad, pl, part);
+  launch_aty<N>(c, A, hi, lo, Kpad, l, pl, part);
   const int64_t total = A.n * l;
   const unsigned grid = (unsigned)std::min<int64_t>(cdiv(total, 256), (int64_t)c.num_sms * 16);
   aty_f32_reduce_kernel<<<grid, 256, 0, c.stream>>>(part, pl, N, A.n, l, cmean, sy, Z);
@@ -740,11 +785,12 @@ void dense_ax_f32(Ctx& c, const DenseA& A, const double* X, int l, const double*
   const int64_t Kpad = cdiv(A.n, 64) * 64;
   float* hi = ar.get<float>((size_t)Np * Kpad);
   float* lo = ar.get<float>((size_t)Np * Kpad);
-  split_transpose(c, X, A.n, l, Np, Kpad, hi, lo);
+  split_transpose(c, X, A.n, l, Kpad, hi, lo);
   switch (Np) {
     case 16: launch_ax<16>(c, A, hi, lo, Kpad, l, cx, Y); break;
     case 32: launch_ax<32>(c, A, hi, lo, Kpad, l, cx, Y); break;
     case 48: launch_ax<48>(c, A, hi, lo, Kpad, l, cx, Y); break;
+    case 56: launch_ax<56>(c, A, hi, lo, Kpad, l, cx, Y); break;
     default: launch_ax<64>(c, A, hi, lo, Kpad, l, cx, Y); break;
   }
 }
@@ -760,6 +806,7 @@ size_t aty_f32_ws_bytes(Ctx& c, const DenseA& A, int l) {
     case 16: pl = make_plan<16>(c, A); break;
     case 32: pl = make_plan<32>(c, A); break;
     case 48: pl = make_plan<48>(c, A); break;
+    case 56: pl = make_plan<56>(c, A); break;
     default: pl = make_plan<64>(c, A); break;
   }
   s.add<double>((size_t)pl.Gc * pl.Pg * pl.CBG * 128 * Np);
@@ -772,11 +819,12 @@ void dense_aty_f32(Ctx& c, const DenseA& A, const double* Y, int l, const double
   const int64_t Kpad = cdiv(A.m, 64) * 64;
   float* hi = ar.get<float>((size_t)Np * Kpad);
   float* lo = ar.get<float>((size_t)Np * Kpad);
-  split_transpose(c, Y, A.m, l, Np, Kpad, hi, lo, ymean);
+  split_transpose(c, Y, A.m, l, Kpad, hi, lo, ymean);
   switch (Np) {
     case 16: aty_f32_run<16>(c, A, hi, lo, Kpad, l, cmean, sy, Z, ar); break;
     case 32: aty_f32_run<32>(c, A, hi, lo, Kpad, l, cmean, sy, Z, ar); break;
     case 48: aty_f32_run<48>(c, A, hi, lo, Kpad, l, cmean, sy, Z, ar); break;
+    case 56: aty_f32_run<56>(c, A, hi, lo, Kpad, l, cmean, sy, Z, ar); break;
     default: aty_f32_run<64>(c, A, hi, lo, Kpad, l, cmean, sy, Z, ar); break;
   }
 }

@@ -58,7 +58,7 @@ def test_streamed_pca_matches_oracle(small_chunks, dtype, raw):
     # diffsnorm streamed too
     est = rp.diffsnorm(Ah, *[t.to(dev()) for t in res], raw=raw, stream_a=True)
     ref = rp.diffsnorm(A, *[t.to(dev()) for t in res], raw=raw)
-    assert abs(est - ref) <= 1e-9 * ref
+    assert abs(est - ref) <= (1e-9 if dtype == torch.float64 else 1e-6) * ref  # fp32: chunked fp32 partial sums
     _ = nch
 
 
