@@ -635,25 +635,40 @@ __global__ void aty_f32_reduce_kernel(const double* __restrict__ part, AtyPlan p
 // 64-row tiles go through shared memory so both the read of X (64·l
 // contiguous doubles, all in flight: 16 loads per thread) and the writes of
 // Xᵀ (runs of 64 k) are coalesced.
-__global__ void __launch_bounds__(256) split_transpose_kernel(const double* __restrict__ X, int64_t K, int l,
+__global__ void __launch_bounds__(256, 2) split_transpose_kernel(const double* __restrict__ X, int64_t K, int l,
                                                               uint32_t lmagic, int64_t Kpad,
                                                               const double* __restrict__ xmean,
                                                               float* __restrict__ hi, float* __restrict__ lo) {
   __shared__ double tile[64][kMaxL + 1];
-  for (int64_t k0 = (int64_t)blockIdx.x * 64; k0 < Kpad; k0 += (int64_t)gridDim.x * 64) {
-    __syncthreads();
+  // the next tile's 16 loads per thread are issued before this tile's
+  // stores, so they are in flight while the stores run (the kernel was
+  // latency-bound on alternating load and store phases: ncu long scoreboard)
+  double v[16];
+  auto load = [&](int64_t k0) {
     const int nrow = (int)imin64(64, K - k0 > 0 ? K - k0 : 0);
     const int cnt = nrow * l;  // ≤ 64·64 = 16·256
-    const double* src = X + k0 * l;
-    double v[16];
+    const double* src = X + k0 * l;  // 512-byte aligned (k0 is a multiple of 64)
 #pragma unroll
-    for (int u = 0; u < 16; ++u) {
-      const int idx = threadIdx.x + u * 256;
-      v[u] = idx < cnt ? src[idx] : 0.0;
+    for (int u = 0; u < 8; ++u) {  // 16-byte loads: elements e, e+1 with e = 2·(tid + 256u)
+      const int e = 2 * (threadIdx.x + u * 256);
+      if (e + 1 < cnt) {
+        const double2 d = *reinterpret_cast<const double2*>(src + e);
+        v[2 * u] = d.x;
+        v[2 * u + 1] = d.y;
+      } else {
+        v[2 * u] = e < cnt ? src[e] : 0.0;
+        v[2 * u + 1] = 0.0;
+      }
     }
+    return cnt;
+  };
+  int64_t k0 = (int64_t)blockIdx.x * 64;
+  int cnt = k0 < Kpad ? load(k0) : 0;
+  for (; k0 < Kpad; k0 += (int64_t)gridDim.x * 64) {
+    __syncthreads();
 #pragma unroll
     for (int u = 0; u < 16; ++u) {
-      const int idx = threadIdx.x + u * 256;
+      const int idx = 2 * (threadIdx.x + (u >> 1) * 256) + (u & 1);
       if (idx < 64 * l) {
         // idx / l by multiply-high (exact for idx < 2^32/l; the kernel was
         // instruction-bound on the integer division: ncu issue 67%)
@@ -662,6 +677,8 @@ __global__ void __launch_bounds__(256) split_transpose_kernel(const double* __re
       }
     }
     __syncthreads();
+    const int64_t kn = k0 + (int64_t)gridDim.x * 64;
+    if (kn < Kpad) cnt = load(kn);
     for (int idx = threadIdx.x; idx < 64 * l; idx += 256) {
       const int j = idx >> 6, r = idx & 63;
       const double x = tile[r][j];

@@ -375,8 +375,32 @@ uint64_t ensure_transpose(Ctx& c, const rpca_mat* A) {
   return fp;
 }
 
-MatV device_view(Ctx& c, const rpca_mat* A, Arena& ar, Streamer* st = nullptr) {
+// A device dense A whose row stride (or base) the TMA pass kernels cannot
+// address — lda·s not a multiple of 16 bytes, e.g. an odd n in fp64 — would
+// fall to the CUDA-core fallback kernels (≈ 4× slower): the
+// drivers copy it once per call into a padded layout instead (one read and
+// one write of A at HBM speed, inside the call's graph).
+int64_t padded_lda(const rpca_mat* A) {
+  const int per16 = 16 / elem_size(A->dtype);
+  return (A->lda + per16 - 1) / per16 * per16;
+}
+bool needs_pad(const rpca_mat* A) {
+  if (A->kind != RPCA_DENSE || A->location != RPCA_DEVICE || A->m_local == 0) return false;
+  static const bool off = getenv("RPCA_NO_PAD") != nullptr;  // ablation: the CUDA-core fallback
+  return !off && (((A->lda * elem_size(A->dtype)) % 16) != 0 || (reinterpret_cast<uintptr_t>(A->a) & 15u) != 0);
+}
+
+MatV device_view(Ctx& c, const rpca_mat* A, Arena& ar, Streamer* st = nullptr, bool pad = true) {
   MatV v = probe_of(A);
+  if (pad && needs_pad(A)) {
+    const int es = elem_size(A->dtype);
+    const int64_t ld = padded_lda(A);
+    char* dev = ar.get<char>((size_t)A->m_local * ld * es);
+    copy_rows(c, A->a, A->lda, dev, ld, A->m_local, A->n, es);  // (cudaMemcpy2D: 1.9 ms for C2's 3.2 GB)
+    v.d.a = dev;
+    v.d.lda = ld;
+    return v;
+  }
   if (st && streamed(c, A)) {
     if (!c.h2d) {
       RPCA_CUDA(cudaStreamCreateWithFlags(&c.h2d, cudaStreamNonBlocking));
@@ -428,6 +452,7 @@ MatV device_view(Ctx& c, const rpca_mat* A, Arena& ar, Streamer* st = nullptr) {
 
 // arena bytes device_view takes for a host A (+ the transpose scratch of a host CSR)
 size_t host_copy_bytes(const Ctx& c, const rpca_mat* A) {
+  if (needs_pad(A)) return (size_t)A->m_local * padded_lda(A) * elem_size(A->dtype) + 256;
   if (A->location != RPCA_HOST) return 0;
   if (streamed(c, A))
     return 2 * Arena::align((size_t)std::min<int64_t>(A->m_local, stream_chunk_rows(A)) * A->lda *
@@ -836,7 +861,7 @@ void apply_step(Ctx& c, const rpca_mat* Am, const double* cm, int adjoint, const
   RPCA_REQUIRE(l >= 1 && l <= kMaxL && X && Y, RPCA_E_SHAPE, "apply: bad l / NULL X, Y");
   ensure_transpose(c, Am);
   const MatV probe = probe_of(Am);
-  Arena ar = c.arena(op_ws(c, probe, (int)l) + 65536);
+  Arena ar = c.arena(op_ws(c, probe, (int)l) + host_copy_bytes(c, Am) + 65536);
   const MatV A = device_view(c, Am, ar);
   const bool sh = check_shard(c, Am);
   profiled_step(c, [&] {
@@ -858,7 +883,7 @@ void apply_emu_step(Ctx& c, const rpca_mat* Am, const double* X, int64_t l, doub
   const MatV probe = probe_of(Am);
   RPCA_REQUIRE(!probe.csr && emu_eligible(probe.d, (int)l), RPCA_E_NOTIMPL,
                "apply_int8emu: needs a dense fp64 A (m ≥ 128, n ≥ 32) and 24 < l ≤ 48");
-  Arena ar = c.arena(op_ws(c, probe, (int)l) + (size_t)probe.m * 4 + 65536);  // = the RPCA_OP_APPLY query
+  Arena ar = c.arena(op_ws(c, probe, (int)l) + (size_t)probe.m * 4 + host_copy_bytes(c, Am) + 65536);
   const MatV A = device_view(c, Am, ar);
   int* E = ar.get<int>(A.d.m);
   profiled_step(c, [&] {
@@ -873,7 +898,7 @@ void colmeans_step(Ctx& c, const rpca_mat* Am, double* cm) {
   RPCA_REQUIRE(Am->location == RPCA_DEVICE && cm, RPCA_E_ARG, "colmeans: device A and c only");
   ensure_transpose(c, Am);
   const MatV probe = probe_of(Am);
-  Arena ar = c.arena((size_t)(cdiv(probe.m, 8192) + 2) * probe.n * 8 + 65536);
+  Arena ar = c.arena((size_t)(cdiv(probe.m, 8192) + 2) * probe.n * 8 + host_copy_bytes(c, Am) + 65536);
   const MatV A = device_view(c, Am, ar);
   colmeans(c, A, Am->m, cm, ar, check_shard(c, Am));
 }
@@ -1330,7 +1355,7 @@ size_t workspace_query(Ctx& c, int op, const rpca_mat* Am, int64_t k, int64_t l,
     case RPCA_OP_APPLY:
       RPCA_REQUIRE(l >= 1 && l <= kMaxL, RPCA_E_SHAPE, "bad l");
       arena = std::max(op_ws(c, probe_of(Am), (int)l) + (size_t)Am->m_local * 4,
-                       (size_t)(cdiv(Am->m_local, 8192) + 2) * Am->n * 8) + 65536;
+                       (size_t)(cdiv(Am->m_local, 8192) + 2) * Am->n * 8) + host_copy_bytes(c, Am) + 65536;
       break;
     default: RPCA_REQUIRE(false, RPCA_E_ARG, "bad op %d", op);
   }

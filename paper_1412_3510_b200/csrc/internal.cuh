@@ -227,6 +227,8 @@ void right_mult(Ctx& c, const double* In, const double* Q, const double* nu, con
 void rank_k_sub(Ctx& c, double* y, const double* U, int64_t ldu, const double* t, int64_t rows, int k);
 // t ← t ⊙ S
 void hadamard(Ctx& c, double* t, const double* S, int k);
+// dst (rows × cols, ld ldd) ← src (ld lds), elements of es bytes (4 or 8)
+void copy_rows(Ctx& c, const void* src, int64_t lds, void* dst, int64_t ldd, int64_t rows, int64_t cols, int es);
 // Z[i] += W[i]
 void add_into(Ctx& c, double* Z, const double* W, int64_t count);
 // *flag = 1 if any of x[0..count) is NaN or ±Inf (flag untouched otherwise)

@@ -341,6 +341,37 @@ void weighted_colsum(Ctx& c, const double* a, const double* X, int64_t rows, int
   count_launch(c, 2);
 }
 
+// dst rows (ld ldd elements) ← src rows (ld lds): a warp per row, 4-byte
+// words, coalesced (the source rows are only 4- or 8-byte aligned)
+__global__ void copy_rows_kernel(const uint32_t* __restrict__ src, int64_t lds, uint32_t* __restrict__ dst,
+                                 int64_t ldd, int64_t rows, int64_t wpr) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t r = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); r < rows; r += warps) {
+    const uint32_t* s = src + r * lds;
+    uint32_t* d = dst + r * ldd;
+    int64_t t = lane;
+    for (; t + 96 < wpr; t += 128) {  // four loads in flight
+      const uint32_t a = s[t], b = s[t + 32], c = s[t + 64], e = s[t + 96];
+      d[t] = a;
+      d[t + 32] = b;
+      d[t + 64] = c;
+      d[t + 96] = e;
+    }
+    for (; t < wpr; t += 32) d[t] = s[t];
+  }
+}
+
+void copy_rows(Ctx& c, const void* src, int64_t lds, void* dst, int64_t ldd, int64_t rows, int64_t cols, int es) {
+  if (rows == 0) return;
+  const int64_t w = es / 4;
+  const unsigned grid = (unsigned)std::min<int64_t>(cdiv(rows, 8), (int64_t)c.num_sms * 16);
+  copy_rows_kernel<<<grid, 256, 0, c.stream>>>(static_cast<const uint32_t*>(src), lds * w, static_cast<uint32_t*>(dst),
+                                               ldd * w, rows, cols * w);
+  RPCA_CHECK_LAUNCH();
+  count_launch(c, 1, "pad_copy");
+}
+
 __global__ void add_into_kernel(double* __restrict__ Z, const double* __restrict__ W, int64_t count) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count; i += (int64_t)gridDim.x * blockDim.x)
     Z[i] += W[i];

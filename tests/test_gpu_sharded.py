@@ -248,6 +248,30 @@ def test_sharded_eigens(variant, P):
     assert cluster_sin_angle(Uo, U, lo, k) < 1e-8
 
 
+@pytest.mark.parametrize("P", [2, 3])
+def test_sharded_reig(P):
+    """reig (§8(f) N1) on virtual ranks: the uniform row partition of a
+    symmetric indefinite A, λ replicated bit for bit, U by shards."""
+    n, k, l = 1537, 12, 16
+    lam_t = (-1.0) ** torch.arange(n, dtype=torch.float64) * torch.arange(1, n + 1, dtype=torch.float64) ** -1.5
+    V = synth.haar_columns(n, n, 99, device=dev())
+    A = (V * lam_t.to(dev())) @ V.T
+    A = (0.5 * (A + A.T)).contiguous()
+    Uo, lo = oracle.reig(A.cpu().numpy(), k, its=2, l=l, seed=0)
+
+    def fn(r):
+        r0, ml = rp.uniform_shard(n, P, r)
+        U, lam = rp.reig(A[r0:r0 + ml].contiguous(), k, its=2, l=l, seed=0, m_total=n, row0=r0)
+        return U.cpu().numpy(), lam.cpu().numpy()
+
+    res = run_ranks(P, fn)
+    for r in range(1, P):
+        assert np.array_equal(res[r][1], res[0][1])
+    U, lam = np.concatenate([x[0] for x in res]), res[0][1]
+    assert np.max(np.abs(lam - lo) / np.abs(lo)) < 1e-10
+    assert cluster_sin_angle(Uo, U, np.abs(lo), k) < 1e-8
+
+
 def test_sharded_apply_and_colmeans():
     m, n, l, P = 3001, 517, 22, 3
     g = torch.Generator(device="cuda").manual_seed(5)
