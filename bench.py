@@ -162,6 +162,16 @@ def plan_shard(cfg, ws, rank):
     return {"scaling": "strong", "m_total": cfg.m, "row0": row0, "m_local": min(pad, cfg.m - row0)}
 
 
+def sum_over_ranks(x, ws, device):
+    """sum of a per-rank number over the process group (identity at ws = 1)."""
+    if ws == 1:
+        return float(x)
+    import torch.distributed as dist
+    t = torch.tensor([float(x)], device=device, dtype=torch.float64)
+    dist.all_reduce(t)
+    return float(t.item())
+
+
 def max_over_ranks(x, ws, device):
     """max of a per-rank float over the process group (identity at ws = 1)."""
     if ws == 1:
@@ -320,7 +330,8 @@ def reference_arm(args):
     what = (f"leading {ms}x{ms} block" if cfg.op == "eigens" else f"leading {ms} of {cfg.m} rows")
     line = {"impl": "reference", "metric": "rank-k PCA wall time (s)", "value": v, "unit": "s",
             "n_gpus": ws, "steps": args.steps, "warmup": args.warmup, "ms_per_step": v * 1e3,
-            "higher_is_better": False, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "higher_is_better": False, "scaling": "strong", "vs_baseline": None,
+            "dtype": "f64" if cfg.dtype == torch.float64 else "f32",
             "data": "synthetic", "config": conf,
             "cpu_baseline": {"value": v, "unit": "s", "cores": oracle.num_threads(), "cpu_model": cpu_model(),
                              "kind": "oracle",
@@ -385,6 +396,7 @@ def main():
     ms_total = e0.elapsed_time(e1)
     launches = rp.launch_count() - launches0
     t_step = max_over_ranks(ms_total / 1e3 / args.steps, ws, dev)
+    a_total = sum_over_ranks(abytes, ws, dev)  # all shards' bytes (strong scaling: the global A)
 
     # per-kernel breakdown: the same K steps again with an event behind every
     # launch (reported as "kernels"; not part of the timed region)
@@ -431,8 +443,9 @@ def main():
         roof["all_passes"] = {"launches_per_step": sum(v[0] for v in passes_k.values()) // args.steps,
                               "gbs_per_pass": round(abytes * passes / (all_pass_ms / 1e3) / 1e9, 1)}
         if ws > 1:  # whole-job A-streaming rate: all shards' bytes over the step time
-            roof["aggregate"] = {"gbs_per_pass_step": round(abytes * ws * passes / t_step / 1e9, 1),
-                                 "peak": hbm * ws, "frac": round(abytes * passes / t_step / 1e9 / hbm, 4)}
+            total = sum_over_ranks(abytes, ws, dev)
+            roof["aggregate"] = {"gbs_per_pass_step": round(total * passes / t_step / 1e9, 1),
+                                 "peak": hbm * ws, "frac": round(total * passes / t_step / 1e9 / (hbm * ws), 4)}
     breakdown = {k: {"launches_per_step": v[0] / args.steps, "ms_per_step": round(v[1] / args.steps, 5)}
                  for k, v in sorted(kern_all.items(), key=lambda kv: -kv[1][1])}
 
@@ -452,7 +465,8 @@ def main():
             out = run_step(rp, cfg, Ah, plan)
         te = max_over_ranks((time.perf_counter() - t0) / ne, ws, dev)
         d2h = sum(o.numel() * o.element_size() for o in out)
-        e2e = {"value": te, "unit": "s", "h2d_bytes_per_step": abytes * ws, "d2h_bytes_per_step": d2h * ws,
+        e2e = {"value": te, "unit": "s", "h2d_bytes_per_step": int(sum_over_ranks(abytes, ws, dev)),
+               "d2h_bytes_per_step": int(sum_over_ranks(d2h, ws, dev)),
                "note": "host-pinned A (shard) copied H2D and the factors copied D2H inside each library call"
                        + ("" if isinstance(A, torch.Tensor) else "; CSR(A^T) rebuilt on the device per call")
                        + "; host wall clock, max over ranks"}
@@ -473,7 +487,7 @@ def main():
                 "kernels_note": "per-launch CUDA events in a second, untimed run of the same steps",
                 "roofline_time_s": abytes * passes / (hbm * 1e9)}
         if ws > 1:
-            line["a_bytes_total"] = abytes * ws
+            line["a_bytes_total"] = a_total
         print(json.dumps(line), flush=True)
     if ws > 1:
         import torch.distributed as dist
