@@ -549,3 +549,23 @@ def test_pca_renorm_odd_vs_oracle(m, n, k, l, its, raw):
         rp.pca(A, k, raw=raw, its=its, l=l, seed=4, renorm_odd=True)
         torch.cuda.synchronize()
     assert p2.total("lu_leaf")[0] < p1.total("lu_leaf")[0]
+
+
+def test_csr_large_operand_spmm():
+    """A gathered operand X of 102 MB (n = 400000, l = 32, near the L2 size):
+    A·X against the oracle elementwise and the whole PCA at the fp64
+    tolerances."""
+    m, n, l = 600000, 400000, 32
+    A, host = csr_case(m, n, seed=13, planted_rows=m // 100)
+    g = torch.Generator(device="cuda").manual_seed(3)
+    X = torch.randn(n, l, generator=g, device=dev(), dtype=torch.float64)
+    got = rp.apply(A, X).cpu().numpy()
+    ref = oracle.apply(host, X.cpu().numpy())
+    rp_, ci, va, _ = host
+    absA_X = np.zeros_like(ref)
+    Xa = np.abs(X.cpu().numpy())
+    rows = np.repeat(np.arange(m), np.diff(rp_))
+    np.add.at(absA_X, rows, np.abs(va)[:, None] * Xa[ci])
+    assert np.all(np.abs(got - ref) <= 2 * gamma(256) * absA_X + 1e-300)
+    res = rp.pca(A, 30, its=2, l=32, seed=0)
+    compare(res, oracle.pca(host, 30, its=2, l=32, seed=0), 30)
