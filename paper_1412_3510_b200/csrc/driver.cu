@@ -341,8 +341,6 @@ void build_transpose(Ctx& c, CsrA& src, int64_t n, char* mem, Arena& scratch, Cs
                      const CsrLayout& L) {
   T = CsrA{reinterpret_cast<int64_t*>(mem), reinterpret_cast<int32_t*>(mem + L.b_ptr), mem + L.b_ptr + L.b_idx,
            src.dtype, n, src.nnz};
-  T.ncols = src.rows;
-  src.ncols = n;
   csr_transpose(c, src, n, T, scratch);
   char* plans = mem + L.b_ptr + L.b_idx + L.b_val;
   csr_build_heavy_plan(c, src, plans, host_ptr);

@@ -59,7 +59,6 @@ struct CsrA {
   const void* vals;
   int dtype;
   int64_t rows, nnz;
-  int64_t ncols = 0;  // columns (= rows of the gathered operand); 0 if unknown
   // heavy-row plan (csr.cu, built once per matrix and cached): rows with more
   // than kHeavyNnz nonzeros are cut into chunks, one warp each, whose partial
   // rows are summed in ascending chunk order.  hc[c] = (row, t0, t1);
