@@ -405,7 +405,6 @@ __global__ void __launch_bounds__(kThreads, SelCfg<LP, RR>::kMinBlocks)
 // whatever the fp64 magnitudes.  A column whose remaining values are all
 // below 2^-100 of its block maximum counts as zero (no elimination).
 
-__device__ __forceinline__ uint32_t piv_key32(float v) { return (__float_as_uint(v) & 0x7FFFFFFFu) >> 3; }
 
 template <int LP, int W>
 __device__ __forceinline__ void trail_update32(float (&w)[LP], const float (*u12)[LP], int ns) {
@@ -432,8 +431,7 @@ __global__ void __launch_bounds__(kThreads, 2)
   constexpr int CAP = kThreads * R;
   __shared__ int64_t ids[CAP];
   __shared__ int setcnt[CAP + 1];
-  __shared__ uint2 slot[2][kWarps];
-  __shared__ float suinv[2][kWarps];
+  __shared__ uint32_t slot[2][kWarps];  // each warp's winning packed key
   __shared__ __align__(16) float pbuf[2][kWarps][8];
   __shared__ float traw[8][LP];
   __shared__ float l11[8][8];
@@ -544,7 +542,16 @@ __global__ void __launch_bounds__(kThreads, 2)
   for (int q = 0; q < R; ++q)
 #pragma unroll
     for (int t = 0; t < LP; ++t) w[q][t] = (act[q] && t < l) ? stage[(tid * R + q) * sl + t] : 0.f;
-  // blocked GEPP in 8-column panels — the fp64 kernel's scheme (lu_select_kernel)
+  // blocked GEPP in 8-column panels — the fp64 kernel's scheme (lu_select_kernel).
+  // The pivot key packs the value and the row: bits [RB, 32) hold
+  // (|v|'s bits ≫ RB) + 1 (a 2^-(23-RB)-relative comparison, RB = log2 CAP),
+  // bits [0, RB) hold CAP−1−row, so ONE unsigned max gives the largest |v|
+  // and, among equal keys, the lowest row — no ballot / find-first per level.
+  // Every warp publishes its winner's whole panel (two 16-byte stores).
+  constexpr int RB = CAP <= 256 ? 8 : (CAP <= 512 ? 9 : 10);
+  auto packed_key = [&](float v, int row) -> uint32_t {
+    return ((((__float_as_uint(v) & 0x7FFFFFFFu) >> RB) + 1u) << RB) | (uint32_t)(CAP - 1 - row);
+  };
   for (int pb = 0; pb < steps; pb += 8) {
     const int ns = min(8, steps - pb);
 #pragma unroll
@@ -552,35 +559,31 @@ __global__ void __launch_bounds__(kThreads, 2)
       if (s >= ns) break;
       const int j = pb + s;
       uint32_t best = 0;
-      int bq = 0;
 #pragma unroll
       for (int q = 0; q < R; ++q)
-        if (act[q]) {
-          const uint32_t k = piv_key32(w[q][s]) + 1u;
-          if (k > best) { best = k; bq = q; }
-        }
+        if (act[q]) best = max(best, packed_key(w[q][s], tid * R + q));
       const uint32_t mk = __reduce_max_sync(0xffffffffu, best);
-      const int wl = __ffs(__ballot_sync(0xffffffffu, best == mk)) - 1;
-      if (lane == wl) {
+      if (best == mk && mk != 0u) {  // the (unique) winning lane of this warp
+        const int bq = (int)(CAP - 1 - (mk & (CAP - 1))) - tid * R;
 #pragma unroll
         for (int q = 0; q < R; ++q)
           if (q == bq) {
-            slot[j & 1][warp] = make_uint2(mk, (uint32_t)(tid * R + q));
-            const float pv = w[q][s];
-            float rc;  // MUFU reciprocal (nomination only needs ~1 ulp); tiny pivot ⇒ a zero column
-            asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(rc) : "f"(pv));
-            suinv[j & 1][warp] = fabsf(pv) >= 0x1p-100f ? rc : 0.f;
-#pragma unroll
-            for (int t = s; t < 8; ++t) pbuf[j & 1][warp][t] = w[q][t];
+            float4* pb4 = reinterpret_cast<float4*>(pbuf[j & 1][warp]);
+            pb4[0] = make_float4(w[q][0], w[q][1], w[q][2], w[q][3]);
+            pb4[1] = make_float4(w[q][4], w[q][5], w[q][6], w[q][7]);
           }
       }
+      if (lane == 0) slot[j & 1][warp] = mk;
       __syncthreads();
-      const uint32_t kv = lane < kWarps ? slot[j & 1][lane].x : 0u;
+      const uint32_t kv = lane < kWarps ? slot[j & 1][lane] : 0u;
       const uint32_t gk = __reduce_max_sync(0xffffffffu, kv);
-      const int ww = __ffs(__ballot_sync(0xffffffffu, kv == gk)) - 1;
-      const int p = (int)slot[j & 1][ww].y;
-      const float uinv = suinv[j & 1][ww];
+      const int p = (int)(CAP - 1 - (gk & (CAP - 1)));
+      const int ww = p / (32 * R);  // the warp that holds row p
       const float* prow = pbuf[j & 1][ww];
+      const float pv = prow[s];
+      float rc;  // MUFU reciprocal (nomination only needs ~1 ulp); tiny pivot ⇒ a zero column
+      asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(rc) : "f"(pv));
+      const float uinv = fabsf(pv) >= 0x1p-100f ? rc : 0.f;
       if (tid == 0) piv[j] = p;
 #pragma unroll
       for (int q = 0; q < R; ++q) {
