@@ -202,11 +202,13 @@ def make_input(cfg, device, rp=None, plan=None):
             t0, t1 = int(rowptr[r0]), int(rowptr[r1])
             rowptr = (rowptr[r0:r1 + 1] - t0).contiguous()
             colind, vals = colind[t0:t1].clone(), vals[t0:t1].clone()
-        torch.cuda.synchronize()
+        if device.type == "cuda":
+            torch.cuda.synchronize()
         return rp.CSR(rowptr, colind, vals, (r1 - r0, cfg.n))
     if (r0, r1) != (0, cfg.m):
         A = A[r0:r1].clone()
-    torch.cuda.synchronize()
+    if device.type == "cuda":
+        torch.cuda.synchronize()
     return A
 
 

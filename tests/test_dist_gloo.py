@@ -98,3 +98,49 @@ def test_sharded_schedule_matches_oracle(m, n, k, l, its, raw, cut):
     assert cluster_sin_angle(Vo, V, So, k) < 1e-8
     # the sign convention is global: U·diag(S)·Vᵀ agrees entrywise
     assert np.allclose((U * S) @ V.T, (Uo * So) @ Vo.T, atol=1e-10 * So[0])
+
+
+# ------------------------------------------------------------------ bench inputs per rank
+class _FakeRp:
+    """Stands in for the binding's CSR container on a CPU-only box."""
+
+    class CSR:
+        def __init__(self, rowptr, colind, vals, shape):
+            self.rowptr, self.colind, self.vals, self.shape = rowptr, colind, vals, tuple(shape)
+
+
+@pytest.mark.parametrize("ws", [2, 3])
+def test_bench_shards_reassemble_the_global_matrix(ws, monkeypatch):
+    """bench.make_input at N > 1 (strong scaling): every rank's rows of the
+    global seeded matrix, dense and CSR — concatenated they are the 1-rank
+    input bit for bit (small versions of C2 and C5 on the CPU)."""
+    import synth as sy
+    monkeypatch.setitem(sy.CONFIGS, "C2", sy.Config("C2", "dense", torch.float64, 1001, 57, 5, 7, 1, True, "pca",
+                                                    "small C2"))
+    monkeypatch.setitem(sy.CONFIGS, "C5", sy.Config("C5", "csr", torch.float64, 3001, 700, 5, 7, 1, True, "pca",
+                                                    "small C5"))
+
+    def small_make(name, device="cpu", **kw):
+        if name == "C2":
+            return sy.make_c2(m=1001, n=57, device=device, **kw)
+        return sy.make_c5(m=3001, n=700, device=device, planted_rows=30, planted_cols=50, **kw)
+
+    monkeypatch.setattr(sy, "make", small_make)
+    dev = torch.device("cpu")
+    for name in ("C2", "C5"):
+        cfg = sy.CONFIGS[name]
+        parts = [bench.make_input(cfg, dev, _FakeRp, bench.plan_shard(cfg, ws, r)) for r in range(ws)]
+        whole = small_make(name)
+        if name == "C2":
+            assert torch.equal(torch.cat(parts), whole)
+        else:
+            rp_, ci, va = whole
+            got_ci = torch.cat([p.colind for p in parts])
+            got_va = torch.cat([p.vals for p in parts])
+            assert torch.equal(got_ci, ci) and torch.equal(got_va, va)
+            offs = [0]
+            for p in parts:
+                assert int(p.rowptr[0]) == 0
+                offs.append(offs[-1] + int(p.rowptr[-1]))
+            rebuilt = torch.cat([parts[0].rowptr] + [p.rowptr[1:] + o for p, o in zip(parts[1:], offs[1:-1])])
+            assert torch.equal(rebuilt, rp_)
