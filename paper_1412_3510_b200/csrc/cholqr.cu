@@ -250,14 +250,14 @@ void orthonormalize(Ctx& c, double* Y, int64_t m, int l, double* R_out, Arena& a
   ar.off = mark;
   chol(c, G, l, U, 0, M1, R1, breakdown_flag(c));  // R1·U
   c.tag = "cholqr_trmm";
-  dense_ax(c, Yd, M1, l, Y, ar);           // Q1 = L·R1⁻¹
+  dense_ax(c, Yd, M1, l, Y, ar, nullptr, true);  // Q1 = L·R1⁻¹
   ar.off = mark;
   c.tag = "cholqr_gram";
   gram(c, Y, Y, m, l, G, ar);              // G = Q1ᵀQ1
   ar.off = mark;
   chol(c, G, l, R1, 1, M2, R2);            // R = D·R2·R1·U
   c.tag = "cholqr_trmm";
-  dense_ax(c, Yd, M2, l, Y, ar);           // Q = Q1·R2⁻¹·D
+  dense_ax(c, Yd, M2, l, Y, ar, nullptr, true);  // Q = Q1·R2⁻¹·D
   ar.off = mark;
   if (R_out) RPCA_CUDA(cudaMemcpyAsync(R_out, R2, sizeof(double) * l * l, cudaMemcpyDeviceToDevice, c.stream));
 }
@@ -287,7 +287,7 @@ void orthonormalize_sharded(Ctx& c, double* Y, int64_t m, int64_t row0, int l, d
   };
   auto trmm = [&](const double* Mx) {
     c.tag = "cholqr_trmm";
-    if (m > 0) dense_ax(c, Yd, Mx, l, Y, ar);
+    if (m > 0) dense_ax(c, Yd, Mx, l, Y, ar, nullptr, true);
     ar.off = mark;
   };
   TagScope ts(c, "cholqr_gram");

@@ -17,6 +17,8 @@
 // multiple of 16): CUDA-core kernel with the same result contract.
 #include <cudaTypedefs.h>
 
+#include <type_traits>
+
 #include "internal.cuh"
 
 namespace rpca {
@@ -61,7 +63,10 @@ struct AxSplit {
   }
 };
 
-template <int NT>
+// UPPER: X is upper triangular (the thin products Y·U⁻¹ of the LU and the
+// Cholesky-QR): a k-step whose smallest k exceeds an n-tile's last column
+// only multiplies zeros there and is skipped (43% of the DMMAs at l = 52).
+template <int NT, bool UPPER>
 __global__ void __launch_bounds__(kThreads, 1)
     ax_f64_tma_kernel(const __grid_constant__ CUtensorMap tmA, const double* __restrict__ Xp, int64_t m, int l,
                       AxSplit sp, const double* __restrict__ cx, double* __restrict__ Y, double* __restrict__ part) {
@@ -124,7 +129,11 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
       for (int nt = 0; nt < NT; ++nt) acc[mt][nt][0] = acc[mt][nt][1] = 0.0;
 
-    for (; kb < kend; ++kb, ++u) {
+    // one k-block of DMMAs; KBS = the k-block index when it is static (the
+    // UPPER kernels: K = l ≤ 64, two k-blocks), so the zero-block skips fold
+    // at compile time, else −1
+    auto kblock = [&](auto KBS) {
+      constexpr int kbs = decltype(KBS)::value;
       mbar_wait(&full[s], ph);
       const uint8_t* As = smem + s * Cfg::kStageBytes;
       const double* Xs = reinterpret_cast<const double*>(As + Cfg::kABytes);
@@ -143,6 +152,8 @@ __global__ void __launch_bounds__(kThreads, 1)
           const int st = 2 * q + ss;
 #pragma unroll
           for (int nt = 0; nt < NT; ++nt) {
+            // X[k][n-tile] = 0 for every k of this k-step (smallest k > the tile's last column)
+            if (kbs >= 0 && kbs * BK + 16 * (q >> 1) + 2 * (q & 1) + ss > nt * 8 + 7) continue;
             const double b = Xs[(st * NT + nt) * 32 + lane];
             dmma(acc[0][nt], ss ? a[0].y : a[0].x, b);
             dmma(acc[1][nt], ss ? a[1].y : a[1].x, b);
@@ -152,6 +163,15 @@ __global__ void __launch_bounds__(kThreads, 1)
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[s]);
       if (++s == Cfg::kStages) { s = 0; ph ^= 1; }
+    };
+    for (; kb < kend; ++kb, ++u) {
+      if constexpr (UPPER) {
+        if (kb == 0) kblock(std::integral_constant<int, 0>{});
+        else if (kb == 1) kblock(std::integral_constant<int, 1>{});
+        else kblock(std::integral_constant<int, -1>{});
+      } else {
+        kblock(std::integral_constant<int, -1>{});
+      }
     }
     // epilogue: D rows = lane>>2, cols 2·(lane&3) + {0,1}
     double* dst = Y;
@@ -198,7 +218,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 // covering CTAs in ascending order and writes its rows of Y.
 __global__ void ax_fixup_kernel(AxSplit sp, int64_t m, int l, int LP, const double* __restrict__ part,
                                 const double* __restrict__ cx, double* __restrict__ Y) {
-  __shared__ int64_t t_s, pa_s;
+  __shared__ int64_t t_s;
   __shared__ int nq_s;
   __shared__ const double* src[32];  // the covering CTAs' partial slots, ascending
   if (threadIdx.x == 0) {
@@ -247,7 +267,6 @@ __global__ void ax_fixup_kernel(AxSplit sp, int64_t m, int l, int LP, const doub
       if (idx < nrow * l) yt[idx] = cx ? s[e] - cx[idx % l] : s[e];
     }
   }
-  (void)pa_s;
 }
 
 // Generic CUDA-core fallback: 64-row tiles, X and A chunks staged in smem (fp64).
@@ -309,7 +328,8 @@ PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
 }
 
 template <int NT>
-void launch_ax_tma(Ctx& c, const DenseA& A, const double* Xp, int l, const double* cx, double* Y, double* part) {
+void launch_ax_tma(Ctx& c, const DenseA& A, const double* Xp, int l, const double* cx, double* Y, double* part,
+                   bool upper) {
   using Cfg = AxCfg<NT>;
   CUtensorMap tm;
   cuuint64_t dims[2] = {(cuuint64_t)A.n, (cuuint64_t)A.m};
@@ -320,7 +340,8 @@ void launch_ax_tma(Ctx& c, const DenseA& A, const double* Xp, int l, const doubl
                             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   RPCA_REQUIRE(r == CUDA_SUCCESS, RPCA_E_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
-  ensure_smem((const void*)ax_f64_tma_kernel<NT>, Cfg::kSmem);
+  ensure_smem((const void*)ax_f64_tma_kernel<NT, false>, Cfg::kSmem);
+  ensure_smem((const void*)ax_f64_tma_kernel<NT, true>, Cfg::kSmem);
   const int64_t ntiles = cdiv(A.m, BM);
   const int KB = (int)cdiv(A.n, BK);
   AxSplit sp;
@@ -343,7 +364,10 @@ void launch_ax_tma(Ctx& c, const DenseA& A, const double* Xp, int l, const doubl
   bool split = false;  // does any CTA boundary cut a tile?
   for (int64_t q = 1; q < sp.P && !split; ++q) split = sp.u0(q) % KB != 0;
   prof_pre(c);
-  ax_f64_tma_kernel<NT><<<(unsigned)sp.P, kThreads, Cfg::kSmem, c.stream>>>(tm, Xp, A.m, l, sp, cx, Y, part);
+  if (upper)
+    ax_f64_tma_kernel<NT, true><<<(unsigned)sp.P, kThreads, Cfg::kSmem, c.stream>>>(tm, Xp, A.m, l, sp, cx, Y, part);
+  else
+    ax_f64_tma_kernel<NT, false><<<(unsigned)sp.P, kThreads, Cfg::kSmem, c.stream>>>(tm, Xp, A.m, l, sp, cx, Y, part);
   RPCA_CHECK_LAUNCH();
   count_launch(c, 1, c.tag ? c.tag : "ax_f64_dmma");
   if (split && sp.P > 1) {
@@ -368,7 +392,7 @@ size_t ax_ws_bytes(const DenseA& A, int l) {
   return std::max(s.total, emu_eligible(A, l) ? emu_ws_bytes(A, l) : (size_t)0);
 }
 
-void dense_ax(Ctx& c, const DenseA& A, const double* X, int l, double* Y, Arena& ar, const double* cx) {
+void dense_ax(Ctx& c, const DenseA& A, const double* X, int l, double* Y, Arena& ar, const double* cx, bool upper) {
   RPCA_REQUIRE(l >= 1 && l <= kMaxL, RPCA_E_SHAPE, "l=%d out of range [1,%d]", l, kMaxL);
   if (A.m == 0) return;
   if (f32_tc_ok(A)) {
@@ -380,7 +404,7 @@ void dense_ax(Ctx& c, const DenseA& A, const double* X, int l, double* Y, Arena&
     return;
   }
   if (cx && !tma_ok(A)) {  // generic kernel: the rank-1 correction as a separate thin pass
-    dense_ax(c, A, X, l, Y, ar, nullptr);
+    dense_ax(c, A, X, l, Y, ar, nullptr, upper);
     sub_rank1(c, Y, A.m, l, nullptr, cx);
     return;
   }
@@ -389,14 +413,14 @@ void dense_ax(Ctx& c, const DenseA& A, const double* X, int l, double* Y, Arena&
     double* part = ar.get<double>((size_t)kMaxSms * 2 * BM * ((l + 7) / 8 * 8));
     pack_x(c, X, A.n, l, Xp);
     switch ((l + 7) / 8) {
-      case 1: launch_ax_tma<1>(c, A, Xp, l, cx, Y, part); break;
-      case 2: launch_ax_tma<2>(c, A, Xp, l, cx, Y, part); break;
-      case 3: launch_ax_tma<3>(c, A, Xp, l, cx, Y, part); break;
-      case 4: launch_ax_tma<4>(c, A, Xp, l, cx, Y, part); break;
-      case 5: launch_ax_tma<5>(c, A, Xp, l, cx, Y, part); break;
-      case 6: launch_ax_tma<6>(c, A, Xp, l, cx, Y, part); break;
-      case 7: launch_ax_tma<7>(c, A, Xp, l, cx, Y, part); break;
-      default: launch_ax_tma<8>(c, A, Xp, l, cx, Y, part); break;
+      case 1: launch_ax_tma<1>(c, A, Xp, l, cx, Y, part, upper); break;
+      case 2: launch_ax_tma<2>(c, A, Xp, l, cx, Y, part, upper); break;
+      case 3: launch_ax_tma<3>(c, A, Xp, l, cx, Y, part, upper); break;
+      case 4: launch_ax_tma<4>(c, A, Xp, l, cx, Y, part, upper); break;
+      case 5: launch_ax_tma<5>(c, A, Xp, l, cx, Y, part, upper); break;
+      case 6: launch_ax_tma<6>(c, A, Xp, l, cx, Y, part, upper); break;
+      case 7: launch_ax_tma<7>(c, A, Xp, l, cx, Y, part, upper); break;
+      default: launch_ax_tma<8>(c, A, Xp, l, cx, Y, part, upper); break;
     }
     return;
   }

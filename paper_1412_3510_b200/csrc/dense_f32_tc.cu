@@ -147,6 +147,9 @@ __device__ __forceinline__ bool elect_one() {
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 
+#ifndef ATY_F32_MAX_STAGES
+#define ATY_F32_MAX_STAGES 8
+#endif
 #ifndef ATY_SLOTS
 #define ATY_SLOTS 2
 #endif
@@ -383,7 +386,8 @@ struct AtyCfg {
   static constexpr int kTN = 2 * N <= 32 ? 32 : (2 * N <= 64 ? 64 : 128);
   static constexpr int kYS = 3;  // Yᵀ chunk buffers
   static constexpr int kYBytes = kYS * 2 * kX;
-  static constexpr int kStages = (212 * 1024 - kYBytes) / kTileBytes > 8 ? 8 : (212 * 1024 - kYBytes) / kTileBytes;
+  static constexpr int kFit = (227 * 1024 - 1536 - kYBytes) / kTileBytes;  // 227 KB per CTA
+  static constexpr int kStages = kFit > ATY_F32_MAX_STAGES ? ATY_F32_MAX_STAGES : kFit;
   static constexpr int kSmem = kStages * kTileBytes + kYBytes + 1024 + 512;
   static constexpr int kNS = ATY_SLOTS;  // A slots after the accumulators: 32 columns A_hi + 32 columns A_lo
   static constexpr int kSlot0 = 512 - 64 * kNS;

@@ -242,7 +242,9 @@ struct DenseA {
 };
 size_t ax_ws_bytes(const DenseA& A, int l);
 // Y = A·X [− 1·cxᵀ]  (cx = c·X, the centring correction of PAPER.md:430; may be NULL)
-void dense_ax(Ctx& c, const DenseA& A, const double* X, int l, double* Y, Arena& ar, const double* cx = nullptr);
+// upper: X is upper triangular (the DMMA path skips its zero blocks)
+void dense_ax(Ctx& c, const DenseA& A, const double* X, int l, double* Y, Arena& ar, const double* cx = nullptr,
+              bool upper = false);
 // dense_ax_emu.cu — fp64 A·X as int8-digit products on tcgen05 (Ozaki scheme I)
 bool emu_eligible(const DenseA& A, int l);
 // E[i] = row i's exponent; wide (may be NULL, not cleared here) set to 1 if a

@@ -18,7 +18,6 @@ namespace rpca {
 namespace {
 
 constexpr int kThreads = 256;
-constexpr int kWarps = kThreads / 32;
 
 // Zero-σ completion (rare): column col of Vout (l×l row-major) with σ = 0 is
 // replaced by the Gram–Schmidt residual of the first e_t that keeps a norm

@@ -43,6 +43,12 @@ constexpr int kWarps = kThreads / 32;
 
 // rows per thread: leaves favour occupancy, tree levels (few CTAs, latency-
 // bound) favour bigger groups so the tournament has fewer levels
+#ifndef LU_NOM_U32
+#define LU_NOM_U32 32  // rows in flight per warp in the nomination loads, l ≤ 32
+#endif
+#ifndef LU_NOM_U64
+#define LU_NOM_U64 16  // … l > 32
+#endif
 #ifndef LU_LEAF_R24
 #define LU_LEAF_R24 1  // rows per thread of the leaves for 16 < LP ≤ 24
 #endif
@@ -406,22 +412,15 @@ __global__ void __launch_bounds__(kThreads, SelCfg<LP, RR>::kMinBlocks)
 // below 2^-100 of its block maximum counts as zero (no elimination).
 
 
-template <int LP, int W>
-__device__ __forceinline__ void trail_update32(float (&w)[LP], const float (*u12)[LP], int ns) {
-  float mm[8];
-#pragma unroll
-  for (int s = 0; s < 8; ++s) mm[s] = s < ns ? w[s] : 0.f;
-#pragma unroll
-  for (int t = 8; t < W; ++t) {
-    float v = w[t];
-#pragma unroll
-    for (int s = 0; s < 8; ++s) v = fmaf(-mm[s], u12[s][t - 8], v);
-    w[t] = v;
-  }
-#pragma unroll
-  for (int t = 0; t + 8 < LP; ++t) w[t] = w[t + 8];
-#pragma unroll
-  for (int t = LP - 8; t < LP; ++t) w[t] = 0.f;
+// a·b + c on both halves of a float pair: one FFMA2
+__device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {
+  float2 d;
+  asm("{\n\t.reg .b64 ra, rb, rc, rd;\n\t"
+      "mov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\tmov.b64 rc, {%6, %7};\n\t"
+      "fma.rn.f32x2 rd, ra, rb, rc;\n\tmov.b64 {%0, %1}, rd;\n\t}"
+      : "=f"(d.x), "=f"(d.y)
+      : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y), "f"(c.x), "f"(c.y));
+  return d;
 }
 
 template <int LP, int R>
@@ -435,7 +434,7 @@ __global__ void __launch_bounds__(kThreads, 2)
   __shared__ __align__(16) float pbuf[2][kWarps][8];
   __shared__ float traw[8][LP];
   __shared__ float l11[8][8];
-  __shared__ float u12[8][LP];
+  __shared__ __align__(16) float u12[8][LP];
   __shared__ int piv[LP];
   __shared__ int colexp[LP];
   __shared__ int nrows_s;
@@ -495,15 +494,18 @@ __global__ void __launch_bounds__(kThreads, 2)
   const int sl = l + 1;
   {
     const double m0 = (mu && lane < l) ? mu[lane] : 0.0, m1 = (mu && lane + 32 < l) ? mu[lane + 32] : 0.0;
-    // eight rows' loads in flight per warp (the loads are latency-bound)
-    constexpr int U8 = 8;
+    // U rows' loads in flight per warp (the loads are latency-bound: a
+    // leaf's rows arrive in ⌈rows / (8·U)⌉ round trips per pass); rows of
+    // l ≤ 32 take one double per lane
+    constexpr bool kTwo = LP > 32;
+    constexpr int U8 = kTwo ? LU_NOM_U64 : LU_NOM_U32;
     auto load8 = [&](int r0, double (&v0)[U8], double (&v1)[U8]) {
 #pragma unroll
       for (int u = 0; u < U8; ++u) {
         const int r = r0 + u * kWarps;
         const double* y = Y + (r < rows ? ids[r] : 0) * l;
         v0[u] = (r < rows && lane < l) ? y[lane] : 0.0;
-        v1[u] = (r < rows && lane + 32 < l) ? y[lane + 32] : 0.0;
+        if constexpr (kTwo) v1[u] = (r < rows && lane + 32 < l) ? y[lane + 32] : 0.0;
       }
     };
     unsigned f0 = 0, f1 = 0;
@@ -514,11 +516,11 @@ __global__ void __launch_bounds__(kThreads, 2)
       for (int u = 0; u < U8; ++u) {
         if (r0 + u * kWarps >= rows) break;
         f0 = max(f0, (unsigned)(__double_as_longlong(v0[u] - m0) >> 52) & 0x7FFu);
-        f1 = max(f1, (unsigned)(__double_as_longlong(v1[u] - m1) >> 52) & 0x7FFu);
+        if constexpr (kTwo) f1 = max(f1, (unsigned)(__double_as_longlong(v1[u] - m1) >> 52) & 0x7FFu);
       }
     }
     if (lane < l && f0) atomicMax(&colexp[lane], (int)f0);
-    if (lane + 32 < l && f1) atomicMax(&colexp[lane + 32], (int)f1);
+    if (kTwo && lane + 32 < l && f1) atomicMax(&colexp[lane + 32], (int)f1);
     __syncthreads();
     // 2^(1023 − f) (field f ≥ 1): the column maximum lands in [1, 2) ([2, 4)
     // for the top binade, whose 2^-1023 would be subnormal)
@@ -532,90 +534,101 @@ __global__ void __launch_bounds__(kThreads, 2)
         const int r = r0 + u * kWarps;
         if (r >= rows) break;
         if (lane < l) stage[r * sl + lane] = (float)((v0[u] - m0) * s0);
-        if (lane + 32 < l) stage[r * sl + lane + 32] = (float)((v1[u] - m1) * s1);
+        if (kTwo && lane + 32 < l) stage[r * sl + lane + 32] = (float)((v1[u] - m1) * s1);
       }
     }
   }
   __syncthreads();
   float w[R][LP];
+  uint32_t amask[R];  // all ones while the row may still be chosen
 #pragma unroll
-  for (int q = 0; q < R; ++q)
+  for (int q = 0; q < R; ++q) {
 #pragma unroll
     for (int t = 0; t < LP; ++t) w[q][t] = (act[q] && t < l) ? stage[(tid * R + q) * sl + t] : 0.f;
-  // blocked GEPP in 8-column panels — the fp64 kernel's scheme (lu_select_kernel).
+    amask[q] = act[q] ? 0xFFFFFFFFu : 0u;
+  }
+  // Blocked GEPP in 8-column panels (the fp64 kernel's scheme, lu_select_kernel),
+  // every panel and step unrolled so each register index is static.
   // The pivot key packs the value and the row: bits [RB, 32) hold
   // (|v|'s bits ≫ RB) + 1 (a 2^-(23-RB)-relative comparison, RB = log2 CAP),
   // bits [0, RB) hold CAP−1−row, so ONE unsigned max gives the largest |v|
-  // and, among equal keys, the lowest row — no ballot / find-first per level.
-  // Every warp publishes its winner's whole panel (two 16-byte stores).
+  // and, among equal keys, the lowest row.  A row leaves the competition by
+  // its key mask only: chosen rows keep being updated like the others (their
+  // values are never read again — the panel end takes their multipliers and
+  // trailing part before any later update reaches them), so a step is
+  // straight-line code.  Every warp publishes its winner's whole panel (two
+  // 16-byte stores).
   constexpr int RB = CAP <= 256 ? 8 : (CAP <= 512 ? 9 : 10);
-  auto packed_key = [&](float v, int row) -> uint32_t {
-    return ((((__float_as_uint(v) & 0x7FFFFFFFu) >> RB) + 1u) << RB) | (uint32_t)(CAP - 1 - row);
-  };
-  for (int pb = 0; pb < steps; pb += 8) {
-    const int ns = min(8, steps - pb);
+#ifdef LU_NOM_LOAD_ONLY  // timing ablation: the loads without the elimination
+  for (int j = tid; j < steps; j += kThreads) piv[j] = j;
+  if (w[0][0] == 1.2345f && w[R - 1][LP - 1] == 2.5f) piv[0] = 1;
+  if (false)
+#endif
+#pragma unroll
+  for (int P = 0; P < LP / 8; ++P) {
+    const int pb = 8 * P;
+    if (pb >= steps) break;
 #pragma unroll
     for (int s = 0; s < 8; ++s) {
-      if (s >= ns) break;
       const int j = pb + s;
-      uint32_t best = 0;
+      if (j >= steps) break;
+      uint32_t key[R], best = 0;
+#pragma unroll
+      for (int q = 0; q < R; ++q) {
+        key[q] = (((((__float_as_uint(w[q][j]) & 0x7FFFFFFFu) >> RB) + 1u) << RB) |
+                  (uint32_t)(CAP - 1 - (tid * R + q))) & amask[q];
+        best = max(best, key[q]);
+      }
+      const uint32_t mk = __reduce_max_sync(0xffffffffu, best);
 #pragma unroll
       for (int q = 0; q < R; ++q)
-        if (act[q]) best = max(best, packed_key(w[q][s], tid * R + q));
-      const uint32_t mk = __reduce_max_sync(0xffffffffu, best);
-      if (best == mk && mk != 0u) {  // the (unique) winning lane of this warp
-        const int bq = (int)(CAP - 1 - (mk & (CAP - 1))) - tid * R;
-#pragma unroll
-        for (int q = 0; q < R; ++q)
-          if (q == bq) {
-            float4* pb4 = reinterpret_cast<float4*>(pbuf[j & 1][warp]);
-            pb4[0] = make_float4(w[q][0], w[q][1], w[q][2], w[q][3]);
-            pb4[1] = make_float4(w[q][4], w[q][5], w[q][6], w[q][7]);
-          }
-      }
+        if (key[q] == mk && mk != 0u) {  // the (unique) winning row of this warp
+          float4* d = reinterpret_cast<float4*>(pbuf[j & 1][warp]);
+          d[0] = make_float4(w[q][pb], w[q][pb + 1], w[q][pb + 2], w[q][pb + 3]);
+          d[1] = make_float4(w[q][pb + 4], w[q][pb + 5], w[q][pb + 6], w[q][pb + 7]);
+        }
       if (lane == 0) slot[j & 1][warp] = mk;
       __syncthreads();
       const uint32_t kv = lane < kWarps ? slot[j & 1][lane] : 0u;
       const uint32_t gk = __reduce_max_sync(0xffffffffu, kv);
       const int p = (int)(CAP - 1 - (gk & (CAP - 1)));
-      const int ww = p / (32 * R);  // the warp that holds row p
-      const float* prow = pbuf[j & 1][ww];
-      const float pv = prow[s];
+      const float4* pr4 = reinterpret_cast<const float4*>(pbuf[j & 1][p / (32 * R)]);
+      const float4 pa = pr4[0], pc = pr4[1];
+      const float pr[8] = {pa.x, pa.y, pa.z, pa.w, pc.x, pc.y, pc.z, pc.w};
       float rc;  // MUFU reciprocal (nomination only needs ~1 ulp); tiny pivot ⇒ a zero column
-      asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(rc) : "f"(pv));
-      const float uinv = fabsf(pv) >= 0x1p-100f ? rc : 0.f;
+      asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(rc) : "f"(pr[s]));
+      const float uinv = fabsf(pr[s]) >= 0x1p-100f ? rc : 0.f;
       if (tid == 0) piv[j] = p;
 #pragma unroll
       for (int q = 0; q < R; ++q) {
-        if (!act[q]) continue;
         if (tid * R + q == p) {
-          act[q] = false;
           pstep[q] = s;
-          continue;
+          amask[q] = 0u;
         }
-        const float mult = w[q][s] * uinv;
-        w[q][s] = mult;
+        const float mult = w[q][j] * uinv;
+        w[q][j] = mult;
 #pragma unroll
-        for (int t = s + 1; t < 8; ++t) w[q][t] = fmaf(-mult, prow[t], w[q][t]);
+        for (int t = s + 1; t < 8; ++t) w[q][pb + t] = fmaf(-mult, pr[t], w[q][pb + t]);
       }
     }
-    if (pb + 8 >= LP) break;
+    if (pb + 8 >= steps) break;  // no later step reads the trailing columns
+    const int nt = LP - pb - 8;  // trailing columns (a constant after unrolling)
 #pragma unroll
     for (int q = 0; q < R; ++q)
-      if (pstep[q] >= 0) {
+      if (pstep[q] >= 0) {  // this panel's pivot rows: multipliers and trailing part
         const int sp = pstep[q];
 #pragma unroll
-        for (int t = 8; t < LP; ++t) traw[sp][t - 8] = w[q][t];
+        for (int t = pb + 8; t < LP; ++t) traw[sp][t - pb - 8] = w[q][t];
 #pragma unroll
-        for (int t = 0; t < 8; ++t) l11[sp][t] = t < sp ? w[q][t] : 0.f;
-        pstep[q] = -2;
+        for (int t = 0; t < 8; ++t) l11[sp][t] = t < sp ? w[q][pb + t] : 0.f;
+        pstep[q] = -1;
       }
     __syncthreads();
-    if (tid < LP - 8) {
+    if (tid < nt) {  // U12 = L11⁻¹·(pivot rows' trailing part), one column per thread
       float u[8];
 #pragma unroll
       for (int sp = 0; sp < 8; ++sp) {
-        float v = sp < ns ? traw[sp][tid] : 0.f;
+        float v = traw[sp][tid];
 #pragma unroll
         for (int s2 = 0; s2 < sp; ++s2) v = fmaf(-l11[sp][s2], u[s2], v);
         u[sp] = v;
@@ -623,12 +636,27 @@ __global__ void __launch_bounds__(kThreads, 2)
       }
     }
     __syncthreads();
-    const int live = LP - pb;
+    // trailing update w[t] −= Σ_s w[pb+s]·U12[s][t] (s ascending), two columns
+    // per FFMA2
 #pragma unroll
     for (int q = 0; q < R; ++q) {
-      if (!act[q]) continue;
-      if (live > LP / 2) trail_update32<LP, LP>(w[q], u12, ns);
-      else trail_update32<LP, LP / 2>(w[q], u12, ns);
+      float2 nm[8];
+#pragma unroll
+      for (int s = 0; s < 8; ++s) nm[s] = make_float2(-w[q][pb + s], -w[q][pb + s]);
+#pragma unroll
+      for (int t = pb + 8; t < LP; t += 4) {
+        float2 v0 = make_float2(w[q][t], w[q][t + 1]), v1 = make_float2(w[q][t + 2], w[q][t + 3]);
+#pragma unroll
+        for (int s = 0; s < 8; ++s) {
+          const float4 u = *reinterpret_cast<const float4*>(&u12[s][t - pb - 8]);
+          v0 = ffma2(nm[s], make_float2(u.x, u.y), v0);
+          v1 = ffma2(nm[s], make_float2(u.z, u.w), v1);
+        }
+        w[q][t] = v0.x;
+        w[q][t + 1] = v0.y;
+        w[q][t + 2] = v1.x;
+        w[q][t + 3] = v1.y;
+      }
     }
   }
   __syncthreads();
@@ -727,7 +755,10 @@ void select(Ctx& c, unsigned grid, const double* Y, int64_t m, int l, int leaf, 
   count_launch(c, 1, leaf == 1 ? "lu_leaf" : "lu_tree");
 }
 
-constexpr int nominate_rows_per_thread(int LP) { return LP <= 16 ? 4 : (LP <= 32 ? 2 : 1); }
+#ifndef LU_NOM_R32
+#define LU_NOM_R32 2
+#endif
+constexpr int nominate_rows_per_thread(int LP) { return LP <= 16 ? 4 : (LP <= 32 ? LU_NOM_R32 : 1); }
 int nominate_cap(int l) { return kThreads * nominate_rows_per_thread(lp_of(l)); }
 
 template <int LP>
@@ -824,7 +855,7 @@ void apply_l(Ctx& c, double* Y, int64_t m, int64_t row0, int l, const double* M,
       count_launch(c, 1, "misc");
     }
     TagScope ts(c, "lu_apply");
-    dense_ax(c, DenseA{Y, RPCA_F64, m, l, l}, M, l, Y, ar, cx);
+    dense_ax(c, DenseA{Y, RPCA_F64, m, l, l}, M, l, Y, ar, cx, true);  // M = U⁻¹ is upper triangular
     ar.off = mark;
   }
   pivot_rows_kernel<<<1, 256, 0, c.stream>>>(Y, m, row0, l, Lp, piv);
