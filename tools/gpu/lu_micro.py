@@ -43,3 +43,14 @@ for m, l in shapes:
     tot = sum(v[1] for v in agg.values()) / 5
     print(f"m={m:9d} l={l:2d} total {1e3 * tot:8.1f}us  maxL {float(L.abs().max()):.3g} sin(Y,L) {sin:.1e}  " +
           " ".join(f"{k}:{v[0] // 5}x{1e3 * v[1] / 5:.1f}us" for k, v in agg.items()), flush=True)
+# per-launch times of one LU (the tree levels in order)
+if os.environ.get("LU_LEVELS"):
+    for m, l in shapes:
+        g = torch.Generator(device="cuda").manual_seed(m + l)
+        Y = torch.randn(m, l, generator=g, device=dev, dtype=torch.float64)
+        rp.lu_renorm(Y.clone())
+        torch.cuda.synchronize()
+        with rp.profile() as p:
+            rp.lu_renorm(Y.clone())
+            torch.cuda.synchronize()
+        print(f"m={m} l={l} levels:", " ".join(f"{n}:{1e3 * ms:.0f}" for n, ms in p.records), flush=True)
