@@ -424,8 +424,11 @@ __device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {
   return d;
 }
 
-template <int LP, int R>
-__global__ void __launch_bounds__(kThreads, 2)
+// MINB: CTAs per SM the registers are capped for — 3 for the wide leaves and
+// big tree levels of 32 < l < 64 (80 registers, a few spilled: the third
+// CTA's step chain hides more of the other two's), else 2
+template <int LP, int R, int MINB>
+__global__ void __launch_bounds__(kThreads, MINB)
     lu_nominate_kernel(const double* __restrict__ Y, int64_t m, int l, int leaf, const int64_t* __restrict__ cand_in,
                        int64_t n_in, int G, int64_t* __restrict__ cand_out, const double* __restrict__ mu) {
   constexpr int CAP = kThreads * R;
@@ -499,7 +502,7 @@ __global__ void __launch_bounds__(kThreads, 2)
     // leaf's rows arrive in ⌈rows / (8·U)⌉ round trips per pass); rows of
     // l ≤ 32 take one double per lane
     constexpr bool kTwo = LP > 32;
-    constexpr int U8 = kTwo ? LU_NOM_U64 : LU_NOM_U32;
+    constexpr int U8 = kTwo ? (MINB >= 3 ? 8 : LU_NOM_U64) : (MINB >= 3 ? 16 : LU_NOM_U32);
     // CONTIG: a full leaf (rows = CAP consecutive rows of Y) — plain strided
     // addresses, no per-row bounds or id lookups (the address arithmetic and
     // predicates were most of the leaf's instructions: ncu, C5 leaf)
@@ -784,8 +787,15 @@ void nominate_lp(Ctx& c, unsigned grid, const double* Y, int64_t m, int l, int l
                  int64_t n_in, int G, int64_t* cout, const double* mu) {
   constexpr int R = nominate_rows_per_thread(LP);
   const int smem = kThreads * R * (l + 1) * 4;
-  ensure_smem((const void*)lu_nominate_kernel<LP, R>, kThreads * R * (LP + 1) * 4);
-  lu_nominate_kernel<LP, R><<<grid, kThreads, smem, c.stream>>>(Y, m, l, leaf, cin, n_in, G, cout, mu);
+  if constexpr (LP > 32 && LP < 64) {
+    if (grid >= 2u * (unsigned)c.num_sms) {  // enough CTAs to fill three per SM
+      ensure_smem((const void*)lu_nominate_kernel<LP, R, 3>, kThreads * R * (LP + 1) * 4);
+      lu_nominate_kernel<LP, R, 3><<<grid, kThreads, smem, c.stream>>>(Y, m, l, leaf, cin, n_in, G, cout, mu);
+      return;
+    }
+  }
+  ensure_smem((const void*)lu_nominate_kernel<LP, R, 2>, kThreads * R * (LP + 1) * 4);
+  lu_nominate_kernel<LP, R, 2><<<grid, kThreads, smem, c.stream>>>(Y, m, l, leaf, cin, n_in, G, cout, mu);
 }
 
 void nominate(Ctx& c, unsigned grid, const double* Y, int64_t m, int l, int leaf, const int64_t* cin, int64_t n_in,
