@@ -360,7 +360,6 @@ __global__ void __launch_bounds__(kThreads, SelCfg<LP, RR>::kMinBlocks)
   }
   // keep[j] = pivot row j as published (columns j.. at 0..LP−j−1); its
   // multiplier of step s < j is msm[s·CAP + piv[j]]
-  double* Ms = keep + LP * LP;  // l×l M = U⁻¹ (U_ic = keep[i·LP + c − i])
   for (int idx = tid; idx < l * l; idx += kThreads) {
     const int j = idx / l, c = idx - j * l;
     const double u = c >= j ? keep[j * LP + c - j] : 0.0;
@@ -377,6 +376,11 @@ __global__ void __launch_bounds__(kThreads, SelCfg<LP, RR>::kMinBlocks)
   // for every input of the row substitution x·U = y, reading Q3).  Thread j
   // owns column j: back substitution M[i][j] = (δ_ij − Σ_{t=i+1..j} U_it M_tj)/U_ii,
   // four partial sums per dot product (U reads are broadcasts).
+  // (A right-looking variant with the partial sums in registers is 6× faster
+  // in isolation — tools/microbench/uinv_probe.cu — but not inside this
+  // kernel, whose register budget it exhausts; its different summation order
+  // also moved a RENORM_ODD parity case past its bound.)
+  double* Ms = keep + LP * LP;  // l×l M = U⁻¹ (U_ic = keep[i·LP + c − i])
   if (tid < l) {
     const int j = tid;
     for (int i = l - 1; i > j; --i) Ms[i * l + j] = 0.0;
