@@ -31,9 +31,15 @@ g = torch.Generator(device=dev).manual_seed(0)
 if op in ("aty", "ax"):
     A = synth.make_c4(device=dev)
     m_, n_, l = A.shape[0], A.shape[1], 52
+    As = None
 elif op in ("aty64", "ax64"):
     A = synth.make("C2", device=dev)
     m_, n_, l = A.shape[0], A.shape[1], 22
+elif op in ("csr_ax", "csr_aty"):
+    rp_, ci, va = synth.make("C5", device=dev)
+    m_, n_, l = 10000000, 1000000, 32
+    A = None
+    As = [mm.CSR(rp_, ci, va, (m_, n_)) for mm in mods]
 if op.startswith("pca:"):
     import bench
     cfg = synth.CONFIGS[op[4:]]
@@ -42,10 +48,11 @@ if op.startswith("pca:"):
 else:
     X = torch.randn(n_, l, generator=g, device=dev, dtype=torch.float64)
     Q = torch.randn(m_, l, generator=g, device=dev, dtype=torch.float64)
-    if op.startswith("aty"):
-        fns = [lambda rp=rp: rp.apply(A, Q, adjoint=True) for rp in mods]
+    Ai = As if A is None else [A] * len(mods)
+    if op.startswith("aty") or op == "csr_aty":
+        fns = [lambda rp=rp, a=a: rp.apply(a, Q, adjoint=True) for rp, a in zip(mods, Ai)]
     else:
-        fns = [lambda rp=rp: rp.apply(A, X) for rp in mods]
+        fns = [lambda rp=rp, a=a: rp.apply(a, X) for rp, a in zip(mods, Ai)]
 
 clocks, stop = [], threading.Event()
 
