@@ -125,11 +125,14 @@ __global__ void __launch_bounds__(kThreads) chol_kernel(const double* __restrict
   }
 }
 
-// The same contract for l ≤ 32 in ONE warp, no shared memory and no
-// barriers: lane b holds column b of G, then of R (and of Rprev), in
-// registers (LP = l rounded up to 8, static indices); the values of other
-// columns arrive by broadcast shuffles.  Order: Cholesky (right-looking), then
-// Rtot = R·Rprev and its row signs, then X = R⁻¹ written with the column signs.
+// The same contract for l ≤ 32 in ONE warp, no barriers: lane b holds column
+// b of G, then of R (and of Rprev), in registers (LP = l rounded up to 8,
+// static indices); during the Cholesky the values of other columns arrive by
+// broadcast shuffles.  Order: Cholesky (right-looking), then Rtot = R·Rprev
+// and its row signs, then X = R⁻¹ written with the column signs.  The two
+// triangular products read the rows of R from a shared-memory copy (broadcast
+// loads): with a shuffle per term they were 80% of the kernel at l = 32 (a
+// shuffle in every link of the FMA chain).  Same FMA order either way.
 template <int LP>
 __global__ void __launch_bounds__(32) chol_warp_kernel(const double* __restrict__ Gin, int l,
                                                        const double* __restrict__ Rprev, int signfix,
@@ -166,6 +169,12 @@ __global__ void __launch_bounds__(32) chol_warp_kernel(const double* __restrict_
       g[a] = fma(-rja, rjb, g[a]);
     }
   }
+  // R row-major in shared memory: Rs[i][t] = R[i][t] (lane t holds column t)
+  __shared__ double Rs[LP][LP + 1];
+#pragma unroll
+  for (int i = 0; i < LP; ++i)
+    if (lane < LP) Rs[i][lane] = r[i];
+  __syncwarp();
   // Rtot = R·Rprev (column `lane`), reusing g; row signs from its diagonal
 #pragma unroll
   for (int i = 0; i < LP; ++i) {
@@ -174,7 +183,7 @@ __global__ void __launch_bounds__(32) chol_warp_kernel(const double* __restrict_
       s = r[i];
     } else {
 #pragma unroll
-      for (int t = i; t < LP; ++t) s = fma(__shfl_sync(FULL, r[i], t), pc[t], s);
+      for (int t = i; t < LP; ++t) s = fma(Rs[i][t], pc[t], s);
     }
     g[i] = s;
   }
@@ -195,7 +204,7 @@ __global__ void __launch_bounds__(32) chol_warp_kernel(const double* __restrict_
     double a0 = 0.0, a1 = 0.0;
 #pragma unroll
     for (int t = i + 1; t < LP; ++t) {
-      const double rit = __shfl_sync(FULL, r[i], t);
+      const double rit = Rs[i][t];
       if ((t - i) & 1) a0 = fma(rit, pc[t], a0);
       else a1 = fma(rit, pc[t], a1);
     }
