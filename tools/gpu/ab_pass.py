@@ -44,7 +44,11 @@ if op.startswith("pca:"):
     import bench
     cfg = synth.CONFIGS[op[4:]]
     A = bench.make_input(cfg, dev, mods[0])
-    fns = [lambda rp=rp: bench.run_step(rp, cfg, A) for rp in mods]
+    if isinstance(A, torch.Tensor):
+        Ai = [A] * len(mods)
+    else:  # each module's own CSR wrapper around the same device arrays
+        Ai = [mm.CSR(A.rowptr, A.colind, A.vals, A.shape) for mm in mods]
+    fns = [lambda rp=rp, a=a: bench.run_step(rp, cfg, a) for rp, a in zip(mods, Ai)]
 else:
     X = torch.randn(n_, l, generator=g, device=dev, dtype=torch.float64)
     Q = torch.randn(m_, l, generator=g, device=dev, dtype=torch.float64)
