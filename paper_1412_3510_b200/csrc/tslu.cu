@@ -372,34 +372,36 @@ __global__ void __launch_bounds__(kThreads, SelCfg<LP, RR>::kMinBlocks)
     udr[j] = uii != 0.0 ? 1.0 / uii : 0.0;
   }
   __syncthreads();
-  // M = U⁻¹ with the zero-pivot rule (a zero U_ii zeroes row i of M: x_i = 0
-  // for every input of the row substitution x·U = y, reading Q3).  Thread j
-  // owns column j: back substitution M[i][j] = (δ_ij − Σ_{t=i+1..j} U_it M_tj)/U_ii,
-  // four partial sums per dot product (U reads are broadcasts).
-  // (A right-looking variant with the partial sums in registers is 6× faster
-  // in isolation — tools/microbench/uinv_probe.cu — but not inside this
-  // kernel, whose register budget it exhausts; its different summation order
-  // also moved a RENORM_ODD parity case past its bound.)
-  double* Ms = keep + LP * LP;  // l×l M = U⁻¹ (U_ic = keep[i·LP + c − i])
-  if (tid < l) {
-    const int j = tid;
-    for (int i = l - 1; i > j; --i) Ms[i * l + j] = 0.0;
-    for (int i = j; i >= 0; --i) {
-      double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
-      const double* ui = keep + i * LP - i;  // U_it = ui[t]
-      int t = i + 1;
-      for (; t + 3 <= j; t += 4) {
-        a0 = fma(ui[t], Ms[t * l + j], a0);
-        a1 = fma(ui[t + 1], Ms[(t + 1) * l + j], a1);
-        a2 = fma(ui[t + 2], Ms[(t + 2) * l + j], a2);
-        a3 = fma(ui[t + 3], Ms[(t + 3) * l + j], a3);
+  if constexpr (LP > 32) {  // l ≤ 32: M by u_inverse_warp_kernel after this kernel
+    // M = U⁻¹ with the zero-pivot rule (a zero U_ii zeroes row i of M: x_i = 0
+    // for every input of the row substitution x·U = y, reading Q3).  Thread j
+    // owns column j: back substitution M[i][j] = (δ_ij − Σ_{t=i+1..j} U_it M_tj)/U_ii,
+    // four partial sums per dot product (U reads are broadcasts).
+    // (A right-looking variant with the partial sums in registers is 6× faster
+    // in isolation — tools/microbench/uinv_probe.cu — but not inside this
+    // kernel, whose register budget it exhausts; its different summation order
+    // also moved a RENORM_ODD parity case past its bound.)
+    double* Ms = keep + LP * LP;  // l×l M = U⁻¹ (U_ic = keep[i·LP + c − i])
+    if (tid < l) {
+      const int j = tid;
+      for (int i = l - 1; i > j; --i) Ms[i * l + j] = 0.0;
+      for (int i = j; i >= 0; --i) {
+        double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+        const double* ui = keep + i * LP - i;  // U_it = ui[t]
+        int t = i + 1;
+        for (; t + 3 <= j; t += 4) {
+          a0 = fma(ui[t], Ms[t * l + j], a0);
+          a1 = fma(ui[t + 1], Ms[(t + 1) * l + j], a1);
+          a2 = fma(ui[t + 2], Ms[(t + 2) * l + j], a2);
+          a3 = fma(ui[t + 3], Ms[(t + 3) * l + j], a3);
+        }
+        for (; t <= j; ++t) a0 = fma(ui[t], Ms[t * l + j], a0);
+        Ms[i * l + j] = ((i == j ? 1.0 : 0.0) - ((a0 + a1) + (a2 + a3))) * udr[i];
       }
-      for (; t <= j; ++t) a0 = fma(ui[t], Ms[t * l + j], a0);
-      Ms[i * l + j] = ((i == j ? 1.0 : 0.0) - ((a0 + a1) + (a2 + a3))) * udr[i];
     }
+    __syncthreads();
+    for (int idx = tid; idx < l * l; idx += kThreads) M[idx] = Ms[idx];
   }
-  __syncthreads();
-  for (int idx = tid; idx < l * l; idx += kThreads) M[idx] = Ms[idx];
   }  // leaves
 }
 
@@ -757,6 +759,62 @@ void select_lp(Ctx& c, unsigned grid, const double* Y, int64_t m, int l, int lea
                                              rows_in, rows_out, mu);
 }
 
+// M = U⁻¹ for l ≤ 32 in one warp (the last tournament level's U), lane j =
+// column j of M in registers, U's rows broadcast from shared memory: the
+// same sums in the same order as the column-serial loop of lu_select_kernel
+// — a term goes to accumulator (t−i−1) mod 4 while it belongs to that loop's
+// unrolled-by-4 part, else to a0 — so M is bitwise the same; there every
+// term re-read its M[t][j] from shared memory (≈ 20k cycles at l = 22).
+// Terms beyond j multiply M[t][j] = 0 and leave the sums unchanged.
+template <int LP>
+__global__ void __launch_bounds__(32) u_inverse_warp_kernel(const double* __restrict__ U, int l,
+                                                            double* __restrict__ M) {
+  __shared__ double Us[LP][LP + 1];
+  __shared__ double udr[LP];
+  const int j = threadIdx.x;
+#pragma unroll
+  for (int i = 0; i < LP; ++i)
+    if (j < LP) Us[i][j] = (i < l && j < l) ? U[i * l + j] : 0.0;
+  if (j < LP) {
+    const double uii = j < l ? U[j * l + j] : 0.0;
+    udr[j] = uii != 0.0 ? 1.0 / uii : 0.0;
+  }
+  __syncwarp();
+  double mc[LP];
+#pragma unroll
+  for (int i = LP - 1; i >= 0; --i) {
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+    const int mainend = i + 4 * ((j - i) >> 2);  // last term of the unrolled part (j ≥ i)
+#pragma unroll
+    for (int t = i + 1; t < LP; ++t) {
+      const double u = Us[i][t];
+      const int k = (t - i - 1) & 3;
+      if (k == 0) {
+        a0 = fma(u, mc[t], a0);
+      } else {  // branch-free: the choice differs across lanes
+        const bool main_ = t <= mainend;
+        const double x0 = fma(u, mc[t], a0);
+        if (k == 1) {
+          const double xk = fma(u, mc[t], a1);
+          a1 = main_ ? xk : a1;
+        } else if (k == 2) {
+          const double xk = fma(u, mc[t], a2);
+          a2 = main_ ? xk : a2;
+        } else {
+          const double xk = fma(u, mc[t], a3);
+          a3 = main_ ? xk : a3;
+        }
+        a0 = main_ ? a0 : x0;
+      }
+    }
+    mc[i] = (i < l && j < l && j >= i) ? ((i == j ? 1.0 : 0.0) - ((a0 + a1) + (a2 + a3))) * udr[i] : 0.0;
+  }
+  if (j < l)
+#pragma unroll
+    for (int i = 0; i < LP; ++i)
+      if (i < l) M[i * l + j] = mc[i];
+}
+
 void select(Ctx& c, unsigned grid, const double* Y, int64_t m, int l, int leaf, const int64_t* cin, int64_t n_in,
             int G, int64_t* cout, int final_, double* U, double* Lp, int64_t* piv, double* M,
             const double* rows_in = nullptr, double* rows_out = nullptr, const double* mu = nullptr) {
@@ -778,6 +836,16 @@ void select(Ctx& c, unsigned grid, const double* Y, int64_t m, int l, int leaf, 
 #undef RPCA_SEL
   RPCA_CHECK_LAUNCH();
   count_launch(c, 1, leaf == 1 ? "lu_leaf" : "lu_tree");
+  if (final_ && lp_of(l) <= 32) {
+    switch (lp_of(l)) {
+      case 8: u_inverse_warp_kernel<8><<<1, 32, 0, c.stream>>>(U, l, M); break;
+      case 16: u_inverse_warp_kernel<16><<<1, 32, 0, c.stream>>>(U, l, M); break;
+      case 24: u_inverse_warp_kernel<24><<<1, 32, 0, c.stream>>>(U, l, M); break;
+      default: u_inverse_warp_kernel<32><<<1, 32, 0, c.stream>>>(U, l, M); break;
+    }
+    RPCA_CHECK_LAUNCH();
+    count_launch(c, 1, "lu_tree");
+  }
 }
 
 #ifndef LU_NOM_R32
