@@ -112,7 +112,8 @@ __device__ __forceinline__ void trail_update(double (&w)[LP], const double (*u12
 
 // One CTA: rows from Y (leaf: contiguous block; tree: a group of candidate
 // sets), GEPP, l nominated original rows → cand_out[blockIdx.x*l ...] (-1 pad).
-// If final, also U, Lp, the original pivot rows piv_out and M = U⁻¹.
+// If final, also U, Lp and the original pivot rows piv_out (M = U⁻¹ follows in
+// u_inverse_warp_kernel).
 //   leaf: 1 = contiguous rows of Y; 0 = candidate ids into Y; 2 = candidate
 //   rows given directly (rows_in, one l-vector per slot; ids are global rows
 //   — the all-gathered local winners of a row-sharded LU)
@@ -137,11 +138,10 @@ __global__ void __launch_bounds__(kThreads, SelCfg<LP, RR>::kMinBlocks)
   __shared__ int nrows_s;
   __shared__ int setcnt[CAP + 1];
   __shared__ uint64_t full_bar;
-  __shared__ double udr[LP];
-  // final: LP × LP published pivot rows, U, M, multipliers; bulk: the staged
+  // final: LP × LP published pivot rows and the multipliers; bulk: the staged
   // rows of the next leaf (CAP × l, row-major as in Y)
   extern __shared__ double keep[];
-  double* msm = keep + LP * LP + l * l;  // final only: multiplier of (step j, row r) at j·CAP + r
+  double* msm = keep + LP * LP;  // final only: multiplier of (step j, row r) at j·CAP + r
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
 
   // bulk (leaves only, never final): a persistent CTA walks leaves b, b+grid, …
@@ -366,42 +366,10 @@ __global__ void __launch_bounds__(kThreads, SelCfg<LP, RR>::kMinBlocks)
     U[idx] = u;
     Lp[idx] = c < j ? msm[c * CAP + piv[j]] : (c == j ? 1.0 : 0.0);
   }
-  for (int j = tid; j < l; j += kThreads) {
-    piv_out[j] = ids[piv[j]];
-    const double uii = keep[j * LP];
-    udr[j] = uii != 0.0 ? 1.0 / uii : 0.0;
-  }
-  __syncthreads();
-  if constexpr (LP > 32) {  // l ≤ 32: M by u_inverse_warp_kernel after this kernel
-    // M = U⁻¹ with the zero-pivot rule (a zero U_ii zeroes row i of M: x_i = 0
-    // for every input of the row substitution x·U = y, reading Q3).  Thread j
-    // owns column j: back substitution M[i][j] = (δ_ij − Σ_{t=i+1..j} U_it M_tj)/U_ii,
-    // four partial sums per dot product (U reads are broadcasts).
-    // (A right-looking variant with the partial sums in registers is 6× faster
-    // in isolation — tools/microbench/uinv_probe.cu — but not inside this
-    // kernel, whose register budget it exhausts; its different summation order
-    // also moved a RENORM_ODD parity case past its bound.)
-    double* Ms = keep + LP * LP;  // l×l M = U⁻¹ (U_ic = keep[i·LP + c − i])
-    if (tid < l) {
-      const int j = tid;
-      for (int i = l - 1; i > j; --i) Ms[i * l + j] = 0.0;
-      for (int i = j; i >= 0; --i) {
-        double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
-        const double* ui = keep + i * LP - i;  // U_it = ui[t]
-        int t = i + 1;
-        for (; t + 3 <= j; t += 4) {
-          a0 = fma(ui[t], Ms[t * l + j], a0);
-          a1 = fma(ui[t + 1], Ms[(t + 1) * l + j], a1);
-          a2 = fma(ui[t + 2], Ms[(t + 2) * l + j], a2);
-          a3 = fma(ui[t + 3], Ms[(t + 3) * l + j], a3);
-        }
-        for (; t <= j; ++t) a0 = fma(ui[t], Ms[t * l + j], a0);
-        Ms[i * l + j] = ((i == j ? 1.0 : 0.0) - ((a0 + a1) + (a2 + a3))) * udr[i];
-      }
-    }
-    __syncthreads();
-    for (int idx = tid; idx < l * l; idx += kThreads) M[idx] = Ms[idx];
-  }
+  for (int j = tid; j < l; j += kThreads) piv_out[j] = ids[piv[j]];
+  // M = U⁻¹ follows in u_inverse_warp_kernel (one thread per column in
+  // registers; here, one column per thread re-read every term from shared
+  // memory — 20-66k cycles, up to half of this kernel)
   }  // leaves
 }
 
@@ -731,7 +699,7 @@ void select_lpr(Ctx& c, unsigned grid, const double* Y, int64_t m, int l, int le
   // the staging state)
   constexpr bool kBulkOK = SelCfg<LP, R>::kMinBlocks == 1;
   const int bulk = kBulkOK && leaf == 1 && !final_ && (reinterpret_cast<uintptr_t>(Y) & 15) == 0;
-  const size_t smem = final_ ? (size_t)(LP * LP + l * l + (size_t)CAP * l) * 8 : bulk ? (size_t)CAP * l * 8 : 0;
+  const size_t smem = final_ ? (size_t)(LP * LP + (size_t)CAP * l) * 8 : bulk ? (size_t)CAP * l * 8 : 0;
   const void* fn = bulk ? (const void*)lu_select_kernel<LP, R, kBulkOK> : (const void*)lu_select_kernel<LP, R, false>;
   if (smem) ensure_smem(fn, (int)smem);
   if (bulk) {
@@ -771,7 +739,7 @@ __global__ void __launch_bounds__(32) u_inverse_warp_kernel(const double* __rest
                                                             double* __restrict__ M) {
   __shared__ double Us[LP][LP + 1];
   __shared__ double udr[LP];
-  const int j = threadIdx.x;
+  const int j = threadIdx.x;  // one thread per column
 #pragma unroll
   for (int i = 0; i < LP; ++i)
     if (j < LP) Us[i][j] = (i < l && j < l) ? U[i * l + j] : 0.0;
@@ -815,6 +783,39 @@ __global__ void __launch_bounds__(32) u_inverse_warp_kernel(const double* __rest
       if (i < l) M[i * l + j] = mc[i];
 }
 
+// M = U⁻¹ for 32 < l ≤ 64: two warps, thread j = column j, right-looking —
+// as soon as M[t][j] is known it updates every row above it, acc_i +=
+// U_it·M_tj (independent across i; U's column t broadcast from shared
+// memory), so the dependence chain per row is one FMA and the scaling.  The
+// column-serial order of u_inverse_warp_kernel would chain every term through
+// one accumulator (68 µs at l = 52); here the sum for M[i][j] runs over t
+// descending (deterministic; ≈ 1 ulp from the column-serial sums).
+template <int LP>
+__global__ void __launch_bounds__(64) u_inverse_rl_kernel(const double* __restrict__ U, int l,
+                                                          double* __restrict__ M) {
+  __shared__ double Us[LP][LP + 1];
+  __shared__ double udr[LP];
+  const int j = threadIdx.x;
+#pragma unroll
+  for (int i = 0; i < LP; ++i)
+    if (j < LP) Us[i][j] = (i < l && j < l) ? U[i * l + j] : 0.0;
+  if (j < LP) {
+    const double uii = j < l ? U[j * l + j] : 0.0;
+    udr[j] = uii != 0.0 ? 1.0 / uii : 0.0;
+  }
+  __syncthreads();
+  double acc[LP];
+#pragma unroll
+  for (int i = 0; i < LP; ++i) acc[i] = 0.0;
+#pragma unroll
+  for (int t = LP - 1; t >= 0; --t) {
+    const double mt = (t < l && j < l && j >= t) ? ((t == j ? 1.0 : 0.0) - acc[t]) * udr[t] : 0.0;
+    if (t < l && j < l) M[t * l + j] = mt;
+#pragma unroll
+    for (int i = 0; i < t; ++i) acc[i] = fma(Us[i][t], mt, acc[i]);
+  }
+}
+
 void select(Ctx& c, unsigned grid, const double* Y, int64_t m, int l, int leaf, const int64_t* cin, int64_t n_in,
             int G, int64_t* cout, int final_, double* U, double* Lp, int64_t* piv, double* M,
             const double* rows_in = nullptr, double* rows_out = nullptr, const double* mu = nullptr) {
@@ -836,12 +837,16 @@ void select(Ctx& c, unsigned grid, const double* Y, int64_t m, int l, int leaf, 
 #undef RPCA_SEL
   RPCA_CHECK_LAUNCH();
   count_launch(c, 1, leaf == 1 ? "lu_leaf" : "lu_tree");
-  if (final_ && lp_of(l) <= 32) {
+  if (final_) {
     switch (lp_of(l)) {
       case 8: u_inverse_warp_kernel<8><<<1, 32, 0, c.stream>>>(U, l, M); break;
       case 16: u_inverse_warp_kernel<16><<<1, 32, 0, c.stream>>>(U, l, M); break;
       case 24: u_inverse_warp_kernel<24><<<1, 32, 0, c.stream>>>(U, l, M); break;
-      default: u_inverse_warp_kernel<32><<<1, 32, 0, c.stream>>>(U, l, M); break;
+      case 32: u_inverse_warp_kernel<32><<<1, 32, 0, c.stream>>>(U, l, M); break;
+      case 40: u_inverse_rl_kernel<40><<<1, 64, 0, c.stream>>>(U, l, M); break;
+      case 48: u_inverse_rl_kernel<48><<<1, 64, 0, c.stream>>>(U, l, M); break;
+      case 56: u_inverse_rl_kernel<56><<<1, 64, 0, c.stream>>>(U, l, M); break;
+      default: u_inverse_rl_kernel<64><<<1, 64, 0, c.stream>>>(U, l, M); break;
     }
     RPCA_CHECK_LAUNCH();
     count_launch(c, 1, "lu_tree");
