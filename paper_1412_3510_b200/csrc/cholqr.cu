@@ -29,7 +29,6 @@ constexpr double kBreakdown = 0x1p-40;
 // One CTA: R = chol(G) (upper, RᵀR = G, G full l×l) → X = R⁻¹ (upper);
 // Rtot = R·Rprev (Rprev upper or NULL); if `signfix`, D = sign(diag(Rtot)):
 // Minv = X·D, Rtot ← D·Rtot.
-template <int LP>
 __global__ void __launch_bounds__(kThreads) chol_kernel(const double* __restrict__ Gin, int l,
                                                         const double* __restrict__ Rprev, int signfix,
                                                         double* __restrict__ Minv, double* __restrict__ Rtot,
@@ -85,22 +84,23 @@ __global__ void __launch_bounds__(kThreads) chol_kernel(const double* __restrict
     }
     __syncthreads();
   }
-  // X = R⁻¹ (upper): thread j owns column j in registers, right-looking — as
-  // soon as X[t][j] is known it updates every row above it, acc_i +=
-  // R_it·X_tj (independent across i, R's column t broadcast from shared
-  // memory): one FMA and the scaling per row on the dependence chain
+  // X = R⁻¹ (upper): thread j owns column j, back substitution with i
+  // descending (R reads are broadcasts), four partial sums per dot product
   if (tid < l) {
     const int j = tid;
-    double acc[LP];
-#pragma unroll
-    for (int i = 0; i < LP; ++i) acc[i] = 0.0;
-#pragma unroll
-    for (int t = LP - 1; t >= 0; --t) {
-      if (t >= l) continue;
-      const double xt = j >= t ? ((t == j ? 1.0 : 0.0) - acc[t]) * d[t] : 0.0;
-      X[t * l + j] = xt;
-#pragma unroll
-      for (int i = 0; i < t; ++i) acc[i] = fma(R[i * l + t], xt, acc[i]);
+    for (int i = l - 1; i > j; --i) X[i * l + j] = 0.0;
+    for (int i = j; i >= 0; --i) {
+      double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+      const double* ri = R + i * l;
+      int t = i + 1;
+      for (; t + 3 <= j; t += 4) {
+        a0 = fma(ri[t], X[t * l + j], a0);
+        a1 = fma(ri[t + 1], X[(t + 1) * l + j], a1);
+        a2 = fma(ri[t + 2], X[(t + 2) * l + j], a2);
+        a3 = fma(ri[t + 3], X[(t + 3) * l + j], a3);
+      }
+      for (; t <= j; ++t) a0 = fma(ri[t], X[t * l + j], a0);
+      X[i * l + j] = ((i == j ? 1.0 : 0.0) - ((a0 + a1) + (a2 + a3))) * d[i];
     }
   }
   __syncthreads();
@@ -223,21 +223,9 @@ void chol(Ctx& c, const double* G, int l, const double* Rprev, int signfix, doub
     case 16: chol_warp_kernel<16><<<1, 32, 0, c.stream>>>(G, l, Rprev, signfix, Minv, Rtot, bd); break;
     case 24: chol_warp_kernel<24><<<1, 32, 0, c.stream>>>(G, l, Rprev, signfix, Minv, Rtot, bd); break;
     case 32: chol_warp_kernel<32><<<1, 32, 0, c.stream>>>(G, l, Rprev, signfix, Minv, Rtot, bd); break;
-    case 40:
-      ensure_smem((const void*)chol_kernel<40>, 4 * kMaxL * kMaxL * 8);
-      chol_kernel<40><<<1, kThreads, 4 * l * l * 8, c.stream>>>(G, l, Rprev, signfix, Minv, Rtot, bd);
-      break;
-    case 48:
-      ensure_smem((const void*)chol_kernel<48>, 4 * kMaxL * kMaxL * 8);
-      chol_kernel<48><<<1, kThreads, 4 * l * l * 8, c.stream>>>(G, l, Rprev, signfix, Minv, Rtot, bd);
-      break;
-    case 56:
-      ensure_smem((const void*)chol_kernel<56>, 4 * kMaxL * kMaxL * 8);
-      chol_kernel<56><<<1, kThreads, 4 * l * l * 8, c.stream>>>(G, l, Rprev, signfix, Minv, Rtot, bd);
-      break;
     default:
-      ensure_smem((const void*)chol_kernel<64>, 4 * kMaxL * kMaxL * 8);
-      chol_kernel<64><<<1, kThreads, 4 * l * l * 8, c.stream>>>(G, l, Rprev, signfix, Minv, Rtot, bd);
+      ensure_smem((const void*)chol_kernel, 4 * kMaxL * kMaxL * 8);
+      chol_kernel<<<1, kThreads, 4 * l * l * 8, c.stream>>>(G, l, Rprev, signfix, Minv, Rtot, bd);
   }
   RPCA_CHECK_LAUNCH();
   count_launch(c, 1, "cholqr_chol");
