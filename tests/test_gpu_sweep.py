@@ -70,3 +70,42 @@ def test_sweep_vs_oracle(m, n, k, l, its, raw, kind):
     assert np.max(np.abs(Sg[nz] - So[nz]) / So[nz]) < tol_s, (Sg[:4], So[:4])
     assert cluster_sin_angle(Uo, U.double().cpu().numpy(), So, k) < tol_a
     assert cluster_sin_angle(Vo, V.double().cpu().numpy(), So, k) < tol_a
+
+
+# Nyström (SHIFT_CHOL and SQRT) and reig across the same widths: PSD
+# A = V·diag(0.8^j)·Vᵀ, indefinite A = V·diag(±0.85^j)·Vᵀ (alternating signs)
+EIG_CASES = [(1500, 6, 8, 2), (1500, 15, 17, 2), (2000, 22, 24, 1), (2000, 31, 33, 2), (2500, 39, 41, 2),
+             (2500, 46, 48, 2), (3000, 55, 57, 1), (3000, 62, 64, 2)]
+
+
+def sym(n, l, signed):
+    q = 0.85 if signed else 0.8
+    lam = torch.tensor([q ** j for j in range(n)], dtype=torch.float64)
+    if signed:
+        lam = lam * (-1.0) ** torch.arange(n, dtype=torch.float64)
+    V = synth.haar_columns(n, n, 7 * n + l)
+    A = (V * lam) @ V.T
+    return (0.5 * (A + A.T)).contiguous()
+
+
+@pytest.mark.parametrize("n,k,l,its", EIG_CASES)
+@pytest.mark.parametrize("variant", ["shift_chol", "sqrt"])
+def test_sweep_eigens_vs_oracle(n, k, l, its, variant):
+    A = sym(n, l, signed=False)
+    U, lam = rp.eigens(A.to(dev()), k, its=its, l=l, seed=5, variant=variant)
+    Uo, lo = oracle.eigens(A.numpy(), k, its=its, l=l, seed=5,
+                           variant=oracle.SHIFT_CHOL if variant == "shift_chol" else oracle.SQRT)
+    lg = lam.cpu().numpy()
+    assert np.max(np.abs(lg - lo) / lo) < 1e-10, (lg[:4], lo[:4])
+    assert cluster_sin_angle(Uo, U.cpu().numpy(), lo, k) < 1e-8
+
+
+@pytest.mark.parametrize("n,k,l,its", EIG_CASES)
+def test_sweep_reig_vs_oracle(n, k, l, its):
+    A = sym(n, l, signed=True)
+    U, lam = rp.reig(A.to(dev()), k, its=its, l=l, seed=5)
+    Uo, lo = oracle.reig(A.numpy(), k, its=its, l=l, seed=5)
+    lg = lam.cpu().numpy()
+    assert np.all(np.sign(lg) == np.sign(lo))
+    assert np.max(np.abs(lg - lo) / np.abs(lo)) < 1e-10, (lg[:4], lo[:4])
+    assert cluster_sin_angle(Uo, U.cpu().numpy(), np.abs(lo), k) < 1e-8
