@@ -59,7 +59,10 @@ constexpr int kWarps = kThreads / 32;
 constexpr int leaf_rows_per_thread(int LP) {
   return LP <= 8 ? 4 : (LP <= 16 ? 2 : (LP <= 24 ? LU_LEAF_R24 : (LP <= 32 ? LU_LEAF_R32 : 1)));
 }
-constexpr int tree_rows_per_thread(int LP) { return LP <= 8 ? 4 : (LP <= 32 ? 2 : 1); }
+#ifndef LU_TREE_R32
+#define LU_TREE_R32 1  // rows per thread of the fp64 last level for 8 < LP ≤ 32 (1: −21% vs 2)
+#endif
+constexpr int tree_rows_per_thread(int LP) { return LP <= 8 ? 4 : (LP <= 32 ? LU_TREE_R32 : 1); }
 
 // two CTAs per SM (registers capped at 128) while a thread's rows fit
 #ifndef LU_TWO_BLOCK_MAX
