@@ -484,16 +484,19 @@ __global__ void __launch_bounds__(kThreads, MINB)
     // addresses, no per-row bounds or id lookups (the address arithmetic and
     // predicates were most of the leaf's instructions: ncu, C5 leaf)
     const double* yb = Y + (leaf == 1 ? blk * (int64_t)CAP * l : 0) + lane;
-    auto passes = [&](auto CONTIG) {
+    // EXACT: l == LP (C5's l = 32) — row stride, bounds and the stage stride
+    // become compile-time constants (immediate address offsets)
+    auto passes = [&](auto CONTIG, auto EXACT) {
       constexpr bool kContig = decltype(CONTIG)::value;
+      const int ll = decltype(EXACT)::value ? LP : l, sll = ll + 1;
       auto load8 = [&](int r0, double (&v0)[U8], double (&v1)[U8]) {
 #pragma unroll
         for (int u = 0; u < U8; ++u) {
           const int r = r0 + u * kWarps;
           if constexpr (kContig) {
-            const int o = r * l;
-            v0[u] = lane < l ? yb[o] : 0.0;
-            if constexpr (kTwo) v1[u] = lane + 32 < l ? yb[o + 32] : 0.0;
+            const int o = r * ll;
+            v0[u] = lane < ll ? yb[o] : 0.0;
+            if constexpr (kTwo) v1[u] = lane + 32 < ll ? yb[o + 32] : 0.0;
           } else {
             const double* y = Y + (r < rows ? ids[r] : 0) * l;
             v0[u] = (r < rows && lane < l) ? y[lane] : 0.0;
@@ -513,13 +516,13 @@ __global__ void __launch_bounds__(kThreads, MINB)
           if constexpr (kTwo) f1 = max(f1, (unsigned)(__double_as_longlong(v1[u] - m1) >> 52) & 0x7FFu);
         }
       }
-      if (lane < l && f0) atomicMax(&colexp[lane], (int)f0);
-      if (kTwo && lane + 32 < l && f1) atomicMax(&colexp[lane + 32], (int)f1);
+      if (lane < ll && f0) atomicMax(&colexp[lane], (int)f0);
+      if (kTwo && lane + 32 < ll && f1) atomicMax(&colexp[lane + 32], (int)f1);
       __syncthreads();
       // 2^(1023 − f) (field f ≥ 1): the column maximum lands in [1, 2) ([2, 4)
       // for the top binade, whose 2^-1023 would be subnormal)
       auto scale = [](int f) { return f ? __longlong_as_double((long long)(2046 - min(f, 2045)) << 52) : 0.0; };
-      const double s0 = lane < l ? scale(colexp[lane]) : 0.0, s1 = lane + 32 < l ? scale(colexp[lane + 32]) : 0.0;
+      const double s0 = lane < ll ? scale(colexp[lane]) : 0.0, s1 = lane + 32 < ll ? scale(colexp[lane + 32]) : 0.0;
       for (int r0 = warp; r0 < nr; r0 += kWarps * U8) {
         double v0[U8], v1[U8];
         load8(r0, v0, v1);
@@ -527,14 +530,15 @@ __global__ void __launch_bounds__(kThreads, MINB)
         for (int u = 0; u < U8; ++u) {
           const int r = r0 + u * kWarps;
           if (!kContig && r >= rows) break;
-          if (lane < l) stage[r * sl + lane] = (float)((v0[u] - m0) * s0);
-          if (kTwo && lane + 32 < l) stage[r * sl + lane + 32] = (float)((v1[u] - m1) * s1);
+          if (lane < ll) stage[r * sll + lane] = (float)((v0[u] - m0) * s0);
+          if (kTwo && lane + 32 < ll) stage[r * sll + lane + 32] = (float)((v1[u] - m1) * s1);
         }
       }
     };
     static_assert(CAP % (kWarps * U8) == 0, "a full leaf is a whole number of load batches");
-    if (leaf == 1 && rows == CAP) passes(std::true_type{});
-    else passes(std::false_type{});
+    if (leaf == 1 && rows == CAP && l == LP) passes(std::true_type{}, std::true_type{});
+    else if (leaf == 1 && rows == CAP) passes(std::true_type{}, std::false_type{});
+    else passes(std::false_type{}, std::false_type{});
   }
   __syncthreads();
   float w[R][LP];
