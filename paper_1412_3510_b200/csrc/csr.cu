@@ -110,8 +110,11 @@ __global__ void __launch_bounds__(kThreads) csr_spmm_kernel(const int64_t* __res
 #ifndef CSR_PAIR_B
 #define CSR_PAIR_B 8
 #endif
-template <class T, int W>
-__global__ void __launch_bounds__(kThreads, CSR_PAIR_MINB) csr_spmm_pair_kernel(const int64_t* __restrict__ rowptr,
+// Short rows (avg < 32 nonzeros: C5's A·X) take B = 4 gathers per batch at 6
+// CTAs per SM (A·X −3.5% against 8 at 5, interleaved A/B; long rows, C5's
+// Aᵀ·Y, unchanged).  The batch size does not change the order of the sums.
+template <class T, int W, int B = CSR_PAIR_B, int MINB = CSR_PAIR_MINB>
+__global__ void __launch_bounds__(kThreads, MINB) csr_spmm_pair_kernel(const int64_t* __restrict__ rowptr,
                                                                  const int32_t* __restrict__ colind,
                                                                  const T* __restrict__ vals, int64_t rows,
                                                                  const double* __restrict__ X, int l, int64_t heavy,
@@ -140,23 +143,23 @@ __global__ void __launch_bounds__(kThreads, CSR_PAIR_MINB) csr_spmm_pair_kernel(
       }
       vs += myv;
       int k = 0;
-      for (; k + CSR_PAIR_B <= cnt; k += CSR_PAIR_B) {
-        int c[CSR_PAIR_B];
-        double v[CSR_PAIR_B];
+      for (; k + B <= cnt; k += B) {
+        int c[B];
+        double v[B];
 #pragma unroll
-        for (int u = 0; u < CSR_PAIR_B; ++u) {
+        for (int u = 0; u < B; ++u) {
           c[u] = __shfl_sync(hm, myc, k + u, W);
           v[u] = __shfl_sync(hm, myv, k + u, W);
         }
         if (act) {
-          double2 x[CSR_PAIR_B][C / 2];
+          double2 x[B][C / 2];
 #pragma unroll
-          for (int u = 0; u < CSR_PAIR_B; ++u)
+          for (int u = 0; u < B; ++u)
 #pragma unroll
             for (int h = 0; h < C / 2; ++h)
               x[u][h] = *reinterpret_cast<const double2*>(X + (int64_t)c[u] * l + C * s + 2 * h);
 #pragma unroll
-          for (int u = 0; u < CSR_PAIR_B; ++u)
+          for (int u = 0; u < B; ++u)
 #pragma unroll
             for (int h = 0; h < C / 2; ++h) {
               a[2 * h] += v[u] * x[u][h].x;
@@ -317,6 +320,14 @@ void csr_spmm_rows(Ctx& c, const CsrA& Afull, int64_t r0, int64_t r1, const doub
     else
       csr_spmm_pair_kernel<float, 8><<<gp, kThreads, 0, c.stream>>>(A.ptr, A.idx, (const float*)A.vals, A.rows, X, l,
                                                                     heavy, xmean, Y);
+  } else if (pair && avg < 32) {
+    const unsigned gp = grid_cap(c, A.rows, kThreads / 16);
+    if (A.dtype == RPCA_F64)
+      csr_spmm_pair_kernel<double, 16, 4, 6><<<gp, kThreads, 0, c.stream>>>(A.ptr, A.idx, (const double*)A.vals, A.rows,
+                                                                            X, l, heavy, xmean, Y);
+    else
+      csr_spmm_pair_kernel<float, 16, 4, 6><<<gp, kThreads, 0, c.stream>>>(A.ptr, A.idx, (const float*)A.vals, A.rows,
+                                                                           X, l, heavy, xmean, Y);
   } else if (pair) {
     const unsigned gp = grid_cap(c, A.rows, kThreads / 16);
     if (A.dtype == RPCA_F64)
