@@ -62,6 +62,7 @@ def ncu_traffic(config, kernel):
         return {"bytes": sum(r["traffic_bytes"] for r in recs) / len(recs), "source": recs[0]["source"]}
     r = max(recs, key=lambda r: r["traffic_bytes"])
     return {"bytes": r["traffic_bytes"], "source": r["source"]}
+DMMA_PEAK_TF = 37.1  # fp64 tensor (DMMA) throughput measured by tools/microbench/peaks.cu, TF/s
 FALLBACK_HBM = 6650.0  # B200_PROFILING.md fallback, GB/s
 
 
@@ -441,6 +442,17 @@ def main():
             roof["dram_based"] = {"achieved": round(tr["bytes"] / (avg_ms / 1e3) / 1e9, 1),
                                   "frac": round(tr["bytes"] / (avg_ms / 1e3) / 1e9 / hbm, 4),
                                   "note": "ncu dram bytes per launch / live launch time"}
+        if dom[0] in ("ax_f64_dmma", "aty_f64_dmma") and isinstance(A, torch.Tensor):
+            # the fp64 passes issue DMMA (m8n8k4) on l padded to a multiple of 8:
+            # the fp64 tensor pipe, not HBM, caps them
+            lp = -(-cfg.l // 8) * 8
+            fl = 2.0 * A.shape[0] * A.shape[1] * lp
+            tf = fl / (avg_ms / 1e3) / 1e12
+            roof["fp64_tensor"] = {
+                "issued_flops_per_launch": fl, "achieved_tflops": round(tf, 2), "peak_tflops": DMMA_PEAK_TF,
+                "frac": round(tf / DMMA_PEAK_TF, 4),
+                "hbm_frac_ceiling": round(8 * DMMA_PEAK_TF * 1e12 / (2 * lp) / 1e9 / hbm, 4),
+                "peak_source": "dmma_peak of tools/microbench/peaks.cu at 1965 MHz (DESIGN.md §6)"}
         all_pass_ms = sum(v[1] for v in passes_k.values()) / args.steps
         roof["all_passes"] = {"launches_per_step": sum(v[0] for v in passes_k.values()) // args.steps,
                               "gbs_per_pass": round(abytes * passes / (all_pass_ms / 1e3) / 1e9, 1)}
