@@ -455,6 +455,14 @@ __global__ void __launch_bounds__(kThreadsEmu, 1)
           planes4(lo, hi, w[g]);
 #endif
         }
+        // the digits (computed from every loaded value) must exist before the
+        // stage is released, else the arithmetic — and the wait for the loads
+        // — may be scheduled after the arrive and the TMA refill the stage
+        // under loads in flight (as found in dense_f32_tc.cu's Aᵀ·Y split)
+#pragma unroll
+        for (int g = 0; g < kGroups; ++g)
+#pragma unroll
+          for (int p = 0; p < kDigits; ++p) asm volatile("" ::"r"(w[g][p]) : "memory");
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[rg.s]);  // the row is in registers
         mbar_wait(&sfree[rb.s], rb.ph ^ 1u);

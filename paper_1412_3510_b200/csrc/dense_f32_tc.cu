@@ -101,6 +101,20 @@ __device__ __forceinline__ void mma_commit(uint64_t* bar) {
                : "memory");
 }
 
+// Release a shared-memory stage only after its loads have RETURNED.  An
+// mbarrier arrive is a volatile asm that stays in program order with other
+// volatile asms, but the register arithmetic on the loaded values (the first
+// instructions that wait for the loads' data) may be scheduled below it, so
+// the TMA could refill the stage under loads still in flight.  Pass this
+// empty volatile asm values COMPUTED from the loads (it emits no instruction
+// itself, so raw load results would not do): the arithmetic producing them,
+// and with it the wait for every load, must then come before the arrive.
+__device__ __forceinline__ void loads_done16(const float* v) {
+  asm volatile("" ::"f"(v[0]), "f"(v[1]), "f"(v[2]), "f"(v[3]), "f"(v[4]), "f"(v[5]), "f"(v[6]), "f"(v[7]),
+               "f"(v[8]), "f"(v[9]), "f"(v[10]), "f"(v[11]), "f"(v[12]), "f"(v[13]), "f"(v[14]), "f"(v[15])
+               : "memory");
+}
+
 __device__ __forceinline__ void tmem_ld16(uint32_t addr, float (&v)[16]) {
   uint32_t r[16];
   asm volatile(
@@ -306,14 +320,16 @@ __global__ void __launch_bounds__(kThreadsAx, 1)
           hi[4 * c + 2] = x.z;
           hi[4 * c + 3] = x.w;
         }
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&empty[rg.s]);  // the row is in registers
 #pragma unroll
         for (int k = 0; k < 32; ++k) {
           const float a = hi[k];
           hi[k] = __uint_as_float(__float_as_uint(a) & 0xFFFFE000u);
           lo[k] = a - hi[k];
         }
+        loads_done16(lo);  // the row is in registers (see loads_done16)
+        loads_done16(lo + 16);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[rg.s]);
         mbar_wait(&tfree[rt.s], rt.ph ^ 1u);
         tc_fence_after();
         const uint32_t at = tmem + lane_off + (uint32_t)(Cfg::kSlot0 + 64 * rt.s);
@@ -384,7 +400,10 @@ struct AtyCfg {
   static constexpr int kX = N * 128;  // one Yᵀ chunk: N rows × 32 fp32
   // [0, N) A_hi·Y_hi + A_lo·Y_hi, [N, 2N) A_hi·Y_lo (one N = 2N MMA)
   static constexpr int kTN = 2 * N <= 32 ? 32 : (2 * N <= 64 ? 64 : 128);
-  static constexpr int kYS = 3;  // Yᵀ chunk buffers
+#ifndef ATY_YS
+#define ATY_YS 3
+#endif
+  static constexpr int kYS = ATY_YS;  // Yᵀ chunk buffers
   static constexpr int kYBytes = kYS * 2 * kX;
   static constexpr int kFit = (227 * 1024 - 1536 - kYBytes) / kTileBytes;  // 227 KB per CTA
   static constexpr int kStages = kFit > ATY_F32_MAX_STAGES ? ATY_F32_MAX_STAGES : kFit;
@@ -540,14 +559,22 @@ __global__ void __launch_bounds__(kThreadsAty, 1)
       float hi[16], lo[16];
 #pragma unroll
       for (int rho = 0; rho < 16; ++rho) hi[rho] = tile[rho * 128];  // a warp reads 128 contiguous bytes
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[rg.s]);  // the rows are in registers: the stage may be refilled
+      // the stage may be refilled only once the loads have RETURNED
+      // (loads_done16): arriving right after issuing them let the TMA
+      // overwrite the stage under loads still in flight — stale A values in
+      // some TMEM lanes, Z rows off by ~1e-3 relative, in 11 of 60 calls
+      // (l = 40-64, 400000 × 600) and in every call with 4 stages
+      // (tools/gpu/aty_f32_diag.py; 0 of 600 after this change)
 #pragma unroll
       for (int rho = 0; rho < 16; ++rho) {
         const float a = hi[rho];
         hi[rho] = __uint_as_float(__float_as_uint(a) & 0xFFFFE000u);
         lo[rho] = a - hi[rho];
       }
+      loads_done16(hi);
+      loads_done16(lo);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[rg.s]);
       mbar_wait(&tfree[rt.s], rt.ph ^ 1u);
       tc_fence_after();
       const uint32_t at = tmem + lane_off + (uint32_t)(Cfg::kSlot0 + 64 * rt.s + 16 * h);

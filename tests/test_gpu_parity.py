@@ -569,3 +569,21 @@ def test_csr_large_operand_spmm():
     assert np.all(np.abs(got - ref) <= 2 * gamma(256) * absA_X + 1e-300)
     res = rp.pca(A, 30, its=2, l=32, seed=0)
     compare(res, oracle.pca(host, 30, its=2, l=32, seed=0), 30)
+
+
+@pytest.mark.parametrize("l", [40, 44, 52, 64])
+def test_aty_f32_repeated_calls_bitwise_stable(l):
+    """The fp32 tcgen05 Aᵀ·Y pass, called repeatedly on the same inputs, gives
+    the same bits every time, within 1e-4 (relative to the largest entry) of
+    the fp64 product.  Regression: its split warps released each shared-memory A stage
+    before their loads had returned, so the TMA could refill it under them —
+    ~1 call in 6 at these shapes came back with some rows of Z off by ~1e-3
+    (dense_f32_tc.cu, loads_done16)."""
+    g = torch.Generator(device=dev()).manual_seed(7)
+    A = torch.randn(400000, 600, generator=g, device=dev(), dtype=torch.float32) + 3.0
+    Q = torch.randn(400000, l, generator=g, device=dev(), dtype=torch.float64)
+    ref = A.double().T @ Q
+    first = rp.apply(A, Q, adjoint=True)
+    assert (first - ref).abs().max().item() <= 1e-4 * ref.abs().max().item()
+    for _ in range(12):
+        assert torch.equal(rp.apply(A, Q, adjoint=True), first)
