@@ -566,6 +566,113 @@ __global__ void __launch_bounds__(kThreads, MINB)
   if (w[0][0] == 1.2345f && w[R - 1][LP - 1] == 2.5f) piv[0] = 1;
   if (false)
 #endif
+#ifndef LU_NOM_ROLLED
+#define LU_NOM_ROLLED 1
+#endif
+#if LU_NOM_ROLLED
+  // Panels as a rolled loop over a register window: the panel is always
+  // w[·][0, 8) and its trailing columns w[·][8, LP); after each panel the
+  // window shifts left by 8 columns.  Same operations in the same order as
+  // the unrolled form below (the shifted-in tail holds zeros and gets zero
+  // U12 columns), at 1/(LP/8) of its code: the unrolled kernel (~6k
+  // instructions for LP = 24) stalled on instruction fetch ("no_instructions"
+  // 44% of the leaf's samples, most of a 9-CTA tree level's).
+#pragma unroll 1
+  for (int pb = 0; pb < steps; pb += 8) {
+#pragma unroll
+    for (int s = 0; s < 8; ++s) {
+      const int j = pb + s;
+      if (j >= steps) break;
+      uint32_t key[R], best = 0;
+#pragma unroll
+      for (int q = 0; q < R; ++q) {
+        key[q] = (((((__float_as_uint(w[q][s]) & 0x7FFFFFFFu) >> RB) + 1u) << RB) |
+                  (uint32_t)(CAP - 1 - (tid * R + q))) & amask[q];
+        best = max(best, key[q]);
+      }
+      const uint32_t mk = __reduce_max_sync(0xffffffffu, best);
+#pragma unroll
+      for (int q = 0; q < R; ++q)
+        if (key[q] == mk && mk != 0u) {  // the (unique) winning row of this warp
+          float4* d = reinterpret_cast<float4*>(pbuf[j & 1][warp]);
+          d[0] = make_float4(w[q][0], w[q][1], w[q][2], w[q][3]);
+          d[1] = make_float4(w[q][4], w[q][5], w[q][6], w[q][7]);
+        }
+      if (lane == 0) slot[j & 1][warp] = mk;
+      __syncthreads();
+      const uint32_t kv = lane < kWarps ? slot[j & 1][lane] : 0u;
+      const uint32_t gk = __reduce_max_sync(0xffffffffu, kv);
+      const int p = (int)(CAP - 1 - (gk & (CAP - 1)));
+      const float4* pr4 = reinterpret_cast<const float4*>(pbuf[j & 1][p / (32 * R)]);
+      const float4 pa = pr4[0], pc = pr4[1];
+      const float pr[8] = {pa.x, pa.y, pa.z, pa.w, pc.x, pc.y, pc.z, pc.w};
+      float rc;  // MUFU reciprocal (nomination only needs ~1 ulp); tiny pivot ⇒ a zero column
+      asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(rc) : "f"(pr[s]));
+      const float uinv = fabsf(pr[s]) >= 0x1p-100f ? rc : 0.f;
+      if (tid == 0) piv[j] = p;
+#pragma unroll
+      for (int q = 0; q < R; ++q) {
+        if (tid * R + q == p) {
+          pstep[q] = s;
+          amask[q] = 0u;
+        }
+        const float mult = w[q][s] * uinv;
+        w[q][s] = mult;
+#pragma unroll
+        for (int t = s + 1; t < 8; ++t) w[q][t] = fmaf(-mult, pr[t], w[q][t]);
+      }
+    }
+    if (pb + 8 >= steps || LP == 8) break;  // no later step reads the trailing columns
+    const int nt = LP - pb - 8;             // real trailing columns
+#pragma unroll
+    for (int q = 0; q < R; ++q)
+      if (pstep[q] >= 0) {  // this panel's pivot rows: multipliers and trailing part
+        const int sp = pstep[q];
+#pragma unroll
+        for (int t = 8; t < LP; ++t) traw[sp][t - 8] = w[q][t];
+#pragma unroll
+        for (int t = 0; t < 8; ++t) l11[sp][t] = t < sp ? w[q][t] : 0.f;
+        pstep[q] = -1;
+      }
+    __syncthreads();
+    if (tid < LP - 8) {  // U12 = L11⁻¹·(pivot rows' trailing part), one column per thread
+      float u[8];
+#pragma unroll
+      for (int sp = 0; sp < 8; ++sp) {
+        float v = traw[sp][tid];
+#pragma unroll
+        for (int s2 = 0; s2 < sp; ++s2) v = fmaf(-l11[sp][s2], u[s2], v);
+        u[sp] = v;
+        u12[sp][tid] = tid < nt ? v : 0.f;
+      }
+    }
+    __syncthreads();
+    // trailing update w[t] −= Σ_s w[s]·U12[s][t] (s ascending), two columns
+    // per FFMA2, then the window moves to the next panel
+#pragma unroll
+    for (int q = 0; q < R; ++q) {
+      float2 nm[8];
+#pragma unroll
+      for (int s = 0; s < 8; ++s) nm[s] = make_float2(-w[q][s], -w[q][s]);
+#pragma unroll
+      for (int t = 8; t < LP; t += 4) {
+        float2 v0 = make_float2(w[q][t], w[q][t + 1]), v1 = make_float2(w[q][t + 2], w[q][t + 3]);
+#pragma unroll
+        for (int s = 0; s < 8; ++s) {
+          const float4 u = *reinterpret_cast<const float4*>(&u12[s][t - 8]);
+          v0 = ffma2(nm[s], make_float2(u.x, u.y), v0);
+          v1 = ffma2(nm[s], make_float2(u.z, u.w), v1);
+        }
+        w[q][t - 8] = v0.x;
+        w[q][t - 7] = v0.y;
+        w[q][t - 6] = v1.x;
+        w[q][t - 5] = v1.y;
+      }
+#pragma unroll
+      for (int t = LP - 8; t < LP; ++t) w[q][t] = 0.f;
+    }
+  }
+#else
 #pragma unroll
   for (int P = 0; P < LP / 8; ++P) {
     const int pb = 8 * P;
@@ -661,6 +768,7 @@ __global__ void __launch_bounds__(kThreads, MINB)
       }
     }
   }
+#endif
   __syncthreads();
   for (int j = tid; j < l; j += kThreads) cand_out[blk * l + j] = j < steps ? ids[piv[j]] : -1;
 }
