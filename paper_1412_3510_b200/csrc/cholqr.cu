@@ -153,6 +153,45 @@ __global__ void __launch_bounds__(32) chol_warp_kernel(const double* __restrict_
 #pragma unroll
   for (int j = 0; j < LP; ++j) gmax = fmax(gmax, __shfl_sync(FULL, g[j], j));  // lanes ≥ l hold 0
   const double floor_ = 0x1p-104 * gmax;
+#ifndef CHOL_ROLLED
+#define CHOL_ROLLED 1
+#endif
+  // R row-major in shared memory: Rs[i][t] = R[i][t] (lane t holds column t)
+  __shared__ double Rs[LP][LP + 1];
+#if CHOL_ROLLED
+  // Column steps as a rolled loop over a register window (window slot t holds
+  // column j + t at step j, shifted left after each step): the same FMAs in
+  // the same order as the unrolled form below, at 1/LP of its code — the
+  // unrolled kernel (one warp, run once per call) was bound by instruction
+  // fetch.  Slots past column LP−1 hold values never read back.
+  __shared__ double ds[LP];
+#pragma unroll 1
+  for (int j = 0; j < l; ++j) {
+    const double dj = __shfl_sync(FULL, g[0], j);
+    if (breakdown && lane == 0 && !(dj > kBreakdown * gmax)) *breakdown = 1;
+    const double dc = dj > floor_ ? dj : (floor_ > 0.0 ? floor_ : 1.0);
+    const double ri = rsqrt(dc);
+    if (lane == 0) ds[j] = ri;
+    const double rjb = lane == j ? dc * ri : (lane > j ? g[0] * ri : 0.0);  // R[j][lane]
+    if (lane < LP) Rs[j][lane] = rjb;
+#pragma unroll
+    for (int t = 1; t < LP; ++t) {
+      const double rja = __shfl_sync(FULL, rjb, (j + t) & 31);
+      g[t] = fma(-rja, rjb, g[t]);
+    }
+#pragma unroll
+    for (int t = 0; t < LP - 1; ++t) g[t] = g[t + 1];
+    g[LP - 1] = 0.0;
+  }
+  for (int j = l; j < LP; ++j)
+    if (lane < LP) Rs[j][lane] = 0.0;
+  __syncwarp();
+#pragma unroll
+  for (int i = 0; i < LP; ++i) {
+    r[i] = lane < LP ? Rs[i][lane] : 0.0;
+    d[i] = i < l ? ds[i] : 0.0;
+  }
+#else
 #pragma unroll
   for (int j = 0; j < LP; ++j) {
     if (j >= l) break;
@@ -169,12 +208,13 @@ __global__ void __launch_bounds__(32) chol_warp_kernel(const double* __restrict_
       g[a] = fma(-rja, rjb, g[a]);
     }
   }
-  // R row-major in shared memory: Rs[i][t] = R[i][t] (lane t holds column t)
-  __shared__ double Rs[LP][LP + 1];
+#if !CHOL_ROLLED
 #pragma unroll
   for (int i = 0; i < LP; ++i)
     if (lane < LP) Rs[i][lane] = r[i];
   __syncwarp();
+#endif
+#endif
   // Rtot = R·Rprev (column `lane`), reusing g; row signs from its diagonal
 #pragma unroll
   for (int i = 0; i < LP; ++i) {
